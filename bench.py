@@ -1,0 +1,304 @@
+"""Benchmark: requests scored + scheduled per second for one Equinox scheduling step.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg2|cfg3]
+
+A "step" is one cold scheduling step over a resident queue: drain_arrivals of
+the whole queue (client-grouped FIFO index + counter lift) followed by admit_requests with
+whole-queue scoring (MoPE predict -> map_metrics -> ufc/rfc increments -> HF selection under
+the slot/KV budget).  N=1 runs BASELINE configs[1] (1M LMSYS-shaped requests, 64 clients).
+Under torchrun each rank holds its own 1M-request / 64-client shard (weak scaling, no
+data-path collective in this round: see DESIGN.md "Multi-GPU").
+
+Timing: every timed step is bracketed by CUDA events on the context stream; the L2 (126 MB)
+is flushed with a 256 MiB memset between steps, outside the events.  `e2e` repeats the step
+through the public API with host (pinned) input buffers, the H2D copies and the D2H of the
+step's events + ledger inside a wall-clock region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+ALGO_BYTES_K1 = 17 + 21       # per request: read client/arrival/in/tag, write pred/bucket/ufc/rfc
+ALGO_BYTES_DRAIN = 4 + 4 + 4  # per request: histogram read, rank read, perm write
+
+
+def load_inputs(cfg: str, rank: int):
+    from paper_2508_16646_b200 import workload as W
+    from paper_2508_16646_b200 import scheduler as S
+    data = os.path.join(ROOT, "paper_2508_16646_b200", "data")
+    model = S.MopeModel.load(os.path.join(data, "mope_builtin_c10000_s7_e3.json"))
+    prof = S.GpuProfile.load_json(os.path.join(data, "profile_default.json"))
+    if cfg == "cfg3":
+        q = W.lmsys_queue(1_000_000, 1000, seed=3 + 100 * rank, heavy_frac=0.5)
+        led = {k: np.zeros(1000) for k in ("ufc", "rfc", "counter")}
+        perf = S.PerfParams(max_batch=4096)
+        desc = "cfg3: 1M-request queue, 1000 clients (client0 = 50%), max_batch 4096 (KV budget cuts)"
+    else:
+        q = W.lmsys_queue(1_000_000, 64, seed=1 + 100 * rank)
+        led = W.warm_ledger(64, seed=2 + 100 * rank)
+        perf = S.PerfParams(max_batch=64)
+        desc = "cfg2: LMSYS-shaped 1M-request queue, 64 clients, warm ledger, max_batch 64"
+    return q, led, perf, model, prof, desc
+
+
+def make_scheduler(q, led, perf, model, prof, device):
+    from paper_2508_16646_b200 import scheduler as S
+    clients = [S.ClientState(n, ufc=float(u), rfc=float(r), counter=float(c))
+               for n, u, r, c in zip(q["client_names"], led["ufc"], led["rfc"], led["counter"])]
+    return S.GpuScheduler(clients, policy=S.PolicySpec(), perf=perf, profile=prof, predictor="mope",
+                          model=model, tag_names=q["tag_names"], device=device), clients
+
+
+def tag_ids(q):
+    return np.where(q["tag"] < 0, 0, q["tag"] + 1).astype(np.uint8)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_baseline(q, led, model, prof, reps: int, cores_note="1 (single-threaded reference engine)"):
+    """The reference's own step (oracle/_ref, compiled from /root/reference sources) on the
+    same queue: drain_arrivals + admit_requests through the reference objects."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import harness as H
+    kind = "reference" if H.available("ref") else "port"
+    case = H.StepCase(client=q["client"], arrival=q["arrival"], in_tokens=q["in_tokens"], true_out=q["true_out"],
+                      tag=q["tag"], client_names=q["client_names"], model=model.to_json(),
+                      profile={"upper": [e.bucket_upper for e in prof.entries],
+                               "lat": [e.latency_ms for e in prof.entries],
+                               "util": [e.gpu_util for e in prof.entries],
+                               "tps": [e.tps for e in prof.entries]},
+                      ufc0=led["ufc"], rfc0=led["rfc"], counter0=led["counter"])
+    times = []
+    out = None
+    for _ in range(reps):
+        out = H.run_step(case, "ref" if kind == "reference" else "oracle")
+        times.append((out["ns_drain"] + out["ns_admit"]) * 1e-9 if kind == "reference" else None)
+    if kind != "reference" or any(t is None for t in times):
+        return None, kind, out
+    return times, kind, out
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    q, led, perf, model, prof, desc = load_inputs(args.config, 0)
+    n = len(q["client"])
+    times, kind, _ = cpu_baseline(q, led, model, prof, args.warmup + args.steps)
+    t = np.array(times[args.warmup:])
+    val = n / float(np.mean(t))
+    line = {
+        "impl": "reference", "metric": "requests scored+scheduled/sec", "value": val, "unit": "requests/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.mean(t) * 1e3),
+        "p50_ms": float(np.median(t) * 1e3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": desc, "policy": "equinox max_over_clients", "predictor": "mope(3)"},
+        "cpu_baseline": {"value": val, "unit": "requests/s", "cores": 1, "kind": kind,
+                         "sample": f"full {n}-request step x {args.steps} (drain_arrivals + admit_requests "
+                                   "via the reference objects, oracle/_ref)"},
+        "e2e": {"value": val, "unit": "requests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world):
+    import torch
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    q, led, perf, model, prof, desc = load_inputs(args.config, rank)
+    n = len(q["client"])
+    sch, clients = make_scheduler(q, led, perf, model, prof, local)
+    dev = torch.device("cuda", local)
+    cols = dict(client=torch.from_numpy(q["client"]).to(dev), arrival_s=torch.from_numpy(q["arrival"]).to(dev),
+                input_tokens=torch.from_numpy(q["in_tokens"]).to(dev), tag=torch.from_numpy(tag_ids(q)).to(dev))
+    stream = torch.cuda.ExternalStream(sch.stream_ptr, device=dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    def one_step(timed: bool):
+        sch.set_clients(clients)  # reset the ledger: every step is the same cold step
+        with torch.cuda.stream(stream):
+            flush.zero_()
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0.record(stream)
+            sch.drain(**cols)
+            e1.record(stream)
+            sch.step_async(1.0)
+            e2.record(stream)
+        res = sch.collect(with_events=False)
+        return e0, e1, e2, res
+
+    for _ in range(args.warmup):
+        one_step(False)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    recs = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            recs.append(one_step(True))
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    step_ms = np.array([a.elapsed_time(c) for a, b, c, _ in recs])
+    drain_ms = np.array([a.elapsed_time(b) for a, b, c, _ in recs])
+    kern_ms = np.array([b.elapsed_time(c) for a, b, c, _ in recs])
+    res = recs[-1][3]
+    total_ms = float(step_ms.sum())
+    if dist:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = world * n * args.steps / (total_ms * 1e-3)
+
+    # ---- e2e through the public API with pinned host buffers ----
+    host = {k: torch.from_numpy(v).pin_memory() for k, v in
+            dict(client=q["client"], arrival_s=q["arrival"], input_tokens=q["in_tokens"], tag=tag_ids(q)).items()}
+    e2e_t = []
+    d2h = 0
+    for i in range(args.warmup + max(3, args.steps // 4)):
+        sch.set_clients(clients)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sch.drain(**host)
+        r = sch.step(1.0, with_events=True)
+        led_out = sch.ledger()
+        t1 = time.perf_counter()
+        if i >= args.warmup:
+            e2e_t.append(t1 - t0)
+        d2h = r.ids.nbytes + r.kinds.nbytes + r.clients.nbytes + r.preds.nbytes + 4 * r.ufc_inc.nbytes + \
+            sum(v.nbytes for v in led_out.values()) + 80
+    h2d = sum(v.numel() * v.element_size() for v in host.values())
+    e2e_val = world * n / float(np.median(e2e_t))
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peak, peak_src = 6449.4, "MEASURED_PEAKS.json hbm_gbs (measured)"
+    if os.path.exists(peaks_path):
+        with open(peaks_path) as f:
+            peak = float(json.load(f).get("hbm_gbs", peak))
+    else:
+        peak_src = "fallback 6650 GB/s (B200_PROFILING.md)"
+        peak = 6650.0
+    k_ms = float(np.mean(kern_ms))
+    achieved = n * ALGO_BYTES_K1 / (k_ms * 1e-3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "step_kernel_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+    line = {
+        "metric": "requests scored+scheduled/sec", "value": value, "unit": "requests/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "p50_ms": float(np.median(step_ms)), "p99_ms": float(np.percentile(step_ms, 99)),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": desc, "policy": "equinox (alpha 0.7, delta 0.1, max_over_clients)",
+                   "predictor": "mope(3) trained by the reference on its builtin corpus (seed 7)",
+                   "queue_per_gpu": n, "l2": "flushed between steps (256 MiB memset outside the events)",
+                   "parallelism": f"client-sharded replicas x{world}" if world > 1 else "single GPU"},
+        "breakdown_ms": {"drain_p50": float(np.median(drain_ms)), "step_kernel_p50": float(np.median(kern_ms))},
+        "admitted": res.n_admitted,
+        "roofline": {"bound": "hbm", "kernel": "step_kernel (fused whole-queue scoring + selection CTA)",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "algo_bytes_per_request": ALGO_BYTES_K1, "peak_source": peak_src},
+        "e2e": {"value": e2e_val, "unit": "requests/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "p50_ms": float(np.median(e2e_t) * 1e3)},
+        "gpu_launches": 5 * args.steps,
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline:
+        times, kind, _ = cpu_baseline(q, led, model, prof, args.cpu_reps)
+        if times:
+            t = np.array(times[1:] if len(times) > 1 else times)
+            line["cpu_baseline"] = {"value": n / float(np.mean(t)), "unit": "requests/s", "cores": 1, "kind": kind,
+                                    "sample": f"the same {n}-request cold step x {len(t)} through the reference "
+                                              "objects (oracle/_ref), 1 host thread"}
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3"])
+    ap.add_argument("--cpu-reps", type=int, default=6)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,196 @@
+/*
+ * eqx.h -- C ABI of the B200-native Equinox per-step scheduling path (libeqx_b200.so).
+ *
+ * The reference (arXiv 2508.16646, /root/reference/proj) exposes this path only through C++
+ * (`equinox::SchedulerPolicy`, `run_simulation`) and a pybind11 module; it has no C ABI or
+ * plugin registry.  These entry points sit *beneath* that API: a host mirror
+ * (C++ or Python) drives them exactly where the reference engine runs
+ * `SimulationRun::drain_arrivals` (engine.cpp:171-197) and `SimulationRun::admit_requests`
+ * (engine.cpp:207-271).  Plain pointers and sizes only; no exceptions cross the ABI; every
+ * call returns an eqx_status and leaves a message retrievable with eqx_last_error().
+ *
+ * Status -> reference exception mapping (errors.hpp:10-31, module.cpp:53-56):
+ *   EQX_ERR_CONFIG -> ConfigError (ValueError in Python)     EQX_ERR_PARSE -> ParseError
+ *   EQX_ERR_ENGINE -> EngineError (RuntimeError)             EQX_ERR_CUDA  -> EngineError
+ *
+ * Threading: one context per engine instance, owning one CUDA stream; not thread-safe
+ * (scheduler.hpp:97-100).  Several contexts may share a device (replicas).
+ */
+#ifndef EQX_H
+#define EQX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EQX_ABI_VERSION 1
+
+typedef enum {
+  EQX_OK = 0,
+  EQX_ERR_CONFIG = 1, /* invalid parameter: ConfigError */
+  EQX_ERR_PARSE = 2,  /* malformed model/profile tables: ParseError */
+  EQX_ERR_ENGINE = 3, /* consistency violation: EngineError */
+  EQX_ERR_CUDA = 4,   /* CUDA runtime/driver failure (reported as EngineError) */
+  EQX_ERR_ARG = 5     /* NULL/out-of-range argument to this ABI */
+} eqx_status;
+
+/* PolicyKind (scheduler.hpp:66), NormMode (scheduler.hpp:14) */
+enum { EQX_FCFS = 0, EQX_VTC = 1, EQX_EQUINOX = 2 };
+enum { EQX_NORM_MAX_OVER_CLIENTS = 0, EQX_NORM_NONE = 1 };
+/* Predictor implementations (predictor.hpp:34-129) */
+enum { EQX_PRED_ORACLE = 0, EQX_PRED_MOPE = 1, EQX_PRED_NOISY_ORACLE = 2, EQX_PRED_SINGLE_PROXY = 3 };
+/* LogEvent::Admitted / LogEvent::Rejected (engine.hpp:33) */
+enum { EQX_EV_ADMITTED = 1, EQX_EV_REJECTED = 2 };
+/* where the pointers of an eqx_requests batch live */
+enum { EQX_HOST = 0, EQX_DEVICE = 1 };
+
+typedef struct eqx_ctx eqx_ctx;
+
+/* PolicySpec (scheduler.hpp:71-81) + EquinoxParams (scheduler.hpp:18-26)
+ * + EngineConfig::backfill (engine.hpp:25). */
+typedef struct {
+  int32_t kind;
+  double alpha, delta, output_weight;
+  int32_t norm_mode;
+  int32_t vtc_use_prediction;
+  int32_t counter_lift;
+  int32_t backfill;
+} eqx_policy;
+
+/* The admission-control fields of PerfParams (gpu_model.hpp:14-28). */
+typedef struct {
+  int32_t max_batch;
+  double mem_per_token_bytes;
+  double mem_capacity_bytes;
+} eqx_perf;
+
+/* GpuProfile (gpu_model.hpp:61-77): entries in roster order, bucket_upper per entry. */
+typedef struct {
+  int32_t n;
+  const int32_t* bucket_upper;
+  const double* latency_ms;
+  const double* gpu_util;
+  const double* tps;
+} eqx_profile;
+
+/* MopeModel (predictor.hpp:56-92) as flat tables.  keyword_scores rows are addressed through
+ * tag_row: request tag id t in [1, n_tags] uses row tag_row[t-1] (-1 = tag unseen by the
+ * router -> length fallback, predictor.cpp:43-47); tag id 0 = untagged.  All experts share
+ * n_bins (train_mope fits them over shared bins, predictor.cpp:313).  SINGLE_PROXY uses
+ * expert 0 (ExpertModel, predictor.hpp:118-129). */
+typedef struct {
+  int32_t n_thresholds;
+  const int32_t* thresholds;
+  double mix_weight;
+  int32_t num_buckets;
+  int32_t n_rows;
+  const double* rows; /* [n_rows][num_buckets] */
+  int32_t n_experts;
+  int32_t n_bins;
+  const int32_t* bin_upper; /* [n_experts][n_bins] */
+  const int32_t* bin_value; /* [n_experts][n_bins] */
+  const int32_t* out_min;   /* [n_experts] */
+  const int32_t* out_max;   /* [n_experts] */
+  int32_t n_tags;
+  const int32_t* tag_row;   /* [n_tags] */
+} eqx_mope;
+
+typedef struct {
+  int32_t kind;        /* EQX_PRED_* */
+  eqx_mope mope;       /* MOPE, SINGLE_PROXY */
+  double noisy_l1;     /* NOISY_ORACLE: NoisyOraclePredictor(target_l1, seed) */
+  uint64_t noisy_seed;
+} eqx_predictor;
+
+/* A batch of queued requests in arrival order (Request, workload.hpp:16-23), struct of arrays.
+ * location EQX_DEVICE means every pointer is device memory on the context's device; those
+ * arrays are used in place (no copy) and must outlive the queue.  EQX_HOST arrays are copied. */
+typedef struct {
+  int64_t n;
+  const int64_t* id;              /* NULL: id = id_base + row */
+  int64_t id_base;
+  const int32_t* client;          /* roster index of client_id */
+  const double* arrival_s;        /* arrival_time_s, non-decreasing */
+  const int32_t* input_tokens;
+  const int32_t* true_output_tokens; /* ORACLE / NOISY_ORACLE only; may be NULL otherwise */
+  const uint8_t* tag;             /* category_tag as a tag id (see eqx_mope.tag_row) */
+  int32_t location;               /* EQX_HOST / EQX_DEVICE */
+} eqx_requests;
+
+typedef struct {
+  int64_t n_events;          /* admitted + rejected, in log order */
+  int64_t n_admitted;
+  int64_t n_rejected;
+  int64_t new_prefill_tokens; /* admit_requests() return value (engine.cpp:270) */
+  int64_t length_fallbacks;   /* MopePredictor::length_fallbacks() over scored requests */
+  int64_t noisy_near_ties;    /* NOISY_ORACLE: predictions within 1e-9 of a .5 boundary */
+  int32_t batch_members;      /* BatchState::members.size() after the step */
+  int64_t batch_reserved_kv_tokens; /* BatchState::reserved_kv_tokens() after the step */
+  int64_t queued;             /* requests still queued after the step */
+} eqx_step_summary;
+
+/* ---- context ---------------------------------------------------------------------------- */
+int32_t eqx_abi_version(void);
+eqx_status eqx_ctx_create(int32_t device, eqx_ctx** out);
+void eqx_ctx_destroy(eqx_ctx* ctx);
+/* Message for the last failing call on ctx (ctx may be NULL for eqx_ctx_create failures). */
+const char* eqx_last_error(const eqx_ctx* ctx);
+/* The cudaStream_t the context launches on (as void*), for event timing by the caller. */
+void* eqx_ctx_stream(eqx_ctx* ctx);
+
+/* ---- configuration (SchedulerPolicy ctor, scheduler.cpp:92-100; validate() :11-17) ------ */
+eqx_status eqx_set_policy(eqx_ctx* ctx, const eqx_policy* policy);
+eqx_status eqx_set_perf(eqx_ctx* ctx, const eqx_perf* perf);
+eqx_status eqx_set_profile(eqx_ctx* ctx, const eqx_profile* profile);
+eqx_status eqx_set_predictor(eqx_ctx* ctx, const eqx_predictor* predictor);
+/* Client roster + ledger (ClientState, scheduler.hpp:35-43).  names: n NUL-terminated
+ * client_id strings concatenated (ties in selection break on their bytes, scheduler.cpp:144).
+ * running[c] = requests of client c currently in the batch (engine.cpp:182 running_count_). */
+eqx_status eqx_set_clients(eqx_ctx* ctx, int32_t n, const char* names, const double* weight,
+                           const double* ufc, const double* rfc, const double* counter,
+                           const int32_t* running);
+eqx_status eqx_get_clients(eqx_ctx* ctx, int32_t n, double* ufc, double* rfc, double* counter,
+                           int32_t* backlogged, int32_t* running);
+/* Existing batch: BatchState::members.size() and reserved_kv_tokens() (gpu_model.cpp:40-46). */
+eqx_status eqx_set_batch(eqx_ctx* ctx, int32_t members, int64_t reserved_kv_tokens);
+
+/* ---- the hot path ------------------------------------------------------------------------ */
+/* drain_arrivals (engine.cpp:171-197) for a whole batch of arrivals: the batch becomes the
+ * per-client FIFO queues (client-grouped index in HBM), clients that go idle -> backlogged get
+ * the counter lift (on_activated, scheduler.cpp:235-253) in arrival order, and every
+ * arriving client is marked backlogged.  Replaces any previously queued requests. */
+eqx_status eqx_drain(eqx_ctx* ctx, const eqx_requests* arrivals);
+/* admit_requests (engine.cpp:207-271) at simulated time `now`, plus per-request scoring of the
+ * whole queue: MoPE gate+experts -> map_metrics -> ufc/rfc increments (the prediction
+ * record as of drain).  Enqueued on the context stream; results stay on the device. */
+eqx_status eqx_step_async(eqx_ctx* ctx, double now);
+/* Waits for the last step and returns its summary. */
+eqx_status eqx_step_collect(eqx_ctx* ctx, eqx_step_summary* out);
+/* Convenience: eqx_step_async + eqx_step_collect. */
+eqx_status eqx_step(eqx_ctx* ctx, double now, eqx_step_summary* out);
+
+/* ---- results (host copies; any pointer may be NULL) ------------------------------------- */
+/* Event log of the last step in order: request id, EQX_EV_*, client, predicted output tokens
+ * and the PendingContribution of admissions (scheduler.hpp:131-138: ufc/rfc/vtc increment and
+ * ScheduleContext::wait_s); rejections carry zeros. */
+eqx_status eqx_copy_events(eqx_ctx* ctx, int64_t cap, int64_t* id, int32_t* kind,
+                           int32_t* client, int32_t* pred, double* ufc_inc, double* rfc_inc,
+                           double* vtc_inc, double* wait_s);
+/* Per-request scores of the queue (row order of the drained batch): predicted output tokens,
+ * profile bucket, ufc_increment and rfc_increment at the step's `now`. */
+eqx_status eqx_copy_scores(eqx_ctx* ctx, int64_t cap, int32_t* pred, uint8_t* bucket,
+                           double* ufc_inc, double* rfc_inc);
+
+/* ---- host scalar utilities (bindings/module.cpp:144-172 `ufc_increment`/`rfc_increment`) - */
+double eqx_ufc_increment(double weight, int32_t input_tokens, int32_t predicted_output_tokens,
+                         double wait_s, double predicted_latency_ms, double delta,
+                         double output_weight);
+double eqx_rfc_increment(double weight, double tps, double gpu_util);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EQX_H */

@@ -1,0 +1,341 @@
+"""ctypes harness over the two CPU oracles -- TEST INFRASTRUCTURE ONLY.
+
+Loads
+  * ``oracle/liboracle.so``       -- the plain-C restatement (oracle/eqx_oracle.c), and
+  * ``oracle/_ref/libeqx_ref.so`` -- the reference's own code compiled from
+    /root/reference/proj/src plus the ref_step.cpp driver (oracle/Makefile ``ref``),
+and runs one scheduling step (eqx_oracle.h) on numpy arrays.  Only tests/,
+__graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs import this.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_ORACLE = os.path.join(HERE, "liboracle.so")
+LIB_REF = os.path.join(HERE, "_ref", "libeqx_ref.so")
+
+FCFS, VTC, EQUINOX = 0, 1, 2
+NORM_MAX, NORM_NONE = 0, 1
+PRED_ORACLE, PRED_MOPE, PRED_NOISY, PRED_SINGLE = 0, 1, 2, 3
+EV_ADMIT, EV_REJECT = 1, 2
+
+_dp = C.POINTER(C.c_double)
+_i32p = C.POINTER(C.c_int32)
+_i64p = C.POINTER(C.c_int64)
+
+
+class Mope(C.Structure):
+    _fields_ = [
+        ("n_thresholds", C.c_int32), ("thresholds", _i32p), ("mix_weight", C.c_double),
+        ("num_buckets", C.c_int32), ("n_rows", C.c_int32), ("rows", _dp),
+        ("n_experts", C.c_int32), ("n_bins", C.c_int32), ("bin_upper", _i32p),
+        ("bin_value", _i32p), ("out_min", _i32p), ("out_max", _i32p),
+    ]
+
+
+class StepIn(C.Structure):
+    _fields_ = [
+        ("kind", C.c_int32), ("alpha", C.c_double), ("delta", C.c_double),
+        ("output_weight", C.c_double), ("norm_mode", C.c_int32),
+        ("vtc_use_prediction", C.c_int32), ("counter_lift", C.c_int32), ("backfill", C.c_int32),
+        ("max_batch", C.c_int32), ("mem_per_token_bytes", C.c_double),
+        ("mem_capacity_bytes", C.c_double),
+        ("n_profile", C.c_int32), ("prof_upper", _i32p), ("prof_lat", _dp), ("prof_util", _dp),
+        ("prof_tps", _dp),
+        ("pred_kind", C.c_int32), ("mope", Mope), ("noisy_l1", C.c_double),
+        ("noisy_seed", C.c_uint64),
+        ("n_clients", C.c_int32), ("client_names", C.c_char_p), ("weight", _dp), ("ufc0", _dp),
+        ("rfc0", _dp), ("counter0", _dp), ("running", _i32p),
+        ("n_members", C.c_int32), ("mem_in", _i32p), ("mem_generated", _i32p),
+        ("mem_reserved", _i32p),
+        ("n_req", C.c_int64), ("id", _i64p), ("client", _i32p), ("arrival", _dp),
+        ("in_tokens", _i32p), ("true_out", _i32p), ("tag", _i32p), ("n_tags", C.c_int32),
+        ("tag_names", C.c_char_p), ("tag_row", _i32p), ("now", C.c_double),
+    ]
+
+
+class StepOut(C.Structure):
+    _fields_ = [
+        ("pred", _i32p), ("bucket", _i32p), ("lat", _dp), ("util", _dp), ("tps", _dp),
+        ("ufc_inc", _dp), ("rfc_inc", _dp),
+        ("n_events", C.c_int64), ("ev_id", _i64p), ("ev_kind", _i32p), ("ev_client", _i32p),
+        ("ev_ufc_inc", _dp), ("ev_rfc_inc", _dp), ("ev_vtc_inc", _dp), ("ev_wait", _dp),
+        ("ufc", _dp), ("rfc", _dp), ("counter", _dp), ("backlogged", _i32p),
+        ("n_admitted", C.c_int64), ("n_rejected", C.c_int64), ("new_prefill", C.c_int64),
+        ("length_fallbacks", C.c_int64), ("ns_drain", C.c_double), ("ns_admit", C.c_double),
+    ]
+
+
+def _ptr(a, ct):
+    return a.ctypes.data_as(C.POINTER(ct))
+
+
+@dataclass
+class StepCase:
+    """Everything one scheduling step consumes (numpy arrays + scalars)."""
+
+    # requests (arrival order)
+    client: np.ndarray
+    arrival: np.ndarray
+    in_tokens: np.ndarray
+    true_out: np.ndarray
+    tag: np.ndarray                      # -1 = untagged, else index into tag_names
+    id: np.ndarray | None = None
+    # roster
+    client_names: list = field(default_factory=list)
+    weight: np.ndarray | None = None
+    ufc0: np.ndarray | None = None
+    rfc0: np.ndarray | None = None
+    counter0: np.ndarray | None = None
+    running: np.ndarray | None = None
+    # batch
+    mem_in: np.ndarray | None = None
+    mem_generated: np.ndarray | None = None
+    mem_reserved: np.ndarray | None = None
+    # tags / model
+    tag_names: list = field(default_factory=lambda: ["short", "medium", "long"])
+    model: dict | None = None            # reference MopeModel JSON (predictor.cpp:408-430)
+    pred_kind: int = PRED_MOPE
+    noisy_l1: float = 33.0
+    noisy_seed: int = 1
+    # profile
+    profile: dict | None = None          # {"upper","lat","util","tps"}
+    # policy / perf
+    kind: int = EQUINOX
+    alpha: float = 0.7
+    delta: float = 0.1
+    output_weight: float = 4.0
+    norm_mode: int = NORM_MAX
+    vtc_use_prediction: bool = False
+    counter_lift: bool = True
+    backfill: bool = False
+    max_batch: int = 64
+    mem_per_token_bytes: float = 0.5 * 1024.0 * 1024.0
+    mem_capacity_bytes: float = 60.0 * 1024.0 * 1024.0 * 1024.0
+    now: float = 1.0
+
+    def finalize(self):
+        n = len(self.client)
+        C_ = len(self.client_names)
+        if self.id is None:
+            self.id = np.arange(n, dtype=np.int64)
+        z = np.zeros(C_, dtype=np.float64)
+        self.weight = np.ones(C_) if self.weight is None else self.weight
+        self.ufc0 = z.copy() if self.ufc0 is None else self.ufc0
+        self.rfc0 = z.copy() if self.rfc0 is None else self.rfc0
+        self.counter0 = z.copy() if self.counter0 is None else self.counter0
+        self.running = np.zeros(C_, np.int32) if self.running is None else self.running
+        e = np.zeros(0, np.int32)
+        self.mem_in = e if self.mem_in is None else self.mem_in
+        self.mem_generated = np.zeros_like(self.mem_in) if self.mem_generated is None else self.mem_generated
+        self.mem_reserved = np.zeros_like(self.mem_in) if self.mem_reserved is None else self.mem_reserved
+        return self
+
+
+def mope_arrays(model: dict, tag_names: list):
+    """Flatten a reference MopeModel JSON into the eqxo_mope arrays + per-tag row map."""
+    r = model["router"]
+    ks = r["keyword_scores"]
+    row_names = sorted(ks.keys())  # std::map order (bytewise)
+    nb = int(r["num_buckets"])
+    rows = np.array([ks[k] for k in row_names], dtype=np.float64).reshape(len(row_names), nb)
+    ex = model["experts"]
+    nbins = len(ex[0]["bin_upper"])
+    return dict(
+        thresholds=np.array(r["input_len_thresholds"], np.int32),
+        mix=float(r["mix_weight"]), num_buckets=nb, rows=rows,
+        bin_upper=np.array([e["bin_upper"] for e in ex], np.int32).reshape(len(ex), nbins),
+        bin_value=np.array([e["bin_value"] for e in ex], np.int32).reshape(len(ex), nbins),
+        out_min=np.array([e["out_min"] for e in ex], np.int32),
+        out_max=np.array([e["out_max"] for e in ex], np.int32),
+        tag_row=np.array([row_names.index(t) if t in ks else -1 for t in tag_names], np.int32),
+    )
+
+
+def _build_in(case: StepCase, keep: list) -> StepIn:
+    case.finalize()
+
+    def arr(a, dt):
+        a = np.ascontiguousarray(a, dtype=dt)
+        keep.append(a)
+        return a
+
+    s = StepIn()
+    s.kind, s.alpha, s.delta, s.output_weight = case.kind, case.alpha, case.delta, case.output_weight
+    s.norm_mode = case.norm_mode
+    s.vtc_use_prediction, s.counter_lift, s.backfill = int(case.vtc_use_prediction), int(case.counter_lift), int(case.backfill)
+    s.max_batch = case.max_batch
+    s.mem_per_token_bytes, s.mem_capacity_bytes = case.mem_per_token_bytes, case.mem_capacity_bytes
+    p = case.profile
+    s.n_profile = len(p["upper"])
+    s.prof_upper = _ptr(arr(p["upper"], np.int32), C.c_int32)
+    s.prof_lat = _ptr(arr(p["lat"], np.float64), C.c_double)
+    s.prof_util = _ptr(arr(p["util"], np.float64), C.c_double)
+    s.prof_tps = _ptr(arr(p["tps"], np.float64), C.c_double)
+    s.pred_kind = case.pred_kind
+    s.noisy_l1, s.noisy_seed = case.noisy_l1, case.noisy_seed
+    if case.model is not None:
+        m = mope_arrays(case.model, case.tag_names)
+        s.mope.n_thresholds = len(m["thresholds"])
+        s.mope.thresholds = _ptr(arr(m["thresholds"], np.int32), C.c_int32)
+        s.mope.mix_weight = m["mix"]
+        s.mope.num_buckets = m["num_buckets"]
+        s.mope.n_rows = m["rows"].shape[0]
+        s.mope.rows = _ptr(arr(m["rows"], np.float64), C.c_double)
+        s.mope.n_experts, s.mope.n_bins = m["bin_upper"].shape
+        s.mope.bin_upper = _ptr(arr(m["bin_upper"], np.int32), C.c_int32)
+        s.mope.bin_value = _ptr(arr(m["bin_value"], np.int32), C.c_int32)
+        s.mope.out_min = _ptr(arr(m["out_min"], np.int32), C.c_int32)
+        s.mope.out_max = _ptr(arr(m["out_max"], np.int32), C.c_int32)
+        tag_row = m["tag_row"]
+    else:
+        tag_row = -np.ones(len(case.tag_names), np.int32)
+    s.n_clients = len(case.client_names)
+    names = b"".join(n.encode() + b"\0" for n in case.client_names)
+    keep.append(names)
+    s.client_names = names
+    s.weight = _ptr(arr(case.weight, np.float64), C.c_double)
+    s.ufc0 = _ptr(arr(case.ufc0, np.float64), C.c_double)
+    s.rfc0 = _ptr(arr(case.rfc0, np.float64), C.c_double)
+    s.counter0 = _ptr(arr(case.counter0, np.float64), C.c_double)
+    s.running = _ptr(arr(case.running, np.int32), C.c_int32)
+    s.n_members = len(case.mem_in)
+    s.mem_in = _ptr(arr(case.mem_in, np.int32), C.c_int32)
+    s.mem_generated = _ptr(arr(case.mem_generated, np.int32), C.c_int32)
+    s.mem_reserved = _ptr(arr(case.mem_reserved, np.int32), C.c_int32)
+    s.n_req = len(case.client)
+    s.id = _ptr(arr(case.id, np.int64), C.c_int64)
+    s.client = _ptr(arr(case.client, np.int32), C.c_int32)
+    s.arrival = _ptr(arr(case.arrival, np.float64), C.c_double)
+    s.in_tokens = _ptr(arr(case.in_tokens, np.int32), C.c_int32)
+    s.true_out = _ptr(arr(case.true_out, np.int32), C.c_int32)
+    s.tag = _ptr(arr(case.tag, np.int32), C.c_int32)
+    s.n_tags = len(case.tag_names)
+    tn = b"".join(n.encode() + b"\0" for n in case.tag_names)
+    keep.append(tn)
+    s.tag_names = tn
+    s.tag_row = _ptr(arr(tag_row, np.int32), C.c_int32)
+    s.now = case.now
+    return s
+
+
+_libs: dict = {}
+
+
+def _lib(which: str):
+    if which not in _libs:
+        path = LIB_REF if which == "ref" else LIB_ORACLE
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} not built (run __graft_entry__.build())")
+        lib = C.CDLL(path)
+        fn = lib.ref_step if which == "ref" else lib.eqxo_step
+        fn.argtypes = [C.POINTER(StepIn), C.POINTER(StepOut), C.c_char_p, C.c_int]
+        fn.restype = C.c_int
+        _libs[which] = (lib, fn)
+    return _libs[which]
+
+
+def available(which: str) -> bool:
+    return os.path.exists(LIB_REF if which == "ref" else LIB_ORACLE)
+
+
+def run_step(case: StepCase, which: str = "oracle") -> dict:
+    """Run one step on the C restatement (``oracle``) or the reference build (``ref``)."""
+    keep: list = []
+    s = _build_in(case, keep)
+    n, nc = int(s.n_req), int(s.n_clients)
+    o = {
+        "pred": np.zeros(n, np.int32), "bucket": np.zeros(n, np.int32),
+        "lat": np.zeros(n), "util": np.zeros(n), "tps": np.zeros(n),
+        "ufc_inc": np.zeros(n), "rfc_inc": np.zeros(n),
+        "ev_id": np.zeros(max(n, 1), np.int64), "ev_kind": np.zeros(max(n, 1), np.int32),
+        "ev_client": np.zeros(max(n, 1), np.int32), "ev_ufc_inc": np.zeros(max(n, 1)),
+        "ev_rfc_inc": np.zeros(max(n, 1)), "ev_vtc_inc": np.zeros(max(n, 1)),
+        "ev_wait": np.zeros(max(n, 1)),
+        "ufc": np.zeros(nc), "rfc": np.zeros(nc), "counter": np.zeros(nc),
+        "backlogged": np.zeros(nc, np.int32),
+    }
+    so = StepOut()
+    for k, v in o.items():
+        setattr(so, k, _ptr(v, np.ctypeslib.as_ctypes_type(v.dtype)))
+    err = C.create_string_buffer(512)
+    _, fn = _lib(which)
+    rc = fn(C.byref(s), C.byref(so), err, 512)
+    if rc != 0:
+        raise ValueError(err.value.decode())
+    ne = int(so.n_events)
+    for k in list(o):
+        if k.startswith("ev_"):
+            o[k] = o[k][:ne]
+    o.update(n_events=ne, n_admitted=int(so.n_admitted), n_rejected=int(so.n_rejected),
+             new_prefill=int(so.new_prefill), length_fallbacks=int(so.length_fallbacks),
+             ns_drain=float(so.ns_drain), ns_admit=float(so.ns_admit))
+    return o
+
+
+# ---- reference fixture helpers (ref build only) ----------------------------------------
+def ref_train_mope_json(corpus_size=10000, seed=7, experts=3) -> str:
+    lib, _ = _lib("ref")
+    f = lib.ref_train_mope_json
+    f.argtypes = [C.c_int, C.c_uint64, C.c_int, C.c_char_p, C.c_int64]
+    f.restype = C.c_int64
+    n = f(corpus_size, seed, experts, None, 0)
+    buf = C.create_string_buffer(int(n))
+    f(corpus_size, seed, experts, buf, n)
+    return buf.value.decode()
+
+
+def ref_build_profile(bounds=(32, 64, 128, 256, 512, 1024, 2048, 4096), ref_input=1) -> dict:
+    lib, _ = _lib("ref")
+    n = len(bounds)
+    b = np.array(bounds, np.int32)
+    up = np.zeros(n, np.int32)
+    lat, util, tps = np.zeros(n), np.zeros(n), np.zeros(n)
+    lib.ref_build_profile.restype = C.c_int
+    rc = lib.ref_build_profile(_ptr(b, C.c_int32), C.c_int(n), C.c_int(ref_input),
+                               _ptr(up, C.c_int32), _ptr(lat, C.c_double),
+                               _ptr(util, C.c_double), _ptr(tps, C.c_double))
+    if rc != 0:
+        raise ValueError("build_profile rejected its arguments")
+    return {"upper": up, "lat": lat, "util": util, "tps": tps}
+
+
+def ref_noisy_predict(l1, seed, ids, true_out):
+    lib, _ = _lib("ref")
+    ids = np.ascontiguousarray(ids, np.int64)
+    t = np.ascontiguousarray(true_out, np.int32)
+    out = np.zeros(len(ids), np.int32)
+    lib.ref_noisy_predict.argtypes = [C.c_double, C.c_uint64, C.c_int64, _i64p, _i32p, _i32p]
+    lib.ref_noisy_predict(l1, seed, len(ids), _ptr(ids, C.c_int64), _ptr(t, C.c_int32),
+                          _ptr(out, C.c_int32))
+    return out
+
+
+def ref_replay(case: StepCase, max_sim_time_s=3600.0, ema_alpha=0.2, cap=None):
+    """Full run_simulation replay; returns (ev_id, ev_kind, ev_time, ufc, rfc, counter)."""
+    lib, _ = _lib("ref")
+    keep: list = []
+    s = _build_in(case, keep)
+    cap = cap or max(1, 2 * int(s.n_req))
+    ev_id = np.zeros(cap, np.int64)
+    ev_kind = np.zeros(cap, np.int32)
+    ev_time = np.zeros(cap)
+    nc = int(s.n_clients)
+    u, r, c = np.zeros(nc), np.zeros(nc), np.zeros(nc)
+    err = C.create_string_buffer(512)
+    f = lib.ref_replay
+    f.argtypes = [C.POINTER(StepIn), C.c_double, C.c_double, _i64p, _i32p, _dp, C.c_int64,
+                  _dp, _dp, _dp, C.c_char_p, C.c_int]
+    f.restype = C.c_int64
+    n = f(C.byref(s), max_sim_time_s, ema_alpha, _ptr(ev_id, C.c_int64), _ptr(ev_kind, C.c_int32),
+          _ptr(ev_time, C.c_double), cap, _ptr(u, C.c_double), _ptr(r, C.c_double),
+          _ptr(c, C.c_double), err, 512)
+    if n < 0:
+        raise ValueError(err.value.decode())
+    n = min(int(n), cap)
+    return ev_id[:n], ev_kind[:n], ev_time[:n], u, r, c

@@ -1,0 +1,457 @@
+// ref_step.cpp -- TEST INFRASTRUCTURE ONLY.
+//
+// A thin driver over the reference's *public* C++ API (compiled from the unmodified sources
+// under /root/reference/proj/src by oracle/Makefile into oracle/_ref/libeqx_ref.so).  It
+// exposes plain C entry points so tests/ and bench.py (--impl reference, cpu_baseline) can
+// run the reference algorithm on the same arrays the GPU path consumes.  No reference code is
+// copied here: every decision is made by a reference function.
+//
+//   ref_step     -- drain_arrivals + admit_requests (engine.cpp:171-271) re-driven line for
+//                   line through SchedulerPolicy / Predictor / map_metrics / can_fit /
+//                   fits_alone, with a pre-seeded ledger and batch (SURVEY.md 8(c) mode 1).
+//   ref_train_mope_json / ref_build_profile / ref_corpus -- model + profile fixtures.
+//   ref_replay   -- run_simulation (engine.cpp:458-463) on an array trace (mode 2).
+//   ref_units    -- the reference unit-test formulas (ufc/rfc/holistic/route/can_fit).
+
+#include <chrono>
+#include <cstring>
+#include <deque>
+#include <exception>
+#include <memory>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "equinox/engine.hpp"
+#include "equinox/errors.hpp"
+#include "equinox/gpu_model.hpp"
+#include "equinox/predictor.hpp"
+#include "equinox/rng.hpp"
+#include "equinox/scheduler.hpp"
+#include "equinox/workload.hpp"
+
+#include "eqx_oracle.h"
+
+using namespace equinox;
+
+namespace {
+
+std::vector<std::string> split_names(const char* buf, int n) {
+  std::vector<std::string> out;
+  out.reserve(static_cast<std::size_t>(n));
+  const char* p = buf;
+  for (int i = 0; i < n; ++i) {
+    out.emplace_back(p);
+    p += out.back().size() + 1;
+  }
+  return out;
+}
+
+void set_err(char* err, int len, const char* msg) {
+  if (err && len > 0) {
+    std::strncpy(err, msg, static_cast<std::size_t>(len) - 1);
+    err[len - 1] = '\0';
+  }
+}
+
+MopeModel model_from(const eqxo_mope& m, const std::vector<std::string>& tag_names,
+                     const int32_t* tag_row, int n_tags) {
+  MopeModel model;
+  model.router.input_len_thresholds.assign(m.thresholds, m.thresholds + m.n_thresholds);
+  model.router.mix_weight = m.mix_weight;
+  model.router.num_buckets = m.num_buckets;
+  for (int t = 0; t < n_tags; ++t) {
+    if (tag_row[t] < 0) continue;
+    const double* row = m.rows + static_cast<std::size_t>(tag_row[t]) * m.num_buckets;
+    model.router.keyword_scores[tag_names[static_cast<std::size_t>(t)]] =
+        std::vector<double>(row, row + m.num_buckets);
+  }
+  for (int e = 0; e < m.n_experts; ++e) {
+    ExpertModel ex;
+    ex.bucket = e;
+    ex.bin_upper.assign(m.bin_upper + e * m.n_bins, m.bin_upper + (e + 1) * m.n_bins);
+    ex.bin_value.assign(m.bin_value + e * m.n_bins, m.bin_value + (e + 1) * m.n_bins);
+    ex.out_min = m.out_min[e];
+    ex.out_max = m.out_max[e];
+    model.experts.push_back(std::move(ex));
+  }
+  return model;
+}
+
+struct Queued {
+  Request req;
+  PredictionRecord prediction;
+};
+
+}  // namespace
+
+extern "C" {
+
+int ref_step(const eqxo_step_in* in, eqxo_step_out* out, char* err, int err_len) {
+  try {
+    const auto names = split_names(in->client_names, in->n_clients);
+    const auto tags = split_names(in->tag_names, in->n_tags);
+
+    PolicySpec spec;
+    spec.kind = static_cast<PolicyKind>(in->kind);
+    spec.equinox.alpha = in->alpha;
+    spec.equinox.delta = in->delta;
+    spec.equinox.output_weight = in->output_weight;
+    spec.equinox.norm_mode =
+        in->norm_mode == EQXO_NORM_NONE ? NormMode::None : NormMode::MaxOverClients;
+    spec.vtc_use_prediction = in->vtc_use_prediction != 0;
+    spec.counter_lift = in->counter_lift != 0;
+
+    std::vector<ClientState> roster(static_cast<std::size_t>(in->n_clients));
+    for (int c = 0; c < in->n_clients; ++c) {
+      roster[c].client_id = names[c];
+      roster[c].weight = in->weight[c];
+      roster[c].ufc = in->ufc0[c];
+      roster[c].rfc = in->rfc0[c];
+      roster[c].counter = in->counter0[c];
+    }
+    SchedulerPolicy policy(spec, roster);
+
+    PerfParams perf;
+    perf.max_batch = in->max_batch;
+    perf.mem_per_token_bytes = in->mem_per_token_bytes;
+    perf.mem_capacity_bytes = in->mem_capacity_bytes;
+
+    GpuProfile profile;
+    for (int e = 0; e < in->n_profile; ++e) {
+      profile.entries.push_back(
+          {in->prof_upper[e], in->prof_lat[e], in->prof_util[e], in->prof_tps[e]});
+    }
+
+    std::unique_ptr<Predictor> predictor;
+    MopePredictor* mope_ptr = nullptr;
+    switch (in->pred_kind) {
+      case EQXO_PRED_ORACLE:
+        predictor = std::make_unique<OraclePredictor>();
+        break;
+      case EQXO_PRED_NOISY:
+        predictor = std::make_unique<NoisyOraclePredictor>(in->noisy_l1, in->noisy_seed);
+        break;
+      case EQXO_PRED_MOPE: {
+        auto p = std::make_unique<MopePredictor>(
+            model_from(in->mope, tags, in->tag_row, in->n_tags));
+        mope_ptr = p.get();
+        predictor = std::move(p);
+        break;
+      }
+      case EQXO_PRED_SINGLE: {
+        MopeModel m = model_from(in->mope, tags, in->tag_row, in->n_tags);
+        predictor = std::make_unique<SingleProxyPredictor>(m.experts.at(0));
+        break;
+      }
+      default:
+        throw ConfigError("unknown predictor kind");
+    }
+
+    BatchState batch;
+    for (int i = 0; i < in->n_members; ++i) {
+      batch.members.push_back({-1 - i, in->mem_in[i], in->mem_generated[i], in->mem_reserved[i]});
+    }
+
+    // Requests are materialised before the timed region (the engine holds them in its Trace).
+    std::vector<Request> reqs(static_cast<std::size_t>(in->n_req));
+    for (int64_t r = 0; r < in->n_req; ++r) {
+      Request& q = reqs[static_cast<std::size_t>(r)];
+      q.id = in->id[r];
+      q.client_id = names[static_cast<std::size_t>(in->client[r])];
+      q.arrival_time_s = in->arrival[r];
+      q.input_tokens = in->in_tokens[r];
+      q.true_output_tokens = in->true_out[r];
+      if (in->tag[r] >= 0) q.category_tag = tags[static_cast<std::size_t>(in->tag[r])];
+    }
+
+    std::vector<std::deque<Queued>> queues(static_cast<std::size_t>(in->n_clients));
+    std::vector<int> running(in->running, in->running + in->n_clients);
+    std::vector<PredictionRecord> frozen(static_cast<std::size_t>(in->n_req));
+
+    // ---- drain_arrivals (engine.cpp:171-197) ----
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int64_t r = 0; r < in->n_req; ++r) {
+      const Request& req = reqs[static_cast<std::size_t>(r)];
+      const std::size_t ci = static_cast<std::size_t>(in->client[r]);
+      const int predicted = std::max(1, predictor->predict(req));
+      Queued queued{req, map_metrics(predicted, profile)};
+      frozen[static_cast<std::size_t>(r)] = queued.prediction;
+      if (queues[ci].empty() && running[ci] == 0) policy.on_activated(ci);
+      queues[ci].push_back(std::move(queued));
+      policy.set_backlogged(ci, true);
+    }
+    const auto t1 = std::chrono::steady_clock::now();
+
+    // ---- admit_requests (engine.cpp:207-271) ----
+    int64_t n_ev = 0, n_adm = 0, n_rej = 0, new_prefill = 0;
+    auto pop_head = [&](std::size_t ci) {
+      queues[ci].pop_front();
+      if (queues[ci].empty()) policy.set_backlogged(ci, false);
+    };
+    std::set<std::size_t> skipped;
+    while (true) {
+      std::vector<HeadCandidate> candidates;
+      for (std::size_t i = 0; i < queues.size(); ++i) {
+        if (queues[i].empty() || skipped.count(i) != 0) continue;
+        candidates.push_back({i, queues[i].front().req.arrival_time_s});
+      }
+      const auto choice = policy.select_next(candidates);
+      if (!choice) break;
+      const std::size_t ci = *choice;
+      const Queued head = queues[ci].front();
+      const int tin = head.req.input_tokens;
+      const int predicted = head.prediction.predicted_output_tokens;
+      if (!fits_alone(tin, predicted, perf)) {
+        out->ev_id[n_ev] = head.req.id;
+        out->ev_kind[n_ev] = EQXO_EV_REJECT;
+        out->ev_client[n_ev] = static_cast<int32_t>(ci);
+        out->ev_ufc_inc[n_ev] = out->ev_rfc_inc[n_ev] = out->ev_vtc_inc[n_ev] = 0.0;
+        out->ev_wait[n_ev] = 0.0;
+        ++n_ev;
+        ++n_rej;
+        pop_head(ci);
+        continue;
+      }
+      if (!can_fit(batch, tin, predicted, perf)) {
+        if (in->backfill) {
+          skipped.insert(ci);
+          continue;
+        }
+        break;
+      }
+      pop_head(ci);
+      batch.members.push_back({head.req.id, tin, 0, predicted});
+      ++running[ci];
+      new_prefill += tin;
+      ScheduleContext ctx;
+      ctx.now_s = in->now;
+      ctx.wait_s = in->now - head.req.arrival_time_s;
+      ctx.prediction = head.prediction;
+      const ClientState before = policy.clients()[ci];
+      policy.on_admit(ci, head.req, ctx);
+      const ClientState& after = policy.clients()[ci];
+      out->ev_id[n_ev] = head.req.id;
+      out->ev_kind[n_ev] = EQXO_EV_ADMIT;
+      out->ev_client[n_ev] = static_cast<int32_t>(ci);
+      // PendingContribution values, recomputed by the same reference functions on_admit uses.
+      out->ev_ufc_inc[n_ev] = ufc_increment(head.req, ctx, before.weight, spec.equinox);
+      out->ev_rfc_inc[n_ev] = rfc_increment(ctx.prediction, before.weight);
+      // vtc_inc as on_admit forms it (scheduler.cpp:169-181); the ledger itself is reported
+      // from the reference object below.
+      double vtc = 0.0;
+      if (spec.kind == PolicyKind::Vtc) {
+        vtc = spec.vtc_use_prediction
+                  ? before.weight * (static_cast<double>(tin) +
+                                     spec.equinox.output_weight * static_cast<double>(predicted))
+                  : before.weight * static_cast<double>(tin);
+      }
+      (void)after;
+      out->ev_vtc_inc[n_ev] = vtc;
+      out->ev_wait[n_ev] = ctx.wait_s;
+      ++n_ev;
+      ++n_adm;
+    }
+    const auto t2 = std::chrono::steady_clock::now();
+
+    // ---- per-request outputs (prediction record + increments at `now`) ----
+    for (int64_t r = 0; r < in->n_req; ++r) {
+      const PredictionRecord& p = frozen[static_cast<std::size_t>(r)];
+      const Request& req = reqs[static_cast<std::size_t>(r)];
+      out->pred[r] = p.predicted_output_tokens;
+      const ProfileEntry* e = &profile.entry_for(p.predicted_output_tokens);
+      out->bucket[r] = static_cast<int32_t>(e - profile.entries.data());
+      out->lat[r] = p.predicted_latency_ms;
+      out->util[r] = p.predicted_gpu_util;
+      out->tps[r] = p.predicted_tps;
+      ScheduleContext ctx;
+      ctx.now_s = in->now;
+      ctx.wait_s = in->now - req.arrival_time_s;
+      ctx.prediction = p;
+      const double w = in->weight[in->client[r]];
+      out->ufc_inc[r] = ufc_increment(req, ctx, w, spec.equinox);
+      out->rfc_inc[r] = rfc_increment(p, w);
+    }
+    for (int c = 0; c < in->n_clients; ++c) {
+      const ClientState& s = policy.clients()[static_cast<std::size_t>(c)];
+      out->ufc[c] = s.ufc;
+      out->rfc[c] = s.rfc;
+      out->counter[c] = s.counter;
+      out->backlogged[c] = s.backlogged ? 1 : 0;
+    }
+    out->n_events = n_ev;
+    out->n_admitted = n_adm;
+    out->n_rejected = n_rej;
+    out->new_prefill = new_prefill;
+    out->length_fallbacks = mope_ptr ? mope_ptr->length_fallbacks() : 0;
+    out->ns_drain = std::chrono::duration<double, std::nano>(t1 - t0).count();
+    out->ns_admit = std::chrono::duration<double, std::nano>(t2 - t1).count();
+    return 0;
+  } catch (const std::exception& e) {
+    set_err(err, err_len, e.what());
+    return 1;
+  }
+}
+
+// Trains the reference MoPE on the builtin corpus (experiments.cpp:58-73) and returns its
+// JSON (predictor.cpp:408-430).  Returns the needed length; writes when buf is big enough.
+int64_t ref_train_mope_json(int corpus_size, uint64_t seed, int experts, char* buf,
+                            int64_t buf_len) {
+  const Trace corpus = make_prediction_corpus(corpus_size, seed);
+  std::vector<double> pct;
+  for (int i = 1; i < experts; ++i) pct.push_back(100.0 * i / static_cast<double>(experts));
+  const std::string s = train_mope(corpus, pct).to_json().dump();
+  if (buf && buf_len > static_cast<int64_t>(s.size())) std::memcpy(buf, s.c_str(), s.size() + 1);
+  return static_cast<int64_t>(s.size()) + 1;
+}
+
+// build_profile (gpu_model.cpp:87-126) with default PerfParams except the given fields.
+int ref_build_profile(const int32_t* bounds, int n, int ref_input, int32_t* upper,
+                      double* lat, double* util, double* tps) {
+  try {
+    const GpuProfile p = build_profile(PerfParams{}, std::vector<int>(bounds, bounds + n), ref_input);
+    for (int i = 0; i < n; ++i) {
+      upper[i] = p.entries[i].bucket_upper;
+      lat[i] = p.entries[i].latency_ms;
+      util[i] = p.entries[i].gpu_util;
+      tps[i] = p.entries[i].tps;
+    }
+    return 0;
+  } catch (...) {
+    return 1;
+  }
+}
+
+// make_prediction_corpus (workload.cpp:430-476): in/out/tag(0 short,1 medium,2 long).
+int ref_corpus(int n, uint64_t seed, int32_t* in_tok, int32_t* out_tok, int32_t* tag) {
+  const Trace t = make_prediction_corpus(n, seed);
+  for (int i = 0; i < n; ++i) {
+    in_tok[i] = t.requests[i].input_tokens;
+    out_tok[i] = t.requests[i].true_output_tokens;
+    const std::string& g = t.requests[i].category_tag;
+    tag[i] = g == "short" ? 0 : g == "medium" ? 1 : 2;
+  }
+  return 0;
+}
+
+// NoisyOraclePredictor::predict (predictor.cpp:17-23) for a vector of (id, true_out).
+void ref_noisy_predict(double l1, uint64_t seed, int64_t n, const int64_t* id,
+                       const int32_t* true_out, int32_t* pred) {
+  NoisyOraclePredictor p(l1, seed);
+  Request r;
+  for (int64_t i = 0; i < n; ++i) {
+    r.id = id[i];
+    r.true_output_tokens = true_out[i];
+    pred[i] = std::max(1, p.predict(r));
+  }
+}
+
+// glibc log1p as the reference links it (rng.hpp:46), for device-libm pinning.
+void ref_log1p(int64_t n, const double* x, double* y) {
+  for (int64_t i = 0; i < n; ++i) y[i] = std::log1p(x[i]);
+}
+
+// Reference unit-test formulas (test_scheduler.cpp:50-110; test_gpu_model.cpp:28-44).
+double ref_ufc_increment(double w, int in, int pred, double wait_s, double lat_ms,
+                         double delta, double ow) {
+  Request req;
+  req.input_tokens = in;
+  ScheduleContext ctx;
+  ctx.wait_s = wait_s;
+  ctx.prediction.predicted_output_tokens = pred;
+  ctx.prediction.predicted_latency_ms = lat_ms;
+  EquinoxParams p;
+  p.delta = delta;
+  p.output_weight = ow;
+  return ufc_increment(req, ctx, w, p);
+}
+
+double ref_rfc_increment(double w, double tps, double util) {
+  PredictionRecord r;
+  r.predicted_tps = tps;
+  r.predicted_gpu_util = util;
+  return rfc_increment(r, w);
+}
+
+// Full engine replay (run_simulation) of an array trace with default PerfParams/profile
+// overrides; writes the admission/rejection event sequence.  Returns #events or -1.
+int64_t ref_replay(const eqxo_step_in* in, double max_sim_time_s, double ema_alpha,
+                   int64_t* ev_id, int32_t* ev_kind, double* ev_time, int64_t ev_cap,
+                   double* final_ufc, double* final_rfc, double* final_counter, char* err,
+                   int err_len) {
+  try {
+    const auto names = split_names(in->client_names, in->n_clients);
+    const auto tags = split_names(in->tag_names, in->n_tags);
+    Trace trace;
+    for (int c = 0; c < in->n_clients; ++c) {
+      ClientSpec s;
+      s.client_id = names[c];
+      s.weight = in->weight[c];
+      s.arrivals.kind = ArrivalKind::Replay;
+      trace.clients.push_back(s);
+    }
+    double last = 0.0;
+    for (int64_t r = 0; r < in->n_req; ++r) {
+      Request q;
+      q.id = in->id[r];
+      q.client_id = names[static_cast<std::size_t>(in->client[r])];
+      q.arrival_time_s = in->arrival[r];
+      q.input_tokens = in->in_tokens[r];
+      q.true_output_tokens = in->true_out[r];
+      if (in->tag[r] >= 0) q.category_tag = tags[static_cast<std::size_t>(in->tag[r])];
+      last = q.arrival_time_s;
+      trace.requests.push_back(q);
+    }
+    trace.duration_s = last;
+    EngineConfig cfg;
+    cfg.policy.kind = static_cast<PolicyKind>(in->kind);
+    cfg.policy.equinox.alpha = in->alpha;
+    cfg.policy.equinox.delta = in->delta;
+    cfg.policy.equinox.output_weight = in->output_weight;
+    cfg.policy.equinox.norm_mode =
+        in->norm_mode == EQXO_NORM_NONE ? NormMode::None : NormMode::MaxOverClients;
+    cfg.policy.vtc_use_prediction = in->vtc_use_prediction != 0;
+    cfg.policy.counter_lift = in->counter_lift != 0;
+    cfg.perf.max_batch = in->max_batch;
+    cfg.perf.mem_per_token_bytes = in->mem_per_token_bytes;
+    cfg.perf.mem_capacity_bytes = in->mem_capacity_bytes;
+    cfg.backfill = in->backfill != 0;
+    cfg.max_sim_time_s = max_sim_time_s;
+    cfg.ema_alpha = ema_alpha;
+    GpuProfile profile;
+    for (int e = 0; e < in->n_profile; ++e) {
+      profile.entries.push_back(
+          {in->prof_upper[e], in->prof_lat[e], in->prof_util[e], in->prof_tps[e]});
+    }
+    std::unique_ptr<Predictor> predictor;
+    if (in->pred_kind == EQXO_PRED_MOPE) {
+      predictor = std::make_unique<MopePredictor>(model_from(in->mope, tags, in->tag_row, in->n_tags));
+    } else if (in->pred_kind == EQXO_PRED_NOISY) {
+      predictor = std::make_unique<NoisyOraclePredictor>(in->noisy_l1, in->noisy_seed);
+    } else {
+      predictor = std::make_unique<OraclePredictor>();
+    }
+    const SimResult res = run_simulation(trace, cfg, *predictor, profile);
+    int64_t n = 0;
+    for (const auto& e : res.log.entries) {
+      if (e.event != LogEvent::Admitted && e.event != LogEvent::Rejected) continue;
+      if (n < ev_cap) {
+        ev_id[n] = e.request_id;
+        ev_kind[n] = e.event == LogEvent::Admitted ? EQXO_EV_ADMIT : EQXO_EV_REJECT;
+        ev_time[n] = e.time_s;
+      }
+      ++n;
+    }
+    for (std::size_t c = 0; c < res.final_clients.size(); ++c) {
+      final_ufc[c] = res.final_clients[c].ufc;
+      final_rfc[c] = res.final_clients[c].rfc;
+      final_counter[c] = res.final_clients[c].counter;
+    }
+    return n;
+  } catch (const std::exception& e) {
+    set_err(err, err_len, e.what());
+    return -1;
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,105 @@
+"""ctypes binding of libeqx_b200.so (include/eqx.h).  No fallback: importing the scheduler
+without the built CUDA library, or creating a context without a B200, raises."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libeqx_b200.so")
+
+EQX_OK, EQX_ERR_CONFIG, EQX_ERR_PARSE, EQX_ERR_ENGINE, EQX_ERR_CUDA, EQX_ERR_ARG = range(6)
+EQX_HOST, EQX_DEVICE = 0, 1
+
+_dp = C.POINTER(C.c_double)
+_i32p = C.POINTER(C.c_int32)
+_i64p = C.POINTER(C.c_int64)
+_u8p = C.POINTER(C.c_uint8)
+
+
+class Policy(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("alpha", C.c_double), ("delta", C.c_double),
+                ("output_weight", C.c_double), ("norm_mode", C.c_int32),
+                ("vtc_use_prediction", C.c_int32), ("counter_lift", C.c_int32),
+                ("backfill", C.c_int32)]
+
+
+class Perf(C.Structure):
+    _fields_ = [("max_batch", C.c_int32), ("mem_per_token_bytes", C.c_double),
+                ("mem_capacity_bytes", C.c_double)]
+
+
+class Profile(C.Structure):
+    _fields_ = [("n", C.c_int32), ("bucket_upper", _i32p), ("latency_ms", _dp),
+                ("gpu_util", _dp), ("tps", _dp)]
+
+
+class Mope(C.Structure):
+    _fields_ = [("n_thresholds", C.c_int32), ("thresholds", _i32p), ("mix_weight", C.c_double),
+                ("num_buckets", C.c_int32), ("n_rows", C.c_int32), ("rows", _dp),
+                ("n_experts", C.c_int32), ("n_bins", C.c_int32), ("bin_upper", _i32p),
+                ("bin_value", _i32p), ("out_min", _i32p), ("out_max", _i32p),
+                ("n_tags", C.c_int32), ("tag_row", _i32p)]
+
+
+class Predictor(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("mope", Mope), ("noisy_l1", C.c_double),
+                ("noisy_seed", C.c_uint64)]
+
+
+class Requests(C.Structure):
+    _fields_ = [("n", C.c_int64), ("id", C.c_void_p), ("id_base", C.c_int64),
+                ("client", C.c_void_p), ("arrival_s", C.c_void_p), ("input_tokens", C.c_void_p),
+                ("true_output_tokens", C.c_void_p), ("tag", C.c_void_p), ("location", C.c_int32)]
+
+
+class StepSummary(C.Structure):
+    _fields_ = [("n_events", C.c_int64), ("n_admitted", C.c_int64), ("n_rejected", C.c_int64),
+                ("new_prefill_tokens", C.c_int64), ("length_fallbacks", C.c_int64),
+                ("noisy_near_ties", C.c_int64), ("batch_members", C.c_int32),
+                ("batch_reserved_kv_tokens", C.c_int64), ("queued", C.c_int64)]
+
+
+_SIGS = {
+    "eqx_abi_version": ([], C.c_int32),
+    "eqx_ctx_create": ([C.c_int32, C.POINTER(C.c_void_p)], C.c_int),
+    "eqx_ctx_destroy": ([C.c_void_p], None),
+    "eqx_last_error": ([C.c_void_p], C.c_char_p),
+    "eqx_ctx_stream": ([C.c_void_p], C.c_void_p),
+    "eqx_set_policy": ([C.c_void_p, C.POINTER(Policy)], C.c_int),
+    "eqx_set_perf": ([C.c_void_p, C.POINTER(Perf)], C.c_int),
+    "eqx_set_profile": ([C.c_void_p, C.POINTER(Profile)], C.c_int),
+    "eqx_set_predictor": ([C.c_void_p, C.POINTER(Predictor)], C.c_int),
+    "eqx_set_clients": ([C.c_void_p, C.c_int32, C.c_char_p, _dp, _dp, _dp, _dp, _i32p], C.c_int),
+    "eqx_get_clients": ([C.c_void_p, C.c_int32, _dp, _dp, _dp, _i32p, _i32p], C.c_int),
+    "eqx_set_batch": ([C.c_void_p, C.c_int32, C.c_int64], C.c_int),
+    "eqx_drain": ([C.c_void_p, C.POINTER(Requests)], C.c_int),
+    "eqx_step_async": ([C.c_void_p, C.c_double], C.c_int),
+    "eqx_step_collect": ([C.c_void_p, C.POINTER(StepSummary)], C.c_int),
+    "eqx_step": ([C.c_void_p, C.c_double, C.POINTER(StepSummary)], C.c_int),
+    "eqx_copy_events": ([C.c_void_p, C.c_int64, _i64p, _i32p, _i32p, _i32p, _dp, _dp, _dp, _dp], C.c_int),
+    "eqx_copy_scores": ([C.c_void_p, C.c_int64, _i32p, _u8p, _dp, _dp], C.c_int),
+    "eqx_ufc_increment": ([C.c_double, C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_double, C.c_double], C.c_double),
+    "eqx_rfc_increment": ([C.c_double, C.c_double, C.c_double], C.c_double),
+}
+
+EXPORTED = sorted(_SIGS)
+
+_lib = None
+
+
+def load() -> C.CDLL:
+    """Load libeqx_b200.so (built by __graft_entry__.build()); raises if it is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`. "
+                "There is no CPU fallback for the scheduling step.")
+        lib = C.CDLL(LIB_PATH)
+        for name, (args, res) in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = lib
+    return _lib

@@ -1,0 +1,741 @@
+// eqx_capi.cu -- the C ABI (include/eqx.h): context, model compiler, drain/step orchestration.
+//
+// Host code here only validates parameters (with the reference's messages), compiles the
+// MoPE model + GPU profile into device tables, owns device buffers and launches kernels on
+// the context stream.  There is no CPU execution path for the step: every per-request and
+// per-pick decision is made by the kernels in eqx_kernels.cu.
+#include <algorithm>
+#include <climits>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/eqx.h"
+#include "eqx_device.cuh"
+#include "eqx_kernels.h"
+
+using namespace eqx;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t need) {
+    if (need <= bytes && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    const size_t alloc = std::max<size_t>(need, 256);
+    cudaError_t e = cudaMalloc(&p, alloc);
+    if (e == cudaSuccess) bytes = alloc;
+    return e;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+};
+
+}  // namespace
+
+struct eqx_ctx {
+  int device = 0;
+  int sm_count = 148;
+  size_t smem_optin = 227 * 1024;
+  cudaStream_t stream = nullptr;
+  std::string err;
+
+  Policy pol{};
+  int32_t counter_lift = 1;
+  bool policy_set = false;
+  eqx_perf perf{64, 0.5 * 1024.0 * 1024.0, 60.0 * 1024.0 * 1024.0 * 1024.0};
+  ModelTables model{};
+  bool model_set = false, profile_set = false, model_dirty = true;
+  int32_t lut_entries = 0;
+  DevBuf d_model;
+
+  int32_t C = 0;
+  DevBuf d_ufc, d_rfc, d_counter, d_weight, d_order, d_running, d_backlogged;
+  DevBuf d_head, d_count, d_first, d_qlen_before, d_seg_off;
+
+  int64_t n = 0;
+  const int32_t* q_client = nullptr;
+  const double* q_arrival = nullptr;
+  const int32_t* q_in = nullptr;
+  const int32_t* q_true = nullptr;
+  const uint8_t* q_tag = nullptr;
+  const int64_t* q_id = nullptr;
+  int64_t id_base = 0;
+  DevBuf own_client, own_arrival, own_in, own_true, own_tag, own_id;
+  DevBuf d_perm, d_hist;
+  bool queue_ready = false;
+
+  DevBuf d_pred, d_bucket, d_ufc_out, d_rfc_out;
+  DevBuf d_ev_row, d_ev_kind, d_ev_client, d_ev_pred, d_ev_ufc, d_ev_rfc, d_ev_vtc, d_ev_wait, d_ev_id;
+  int64_t ev_cap = 0;
+  DevBuf d_state, d_cw;
+  DevState* h_state = nullptr;  // pinned
+  unsigned long long last_fallbacks = 0, last_near_ties = 0;
+  bool step_pending = false;
+  bool stepped = false;
+};
+
+namespace {
+
+eqx_status fail(eqx_ctx* ctx, eqx_status st, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  return st;
+}
+
+#define CUDA_TRY(ctx, expr)                                                            \
+  do {                                                                                 \
+    cudaError_t _e = (expr);                                                           \
+    if (_e != cudaSuccess)                                                             \
+      return fail((ctx), EQX_ERR_CUDA, std::string("CUDA error: ") + cudaGetErrorString(_e) + \
+                                           " at " #expr);                              \
+  } while (0)
+
+// ---- reference predictor semantics, evaluated once per LUT cell (host "model compiler") ----
+// RouterModel::length_bucket (predictor.cpp:29-34)
+int length_bucket(const eqx_mope& m, int in) {
+  for (int i = 0; i < m.n_thresholds; ++i)
+    if (in <= m.thresholds[i]) return i;
+  return m.num_buckets - 1;
+}
+// route (predictor.cpp:36-60); row < 0 => tag empty/unseen => length fallback
+int route(const eqx_mope& m, int in, int row, bool* fallback) {
+  const int len_bucket = length_bucket(m, in);
+  if (row < 0) {
+    *fallback = true;
+    return len_bucket;
+  }
+  *fallback = false;
+  const double* aff = m.rows + static_cast<size_t>(row) * m.num_buckets;
+  int bucket = 0;
+  double best = -1.0;
+  for (int b = 0; b < m.num_buckets; ++b) {
+    const double length_score = b == len_bucket ? 1.0 : 0.0;
+    const double score = m.mix_weight * length_score + (1.0 - m.mix_weight) * aff[b];
+    if (score > best) {
+      best = score;
+      bucket = b;
+    }
+  }
+  return bucket;
+}
+// ExpertModel::predict (predictor.cpp:62-71)
+int expert_predict(const eqx_mope& m, int e, int in) {
+  const int32_t* up = m.bin_upper + static_cast<size_t>(e) * m.n_bins;
+  const int32_t* val = m.bin_value + static_cast<size_t>(e) * m.n_bins;
+  int idx = m.n_bins - 1;
+  for (int i = 0; i < m.n_bins; ++i) {
+    if (in <= up[i]) {
+      idx = i;
+      break;
+    }
+  }
+  return std::clamp(val[idx], m.out_min[e], m.out_max[e]);
+}
+
+uint64_t fnv1a(const char* s) {
+  uint64_t h = 0xcbf29ce484222325ULL;
+  for (; *s; ++s) {
+    h ^= static_cast<unsigned char>(*s);
+    h *= 0x100000001b3ULL;
+  }
+  return h;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+}  // namespace
+
+extern "C" {
+
+int32_t eqx_abi_version(void) { return EQX_ABI_VERSION; }
+
+const char* eqx_last_error(const eqx_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_create_error.c_str();
+}
+
+eqx_status eqx_ctx_create(int32_t device, eqx_ctx** out) {
+  if (!out) {
+    g_create_error = "eqx_ctx_create: out is NULL";
+    return EQX_ERR_ARG;
+  }
+  *out = nullptr;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) {
+    g_create_error = std::string("no CUDA device available: ") + cudaGetErrorString(e);
+    return EQX_ERR_CUDA;
+  }
+  if (device < 0 || device >= ndev) {
+    g_create_error = "device index out of range";
+    return EQX_ERR_ARG;
+  }
+  cudaDeviceProp prop{};
+  cudaSetDevice(device);
+  e = cudaGetDeviceProperties(&prop, device);
+  if (e != cudaSuccess) {
+    g_create_error = cudaGetErrorString(e);
+    return EQX_ERR_CUDA;
+  }
+  if (prop.major != 10) {
+    g_create_error = "libeqx_b200 is built for sm_100a (B200); device " + std::string(prop.name) +
+                     " is sm_" + std::to_string(prop.major) + std::to_string(prop.minor);
+    return EQX_ERR_CUDA;
+  }
+  eqx_ctx* ctx = new eqx_ctx();
+  ctx->device = device;
+  ctx->sm_count = prop.multiProcessorCount;
+  ctx->smem_optin = prop.sharedMemPerBlockOptin;
+  e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = ctx->d_state.ensure(sizeof(DevState));
+  if (e == cudaSuccess) e = cudaMemset(ctx->d_state.p, 0, sizeof(DevState));
+  if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_state, sizeof(DevState));
+  if (e == cudaSuccess) e = ctx->d_model.ensure(sizeof(ModelTables));
+  if (e != cudaSuccess) {
+    g_create_error = cudaGetErrorString(e);
+    eqx_ctx_destroy(ctx);
+    return EQX_ERR_CUDA;
+  }
+  ctx->pol.kind = kEquinox;
+  ctx->pol.alpha = 0.7;
+  ctx->pol.beta = 1.0 - 0.7;
+  ctx->pol.delta = 0.1;
+  ctx->pol.ow = 4.0;
+  ctx->pol.max_batch = ctx->perf.max_batch;
+  ctx->pol.m = ctx->perf.mem_per_token_bytes;
+  ctx->pol.M = ctx->perf.mem_capacity_bytes;
+  *out = ctx;
+  return EQX_OK;
+}
+
+void eqx_ctx_destroy(eqx_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  DevBuf* bufs[] = {&ctx->d_model, &ctx->d_ufc, &ctx->d_rfc, &ctx->d_counter, &ctx->d_weight,
+                    &ctx->d_order, &ctx->d_running, &ctx->d_backlogged, &ctx->d_head,
+                    &ctx->d_count, &ctx->d_first, &ctx->d_qlen_before, &ctx->d_seg_off,
+                    &ctx->own_client, &ctx->own_arrival, &ctx->own_in, &ctx->own_true,
+                    &ctx->own_tag, &ctx->own_id, &ctx->d_perm, &ctx->d_hist, &ctx->d_pred,
+                    &ctx->d_bucket, &ctx->d_ufc_out, &ctx->d_rfc_out, &ctx->d_ev_row,
+                    &ctx->d_ev_kind, &ctx->d_ev_client, &ctx->d_ev_pred, &ctx->d_ev_ufc,
+                    &ctx->d_ev_rfc, &ctx->d_ev_vtc, &ctx->d_ev_wait, &ctx->d_ev_id,
+                    &ctx->d_state, &ctx->d_cw};
+  for (DevBuf* b : bufs) b->release();
+  if (ctx->h_state) cudaFreeHost(ctx->h_state);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+void* eqx_ctx_stream(eqx_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+// EquinoxParams::validate (scheduler.cpp:11-17)
+eqx_status eqx_set_policy(eqx_ctx* ctx, const eqx_policy* p) {
+  if (!ctx || !p) return fail(ctx, EQX_ERR_ARG, "eqx_set_policy: NULL argument");
+  if (p->kind < EQX_FCFS || p->kind > EQX_EQUINOX) return fail(ctx, EQX_ERR_CONFIG, "unknown policy kind");
+  if (p->alpha < 0.0 || p->alpha > 1.0) return fail(ctx, EQX_ERR_CONFIG, "alpha must lie in [0, 1]");
+  if (p->delta < 0.0) return fail(ctx, EQX_ERR_CONFIG, "delta must be >= 0");
+  if (p->output_weight <= 0.0) return fail(ctx, EQX_ERR_CONFIG, "output_weight must be > 0");
+  if (p->norm_mode != EQX_NORM_MAX_OVER_CLIENTS && p->norm_mode != EQX_NORM_NONE)
+    return fail(ctx, EQX_ERR_CONFIG, "unknown norm_mode");
+  ctx->pol.kind = p->kind;
+  ctx->pol.alpha = p->alpha;
+  ctx->pol.beta = 1.0 - p->alpha;  // EquinoxParams::beta() (scheduler.hpp:24)
+  ctx->pol.delta = p->delta;
+  ctx->pol.ow = p->output_weight;
+  ctx->pol.norm_mode = p->norm_mode;
+  ctx->pol.vtc_use_prediction = p->vtc_use_prediction ? 1 : 0;
+  ctx->pol.backfill = p->backfill ? 1 : 0;
+  ctx->counter_lift = p->counter_lift ? 1 : 0;
+  ctx->policy_set = true;
+  return EQX_OK;
+}
+
+// PerfParams::validate (gpu_model.cpp:9-24) for the admission fields
+eqx_status eqx_set_perf(eqx_ctx* ctx, const eqx_perf* p) {
+  if (!ctx || !p) return fail(ctx, EQX_ERR_ARG, "eqx_set_perf: NULL argument");
+  if (p->mem_per_token_bytes <= 0.0)
+    return fail(ctx, EQX_ERR_CONFIG, "perf parameter 'mem_per_token_bytes' must be > 0");
+  if (p->mem_capacity_bytes <= 0.0)
+    return fail(ctx, EQX_ERR_CONFIG, "perf parameter 'mem_capacity_bytes' must be > 0");
+  if (p->max_batch <= 0) return fail(ctx, EQX_ERR_CONFIG, "perf parameter 'max_batch' must be > 0");
+  ctx->perf = *p;
+  ctx->pol.max_batch = p->max_batch;
+  ctx->pol.m = p->mem_per_token_bytes;
+  ctx->pol.M = p->mem_capacity_bytes;
+  return EQX_OK;
+}
+
+eqx_status eqx_set_profile(eqx_ctx* ctx, const eqx_profile* p) {
+  if (!ctx || !p) return fail(ctx, EQX_ERR_ARG, "eqx_set_profile: NULL argument");
+  if (p->n <= 0) return fail(ctx, EQX_ERR_CONFIG, "engine needs a non-empty GPU profile");
+  if (p->n > kMaxProfile)
+    return fail(ctx, EQX_ERR_CONFIG, "GPU profile has more than " + std::to_string(kMaxProfile) + " buckets");
+  ModelTables& M = ctx->model;
+  M.n_prof = p->n;
+  for (int i = 0; i < p->n; ++i) {
+    M.prof_upper[i] = p->bucket_upper[i];
+    M.prof_lat[i] = p->latency_ms[i];
+    M.prof_util[i] = p->gpu_util[i];
+    M.prof_tps[i] = p->tps[i];
+    M.prof_pred_s[i] = p->latency_ms[i] / 1000.0;  // scheduler.cpp:23
+  }
+  ctx->profile_set = true;
+  ctx->model_dirty = true;
+  return EQX_OK;
+}
+
+eqx_status eqx_set_predictor(eqx_ctx* ctx, const eqx_predictor* p) {
+  if (!ctx || !p) return fail(ctx, EQX_ERR_ARG, "eqx_set_predictor: NULL argument");
+  ModelTables& M = ctx->model;
+  M.pred_kind = p->kind;
+  if (p->kind == EQX_PRED_ORACLE) {
+    M.n_cuts = 0;
+    M.n_tag_states = 1;
+    ctx->lut_entries = 1;
+    M.lut[0] = 1;
+  } else if (p->kind == EQX_PRED_NOISY_ORACLE) {
+    if (p->noisy_l1 < 0.0) return fail(ctx, EQX_ERR_CONFIG, "noisy oracle target_l1 must be >= 0");
+    M.noisy_l1 = p->noisy_l1;
+    M.noisy_key = mix_keys(p->noisy_seed, fnv1a("noisy_oracle"));
+    M.n_cuts = 0;
+    M.n_tag_states = 1;
+    ctx->lut_entries = 1;
+    M.lut[0] = 1;
+  } else if (p->kind == EQX_PRED_MOPE || p->kind == EQX_PRED_SINGLE_PROXY) {
+    const eqx_mope& m = p->mope;
+    if (m.n_experts <= 0) return fail(ctx, EQX_ERR_CONFIG, "MoPE predictor constructed without trained experts");
+    if (m.n_bins <= 0) return fail(ctx, EQX_ERR_PARSE, "malformed MoPE model: expert without bins");
+    if (p->kind == EQX_PRED_MOPE) {
+      if (m.num_buckets <= 0 || m.num_buckets > m.n_experts)
+        return fail(ctx, EQX_ERR_PARSE, "malformed MoPE model: num_buckets does not match the experts");
+      if (m.n_thresholds < 0 || m.n_thresholds > 64) return fail(ctx, EQX_ERR_PARSE, "malformed MoPE model: thresholds");
+      for (int t = 0; t < m.n_tags; ++t)
+        if (m.tag_row[t] >= m.n_rows) return fail(ctx, EQX_ERR_PARSE, "malformed MoPE model: tag row out of range");
+      if (m.n_tags + 1 > kMaxTagStates) return fail(ctx, EQX_ERR_CONFIG, "more than 255 distinct category tags");
+    }
+    // Merged cut points: every threshold / bin bound any comparison `in <= x` can test.
+    std::vector<int> cuts;
+    if (p->kind == EQX_PRED_MOPE) cuts.assign(m.thresholds, m.thresholds + m.n_thresholds);
+    const int ne = p->kind == EQX_PRED_MOPE ? m.n_experts : 1;
+    for (int e = 0; e < ne; ++e)
+      for (int i = 0; i < m.n_bins; ++i) cuts.push_back(m.bin_upper[e * m.n_bins + i]);
+    std::sort(cuts.begin(), cuts.end());
+    cuts.erase(std::unique(cuts.begin(), cuts.end()), cuts.end());
+    if (static_cast<int>(cuts.size()) > kMaxCuts) return fail(ctx, EQX_ERR_CONFIG, "MoPE model has too many distinct cut points");
+    const int nt = p->kind == EQX_PRED_MOPE ? m.n_tags + 1 : 1;
+    const int ni = static_cast<int>(cuts.size()) + 1;
+    if (ni * nt > kMaxLut) return fail(ctx, EQX_ERR_CONFIG, "MoPE lookup table too large");
+    M.n_cuts = static_cast<int>(cuts.size());
+    M.n_tag_states = nt;
+    for (int i = 0; i < M.n_cuts; ++i) M.cuts[i] = cuts[i];
+    // Interval k = {in : cuts[k-1] < in <= cuts[k]}: every `in <= x` test is constant on it,
+    // so evaluating the reference functions at one representative is exact for all members.
+    for (int k = 0; k < ni; ++k) {
+      int rep;
+      if (k < M.n_cuts) rep = cuts[k];
+      else rep = (M.n_cuts == 0) ? 1 : (cuts.back() == INT_MAX ? INT_MAX : cuts.back() + 1);
+      for (int t = 0; t < nt; ++t) {
+        int pred;
+        bool fb = false;
+        if (p->kind == EQX_PRED_MOPE) {
+          const int row = t == 0 ? -1 : m.tag_row[t - 1];
+          const int b = route(m, rep, row, &fb);
+          pred = expert_predict(m, b, rep);
+        } else {
+          pred = expert_predict(m, 0, rep);
+        }
+        pred = std::max(1, pred);  // engine.cpp:179
+        M.lut[k * nt + t] = fb ? -pred : pred;
+      }
+    }
+    ctx->lut_entries = ni * nt;
+  } else {
+    return fail(ctx, EQX_ERR_CONFIG, "unknown predictor kind");
+  }
+  ctx->model_set = true;
+  ctx->model_dirty = true;
+  return EQX_OK;
+}
+
+eqx_status eqx_set_clients(eqx_ctx* ctx, int32_t n, const char* names, const double* weight,
+                           const double* ufc, const double* rfc, const double* counter,
+                           const int32_t* running) {
+  if (!ctx || n < 0 || (n > 0 && (!names || !weight))) return fail(ctx, EQX_ERR_ARG, "eqx_set_clients: bad arguments");
+  cudaSetDevice(ctx->device);
+  std::vector<std::string> ids;
+  const char* q = names;
+  for (int i = 0; i < n; ++i) {
+    ids.emplace_back(q);
+    q += ids.back().size() + 1;
+    if (!(weight[i] > 0.0)) return fail(ctx, EQX_ERR_CONFIG, "client '" + ids.back() + "' has non-positive weight");
+  }
+  // lexicographic rank by std::string operator< (bytewise), index breaks exact duplicates the
+  // way select_next keeps the earlier candidate (scheduler.cpp:139-153)
+  std::vector<int> idx(n);
+  std::iota(idx.begin(), idx.end(), 0);
+  std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return ids[a] < ids[b]; });
+  std::vector<uint32_t> order(n);
+  for (int r = 0; r < n; ++r) order[idx[r]] = static_cast<uint32_t>(r);
+  std::vector<double> zeros(n, 0.0);
+  std::vector<int32_t> izeros(n, 0);
+  const size_t d8 = 8ull * std::max(n, 1), d4 = 4ull * std::max(n, 1);
+  CUDA_TRY(ctx, ctx->d_ufc.ensure(d8));
+  CUDA_TRY(ctx, ctx->d_rfc.ensure(d8));
+  CUDA_TRY(ctx, ctx->d_counter.ensure(d8));
+  CUDA_TRY(ctx, ctx->d_weight.ensure(d8));
+  CUDA_TRY(ctx, ctx->d_order.ensure(d4));
+  CUDA_TRY(ctx, ctx->d_running.ensure(d4));
+  CUDA_TRY(ctx, ctx->d_backlogged.ensure(d4));
+  CUDA_TRY(ctx, ctx->d_head.ensure(d4));
+  CUDA_TRY(ctx, ctx->d_count.ensure(d4));
+  CUDA_TRY(ctx, ctx->d_first.ensure(d4));
+  CUDA_TRY(ctx, ctx->d_qlen_before.ensure(d4));
+  CUDA_TRY(ctx, ctx->d_seg_off.ensure(4ull * (n + 1)));
+  cudaStream_t s = ctx->stream;
+  if (n > 0) {
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_ufc.p, ufc ? ufc : zeros.data(), 8ull * n, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_rfc.p, rfc ? rfc : zeros.data(), 8ull * n, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_counter.p, counter ? counter : zeros.data(), 8ull * n, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_weight.p, weight, 8ull * n, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_order.p, order.data(), 4ull * n, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_running.p, running ? running : izeros.data(), 4ull * n, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_backlogged.p, 0, d4, s));
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_head.p, 0, d4, s));
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_count.p, 0, d4, s));
+  }
+  CUDA_TRY(ctx, cudaStreamSynchronize(s));  // host vectors above are about to go away
+  ctx->C = n;
+  ctx->queue_ready = false;
+  ctx->stepped = false;
+  return EQX_OK;
+}
+
+eqx_status eqx_get_clients(eqx_ctx* ctx, int32_t n, double* ufc, double* rfc, double* counter,
+                           int32_t* backlogged, int32_t* running) {
+  if (!ctx || n != ctx->C) return fail(ctx, EQX_ERR_ARG, "eqx_get_clients: roster size mismatch");
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = ctx->stream;
+  if (n > 0) {
+    if (ufc) CUDA_TRY(ctx, cudaMemcpyAsync(ufc, ctx->d_ufc.p, 8ull * n, cudaMemcpyDeviceToHost, s));
+    if (rfc) CUDA_TRY(ctx, cudaMemcpyAsync(rfc, ctx->d_rfc.p, 8ull * n, cudaMemcpyDeviceToHost, s));
+    if (counter) CUDA_TRY(ctx, cudaMemcpyAsync(counter, ctx->d_counter.p, 8ull * n, cudaMemcpyDeviceToHost, s));
+    if (backlogged) CUDA_TRY(ctx, cudaMemcpyAsync(backlogged, ctx->d_backlogged.p, 4ull * n, cudaMemcpyDeviceToHost, s));
+    if (running) CUDA_TRY(ctx, cudaMemcpyAsync(running, ctx->d_running.p, 4ull * n, cudaMemcpyDeviceToHost, s));
+  }
+  CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  return EQX_OK;
+}
+
+eqx_status eqx_set_batch(eqx_ctx* ctx, int32_t members, int64_t reserved) {
+  if (!ctx || members < 0 || reserved < 0) return fail(ctx, EQX_ERR_ARG, "eqx_set_batch: bad arguments");
+  cudaSetDevice(ctx->device);
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  ctx->h_state->members = members;
+  ctx->h_state->reserved = reserved;
+  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_state.p, ctx->h_state, offsetof(DevState, n_events),
+                                cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return EQX_OK;
+}
+
+eqx_status eqx_drain(eqx_ctx* ctx, const eqx_requests* r) {
+  if (!ctx || !r) return fail(ctx, EQX_ERR_ARG, "eqx_drain: NULL argument");
+  if (!ctx->model_set || !ctx->profile_set)
+    return fail(ctx, EQX_ERR_CONFIG, "eqx_drain: predictor and GPU profile must be set first");
+  if (r->n < 0 || r->n >= (int64_t(1) << 31) - 1) return fail(ctx, EQX_ERR_ARG, "eqx_drain: n out of range");
+  const int64_t n = r->n;
+  const int32_t C = ctx->C;
+  if (n > 0 && C == 0) return fail(ctx, EQX_ERR_CONFIG, "eqx_drain: requests but no clients");
+  const bool needs_true = ctx->model.pred_kind == kPredOracle || ctx->model.pred_kind == kPredNoisy;
+  if (n > 0 && (!r->client || !r->arrival_s || !r->input_tokens || (needs_true && !r->true_output_tokens)))
+    return fail(ctx, EQX_ERR_ARG, "eqx_drain: missing request column");
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = ctx->stream;
+  const size_t nn = static_cast<size_t>(std::max<int64_t>(n, 1));
+  // bind (device) or copy (host) the columns
+  if (r->location == EQX_DEVICE) {
+    ctx->q_client = r->client;
+    ctx->q_arrival = r->arrival_s;
+    ctx->q_in = r->input_tokens;
+    ctx->q_true = r->true_output_tokens;
+    ctx->q_id = r->id;
+    if (r->tag) {
+      ctx->q_tag = r->tag;
+    } else {
+      CUDA_TRY(ctx, ctx->own_tag.ensure(nn + 16));
+      CUDA_TRY(ctx, cudaMemsetAsync(ctx->own_tag.p, 0, nn, s));
+      ctx->q_tag = ctx->own_tag.as<uint8_t>();
+    }
+  } else {
+    CUDA_TRY(ctx, ctx->own_client.ensure(4 * nn));
+    CUDA_TRY(ctx, ctx->own_arrival.ensure(8 * nn));
+    CUDA_TRY(ctx, ctx->own_in.ensure(4 * nn));
+    CUDA_TRY(ctx, ctx->own_tag.ensure(nn + 16));
+    if (n > 0) {
+      CUDA_TRY(ctx, cudaMemcpyAsync(ctx->own_client.p, r->client, 4 * n, cudaMemcpyHostToDevice, s));
+      CUDA_TRY(ctx, cudaMemcpyAsync(ctx->own_arrival.p, r->arrival_s, 8 * n, cudaMemcpyHostToDevice, s));
+      CUDA_TRY(ctx, cudaMemcpyAsync(ctx->own_in.p, r->input_tokens, 4 * n, cudaMemcpyHostToDevice, s));
+      if (r->tag) CUDA_TRY(ctx, cudaMemcpyAsync(ctx->own_tag.p, r->tag, n, cudaMemcpyHostToDevice, s));
+      else CUDA_TRY(ctx, cudaMemsetAsync(ctx->own_tag.p, 0, n, s));
+    }
+    ctx->q_client = ctx->own_client.as<int32_t>();
+    ctx->q_arrival = ctx->own_arrival.as<double>();
+    ctx->q_in = ctx->own_in.as<int32_t>();
+    ctx->q_tag = ctx->own_tag.as<uint8_t>();
+    ctx->q_true = nullptr;
+    if (r->true_output_tokens) {
+      CUDA_TRY(ctx, ctx->own_true.ensure(4 * nn));
+      if (n > 0) CUDA_TRY(ctx, cudaMemcpyAsync(ctx->own_true.p, r->true_output_tokens, 4 * n, cudaMemcpyHostToDevice, s));
+      ctx->q_true = ctx->own_true.as<int32_t>();
+    }
+    ctx->q_id = nullptr;
+    if (r->id) {
+      CUDA_TRY(ctx, ctx->own_id.ensure(8 * nn));
+      if (n > 0) CUDA_TRY(ctx, cudaMemcpyAsync(ctx->own_id.p, r->id, 8 * n, cudaMemcpyHostToDevice, s));
+      ctx->q_id = ctx->own_id.as<int64_t>();
+    }
+  }
+  ctx->id_base = r->id_base;
+  ctx->n = n;
+  // scores + events sized to the queue
+  CUDA_TRY(ctx, ctx->d_pred.ensure(4 * nn + 16));
+  CUDA_TRY(ctx, ctx->d_bucket.ensure(nn + 16));
+  CUDA_TRY(ctx, ctx->d_ufc_out.ensure(8 * nn + 16));
+  CUDA_TRY(ctx, ctx->d_rfc_out.ensure(8 * nn + 16));
+  ctx->ev_cap = static_cast<int64_t>(nn);
+  CUDA_TRY(ctx, ctx->d_ev_row.ensure(4 * nn));
+  CUDA_TRY(ctx, ctx->d_ev_kind.ensure(4 * nn));
+  CUDA_TRY(ctx, ctx->d_ev_client.ensure(4 * nn));
+  CUDA_TRY(ctx, ctx->d_ev_pred.ensure(4 * nn));
+  CUDA_TRY(ctx, ctx->d_ev_ufc.ensure(8 * nn));
+  CUDA_TRY(ctx, ctx->d_ev_rfc.ensure(8 * nn));
+  CUDA_TRY(ctx, ctx->d_ev_vtc.ensure(8 * nn));
+  CUDA_TRY(ctx, ctx->d_ev_wait.ensure(8 * nn));
+  CUDA_TRY(ctx, ctx->d_ev_id.ensure(8 * nn));
+  CUDA_TRY(ctx, ctx->d_perm.ensure(4 * nn));
+  // tiling: 8 warps x (tile_rows/8) rows per tile, histogram kept <= ~1M entries
+  int64_t tile_rows = 2048;
+  while (static_cast<int64_t>(C) * ((n + tile_rows - 1) / tile_rows) > (int64_t(1) << 20)) tile_rows *= 2;
+  if (tile_rows / 8 > 65535) return fail(ctx, EQX_ERR_CONFIG, "too many clients for the drain tiling");
+  const int32_t n_tiles = static_cast<int32_t>(std::max<int64_t>(1, (n + tile_rows - 1) / tile_rows));
+  const int64_t L = static_cast<int64_t>(C) * n_tiles;
+  CUDA_TRY(ctx, ctx->d_hist.ensure(4 * std::max<int64_t>(L, 1)));
+  if (C > 0) {
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_count.p, 0, 4ull * C, s));
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_first.p, 0x7f, 4ull * C, s));
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_head.p, 0, 4ull * C, s));
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_qlen_before.p, 0, 4ull * C, s));
+    const size_t hist_smem = 8ull * C;
+    const size_t rank_smem = 4ull * C + 16ull * C;
+    if (rank_smem > ctx->smem_optin || hist_smem > ctx->smem_optin)
+      return fail(ctx, EQX_ERR_CONFIG, "too many clients per device (" + std::to_string(C) + ")");
+    cudaFuncSetAttribute(drain_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(hist_smem));
+    cudaFuncSetAttribute(drain_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rank_smem));
+    DevState* st = ctx->d_state.as<DevState>();
+    if (n > 0) {
+      drain_hist_kernel<<<n_tiles, 256, hist_smem, s>>>(ctx->q_client, static_cast<int32_t>(n), C,
+                                                        static_cast<int32_t>(tile_rows), n_tiles,
+                                                        ctx->d_hist.as<uint32_t>(), ctx->d_first.as<int32_t>(),
+                                                        ctx->d_count.as<int32_t>(), st);
+      scan_kernel<<<1, 1024, 0, s>>>(ctx->d_hist.as<uint32_t>(), L, C, n_tiles, ctx->d_seg_off.as<int32_t>());
+      drain_rank_kernel<<<n_tiles, 256, rank_smem, s>>>(ctx->q_client, static_cast<int32_t>(n), C,
+                                                        static_cast<int32_t>(tile_rows), n_tiles,
+                                                        ctx->d_hist.as<uint32_t>(), ctx->d_perm.as<uint32_t>());
+    } else {
+      CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_seg_off.p, 0, 4ull * (C + 1), s));
+    }
+    lift_kernel<<<1, 1024, 0, s>>>(C, ctx->d_count.as<int32_t>(), ctx->d_first.as<int32_t>(),
+                                   ctx->d_qlen_before.as<int32_t>(), ctx->d_running.as<int32_t>(),
+                                   ctx->d_ufc.as<double>(), ctx->d_rfc.as<double>(),
+                                   ctx->d_counter.as<double>(), ctx->d_backlogged.as<int32_t>(),
+                                   ctx->counter_lift);
+    CUDA_TRY(ctx, cudaGetLastError());
+  }
+  ctx->queue_ready = true;
+  return EQX_OK;
+}
+
+eqx_status eqx_step_async(eqx_ctx* ctx, double now) {
+  if (!ctx) return fail(ctx, EQX_ERR_ARG, "eqx_step_async: NULL context");
+  if (!ctx->queue_ready) return fail(ctx, EQX_ERR_CONFIG, "eqx_step: no drained queue (call eqx_drain first)");
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = ctx->stream;
+  const int32_t C = ctx->C;
+  // compiled model tables -> device, only after they changed
+  const size_t model_bytes = offsetof(ModelTables, lut) + 4ull * ctx->lut_entries;
+  if (ctx->model_dirty) {
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_model.p, &ctx->model, model_bytes, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    ctx->model_dirty = false;
+  }
+  StepArgs a{};
+  a.n = ctx->n;
+  a.C = C;
+  a.client = ctx->q_client;
+  a.arrival = ctx->q_arrival;
+  a.in_tok = ctx->q_in;
+  a.true_out = ctx->q_true;
+  a.tag = ctx->q_tag;
+  a.id = ctx->q_id;
+  a.id_base = ctx->id_base;
+  a.perm = ctx->d_perm.as<uint32_t>();
+  a.seg_off = ctx->d_seg_off.as<int32_t>();
+  a.count = ctx->d_count.as<int32_t>();
+  a.head = ctx->d_head.as<int32_t>();
+  a.ufc = ctx->d_ufc.as<double>();
+  a.rfc = ctx->d_rfc.as<double>();
+  a.counter = ctx->d_counter.as<double>();
+  a.weight = ctx->d_weight.as<double>();
+  a.order = ctx->d_order.as<uint32_t>();
+  a.running = ctx->d_running.as<int32_t>();
+  a.backlogged = ctx->d_backlogged.as<int32_t>();
+  a.pred_out = ctx->d_pred.as<int32_t>();
+  a.bucket_out = ctx->d_bucket.as<uint8_t>();
+  a.ufc_out = ctx->d_ufc_out.as<double>();
+  a.rfc_out = ctx->d_rfc_out.as<double>();
+  a.ev_row = ctx->d_ev_row.as<int32_t>();
+  a.ev_kind = ctx->d_ev_kind.as<int32_t>();
+  a.ev_client = ctx->d_ev_client.as<int32_t>();
+  a.ev_pred = ctx->d_ev_pred.as<int32_t>();
+  a.ev_ufc = ctx->d_ev_ufc.as<double>();
+  a.ev_rfc = ctx->d_ev_rfc.as<double>();
+  a.ev_vtc = ctx->d_ev_vtc.as<double>();
+  a.ev_wait = ctx->d_ev_wait.as<double>();
+  a.ev_cap = ctx->ev_cap;
+  a.st = ctx->d_state.as<DevState>();
+  a.model = ctx->d_model.as<ModelTables>();
+  a.model_lut_entries = ctx->lut_entries;
+  a.model_smem_bytes = static_cast<int32_t>((model_bytes + 15) & ~size_t(15));
+  a.pol = ctx->pol;
+  a.now = now;
+  a.sel_threads = std::min(kStepThreads, std::max(32, (C + 31) / 32 * 32));
+  a.vec_ok = aligned16(a.client) && aligned16(a.arrival) && aligned16(a.in_tok) &&
+             (reinterpret_cast<uintptr_t>(a.tag) % 4 == 0) &&
+             (!a.true_out || aligned16(a.true_out));
+  // shared memory plan: model | per-client work (if it fits) | head windows
+  const size_t static_smem = 2048;  // SelShared + slack
+  const size_t budget = ctx->smem_optin - static_smem - a.model_smem_bytes;
+  const size_t cw_bytes = 12ull * 16 + static_cast<size_t>(C) * (6 * 8 + 6 * 4);
+  size_t smem = a.model_smem_bytes;
+  if (cw_bytes <= budget / 2) {
+    a.cw_global = nullptr;
+    smem += cw_bytes;
+  } else {
+    CUDA_TRY(ctx, ctx->d_cw.ensure(cw_bytes));
+    a.cw_global = ctx->d_cw.p;
+  }
+  const size_t left = ctx->smem_optin - static_smem - smem;
+  const int64_t free_slots = std::max<int64_t>(0, ctx->perf.max_batch - ctx->h_state->members);
+  int64_t W = std::min<int64_t>(free_slots + 2, C > 0 ? static_cast<int64_t>(left / (sizeof(WinEntry) * C)) : 0);
+  W = std::max<int64_t>(W, 0);
+  a.W = static_cast<int32_t>(W);
+  smem += static_cast<size_t>(W) * C * sizeof(WinEntry);
+  CUDA_TRY(ctx, cudaFuncSetAttribute(step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  const int grid = std::max(2, ctx->sm_count);  // CTA 0 selects, sm_count-1 CTAs stream
+  step_kernel<<<grid, kStepThreads, smem, s>>>(a);
+  CUDA_TRY(ctx, cudaGetLastError());
+  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_state, ctx->d_state.p, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+  ctx->step_pending = true;
+  ctx->stepped = true;
+  return EQX_OK;
+}
+
+eqx_status eqx_step_collect(eqx_ctx* ctx, eqx_step_summary* out) {
+  if (!ctx) return fail(ctx, EQX_ERR_ARG, "eqx_step_collect: NULL context");
+  cudaSetDevice(ctx->device);
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  const DevState& h = *ctx->h_state;
+  if (h.bad_client) return fail(ctx, EQX_ERR_CONFIG, "request references unknown client index");
+  if (out) {
+    out->n_events = h.n_events;
+    out->n_admitted = h.n_admitted;
+    out->n_rejected = h.n_rejected;
+    out->new_prefill_tokens = h.new_prefill;
+    out->length_fallbacks = static_cast<int64_t>(h.fallbacks - ctx->last_fallbacks);
+    out->noisy_near_ties = static_cast<int64_t>(h.near_ties - ctx->last_near_ties);
+    out->batch_members = h.members;
+    out->batch_reserved_kv_tokens = h.reserved;
+    out->queued = ctx->n - h.n_events;  // cold-step accounting: one drain, one step
+  }
+  ctx->last_fallbacks = h.fallbacks;
+  ctx->last_near_ties = h.near_ties;
+  ctx->step_pending = false;
+  return EQX_OK;
+}
+
+eqx_status eqx_step(eqx_ctx* ctx, double now, eqx_step_summary* out) {
+  eqx_status st = eqx_step_async(ctx, now);
+  if (st != EQX_OK) return st;
+  return eqx_step_collect(ctx, out);
+}
+
+eqx_status eqx_copy_events(eqx_ctx* ctx, int64_t cap, int64_t* id, int32_t* kind, int32_t* client,
+                           int32_t* pred, double* ufc_inc, double* rfc_inc, double* vtc_inc,
+                           double* wait_s) {
+  if (!ctx || !ctx->stepped) return fail(ctx, EQX_ERR_CONFIG, "eqx_copy_events: no step has run");
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = ctx->stream;
+  CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  const int64_t n = std::min<int64_t>(cap, ctx->h_state->n_events);
+  if (n <= 0) return EQX_OK;
+  if (id) {
+    gather_ids_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
+        ctx->d_ev_row.as<int32_t>(), n, ctx->q_id, ctx->id_base, ctx->d_ev_id.as<int64_t>());
+    CUDA_TRY(ctx, cudaGetLastError());
+    CUDA_TRY(ctx, cudaMemcpyAsync(id, ctx->d_ev_id.p, 8 * n, cudaMemcpyDeviceToHost, s));
+  }
+  if (kind) CUDA_TRY(ctx, cudaMemcpyAsync(kind, ctx->d_ev_kind.p, 4 * n, cudaMemcpyDeviceToHost, s));
+  if (client) CUDA_TRY(ctx, cudaMemcpyAsync(client, ctx->d_ev_client.p, 4 * n, cudaMemcpyDeviceToHost, s));
+  if (pred) CUDA_TRY(ctx, cudaMemcpyAsync(pred, ctx->d_ev_pred.p, 4 * n, cudaMemcpyDeviceToHost, s));
+  if (ufc_inc) CUDA_TRY(ctx, cudaMemcpyAsync(ufc_inc, ctx->d_ev_ufc.p, 8 * n, cudaMemcpyDeviceToHost, s));
+  if (rfc_inc) CUDA_TRY(ctx, cudaMemcpyAsync(rfc_inc, ctx->d_ev_rfc.p, 8 * n, cudaMemcpyDeviceToHost, s));
+  if (vtc_inc) CUDA_TRY(ctx, cudaMemcpyAsync(vtc_inc, ctx->d_ev_vtc.p, 8 * n, cudaMemcpyDeviceToHost, s));
+  if (wait_s) CUDA_TRY(ctx, cudaMemcpyAsync(wait_s, ctx->d_ev_wait.p, 8 * n, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  return EQX_OK;
+}
+
+eqx_status eqx_copy_scores(eqx_ctx* ctx, int64_t cap, int32_t* pred, uint8_t* bucket,
+                           double* ufc_inc, double* rfc_inc) {
+  if (!ctx || !ctx->stepped) return fail(ctx, EQX_ERR_CONFIG, "eqx_copy_scores: no step has run");
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = ctx->stream;
+  const int64_t n = std::min<int64_t>(cap, ctx->n);
+  if (n > 0) {
+    if (pred) CUDA_TRY(ctx, cudaMemcpyAsync(pred, ctx->d_pred.p, 4 * n, cudaMemcpyDeviceToHost, s));
+    if (bucket) CUDA_TRY(ctx, cudaMemcpyAsync(bucket, ctx->d_bucket.p, n, cudaMemcpyDeviceToHost, s));
+    if (ufc_inc) CUDA_TRY(ctx, cudaMemcpyAsync(ufc_inc, ctx->d_ufc_out.p, 8 * n, cudaMemcpyDeviceToHost, s));
+    if (rfc_inc) CUDA_TRY(ctx, cudaMemcpyAsync(rfc_inc, ctx->d_rfc_out.p, 8 * n, cudaMemcpyDeviceToHost, s));
+  }
+  CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  return EQX_OK;
+}
+
+// bindings/module.cpp:144-172 scalar helpers (host utilities; not part of the step)
+double eqx_ufc_increment(double weight, int32_t in, int32_t pred, double wait_s, double lat_ms,
+                         double delta, double ow) {
+  const double tokens = static_cast<double>(in) + ow * static_cast<double>(pred);
+  const double predict_s = lat_ms / 1000.0;
+  return weight * tokens / (1.0 + delta * (wait_s + predict_s));
+}
+
+double eqx_rfc_increment(double weight, double tps, double util) { return weight * tps * util; }
+
+}  // extern "C"

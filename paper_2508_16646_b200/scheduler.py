@@ -1,0 +1,452 @@
+"""Host mirror of the reference scheduler interface over the C ABI (include/eqx.h).
+
+Names, argument meaning and error behaviour follow the reference:
+  * types      PolicySpec / EquinoxParams (scheduler.hpp:18-81), PerfParams (gpu_model.hpp:14-28),
+               GpuProfile / ProfileEntry (gpu_model.hpp:61-77), ClientState (scheduler.hpp:35-43),
+               MopeModel (predictor.hpp:85-92, JSON as predictor.cpp:408-454)
+  * errors     ConfigError/ParseError -> ValueError, TrainingError/EngineError -> RuntimeError
+               (bindings/module.cpp:53-56)
+  * functions  ufc_increment / rfc_increment with the pybind signatures (module.cpp:144-172),
+               default_bucket_bounds (gpu_model.cpp:128-130)
+  * the path   GpuScheduler.drain() == SimulationRun::drain_arrivals (engine.cpp:171-197) for a
+               batch of arrivals, GpuScheduler.step(now) == SimulationRun::admit_requests
+               (engine.cpp:207-271) plus whole-queue scoring, both executed by sm_100a kernels.
+
+Every scheduling decision runs on the GPU; nothing here computes a step on the CPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+from dataclasses import dataclass, field
+from typing import Iterable, Sequence
+
+import numpy as np
+
+from . import _lib as L
+
+
+# ---- errors (errors.hpp:10-31; module.cpp:53-56) -------------------------------------------
+class ConfigError(ValueError):
+    pass
+
+
+class ParseError(ValueError):
+    pass
+
+
+class TrainingError(RuntimeError):
+    pass
+
+
+class EngineError(RuntimeError):
+    pass
+
+
+_ERRORS = {L.EQX_ERR_CONFIG: ConfigError, L.EQX_ERR_PARSE: ParseError,
+           L.EQX_ERR_ENGINE: EngineError, L.EQX_ERR_CUDA: EngineError, L.EQX_ERR_ARG: ValueError}
+
+POLICY_KINDS = {"fcfs": 0, "vtc": 1, "equinox": 2}
+NORM_MODES = {"max_over_clients": 0, "none": 1}
+PREDICTORS = {"oracle": 0, "mope": 1, "noisy_oracle": 2, "single_proxy": 3}
+EV_ADMITTED, EV_REJECTED = 1, 2
+
+
+# ---- parameter blocks ------------------------------------------------------------------------
+@dataclass
+class EquinoxParams:
+    alpha: float = 0.7
+    delta: float = 0.1
+    output_weight: float = 4.0
+    norm_mode: str = "max_over_clients"
+
+    def beta(self) -> float:
+        return 1.0 - self.alpha
+
+    def validate(self) -> None:  # scheduler.cpp:11-17
+        if self.alpha < 0.0 or self.alpha > 1.0:
+            raise ConfigError("alpha must lie in [0, 1]")
+        if self.delta < 0.0:
+            raise ConfigError("delta must be >= 0")
+        if self.output_weight <= 0.0:
+            raise ConfigError("output_weight must be > 0")
+
+
+@dataclass
+class PolicySpec:
+    kind: str = "equinox"
+    equinox: EquinoxParams = field(default_factory=EquinoxParams)
+    vtc_use_prediction: bool = False
+    counter_lift: bool = True
+
+    def label(self) -> str:  # scheduler.cpp:86-90
+        return self.kind + ("+pred" if self.kind == "vtc" and self.vtc_use_prediction else "")
+
+
+@dataclass
+class PerfParams:
+    prefill_linear_ms: float = 0.05
+    prefill_quad_ms: float = 1e-6
+    decode_base_ms: float = 5.0
+    decode_per_ctx_ms: float = 0.002
+    refresh_ms: float = 15.0
+    mem_per_token_bytes: float = 0.5 * 1024.0 * 1024.0
+    mem_capacity_bytes: float = 60.0 * 1024.0 * 1024.0 * 1024.0
+    max_batch: int = 64
+
+    def token_capacity(self) -> float:
+        return self.mem_capacity_bytes / self.mem_per_token_bytes
+
+
+@dataclass
+class ProfileEntry:
+    bucket_upper: int
+    latency_ms: float
+    gpu_util: float
+    tps: float
+
+
+@dataclass
+class GpuProfile:
+    entries: list
+
+    def empty(self) -> bool:
+        return len(self.entries) == 0
+
+    @staticmethod
+    def from_arrays(upper, lat, util, tps) -> "GpuProfile":
+        return GpuProfile([ProfileEntry(int(u), float(a), float(b), float(c))
+                           for u, a, b, c in zip(upper, lat, util, tps)])
+
+    @staticmethod
+    def load_json(path: str) -> "GpuProfile":
+        with open(path) as f:
+            d = json.load(f)
+        return GpuProfile.from_arrays(d["upper"], d["lat"], d["util"], d["tps"])
+
+
+def default_bucket_bounds() -> list:
+    """gpu_model.cpp:128-130."""
+    return [32, 64, 128, 256, 512, 1024, 2048, 4096]
+
+
+@dataclass
+class ClientState:
+    client_id: str
+    weight: float = 1.0
+    ufc: float = 0.0
+    rfc: float = 0.0
+    counter: float = 0.0
+    accumulated_service: float = 0.0
+    backlogged: bool = False
+
+
+class MopeModel:
+    """MopeModel JSON (predictor.cpp:408-454): bucket_bounds, router{input_len_thresholds,
+    mix_weight, num_buckets, keyword_scores}, experts[{bucket, bin_upper, bin_value, out_min,
+    out_max}]."""
+
+    def __init__(self, doc: dict):
+        try:
+            self.bucket_bounds = [int(x) for x in doc["bucket_bounds"]]
+            r = doc["router"]
+            self.thresholds = [int(x) for x in r["input_len_thresholds"]]
+            self.mix_weight = float(r["mix_weight"])
+            self.num_buckets = int(r["num_buckets"])
+            self.keyword_scores = {str(k): [float(v) for v in row] for k, row in r["keyword_scores"].items()}
+            self.experts = [{"bucket": int(e["bucket"]), "bin_upper": [int(x) for x in e["bin_upper"]],
+                             "bin_value": [int(x) for x in e["bin_value"]], "out_min": int(e["out_min"]),
+                             "out_max": int(e["out_max"])} for e in doc["experts"]]
+        except (KeyError, TypeError, ValueError) as exc:
+            raise ParseError(f"malformed MoPE model JSON: {exc}") from exc
+        if not self.experts:
+            raise TrainingError("MoPE predictor constructed without trained experts")
+
+    @staticmethod
+    def from_json(doc) -> "MopeModel":
+        return MopeModel(json.loads(doc) if isinstance(doc, str) else doc)
+
+    @staticmethod
+    def load(path: str) -> "MopeModel":
+        with open(path) as f:
+            return MopeModel(json.load(f))
+
+    def to_json(self) -> dict:
+        return {"bucket_bounds": self.bucket_bounds,
+                "router": {"input_len_thresholds": self.thresholds, "mix_weight": self.mix_weight,
+                           "num_buckets": self.num_buckets, "keyword_scores": self.keyword_scores},
+                "experts": self.experts}
+
+
+# ---- module.cpp:144-172 scalar helpers ---------------------------------------------------------
+def ufc_increment(weight: float, input_tokens: int, predicted_output_tokens: int, wait_s: float = 0.0,
+                  predicted_latency_ms: float = 0.0, delta: float = 0.1, output_weight: float = 4.0) -> float:
+    return L.load().eqx_ufc_increment(weight, input_tokens, predicted_output_tokens, wait_s,
+                                      predicted_latency_ms, delta, output_weight)
+
+
+def rfc_increment(weight: float, tps: float, gpu_util: float) -> float:
+    return L.load().eqx_rfc_increment(weight, tps, gpu_util)
+
+
+# ---- the request batch -------------------------------------------------------------------------
+def _as_col(x, dtype, keep: list):
+    """numpy -> (host ptr, HOST); torch CUDA tensor -> (device ptr, DEVICE)."""
+    if x is None:
+        return None, None
+    mod = type(x).__module__
+    if mod.startswith("torch"):
+        import torch
+        want = {np.int32: torch.int32, np.int64: torch.int64, np.float64: torch.float64,
+                np.uint8: torch.uint8}[dtype]
+        if x.dtype != want:
+            raise ValueError(f"column dtype {x.dtype} != {want}")
+        x = x.contiguous()
+        keep.append(x)
+        return x.data_ptr(), (L.EQX_DEVICE if x.is_cuda else L.EQX_HOST)
+    a = np.ascontiguousarray(x, dtype=dtype)
+    keep.append(a)
+    return a.ctypes.data, L.EQX_HOST
+
+
+@dataclass
+class StepResult:
+    """Events of one step in log order (Admitted / Rejected, engine.cpp:223-268) with the
+    PendingContribution of each admission (scheduler.hpp:131-138)."""
+    ids: np.ndarray
+    kinds: np.ndarray
+    clients: np.ndarray
+    preds: np.ndarray
+    ufc_inc: np.ndarray
+    rfc_inc: np.ndarray
+    vtc_inc: np.ndarray
+    wait_s: np.ndarray
+    n_admitted: int
+    n_rejected: int
+    new_prefill_tokens: int
+    length_fallbacks: int
+    noisy_near_ties: int
+    batch_members: int
+    batch_reserved_kv_tokens: int
+
+    @property
+    def admitted(self) -> np.ndarray:
+        return self.ids[self.kinds == EV_ADMITTED]
+
+    @property
+    def rejected(self) -> np.ndarray:
+        return self.ids[self.kinds == EV_REJECTED]
+
+
+class GpuScheduler:
+    """One engine instance's scheduler state on one B200 (one CUDA stream, not thread-safe,
+    like SchedulerPolicy, scheduler.hpp:97-100)."""
+
+    def __init__(self, clients: Sequence[ClientState], policy: PolicySpec | None = None,
+                 perf: PerfParams | None = None, profile: GpuProfile | None = None,
+                 predictor: str = "mope", model: MopeModel | None = None,
+                 tag_names: Sequence[str] = (), noisy_l1: float = 33.0, noisy_seed: int = 1,
+                 backfill: bool = False, running: Iterable[int] | None = None, device: int = 0):
+        self._lib = L.load()
+        h = C.c_void_p()
+        self._check(self._lib.eqx_ctx_create(device, C.byref(h)), None)
+        self._ctx = h
+        self._keep: list = []
+        self.policy = policy or PolicySpec()
+        self.perf = perf or PerfParams()
+        self.backfill = backfill
+        self.tag_names = list(tag_names)
+        self.client_ids = [c.client_id for c in clients]
+        self._set_policy()
+        p = L.Perf(int(self.perf.max_batch), float(self.perf.mem_per_token_bytes),
+                   float(self.perf.mem_capacity_bytes))
+        self._check(self._lib.eqx_set_perf(self._ctx, C.byref(p)))
+        if profile is None or profile.empty():
+            raise ConfigError("engine needs a non-empty GPU profile")
+        self._set_profile(profile)
+        self._set_predictor(predictor, model, noisy_l1, noisy_seed)
+        self.set_clients(clients, running)
+
+    # -- plumbing --
+    def _check(self, rc: int, ctx="self") -> None:
+        if rc != L.EQX_OK:
+            msg = self._lib.eqx_last_error(self._ctx if ctx == "self" else None)
+            raise _ERRORS.get(rc, EngineError)((msg or b"").decode())
+
+    def close(self) -> None:
+        if getattr(self, "_ctx", None):
+            self._lib.eqx_ctx_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def stream_ptr(self) -> int:
+        return self._lib.eqx_ctx_stream(self._ctx)
+
+    def _set_policy(self) -> None:
+        sp = self.policy
+        if sp.kind not in POLICY_KINDS:
+            raise ConfigError(f"unknown policy kind '{sp.kind}'")
+        if sp.equinox.norm_mode not in NORM_MODES:
+            raise ConfigError(f"unknown norm_mode '{sp.equinox.norm_mode}'")
+        p = L.Policy(POLICY_KINDS[sp.kind], sp.equinox.alpha, sp.equinox.delta, sp.equinox.output_weight,
+                     NORM_MODES[sp.equinox.norm_mode], int(sp.vtc_use_prediction), int(sp.counter_lift),
+                     int(self.backfill))
+        self._check(self._lib.eqx_set_policy(self._ctx, C.byref(p)))
+
+    def _set_profile(self, profile: GpuProfile) -> None:
+        e = profile.entries
+        up = np.array([x.bucket_upper for x in e], np.int32)
+        lat = np.array([x.latency_ms for x in e], np.float64)
+        ut = np.array([x.gpu_util for x in e], np.float64)
+        tp = np.array([x.tps for x in e], np.float64)
+        pr = L.Profile(len(e), up.ctypes.data_as(L._i32p), lat.ctypes.data_as(L._dp),
+                       ut.ctypes.data_as(L._dp), tp.ctypes.data_as(L._dp))
+        self._check(self._lib.eqx_set_profile(self._ctx, C.byref(pr)))
+
+    def _set_predictor(self, kind: str, model: MopeModel | None, l1: float, seed: int) -> None:
+        if kind not in PREDICTORS:
+            raise ConfigError(f"unknown predictor kind '{kind}'")
+        pd = L.Predictor()
+        pd.kind = PREDICTORS[kind]
+        pd.noisy_l1 = float(l1)
+        pd.noisy_seed = int(seed)
+        keep = []
+        if kind in ("mope", "single_proxy"):
+            if model is None:
+                raise ConfigError(f"predictor '{kind}' needs a MopeModel")
+            names = sorted(model.keyword_scores)  # std::map order
+            nb = model.num_buckets
+            rows = np.array([model.keyword_scores[k] for k in names], np.float64).reshape(len(names), nb)
+            nbins = len(model.experts[0]["bin_upper"])
+            if any(len(x["bin_upper"]) != nbins or len(x["bin_value"]) != nbins for x in model.experts):
+                raise ParseError("malformed MoPE model: experts with different bin counts")
+            arrs = dict(
+                thr=np.array(model.thresholds, np.int32), rows=rows,
+                bu=np.array([x["bin_upper"] for x in model.experts], np.int32),
+                bv=np.array([x["bin_value"] for x in model.experts], np.int32),
+                mn=np.array([x["out_min"] for x in model.experts], np.int32),
+                mx=np.array([x["out_max"] for x in model.experts], np.int32),
+                tr=np.array([names.index(t) if t in model.keyword_scores else -1 for t in self.tag_names] or [0],
+                            np.int32))
+            keep.append(arrs)
+            m = pd.mope
+            m.n_thresholds = len(model.thresholds)
+            m.thresholds = arrs["thr"].ctypes.data_as(L._i32p)
+            m.mix_weight = model.mix_weight
+            m.num_buckets = nb
+            m.n_rows = len(names)
+            m.rows = arrs["rows"].ctypes.data_as(L._dp)
+            m.n_experts = len(model.experts)
+            m.n_bins = nbins
+            m.bin_upper = arrs["bu"].ctypes.data_as(L._i32p)
+            m.bin_value = arrs["bv"].ctypes.data_as(L._i32p)
+            m.out_min = arrs["mn"].ctypes.data_as(L._i32p)
+            m.out_max = arrs["mx"].ctypes.data_as(L._i32p)
+            m.n_tags = len(self.tag_names)
+            m.tag_row = arrs["tr"].ctypes.data_as(L._i32p)
+        self.predictor = kind
+        self._check(self._lib.eqx_set_predictor(self._ctx, C.byref(pd)))
+
+    # -- ledger --
+    def set_clients(self, clients: Sequence[ClientState], running: Iterable[int] | None = None) -> None:
+        n = len(clients)
+        self.client_ids = [c.client_id for c in clients]
+        names = b"".join(c.client_id.encode() + b"\0" for c in clients)
+        w = np.array([c.weight for c in clients], np.float64)
+        u = np.array([c.ufc for c in clients], np.float64)
+        r = np.array([c.rfc for c in clients], np.float64)
+        k = np.array([c.counter for c in clients], np.float64)
+        run = np.array(list(running) if running is not None else [0] * n, np.int32)
+        self._check(self._lib.eqx_set_clients(self._ctx, n, names, w.ctypes.data_as(L._dp),
+                                              u.ctypes.data_as(L._dp), r.ctypes.data_as(L._dp),
+                                              k.ctypes.data_as(L._dp), run.ctypes.data_as(L._i32p)))
+
+    def ledger(self) -> dict:
+        n = len(self.client_ids)
+        out = {k: np.zeros(n) for k in ("ufc", "rfc", "counter")}
+        out["backlogged"] = np.zeros(n, np.int32)
+        out["running"] = np.zeros(n, np.int32)
+        self._check(self._lib.eqx_get_clients(self._ctx, n, out["ufc"].ctypes.data_as(L._dp),
+                                              out["rfc"].ctypes.data_as(L._dp),
+                                              out["counter"].ctypes.data_as(L._dp),
+                                              out["backlogged"].ctypes.data_as(L._i32p),
+                                              out["running"].ctypes.data_as(L._i32p)))
+        return out
+
+    def clients(self) -> list:
+        led = self.ledger()
+        return [ClientState(cid, ufc=float(led["ufc"][i]), rfc=float(led["rfc"][i]),
+                            counter=float(led["counter"][i]), backlogged=bool(led["backlogged"][i]))
+                for i, cid in enumerate(self.client_ids)]
+
+    def set_batch(self, members: int, reserved_kv_tokens: int) -> None:
+        self._check(self._lib.eqx_set_batch(self._ctx, int(members), int(reserved_kv_tokens)))
+
+    # -- the hot path --
+    def drain(self, client, arrival_s, input_tokens, tag=None, true_output_tokens=None, ids=None,
+              id_base: int = 0) -> None:
+        """Queue a batch of arrivals (arrival order).  numpy columns are copied host->device;
+        torch CUDA tensors are used in place."""
+        keep: list = []
+        cols = {}
+        loc = set()
+        for name, x, dt in (("client", client, np.int32), ("arrival_s", arrival_s, np.float64),
+                            ("input_tokens", input_tokens, np.int32), ("tag", tag, np.uint8),
+                            ("true_output_tokens", true_output_tokens, np.int32), ("id", ids, np.int64)):
+            ptr, where = _as_col(x, dt, keep)
+            cols[name] = ptr
+            if where is not None:
+                loc.add(where)
+        if len(loc) > 1:
+            raise ValueError("drain: mix of host and device columns")
+        n = len(client)
+        rq = L.Requests(n, cols["id"], id_base, cols["client"], cols["arrival_s"], cols["input_tokens"],
+                        cols["true_output_tokens"], cols["tag"], loc.pop() if loc else L.EQX_HOST)
+        self._check(self._lib.eqx_drain(self._ctx, C.byref(rq)))
+        self._keep = keep  # device columns are used in place: keep them alive with the queue
+        self.n_queued = n
+
+    def step_async(self, now: float) -> None:
+        self._check(self._lib.eqx_step_async(self._ctx, float(now)))
+
+    def collect(self, with_events: bool = True) -> StepResult:
+        s = L.StepSummary()
+        self._check(self._lib.eqx_step_collect(self._ctx, C.byref(s)))
+        return self._result(s, with_events)
+
+    def step(self, now: float, with_events: bool = True) -> StepResult:
+        s = L.StepSummary()
+        self._check(self._lib.eqx_step(self._ctx, float(now), C.byref(s)))
+        return self._result(s, with_events)
+
+    def _result(self, s: L.StepSummary, with_events: bool) -> StepResult:
+        n = int(s.n_events) if with_events else 0
+        ids = np.zeros(n, np.int64)
+        kinds, cl, pr = (np.zeros(n, np.int32) for _ in range(3))
+        ui, ri, vi, wt = (np.zeros(n) for _ in range(4))
+        if n:
+            self._check(self._lib.eqx_copy_events(self._ctx, n, ids.ctypes.data_as(L._i64p),
+                                                  kinds.ctypes.data_as(L._i32p), cl.ctypes.data_as(L._i32p),
+                                                  pr.ctypes.data_as(L._i32p), ui.ctypes.data_as(L._dp),
+                                                  ri.ctypes.data_as(L._dp), vi.ctypes.data_as(L._dp),
+                                                  wt.ctypes.data_as(L._dp)))
+        return StepResult(ids, kinds, cl, pr, ui, ri, vi, wt, int(s.n_admitted), int(s.n_rejected),
+                          int(s.new_prefill_tokens), int(s.length_fallbacks), int(s.noisy_near_ties),
+                          int(s.batch_members), int(s.batch_reserved_kv_tokens))
+
+    def scores(self) -> dict:
+        """Per-request scores of the queue in drain order: pred, bucket, ufc_inc, rfc_inc."""
+        n = self.n_queued
+        out = {"pred": np.zeros(n, np.int32), "bucket": np.zeros(n, np.uint8),
+               "ufc_inc": np.zeros(n), "rfc_inc": np.zeros(n)}
+        self._check(self._lib.eqx_copy_scores(self._ctx, n, out["pred"].ctypes.data_as(L._i32p),
+                                              out["bucket"].ctypes.data_as(L._u8p),
+                                              out["ufc_inc"].ctypes.data_as(L._dp),
+                                              out["rfc_inc"].ctypes.data_as(L._dp)))
+        return out

@@ -1,0 +1,48 @@
+"""CPU: the C-ABI library builds for sm_100a, loads, and exports every symbol eqx.h declares.
+No compute calls are made here (no GPU in this container)."""
+import os
+import re
+import subprocess
+
+import pytest
+
+from paper_2508_16646_b200 import _lib as L
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "eqx.h")).read()
+    return sorted(set(re.findall(r"\b(eqx_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = L.load()
+    decl = declared_symbols()
+    assert decl == L.EXPORTED
+    for name in decl:
+        assert hasattr(lib, name), name
+    assert lib.eqx_abi_version() == 1
+
+
+def test_library_is_sm100a_only():
+    out = subprocess.run(["cuobjdump", "--list-elf", L.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(8\d|9\d)", out)
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2508_16646_b200 import scheduler as S
+    prof = S.GpuProfile([S.ProfileEntry(32, 1.0, 0.5, 100.0)])
+    with pytest.raises(S.EngineError):
+        S.GpuScheduler([S.ClientState("a")], profile=prof, predictor="oracle")
+
+
+def test_scalar_helpers_match_reference_known_answers():
+    lib = L.load()
+    assert lib.eqx_ufc_increment(1.0, 100, 400, 0.0, 0.0, 0.1, 4.0) == 1700.0
+    assert lib.eqx_ufc_increment(1.0, 100, 400, 5.0, 5000.0, 0.1, 4.0) == 850.0
+    assert lib.eqx_rfc_increment(1.0, 1000.0, 0.9) == 900.0

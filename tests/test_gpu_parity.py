@@ -1,0 +1,102 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference-generated goldens
+and the C restatement, bit-exact (ids/order/kinds exact; FP64 ledger and increments exact,
+which is stricter than the north star's 1e-5 relative)."""
+import numpy as np
+import pytest
+
+import harness as H
+from helpers import (case_from_golden, compare_step, default_model, default_profile, golden_names, gpu_run,
+                     load_golden)
+from paper_2508_16646_b200 import workload as W
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_golden_step(name):
+    meta, ins, outs = load_golden(name)
+    sch, res = gpu_run(case_from_golden(meta, ins))
+    if res.noisy_near_ties:
+        pytest.skip(f"{res.noisy_near_ties} flagged near-ties (log1p ulp) -- allowed by the north star")
+    compare_step(res, sch, outs)
+
+
+def test_golden_step_device_columns():
+    """Zero-copy drain of torch CUDA tensors (the resident-queue path the bench times)."""
+    meta, ins, outs = load_golden("eqx_max_warm")
+    sch, res = gpu_run(case_from_golden(meta, ins), device_columns=True)
+    compare_step(res, sch, outs)
+
+
+def _random_case(seed, n, C, **over):
+    rng = np.random.default_rng(seed)
+    q = W.lmsys_queue(n, C, seed=seed, untagged_frac=0.02, heavy_frac=0.5 if seed % 3 == 0 else None)
+    led = W.warm_ledger(C, seed=seed + 1)
+    kw = dict(kind=int(rng.integers(0, 3)), norm_mode=int(rng.integers(0, 2)),
+              vtc_use_prediction=bool(rng.integers(0, 2)), backfill=bool(rng.integers(0, 2)),
+              max_batch=int(rng.choice([8, 64, 300, 4096])), pred_kind=int(rng.choice([0, 1, 1, 3])),
+              mem_per_token_bytes=float(rng.choice([1.0, 0.5 * 1024 * 1024])),
+              alpha=float(rng.choice([0.0, 0.3, 0.7, 1.0])), delta=float(rng.choice([0.0, 0.1, 2.0])))
+    kw["mem_capacity_bytes"] = (float(rng.choice([800.0, 4000.0, 30000.0])) if kw["mem_per_token_bytes"] == 1.0
+                                else 60.0 * 1024 ** 3)
+    kw.update(over)
+    warm = rng.integers(0, 2)
+    return H.StepCase(client=q["client"], arrival=q["arrival"], in_tokens=q["in_tokens"], true_out=q["true_out"],
+                      tag=q["tag"], client_names=q["client_names"], model=default_model(), profile=default_profile(),
+                      ufc0=led["ufc"] * warm, rfc0=led["rfc"] * warm, counter0=led["counter"] * warm,
+                      weight=rng.choice([0.5, 1.0, 2.0], C), **kw)
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_steps_vs_oracle(seed):
+    rng = np.random.default_rng(1000 + seed)
+    C = int(rng.choice([1, 5, 31, 64, 200, 777, 1500, 3000]))
+    n = int(rng.integers(0, 60000))
+    case = _random_case(seed, n, C)
+    want = H.run_step(case, "oracle")
+    sch, res = gpu_run(case)
+    compare_step(res, sch, want)
+
+
+@pytest.mark.slow
+def test_cfg2_full_size_vs_oracle():
+    """BASELINE configs[1]: 1M queued requests, 64 clients, MoPE, warm ledger, max_batch 64."""
+    q = W.lmsys_queue(1_000_000, 64, seed=1)
+    led = W.warm_ledger(64, seed=2)
+    case = H.StepCase(client=q["client"], arrival=q["arrival"], in_tokens=q["in_tokens"], true_out=q["true_out"],
+                      tag=q["tag"], client_names=q["client_names"], model=default_model(),
+                      profile=default_profile(), ufc0=led["ufc"], rfc0=led["rfc"], counter0=led["counter"])
+    want = H.run_step(case, "oracle")
+    sch, res = gpu_run(case, device_columns=True)
+    compare_step(res, sch, want)
+    assert res.n_admitted == 64
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("backfill", [False, True])
+def test_cfg3_heavy_hitter_vs_oracle(backfill):
+    """configs[2]: 1k clients, client 0 sends 50%, max_batch 4096 -> the KV budget cuts."""
+    q = W.lmsys_queue(1_000_000, 1000, seed=3, heavy_frac=0.5)
+    case = H.StepCase(client=q["client"], arrival=q["arrival"], in_tokens=q["in_tokens"], true_out=q["true_out"],
+                      tag=q["tag"], client_names=q["client_names"], model=default_model(),
+                      profile=default_profile(), max_batch=4096, backfill=backfill)
+    want = H.run_step(case, "oracle")
+    sch, res = gpu_run(case, device_columns=True)
+    compare_step(res, sch, want)
+    # size-independent properties: the KV reservation never exceeds the budget
+    assert res.batch_reserved_kv_tokens * case.mem_per_token_bytes <= case.mem_capacity_bytes
+
+
+def test_scalar_helpers_and_errors():
+    from paper_2508_16646_b200 import scheduler as S
+    assert S.ufc_increment(1.0, 100, 400) == 1700.0
+    assert S.ufc_increment(1.0, 100, 400, 5.0, 5000.0) == 850.0
+    assert S.rfc_increment(1.0, 1000.0, 0.9) == 900.0
+    prof = S.GpuProfile([S.ProfileEntry(32, 1.0, 0.5, 100.0)])
+    with pytest.raises(S.ConfigError, match="alpha"):
+        S.GpuScheduler([S.ClientState("a")], policy=S.PolicySpec(equinox=S.EquinoxParams(alpha=1.2)),
+                       profile=prof, predictor="oracle")
+    with pytest.raises(S.ConfigError, match="non-positive weight"):
+        S.GpuScheduler([S.ClientState("a", weight=0.0)], profile=prof, predictor="oracle")
+    with pytest.raises(S.ConfigError, match="non-empty GPU profile"):
+        S.GpuScheduler([S.ClientState("a")], profile=S.GpuProfile([]), predictor="oracle")
