@@ -173,37 +173,52 @@ def run_ours(args, rank, world):
     stream = torch.cuda.ExternalStream(sch.stream_ptr, device=dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
-    def one_step(timed: bool):
-        sch.set_clients(clients)  # reset the ledger: every step is the same cold step
-        with torch.cuda.stream(stream):
-            flush.zero_()
-            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
-            e0.record(stream)
-            sch.drain(**cols)
-            e1.record(stream)
-            sch.step_async(1.0)
-            e2.record(stream)
-        res = sch.collect(with_events=False)
-        return e0, e1, e2, res
+    sch.set_batch(0, 0)
+    sch.checkpoint()  # device-side snapshot: every timed step restarts from the same cold state
 
-    for _ in range(args.warmup):
-        one_step(False)
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    recs = []
-    with ClockSampler(local) as clk:
-        for _ in range(args.steps):
-            recs.append(one_step(True))
+    def enqueue_step(graph: bool):
+        """All launches are asynchronous: the 256 MiB flush before each step lets the host run
+        ahead, so the events time GPU work only."""
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        with torch.cuda.stream(stream):
+            sch.restore_async()
+            flush.zero_()
+            e0.record(stream)
+            if graph:
+                sch.drain_step_async(1.0, **cols)
+                e1.record(stream)
+            else:
+                sch.drain(**cols)
+                e1.record(stream)
+                sch.step_async(1.0)
+            e2.record(stream)
+        return e0, e1, e2
+
+    def run_loop(graph: bool, steps: int):
+        for _ in range(args.warmup):
+            enqueue_step(graph)
         torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    step_ms = np.array([a.elapsed_time(c) for a, b, c, _ in recs])
-    drain_ms = np.array([a.elapsed_time(b) for a, b, c, _ in recs])
-    kern_ms = np.array([b.elapsed_time(c) for a, b, c, _ in recs])
-    res = recs[-1][3]
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        recs = [enqueue_step(graph) for _ in range(steps)]
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        return recs
+
+    # split launches: per-phase breakdown + the fused kernel's duration for the roofline
+    split = run_loop(False, args.steps)
+    res = sch.collect(with_events=False)
+    drain_ms = np.array([a.elapsed_time(b) for a, b, c in split])
+    kern_ms = np.array([b.elapsed_time(c) for a, b, c in split])
+    # headline: the public one-call path, replayed as a CUDA graph
+    with ClockSampler(local) as clk:
+        recs = run_loop(True, args.steps)
+    res_g = sch.collect(with_events=False)
+    assert res_g.n_admitted == res.n_admitted
+    step_ms = np.array([a.elapsed_time(c) for a, b, c in recs])
     total_ms = float(step_ms.sum())
     if dist:
         t = torch.tensor([total_ms], device=dev)
@@ -216,8 +231,8 @@ def run_ours(args, rank, world):
             dict(client=q["client"], arrival_s=q["arrival"], input_tokens=q["in_tokens"], tag=tag_ids(q)).items()}
     e2e_t = []
     d2h = 0
-    for i in range(args.warmup + max(3, args.steps // 4)):
-        sch.set_clients(clients)
+    for i in range(0 if args.profile else args.warmup + max(3, args.steps // 4)):
+        sch.restore_async()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         sch.drain(**host)
@@ -229,7 +244,7 @@ def run_ours(args, rank, world):
         d2h = r.ids.nbytes + r.kinds.nbytes + r.clients.nbytes + r.preds.nbytes + 4 * r.ufc_inc.nbytes + \
             sum(v.nbytes for v in led_out.values()) + 80
     h2d = sum(v.numel() * v.element_size() for v in host.values())
-    e2e_val = world * n / float(np.median(e2e_t))
+    e2e_val = world * n / float(np.median(e2e_t)) if e2e_t else None
 
     if rank != 0:
         if dist:
@@ -259,17 +274,19 @@ def run_ours(args, rank, world):
                    "predictor": "mope(3) trained by the reference on its builtin corpus (seed 7)",
                    "queue_per_gpu": n, "l2": "flushed between steps (256 MiB memset outside the events)",
                    "parallelism": f"client-sharded replicas x{world}" if world > 1 else "single GPU"},
-        "breakdown_ms": {"drain_p50": float(np.median(drain_ms)), "step_kernel_p50": float(np.median(kern_ms))},
+        "breakdown_ms": {"drain_p50": float(np.median(drain_ms)), "step_kernel_p50": float(np.median(kern_ms)),
+                         "split_launch_step_p50": float(np.median(drain_ms + kern_ms)),
+                         "graph_step_p50": float(np.median(step_ms))},
         "admitted": res.n_admitted,
         "roofline": {"bound": "hbm", "kernel": "step_kernel (fused whole-queue scoring + selection CTA)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "algo_bytes_per_request": ALGO_BYTES_K1, "peak_source": peak_src},
         "e2e": {"value": e2e_val, "unit": "requests/s", "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": int(d2h), "p50_ms": float(np.median(e2e_t) * 1e3)},
-        "gpu_launches": 5 * args.steps,
+                "d2h_bytes_per_step": int(d2h), "p50_ms": float(np.median(e2e_t) * 1e3) if e2e_t else None},
+        "gpu_launches": 5 * args.steps,  # per step: hist, scan, rank, lift, step_kernel
         "clocks": clk.summary(),
     }
-    if not args.no_cpu_baseline:
+    if not (args.no_cpu_baseline or args.profile):
         times, kind, _ = cpu_baseline(q, led, model, prof, args.cpu_reps)
         if times:
             t = np.array(times[1:] if len(times) > 1 else times)
@@ -290,6 +307,7 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3"])
     ap.add_argument("--cpu-reps", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu: no e2e / cpu legs")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     rank = int(os.environ.get("RANK", "0"))

@@ -157,6 +157,11 @@ eqx_status eqx_get_clients(eqx_ctx* ctx, int32_t n, double* ufc, double* rfc, do
 /* Existing batch: BatchState::members.size() and reserved_kv_tokens() (gpu_model.cpp:40-46). */
 eqx_status eqx_set_batch(eqx_ctx* ctx, int32_t members, int64_t reserved_kv_tokens);
 
+/* Device-side snapshot of the ledger (ufc, rfc, counter, running, backlogged) and the batch
+ * state, and its asynchronous restore on the context stream (what-if / replica replays). */
+eqx_status eqx_ledger_checkpoint(eqx_ctx* ctx);
+eqx_status eqx_ledger_restore_async(eqx_ctx* ctx);
+
 /* ---- the hot path ------------------------------------------------------------------------ */
 /* drain_arrivals (engine.cpp:171-197) for a whole batch of arrivals: the batch becomes the
  * per-client FIFO queues (client-grouped index in HBM), clients that go idle -> backlogged get
@@ -167,6 +172,10 @@ eqx_status eqx_drain(eqx_ctx* ctx, const eqx_requests* arrivals);
  * whole queue: MoPE gate+experts -> map_metrics -> ufc/rfc increments (the prediction
  * record as of drain).  Enqueued on the context stream; results stay on the device. */
 eqx_status eqx_step_async(eqx_ctx* ctx, double now);
+/* eqx_drain + eqx_step_async in one call.  For a resident queue (EQX_DEVICE columns) the
+ * whole launch sequence is captured once into a CUDA graph and replayed while every launch
+ * parameter (pointers, sizes, policy, `now`) is unchanged. */
+eqx_status eqx_drain_step_async(eqx_ctx* ctx, const eqx_requests* arrivals, double now);
 /* Waits for the last step and returns its summary. */
 eqx_status eqx_step_collect(eqx_ctx* ctx, eqx_step_summary* out);
 /* Convenience: eqx_step_async + eqx_step_collect. */

@@ -73,8 +73,11 @@ _SIGS = {
     "eqx_set_clients": ([C.c_void_p, C.c_int32, C.c_char_p, _dp, _dp, _dp, _dp, _i32p], C.c_int),
     "eqx_get_clients": ([C.c_void_p, C.c_int32, _dp, _dp, _dp, _i32p, _i32p], C.c_int),
     "eqx_set_batch": ([C.c_void_p, C.c_int32, C.c_int64], C.c_int),
+    "eqx_ledger_checkpoint": ([C.c_void_p], C.c_int),
+    "eqx_ledger_restore_async": ([C.c_void_p], C.c_int),
     "eqx_drain": ([C.c_void_p, C.POINTER(Requests)], C.c_int),
     "eqx_step_async": ([C.c_void_p, C.c_double], C.c_int),
+    "eqx_drain_step_async": ([C.c_void_p, C.POINTER(Requests), C.c_double], C.c_int),
     "eqx_step_collect": ([C.c_void_p, C.POINTER(StepSummary)], C.c_int),
     "eqx_step": ([C.c_void_p, C.c_double, C.POINTER(StepSummary)], C.c_int),
     "eqx_copy_events": ([C.c_void_p, C.c_int64, _i64p, _i32p, _i32p, _i32p, _dp, _dp, _dp, _dp], C.c_int),

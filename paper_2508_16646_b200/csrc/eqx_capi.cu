@@ -86,10 +86,20 @@ struct eqx_ctx {
   DevBuf d_ev_row, d_ev_kind, d_ev_client, d_ev_pred, d_ev_ufc, d_ev_rfc, d_ev_vtc, d_ev_wait, d_ev_id;
   int64_t ev_cap = 0;
   DevBuf d_state, d_cw;
+  DevBuf snap_ufc, snap_rfc, snap_counter, snap_running, snap_backlogged, snap_state;
+  bool snap_valid = false;
   DevState* h_state = nullptr;  // pinned
   unsigned long long last_fallbacks = 0, last_near_ties = 0;
   bool step_pending = false;
   bool stepped = false;
+  // drain plan (set by drain_prepare, consumed by drain_enqueue)
+  int64_t tile_rows = 2048;
+  int32_t n_tiles = 1;
+  int64_t hist_L = 0;
+  size_t hist_smem = 0, rank_smem = 0;
+  // cached CUDA graph of drain + step for a resident (device) queue
+  cudaGraphExec_t graph = nullptr;
+  std::vector<unsigned char> graph_key;
 };
 
 namespace {
@@ -236,9 +246,11 @@ void eqx_ctx_destroy(eqx_ctx* ctx) {
                     &ctx->d_bucket, &ctx->d_ufc_out, &ctx->d_rfc_out, &ctx->d_ev_row,
                     &ctx->d_ev_kind, &ctx->d_ev_client, &ctx->d_ev_pred, &ctx->d_ev_ufc,
                     &ctx->d_ev_rfc, &ctx->d_ev_vtc, &ctx->d_ev_wait, &ctx->d_ev_id,
-                    &ctx->d_state, &ctx->d_cw};
+                    &ctx->d_state, &ctx->d_cw, &ctx->snap_ufc, &ctx->snap_rfc,
+                    &ctx->snap_counter, &ctx->snap_running, &ctx->snap_backlogged, &ctx->snap_state};
   for (DevBuf* b : bufs) b->release();
   if (ctx->h_state) cudaFreeHost(ctx->h_state);
+  if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -443,6 +455,45 @@ eqx_status eqx_get_clients(eqx_ctx* ctx, int32_t n, double* ufc, double* rfc, do
   return EQX_OK;
 }
 
+eqx_status eqx_ledger_checkpoint(eqx_ctx* ctx) {
+  if (!ctx) return fail(ctx, EQX_ERR_ARG, "eqx_ledger_checkpoint: NULL context");
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = ctx->stream;
+  const size_t d8 = 8ull * std::max(ctx->C, 1), d4 = 4ull * std::max(ctx->C, 1);
+  CUDA_TRY(ctx, ctx->snap_ufc.ensure(d8));
+  CUDA_TRY(ctx, ctx->snap_rfc.ensure(d8));
+  CUDA_TRY(ctx, ctx->snap_counter.ensure(d8));
+  CUDA_TRY(ctx, ctx->snap_running.ensure(d4));
+  CUDA_TRY(ctx, ctx->snap_backlogged.ensure(d4));
+  CUDA_TRY(ctx, ctx->snap_state.ensure(sizeof(DevState)));
+  if (ctx->C > 0) {
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->snap_ufc.p, ctx->d_ufc.p, 8ull * ctx->C, cudaMemcpyDeviceToDevice, s));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->snap_rfc.p, ctx->d_rfc.p, 8ull * ctx->C, cudaMemcpyDeviceToDevice, s));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->snap_counter.p, ctx->d_counter.p, 8ull * ctx->C, cudaMemcpyDeviceToDevice, s));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->snap_running.p, ctx->d_running.p, 4ull * ctx->C, cudaMemcpyDeviceToDevice, s));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->snap_backlogged.p, ctx->d_backlogged.p, 4ull * ctx->C, cudaMemcpyDeviceToDevice, s));
+  }
+  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->snap_state.p, ctx->d_state.p, offsetof(DevState, n_events), cudaMemcpyDeviceToDevice, s));
+  CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  ctx->snap_valid = true;
+  return EQX_OK;
+}
+
+eqx_status eqx_ledger_restore_async(eqx_ctx* ctx) {
+  if (!ctx || !ctx->snap_valid) return fail(ctx, EQX_ERR_CONFIG, "eqx_ledger_restore_async: no checkpoint");
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = ctx->stream;
+  if (ctx->C > 0) {
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_ufc.p, ctx->snap_ufc.p, 8ull * ctx->C, cudaMemcpyDeviceToDevice, s));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_rfc.p, ctx->snap_rfc.p, 8ull * ctx->C, cudaMemcpyDeviceToDevice, s));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_counter.p, ctx->snap_counter.p, 8ull * ctx->C, cudaMemcpyDeviceToDevice, s));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_running.p, ctx->snap_running.p, 4ull * ctx->C, cudaMemcpyDeviceToDevice, s));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_backlogged.p, ctx->snap_backlogged.p, 4ull * ctx->C, cudaMemcpyDeviceToDevice, s));
+  }
+  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_state.p, ctx->snap_state.p, offsetof(DevState, n_events), cudaMemcpyDeviceToDevice, s));
+  return EQX_OK;
+}
+
 eqx_status eqx_set_batch(eqx_ctx* ctx, int32_t members, int64_t reserved) {
   if (!ctx || members < 0 || reserved < 0) return fail(ctx, EQX_ERR_ARG, "eqx_set_batch: bad arguments");
   cudaSetDevice(ctx->device);
@@ -455,7 +506,7 @@ eqx_status eqx_set_batch(eqx_ctx* ctx, int32_t members, int64_t reserved) {
   return EQX_OK;
 }
 
-eqx_status eqx_drain(eqx_ctx* ctx, const eqx_requests* r) {
+static eqx_status drain_prepare(eqx_ctx* ctx, const eqx_requests* r) {
   if (!ctx || !r) return fail(ctx, EQX_ERR_ARG, "eqx_drain: NULL argument");
   if (!ctx->model_set || !ctx->profile_set)
     return fail(ctx, EQX_ERR_CONFIG, "eqx_drain: predictor and GPU profile must be set first");
@@ -537,42 +588,53 @@ eqx_status eqx_drain(eqx_ctx* ctx, const eqx_requests* r) {
   const int32_t n_tiles = static_cast<int32_t>(std::max<int64_t>(1, (n + tile_rows - 1) / tile_rows));
   const int64_t L = static_cast<int64_t>(C) * n_tiles;
   CUDA_TRY(ctx, ctx->d_hist.ensure(4 * std::max<int64_t>(L, 1)));
-  if (C > 0) {
-    CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_count.p, 0, 4ull * C, s));
-    CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_first.p, 0x7f, 4ull * C, s));
-    CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_head.p, 0, 4ull * C, s));
-    CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_qlen_before.p, 0, 4ull * C, s));
-    const size_t hist_smem = 8ull * C;
-    const size_t rank_smem = 4ull * C + 16ull * C;
-    if (rank_smem > ctx->smem_optin || hist_smem > ctx->smem_optin)
-      return fail(ctx, EQX_ERR_CONFIG, "too many clients per device (" + std::to_string(C) + ")");
-    cudaFuncSetAttribute(drain_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(hist_smem));
-    cudaFuncSetAttribute(drain_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rank_smem));
-    DevState* st = ctx->d_state.as<DevState>();
-    if (n > 0) {
-      drain_hist_kernel<<<n_tiles, 256, hist_smem, s>>>(ctx->q_client, static_cast<int32_t>(n), C,
-                                                        static_cast<int32_t>(tile_rows), n_tiles,
-                                                        ctx->d_hist.as<uint32_t>(), ctx->d_first.as<int32_t>(),
-                                                        ctx->d_count.as<int32_t>(), st);
-      scan_kernel<<<1, 1024, 0, s>>>(ctx->d_hist.as<uint32_t>(), L, C, n_tiles, ctx->d_seg_off.as<int32_t>());
-      drain_rank_kernel<<<n_tiles, 256, rank_smem, s>>>(ctx->q_client, static_cast<int32_t>(n), C,
-                                                        static_cast<int32_t>(tile_rows), n_tiles,
-                                                        ctx->d_hist.as<uint32_t>(), ctx->d_perm.as<uint32_t>());
-    } else {
-      CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_seg_off.p, 0, 4ull * (C + 1), s));
-    }
-    lift_kernel<<<1, 1024, 0, s>>>(C, ctx->d_count.as<int32_t>(), ctx->d_first.as<int32_t>(),
-                                   ctx->d_qlen_before.as<int32_t>(), ctx->d_running.as<int32_t>(),
-                                   ctx->d_ufc.as<double>(), ctx->d_rfc.as<double>(),
-                                   ctx->d_counter.as<double>(), ctx->d_backlogged.as<int32_t>(),
-                                   ctx->counter_lift);
-    CUDA_TRY(ctx, cudaGetLastError());
-  }
+  ctx->tile_rows = tile_rows;
+  ctx->n_tiles = n_tiles;
+  ctx->hist_L = L;
+  ctx->hist_smem = 8ull * C;
+  ctx->rank_smem = 4ull * C + 16ull * C;
+  if (ctx->rank_smem > ctx->smem_optin || ctx->hist_smem > ctx->smem_optin)
+    return fail(ctx, EQX_ERR_CONFIG, "too many clients per device (" + std::to_string(C) + ")");
+  CUDA_TRY(ctx, cudaFuncSetAttribute(drain_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(std::max<size_t>(ctx->hist_smem, 1))));
+  CUDA_TRY(ctx, cudaFuncSetAttribute(drain_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(std::max<size_t>(ctx->rank_smem, 1))));
   ctx->queue_ready = true;
   return EQX_OK;
 }
 
-eqx_status eqx_step_async(eqx_ctx* ctx, double now) {
+// Pure stream work of a drain (memsets + 4 kernels); capturable into a CUDA graph.
+static eqx_status drain_enqueue(eqx_ctx* ctx) {
+  cudaStream_t s = ctx->stream;
+  const int32_t C = ctx->C;
+  const int64_t n = ctx->n;
+  if (C == 0) return EQX_OK;
+  CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_count.p, 0, 4ull * C, s));
+  CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_first.p, 0x7f, 4ull * C, s));
+  CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_head.p, 0, 4ull * C, s));
+  CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_qlen_before.p, 0, 4ull * C, s));
+  DevState* st = ctx->d_state.as<DevState>();
+  if (n > 0) {
+    drain_hist_kernel<<<ctx->n_tiles, 256, ctx->hist_smem, s>>>(
+        ctx->q_client, static_cast<int32_t>(n), C, static_cast<int32_t>(ctx->tile_rows), ctx->n_tiles,
+        ctx->d_hist.as<uint32_t>(), ctx->d_first.as<int32_t>(), ctx->d_count.as<int32_t>(), st);
+    scan_kernel<<<1, 1024, 0, s>>>(ctx->d_hist.as<uint32_t>(), ctx->hist_L, C, ctx->n_tiles,
+                                   ctx->d_seg_off.as<int32_t>());
+    drain_rank_kernel<<<ctx->n_tiles, 256, ctx->rank_smem, s>>>(
+        ctx->q_client, static_cast<int32_t>(n), C, static_cast<int32_t>(ctx->tile_rows), ctx->n_tiles,
+        ctx->d_hist.as<uint32_t>(), ctx->d_perm.as<uint32_t>());
+  } else {
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_seg_off.p, 0, 4ull * (C + 1), s));
+  }
+  lift_kernel<<<1, 1024, 0, s>>>(C, ctx->d_count.as<int32_t>(), ctx->d_first.as<int32_t>(),
+                                 ctx->d_qlen_before.as<int32_t>(), ctx->d_running.as<int32_t>(),
+                                 ctx->d_ufc.as<double>(), ctx->d_rfc.as<double>(), ctx->d_counter.as<double>(),
+                                 ctx->d_backlogged.as<int32_t>(), ctx->counter_lift);
+  CUDA_TRY(ctx, cudaGetLastError());
+  return EQX_OK;
+}
+
+static eqx_status step_prepare(eqx_ctx* ctx, double now, StepArgs& a, size_t& smem_out) {
   if (!ctx) return fail(ctx, EQX_ERR_ARG, "eqx_step_async: NULL context");
   if (!ctx->queue_ready) return fail(ctx, EQX_ERR_CONFIG, "eqx_step: no drained queue (call eqx_drain first)");
   cudaSetDevice(ctx->device);
@@ -585,7 +647,7 @@ eqx_status eqx_step_async(eqx_ctx* ctx, double now) {
     CUDA_TRY(ctx, cudaStreamSynchronize(s));
     ctx->model_dirty = false;
   }
-  StepArgs a{};
+  std::memset(&a, 0, sizeof(a));
   a.n = ctx->n;
   a.C = C;
   a.client = ctx->q_client;
@@ -642,16 +704,87 @@ eqx_status eqx_step_async(eqx_ctx* ctx, double now) {
     a.cw_global = ctx->d_cw.p;
   }
   const size_t left = ctx->smem_optin - static_smem - smem;
-  const int64_t free_slots = std::max<int64_t>(0, ctx->perf.max_batch - ctx->h_state->members);
-  int64_t W = std::min<int64_t>(free_slots + 2, C > 0 ? static_cast<int64_t>(left / (sizeof(WinEntry) * C)) : 0);
+  // Window depth: a client can be picked at most max_batch times before the slots run out
+  // (+1 for the next head's arrival); rejection streams beyond it take the global path.
+  // Sized from the static budget only, so it never depends on in-flight device state.
+  int64_t W = std::min<int64_t>(static_cast<int64_t>(ctx->perf.max_batch) + 2,
+                                C > 0 ? static_cast<int64_t>(left / (sizeof(WinEntry) * C)) : 0);
   W = std::max<int64_t>(W, 0);
   a.W = static_cast<int32_t>(W);
   smem += static_cast<size_t>(W) * C * sizeof(WinEntry);
   CUDA_TRY(ctx, cudaFuncSetAttribute(step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  smem_out = smem;
+  return EQX_OK;
+}
+
+// Pure stream work of a step (the fused kernel + summary D2H); capturable.
+static eqx_status step_enqueue(eqx_ctx* ctx, const StepArgs& a, size_t smem) {
+  cudaStream_t s = ctx->stream;
   const int grid = std::max(2, ctx->sm_count);  // CTA 0 selects, sm_count-1 CTAs stream
   step_kernel<<<grid, kStepThreads, smem, s>>>(a);
   CUDA_TRY(ctx, cudaGetLastError());
   CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_state, ctx->d_state.p, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+  return EQX_OK;
+}
+
+eqx_status eqx_drain(eqx_ctx* ctx, const eqx_requests* r) {
+  eqx_status st = drain_prepare(ctx, r);
+  if (st != EQX_OK) return st;
+  return drain_enqueue(ctx);
+}
+
+eqx_status eqx_step_async(eqx_ctx* ctx, double now) {
+  StepArgs a;
+  size_t smem = 0;
+  eqx_status st = step_prepare(ctx, now, a, smem);
+  if (st != EQX_OK) return st;
+  st = step_enqueue(ctx, a, smem);
+  if (st != EQX_OK) return st;
+  ctx->step_pending = true;
+  ctx->stepped = true;
+  return EQX_OK;
+}
+
+eqx_status eqx_drain_step_async(eqx_ctx* ctx, const eqx_requests* r, double now) {
+  eqx_status st = drain_prepare(ctx, r);
+  if (st != EQX_OK) return st;
+  StepArgs a;
+  size_t smem = 0;
+  st = step_prepare(ctx, now, a, smem);
+  if (st != EQX_OK) return st;
+  cudaStream_t s = ctx->stream;
+  if (r->location != EQX_DEVICE) {  // host columns: plain launches (H2D copies already queued)
+    st = drain_enqueue(ctx);
+    if (st == EQX_OK) st = step_enqueue(ctx, a, smem);
+  } else {
+    // Resident queue: one CUDA-graph launch replays the drain + step launch sequence.  The
+    // key covers every launch parameter (all pointers, sizes, policy, `now`, smem plan).
+    std::vector<unsigned char> key(sizeof(StepArgs) + 5 * sizeof(int64_t));
+    std::memcpy(key.data(), &a, sizeof(StepArgs));
+    const int64_t extra[5] = {ctx->tile_rows, ctx->n_tiles, static_cast<int64_t>(smem), ctx->counter_lift,
+                              static_cast<int64_t>(ctx->hist_smem)};
+    std::memcpy(key.data() + sizeof(StepArgs), extra, sizeof(extra));
+    if (!ctx->graph || key != ctx->graph_key) {
+      if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
+      ctx->graph = nullptr;
+      cudaGraph_t g = nullptr;
+      CUDA_TRY(ctx, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+      st = drain_enqueue(ctx);
+      if (st == EQX_OK) st = step_enqueue(ctx, a, smem);
+      cudaError_t ce = cudaStreamEndCapture(s, &g);
+      if (st != EQX_OK) {
+        if (g) cudaGraphDestroy(g);
+        return st;
+      }
+      CUDA_TRY(ctx, ce);
+      cudaError_t ie = cudaGraphInstantiate(&ctx->graph, g, 0);
+      cudaGraphDestroy(g);
+      CUDA_TRY(ctx, ie);
+      ctx->graph_key = key;
+    }
+    CUDA_TRY(ctx, cudaGraphLaunch(ctx->graph, s));
+  }
+  if (st != EQX_OK) return st;
   ctx->step_pending = true;
   ctx->stepped = true;
   return EQX_OK;

@@ -379,20 +379,26 @@ struct SelShared {
   int64_t reserved;
 };
 
-__device__ WinEntry fetch_entry(const StepArgs& a, const ModelTables& M, int32_t c, int32_t j) {
-  const int32_t row = static_cast<int32_t>(a.perm[a.seg_off[c] + j]);
+__device__ __forceinline__ WinEntry entry_of_row(const StepArgs& a, const ModelTables& M, int32_t c,
+                                                 int32_t row) {
   const int64_t id = a.id ? a.id[row] : a.id_base + row;
-  const Scored s = score_request(M, a.pol, a.now, a.in_tok[row], a.tag[row],
-                                 a.true_out ? a.true_out[row] : 1, id, a.arrival[row], a.weight[c]);
+  const double arr = a.arrival[row];
+  const int32_t in = a.in_tok[row];
+  const Scored s = score_request(M, a.pol, a.now, in, a.tag[row], a.true_out ? a.true_out[row] : 1, id, arr,
+                                 a.weight[c]);
   WinEntry e;
   e.ufc_inc = s.ufc_inc;
   e.rfc_inc = s.rfc_inc;
-  e.arrival = a.arrival[row];
-  e.in = a.in_tok[row];
+  e.arrival = arr;
+  e.in = in;
   e.pred = s.pred;
   e.row = row;
   e.pad = 0;
   return e;
+}
+
+__device__ WinEntry fetch_entry(const StepArgs& a, const ModelTables& M, int32_t c, int32_t j) {
+  return entry_of_row(a, M, c, static_cast<int32_t>(a.perm[a.seg_off[c] + j]));
 }
 
 __device__ __forceinline__ WinEntry get_entry(const StepArgs& a, const ModelTables& M,
@@ -586,7 +592,7 @@ __device__ void selection(const StepArgs& a, const ModelTables& M, unsigned char
   const int32_t C = a.C;
   const int tid = threadIdx.x;
   const int nthr = a.sel_threads;  // multiple of 32, <= blockDim.x
-  if (tid >= nthr) return;         // spare warps of CTA 0 leave; barriers are named with nthr
+  const int NT = blockDim.x;
   __shared__ SelShared S;
   // ---- carve per-client work arrays + windows ----
   ClientWork cw;
@@ -596,44 +602,30 @@ __device__ void selection(const StepArgs& a, const ModelTables& M, unsigned char
     p += (bytes + 15) & ~size_t(15);
     return q;
   };
-  if (a.cw_global) {
-    unsigned char* g = reinterpret_cast<unsigned char*>(a.cw_global);
-    auto gcarve = [&](size_t bytes) {
-      unsigned char* q = g;
-      g += (bytes + 15) & ~size_t(15);
-      return q;
-    };
-    cw.key = reinterpret_cast<double*>(gcarve(8ull * C));
-    cw.arr = reinterpret_cast<double*>(gcarve(8ull * C));
-    cw.ufc = reinterpret_cast<double*>(gcarve(8ull * C));
-    cw.rfc = reinterpret_cast<double*>(gcarve(8ull * C));
-    cw.cnt = reinterpret_cast<double*>(gcarve(8ull * C));
-    cw.w = reinterpret_cast<double*>(gcarve(8ull * C));
-    cw.pos = reinterpret_cast<int32_t*>(gcarve(4ull * C));
-    cw.end = reinterpret_cast<int32_t*>(gcarve(4ull * C));
-    cw.pos0 = reinterpret_cast<int32_t*>(gcarve(4ull * C));
-    cw.order = reinterpret_cast<uint32_t*>(gcarve(4ull * C));
-    cw.flags = reinterpret_cast<int32_t*>(gcarve(4ull * C));
-    cw.adm = reinterpret_cast<int32_t*>(gcarve(4ull * C));
-  } else {
-    cw.key = reinterpret_cast<double*>(carve(8ull * C));
-    cw.arr = reinterpret_cast<double*>(carve(8ull * C));
-    cw.ufc = reinterpret_cast<double*>(carve(8ull * C));
-    cw.rfc = reinterpret_cast<double*>(carve(8ull * C));
-    cw.cnt = reinterpret_cast<double*>(carve(8ull * C));
-    cw.w = reinterpret_cast<double*>(carve(8ull * C));
-    cw.pos = reinterpret_cast<int32_t*>(carve(4ull * C));
-    cw.end = reinterpret_cast<int32_t*>(carve(4ull * C));
-    cw.pos0 = reinterpret_cast<int32_t*>(carve(4ull * C));
-    cw.order = reinterpret_cast<uint32_t*>(carve(4ull * C));
-    cw.flags = reinterpret_cast<int32_t*>(carve(4ull * C));
-    cw.adm = reinterpret_cast<int32_t*>(carve(4ull * C));
-  }
+  unsigned char* g = reinterpret_cast<unsigned char*>(a.cw_global);
+  auto take = [&](size_t bytes) {
+    if (!a.cw_global) return carve(bytes);
+    unsigned char* q = g;
+    g += (bytes + 15) & ~size_t(15);
+    return q;
+  };
+  cw.key = reinterpret_cast<double*>(take(8ull * C));
+  cw.arr = reinterpret_cast<double*>(take(8ull * C));
+  cw.ufc = reinterpret_cast<double*>(take(8ull * C));
+  cw.rfc = reinterpret_cast<double*>(take(8ull * C));
+  cw.cnt = reinterpret_cast<double*>(take(8ull * C));
+  cw.w = reinterpret_cast<double*>(take(8ull * C));
+  cw.pos = reinterpret_cast<int32_t*>(take(4ull * C));
+  cw.end = reinterpret_cast<int32_t*>(take(4ull * C));
+  cw.pos0 = reinterpret_cast<int32_t*>(take(4ull * C));
+  cw.order = reinterpret_cast<uint32_t*>(take(4ull * C));
+  cw.flags = reinterpret_cast<int32_t*>(take(4ull * C));
+  cw.adm = reinterpret_cast<int32_t*>(take(4ull * C));
   WinEntry* win = reinterpret_cast<WinEntry*>(carve(0));
   const Policy& P = a.pol;
 
-  // ---- load the ledger; fill each client's head window (first W queued entries) ----
-  for (int32_t c = tid; c < C; c += nthr) {
+  // ---- whole CTA: load the ledger, fill each client's head window (first W entries) ----
+  for (int32_t c = tid; c < C; c += NT) {
     cw.ufc[c] = a.ufc[c];
     cw.rfc[c] = a.rfc[c];
     cw.cnt[c] = a.counter[c];
@@ -645,14 +637,29 @@ __device__ void selection(const StepArgs& a, const ModelTables& M, unsigned char
     cw.flags[c] = a.backlogged[c] ? kBacklogged : 0;
     cw.adm[c] = 0;
   }
-  named_sync(1, nthr);
+  __syncthreads();
   const int64_t items = static_cast<int64_t>(C) * a.W;
-  for (int64_t it = tid; it < items; it += nthr) {
-    const int32_t c = static_cast<int32_t>(it / a.W);
-    const int32_t k = static_cast<int32_t>(it % a.W);
-    if (cw.pos0[c] + k < cw.end[c]) win[it] = fetch_entry(a, M, c, cw.pos0[c] + k);
+  constexpr int kU = 4;  // 4 independent gathers in flight per thread
+  for (int64_t base = tid; base < items; base += kU * NT) {
+    int32_t rows[kU], cs[kU];
+#pragma unroll
+    for (int k = 0; k < kU; ++k) {
+      const int64_t it = base + static_cast<int64_t>(k) * NT;
+      rows[k] = -1;
+      cs[k] = 0;
+      if (it < items) {
+        const int32_t c = static_cast<int32_t>(it / a.W);
+        const int32_t j = cw.pos0[c] + static_cast<int32_t>(it % a.W);
+        cs[k] = c;
+        if (j < cw.end[c]) rows[k] = static_cast<int32_t>(a.perm[a.seg_off[c] + j]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kU; ++k)
+      if (rows[k] >= 0) win[base + static_cast<int64_t>(k) * NT] = entry_of_row(a, M, cs[k], rows[k]);
   }
-  named_sync(1, nthr);
+  __syncthreads();
+  if (tid >= nthr) return;  // spare warps leave; the loop's barriers are named with nthr
   for (int32_t c = tid; c < C; c += nthr)
     cw.arr[c] = cw.pos[c] < cw.end[c] ? get_entry(a, M, win, cw, c, cw.pos[c]).arrival : 0.0;
   if (tid == 0) {
@@ -691,7 +698,6 @@ __device__ void selection(const StepArgs& a, const ModelTables& M, unsigned char
     } else {
       const int32_t cc = S.changed;
       if (cc >= 0 && (cc % nthr) == tid) local = rescan_owned(cw, C, tid, nthr);
-      if (nw > 1) named_sync(1, nthr);  // S.flags/S.changed are rewritten next round
     }
   }
   // ---- write back ledger, heads, batch, summary ----

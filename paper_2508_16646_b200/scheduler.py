@@ -388,11 +388,28 @@ class GpuScheduler:
     def set_batch(self, members: int, reserved_kv_tokens: int) -> None:
         self._check(self._lib.eqx_set_batch(self._ctx, int(members), int(reserved_kv_tokens)))
 
+    def checkpoint(self) -> None:
+        """Device-side snapshot of ledger + batch state (restore() replays from it async)."""
+        self._check(self._lib.eqx_ledger_checkpoint(self._ctx))
+
+    def restore_async(self) -> None:
+        self._check(self._lib.eqx_ledger_restore_async(self._ctx))
+
     # -- the hot path --
     def drain(self, client, arrival_s, input_tokens, tag=None, true_output_tokens=None, ids=None,
               id_base: int = 0) -> None:
         """Queue a batch of arrivals (arrival order).  numpy columns are copied host->device;
         torch CUDA tensors are used in place."""
+        rq = self._requests(client, arrival_s, input_tokens, tag, true_output_tokens, ids, id_base)
+        self._check(self._lib.eqx_drain(self._ctx, C.byref(rq)))
+
+    def drain_step_async(self, now: float, client, arrival_s, input_tokens, tag=None,
+                         true_output_tokens=None, ids=None, id_base: int = 0) -> None:
+        """drain + step_async in one call (CUDA-graph replay for a resident device queue)."""
+        rq = self._requests(client, arrival_s, input_tokens, tag, true_output_tokens, ids, id_base)
+        self._check(self._lib.eqx_drain_step_async(self._ctx, C.byref(rq), float(now)))
+
+    def _requests(self, client, arrival_s, input_tokens, tag, true_output_tokens, ids, id_base):
         keep: list = []
         cols = {}
         loc = set()
@@ -408,9 +425,9 @@ class GpuScheduler:
         n = len(client)
         rq = L.Requests(n, cols["id"], id_base, cols["client"], cols["arrival_s"], cols["input_tokens"],
                         cols["true_output_tokens"], cols["tag"], loc.pop() if loc else L.EQX_HOST)
-        self._check(self._lib.eqx_drain(self._ctx, C.byref(rq)))
         self._keep = keep  # device columns are used in place: keep them alive with the queue
         self.n_queued = n
+        return rq
 
     def step_async(self, now: float) -> None:
         self._check(self._lib.eqx_step_async(self._ctx, float(now)))
