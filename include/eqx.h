@@ -193,6 +193,11 @@ eqx_status eqx_copy_events(eqx_ctx* ctx, int64_t cap, int64_t* id, int32_t* kind
 eqx_status eqx_copy_scores(eqx_ctx* ctx, int64_t cap, int32_t* pred, uint8_t* bucket,
                            double* ufc_inc, double* rfc_inc);
 
+/* Profiling: phase timestamps of the last step in microseconds relative to the selection
+ * CTA's start: [0] 0, [1] head windows filled, [2] selection loop start, [3] loop end,
+ * [4] first scoring CTA start, [5] last scoring CTA end. */
+eqx_status eqx_phase_times(eqx_ctx* ctx, double* out_us, int32_t n);
+
 /* ---- host scalar utilities (bindings/module.cpp:144-172 `ufc_increment`/`rfc_increment`) - */
 double eqx_ufc_increment(double weight, int32_t input_tokens, int32_t predicted_output_tokens,
                          double wait_s, double predicted_latency_ms, double delta,

@@ -97,6 +97,10 @@ struct eqx_ctx {
   int32_t n_tiles = 1;
   int64_t hist_L = 0;
   size_t hist_smem = 0, rank_smem = 0;
+  bool staged = true;
+  cudaStream_t stream2 = nullptr;  // side stream for whole-queue scoring
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  DevBuf d_done;                   // last-CTA counters of the drain kernels
   // cached CUDA graph of drain + step for a resident (device) queue
   cudaGraphExec_t graph = nullptr;
   std::vector<unsigned char> graph_key;
@@ -213,6 +217,11 @@ eqx_status eqx_ctx_create(int32_t device, eqx_ctx** out) {
   ctx->sm_count = prop.multiProcessorCount;
   ctx->smem_optin = prop.sharedMemPerBlockOptin;
   e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = ctx->d_done.ensure(64);
+  if (e == cudaSuccess) e = cudaMemset(ctx->d_done.p, 0, 64);
   if (e == cudaSuccess) e = ctx->d_state.ensure(sizeof(DevState));
   if (e == cudaSuccess) e = cudaMemset(ctx->d_state.p, 0, sizeof(DevState));
   if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_state, sizeof(DevState));
@@ -250,6 +259,11 @@ void eqx_ctx_destroy(eqx_ctx* ctx) {
                     &ctx->snap_counter, &ctx->snap_running, &ctx->snap_backlogged, &ctx->snap_state};
   for (DevBuf* b : bufs) b->release();
   if (ctx->h_state) cudaFreeHost(ctx->h_state);
+  if (ctx->stream2) cudaStreamSynchronize(ctx->stream2);
+  ctx->d_done.release();
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+  if (ctx->stream2) cudaStreamDestroy(ctx->stream2);
   if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -581,9 +595,13 @@ static eqx_status drain_prepare(eqx_ctx* ctx, const eqx_requests* r) {
   CUDA_TRY(ctx, ctx->d_ev_wait.ensure(8 * nn));
   CUDA_TRY(ctx, ctx->d_ev_id.ensure(8 * nn));
   CUDA_TRY(ctx, ctx->d_perm.ensure(4 * nn));
-  // tiling: 8 warps x (tile_rows/8) rows per tile, histogram kept <= ~1M entries
-  int64_t tile_rows = 2048;
-  while (static_cast<int64_t>(C) * ((n + tile_rows - 1) / tile_rows) > (int64_t(1) << 20)) tile_rows *= 2;
+  // tiling: 8 warps x (tile_rows/8) rows per tile.  Rosters up to kStageMaxClients use the
+  // smem-staged coalesced scatter with 2048-row tiles; larger rosters grow the tile so the
+  // [client][tile] histogram stays <= ~1M entries.
+  const bool staged = C <= kStageMaxClients;
+  int64_t tile_rows = kTileRows;
+  if (!staged)
+    while (static_cast<int64_t>(C) * ((n + tile_rows - 1) / tile_rows) > (int64_t(1) << 20)) tile_rows *= 2;
   if (tile_rows / 8 > 65535) return fail(ctx, EQX_ERR_CONFIG, "too many clients for the drain tiling");
   const int32_t n_tiles = static_cast<int32_t>(std::max<int64_t>(1, (n + tile_rows - 1) / tile_rows));
   const int64_t L = static_cast<int64_t>(C) * n_tiles;
@@ -591,65 +609,130 @@ static eqx_status drain_prepare(eqx_ctx* ctx, const eqx_requests* r) {
   ctx->tile_rows = tile_rows;
   ctx->n_tiles = n_tiles;
   ctx->hist_L = L;
-  ctx->hist_smem = 8ull * C;
-  ctx->rank_smem = 4ull * C + 16ull * C;
+  ctx->staged = staged;
+  ctx->hist_smem = std::max<size_t>(4ull * C, 16);
+  ctx->rank_smem = 24ull * C + (staged ? 6ull * tile_rows : 0) + 16;
   if (ctx->rank_smem > ctx->smem_optin || ctx->hist_smem > ctx->smem_optin)
     return fail(ctx, EQX_ERR_CONFIG, "too many clients per device (" + std::to_string(C) + ")");
   CUDA_TRY(ctx, cudaFuncSetAttribute(drain_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(std::max<size_t>(ctx->hist_smem, 1))));
+                                     static_cast<int>(ctx->hist_smem)));
   CUDA_TRY(ctx, cudaFuncSetAttribute(drain_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(std::max<size_t>(ctx->rank_smem, 1))));
+                                     static_cast<int>(ctx->rank_smem)));
   ctx->queue_ready = true;
   return EQX_OK;
 }
 
-// Pure stream work of a drain (memsets + 4 kernels); capturable into a CUDA graph.
+static DrainArgs drain_args(eqx_ctx* ctx) {
+  DrainArgs d;
+  std::memset(&d, 0, sizeof(d));
+  d.client = ctx->q_client;
+  d.n = static_cast<int32_t>(ctx->n);
+  d.C = ctx->C;
+  d.tile_rows = static_cast<int32_t>(ctx->tile_rows);
+  d.n_tiles = ctx->n_tiles;
+  d.staged = ctx->staged ? 1 : 0;
+  d.hist = ctx->d_hist.as<uint32_t>();
+  d.hist_L = ctx->hist_L;
+  d.seg_off = ctx->d_seg_off.as<int32_t>();
+  d.perm = ctx->d_perm.as<uint32_t>();
+  d.count = ctx->d_count.as<int32_t>();
+  d.first_row = ctx->d_first.as<int32_t>();
+  d.qlen_before = ctx->d_qlen_before.as<int32_t>();
+  d.running = ctx->d_running.as<int32_t>();
+  d.ufc = ctx->d_ufc.as<double>();
+  d.rfc = ctx->d_rfc.as<double>();
+  d.counter = ctx->d_counter.as<double>();
+  d.backlogged = ctx->d_backlogged.as<int32_t>();
+  d.counter_lift = ctx->counter_lift;
+  d.done = ctx->d_done.as<unsigned int>();
+  d.st = ctx->d_state.as<DevState>();
+  return d;
+}
+
+// Pure stream work of a drain (2 memsets + 2 kernels); capturable into a CUDA graph.
 static eqx_status drain_enqueue(eqx_ctx* ctx) {
   cudaStream_t s = ctx->stream;
   const int32_t C = ctx->C;
-  const int64_t n = ctx->n;
   if (C == 0) return EQX_OK;
-  CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_count.p, 0, 4ull * C, s));
-  CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_first.p, 0x7f, 4ull * C, s));
   CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_head.p, 0, 4ull * C, s));
   CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_qlen_before.p, 0, 4ull * C, s));
-  DevState* st = ctx->d_state.as<DevState>();
-  if (n > 0) {
-    drain_hist_kernel<<<ctx->n_tiles, 256, ctx->hist_smem, s>>>(
-        ctx->q_client, static_cast<int32_t>(n), C, static_cast<int32_t>(ctx->tile_rows), ctx->n_tiles,
-        ctx->d_hist.as<uint32_t>(), ctx->d_first.as<int32_t>(), ctx->d_count.as<int32_t>(), st);
-    scan_kernel<<<1, 1024, 0, s>>>(ctx->d_hist.as<uint32_t>(), ctx->hist_L, C, ctx->n_tiles,
-                                   ctx->d_seg_off.as<int32_t>());
-    drain_rank_kernel<<<ctx->n_tiles, 256, ctx->rank_smem, s>>>(
-        ctx->q_client, static_cast<int32_t>(n), C, static_cast<int32_t>(ctx->tile_rows), ctx->n_tiles,
-        ctx->d_hist.as<uint32_t>(), ctx->d_perm.as<uint32_t>());
-  } else {
-    CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_seg_off.p, 0, 4ull * (C + 1), s));
-  }
-  lift_kernel<<<1, 1024, 0, s>>>(C, ctx->d_count.as<int32_t>(), ctx->d_first.as<int32_t>(),
-                                 ctx->d_qlen_before.as<int32_t>(), ctx->d_running.as<int32_t>(),
-                                 ctx->d_ufc.as<double>(), ctx->d_rfc.as<double>(), ctx->d_counter.as<double>(),
-                                 ctx->d_backlogged.as<int32_t>(), ctx->counter_lift);
+  const DrainArgs d = drain_args(ctx);
+  drain_hist_kernel<<<ctx->n_tiles, kDrainThreads, ctx->hist_smem, s>>>(d);
+  drain_rank_kernel<<<ctx->n_tiles, kDrainThreads, ctx->rank_smem, s>>>(d);
   CUDA_TRY(ctx, cudaGetLastError());
   return EQX_OK;
 }
 
-static eqx_status step_prepare(eqx_ctx* ctx, double now, StepArgs& a, size_t& smem_out) {
+// Largest T with double(T) * m <= M (the can_fit KV test, gpu_model.cpp:64-66).  double(T)
+// and the IEEE product are monotone in T, so the test is exactly T <= tmax for integer T.
+static int64_t kv_threshold(double m, double M) {
+  auto ok = [&](int64_t t) { return static_cast<double>(t) * m <= M; };
+  const int64_t cap = int64_t(1) << 61;
+  if (ok(cap)) return cap;
+  int64_t lo = 0, hi = 1;  // ok(lo) holds (0 * m = 0 <= M for M > 0)
+  while (ok(hi)) {
+    lo = hi;
+    hi *= 2;
+  }
+  while (hi - lo > 1) {
+    const int64_t mid = lo + (hi - lo) / 2;
+    if (ok(mid)) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+struct StepPlan {
+  ScoreArgs sc;
+  SelectArgs se;
+  size_t score_smem, select_smem;
+  int score_grid, select_threads;
+};
+
+static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl) {
   if (!ctx) return fail(ctx, EQX_ERR_ARG, "eqx_step_async: NULL context");
   if (!ctx->queue_ready) return fail(ctx, EQX_ERR_CONFIG, "eqx_step: no drained queue (call eqx_drain first)");
   cudaSetDevice(ctx->device);
   cudaStream_t s = ctx->stream;
   const int32_t C = ctx->C;
-  // compiled model tables -> device, only after they changed
   const size_t model_bytes = offsetof(ModelTables, lut) + 4ull * ctx->lut_entries;
-  if (ctx->model_dirty) {
+  if (ctx->model_dirty) {  // compiled model tables -> device, only after they changed
     CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_model.p, &ctx->model, model_bytes, cudaMemcpyHostToDevice, s));
     CUDA_TRY(ctx, cudaStreamSynchronize(s));
     ctx->model_dirty = false;
   }
-  std::memset(&a, 0, sizeof(a));
-  a.n = ctx->n;
-  a.C = C;
+  const int32_t model_words = static_cast<int32_t>((model_bytes + 3) / 4);
+  const size_t model_smem = (static_cast<size_t>(model_words) * 4 + 15) & ~size_t(15);
+  std::memset(&pl, 0, sizeof(pl));
+  // ---- whole-queue scoring ----
+  ScoreArgs& sc = pl.sc;
+  sc.n = ctx->n;
+  sc.client = ctx->q_client;
+  sc.arrival = ctx->q_arrival;
+  sc.in_tok = ctx->q_in;
+  sc.true_out = ctx->q_true;
+  sc.tag = ctx->q_tag;
+  sc.id = ctx->q_id;
+  sc.id_base = ctx->id_base;
+  sc.weight = ctx->d_weight.as<double>();
+  sc.pred_out = ctx->d_pred.as<int32_t>();
+  sc.bucket_out = ctx->d_bucket.as<uint8_t>();
+  sc.ufc_out = ctx->d_ufc_out.as<double>();
+  sc.rfc_out = ctx->d_rfc_out.as<double>();
+  sc.st = ctx->d_state.as<DevState>();
+  sc.model = ctx->d_model.as<ModelTables>();
+  sc.model_words = model_words;
+  sc.vec_ok = aligned16(sc.client) && aligned16(sc.arrival) && aligned16(sc.in_tok) &&
+              (reinterpret_cast<uintptr_t>(sc.tag) % 8 == 0) && (!sc.true_out || aligned16(sc.true_out));
+  sc.pol = ctx->pol;
+  sc.now = now;
+  pl.score_smem = model_smem;
+  int per_sm = 1;
+  CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, score_kernel, kScoreThreads, pl.score_smem));
+  const int64_t want = (ctx->n / 8 + kScoreThreads - 1) / kScoreThreads;
+  pl.score_grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, static_cast<int64_t>(ctx->sm_count) * std::max(per_sm, 1))));
+  // ---- selection ----
+  SelectArgs& a = pl.se;
   a.client = ctx->q_client;
   a.arrival = ctx->q_arrival;
   a.in_tok = ctx->q_in;
@@ -661,6 +744,7 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepArgs& a, size_t& sm
   a.seg_off = ctx->d_seg_off.as<int32_t>();
   a.count = ctx->d_count.as<int32_t>();
   a.head = ctx->d_head.as<int32_t>();
+  a.C = C;
   a.ufc = ctx->d_ufc.as<double>();
   a.rfc = ctx->d_rfc.as<double>();
   a.counter = ctx->d_counter.as<double>();
@@ -668,10 +752,6 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepArgs& a, size_t& sm
   a.order = ctx->d_order.as<uint32_t>();
   a.running = ctx->d_running.as<int32_t>();
   a.backlogged = ctx->d_backlogged.as<int32_t>();
-  a.pred_out = ctx->d_pred.as<int32_t>();
-  a.bucket_out = ctx->d_bucket.as<uint8_t>();
-  a.ufc_out = ctx->d_ufc_out.as<double>();
-  a.rfc_out = ctx->d_rfc_out.as<double>();
   a.ev_row = ctx->d_ev_row.as<int32_t>();
   a.ev_kind = ctx->d_ev_kind.as<int32_t>();
   a.ev_client = ctx->d_ev_client.as<int32_t>();
@@ -683,46 +763,61 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepArgs& a, size_t& sm
   a.ev_cap = ctx->ev_cap;
   a.st = ctx->d_state.as<DevState>();
   a.model = ctx->d_model.as<ModelTables>();
-  a.model_lut_entries = ctx->lut_entries;
-  a.model_smem_bytes = static_cast<int32_t>((model_bytes + 15) & ~size_t(15));
+  a.model_words = model_words;
+  a.tmax = kv_threshold(ctx->perf.mem_per_token_bytes, ctx->perf.mem_capacity_bytes);
   a.pol = ctx->pol;
   a.now = now;
-  a.sel_threads = std::min(kStepThreads, std::max(32, (C + 31) / 32 * 32));
-  a.vec_ok = aligned16(a.client) && aligned16(a.arrival) && aligned16(a.in_tok) &&
-             (reinterpret_cast<uintptr_t>(a.tag) % 4 == 0) &&
-             (!a.true_out || aligned16(a.true_out));
-  // shared memory plan: model | per-client work (if it fits) | head windows
-  const size_t static_smem = 2048;  // SelShared + slack
-  const size_t budget = ctx->smem_optin - static_smem - a.model_smem_bytes;
-  const size_t cw_bytes = 12ull * 16 + static_cast<size_t>(C) * (6 * 8 + 6 * 4);
-  size_t smem = a.model_smem_bytes;
+  // selection warps: ~64 clients per warp, at most 16 warps; a single warp needs no barrier
+  const int G = std::max(1, std::min(kSelectMaxThreads / 32, (C + 63) / 64));
+  a.sel_threads = 32 * G;
+  pl.select_threads = kSelectMaxThreads;
+  // shared memory: model | per-client work (if it fits) | head windows
+  const size_t static_smem = 4096;
+  const size_t cw_bytes = 13ull * 16 + static_cast<size_t>(C) * (6 * 8 + 7 * 4);
+  size_t smem = model_smem;
+  const size_t budget = ctx->smem_optin - static_smem - model_smem;
   if (cw_bytes <= budget / 2) {
+    a.cw_in_smem = 1;
     a.cw_global = nullptr;
     smem += cw_bytes;
   } else {
     CUDA_TRY(ctx, ctx->d_cw.ensure(cw_bytes));
+    a.cw_in_smem = 0;
     a.cw_global = ctx->d_cw.p;
   }
   const size_t left = ctx->smem_optin - static_smem - smem;
-  // Window depth: a client can be picked at most max_batch times before the slots run out
-  // (+1 for the next head's arrival); rejection streams beyond it take the global path.
-  // Sized from the static budget only, so it never depends on in-flight device state.
+  // A client is picked at most max_batch times before the slots run out (+1 for the next
+  // head's arrival); deeper heads (rejection streams) are scored on demand from HBM.
   int64_t W = std::min<int64_t>(static_cast<int64_t>(ctx->perf.max_batch) + 2,
                                 C > 0 ? static_cast<int64_t>(left / (sizeof(WinEntry) * C)) : 0);
-  W = std::max<int64_t>(W, 0);
-  a.W = static_cast<int32_t>(W);
-  smem += static_cast<size_t>(W) * C * sizeof(WinEntry);
-  CUDA_TRY(ctx, cudaFuncSetAttribute(step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  smem_out = smem;
+  a.W = static_cast<int32_t>(std::max<int64_t>(W, 0));
+  smem += static_cast<size_t>(a.W) * C * sizeof(WinEntry);
+  pl.select_smem = smem;
+  CUDA_TRY(ctx, cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   return EQX_OK;
 }
 
-// Pure stream work of a step (the fused kernel + summary D2H); capturable.
-static eqx_status step_enqueue(eqx_ctx* ctx, const StepArgs& a, size_t smem) {
-  cudaStream_t s = ctx->stream;
-  const int grid = std::max(2, ctx->sm_count);  // CTA 0 selects, sm_count-1 CTAs stream
-  step_kernel<<<grid, kStepThreads, smem, s>>>(a);
+// Stream work of a step.  Scoring (HBM-bound, whole queue) runs on the side stream
+// concurrently with [optional drain ->] selection on the main stream; both join before the
+// summary D2H.  Capturable into a CUDA graph (fork/join through events).
+static eqx_status step_enqueue(eqx_ctx* ctx, const StepPlan& pl, bool with_drain) {
+  cudaStream_t s = ctx->stream, s2 = ctx->stream2;
+  char* st = reinterpret_cast<char*>(ctx->d_state.p);
+  CUDA_TRY(ctx, cudaMemsetAsync(st + offsetof(DevState, t) + 4 * 8, 0xff, 8, s));
+  CUDA_TRY(ctx, cudaMemsetAsync(st + offsetof(DevState, t) + 5 * 8, 0, 8, s));
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fork, s));
+  CUDA_TRY(ctx, cudaStreamWaitEvent(s2, ctx->ev_fork, 0));
+  if (ctx->n > 0)
+    score_kernel<<<pl.score_grid, kScoreThreads, pl.score_smem, s2>>>(pl.sc);
   CUDA_TRY(ctx, cudaGetLastError());
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev_join, s2));
+  if (with_drain) {
+    eqx_status e = drain_enqueue(ctx);
+    if (e != EQX_OK) return e;
+  }
+  select_kernel<<<1, pl.select_threads, pl.select_smem, s>>>(pl.se);
+  CUDA_TRY(ctx, cudaGetLastError());
+  CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_join, 0));
   CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_state, ctx->d_state.p, sizeof(DevState), cudaMemcpyDeviceToHost, s));
   return EQX_OK;
 }
@@ -734,11 +829,10 @@ eqx_status eqx_drain(eqx_ctx* ctx, const eqx_requests* r) {
 }
 
 eqx_status eqx_step_async(eqx_ctx* ctx, double now) {
-  StepArgs a;
-  size_t smem = 0;
-  eqx_status st = step_prepare(ctx, now, a, smem);
+  StepPlan pl;
+  eqx_status st = step_prepare(ctx, now, pl);
   if (st != EQX_OK) return st;
-  st = step_enqueue(ctx, a, smem);
+  st = step_enqueue(ctx, pl, false);
   if (st != EQX_OK) return st;
   ctx->step_pending = true;
   ctx->stepped = true;
@@ -748,29 +842,26 @@ eqx_status eqx_step_async(eqx_ctx* ctx, double now) {
 eqx_status eqx_drain_step_async(eqx_ctx* ctx, const eqx_requests* r, double now) {
   eqx_status st = drain_prepare(ctx, r);
   if (st != EQX_OK) return st;
-  StepArgs a;
-  size_t smem = 0;
-  st = step_prepare(ctx, now, a, smem);
+  StepPlan pl;
+  st = step_prepare(ctx, now, pl);
   if (st != EQX_OK) return st;
   cudaStream_t s = ctx->stream;
   if (r->location != EQX_DEVICE) {  // host columns: plain launches (H2D copies already queued)
-    st = drain_enqueue(ctx);
-    if (st == EQX_OK) st = step_enqueue(ctx, a, smem);
+    st = step_enqueue(ctx, pl, true);
   } else {
-    // Resident queue: one CUDA-graph launch replays the drain + step launch sequence.  The
-    // key covers every launch parameter (all pointers, sizes, policy, `now`, smem plan).
-    std::vector<unsigned char> key(sizeof(StepArgs) + 5 * sizeof(int64_t));
-    std::memcpy(key.data(), &a, sizeof(StepArgs));
-    const int64_t extra[5] = {ctx->tile_rows, ctx->n_tiles, static_cast<int64_t>(smem), ctx->counter_lift,
-                              static_cast<int64_t>(ctx->hist_smem)};
-    std::memcpy(key.data() + sizeof(StepArgs), extra, sizeof(extra));
+    // Resident queue: one CUDA-graph launch replays drain + scoring + selection.  The key
+    // covers every launch parameter (pointers, sizes, policy, `now`, smem/tiling plan).
+    std::vector<unsigned char> key(sizeof(StepPlan) + 6 * sizeof(int64_t));
+    std::memcpy(key.data(), &pl, sizeof(StepPlan));
+    const int64_t extra[6] = {ctx->tile_rows, ctx->n_tiles, ctx->counter_lift, static_cast<int64_t>(ctx->hist_smem),
+                              static_cast<int64_t>(ctx->rank_smem), ctx->staged};
+    std::memcpy(key.data() + sizeof(StepPlan), extra, sizeof(extra));
     if (!ctx->graph || key != ctx->graph_key) {
       if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
       ctx->graph = nullptr;
       cudaGraph_t g = nullptr;
       CUDA_TRY(ctx, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-      st = drain_enqueue(ctx);
-      if (st == EQX_OK) st = step_enqueue(ctx, a, smem);
+      st = step_enqueue(ctx, pl, true);
       cudaError_t ce = cudaStreamEndCapture(s, &g);
       if (st != EQX_OK) {
         if (g) cudaGraphDestroy(g);
@@ -810,6 +901,17 @@ eqx_status eqx_step_collect(eqx_ctx* ctx, eqx_step_summary* out) {
   ctx->last_fallbacks = h.fallbacks;
   ctx->last_near_ties = h.near_ties;
   ctx->step_pending = false;
+  return EQX_OK;
+}
+
+eqx_status eqx_phase_times(eqx_ctx* ctx, double* out_us, int32_t n) {
+  if (!ctx || !out_us) return fail(ctx, EQX_ERR_ARG, "eqx_phase_times: NULL argument");
+  cudaSetDevice(ctx->device);
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  const unsigned long long* t = ctx->h_state->t;
+  const double base = static_cast<double>(t[0]);
+  for (int i = 0; i < n && i < 6; ++i) out_us[i] = (static_cast<double>(t[i]) - base) * 1e-3;
+  for (int i = 6; i < n && i < 8; ++i) out_us[i] = static_cast<double>(t[i]);  // cycles
   return EQX_OK;
 }
 

@@ -49,17 +49,6 @@ struct Policy {
   double m, M;             // mem_per_token_bytes, mem_capacity_bytes
 };
 
-// One head-of-queue entry as the selection loop consumes it (40 B).
-struct WinEntry {
-  double ufc_inc;
-  double rfc_inc;
-  double arrival;
-  int32_t in;
-  int32_t pred;
-  int32_t row;
-  int32_t pad;
-};
-
 // Device-resident scalars of one context.
 struct DevState {
   int32_t members;        // BatchState::members.size()
@@ -70,7 +59,29 @@ struct DevState {
   unsigned long long near_ties;   // noisy predictor near-.5 flags
   int32_t bad_client;     // drain saw a client index out of range
   int32_t pad1;
+  // phase timestamps (%globaltimer ns) of the last step, for profiling:
+  // [0] selection start [1] windows filled [2] loop start [3] loop end
+  // [4] first worker start (min) [5] last worker end (max)
+  unsigned long long t[8];
 };
+
+// Order-preserving map double -> uint64 (IEEE total order on non-NaN values, with -0.0 and
+// +0.0 made equal as operator< / operator== treat them), so tuple comparisons in the
+// selection loop are integer compares.
+__device__ __forceinline__ uint64_t ordered_bits(double d) {
+  const uint64_t b = static_cast<uint64_t>(__double_as_longlong(d == 0.0 ? 0.0 : d));
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+}
+__device__ __forceinline__ double from_ordered_bits(uint64_t o) {
+  const uint64_t b = (o >> 63) ? (o & 0x7fffffffffffffffULL) : ~o;
+  return __longlong_as_double(static_cast<long long>(b));
+}
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 // ---- rng.hpp:13-75 restated for the noisy oracle ----------------------------------------
 __host__ __device__ __forceinline__ uint64_t splitmix_step(uint64_t z) {

@@ -1,4 +1,4 @@
-// eqx_kernels.h -- kernel entry points and the step's argument block (device-side view).
+// eqx_kernels.h -- kernel entry points and argument blocks (device-side view).
 #pragma once
 
 #include <cstdint>
@@ -8,13 +8,71 @@
 
 namespace eqx {
 
-constexpr int kStepThreads = 512;
+constexpr int kDrainThreads = 256;   // 8 warps per tile
+constexpr int kTileRows = 2048;      // rows per drain tile (8 warps x 256 rows)
+constexpr int kStageMaxClients = 2048;  // smem-staged (coalesced) rank path up to this many
+constexpr int kScoreThreads = 256;
+constexpr int kSelectMaxThreads = 512;
 
-struct StepArgs {
-  // queue (arrival-order SoA) + client-grouped FIFO index
-  int64_t n;
+// One head-of-queue entry as the selection loop consumes it (40 B, shared memory).
+struct WinEntry {
+  double ufc_inc;
+  double rfc_inc;
+  uint64_t abits;   // order-preserving bits of arrival_time_s (-0.0 canonicalised to +0.0)
+  int32_t in;
+  int32_t pred;
+  int32_t row;
+  int32_t alone;    // fits_alone(in, pred) (gpu_model.cpp:69-72)
+};
+
+struct DrainArgs {
+  const int32_t* client;
+  int32_t n;
   int32_t C;
-  int32_t W;  // head-window depth cached in shared memory per client
+  int32_t tile_rows;
+  int32_t n_tiles;
+  int32_t staged;       // 1: smem-staged coalesced scatter (C <= kStageMaxClients)
+  uint32_t* hist;       // [C][n_tiles] counts -> exclusive offsets
+  int64_t hist_L;
+  int32_t* seg_off;     // [C+1]
+  uint32_t* perm;       // [n] row indices grouped by client, FIFO order
+  int32_t* count;       // [C] queued requests per client
+  int32_t* first_row;   // [C] first arrival row of the client in this drain
+  const int32_t* qlen_before;
+  const int32_t* running;
+  double* ufc;
+  double* rfc;
+  double* counter;
+  int32_t* backlogged;
+  int32_t counter_lift;
+  unsigned int* done;   // [2] last-CTA counters (hist, rank), reset by their last CTA
+  DevState* st;
+};
+
+struct ScoreArgs {
+  int64_t n;
+  const int32_t* client;
+  const double* arrival;
+  const int32_t* in_tok;
+  const int32_t* true_out;
+  const uint8_t* tag;
+  const int64_t* id;
+  int64_t id_base;
+  const double* weight;
+  int32_t* pred_out;
+  uint8_t* bucket_out;
+  double* ufc_out;
+  double* rfc_out;
+  DevState* st;
+  const ModelTables* model;
+  int32_t model_words;  // uint32 words of ModelTables to stage in smem (header + used LUT)
+  int32_t vec_ok;
+  Policy pol;
+  double now;
+};
+
+struct SelectArgs {
+  // queue columns (head entries are scored in-kernel with the same device function)
   const int32_t* client;
   const double* arrival;
   const int32_t* in_tok;
@@ -26,19 +84,19 @@ struct StepArgs {
   const int32_t* seg_off;
   const int32_t* count;
   int32_t* head;
+  int32_t C;
+  int32_t W;             // head-window depth cached in shared memory per client
+  int32_t sel_threads;   // threads in the selection loop (multiple of 32)
+  int32_t cw_in_smem;
+  void* cw_global;       // per-client work arrays when they do not fit in smem
   // ledger
   double* ufc;
   double* rfc;
   double* counter;
   const double* weight;
-  const uint32_t* order;
+  const uint32_t* order;  // rank of client_id (bytewise), ties by index
   int32_t* running;
   int32_t* backlogged;
-  // per-request scores
-  int32_t* pred_out;
-  uint8_t* bucket_out;
-  double* ufc_out;
-  double* rfc_out;
   // events
   int32_t* ev_row;
   int32_t* ev_kind;
@@ -51,25 +109,16 @@ struct StepArgs {
   int64_t ev_cap;
   DevState* st;
   const ModelTables* model;
-  int32_t model_lut_entries;
-  int32_t model_smem_bytes;
-  void* cw_global;  // per-client work arrays in global memory when they do not fit in smem
-  int32_t sel_threads;
-  int32_t vec_ok;
+  int32_t model_words;
+  int64_t tmax;          // largest T with double(T) * m <= M (exact, host binary search)
   Policy pol;
   double now;
 };
 
-__global__ void drain_hist_kernel(const int32_t* client, int32_t n, int32_t C, int32_t tile_rows,
-                                  int32_t n_tiles, uint32_t* hist, int32_t* first_row,
-                                  int32_t* count, DevState* st);
-__global__ void scan_kernel(uint32_t* data, int64_t L, int32_t C, int32_t n_tiles, int32_t* seg_off);
-__global__ void drain_rank_kernel(const int32_t* client, int32_t n, int32_t C, int32_t tile_rows,
-                                  int32_t n_tiles, const uint32_t* tile_off, uint32_t* perm);
-__global__ void lift_kernel(int32_t C, const int32_t* count, const int32_t* first_row,
-                            const int32_t* qlen_before, const int32_t* running, double* ufc,
-                            double* rfc, double* counter, int32_t* backlogged, int32_t counter_lift);
-__global__ void step_kernel(const StepArgs a);
+__global__ void drain_hist_kernel(DrainArgs a);
+__global__ void drain_rank_kernel(DrainArgs a);
+__global__ void score_kernel(ScoreArgs a);
+__global__ void select_kernel(SelectArgs a);
 __global__ void gather_ids_kernel(const int32_t* rows, int64_t n, const int64_t* id, int64_t id_base,
                                   int64_t* out);
 
