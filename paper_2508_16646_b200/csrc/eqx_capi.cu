@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -101,6 +102,10 @@ struct eqx_ctx {
   cudaStream_t stream2 = nullptr;  // side stream for whole-queue scoring
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   DevBuf d_done;                   // last-CTA counters of the drain kernels
+  DevBuf d_win;                    // [C][W] head windows
+  DevBuf d_wcnt;                   // per-(tile, warp, client) counts of the drain walk
+  DevBuf d_direct;                 // direct predict/map table (see ScoreArgs::direct)
+  int32_t direct_n = 0;
   // cached CUDA graph of drain + step for a resident (device) queue
   cudaGraphExec_t graph = nullptr;
   std::vector<unsigned char> graph_key;
@@ -261,6 +266,9 @@ void eqx_ctx_destroy(eqx_ctx* ctx) {
   if (ctx->h_state) cudaFreeHost(ctx->h_state);
   if (ctx->stream2) cudaStreamSynchronize(ctx->stream2);
   ctx->d_done.release();
+  ctx->d_win.release();
+  ctx->d_wcnt.release();
+  ctx->d_direct.release();
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->stream2) cudaStreamDestroy(ctx->stream2);
@@ -595,23 +603,23 @@ static eqx_status drain_prepare(eqx_ctx* ctx, const eqx_requests* r) {
   CUDA_TRY(ctx, ctx->d_ev_wait.ensure(8 * nn));
   CUDA_TRY(ctx, ctx->d_ev_id.ensure(8 * nn));
   CUDA_TRY(ctx, ctx->d_perm.ensure(4 * nn));
-  // tiling: 8 warps x (tile_rows/8) rows per tile.  Rosters up to kStageMaxClients use the
-  // smem-staged coalesced scatter with 2048-row tiles; larger rosters grow the tile so the
-  // [client][tile] histogram stays <= ~1M entries.
-  const bool staged = C <= kStageMaxClients;
-  int64_t tile_rows = kTileRows;
-  if (!staged)
-    while (static_cast<int64_t>(C) * ((n + tile_rows - 1) / tile_rows) > (int64_t(1) << 20)) tile_rows *= 2;
-  if (tile_rows / 8 > 65535) return fail(ctx, EQX_ERR_CONFIG, "too many clients for the drain tiling");
+  // tiling: one wave of tiles (~n / #SMs rows each, a multiple of 32 warps x 32 rows), so the
+  // [client][tile] histogram stays ~C x #SMs entries and its scan is short.  Each tile is
+  // staged in shared memory (coalesced per-client runs) when it fits.
+  int64_t tile_rows = (n + ctx->sm_count - 1) / std::max(ctx->sm_count, 1);
+  tile_rows = std::max<int64_t>(1024, (tile_rows + 1023) / 1024 * 1024);
+  if (tile_rows / kDrainWarps > 65535) return fail(ctx, EQX_ERR_CONFIG, "queue too long for the drain tiling");
   const int32_t n_tiles = static_cast<int32_t>(std::max<int64_t>(1, (n + tile_rows - 1) / tile_rows));
   const int64_t L = static_cast<int64_t>(C) * n_tiles;
   CUDA_TRY(ctx, ctx->d_hist.ensure(4 * std::max<int64_t>(L, 1)));
   ctx->tile_rows = tile_rows;
   ctx->n_tiles = n_tiles;
   ctx->hist_L = L;
-  ctx->staged = staged;
-  ctx->hist_smem = std::max<size_t>(4ull * C, 16);
-  ctx->rank_smem = 24ull * C + (staged ? 6ull * tile_rows : 0) + 16;
+  const size_t rank_base = (8ull + 2ull * kDrainWarps) * C + 64;
+  ctx->staged = rank_base + 6ull * tile_rows <= ctx->smem_optin;
+  ctx->hist_smem = std::max<size_t>(2ull * kDrainWarps * C, 16);
+  CUDA_TRY(ctx, ctx->d_wcnt.ensure(std::max<size_t>(2ull * kDrainWarps * C * n_tiles, 64)));
+  ctx->rank_smem = rank_base + (ctx->staged ? 6ull * tile_rows : 0);
   if (ctx->rank_smem > ctx->smem_optin || ctx->hist_smem > ctx->smem_optin)
     return fail(ctx, EQX_ERR_CONFIG, "too many clients per device (" + std::to_string(C) + ")");
   CUDA_TRY(ctx, cudaFuncSetAttribute(drain_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -645,6 +653,7 @@ static DrainArgs drain_args(eqx_ctx* ctx) {
   d.backlogged = ctx->d_backlogged.as<int32_t>();
   d.counter_lift = ctx->counter_lift;
   d.done = ctx->d_done.as<unsigned int>();
+  d.wcnt = ctx->d_wcnt.as<uint16_t>();
   d.st = ctx->d_state.as<DevState>();
   return d;
 }
@@ -684,9 +693,10 @@ static int64_t kv_threshold(double m, double M) {
 
 struct StepPlan {
   ScoreArgs sc;
+  WindowArgs wi;
   SelectArgs se;
-  size_t score_smem, select_smem;
-  int score_grid, select_threads;
+  size_t score_smem, select_smem, window_smem;
+  int score_grid, select_threads, window_grid;
 };
 
 static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl) {
@@ -698,6 +708,47 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl) {
   const size_t model_bytes = offsetof(ModelTables, lut) + 4ull * ctx->lut_entries;
   if (ctx->model_dirty) {  // compiled model tables -> device, only after they changed
     CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_model.p, &ctx->model, model_bytes, cudaMemcpyHostToDevice, s));
+    // direct table: the LUT + entry_for evaluated for every small input (MoPE / single proxy)
+    // or every small prediction (oracle); same functions, so the same results.
+    const ModelTables& M = ctx->model;
+    auto entry_for = [&](int pred) {
+      int b = M.n_prof - 1;
+      for (int e = M.n_prof - 1; e >= 0; --e)
+        if (pred <= M.prof_upper[e]) b = e;
+      return b;
+    };
+    std::vector<uint32_t> tab;
+    ctx->direct_n = 0;
+    if (M.pred_kind == kPredMope || M.pred_kind == kPredSingle) {
+      const int dn = 2048;
+      bool ok = true;
+      tab.resize(static_cast<size_t>(M.n_tag_states) * dn);
+      for (int t = 0; t < M.n_tag_states && ok; ++t) {
+        for (int in = 0; in < dn; ++in) {
+          int iv = 0;
+          for (int i = 0; i < M.n_cuts; ++i) iv += M.cuts[i] < in ? 1 : 0;
+          const int e = M.lut[iv * M.n_tag_states + t];
+          const int pred = e < 0 ? -e : e;
+          if (pred >= 65536) {
+            ok = false;
+            break;
+          }
+          tab[static_cast<size_t>(t) * dn + in] = static_cast<uint32_t>(pred) |
+                                                  (static_cast<uint32_t>(entry_for(pred)) << 16) |
+                                                  (static_cast<uint32_t>(e < 0 ? 1 : 0) << 24);
+        }
+      }
+      if (ok) ctx->direct_n = dn;
+    } else if (M.pred_kind == kPredOracle) {
+      const int dn = 8192;
+      tab.resize(dn);
+      for (int p = 0; p < dn; ++p) tab[p] = static_cast<uint32_t>(entry_for(p));
+      ctx->direct_n = dn;
+    }
+    if (ctx->direct_n) {
+      CUDA_TRY(ctx, ctx->d_direct.ensure(tab.size() * 4));
+      CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_direct.p, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice, s));
+    }
     CUDA_TRY(ctx, cudaStreamSynchronize(s));
     ctx->model_dirty = false;
   }
@@ -722,6 +773,8 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl) {
   sc.st = ctx->d_state.as<DevState>();
   sc.model = ctx->d_model.as<ModelTables>();
   sc.model_words = model_words;
+  sc.direct = ctx->d_direct.as<uint32_t>();
+  sc.direct_n = ctx->direct_n;
   sc.vec_ok = aligned16(sc.client) && aligned16(sc.arrival) && aligned16(sc.in_tok) &&
               (reinterpret_cast<uintptr_t>(sc.tag) % 8 == 0) && (!sc.true_out || aligned16(sc.true_out));
   sc.pol = ctx->pol;
@@ -767,12 +820,30 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl) {
   a.tmax = kv_threshold(ctx->perf.mem_per_token_bytes, ctx->perf.mem_capacity_bytes);
   a.pol = ctx->pol;
   a.now = now;
-  // selection warps: ~64 clients per warp, at most 16 warps; a single warp needs no barrier
-  const int G = std::max(1, std::min(kSelectMaxThreads / 32, (C + 63) / 64));
-  a.sel_threads = 32 * G;
   pl.select_threads = kSelectMaxThreads;
-  // shared memory: model | per-client work (if it fits) | head windows
-  const size_t static_smem = 4096;
+  // selection threads: one warp holding up to 8 clients per lane when C <= 256 (no barriers),
+  // otherwise up to 8 warps with 1/2/4/8 register slots per thread; beyond 2048 clients the
+  // shared-memory loop (seq_phase) takes over.
+  const int max_warps = kSelectMaxThreads / 32;
+  int K = 0, G = 1;
+  if (C <= 32) K = 1;
+  else if (C <= 64) K = 2;
+  else if (C <= 128) K = 4;
+  else if (C <= 256) K = 8;
+  else {
+    for (int k : {1, 2, 4, 8}) {
+      if (C <= 32 * max_warps * k) {
+        K = k;
+        G = (C + 32 * k - 1) / (32 * k);
+        break;
+      }
+    }
+    if (K == 0) G = max_warps;
+  }
+  a.K = K;
+  a.sel_threads = 32 * G;
+  // shared memory: model | per-client work (if it fits) | batch scratch | head windows
+  const size_t static_smem = 12288;
   const size_t cw_bytes = 13ull * 16 + static_cast<size_t>(C) * (6 * 8 + 7 * 4);
   size_t smem = model_smem;
   const size_t budget = ctx->smem_optin - static_smem - model_smem;
@@ -785,6 +856,28 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl) {
     a.cw_in_smem = 0;
     a.cw_global = ctx->d_cw.p;
   }
+  const size_t left0 = ctx->smem_optin - static_smem - smem;
+  // Batch lookahead D: about twice the picks a client can get (slots spread over clients),
+  // 2..8, with the C*D-item sort (24 B + 1 B per item) and W >= D windows fitting in smem.
+  auto pow2 = [](int64_t x) { int64_t t = 1; while (t < x) t <<= 1; return t; };
+  auto batch_bytes = [&](int64_t D) {
+    const int64_t tn = pow2(std::max<int64_t>(C * D, 2));
+    return static_cast<size_t>(tn * (sizeof(BatchItem) + 1) + 16 * 3 + 4ll * C);
+  };
+  int64_t D = std::min<int64_t>(8, std::max<int64_t>(2, 2 * static_cast<int64_t>(ctx->perf.max_batch) / std::max(C, 1) + 2));
+  while (D >= 2 && (static_cast<int64_t>(C) * D > 8192 ||
+                    batch_bytes(D) + static_cast<size_t>(D) * C * sizeof(WinEntry) > left0))
+    --D;
+  if (D < 2 || C == 0) D = 0;
+  // Default: register-resident sequential picks (measured faster than speculative batches on
+  // cfg2/cfg3, profiles/); EQX_SELECT_MODE=batch enables the batch path for experiments.
+  {
+    const char* m = std::getenv("EQX_SELECT_MODE");
+    if (!(m && std::string(m) == "batch") && K > 0) D = 0;
+  }
+  a.D = static_cast<int32_t>(D);
+  a.Tn = D ? static_cast<int32_t>(pow2(std::max<int64_t>(C * D, 2))) : 0;
+  if (D) smem += batch_bytes(D);
   const size_t left = ctx->smem_optin - static_smem - smem;
   // A client is picked at most max_batch times before the slots run out (+1 for the next
   // head's arrival); deeper heads (rejection streams) are scored on demand from HBM.
@@ -793,6 +886,31 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl) {
   a.W = static_cast<int32_t>(std::max<int64_t>(W, 0));
   smem += static_cast<size_t>(a.W) * C * sizeof(WinEntry);
   pl.select_smem = smem;
+  CUDA_TRY(ctx, ctx->d_win.ensure(std::max<size_t>(static_cast<size_t>(a.W) * C * sizeof(WinEntry), 64)));
+  a.win_g = ctx->d_win.as<WinEntry>();
+  WindowArgs& wi = pl.wi;
+  wi.arrival = ctx->q_arrival;
+  wi.in_tok = ctx->q_in;
+  wi.true_out = ctx->q_true;
+  wi.tag = ctx->q_tag;
+  wi.id = ctx->q_id;
+  wi.id_base = ctx->id_base;
+  wi.perm = ctx->d_perm.as<uint32_t>();
+  wi.seg_off = ctx->d_seg_off.as<int32_t>();
+  wi.count = ctx->d_count.as<int32_t>();
+  wi.head = ctx->d_head.as<int32_t>();
+  wi.weight = ctx->d_weight.as<double>();
+  wi.C = C;
+  wi.W = a.W;
+  wi.win = ctx->d_win.as<WinEntry>();
+  wi.model = ctx->d_model.as<ModelTables>();
+  wi.model_words = model_words;
+  wi.tmax = a.tmax;
+  wi.pol = ctx->pol;
+  wi.now = now;
+  pl.window_smem = model_smem;
+  const int64_t witems = static_cast<int64_t>(C) * a.W;
+  pl.window_grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((witems + 255) / 256, 8ll * ctx->sm_count)));
   CUDA_TRY(ctx, cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   return EQX_OK;
 }
@@ -815,9 +933,32 @@ static eqx_status step_enqueue(eqx_ctx* ctx, const StepPlan& pl, bool with_drain
     eqx_status e = drain_enqueue(ctx);
     if (e != EQX_OK) return e;
   }
+  window_kernel<<<pl.window_grid, 256, pl.window_smem, s>>>(pl.wi);
   select_kernel<<<1, pl.select_threads, pl.select_smem, s>>>(pl.se);
   CUDA_TRY(ctx, cudaGetLastError());
   CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_join, 0));
+  EventFillArgs ef;
+  std::memset(&ef, 0, sizeof(ef));
+  ef.n_events = &ctx->d_state.as<DevState>()->n_events;
+  ef.ev_cap = ctx->ev_cap;
+  ef.ev_row = ctx->d_ev_row.as<int32_t>();
+  ef.ev_kind = ctx->d_ev_kind.as<int32_t>();
+  ef.ev_client = ctx->d_ev_client.as<int32_t>();
+  ef.ev_pred = ctx->d_ev_pred.as<int32_t>();
+  ef.ev_ufc = ctx->d_ev_ufc.as<double>();
+  ef.ev_rfc = ctx->d_ev_rfc.as<double>();
+  ef.ev_vtc = ctx->d_ev_vtc.as<double>();
+  ef.ev_wait = ctx->d_ev_wait.as<double>();
+  ef.pred = ctx->d_pred.as<int32_t>();
+  ef.ufc_inc = ctx->d_ufc_out.as<double>();
+  ef.rfc_inc = ctx->d_rfc_out.as<double>();
+  ef.arrival = ctx->q_arrival;
+  ef.in_tok = ctx->q_in;
+  ef.weight = ctx->d_weight.as<double>();
+  ef.pol = ctx->pol;
+  ef.now = pl.se.now;
+  if (ctx->n > 0) event_fill_kernel<<<ctx->sm_count, 256, 0, s>>>(ef);
+  CUDA_TRY(ctx, cudaGetLastError());
   CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_state, ctx->d_state.p, sizeof(DevState), cudaMemcpyDeviceToHost, s));
   return EQX_OK;
 }
@@ -911,7 +1052,7 @@ eqx_status eqx_phase_times(eqx_ctx* ctx, double* out_us, int32_t n) {
   const unsigned long long* t = ctx->h_state->t;
   const double base = static_cast<double>(t[0]);
   for (int i = 0; i < n && i < 6; ++i) out_us[i] = (static_cast<double>(t[i]) - base) * 1e-3;
-  for (int i = 6; i < n && i < 8; ++i) out_us[i] = static_cast<double>(t[i]);  // cycles
+  for (int i = 6; i < n && i < 16; ++i) out_us[i] = static_cast<double>(t[i]);  // counts / cycles
   return EQX_OK;
 }
 

@@ -61,8 +61,9 @@ struct DevState {
   int32_t pad1;
   // phase timestamps (%globaltimer ns) of the last step, for profiling:
   // [0] selection start [1] windows filled [2] loop start [3] loop end
-  // [4] first worker start (min) [5] last worker end (max)
-  unsigned long long t[8];
+  // [4] first worker start (min) [5] last worker end (max) [6] #batches [7] #seq phases
+  // [8..11] batch cycles: stream generation, sort, verify, commit
+  unsigned long long t[16];
 };
 
 // Order-preserving map double -> uint64 (IEEE total order on non-NaN values, with -0.0 and
@@ -104,26 +105,29 @@ struct Scored {
 
 // Predict + map_metrics + ufc_increment + rfc_increment for one request.
 //   MoPE:   route (predictor.cpp:36-60) + ExpertModel::predict (:62-71) through the LUT
+//           (single-proxy uses the same LUT path, compiled from one expert)
 //   oracle: true_output_tokens (predictor.hpp:36); noisy: predictor.cpp:17-23
 //   map:    GpuProfile::entry_for (gpu_model.cpp:74-80), first bucket with pred <= upper
 //   ufc:    w * (in + ow * pred) / (1 + delta * ((now - arrival) + lat_ms / 1000))
 //           (scheduler.cpp:19-27 with wait = now - arrival, engine.cpp:257)
 //   rfc:    (w * tps) * util (scheduler.cpp:29-31)
-__device__ __forceinline__ Scored score_request(const ModelTables& M, const Policy& P, double now,
-                                                int32_t in, uint32_t tag, int32_t true_out,
-                                                int64_t id, double arrival, double w) {
+// KIND is the predictor family (kPredMope for MoPE and single-proxy tables).
+template <int KIND>
+__device__ __forceinline__ Scored score_request_t(const ModelTables& M, const Policy& P, double now, int32_t in,
+                                                  uint32_t tag, int32_t true_out, int64_t id, double arrival,
+                                                  double w) {
   Scored s;
   s.fallback = 0;
   s.near_tie = 0;
   int32_t pred;
-  if (M.pred_kind == kPredMope || M.pred_kind == kPredSingle) {
+  if constexpr (KIND == kPredMope) {
     int32_t iv = 0;
     for (int i = 0; i < M.n_cuts; ++i) iv += (M.cuts[i] < in) ? 1 : 0;
     const uint32_t t = tag < static_cast<uint32_t>(M.n_tag_states) ? tag : 0u;
     const int32_t e = M.lut[iv * M.n_tag_states + static_cast<int32_t>(t)];
     s.fallback = e < 0 ? 1u : 0u;
     pred = e < 0 ? -e : e;
-  } else if (M.pred_kind == kPredOracle) {
+  } else if constexpr (KIND == kPredOracle) {
     pred = true_out > 1 ? true_out : 1;
   } else {
     // NoisyOraclePredictor: Rng(mix_keys(mix_keys(seed, fnv1a("noisy_oracle")), id)).laplace(l1)
@@ -153,6 +157,55 @@ __device__ __forceinline__ Scored score_request(const ModelTables& M, const Poli
   s.ufc_inc = __ddiv_rn(__dmul_rn(w, tokens), denom);
   s.rfc_inc = __dmul_rn(__dmul_rn(w, M.prof_tps[b]), M.prof_util[b]);
   return s;
+}
+
+// Same result as score_request_t<KIND>, with the predict + map_metrics lookups served by the
+// host-compiled direct table when the input is inside it (one read-only-cache load instead of
+// the interval and bucket searches).
+template <int KIND>
+__device__ __forceinline__ Scored score_request_direct(const ModelTables& M, const Policy& P, const uint32_t* direct,
+                                                       int32_t direct_n, double now, int32_t in, uint32_t tag,
+                                                       int32_t true_out, int64_t id, double arrival, double w) {
+  int32_t pred, b;
+  Scored s;
+  s.fallback = 0;
+  s.near_tie = 0;
+  if constexpr (KIND == kPredMope) {
+    const uint32_t t = tag < static_cast<uint32_t>(M.n_tag_states) ? tag : 0u;
+    if (static_cast<uint32_t>(in) < static_cast<uint32_t>(direct_n)) {
+      const uint32_t e = __ldg(direct + t * static_cast<uint32_t>(direct_n) + static_cast<uint32_t>(in));
+      pred = static_cast<int32_t>(e & 0xffffu);
+      b = static_cast<int32_t>((e >> 16) & 0xffu);
+      s.fallback = e >> 24;
+    } else {
+      return score_request_t<KIND>(M, P, now, in, tag, true_out, id, arrival, w);
+    }
+  } else if constexpr (KIND == kPredOracle) {
+    pred = true_out > 1 ? true_out : 1;
+    if (pred < direct_n) {
+      b = static_cast<int32_t>(__ldg(direct + pred));
+    } else {
+      return score_request_t<KIND>(M, P, now, in, tag, true_out, id, arrival, w);
+    }
+  } else {
+    return score_request_t<KIND>(M, P, now, in, tag, true_out, id, arrival, w);
+  }
+  const double tokens = __dadd_rn(static_cast<double>(in), __dmul_rn(P.ow, static_cast<double>(pred)));
+  const double wait = __dsub_rn(now, arrival);
+  const double denom = __dadd_rn(1.0, __dmul_rn(P.delta, __dadd_rn(wait, M.prof_pred_s[b])));
+  s.pred = pred;
+  s.bucket = b;
+  s.ufc_inc = __ddiv_rn(__dmul_rn(w, tokens), denom);
+  s.rfc_inc = __dmul_rn(__dmul_rn(w, M.prof_tps[b]), M.prof_util[b]);
+  return s;
+}
+
+// Runtime-dispatched variant (cold paths: head windows, deep heads).
+static __device__ __noinline__ Scored score_request(const ModelTables& M, const Policy& P, double now, int32_t in,
+                                             uint32_t tag, int32_t true_out, int64_t id, double arrival, double w) {
+  if (M.pred_kind == kPredOracle) return score_request_t<kPredOracle>(M, P, now, in, tag, true_out, id, arrival, w);
+  if (M.pred_kind == kPredNoisy) return score_request_t<kPredNoisy>(M, P, now, in, tag, true_out, id, arrival, w);
+  return score_request_t<kPredMope>(M, P, now, in, tag, true_out, id, arrival, w);
 }
 
 }  // namespace eqx

@@ -15,6 +15,7 @@
 //   gather_ids_kernel    event rows -> request ids for the caller.
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <cstdio>
 
 #include "eqx_device.cuh"
 #include "eqx_kernels.h"
@@ -108,21 +109,35 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* o
 __global__ void __launch_bounds__(kDrainThreads) drain_hist_kernel(const DrainArgs a) {
   extern __shared__ __align__(16) uint32_t sh[];
   const int32_t C = a.C;
-  for (int c = threadIdx.x; c < C; c += blockDim.x) sh[c] = 0;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint16_t* wc = reinterpret_cast<uint16_t*>(sh);  // [kDrainWarps][C]
+  for (int i = tid; i < kDrainWarps * C; i += blockDim.x) wc[i] = 0;
   __syncthreads();
   const int32_t tile = blockIdx.x;
-  const int32_t r0 = tile * a.tile_rows;
-  const int32_t r1 = min(a.n, r0 + a.tile_rows);
-  for (int32_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
-    const int32_t c = a.client[r];
-    if (static_cast<uint32_t>(c) >= static_cast<uint32_t>(C)) {
-      a.st->bad_client = 1;
-      continue;
-    }
-    atomicAdd(&sh[c], 1u);
+  const int32_t sub = a.tile_rows / kDrainWarps;
+  const int32_t r0 = tile * a.tile_rows + warp * sub;
+  const int32_t r1 = min(a.n, r0 + sub);
+  uint16_t* my = wc + warp * C;
+  bool bad = false;
+  for (int32_t r = r0; r < r1; r += 32) {  // per-warp counts: one writer per (warp, client)
+    const int32_t row = r + lane;
+    const int32_t c = row < r1 ? a.client[row] : -1;
+    const bool ok = static_cast<uint32_t>(c) < static_cast<uint32_t>(C);
+    bad |= row < r1 && !ok;
+    const unsigned peers = __match_any_sync(0xffffffffu, ok ? c : -1);
+    if (ok && lane == __ffs(peers) - 1) my[c] = static_cast<uint16_t>(my[c] + __popc(peers));
+    __syncwarp();
   }
+  if (bad) a.st->bad_client = 1;
   __syncthreads();
-  for (int c = threadIdx.x; c < C; c += blockDim.x) a.hist[static_cast<int64_t>(c) * a.n_tiles + tile] = sh[c];
+  uint16_t* g = a.wcnt + static_cast<int64_t>(tile) * kDrainWarps * C;
+  for (int i = tid; i < kDrainWarps * C; i += blockDim.x) g[i] = wc[i];
+  for (int c = tid; c < C; c += blockDim.x) {
+    uint32_t t = 0;
+#pragma unroll 8
+    for (int w = 0; w < kDrainWarps; ++w) t += wc[w * C + c];
+    a.hist[static_cast<int64_t>(c) * a.n_tiles + tile] = t;
+  }
   if (!last_cta(&a.done[0])) return;
   // ---- epilogue (one CTA): exclusive scan of hist in [client][tile] order ----
   __shared__ uint32_t warp_buf[32];
@@ -130,14 +145,28 @@ __global__ void __launch_bounds__(kDrainThreads) drain_hist_kernel(const DrainAr
   const int64_t per = (L + blockDim.x - 1) / blockDim.x;
   const int64_t b0 = ::min(L, per * static_cast<int64_t>(threadIdx.x)), b1 = ::min(L, b0 + per);
   uint32_t sum = 0;
-  for (int64_t i = b0; i < b1; ++i) sum += __ldcg(a.hist + i);
+  for (int64_t i0 = b0; i0 < b1; i0 += 8) {  // 8 independent L2 loads in flight
+    uint32_t v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = (i0 + k < b1) ? __ldcg(a.hist + i0 + k) : 0u;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) sum += v[k];
+  }
   uint32_t run;
   const uint32_t total = block_exclusive_scan(sum, &run, warp_buf);
-  for (int64_t i = b0; i < b1; ++i) {
-    const uint32_t v = __ldcg(a.hist + i);
-    __stcg(a.hist + i, run);
-    if (i % a.n_tiles == 0) a.seg_off[i / a.n_tiles] = static_cast<int32_t>(run);
-    run += v;
+  for (int64_t i0 = b0; i0 < b1; i0 += 8) {
+    uint32_t v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = (i0 + k < b1) ? __ldcg(a.hist + i0 + k) : 0u;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int64_t i = i0 + k;
+      if (i < b1) {
+        __stcg(a.hist + i, run);
+        if (i % a.n_tiles == 0) a.seg_off[i / a.n_tiles] = static_cast<int32_t>(run);
+        run += v[k];
+      }
+    }
   }
   if (threadIdx.x == 0) {
     a.seg_off[C] = static_cast<int32_t>(total);
@@ -260,7 +289,7 @@ __global__ void __launch_bounds__(kDrainThreads) drain_rank_kernel(const DrainAr
   const int32_t C = a.C;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int32_t tile = blockIdx.x;
-  const int32_t sub = a.tile_rows / 8;
+  const int32_t sub = a.tile_rows / kDrainWarps;
   const int32_t t0 = tile * a.tile_rows;
   const int32_t t1 = min(a.n, t0 + a.tile_rows);
   const int32_t r0 = t0 + warp * sub;
@@ -268,25 +297,18 @@ __global__ void __launch_bounds__(kDrainThreads) drain_rank_kernel(const DrainAr
   const unsigned lt = (1u << lane) - 1u;
   uint32_t* base = sh;                                     // [C] global start of this tile's run
   uint32_t* toff = sh + C;                                 // [C] tile-local start / totals
-  uint16_t* wc = reinterpret_cast<uint16_t*>(sh + 2 * C);  // [8][C]
+  uint16_t* wc = reinterpret_cast<uint16_t*>(sh + 2 * C);  // [kDrainWarps][C]
   for (int c = tid; c < C; c += blockDim.x) base[c] = a.hist[static_cast<int64_t>(c) * a.n_tiles + tile];
-  for (int i = tid; i < 8 * C; i += blockDim.x) wc[i] = 0;
-  __syncthreads();
-  uint16_t* my = wc + warp * C;
-  for (int32_t r = r0; r < r1; r += 32) {  // walk 1: counts per (warp, client)
-    const int32_t row = r + lane;
-    const int32_t c = row < r1 ? a.client[row] : -1;
-    const unsigned peers = __match_any_sync(0xffffffffu, c);
-    const int leader = __ffs(peers) - 1;
-    if (static_cast<uint32_t>(c) < static_cast<uint32_t>(C) && lane == leader)
-      my[c] = static_cast<uint16_t>(my[c] + __popc(peers));
-    __syncwarp();
+  {  // per-warp client counts from drain_hist_kernel's walk
+    const uint16_t* g = a.wcnt + static_cast<int64_t>(tile) * kDrainWarps * C;
+    for (int i = tid; i < kDrainWarps * C; i += blockDim.x) wc[i] = g[i];
   }
   __syncthreads();
+  uint16_t* my = wc + warp * C;
   for (int c = tid; c < C; c += blockDim.x) {  // exclusive over warps; total per client
     uint32_t run = 0;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) {
+#pragma unroll 8
+    for (int w = 0; w < kDrainWarps; ++w) {
       const uint32_t t = wc[w * C + c];
       wc[w * C + c] = static_cast<uint16_t>(run);
       run += t;
@@ -309,7 +331,7 @@ __global__ void __launch_bounds__(kDrainThreads) drain_rank_kernel(const DrainAr
       run += t;
     }
     __syncthreads();
-    uint32_t* srow = sh + 6 * C;                                      // [tile_rows]
+    uint32_t* srow = sh + 2 * C + (kDrainWarps / 2) * C;             // [tile_rows]
     uint16_t* scl = reinterpret_cast<uint16_t*>(srow + a.tile_rows);  // [tile_rows]
     for (int32_t r = r0; r < r1; r += 32) {  // walk 2: slot in the client-sorted tile
       const int32_t row = r + lane;
@@ -360,67 +382,52 @@ __global__ void __launch_bounds__(kDrainThreads) drain_rank_kernel(const DrainAr
 
 // ===================================== scoring ===========================================
 
-// Whole-queue scoring: 8 requests per thread per iteration (two 16-byte vectors of every
-// column issued before any compute), streaming stores of pred/bucket/ufc_inc/rfc_inc.
-__global__ void __launch_bounds__(kScoreThreads) score_kernel(const ScoreArgs a) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  stage_model(a.model, a.model_words, smem);
-  __syncthreads();
-  const ModelTables& M = *reinterpret_cast<const ModelTables*>(smem);
-  if (threadIdx.x == 0) atomicMin(&a.st->t[4], global_ns());
+// Whole-queue scoring: 4 requests per thread per iteration through 16-byte loads of every
+// column, predict + map_metrics through the direct table (read-only cache), FP64 increments,
+// streaming stores of pred/bucket/ufc_inc/rfc_inc.
+template <int KIND>
+__device__ __forceinline__ void score_body(const ScoreArgs& a, const ModelTables& M) {
   const int64_t n = a.n;
   uint32_t fb = 0, nt = 0;
-  const bool oracle_like = M.pred_kind == kPredOracle || M.pred_kind == kPredNoisy;
-  const int64_t nvec = a.vec_ok ? n / 8 : 0;  // groups of 8 rows
+  constexpr bool oracle_like = KIND == kPredOracle || KIND == kPredNoisy;
+  const int64_t nvec = a.vec_ok ? n / 4 : 0;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t v = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < nvec; v += stride) {
-    int4 cl[2], in4[2], to[2];
-    double2 ar[4];
-    uint32_t tg[2];
+    const int4 cl = ldg_stream(reinterpret_cast<const int4*>(a.client) + v);
+    const int4 in4 = ldg_stream(reinterpret_cast<const int4*>(a.in_tok) + v);
+    const double2 a01 = ldg_stream(reinterpret_cast<const double2*>(a.arrival) + 2 * v);
+    const double2 a23 = ldg_stream(reinterpret_cast<const double2*>(a.arrival) + 2 * v + 1);
+    const uint32_t tg = ldg_stream(reinterpret_cast<const uint32_t*>(a.tag) + v);
+    const int4 to = oracle_like ? ldg_stream(reinterpret_cast<const int4*>(a.true_out) + v) : make_int4(1, 1, 1, 1);
+    const int64_t r0 = 4 * v;
+    const int cs[4] = {cl.x, cl.y, cl.z, cl.w};
+    const int ins[4] = {in4.x, in4.y, in4.z, in4.w};
+    const int tos[4] = {to.x, to.y, to.z, to.w};
+    const double arr[4] = {a01.x, a01.y, a23.x, a23.y};
+    Scored s[4];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      cl[h] = ldg_stream(reinterpret_cast<const int4*>(a.client) + 2 * v + h);
-      in4[h] = ldg_stream(reinterpret_cast<const int4*>(a.in_tok) + 2 * v + h);
-      tg[h] = ldg_stream(reinterpret_cast<const uint32_t*>(a.tag) + 2 * v + h);
-      to[h] = oracle_like ? ldg_stream(reinterpret_cast<const int4*>(a.true_out) + 2 * v + h)
-                          : make_int4(1, 1, 1, 1);
-    }
-#pragma unroll
-    for (int h = 0; h < 4; ++h) ar[h] = ldg_stream(reinterpret_cast<const double2*>(a.arrival) + 4 * v + h);
-    const int64_t r0 = 8 * v;
-    const int cs[8] = {cl[0].x, cl[0].y, cl[0].z, cl[0].w, cl[1].x, cl[1].y, cl[1].z, cl[1].w};
-    const int ins[8] = {in4[0].x, in4[0].y, in4[0].z, in4[0].w, in4[1].x, in4[1].y, in4[1].z, in4[1].w};
-    const int tos[8] = {to[0].x, to[0].y, to[0].z, to[0].w, to[1].x, to[1].y, to[1].z, to[1].w};
-    const double arr[8] = {ar[0].x, ar[0].y, ar[1].x, ar[1].y, ar[2].x, ar[2].y, ar[3].x, ar[3].y};
-    Scored s[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int64_t id = (M.pred_kind == kPredNoisy && a.id) ? a.id[r0 + k] : a.id_base + r0 + k;
+    for (int k = 0; k < 4; ++k) {
+      const int64_t id = (KIND == kPredNoisy && a.id) ? a.id[r0 + k] : a.id_base + r0 + k;
       const double w = __ldg(a.weight + cs[k]);
-      s[k] = score_request(M, a.pol, a.now, ins[k], (tg[k >> 2] >> (8 * (k & 3))) & 0xffu, tos[k], id, arr[k], w);
+      s[k] = score_request_direct<KIND>(M, a.pol, a.direct, a.direct_n, a.now, ins[k], (tg >> (8 * k)) & 0xffu, tos[k],
+                                        id, arr[k], w);
       fb += s[k].fallback;
       nt += s[k].near_tie;
     }
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      stg_stream(reinterpret_cast<int4*>(a.pred_out) + 2 * v + h,
-                 make_int4(s[4 * h].pred, s[4 * h + 1].pred, s[4 * h + 2].pred, s[4 * h + 3].pred));
-      stg_stream(reinterpret_cast<uint32_t*>(a.bucket_out) + 2 * v + h,
-                 static_cast<uint32_t>(s[4 * h].bucket) | (static_cast<uint32_t>(s[4 * h + 1].bucket) << 8) |
-                     (static_cast<uint32_t>(s[4 * h + 2].bucket) << 16) |
-                     (static_cast<uint32_t>(s[4 * h + 3].bucket) << 24));
-    }
-#pragma unroll
-    for (int h = 0; h < 4; ++h) {
-      stg_stream(reinterpret_cast<double2*>(a.ufc_out) + 4 * v + h, make_double2(s[2 * h].ufc_inc, s[2 * h + 1].ufc_inc));
-      stg_stream(reinterpret_cast<double2*>(a.rfc_out) + 4 * v + h, make_double2(s[2 * h].rfc_inc, s[2 * h + 1].rfc_inc));
-    }
+    stg_stream(reinterpret_cast<int4*>(a.pred_out) + v, make_int4(s[0].pred, s[1].pred, s[2].pred, s[3].pred));
+    stg_stream(reinterpret_cast<uint32_t*>(a.bucket_out) + v,
+               static_cast<uint32_t>(s[0].bucket) | (static_cast<uint32_t>(s[1].bucket) << 8) |
+                   (static_cast<uint32_t>(s[2].bucket) << 16) | (static_cast<uint32_t>(s[3].bucket) << 24));
+    stg_stream(reinterpret_cast<double2*>(a.ufc_out) + 2 * v, make_double2(s[0].ufc_inc, s[1].ufc_inc));
+    stg_stream(reinterpret_cast<double2*>(a.ufc_out) + 2 * v + 1, make_double2(s[2].ufc_inc, s[3].ufc_inc));
+    stg_stream(reinterpret_cast<double2*>(a.rfc_out) + 2 * v, make_double2(s[0].rfc_inc, s[1].rfc_inc));
+    stg_stream(reinterpret_cast<double2*>(a.rfc_out) + 2 * v + 1, make_double2(s[2].rfc_inc, s[3].rfc_inc));
   }
-  for (int64_t r = 8 * nvec + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < n; r += stride) {
+  for (int64_t r = 4 * nvec + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < n; r += stride) {
     const int32_t c = a.client[r];
     const int64_t id = a.id ? a.id[r] : a.id_base + r;
-    const Scored s = score_request(M, a.pol, a.now, a.in_tok[r], a.tag[r], oracle_like ? a.true_out[r] : 1, id,
-                                   a.arrival[r], a.weight[c]);
+    const Scored s = score_request_direct<KIND>(M, a.pol, a.direct, a.direct_n, a.now, a.in_tok[r], a.tag[r],
+                                                oracle_like ? a.true_out[r] : 1, id, a.arrival[r], a.weight[c]);
     a.pred_out[r] = s.pred;
     a.bucket_out[r] = static_cast<uint8_t>(s.bucket);
     a.ufc_out[r] = s.ufc_inc;
@@ -434,6 +441,17 @@ __global__ void __launch_bounds__(kScoreThreads) score_kernel(const ScoreArgs a)
     if (fb) atomicAdd(&a.st->fallbacks, static_cast<unsigned long long>(fb));
     if (nt) atomicAdd(&a.st->near_ties, static_cast<unsigned long long>(nt));
   }
+}
+
+__global__ void __launch_bounds__(kScoreThreads, 4) score_kernel(const ScoreArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  stage_model(a.model, a.model_words, smem);
+  __syncthreads();
+  const ModelTables& M = *reinterpret_cast<const ModelTables*>(smem);
+  if (threadIdx.x == 0) atomicMin(&a.st->t[4], global_ns());
+  if (M.pred_kind == kPredOracle) score_body<kPredOracle>(a, M);
+  else if (M.pred_kind == kPredNoisy) score_body<kPredNoisy>(a, M);
+  else score_body<kPredMope>(a, M);
   __syncthreads();
   if (threadIdx.x == 0) atomicMax(&a.st->t[5], global_ns());
 }
@@ -453,18 +471,51 @@ __device__ __forceinline__ bool better(const Cand& x, const Cand& y) {
   return (x.o != 0xffffffffu) & ((y.o == 0xffffffffu) | lt);
 }
 
-__device__ __forceinline__ Cand no_cand() { return Cand{0ull, 0ull, 0xffffffffu}; }
+__device__ __forceinline__ Cand no_cand() { return Cand{~0ull, ~0ull, 0xffffffffu}; }
 
+// Warp argmin of the (key, arrival, rank) tuples: two redux.sync mins on the key halves and a
+// ballot settle it unless several lanes share the minimal key (then arrival and rank decide
+// through the same redux pattern).  Sentinels carry k = a = ~0 and o = ~0.
 __device__ __forceinline__ Cand warp_argmin(Cand v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    Cand w;
-    w.k = __shfl_xor_sync(0xffffffffu, v.k, o);
-    w.a = __shfl_xor_sync(0xffffffffu, v.a, o);
-    w.o = __shfl_xor_sync(0xffffffffu, v.o, o);
-    if (better(w, v)) v = w;
+  const uint32_t hi = static_cast<uint32_t>(v.k >> 32), lo = static_cast<uint32_t>(v.k);
+  const uint32_t mhi = __reduce_min_sync(0xffffffffu, hi);
+  const uint32_t mlo = __reduce_min_sync(0xffffffffu, hi == mhi ? lo : 0xffffffffu);
+  unsigned m = __ballot_sync(0xffffffffu, hi == mhi && lo == mlo);
+  if (__popc(m) > 1) {  // equal keys: arrival, then client rank
+    const bool in = (m >> (threadIdx.x & 31)) & 1u;
+    const uint32_t ahi = static_cast<uint32_t>(v.a >> 32), alo = static_cast<uint32_t>(v.a);
+    const uint32_t mahi = __reduce_min_sync(0xffffffffu, in ? ahi : 0xffffffffu);
+    const bool in2 = in && ahi == mahi;
+    const uint32_t malo = __reduce_min_sync(0xffffffffu, in2 ? alo : 0xffffffffu);
+    const bool in3 = in2 && alo == malo;
+    const uint32_t mo = __reduce_min_sync(0xffffffffu, in3 ? v.o : 0xffffffffu);
+    m = __ballot_sync(0xffffffffu, in3 && v.o == mo);
   }
-  return v;
+  const int src = __ffs(m) - 1;
+  Cand w;
+  w.k = __shfl_sync(0xffffffffu, v.k, src);
+  w.a = __shfl_sync(0xffffffffu, v.a, src);
+  w.o = __shfl_sync(0xffffffffu, v.o, src);
+  return w;
+}
+
+// Lane holding the warp minimum (same tie-break as warp_argmin).
+__device__ __forceinline__ int warp_argmin_lane(const Cand& v) {
+  const uint32_t hi = static_cast<uint32_t>(v.k >> 32), lo = static_cast<uint32_t>(v.k);
+  const uint32_t mhi = __reduce_min_sync(0xffffffffu, hi);
+  const uint32_t mlo = __reduce_min_sync(0xffffffffu, hi == mhi ? lo : 0xffffffffu);
+  unsigned m = __ballot_sync(0xffffffffu, hi == mhi && lo == mlo);
+  if (__popc(m) > 1) {
+    const bool in = (m >> (threadIdx.x & 31)) & 1u;
+    const uint32_t ahi = static_cast<uint32_t>(v.a >> 32), alo = static_cast<uint32_t>(v.a);
+    const uint32_t mahi = __reduce_min_sync(0xffffffffu, in ? ahi : 0xffffffffu);
+    const bool in2 = in && ahi == mahi;
+    const uint32_t malo = __reduce_min_sync(0xffffffffu, in2 ? alo : 0xffffffffu);
+    const bool in3 = in2 && alo == malo;
+    const uint32_t mo = __reduce_min_sync(0xffffffffu, in3 ? v.o : 0xffffffffu);
+    m = __ballot_sync(0xffffffffu, in3 && v.o == mo);
+  }
+  return __ffs(m) - 1;
 }
 
 // Per-client working state of the loop (shared memory, or global scratch for huge rosters).
@@ -506,8 +557,9 @@ __device__ __forceinline__ double hf_key(const Policy& P, double u, double r, do
   return __dadd_rn(__dmul_rn(P.alpha, uu), __dmul_rn(P.beta, rr));
 }
 
-__device__ __forceinline__ WinEntry entry_of_row(const SelectArgs& a, const ModelTables& M, int32_t c,
-                                                 int32_t row, double w) {
+// Score one queued row into a head-window entry (shared by window_kernel and deep heads).
+template <class A>
+__device__ __forceinline__ WinEntry make_entry(const A& a, const ModelTables& M, int32_t row, double w) {
   const int64_t id = a.id ? a.id[row] : a.id_base + row;
   const double arr = a.arrival[row];
   const int32_t in = a.in_tok[row];
@@ -524,11 +576,31 @@ __device__ __forceinline__ WinEntry entry_of_row(const SelectArgs& a, const Mode
   return e;
 }
 
+// Head at FIFO position j beyond the cached window (rejection streams): scored from HBM.
+__device__ __noinline__ WinEntry deep_entry(const SelectArgs& a, const ModelTables& M, int32_t c, int32_t j, double w) {
+  return make_entry(a, M, static_cast<int32_t>(a.perm[a.seg_off[c] + j]), w);
+}
+
 __device__ __forceinline__ WinEntry get_entry(const SelectArgs& a, const ModelTables& M, const WinEntry* win,
                                               const ClientWork& cw, int32_t c, int32_t j) {
   const int32_t k = j - cw.pos0[c];
   if (k < a.W) return win[static_cast<int64_t>(c) * a.W + k];
-  return entry_of_row(a, M, c, static_cast<int32_t>(a.perm[a.seg_off[c] + j]), cw.w[c]);  // deep head
+  return deep_entry(a, M, c, j, cw.w[c]);
+}
+
+// First W queued entries of every client (C*W items, one per thread across many CTAs).
+__global__ void __launch_bounds__(256) window_kernel(const WindowArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  stage_model(a.model, a.model_words, smem);
+  __syncthreads();
+  const ModelTables& M = *reinterpret_cast<const ModelTables*>(smem);
+  const int64_t items = static_cast<int64_t>(a.C) * a.W;
+  for (int64_t it = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; it < items;
+       it += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t c = static_cast<int32_t>(it / a.W);
+    const int32_t j = a.head[c] + static_cast<int32_t>(it % a.W);
+    if (j < a.count[c]) a.win[it] = make_entry(a, M, static_cast<int32_t>(a.perm[a.seg_off[c] + j]), a.weight[c]);
+  }
 }
 
 __device__ __forceinline__ Cand cand_of(const ClientWork& cw, int32_t c) {
@@ -550,11 +622,6 @@ __device__ __forceinline__ int32_t process_pick(const SelectArgs& a, const Model
       a.ev_row[k] = e.row;
       a.ev_kind[k] = 2;
       a.ev_client[k] = c;
-      a.ev_pred[k] = e.pred;
-      a.ev_ufc[k] = 0.0;
-      a.ev_rfc[k] = 0.0;
-      a.ev_vtc[k] = 0.0;
-      a.ev_wait[k] = 0.0;
     }
     S.n_rej++;
     cw.pos[c] = j + 1;
@@ -596,11 +663,6 @@ __device__ __forceinline__ int32_t process_pick(const SelectArgs& a, const Model
     a.ev_row[k] = e.row;
     a.ev_kind[k] = 1;
     a.ev_client[k] = c;
-    a.ev_pred[k] = e.pred;
-    a.ev_ufc[k] = e.ufc_inc;
-    a.ev_rfc[k] = e.rfc_inc;
-    a.ev_vtc[k] = vtc;
-    a.ev_wait[k] = __dsub_rn(a.now, from_ordered_bits(e.abits));
   }
   S.n_adm++;
   cw.pos[c] = j + 1;
@@ -688,20 +750,655 @@ __device__ __forceinline__ void group_maxima(const ClientWork& cw, int32_t C, in
   named_sync(1, nthr);
 }
 
+// ---- speculative batch selection ---------------------------------------------------------
+// With the maxima fixed, every client's key only grows along its FIFO (increments >= 0, IEEE
+// rounding monotone), so the greedy argmin over heads is a merge of sorted per-client streams,
+// i.e. a sort.  A batch generates each client's next D keys under the current
+// maxima, sorts the C*D tuples, and accepts the longest prefix whose sequential semantics are
+// unaffected: it stops at the first admission that would move a maximum (kept), a max holder
+// leaving the backlog (kept), a client whose lookahead ran out (kept), or the first request
+// that does not fit (the step ends, or under backfill its client is skipped).
+enum : uint32_t { kFlAlone = 1, kFlMaxChg = 2, kFlHolder = 4, kFlExh = 8 };
+
+// (key, arrival, client rank, lookahead index): the index makes equal tuples of one client
+// keep their FIFO order, so the (non-stable) sort reproduces repeated picks of one head.
+__device__ __forceinline__ bool item_better(const BatchItem& x, const BatchItem& y) {
+  const uint32_t xi = x.meta & 0xffffffu, yi = y.meta & 0xffffffu;
+  const bool lt =
+      (x.k < y.k) | ((x.k == y.k) & ((x.a < y.a) | ((x.a == y.a) & ((x.o < y.o) | ((x.o == y.o) & (xi < yi))))));
+  return (x.o != 0xffffffffu) & ((y.o == 0xffffffffu) | lt);
+}
+
+__device__ __forceinline__ double vtc_inc(const Policy& P, const WinEntry& e, double w) {
+  if (P.kind != kVtc) return 0.0;  // scheduler.cpp:169-181
+  return P.vtc_use_prediction
+             ? __dmul_rn(w, __dadd_rn(static_cast<double>(e.in), __dmul_rn(P.ow, static_cast<double>(e.pred))))
+             : __dmul_rn(w, static_cast<double>(e.in));
+}
+
+// Max over backlogged clients (scheduler.cpp:40-48) by the whole CTA.
+__device__ void cta_maxima(const ClientWork& cw, int32_t C, SelShared& S) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  double mu = 0.0, mr = 0.0;
+  for (int32_t c = tid; c < C; c += blockDim.x) {
+    if (!(cw.flags[c] & kBacklogged)) continue;
+    if (mu < cw.ufc[c]) mu = cw.ufc[c];
+    if (mr < cw.rfc[c]) mr = cw.rfc[c];
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const double ou = __shfl_xor_sync(0xffffffffu, mu, o), orr = __shfl_xor_sync(0xffffffffu, mr, o);
+    if (mu < ou) mu = ou;
+    if (mr < orr) mr = orr;
+  }
+  if (lane == 0) {
+    S.red_u[warp] = mu;
+    S.red_r[warp] = mr;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double u = 0.0, r = 0.0;
+    for (int w = 0; w < nw; ++w) {
+      if (u < S.red_u[w]) u = S.red_u[w];
+      if (r < S.red_r[w]) r = S.red_r[w];
+    }
+    S.max_u = u;
+    S.max_r = r;
+  }
+  __syncthreads();
+}
+
+enum : int32_t { kBatchDone = 1, kBatchNeedMax = 2 };
+
+struct BatchScratch {
+  BatchItem* items;  // [Tn]
+  uint8_t* acc;      // [Tn] 0 = not accepted, 1 = admitted, 2 = rejected
+  int32_t* cnsm;     // [C] entries consumed this batch
+  int32_t* evx;      // [Tn] event index of accepted items
+};
+
+// One batch by the whole CTA.  Returns kBatchDone / kBatchNeedMax; *accepted = events emitted.
+__device__ int32_t batch_phase(const SelectArgs& a, const WinEntry* win, const ClientWork& cw, SelShared& S,
+                               const BatchScratch& B, int32_t* accepted) {
+  const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  const int32_t C = a.C, D = a.D, Tn = a.Tn, W = a.W;
+  const Policy& P = a.pol;
+  const bool maxmode = P.kind == kEquinox && P.norm_mode == 0;
+  const double mu = S.max_u, mr = S.max_r;
+  long long c0 = clock64();
+  // 1. per-client key streams under the current maxima
+  for (int32_t c = tid; c < C; c += NT) {
+    B.cnsm[c] = 0;
+    int32_t d = 0;
+    if (cw.pos[c] < cw.end[c] && !(cw.flags[c] & kSkipped)) {
+      double u = cw.ufc[c], r = cw.rfc[c], k = cw.cnt[c];
+      const int32_t pos = cw.pos[c], k0 = pos - cw.pos0[c], end = cw.end[c];
+      const uint32_t o = cw.order[c];
+      for (; d < D; ++d) {
+        const int32_t j = pos + d, kk = k0 + d;
+        if (j >= end || kk >= W) break;
+        const WinEntry e = win[static_cast<int64_t>(c) * W + kk];
+        const uint64_t key = ordered_bits(hf_key(P, u, r, mu, mr, k));
+        uint32_t fl = 0;
+        double nu = u, nr = r, nk = k;
+        if (e.alone) {
+          fl |= kFlAlone;
+          nu = __dadd_rn(u, e.ufc_inc);
+          nr = __dadd_rn(r, e.rfc_inc);
+          nk = (P.kind == kVtc) ? __dadd_rn(k, vtc_inc(P, e, cw.w[c])) : k;
+          if (maxmode && (mu < nu || mr < nr)) fl |= kFlMaxChg;
+        }
+        if (j + 1 == end) {
+          if (maxmode && (u == mu || r == mr)) fl |= kFlHolder;  // holder leaves the backlog
+        } else if (d + 1 == D || kk + 1 >= W) {
+          fl |= kFlExh;  // next entry of this client not generated: later items unordered
+        }
+        B.items[c * D + d] = BatchItem{key, e.abits, o, static_cast<uint32_t>(c * D + d) | (fl << 24)};
+        u = nu;
+        r = nr;
+        k = nk;
+      }
+    }
+    for (; d < D; ++d) B.items[c * D + d] = BatchItem{~0ull, ~0ull, 0xffffffffu, 0u};
+  }
+  for (int32_t i = C * D + tid; i < Tn; i += NT) B.items[i] = BatchItem{~0ull, ~0ull, 0xffffffffu, 0u};
+  for (int32_t i = tid; i < Tn; i += NT) B.acc[i] = 0;
+  __syncthreads();
+  long long c1 = clock64();
+  // 2. bitonic sort of the Tn tuples
+  for (int32_t kk = 2; kk <= Tn; kk <<= 1) {
+    for (int32_t j = kk >> 1; j > 0; j >>= 1) {
+      for (int32_t i = tid; i < Tn; i += NT) {
+        const int32_t ixj = i ^ j;
+        if (ixj > i) {
+          const BatchItem x = B.items[i], y = B.items[ixj];
+          const bool up = (i & kk) == 0;
+          if (up ? item_better(y, x) : item_better(x, y)) {
+            B.items[i] = y;
+            B.items[ixj] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  long long c2 = clock64();
+  // 3. verify the sequential semantics (warp 0, 32 items per step)
+  __shared__ int32_t s_end, s_flags;
+  if (warp == 0) {
+    int32_t carry_a = 0, flags = 0, base = 0;
+    int64_t carry_r = 0;
+    const int32_t members0 = S.members;
+    const int64_t reserved0 = S.reserved;
+    for (;;) {
+      const int32_t p = base + lane;
+      const BatchItem it = p < Tn ? B.items[p] : BatchItem{~0ull, ~0ull, 0xffffffffu, 0u};
+      const bool valid = it.o != 0xffffffffu;
+      if (!__any_sync(0xffffffffu, valid)) {  // every generated item consumed without a cut
+        if (lane == 0) {
+          s_end = min(base, Tn);
+          s_flags = flags | kBatchDone;
+        }
+        break;
+      }
+      const uint32_t idx = it.meta & 0xffffffu, fl = it.meta >> 24;
+      const int32_t c = valid ? static_cast<int32_t>(idx / D) : 0, d = valid ? static_cast<int32_t>(idx % D) : 0;
+      const bool live = valid && !(cw.flags[c] & kSkipped);
+      const bool alone = live && (fl & kFlAlone);
+      int64_t res = 0;
+      if (alone) {
+        const WinEntry& e = win[static_cast<int64_t>(c) * W + (cw.pos[c] - cw.pos0[c]) + d];
+        res = static_cast<int64_t>(e.in) + e.pred;
+      }
+      int32_t ax = alone ? 1 : 0;
+      int64_t rx = res;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {  // inclusive scans
+        const int32_t t1 = __shfl_up_sync(0xffffffffu, ax, o);
+        const int64_t t2 = __shfl_up_sync(0xffffffffu, rx, o);
+        if (lane >= o) {
+          ax += t1;
+          rx += t2;
+        }
+      }
+      const int32_t a_ex = ax - (alone ? 1 : 0);
+      const int64_t r_ex = rx - res;
+      const bool fits = (members0 + carry_a + a_ex + 1 <= P.max_batch) && (reserved0 + carry_r + r_ex + res <= a.tmax);
+      const bool fail = alone && !fits;
+      const bool cut = live && ((fl & (kFlHolder | kFlExh)) || (alone && fits && (fl & kFlMaxChg)));
+      const unsigned fm = __ballot_sync(0xffffffffu, fail), cm = __ballot_sync(0xffffffffu, cut);
+      const int ff = fm ? __ffs(fm) - 1 : 32, fc = cm ? __ffs(cm) - 1 : 32;
+      const int stop = ff <= fc ? ff : fc + 1;  // lanes [0, stop) are accepted if live
+      if (lane < stop && live) B.acc[p] = alone ? 1 : 2;
+      const int32_t a_tot = __shfl_sync(0xffffffffu, ax, stop > 0 ? stop - 1 : 0);
+      const int64_t r_tot = __shfl_sync(0xffffffffu, rx, stop > 0 ? stop - 1 : 0);
+      if (ff < 32 && ff <= fc) {
+        if (!P.backfill) {  // engine.cpp:239: the step ends at the first head that does not fit
+          if (lane == 0) {
+            s_end = base + ff;
+            s_flags = flags | kBatchDone;
+          }
+          break;
+        }
+        if (lane == ff) cw.flags[c] |= kSkipped;  // engine.cpp:236-238
+        __syncwarp();
+        if (stop > 0) {
+          carry_a += a_tot;
+          carry_r += r_tot;
+        }
+        base += ff + 1;
+        continue;
+      }
+      if (fc < 32) {
+        const uint32_t cfl = __shfl_sync(0xffffffffu, fl, fc);
+        const bool cadm = __shfl_sync(0xffffffffu, alone ? 1 : 0, fc);
+        if ((cfl & kFlHolder) || (cadm && (cfl & kFlMaxChg))) flags |= kBatchNeedMax;
+        if (lane == 0) {
+          s_end = base + fc + 1;
+          s_flags = flags;
+        }
+        break;
+      }
+      carry_a += a_tot;
+      carry_r += r_tot;
+      base += 32;
+    }
+  }
+  __syncthreads();
+  long long c3 = clock64();
+  const int32_t end_pos = s_end, bflags = s_flags;
+  // 4. commit: event slots (exclusive scan of accepted), ledger per client, batch counters
+  __shared__ uint32_t warp_buf[32];
+  const int32_t per = (end_pos + NT - 1) / NT;
+  const int32_t p0 = min(end_pos, per * tid), p1 = min(end_pos, p0 + per);
+  uint32_t cnt = 0;
+  for (int32_t q = p0; q < p1; ++q) cnt += B.acc[q] ? 1u : 0u;
+  uint32_t run;
+  const uint32_t total = block_exclusive_scan(cnt, &run, warp_buf);
+  const int64_t ev0 = S.n_ev;
+  for (int32_t q = p0; q < p1; ++q) {
+    const uint8_t kind = B.acc[q];
+    if (!kind) continue;
+    const uint32_t idx = B.items[q].meta & 0xffffffu;
+    const int32_t c = static_cast<int32_t>(idx / D), d = static_cast<int32_t>(idx % D);
+#ifdef EQX_DEBUG
+    if (c >= C || (cw.pos[c] - cw.pos0[c]) + d >= W)
+      printf("EQX_DEBUG commit q=%d end=%d idx=%u c=%d d=%d pos=%d pos0=%d W=%d meta=%x o=%u\n", q, end_pos, idx, c, d,
+             cw.pos[c], cw.pos0[c], W, B.items[q].meta, B.items[q].o);
+#endif
+    const WinEntry& e = win[static_cast<int64_t>(c) * W + (cw.pos[c] - cw.pos0[c]) + d];
+    const int64_t k = ev0 + run++;
+    if (k < a.ev_cap) {
+      a.ev_row[k] = e.row;
+      a.ev_kind[k] = kind;
+      a.ev_client[k] = c;
+    }
+    atomicMax(&B.cnsm[c], d + 1);
+  }
+  __syncthreads();
+  int32_t nadm = 0, nrej = 0;
+  int64_t res_sum = 0, pre_sum = 0;
+  for (int32_t c = tid; c < C; c += NT) {
+    const int32_t n = B.cnsm[c];
+    if (!n) continue;
+    double u = cw.ufc[c], r = cw.rfc[c], k = cw.cnt[c];
+    const int32_t kb = cw.pos[c] - cw.pos0[c];
+    for (int32_t d = 0; d < n; ++d) {  // the same sequential adds as the stream generation
+      const WinEntry& e = win[static_cast<int64_t>(c) * W + kb + d];
+      if (e.alone) {
+        u = __dadd_rn(u, e.ufc_inc);
+        r = __dadd_rn(r, e.rfc_inc);
+        if (P.kind == kVtc) k = __dadd_rn(k, vtc_inc(P, e, cw.w[c]));
+        ++nadm;
+        res_sum += static_cast<int64_t>(e.in) + e.pred;
+        pre_sum += e.in;
+        cw.adm[c] += 1;
+      } else {
+        ++nrej;
+      }
+    }
+    cw.ufc[c] = u;
+    cw.rfc[c] = r;
+    cw.cnt[c] = k;
+    cw.pos[c] += n;
+    if (cw.pos[c] == cw.end[c]) cw.flags[c] &= ~kBacklogged;
+  }
+  nadm = __reduce_add_sync(0xffffffffu, nadm);
+  nrej = __reduce_add_sync(0xffffffffu, nrej);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    res_sum += __shfl_xor_sync(0xffffffffu, res_sum, o);
+    pre_sum += __shfl_xor_sync(0xffffffffu, pre_sum, o);
+  }
+  __syncthreads();  // everyone has read S.n_ev before it moves
+  if (lane == 0 && (nadm | nrej)) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(&S.n_adm), static_cast<unsigned long long>(nadm));
+    atomicAdd(reinterpret_cast<unsigned long long*>(&S.n_rej), static_cast<unsigned long long>(nrej));
+    atomicAdd(&S.members, nadm);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&S.reserved), static_cast<unsigned long long>(res_sum));
+    atomicAdd(reinterpret_cast<unsigned long long*>(&S.prefill), static_cast<unsigned long long>(pre_sum));
+  }
+  if (tid == 0) S.n_ev += total;
+  __syncthreads();
+  if (tid == 0) {
+    const long long c4 = clock64();
+    a.st->t[8] += c1 - c0;
+    a.st->t[9] += c2 - c1;
+    a.st->t[10] += c3 - c2;
+    a.st->t[11] += c4 - c3;
+  }
+  *accepted = static_cast<int32_t>(total);
+  return bflags;
+}
+
+// Sequential picks (the exact admit_requests loop) for up to max_picks picks by the first
+// a.sel_threads threads; the others wait at the CTA barrier that follows.
+__device__ void seq_phase(const SelectArgs& a, const ModelTables& M, const WinEntry* win, const ClientWork& cw,
+                          SelShared& S, int32_t max_picks) {
+  const int32_t C = a.C;
+  const int tid = threadIdx.x, nthr = a.sel_threads;
+  if (tid >= nthr) return;
+  const Policy& P = a.pol;
+  const int lane = tid & 31, warp = tid >> 5, nw = nthr >> 5;
+  for (int32_t c = tid; c < C; c += nthr)
+    cw.ab[c] = cw.pos[c] < cw.end[c] ? get_entry(a, M, win, cw, c, cw.pos[c]).abits : 0ull;
+  Cand local = recompute_owned(P, cw, C, tid, nthr, S.max_u, S.max_r);
+  named_sync(1, nthr);
+  int32_t picks = 0;
+  long long cy_arg = 0, cy_proc = 0, cy_tail = 0, t_a = clock64();
+  for (;;) {
+    if (picks++ >= max_picks) break;
+    Cand v = warp_argmin(local);
+    if (nw > 1) {  // every warp reduces the warp winners redundantly: one barrier per pick
+      if (lane == 0) S.wbest[warp] = v;
+      named_sync(1, nthr);
+      v = warp_argmin(lane < nw ? S.wbest[lane] : no_cand());
+    }
+    if (v.o == 0xffffffffu) {  // no candidates (engine.cpp:217)
+      if (tid == 0) S.flags = kDone;
+      break;
+    }
+    const int32_t c = cw.by_order[v.o];
+    const int owner = c % nthr;
+    int32_t f = 0;
+    const long long t_b = clock64();
+    if (tid == owner) f = process_pick(a, M, win, cw, S, c);
+    if (nw == 1) {
+      f = __shfl_sync(0xffffffffu, f, owner);
+      __syncwarp();
+      const long long t_c = clock64();
+      cy_arg += t_b - t_a;
+      cy_proc += t_c - t_b;
+      t_a = t_c;
+    } else {
+      if (tid == owner) S.flags = f;
+      named_sync(1, nthr);
+      f = S.flags;
+    }
+    if (f & kDone) {
+      if (tid == 0) S.flags = kDone;
+      break;
+    }
+    if (f & kDirty) {
+      if (f & kNeedMax) group_maxima(cw, C, tid, nthr, S);
+      local = recompute_owned(P, cw, C, tid, nthr, S.max_u, S.max_r);
+    } else if (tid == owner) {
+      local = rescan_owned(cw, C, tid, nthr);
+    }
+    if (nw > 1) named_sync(1, nthr);
+    if (nw == 1) {
+      const long long t_d = clock64();
+      cy_tail += t_d - t_a;
+      t_a = t_d;
+    }
+  }
+  if (tid == 0) {
+    a.st->t[12] += cy_arg;
+    a.st->t[13] += cy_proc;
+    a.st->t[14] += cy_tail;
+    a.st->t[15] += picks;
+  }
+}
+
+// ---- register-resident sequential picks ---------------------------------------------------
+// Every selection thread owns K client slots in registers.  Per pick: slot-local best, a warp
+// argmin (redux), for several warps one barrier on double-buffered per-warp winners; then
+// every thread evaluates the pick *uniformly* (replicated batch counters and maxima), so there
+// is no divergence and no dependent memory chain; only the owner writes its slot registers.
+struct WarpWin {
+  uint64_t k, a;
+  uint32_t o;
+  int32_t c, pos, pos0, end, pad;
+  double u, r, cnt;
+};
+
+template <int K>
+__device__ void seq_reg_phase(const SelectArgs& a, const ModelTables& M, const WinEntry* win, const ClientWork& cw,
+                              SelShared& S, int32_t max_picks) {
+  const int nthr = a.sel_threads, tid = threadIdx.x;
+  if (tid >= nthr) return;
+  __shared__ WarpWin s_ww[2][kSelectMaxThreads / 32];
+  __shared__ double s_mx[2][kSelectMaxThreads / 32][2];
+  const int lane = tid & 31, warp = tid >> 5, G = nthr >> 5;
+  const int32_t C = a.C, W = a.W;
+  const Policy P = a.pol;
+  const bool maxmode = P.kind == kEquinox && P.norm_mode == 0;
+  const int64_t tmax = a.tmax;
+  double su[K], sr[K], sk[K];
+  uint64_t skb[K], sab[K];
+  int32_t spos[K], send[K], spos0[K], sfl[K], sadm[K];
+  uint32_t so[K];
+#pragma unroll
+  for (int s = 0; s < K; ++s) {
+    const int32_t c = tid + s * nthr;
+    if (c < C) {
+      su[s] = cw.ufc[c];
+      sr[s] = cw.rfc[c];
+      sk[s] = cw.cnt[c];
+      spos[s] = cw.pos[c];
+      send[s] = cw.end[c];
+      spos0[s] = cw.pos0[c];
+      sfl[s] = cw.flags[c];
+      sadm[s] = cw.adm[c];
+      so[s] = cw.order[c];
+    } else {
+      su[s] = sr[s] = sk[s] = 0.0;
+      spos[s] = send[s] = spos0[s] = 0;
+      sfl[s] = kSkipped;
+      sadm[s] = 0;
+      so[s] = 0xffffffffu;
+    }
+  }
+  int32_t members = S.members;
+  int64_t reserved = S.reserved, n_ev = S.n_ev, n_adm = S.n_adm, n_rej = S.n_rej, prefill = S.prefill;
+  double mu = S.max_u, mr = S.max_r;
+  auto head_abits = [&](int32_t c, int32_t j, int32_t pos0) -> uint64_t {
+    const int32_t k = j - pos0;
+    return k < W ? win[static_cast<int64_t>(c) * W + k].abits : deep_entry(a, M, c, j, cw.w[c]).abits;
+  };
+  auto recompute = [&]() {
+#pragma unroll
+    for (int s = 0; s < K; ++s) {
+      const int32_t c = tid + s * nthr;
+      if (spos[s] < send[s] && !(sfl[s] & kSkipped)) {
+        skb[s] = ordered_bits(hf_key(P, su[s], sr[s], mu, mr, sk[s]));
+        sab[s] = head_abits(c, spos[s], spos0[s]);
+      }
+    }
+  };
+  recompute();
+  int parity = 0;
+  bool done = false;
+  for (int32_t pick = 0; pick < max_picks; ++pick) {
+    // slot-local best
+    Cand best = no_cand();
+    int bs = 0;
+#pragma unroll
+    for (int s = 0; s < K; ++s) {
+      if (spos[s] < send[s] && !(sfl[s] & kSkipped)) {
+        const Cand v{skb[s], sab[s], so[s]};
+        if (better(v, best)) {
+          best = v;
+          bs = s;
+        }
+      }
+    }
+    const int src = warp_argmin_lane(best);
+    WarpWin w;
+    {  // the source lane publishes its winning slot's state
+      double u = 0.0, r = 0.0, cn = 0.0;
+      int32_t pos = 0, pos0 = 0, end = 0;
+#pragma unroll
+      for (int s = 0; s < K; ++s)
+        if (s == bs) {
+          u = su[s];
+          r = sr[s];
+          cn = sk[s];
+          pos = spos[s];
+          pos0 = spos0[s];
+          end = send[s];
+        }
+      const int32_t cc = tid + bs * nthr;
+      if (G == 1) {
+        w.k = __shfl_sync(0xffffffffu, best.k, src);
+        w.a = __shfl_sync(0xffffffffu, best.a, src);
+        w.o = __shfl_sync(0xffffffffu, best.o, src);
+        w.c = __shfl_sync(0xffffffffu, cc, src);
+        w.pos = __shfl_sync(0xffffffffu, pos, src);
+        w.pos0 = __shfl_sync(0xffffffffu, pos0, src);
+        w.end = __shfl_sync(0xffffffffu, end, src);
+        w.u = __shfl_sync(0xffffffffu, u, src);
+        w.r = __shfl_sync(0xffffffffu, r, src);
+        w.cnt = __shfl_sync(0xffffffffu, cn, src);
+      } else {
+        if (lane == src) s_ww[parity][warp] = WarpWin{best.k, best.a, best.o, cc, pos, pos0, end, 0, u, r, cn};
+        named_sync(1, nthr);
+        const WarpWin x = lane < G ? s_ww[parity][lane] : WarpWin{~0ull, ~0ull, 0xffffffffu, 0, 0, 0, 0, 0, 0.0, 0.0, 0.0};
+        const int wl = warp_argmin_lane(Cand{x.k, x.a, x.o});
+        w = s_ww[parity][wl < G ? wl : 0];
+        if (wl >= G) w.o = 0xffffffffu;
+        parity ^= 1;
+      }
+    }
+    if (w.o == 0xffffffffu) {  // no candidates (engine.cpp:217)
+      done = true;
+      break;
+    }
+    // ---- uniform evaluation of the pick (engine.cpp:216-268) ----
+    const int32_t c = w.c, j = w.pos;
+    const WinEntry e = (j - w.pos0 < W) ? win[static_cast<int64_t>(c) * W + (j - w.pos0)] : deep_entry(a, M, c, j, cw.w[c]);
+    const bool owner = (c % nthr) == tid;
+    const int os = c / nthr;  // owner's slot
+    bool dirty = false, needmax = false, skip = false;
+    double nu = w.u, nr = w.r, ncn = w.cnt;
+    int32_t kind;
+    if (!e.alone) {
+      kind = 2;  // Rejected, pop_head, no counter change
+      ++n_rej;
+    } else if (!((members + 1 <= P.max_batch) && (reserved + e.in + e.pred <= tmax))) {
+      if (!P.backfill) {
+        done = true;
+        break;
+      }
+      kind = 0;
+      skip = true;
+    } else {
+      kind = 1;
+      members += 1;
+      reserved += static_cast<int64_t>(e.in) + e.pred;
+      prefill += e.in;
+      ++n_adm;
+      nu = __dadd_rn(w.u, e.ufc_inc);
+      nr = __dadd_rn(w.r, e.rfc_inc);
+      if (P.kind == kVtc) ncn = __dadd_rn(w.cnt, vtc_inc(P, e, cw.w[c]));
+    }
+    uint64_t nkb = 0, nab = 0;
+    const bool leaving = kind != 0 && j + 1 == w.end;
+    if (kind != 0) {
+      if (lane == 0 && warp == 0 && n_ev < a.ev_cap) {
+        a.ev_row[n_ev] = e.row;
+        a.ev_kind[n_ev] = kind;
+        a.ev_client[n_ev] = c;
+      }
+      ++n_ev;
+      if (leaving) {
+        if (maxmode && (w.u == mu || w.r == mr)) dirty = needmax = true;
+      } else {
+        nab = head_abits(c, j + 1, w.pos0);
+        if (kind == 1 && maxmode) {
+          if (mu < nu) {
+            mu = nu;
+            dirty = true;
+          }
+          if (mr < nr) {
+            mr = nr;
+            dirty = true;
+          }
+        }
+        if (!dirty && kind == 1) nkb = ordered_bits(hf_key(P, nu, nr, mu, mr, ncn));
+      }
+    }
+    if (owner) {
+#pragma unroll
+      for (int s = 0; s < K; ++s)
+        if (s == os) {
+          if (skip) {
+            sfl[s] |= kSkipped;
+          } else {
+            spos[s] = j + 1;
+            if (leaving) sfl[s] &= ~kBacklogged;
+            else sab[s] = nab;
+            if (kind == 1) {
+              su[s] = nu;
+              sr[s] = nr;
+              sk[s] = ncn;
+              sadm[s] += 1;
+              if (!leaving && !dirty) skb[s] = nkb;
+            }
+          }
+        }
+    }
+    if (needmax) {  // max over backlogged clients (scheduler.cpp:40-48)
+      double xu = 0.0, xr = 0.0;
+#pragma unroll
+      for (int s = 0; s < K; ++s)
+        if (sfl[s] & kBacklogged) {
+          if (xu < su[s]) xu = su[s];
+          if (xr < sr[s]) xr = sr[s];
+        }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const double ou = __shfl_xor_sync(0xffffffffu, xu, o), orr = __shfl_xor_sync(0xffffffffu, xr, o);
+        if (xu < ou) xu = ou;
+        if (xr < orr) xr = orr;
+      }
+      if (G > 1) {
+        if (lane == 0) {
+          s_mx[parity][warp][0] = xu;
+          s_mx[parity][warp][1] = xr;
+        }
+        named_sync(1, nthr);
+        xu = 0.0;
+        xr = 0.0;
+        for (int g = 0; g < G; ++g) {
+          if (xu < s_mx[parity][g][0]) xu = s_mx[parity][g][0];
+          if (xr < s_mx[parity][g][1]) xr = s_mx[parity][g][1];
+        }
+        parity ^= 1;
+      }
+      mu = xu;
+      mr = xr;
+    }
+    if (dirty) recompute();
+  }
+  // write back slots and counters
+#pragma unroll
+  for (int s = 0; s < K; ++s) {
+    const int32_t c = tid + s * nthr;
+    if (c < C) {
+      cw.ufc[c] = su[s];
+      cw.rfc[c] = sr[s];
+      cw.cnt[c] = sk[s];
+      cw.pos[c] = spos[s];
+      cw.flags[c] = sfl[s];
+      cw.adm[c] = sadm[s];
+    }
+  }
+  if (tid == 0) {
+    S.members = members;
+    S.reserved = reserved;
+    S.n_ev = n_ev;
+    S.n_adm = n_adm;
+    S.n_rej = n_rej;
+    S.prefill = prefill;
+    S.max_u = mu;
+    S.max_r = mr;
+    S.flags = done ? kDone : 0;
+  }
+}
+
 __global__ void __launch_bounds__(kSelectMaxThreads, 1) select_kernel(const SelectArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ SelShared S;
   const int32_t C = a.C;
   const int tid = threadIdx.x, NT = blockDim.x;
   stage_model(a.model, a.model_words, smem);
-  if (tid == 0) a.st->t[0] = global_ns();
-  // ---- carve per-client work arrays + windows ----
+  if (tid == 0) {
+    a.st->t[0] = global_ns();
+    for (int i = 8; i < 16; ++i) a.st->t[i] = 0;
+  }
+  // ---- carve per-client work arrays, batch scratch, windows ----
   unsigned char* p = smem + ((a.model_words * 4 + 15) & ~15);
   unsigned char* g = reinterpret_cast<unsigned char*>(a.cw_global);
+  auto carve = [&](size_t bytes) {
+    unsigned char* r = p;
+    p += (bytes + 15) & ~size_t(15);
+    return r;
+  };
   auto take = [&](size_t bytes) {
-    unsigned char** q = a.cw_in_smem ? &p : &g;
-    unsigned char* r = *q;
-    *q += (bytes + 15) & ~size_t(15);
+    if (a.cw_in_smem) return carve(bytes);
+    unsigned char* r = g;
+    g += (bytes + 15) & ~size_t(15);
     return r;
   };
   ClientWork cw;
@@ -718,12 +1415,18 @@ __global__ void __launch_bounds__(kSelectMaxThreads, 1) select_kernel(const Sele
   cw.flags = reinterpret_cast<int32_t*>(take(4ull * C));
   cw.adm = reinterpret_cast<int32_t*>(take(4ull * C));
   cw.by_order = reinterpret_cast<int32_t*>(take(4ull * C));
+  BatchScratch B;
+  if (a.D > 0) {
+    B.items = reinterpret_cast<BatchItem*>(carve(sizeof(BatchItem) * static_cast<size_t>(a.Tn)));
+    B.acc = reinterpret_cast<uint8_t*>(carve(static_cast<size_t>(a.Tn)));
+    B.cnsm = reinterpret_cast<int32_t*>(carve(4ull * C));
+    B.evx = nullptr;
+  }
   WinEntry* win = reinterpret_cast<WinEntry*>(p);
   __syncthreads();
   const ModelTables& M = *reinterpret_cast<const ModelTables*>(smem);
-  const Policy& P = a.pol;
 
-  // ---- whole CTA: ledger in, head windows (first W queued entries per client) ----
+  // ---- ledger in, head windows (bulk copy of window_kernel's [C][W] entries) ----
   for (int32_t c = tid; c < C; c += NT) {
     cw.ufc[c] = a.ufc[c];
     cw.rfc[c] = a.rfc[c];
@@ -738,77 +1441,63 @@ __global__ void __launch_bounds__(kSelectMaxThreads, 1) select_kernel(const Sele
     cw.flags[c] = a.backlogged[c] ? kBacklogged : 0;
     cw.adm[c] = 0;
   }
-  __syncthreads();
-  const int64_t items = static_cast<int64_t>(C) * a.W;
-  constexpr int kU = 4;  // independent gathers in flight per thread
-  for (int64_t b = tid; b < items; b += kU * NT) {
-    int32_t rows[kU], cs[kU];
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const int64_t it = b + static_cast<int64_t>(u) * NT;
-      rows[u] = -1;
-      cs[u] = 0;
-      if (it < items) {
-        const int32_t c = static_cast<int32_t>(it / a.W);
-        const int32_t j = cw.pos0[c] + static_cast<int32_t>(it % a.W);
-        cs[u] = c;
-        if (j < cw.end[c]) rows[u] = static_cast<int32_t>(a.perm[a.seg_off[c] + j]);
-      }
+  {
+    const int64_t words = static_cast<int64_t>(C) * a.W * (sizeof(WinEntry) / 8);
+    const uint2* src = reinterpret_cast<const uint2*>(a.win_g);
+    uint2* dst = reinterpret_cast<uint2*>(win);
+    int64_t i = tid;
+    for (; i + 3 * NT < words; i += 4 * NT) {  // 4 independent loads in flight per thread
+      const uint2 v0 = __ldcg(src + i), v1 = __ldcg(src + i + NT), v2 = __ldcg(src + i + 2 * NT),
+                  v3 = __ldcg(src + i + 3 * NT);
+      dst[i] = v0;
+      dst[i + NT] = v1;
+      dst[i + 2 * NT] = v2;
+      dst[i + 3 * NT] = v3;
     }
-#pragma unroll
-    for (int u = 0; u < kU; ++u)
-      if (rows[u] >= 0) win[b + static_cast<int64_t>(u) * NT] = entry_of_row(a, M, cs[u], rows[u], cw.w[cs[u]]);
+    for (; i < words; i += NT) dst[i] = __ldcg(src + i);
   }
-  __syncthreads();
   if (tid == 0) {
-    a.st->t[1] = global_ns();
     S.n_ev = S.n_adm = S.n_rej = S.prefill = 0;
     S.members = a.st->members;
     S.reserved = a.st->reserved;
+    S.flags = 0;
   }
-  const int nthr = a.sel_threads;
-  if (tid >= nthr) return;  // spare warps leave; the loop's barriers are named with nthr
-  for (int32_t c = tid; c < C; c += nthr)
-    cw.ab[c] = cw.pos[c] < cw.end[c] ? get_entry(a, M, win, cw, c, cw.pos[c]).abits : 0ull;
-  named_sync(1, nthr);
-  group_maxima(cw, C, tid, nthr, S);
-  Cand local = recompute_owned(P, cw, C, tid, nthr, S.max_u, S.max_r);
-  const int lane = tid & 31, warp = tid >> 5, nw = nthr >> 5;
-  named_sync(1, nthr);
+  __syncthreads();
+  if (tid == 0) a.st->t[1] = global_ns();
+  cta_maxima(cw, C, S);
   if (tid == 0) a.st->t[2] = global_ns();
 
+  // ---- batches; short batches (maxima moving every pick) fall back to sequential picks ----
+  unsigned long long nb = 0, ns = 0;
   for (;;) {
-    Cand v = warp_argmin(local);
-    if (nw > 1) {  // every warp reduces the warp winners redundantly: one barrier per pick
-      if (lane == 0) S.wbest[warp] = v;
-      named_sync(1, nthr);
-      v = warp_argmin(lane < nw ? S.wbest[lane] : no_cand());
+    if (a.D > 0) {
+      int32_t acc = 0;
+      const int32_t bf = batch_phase(a, win, cw, S, B, &acc);
+      ++nb;
+      if (bf & kBatchDone) break;
+      if (bf & kBatchNeedMax) cta_maxima(cw, C, S);
+      if (acc >= 4) continue;
     }
-    if (v.o == 0xffffffffu) break;  // no candidates (engine.cpp:217)
-    const int32_t c = cw.by_order[v.o];
-    const int owner = c % nthr;
-    int32_t f = 0;
-    if (tid == owner) f = process_pick(a, M, win, cw, S, c);
-    if (nw == 1) {
-      f = __shfl_sync(0xffffffffu, f, owner);
-      __syncwarp();
-    } else {
-      if (tid == owner) S.flags = f;
-      named_sync(1, nthr);
-      f = S.flags;
+    const int32_t picks = a.D > 0 ? 8 : 0x7fffffff;
+    switch (a.K) {  // register-resident slots per thread (selection threads = a.sel_threads)
+      case 1: seq_reg_phase<1>(a, M, win, cw, S, picks); break;
+      case 2: seq_reg_phase<2>(a, M, win, cw, S, picks); break;
+      case 4: seq_reg_phase<4>(a, M, win, cw, S, picks); break;
+      case 8: seq_reg_phase<8>(a, M, win, cw, S, picks); break;
+      default: seq_phase(a, M, win, cw, S, picks); break;
     }
-    if (f & kDone) break;
-    if (f & kDirty) {
-      if (f & kNeedMax) group_maxima(cw, C, tid, nthr, S);
-      local = recompute_owned(P, cw, C, tid, nthr, S.max_u, S.max_r);
-    } else if (tid == owner) {
-      local = rescan_owned(cw, C, tid, nthr);
-    }
+    ++ns;
+    __syncthreads();
+    if (S.flags & kDone) break;
+    cta_maxima(cw, C, S);
   }
-  named_sync(1, nthr);
-  if (tid == 0) a.st->t[3] = global_ns();
+  if (tid == 0) {
+    a.st->t[3] = global_ns();
+    a.st->t[6] = nb;
+    a.st->t[7] = ns;
+  }
   // ---- write back ledger, heads, batch, summary ----
-  for (int32_t c = tid; c < C; c += nthr) {
+  for (int32_t c = tid; c < C; c += NT) {
     a.ufc[c] = cw.ufc[c];
     a.rfc[c] = cw.rfc[c];
     a.counter[c] = cw.cnt[c];
@@ -823,6 +1512,31 @@ __global__ void __launch_bounds__(kSelectMaxThreads, 1) select_kernel(const Sele
     a.st->n_admitted = S.n_adm;
     a.st->n_rejected = S.n_rej;
     a.st->new_prefill = S.prefill;
+  }
+}
+
+// Event payloads (scheduler.hpp:131-138 PendingContribution) from the per-request scores the
+// scoring kernel wrote: predicted tokens, ufc/rfc increments, the VTC charge and wait_s.
+__global__ void event_fill_kernel(const EventFillArgs a) {
+  const int64_t n = *a.n_events;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n && i < a.ev_cap;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t row = a.ev_row[i];
+    const bool adm = a.ev_kind[i] == 1;
+    const int32_t pred = a.pred[row];
+    a.ev_pred[i] = pred;
+    a.ev_ufc[i] = adm ? a.ufc_inc[row] : 0.0;
+    a.ev_rfc[i] = adm ? a.rfc_inc[row] : 0.0;
+    double v = 0.0;
+    if (adm && a.pol.kind == kVtc) {  // scheduler.cpp:169-181
+      const double w = a.weight[a.ev_client[i]];
+      const int32_t in = a.in_tok[row];
+      v = a.pol.vtc_use_prediction
+              ? __dmul_rn(w, __dadd_rn(static_cast<double>(in), __dmul_rn(a.pol.ow, static_cast<double>(pred))))
+              : __dmul_rn(w, static_cast<double>(in));
+    }
+    a.ev_vtc[i] = v;
+    a.ev_wait[i] = adm ? __dsub_rn(a.now, a.arrival[row]) : 0.0;  // engine.cpp:257
   }
 }
 

@@ -8,11 +8,10 @@
 
 namespace eqx {
 
-constexpr int kDrainThreads = 256;   // 8 warps per tile
-constexpr int kTileRows = 2048;      // rows per drain tile (8 warps x 256 rows)
-constexpr int kStageMaxClients = 2048;  // smem-staged (coalesced) rank path up to this many
+constexpr int kDrainThreads = 1024;  // 32 warps per tile
+constexpr int kDrainWarps = kDrainThreads / 32;
 constexpr int kScoreThreads = 256;
-constexpr int kSelectMaxThreads = 512;
+constexpr int kSelectMaxThreads = 256;
 
 // One head-of-queue entry as the selection loop consumes it (40 B, shared memory).
 struct WinEntry {
@@ -25,13 +24,21 @@ struct WinEntry {
   int32_t alone;    // fits_alone(in, pred) (gpu_model.cpp:69-72)
 };
 
+// One (client, lookahead) tuple of a speculative selection batch (24 B, shared memory).
+struct BatchItem {
+  uint64_t k;     // ordered bits of the key
+  uint64_t a;     // ordered bits of the head arrival
+  uint32_t o;     // client_id rank; 0xffffffff = sentinel
+  uint32_t meta;  // (c * D + d) | flags << 24
+};
+
 struct DrainArgs {
   const int32_t* client;
   int32_t n;
   int32_t C;
   int32_t tile_rows;
   int32_t n_tiles;
-  int32_t staged;       // 1: smem-staged coalesced scatter (C <= kStageMaxClients)
+  int32_t staged;       // 1: smem-staged coalesced scatter (when the tile fits in smem)
   uint32_t* hist;       // [C][n_tiles] counts -> exclusive offsets
   int64_t hist_L;
   int32_t* seg_off;     // [C+1]
@@ -46,6 +53,7 @@ struct DrainArgs {
   int32_t* backlogged;
   int32_t counter_lift;
   unsigned int* done;   // [2] last-CTA counters (hist, rank), reset by their last CTA
+  uint16_t* wcnt;       // [n_tiles][kDrainWarps][C] per-warp client counts (hist -> rank)
   DevState* st;
 };
 
@@ -66,7 +74,37 @@ struct ScoreArgs {
   DevState* st;
   const ModelTables* model;
   int32_t model_words;  // uint32 words of ModelTables to stage in smem (header + used LUT)
+  // Direct tables compiled on the host from the same LUT/profile (bit-identical results):
+  //   direct[tag * direct_n + in] = pred | bucket << 16 | fallback << 24  (MoPE/single proxy)
+  //   direct[pred]                = bucket                              (oracle / noisy)
+  // Inputs outside [0, direct_n) take the interval/profile search.
+  const uint32_t* direct;
+  int32_t direct_n;
   int32_t vec_ok;
+  Policy pol;
+  double now;
+};
+
+// Head windows: the first W queued entries of every client, scored once per step by many
+// CTAs (window_kernel) and bulk-loaded into the selection CTA's shared memory.
+struct WindowArgs {
+  const double* arrival;
+  const int32_t* in_tok;
+  const int32_t* true_out;
+  const uint8_t* tag;
+  const int64_t* id;
+  int64_t id_base;
+  const uint32_t* perm;
+  const int32_t* seg_off;
+  const int32_t* count;
+  const int32_t* head;
+  const double* weight;
+  int32_t C;
+  int32_t W;
+  WinEntry* win;         // [C][W]
+  const ModelTables* model;
+  int32_t model_words;
+  int64_t tmax;
   Policy pol;
   double now;
 };
@@ -86,7 +124,11 @@ struct SelectArgs {
   int32_t* head;
   int32_t C;
   int32_t W;             // head-window depth cached in shared memory per client
+  const WinEntry* win_g; // [C][W] windows produced by window_kernel
+  int32_t D;             // batch lookahead per client (0 = sequential picks only)
+  int32_t Tn;            // batch sort size (power of two >= C * D)
   int32_t sel_threads;   // threads in the selection loop (multiple of 32)
+  int32_t K;             // register client slots per selection thread (1/2/4; 0 = smem loop)
   int32_t cw_in_smem;
   void* cw_global;       // per-client work arrays when they do not fit in smem
   // ledger
@@ -115,9 +157,32 @@ struct SelectArgs {
   double now;
 };
 
+struct EventFillArgs {
+  const int64_t* n_events;  // &DevState::n_events
+  int64_t ev_cap;
+  const int32_t* ev_row;
+  const int32_t* ev_kind;
+  const int32_t* ev_client;
+  int32_t* ev_pred;
+  double* ev_ufc;
+  double* ev_rfc;
+  double* ev_vtc;
+  double* ev_wait;
+  const int32_t* pred;
+  const double* ufc_inc;
+  const double* rfc_inc;
+  const double* arrival;
+  const int32_t* in_tok;
+  const double* weight;
+  Policy pol;
+  double now;
+};
+
 __global__ void drain_hist_kernel(DrainArgs a);
+__global__ void event_fill_kernel(EventFillArgs a);
 __global__ void drain_rank_kernel(DrainArgs a);
 __global__ void score_kernel(ScoreArgs a);
+__global__ void window_kernel(WindowArgs a);
 __global__ void select_kernel(SelectArgs a);
 __global__ void gather_ids_kernel(const int32_t* rows, int64_t n, const int64_t* id, int64_t id_base,
                                   int64_t* out);
