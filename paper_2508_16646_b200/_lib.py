@@ -82,6 +82,7 @@ _SIGS = {
     "eqx_step": ([C.c_void_p, C.c_double, C.POINTER(StepSummary)], C.c_int),
     "eqx_copy_events": ([C.c_void_p, C.c_int64, _i64p, _i32p, _i32p, _i32p, _dp, _dp, _dp, _dp], C.c_int),
     "eqx_phase_times": ([C.c_void_p, _dp, C.c_int32], C.c_int),
+    "eqx_kernel_times": ([C.c_void_p, C.POINTER(C.c_float)], C.c_int),
     "eqx_copy_scores": ([C.c_void_p, C.c_int64, _i32p, _u8p, _dp, _dp], C.c_int),
     "eqx_ufc_increment": ([C.c_double, C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_double, C.c_double], C.c_double),
     "eqx_rfc_increment": ([C.c_double, C.c_double, C.c_double], C.c_double),

@@ -101,6 +101,7 @@ struct eqx_ctx {
   bool staged = true;
   cudaStream_t stream2 = nullptr;  // side stream for whole-queue scoring
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_k[6] = {};        // timing: score start/end, select start/end, drain start/end
   DevBuf d_done;                   // last-CTA counters of the drain kernels
   DevBuf d_win;                    // [C][W] head windows
   DevBuf d_wcnt;                   // per-(tile, warp, client) counts of the drain walk
@@ -225,6 +226,7 @@ eqx_status eqx_ctx_create(int32_t device, eqx_ctx** out) {
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming);
+  for (int i = 0; i < 6 && e == cudaSuccess; ++i) e = cudaEventCreate(&ctx->ev_k[i]);
   if (e == cudaSuccess) e = ctx->d_done.ensure(64);
   if (e == cudaSuccess) e = cudaMemset(ctx->d_done.p, 0, 64);
   if (e == cudaSuccess) e = ctx->d_state.ensure(sizeof(DevState));
@@ -270,6 +272,8 @@ void eqx_ctx_destroy(eqx_ctx* ctx) {
   ctx->d_wcnt.release();
   ctx->d_direct.release();
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  for (auto& ev : ctx->ev_k)
+    if (ev) cudaEventDestroy(ev);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->stream2) cudaStreamDestroy(ctx->stream2);
   if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
@@ -878,6 +882,20 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl) {
   a.D = static_cast<int32_t>(D);
   a.Tn = D ? static_cast<int32_t>(pow2(std::max<int64_t>(C * D, 2))) : 0;
   if (D) smem += batch_bytes(D);
+  // key streams of the register loop: up to 16 lookahead items (33 B each) per client, using
+  // at most a third of what is left (the head windows get the rest)
+  int64_t Ds = 0;
+  if (K > 0 && C > 0) {
+    const size_t left_s = ctx->smem_optin - static_smem - smem;
+    Ds = std::min<int64_t>(16, static_cast<int64_t>(left_s / 3 / (33ull * C + 5 * 16)));
+    if (Ds < 1) {
+      Ds = 0;
+      K = 0;  // no room: shared-memory loop
+    }
+    a.K = K;
+  }
+  a.Ds = static_cast<int32_t>(Ds);
+  if (Ds) smem += 4 * ((8ull * C * Ds + 15) & ~15ull) + ((1ull * C * Ds + 15) & ~15ull);
   const size_t left = ctx->smem_optin - static_smem - smem;
   // A client is picked at most max_batch times before the slots run out (+1 for the next
   // head's arrival); deeper heads (rejection streams) are scored on demand from HBM.
@@ -925,16 +943,22 @@ static eqx_status step_enqueue(eqx_ctx* ctx, const StepPlan& pl, bool with_drain
   CUDA_TRY(ctx, cudaMemsetAsync(st + offsetof(DevState, t) + 5 * 8, 0, 8, s));
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fork, s));
   CUDA_TRY(ctx, cudaStreamWaitEvent(s2, ctx->ev_fork, 0));
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[0], s2));
   if (ctx->n > 0)
     score_kernel<<<pl.score_grid, kScoreThreads, pl.score_smem, s2>>>(pl.sc);
   CUDA_TRY(ctx, cudaGetLastError());
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[1], s2));
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_join, s2));
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[4], s));
   if (with_drain) {
     eqx_status e = drain_enqueue(ctx);
     if (e != EQX_OK) return e;
   }
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[5], s));
   window_kernel<<<pl.window_grid, 256, pl.window_smem, s>>>(pl.wi);
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[2], s));
   select_kernel<<<1, pl.select_threads, pl.select_smem, s>>>(pl.se);
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[3], s));
   CUDA_TRY(ctx, cudaGetLastError());
   CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_join, 0));
   EventFillArgs ef;
@@ -1053,6 +1077,16 @@ eqx_status eqx_phase_times(eqx_ctx* ctx, double* out_us, int32_t n) {
   const double base = static_cast<double>(t[0]);
   for (int i = 0; i < n && i < 6; ++i) out_us[i] = (static_cast<double>(t[i]) - base) * 1e-3;
   for (int i = 6; i < n && i < 16; ++i) out_us[i] = static_cast<double>(t[i]);  // counts / cycles
+  return EQX_OK;
+}
+
+eqx_status eqx_kernel_times(eqx_ctx* ctx, float* out_ms) {
+  if (!ctx || !out_ms) return fail(ctx, EQX_ERR_ARG, "eqx_kernel_times: NULL argument");
+  cudaSetDevice(ctx->device);
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  CUDA_TRY(ctx, cudaEventElapsedTime(&out_ms[0], ctx->ev_k[0], ctx->ev_k[1]));  // score_kernel
+  CUDA_TRY(ctx, cudaEventElapsedTime(&out_ms[1], ctx->ev_k[2], ctx->ev_k[3]));  // select_kernel
+  CUDA_TRY(ctx, cudaEventElapsedTime(&out_ms[2], ctx->ev_k[4], ctx->ev_k[5]));  // drain (in-step)
   return EQX_OK;
 }
 

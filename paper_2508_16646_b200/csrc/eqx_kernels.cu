@@ -119,14 +119,23 @@ __global__ void __launch_bounds__(kDrainThreads) drain_hist_kernel(const DrainAr
   const int32_t r1 = min(a.n, r0 + sub);
   uint16_t* my = wc + warp * C;
   bool bad = false;
-  for (int32_t r = r0; r < r1; r += 32) {  // per-warp counts: one writer per (warp, client)
-    const int32_t row = r + lane;
-    const int32_t c = row < r1 ? a.client[row] : -1;
-    const bool ok = static_cast<uint32_t>(c) < static_cast<uint32_t>(C);
-    bad |= row < r1 && !ok;
-    const unsigned peers = __match_any_sync(0xffffffffu, ok ? c : -1);
-    if (ok && lane == __ffs(peers) - 1) my[c] = static_cast<uint16_t>(my[c] + __popc(peers));
-    __syncwarp();
+  for (int32_t rb = r0; rb < r1; rb += 32 * 8) {  // 8 loads in flight per lane, then walk
+    int32_t cv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int32_t row = rb + 32 * u + lane;
+      cv[u] = row < r1 ? a.client[row] : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {  // per-warp counts: one writer per (warp, client)
+      const int32_t row = rb + 32 * u + lane;
+      const int32_t c = cv[u];
+      const bool ok = static_cast<uint32_t>(c) < static_cast<uint32_t>(C);
+      bad |= row < r1 && !ok;
+      const unsigned peers = __match_any_sync(0xffffffffu, ok ? c : -1);
+      if (ok && lane == __ffs(peers) - 1) my[c] = static_cast<uint16_t>(my[c] + __popc(peers));
+      __syncwarp();
+    }
   }
   if (bad) a.st->bad_client = 1;
   __syncthreads();
@@ -333,24 +342,33 @@ __global__ void __launch_bounds__(kDrainThreads) drain_rank_kernel(const DrainAr
     __syncthreads();
     uint32_t* srow = sh + 2 * C + (kDrainWarps / 2) * C;             // [tile_rows]
     uint16_t* scl = reinterpret_cast<uint16_t*>(srow + a.tile_rows);  // [tile_rows]
-    for (int32_t r = r0; r < r1; r += 32) {  // walk 2: slot in the client-sorted tile
-      const int32_t row = r + lane;
-      const int32_t c = row < r1 ? a.client[row] : -1;
-      const unsigned peers = __match_any_sync(0xffffffffu, c);
-      const int leader = __ffs(peers) - 1;
-      uint32_t start = 0;
-      const bool ok = static_cast<uint32_t>(c) < static_cast<uint32_t>(C);
-      if (ok && lane == leader) {
-        start = my[c];
-        my[c] = static_cast<uint16_t>(start + __popc(peers));
+    for (int32_t rb = r0; rb < r1; rb += 32 * 8) {  // walk 2: slot in the client-sorted tile
+      int32_t cv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int32_t row = rb + 32 * u + lane;
+        cv[u] = row < r1 ? a.client[row] : -1;
       }
-      start = __shfl_sync(0xffffffffu, start, leader);
-      if (ok) {
-        const uint32_t slot = toff[c] + start + __popc(peers & lt);
-        srow[slot] = static_cast<uint32_t>(row);
-        scl[slot] = static_cast<uint16_t>(c);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int32_t row = rb + 32 * u + lane;
+        const int32_t c = cv[u];
+        const bool ok = static_cast<uint32_t>(c) < static_cast<uint32_t>(C);
+        const unsigned peers = __match_any_sync(0xffffffffu, ok ? c : -1);
+        const int leader = __ffs(peers) - 1;
+        uint32_t start = 0;
+        if (ok && lane == leader) {
+          start = my[c];
+          my[c] = static_cast<uint16_t>(start + __popc(peers));
+        }
+        start = __shfl_sync(0xffffffffu, start, leader);
+        if (ok) {
+          const uint32_t slot = toff[c] + start + __popc(peers & lt);
+          srow[slot] = static_cast<uint32_t>(row);
+          scl[slot] = static_cast<uint16_t>(c);
+        }
+        __syncwarp();
       }
-      __syncwarp();
     }
     __syncthreads();
     const int32_t rows = t1 - t0;
@@ -1120,37 +1138,50 @@ __device__ void seq_phase(const SelectArgs& a, const ModelTables& M, const WinEn
   }
 }
 
-// ---- register-resident sequential picks ---------------------------------------------------
-// Every selection thread owns K client slots in registers.  Per pick: slot-local best, a warp
-// argmin (redux), for several warps one barrier on double-buffered per-warp winners; then
-// every thread evaluates the pick *uniformly* (replicated batch counters and maxima), so there
-// is no divergence and no dependent memory chain; only the owner writes its slot registers.
+// ---- register-resident sequential picks over precomputed key streams ----------------------
+// Every selection thread owns K client slots in registers.  For each slot the next Ds keys
+// (and the ledger after each of those requests) are generated ahead under the current maxima
+// (the same sequential FP64 adds and divisions as on_admit + holistic_score), so a pick is a
+// warp argmin (redux) plus shared-memory lookups evaluated *uniformly* by every thread
+// (replicated batch counters and maxima, no divergence); only the owner writes its slot.
+// Streams are regenerated when a maximum moves (an admission above it, or a max holder
+// leaving the backlog) and per client when its stream runs out.
 struct WarpWin {
   uint64_t k, a;
   uint32_t o;
-  int32_t c, pos, pos0, end, pad;
-  double u, r, cnt;
+  int32_t c, pos, pos0, end, d;
+};
+
+struct StreamScratch {
+  uint64_t* k;  // [C][Ds] key of lookahead item d
+  double* u;    // [C][Ds] ufc after item d (unchanged when rejected)
+  double* r;
+  double* cn;   // VTC counter after item d
+  uint8_t* fl;  // [C][Ds] kFlAlone | kFlMaxChg | kFlHolder
+  int32_t Ds;
 };
 
 template <int K>
 __device__ void seq_reg_phase(const SelectArgs& a, const ModelTables& M, const WinEntry* win, const ClientWork& cw,
-                              SelShared& S, int32_t max_picks) {
+                              SelShared& S, int32_t max_picks, const StreamScratch& T) {
   const int nthr = a.sel_threads, tid = threadIdx.x;
   if (tid >= nthr) return;
   __shared__ WarpWin s_ww[2][kSelectMaxThreads / 32];
   __shared__ double s_mx[2][kSelectMaxThreads / 32][2];
   const int lane = tid & 31, warp = tid >> 5, G = nthr >> 5;
-  const int32_t C = a.C, W = a.W;
+  const int32_t C = a.C, W = a.W, Ds = T.Ds;
   const Policy P = a.pol;
   const bool maxmode = P.kind == kEquinox && P.norm_mode == 0;
   const int64_t tmax = a.tmax;
   double su[K], sr[K], sk[K];
   uint64_t skb[K], sab[K];
-  int32_t spos[K], send[K], spos0[K], sfl[K], sadm[K];
+  int32_t spos[K], send[K], spos0[K], sfl[K], sadm[K], sd[K], sdl[K];
   uint32_t so[K];
 #pragma unroll
   for (int s = 0; s < K; ++s) {
     const int32_t c = tid + s * nthr;
+    sd[s] = sdl[s] = 0;
+    skb[s] = sab[s] = ~0ull;
     if (c < C) {
       su[s] = cw.ufc[c];
       sr[s] = cw.rfc[c];
@@ -1172,25 +1203,61 @@ __device__ void seq_reg_phase(const SelectArgs& a, const ModelTables& M, const W
   int32_t members = S.members;
   int64_t reserved = S.reserved, n_ev = S.n_ev, n_adm = S.n_adm, n_rej = S.n_rej, prefill = S.prefill;
   double mu = S.max_u, mr = S.max_r;
-  auto head_abits = [&](int32_t c, int32_t j, int32_t pos0) -> uint64_t {
+  auto entry = [&](int32_t c, int32_t j, int32_t pos0) -> WinEntry {
     const int32_t k = j - pos0;
-    return k < W ? win[static_cast<int64_t>(c) * W + k].abits : deep_entry(a, M, c, j, cw.w[c]).abits;
+    return k < W ? win[static_cast<int64_t>(c) * W + k] : deep_entry(a, M, c, j, cw.w[c]);
   };
-  auto recompute = [&]() {
-#pragma unroll
-    for (int s = 0; s < K; ++s) {
-      const int32_t c = tid + s * nthr;
-      if (spos[s] < send[s] && !(sfl[s] & kSkipped)) {
-        skb[s] = ordered_bits(hf_key(P, su[s], sr[s], mu, mr, sk[s]));
-        sab[s] = head_abits(c, spos[s], spos0[s]);
+  // (re)generate the lookahead stream of slot s under the current maxima
+  auto gen = [&](int s, int depth) {
+    const int32_t c = tid + s * nthr;
+    sd[s] = 0;
+    sdl[s] = 0;
+    if (!(spos[s] < send[s]) || (sfl[s] & kSkipped)) return;
+    double u = su[s], r = sr[s], k = sk[s];
+    const int32_t pos = spos[s], end = send[s], pos0 = spos0[s];
+    int d = 0;
+    for (; d < depth; ++d) {
+      const int32_t j = pos + d;
+      if (j >= end) break;
+      const WinEntry e = entry(c, j, pos0);
+      const uint64_t key = ordered_bits(hf_key(P, u, r, mu, mr, k));
+      uint8_t f = 0;
+      double nu = u, nr = r, nk = k;
+      if (e.alone) {
+        f |= kFlAlone;
+        nu = __dadd_rn(u, e.ufc_inc);
+        nr = __dadd_rn(r, e.rfc_inc);
+        if (P.kind == kVtc) nk = __dadd_rn(k, vtc_inc(P, e, cw.w[c]));
       }
+      if (j + 1 == end) {
+        if (maxmode && (u == mu || r == mr)) f |= kFlHolder;  // a max holder leaves the backlog
+      } else if (e.alone && maxmode && (mu < nu || mr < nr)) {
+        f |= kFlMaxChg;  // this admission raises a maximum
+      }
+      const int64_t x = static_cast<int64_t>(c) * Ds + d;
+      T.k[x] = key;
+      T.u[x] = nu;
+      T.r[x] = nr;
+      T.cn[x] = nk;
+      T.fl[x] = f;
+      u = nu;
+      r = nr;
+      k = nk;
+    }
+    sdl[s] = d;
+    if (d > 0) {
+      skb[s] = T.k[static_cast<int64_t>(c) * Ds];
+      sab[s] = entry(c, pos, pos0).abits;
     }
   };
-  recompute();
+  int depth = Ds, since_regen = 1 << 30;
+#pragma unroll
+  for (int s = 0; s < K; ++s) gen(s, depth);
+  __syncwarp();
+  if (G > 1) named_sync(1, nthr);
   int parity = 0;
   bool done = false;
   for (int32_t pick = 0; pick < max_picks; ++pick) {
-    // slot-local best
     Cand best = no_cand();
     int bs = 0;
 #pragma unroll
@@ -1205,35 +1272,28 @@ __device__ void seq_reg_phase(const SelectArgs& a, const ModelTables& M, const W
     }
     const int src = warp_argmin_lane(best);
     WarpWin w;
-    {  // the source lane publishes its winning slot's state
-      double u = 0.0, r = 0.0, cn = 0.0;
-      int32_t pos = 0, pos0 = 0, end = 0;
+    {
+      int32_t pos = 0, pos0 = 0, end = 0, dd = 0;
 #pragma unroll
       for (int s = 0; s < K; ++s)
         if (s == bs) {
-          u = su[s];
-          r = sr[s];
-          cn = sk[s];
           pos = spos[s];
           pos0 = spos0[s];
           end = send[s];
+          dd = sd[s];
         }
       const int32_t cc = tid + bs * nthr;
       if (G == 1) {
-        w.k = __shfl_sync(0xffffffffu, best.k, src);
-        w.a = __shfl_sync(0xffffffffu, best.a, src);
         w.o = __shfl_sync(0xffffffffu, best.o, src);
         w.c = __shfl_sync(0xffffffffu, cc, src);
         w.pos = __shfl_sync(0xffffffffu, pos, src);
         w.pos0 = __shfl_sync(0xffffffffu, pos0, src);
         w.end = __shfl_sync(0xffffffffu, end, src);
-        w.u = __shfl_sync(0xffffffffu, u, src);
-        w.r = __shfl_sync(0xffffffffu, r, src);
-        w.cnt = __shfl_sync(0xffffffffu, cn, src);
+        w.d = __shfl_sync(0xffffffffu, dd, src);
       } else {
-        if (lane == src) s_ww[parity][warp] = WarpWin{best.k, best.a, best.o, cc, pos, pos0, end, 0, u, r, cn};
+        if (lane == src) s_ww[parity][warp] = WarpWin{best.k, best.a, best.o, cc, pos, pos0, end, dd};
         named_sync(1, nthr);
-        const WarpWin x = lane < G ? s_ww[parity][lane] : WarpWin{~0ull, ~0ull, 0xffffffffu, 0, 0, 0, 0, 0, 0.0, 0.0, 0.0};
+        const WarpWin x = lane < G ? s_ww[parity][lane] : WarpWin{~0ull, ~0ull, 0xffffffffu, 0, 0, 0, 0, 0};
         const int wl = warp_argmin_lane(Cand{x.k, x.a, x.o});
         w = s_ww[parity][wl < G ? wl : 0];
         if (wl >= G) w.o = 0xffffffffu;
@@ -1246,11 +1306,11 @@ __device__ void seq_reg_phase(const SelectArgs& a, const ModelTables& M, const W
     }
     // ---- uniform evaluation of the pick (engine.cpp:216-268) ----
     const int32_t c = w.c, j = w.pos;
-    const WinEntry e = (j - w.pos0 < W) ? win[static_cast<int64_t>(c) * W + (j - w.pos0)] : deep_entry(a, M, c, j, cw.w[c]);
+    const int64_t x = static_cast<int64_t>(c) * Ds + w.d;
+    const WinEntry e = entry(c, j, w.pos0);
+    const uint8_t fl = T.fl[x];
     const bool owner = (c % nthr) == tid;
-    const int os = c / nthr;  // owner's slot
-    bool dirty = false, needmax = false, skip = false;
-    double nu = w.u, nr = w.r, ncn = w.cnt;
+    const int os = c / nthr;
     int32_t kind;
     if (!e.alone) {
       kind = 2;  // Rejected, pop_head, no counter change
@@ -1260,20 +1320,18 @@ __device__ void seq_reg_phase(const SelectArgs& a, const ModelTables& M, const W
         done = true;
         break;
       }
-      kind = 0;
-      skip = true;
+      kind = 0;  // skipped for the rest of the step
     } else {
       kind = 1;
       members += 1;
       reserved += static_cast<int64_t>(e.in) + e.pred;
       prefill += e.in;
       ++n_adm;
-      nu = __dadd_rn(w.u, e.ufc_inc);
-      nr = __dadd_rn(w.r, e.rfc_inc);
-      if (P.kind == kVtc) ncn = __dadd_rn(w.cnt, vtc_inc(P, e, cw.w[c]));
     }
-    uint64_t nkb = 0, nab = 0;
     const bool leaving = kind != 0 && j + 1 == w.end;
+    const bool maxchg = kind == 1 && (fl & kFlMaxChg);
+    const bool holder = kind != 0 && (fl & kFlHolder);
+    double nu = 0.0, nr = 0.0;
     if (kind != 0) {
       if (lane == 0 && warp == 0 && n_ev < a.ev_cap) {
         a.ev_row[n_ev] = e.row;
@@ -1281,77 +1339,85 @@ __device__ void seq_reg_phase(const SelectArgs& a, const ModelTables& M, const W
         a.ev_client[n_ev] = c;
       }
       ++n_ev;
-      if (leaving) {
-        if (maxmode && (w.u == mu || w.r == mr)) dirty = needmax = true;
-      } else {
-        nab = head_abits(c, j + 1, w.pos0);
-        if (kind == 1 && maxmode) {
-          if (mu < nu) {
-            mu = nu;
-            dirty = true;
-          }
-          if (mr < nr) {
-            mr = nr;
-            dirty = true;
-          }
-        }
-        if (!dirty && kind == 1) nkb = ordered_bits(hf_key(P, nu, nr, mu, mr, ncn));
-      }
+      nu = T.u[x];
+      nr = T.r[x];
     }
+    bool own_regen = false;
     if (owner) {
 #pragma unroll
       for (int s = 0; s < K; ++s)
         if (s == os) {
-          if (skip) {
+          if (kind == 0) {
             sfl[s] |= kSkipped;
           } else {
             spos[s] = j + 1;
-            if (leaving) sfl[s] &= ~kBacklogged;
-            else sab[s] = nab;
-            if (kind == 1) {
-              su[s] = nu;
-              sr[s] = nr;
-              sk[s] = ncn;
-              sadm[s] += 1;
-              if (!leaving && !dirty) skb[s] = nkb;
+            su[s] = nu;
+            sr[s] = nr;
+            sk[s] = T.cn[x];
+            if (kind == 1) sadm[s] += 1;
+            if (leaving) {
+              sfl[s] &= ~kBacklogged;
+            } else {
+              sd[s] += 1;
+              if (sd[s] < sdl[s]) {
+                skb[s] = T.k[x + 1];
+                sab[s] = entry(c, j + 1, spos0[s]).abits;
+              } else {
+                own_regen = true;
+              }
             }
           }
         }
     }
-    if (needmax) {  // max over backlogged clients (scheduler.cpp:40-48)
-      double xu = 0.0, xr = 0.0;
+    ++since_regen;
+    if (maxchg || holder) {
+      if (maxchg) {  // the new maximum is the admitted client's counter
+        if (mu < nu) mu = nu;
+        if (mr < nr) mr = nr;
+      } else {  // max over backlogged clients (scheduler.cpp:40-48)
+        double xu = 0.0, xr = 0.0;
+#pragma unroll
+        for (int s = 0; s < K; ++s)
+          if (sfl[s] & kBacklogged) {
+            if (xu < su[s]) xu = su[s];
+            if (xr < sr[s]) xr = sr[s];
+          }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          const double ou = __shfl_xor_sync(0xffffffffu, xu, o), orr = __shfl_xor_sync(0xffffffffu, xr, o);
+          if (xu < ou) xu = ou;
+          if (xr < orr) xr = orr;
+        }
+        if (G > 1) {
+          if (lane == 0) {
+            s_mx[parity][warp][0] = xu;
+            s_mx[parity][warp][1] = xr;
+          }
+          named_sync(1, nthr);
+          xu = 0.0;
+          xr = 0.0;
+          for (int g = 0; g < G; ++g) {
+            if (xu < s_mx[parity][g][0]) xu = s_mx[parity][g][0];
+            if (xr < s_mx[parity][g][1]) xr = s_mx[parity][g][1];
+          }
+          parity ^= 1;
+        }
+        mu = xu;
+        mr = xr;
+      }
+      // maxima moving every few picks (cold ledgers): short lookahead; otherwise the full one
+      depth = since_regen < 4 ? 1 : Ds;
+      since_regen = 0;
+#pragma unroll
+      for (int s = 0; s < K; ++s) gen(s, depth);
+    } else if (own_regen) {
 #pragma unroll
       for (int s = 0; s < K; ++s)
-        if (sfl[s] & kBacklogged) {
-          if (xu < su[s]) xu = su[s];
-          if (xr < sr[s]) xr = sr[s];
-        }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        const double ou = __shfl_xor_sync(0xffffffffu, xu, o), orr = __shfl_xor_sync(0xffffffffu, xr, o);
-        if (xu < ou) xu = ou;
-        if (xr < orr) xr = orr;
-      }
-      if (G > 1) {
-        if (lane == 0) {
-          s_mx[parity][warp][0] = xu;
-          s_mx[parity][warp][1] = xr;
-        }
-        named_sync(1, nthr);
-        xu = 0.0;
-        xr = 0.0;
-        for (int g = 0; g < G; ++g) {
-          if (xu < s_mx[parity][g][0]) xu = s_mx[parity][g][0];
-          if (xr < s_mx[parity][g][1]) xr = s_mx[parity][g][1];
-        }
-        parity ^= 1;
-      }
-      mu = xu;
-      mr = xr;
+        if (s == os) gen(s, Ds);
     }
-    if (dirty) recompute();
+    __syncwarp();
+    if (G > 1) named_sync(1, nthr);
   }
-  // write back slots and counters
 #pragma unroll
   for (int s = 0; s < K; ++s) {
     const int32_t c = tid + s * nthr;
@@ -1422,6 +1488,16 @@ __global__ void __launch_bounds__(kSelectMaxThreads, 1) select_kernel(const Sele
     B.cnsm = reinterpret_cast<int32_t*>(carve(4ull * C));
     B.evx = nullptr;
   }
+  StreamScratch T;
+  T.Ds = a.Ds;
+  if (a.Ds > 0) {
+    const size_t items = static_cast<size_t>(C) * a.Ds;
+    T.k = reinterpret_cast<uint64_t*>(carve(8 * items));
+    T.u = reinterpret_cast<double*>(carve(8 * items));
+    T.r = reinterpret_cast<double*>(carve(8 * items));
+    T.cn = reinterpret_cast<double*>(carve(8 * items));
+    T.fl = reinterpret_cast<uint8_t*>(carve(items));
+  }
   WinEntry* win = reinterpret_cast<WinEntry*>(p);
   __syncthreads();
   const ModelTables& M = *reinterpret_cast<const ModelTables*>(smem);
@@ -1480,10 +1556,10 @@ __global__ void __launch_bounds__(kSelectMaxThreads, 1) select_kernel(const Sele
     }
     const int32_t picks = a.D > 0 ? 8 : 0x7fffffff;
     switch (a.K) {  // register-resident slots per thread (selection threads = a.sel_threads)
-      case 1: seq_reg_phase<1>(a, M, win, cw, S, picks); break;
-      case 2: seq_reg_phase<2>(a, M, win, cw, S, picks); break;
-      case 4: seq_reg_phase<4>(a, M, win, cw, S, picks); break;
-      case 8: seq_reg_phase<8>(a, M, win, cw, S, picks); break;
+      case 1: seq_reg_phase<1>(a, M, win, cw, S, picks, T); break;
+      case 2: seq_reg_phase<2>(a, M, win, cw, S, picks, T); break;
+      case 4: seq_reg_phase<4>(a, M, win, cw, S, picks, T); break;
+      case 8: seq_reg_phase<8>(a, M, win, cw, S, picks, T); break;
       default: seq_phase(a, M, win, cw, S, picks); break;
     }
     ++ns;

@@ -128,7 +128,8 @@ struct SelectArgs {
   int32_t D;             // batch lookahead per client (0 = sequential picks only)
   int32_t Tn;            // batch sort size (power of two >= C * D)
   int32_t sel_threads;   // threads in the selection loop (multiple of 32)
-  int32_t K;             // register client slots per selection thread (1/2/4; 0 = smem loop)
+  int32_t K;             // register client slots per selection thread (1/2/4/8; 0 = smem loop)
+  int32_t Ds;            // key-stream lookahead per client for the register loop
   int32_t cw_in_smem;
   void* cw_global;       // per-client work arrays when they do not fit in smem
   // ledger

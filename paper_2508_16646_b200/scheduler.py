@@ -457,6 +457,12 @@ class GpuScheduler:
                           int(s.new_prefill_tokens), int(s.length_fallbacks), int(s.noisy_near_ties),
                           int(s.batch_members), int(s.batch_reserved_kv_tokens))
 
+    def kernel_times_ms(self) -> dict:
+        """CUDA-event durations of the last (non-graph) step's kernels."""
+        out = (C.c_float * 3)()
+        self._check(self._lib.eqx_kernel_times(self._ctx, out))
+        return {"score_kernel": out[0], "select_kernel": out[1], "drain": out[2]}
+
     def scores(self) -> dict:
         """Per-request scores of the queue in drain order: pred, bucket, ufc_inc, rfc_inc."""
         n = self.n_queued
