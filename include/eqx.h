@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define EQX_ABI_VERSION 1
+#define EQX_ABI_VERSION 2
 
 typedef enum {
   EQX_OK = 0,
@@ -130,6 +130,8 @@ typedef struct {
   int32_t batch_members;      /* BatchState::members.size() after the step */
   int64_t batch_reserved_kv_tokens; /* BatchState::reserved_kv_tokens() after the step */
   int64_t queued;             /* requests still queued after the step */
+  int32_t window_underflow;   /* sharded step only: a gathered head window ran out -- the
+                                 events are not valid; restore the ledger, re-export deeper */
 } eqx_step_summary;
 
 /* ---- context ---------------------------------------------------------------------------- */
@@ -140,6 +142,10 @@ void eqx_ctx_destroy(eqx_ctx* ctx);
 const char* eqx_last_error(const eqx_ctx* ctx);
 /* The cudaStream_t the context launches on (as void*), for event timing by the caller. */
 void* eqx_ctx_stream(eqx_ctx* ctx);
+/* Launch on the caller's cudaStream_t from now on (e.g. the stream a torch.distributed / NCCL
+ * collective runs on), so contexts and collectives order without host synchronisation.  The
+ * context no longer owns (or destroys) a stream. */
+eqx_status eqx_ctx_set_stream(eqx_ctx* ctx, void* stream);
 
 /* ---- configuration (SchedulerPolicy ctor, scheduler.cpp:92-100; validate() :11-17) ------ */
 eqx_status eqx_set_policy(eqx_ctx* ctx, const eqx_policy* policy);
@@ -180,6 +186,31 @@ eqx_status eqx_drain_step_async(eqx_ctx* ctx, const eqx_requests* arrivals, doub
 eqx_status eqx_step_collect(eqx_ctx* ctx, eqx_step_summary* out);
 /* Convenience: eqx_step_async + eqx_step_collect. */
 eqx_status eqx_step(eqx_ctx* ctx, double now, eqx_step_summary* out);
+
+/* ---- client-sharded step over several GPUs ------------------------------
+ * The queue shards by client: rank r owns the contiguous client_id-rank block
+ * [client_off[r], client_off[r+1]) of the global roster and every queued request of those
+ * clients (ids must be global trace positions, the reference's arrival order,
+ * workload.cpp:235-237).  Per step:
+ *   1. each rank: eqx_drain (its requests, local client indices) then eqx_shard_export_async,
+ *      which scores the whole local queue and writes the rank's exchange record -- queue
+ *      length, first-arrival trace position and the first W queued requests of each of its
+ *      clients (scored at `now`, with ids) -- into device memory `rec`;
+ *   2. all-gather the records (ncclAllGather / torch.distributed.all_gather_into_tensor);
+ *   3. every rank: eqx_shard_select_async on a context holding the *global* roster and a
+ *      replicated ledger -- it applies the drain's backlog flags and counter lift in global
+ *      arrival order (on_activated, scheduler.cpp:235-253) and runs admit_requests
+ *      (engine.cpp:207-271) over the gathered heads.  All ranks compute the same schedule with
+ *      no further exchange.  A client that would need a head beyond W sets
+ *      eqx_step_summary.window_underflow: restore the ledger (eqx_ledger_restore_async) and
+ *      repeat with a larger W.  W = free batch slots + 1 never underflows without rejections.
+ * Records are rec_bytes = eqx_shard_record_bytes(cmax, W) bytes, cmax = the largest block. */
+int64_t eqx_shard_record_bytes(int32_t cmax, int32_t W);
+eqx_status eqx_shard_export_async(eqx_ctx* ctx, double now, int32_t cmax, int32_t W, void* rec);
+/* recs: device pointer to `world` records, rank r's at recs + r * stride; client_off: host
+ * array of world + 1 offsets.  Events: eqx_copy_events (ids are the global trace ids). */
+eqx_status eqx_shard_select_async(eqx_ctx* ctx, const void* recs, int32_t world, int64_t stride,
+                                  const int32_t* client_off, int32_t cmax, int32_t W, double now);
 
 /* ---- results (host copies; any pointer may be NULL) ------------------------------------- */
 /* Event log of the last step in order: request id, EQX_EV_*, client, predicted output tokens

@@ -57,7 +57,8 @@ class StepSummary(C.Structure):
     _fields_ = [("n_events", C.c_int64), ("n_admitted", C.c_int64), ("n_rejected", C.c_int64),
                 ("new_prefill_tokens", C.c_int64), ("length_fallbacks", C.c_int64),
                 ("noisy_near_ties", C.c_int64), ("batch_members", C.c_int32),
-                ("batch_reserved_kv_tokens", C.c_int64), ("queued", C.c_int64)]
+                ("batch_reserved_kv_tokens", C.c_int64), ("queued", C.c_int64),
+                ("window_underflow", C.c_int32)]
 
 
 _SIGS = {
@@ -66,6 +67,11 @@ _SIGS = {
     "eqx_ctx_destroy": ([C.c_void_p], None),
     "eqx_last_error": ([C.c_void_p], C.c_char_p),
     "eqx_ctx_stream": ([C.c_void_p], C.c_void_p),
+    "eqx_ctx_set_stream": ([C.c_void_p, C.c_void_p], C.c_int),
+    "eqx_shard_record_bytes": ([C.c_int32, C.c_int32], C.c_int64),
+    "eqx_shard_export_async": ([C.c_void_p, C.c_double, C.c_int32, C.c_int32, C.c_void_p], C.c_int),
+    "eqx_shard_select_async": ([C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, _i32p, C.c_int32, C.c_int32,
+                                C.c_double], C.c_int),
     "eqx_set_policy": ([C.c_void_p, C.POINTER(Policy)], C.c_int),
     "eqx_set_perf": ([C.c_void_p, C.POINTER(Perf)], C.c_int),
     "eqx_set_profile": ([C.c_void_p, C.POINTER(Profile)], C.c_int),

@@ -110,6 +110,10 @@ struct eqx_ctx {
   // cached CUDA graph of drain + step for a resident (device) queue
   cudaGraphExec_t graph = nullptr;
   std::vector<unsigned char> graph_key;
+  bool owns_stream = true;         // false after eqx_ctx_set_stream (caller's stream)
+  // client-sharded step (selection context): gathered windows and their ids
+  DevBuf d_first64, d_gid;
+  int32_t shard_W = 0;             // > 0: the last step was a sharded selection
 };
 
 namespace {
@@ -277,11 +281,26 @@ void eqx_ctx_destroy(eqx_ctx* ctx) {
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->stream2) cudaStreamDestroy(ctx->stream2);
   if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
-  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  ctx->d_first64.release();
+  ctx->d_gid.release();
+  if (ctx->stream && ctx->owns_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
 
 void* eqx_ctx_stream(eqx_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+eqx_status eqx_ctx_set_stream(eqx_ctx* ctx, void* stream) {
+  if (!ctx) return fail(ctx, EQX_ERR_ARG, "eqx_ctx_set_stream: NULL context");  // stream 0 = legacy default
+  cudaSetDevice(ctx->device);
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  if (ctx->owns_stream) CUDA_TRY(ctx, cudaStreamDestroy(ctx->stream));
+  ctx->stream = static_cast<cudaStream_t>(stream);
+  ctx->owns_stream = false;
+  if (ctx->graph) cudaGraphExecDestroy(ctx->graph);  // captured on the old stream's plan
+  ctx->graph = nullptr;
+  ctx->graph_key.clear();
+  return EQX_OK;
+}
 
 // EquinoxParams::validate (scheduler.cpp:11-17)
 eqx_status eqx_set_policy(eqx_ctx* ctx, const eqx_policy* p) {
@@ -703,9 +722,13 @@ struct StepPlan {
   int score_grid, select_threads, window_grid;
 };
 
-static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl) {
+// gW > 0 plans the selection of a client-sharded step over gathered [C][gW] head windows
+// (no local queue; see eqx_shard_select_async).
+static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl, int32_t gW = 0) {
   if (!ctx) return fail(ctx, EQX_ERR_ARG, "eqx_step_async: NULL context");
-  if (!ctx->queue_ready) return fail(ctx, EQX_ERR_CONFIG, "eqx_step: no drained queue (call eqx_drain first)");
+  if (!ctx->model_set || !ctx->profile_set)
+    return fail(ctx, EQX_ERR_CONFIG, "eqx_step: predictor and GPU profile must be set first");
+  if (!gW && !ctx->queue_ready) return fail(ctx, EQX_ERR_CONFIG, "eqx_step: no drained queue (call eqx_drain first)");
   cudaSetDevice(ctx->device);
   cudaStream_t s = ctx->stream;
   const int32_t C = ctx->C;
@@ -901,10 +924,12 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl) {
   // head's arrival); deeper heads (rejection streams) are scored on demand from HBM.
   int64_t W = std::min<int64_t>(static_cast<int64_t>(ctx->perf.max_batch) + 2,
                                 C > 0 ? static_cast<int64_t>(left / (sizeof(WinEntry) * C)) : 0);
+  if (gW > 0) W = std::min<int64_t>(W, gW);
   a.W = static_cast<int32_t>(std::max<int64_t>(W, 0));
+  a.gW = gW;
   smem += static_cast<size_t>(a.W) * C * sizeof(WinEntry);
   pl.select_smem = smem;
-  CUDA_TRY(ctx, ctx->d_win.ensure(std::max<size_t>(static_cast<size_t>(a.W) * C * sizeof(WinEntry), 64)));
+  CUDA_TRY(ctx, ctx->d_win.ensure(std::max<size_t>(static_cast<size_t>(gW > 0 ? gW : a.W) * C * sizeof(WinEntry), 64)));
   a.win_g = ctx->d_win.as<WinEntry>();
   WindowArgs& wi = pl.wi;
   wi.arrival = ctx->q_arrival;
@@ -990,6 +1015,7 @@ static eqx_status step_enqueue(eqx_ctx* ctx, const StepPlan& pl, bool with_drain
 eqx_status eqx_drain(eqx_ctx* ctx, const eqx_requests* r) {
   eqx_status st = drain_prepare(ctx, r);
   if (st != EQX_OK) return st;
+  ctx->shard_W = 0;
   return drain_enqueue(ctx);
 }
 
@@ -997,6 +1023,7 @@ eqx_status eqx_step_async(eqx_ctx* ctx, double now) {
   StepPlan pl;
   eqx_status st = step_prepare(ctx, now, pl);
   if (st != EQX_OK) return st;
+  ctx->shard_W = 0;
   st = step_enqueue(ctx, pl, false);
   if (st != EQX_OK) return st;
   ctx->step_pending = true;
@@ -1007,6 +1034,7 @@ eqx_status eqx_step_async(eqx_ctx* ctx, double now) {
 eqx_status eqx_drain_step_async(eqx_ctx* ctx, const eqx_requests* r, double now) {
   eqx_status st = drain_prepare(ctx, r);
   if (st != EQX_OK) return st;
+  ctx->shard_W = 0;
   StepPlan pl;
   st = step_prepare(ctx, now, pl);
   if (st != EQX_OK) return st;
@@ -1046,6 +1074,135 @@ eqx_status eqx_drain_step_async(eqx_ctx* ctx, const eqx_requests* r, double now)
   return EQX_OK;
 }
 
+// ---- client-sharded step ---------------------------------------------------
+int64_t eqx_shard_record_bytes(int32_t cmax, int32_t W) {
+  if (cmax < 0 || W < 1) return -1;
+  return rec_layout(cmax, W).bytes;
+}
+
+eqx_status eqx_shard_export_async(eqx_ctx* ctx, double now, int32_t cmax, int32_t W, void* rec) {
+  if (!ctx || !rec) return fail(ctx, EQX_ERR_ARG, "eqx_shard_export_async: NULL argument");
+  if (W < 1) return fail(ctx, EQX_ERR_ARG, "eqx_shard_export_async: window depth must be >= 1");
+  if (cmax < ctx->C) return fail(ctx, EQX_ERR_ARG, "eqx_shard_export_async: cmax is smaller than the shard's client count");
+  if (reinterpret_cast<uintptr_t>(rec) & 15u) return fail(ctx, EQX_ERR_ARG, "eqx_shard_export_async: record must be 16-byte aligned");
+  StepPlan pl;
+  eqx_status st = step_prepare(ctx, now, pl);
+  if (st != EQX_OK) return st;
+  cudaStream_t s = ctx->stream, s2 = ctx->stream2;
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fork, s));
+  CUDA_TRY(ctx, cudaStreamWaitEvent(s2, ctx->ev_fork, 0));
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[0], s2));
+  if (ctx->n > 0) score_kernel<<<pl.score_grid, kScoreThreads, pl.score_smem, s2>>>(pl.sc);
+  CUDA_TRY(ctx, cudaGetLastError());
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[1], s2));
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev_join, s2));
+  WindowArgs wi = pl.wi;
+  wi.W = W;
+  const int64_t items = static_cast<int64_t>(cmax) * W;
+  if (items > 0) {
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, 8ll * ctx->sm_count)));
+    shard_export_kernel<<<grid, 256, pl.window_smem, s>>>(wi, cmax, static_cast<unsigned char*>(rec));
+    CUDA_TRY(ctx, cudaGetLastError());
+  }
+  CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_join, 0));
+  ctx->stepped = true;
+  ctx->shard_W = 0;
+  return EQX_OK;
+}
+
+eqx_status eqx_shard_select_async(eqx_ctx* ctx, const void* recs, int32_t world, int64_t stride,
+                                  const int32_t* client_off, int32_t cmax, int32_t W, double now) {
+  if (!ctx || !recs || !client_off) return fail(ctx, EQX_ERR_ARG, "eqx_shard_select_async: NULL argument");
+  if (world < 1 || world > kMaxWorld) return fail(ctx, EQX_ERR_ARG, "eqx_shard_select_async: world size out of range (1..64)");
+  if (W < 1 || cmax < 0) return fail(ctx, EQX_ERR_ARG, "eqx_shard_select_async: bad window depth / cmax");
+  if (stride < rec_layout(cmax, W).bytes || (stride & 15))
+    return fail(ctx, EQX_ERR_ARG, "eqx_shard_select_async: record stride too small or not 16-byte aligned");
+  const int32_t C = ctx->C;
+  if (client_off[0] != 0 || client_off[world] != C)
+    return fail(ctx, EQX_ERR_ARG, "eqx_shard_select_async: client offsets must span [0, C]");
+  ShardMap m;
+  std::memset(&m, 0, sizeof(m));
+  for (int r = 0; r <= world; ++r) {
+    if (r > 0 && (client_off[r] < client_off[r - 1] || client_off[r] - client_off[r - 1] > cmax))
+      return fail(ctx, EQX_ERR_ARG, "eqx_shard_select_async: client blocks must be ordered and <= cmax");
+    m.off[r] = client_off[r];
+  }
+  m.recs = static_cast<const unsigned char*>(recs);
+  m.stride = stride;
+  m.world = world;
+  m.cmax = cmax;
+  m.W = W;
+  m.C = C;
+  cudaSetDevice(ctx->device);
+  const size_t items = static_cast<size_t>(std::max<int64_t>(static_cast<int64_t>(C) * W, 1));
+  CUDA_TRY(ctx, ctx->d_first64.ensure(8ull * std::max(C, 1)));
+  CUDA_TRY(ctx, ctx->d_gid.ensure(8 * items));
+  CUDA_TRY(ctx, ctx->d_ev_row.ensure(4 * items));
+  CUDA_TRY(ctx, ctx->d_ev_kind.ensure(4 * items));
+  CUDA_TRY(ctx, ctx->d_ev_client.ensure(4 * items));
+  CUDA_TRY(ctx, ctx->d_ev_pred.ensure(4 * items));
+  CUDA_TRY(ctx, ctx->d_ev_ufc.ensure(8 * items));
+  CUDA_TRY(ctx, ctx->d_ev_rfc.ensure(8 * items));
+  CUDA_TRY(ctx, ctx->d_ev_vtc.ensure(8 * items));
+  CUDA_TRY(ctx, ctx->d_ev_wait.ensure(8 * items));
+  CUDA_TRY(ctx, ctx->d_ev_id.ensure(8 * items));
+  ctx->ev_cap = static_cast<int64_t>(items);
+  ctx->queue_ready = false;  // the selection context holds no local queue
+  ctx->n = 0;
+  StepPlan pl;
+  eqx_status st = step_prepare(ctx, now, pl, W);
+  if (st != EQX_OK) return st;
+  cudaStream_t s = ctx->stream;
+  ShardSelectBufs b;
+  b.count = ctx->d_count.as<int32_t>();
+  b.first = ctx->d_first64.as<int64_t>();
+  b.head = ctx->d_head.as<int32_t>();
+  b.qlen_before = ctx->d_qlen_before.as<int32_t>();
+  b.running = ctx->d_running.as<int32_t>();
+  b.ufc = ctx->d_ufc.as<double>();
+  b.rfc = ctx->d_rfc.as<double>();
+  b.counter = ctx->d_counter.as<double>();
+  b.backlogged = ctx->d_backlogged.as<int32_t>();
+  b.counter_lift = ctx->counter_lift;
+  b.win = ctx->d_win.as<WinEntry>();
+  b.gid = ctx->d_gid.as<int64_t>();
+  b.st = ctx->d_state.as<DevState>();
+  if (C > 0) {
+    shard_ingest_kernel<<<1, 1024, 0, s>>>(m, b);
+    const int grid = static_cast<int>(std::min<int64_t>((static_cast<int64_t>(C) * W + 255) / 256, 8ll * ctx->sm_count));
+    shard_unpack_kernel<<<grid, 256, 0, s>>>(m, b);
+    CUDA_TRY(ctx, cudaGetLastError());
+  }
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[2], s));
+  select_kernel<<<1, pl.select_threads, pl.select_smem, s>>>(pl.se);
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[3], s));
+  CUDA_TRY(ctx, cudaGetLastError());
+  EventFillArgs ef;
+  std::memset(&ef, 0, sizeof(ef));
+  ef.n_events = &ctx->d_state.as<DevState>()->n_events;
+  ef.ev_cap = ctx->ev_cap;
+  ef.ev_row = ctx->d_ev_row.as<int32_t>();
+  ef.ev_kind = ctx->d_ev_kind.as<int32_t>();
+  ef.ev_client = ctx->d_ev_client.as<int32_t>();
+  ef.ev_pred = ctx->d_ev_pred.as<int32_t>();
+  ef.ev_ufc = ctx->d_ev_ufc.as<double>();
+  ef.ev_rfc = ctx->d_ev_rfc.as<double>();
+  ef.ev_vtc = ctx->d_ev_vtc.as<double>();
+  ef.ev_wait = ctx->d_ev_wait.as<double>();
+  ef.weight = ctx->d_weight.as<double>();
+  ef.pol = ctx->pol;
+  ef.now = now;
+  shard_event_fill_kernel<<<std::max(1, ctx->sm_count / 4), 256, 0, s>>>(ef, ctx->d_win.as<WinEntry>());
+  CUDA_TRY(ctx, cudaGetLastError());
+  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_state, ctx->d_state.p, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+  ctx->q_id = ctx->d_gid.as<int64_t>();
+  ctx->id_base = 0;
+  ctx->shard_W = W;
+  ctx->step_pending = true;
+  ctx->stepped = true;
+  return EQX_OK;
+}
+
 eqx_status eqx_step_collect(eqx_ctx* ctx, eqx_step_summary* out) {
   if (!ctx) return fail(ctx, EQX_ERR_ARG, "eqx_step_collect: NULL context");
   cudaSetDevice(ctx->device);
@@ -1061,7 +1218,9 @@ eqx_status eqx_step_collect(eqx_ctx* ctx, eqx_step_summary* out) {
     out->noisy_near_ties = static_cast<int64_t>(h.near_ties - ctx->last_near_ties);
     out->batch_members = h.members;
     out->batch_reserved_kv_tokens = h.reserved;
-    out->queued = ctx->n - h.n_events;  // cold-step accounting: one drain, one step
+    // cold-step accounting: one drain, one step
+    out->queued = (ctx->shard_W > 0 ? h.n_queued : ctx->n) - h.n_events;
+    out->window_underflow = ctx->shard_W > 0 ? h.underflow : 0;
   }
   ctx->last_fallbacks = h.fallbacks;
   ctx->last_near_ties = h.near_ties;
@@ -1103,7 +1262,7 @@ eqx_status eqx_copy_events(eqx_ctx* ctx, int64_t cap, int64_t* id, int32_t* kind
   cudaSetDevice(ctx->device);
   cudaStream_t s = ctx->stream;
   CUDA_TRY(ctx, cudaStreamSynchronize(s));
-  const int64_t n = std::min<int64_t>(cap, ctx->h_state->n_events);
+  const int64_t n = std::min<int64_t>(std::min<int64_t>(cap, ctx->h_state->n_events), ctx->ev_cap);
   if (n <= 0) return EQX_OK;
   if (id) {
     gather_ids_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
@@ -1125,6 +1284,8 @@ eqx_status eqx_copy_events(eqx_ctx* ctx, int64_t cap, int64_t* id, int32_t* kind
 eqx_status eqx_copy_scores(eqx_ctx* ctx, int64_t cap, int32_t* pred, uint8_t* bucket,
                            double* ufc_inc, double* rfc_inc) {
   if (!ctx || !ctx->stepped) return fail(ctx, EQX_ERR_CONFIG, "eqx_copy_scores: no step has run");
+  if (ctx->shard_W > 0)
+    return fail(ctx, EQX_ERR_CONFIG, "eqx_copy_scores: a sharded selection context holds no queue (scores live on the ranks' contexts)");
   cudaSetDevice(ctx->device);
   cudaStream_t s = ctx->stream;
   const int64_t n = std::min<int64_t>(cap, ctx->n);

@@ -58,12 +58,13 @@ struct DevState {
   unsigned long long fallbacks;   // MopePredictor::length_fallbacks_ over scored rows
   unsigned long long near_ties;   // noisy predictor near-.5 flags
   int32_t bad_client;     // drain saw a client index out of range
-  int32_t pad1;
+  int32_t underflow;      // client-sharded step: a gathered head window ran out (retry deeper)
   // phase timestamps (%globaltimer ns) of the last step, for profiling:
   // [0] selection start [1] windows filled [2] loop start [3] loop end
   // [4] first worker start (min) [5] last worker end (max) [6] #batches [7] #seq phases
   // [8..11] batch cycles: stream generation, sort, verify, commit
   unsigned long long t[16];
+  int64_t n_queued;       // client-sharded step: queued requests over all ranks at step start
 };
 
 // Order-preserving map double -> uint64 (IEEE total order on non-NaN values, with -0.0 and

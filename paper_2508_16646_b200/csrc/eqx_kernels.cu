@@ -189,22 +189,33 @@ __global__ void __launch_bounds__(kDrainThreads) drain_hist_kernel(const DrainAr
 // lifted joins the backlog: pre-backlogged clients (qlen_before > 0), the very first arrival
 // when nobody was backlogged, and clients with running requests (engine.cpp:182).  Hence
 // m(c) = min(base, {vals(r) : r non-lifted arrival, first_row[r] < first_row[c]}).
-__device__ void lift_epilogue(const DrainArgs& a) {
+// Arrival keys are drain rows (one queue) or global trace positions (client-sharded step,
+// where the clients' first arrivals live on different ranks).
+struct LiftIn {
+  int32_t C;
+  int32_t counter_lift;
+  const int32_t* count;
+  const int32_t* qlen_before;
+  const int32_t* running;
+  double* ufc;
+  double* rfc;
+  double* counter;
+  int32_t* backlogged;
+};
+
+template <class Key>
+__device__ void lift_core(const LiftIn& a, const Key* first_row) {
   __shared__ double s_min[3][32];
-  __shared__ int s_first[32], s_firstc[32], s_flags[32];
+  __shared__ Key s_first[32];
+  __shared__ int s_firstc[32], s_flags[32];
   const int32_t C = a.C;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  // counts and first arrival rows from the segment offsets / perm
-  for (int c = tid; c < C; c += blockDim.x) {
-    const int32_t s0 = __ldcg(a.seg_off + c), s1 = __ldcg(a.seg_off + c + 1);
-    a.count[c] = s1 - s0;
-    a.first_row[c] = s1 > s0 ? static_cast<int32_t>(__ldcg(a.perm + s0)) : 0x7fffffff;
-  }
-  __syncthreads();
+  const Key kNone = sizeof(Key) == 8 ? static_cast<Key>(0x7fffffffffffffffLL) : static_cast<Key>(0x7fffffff);
   if (a.counter_lift) {
     double mu = INFINITY, mr = INFINITY, mc = INFINITY;
     int any0 = 0, anyR = 0;
-    int fr = 0x7fffffff, fc = -1;
+    Key fr = kNone;
+    int fc = -1;
     for (int c = tid; c < C; c += blockDim.x) {
       const int32_t cnt = a.count[c];
       if (a.qlen_before[c] > 0) {
@@ -215,8 +226,8 @@ __device__ void lift_epilogue(const DrainArgs& a) {
       } else if (cnt > 0 && a.running[c] != 0) {
         anyR = 1;
       }
-      if (cnt > 0 && a.first_row[c] < fr) {
-        fr = a.first_row[c];
+      if (cnt > 0 && first_row[c] < fr) {
+        fr = first_row[c];
         fc = c;
       }
     }
@@ -227,7 +238,7 @@ __device__ void lift_epilogue(const DrainArgs& a) {
       mc = fmin(mc, __shfl_xor_sync(0xffffffffu, mc, o));
       any0 |= __shfl_xor_sync(0xffffffffu, any0, o);
       anyR |= __shfl_xor_sync(0xffffffffu, anyR, o);
-      const int ofr = __shfl_xor_sync(0xffffffffu, fr, o);
+      const Key ofr = __shfl_xor_sync(0xffffffffu, fr, o);
       const int ofc = __shfl_xor_sync(0xffffffffu, fc, o);
       if (ofr < fr) {
         fr = ofr;
@@ -244,7 +255,8 @@ __device__ void lift_epilogue(const DrainArgs& a) {
     }
     __syncthreads();
     double bu = INFINITY, br = INFINITY, bc = INFINITY;
-    int f0 = 0x7fffffff, fc0 = -1, flags = 0;
+    Key f0 = kNone;
+    int fc0 = -1, flags = 0;
     for (int w = 0; w < nw; ++w) {
       bu = fmin(bu, s_min[0][w]);
       br = fmin(br, s_min[1][w]);
@@ -268,10 +280,10 @@ __device__ void lift_epilogue(const DrainArgs& a) {
         if (!any_s0 && c == fc0) continue;
         double u = bu, r = br, k = bc;
         if (any_r) {
-          const int fcr = a.first_row[c];
+          const Key fcr = first_row[c];
           for (int x = 0; x < C; ++x) {  // non-lifted arrivals before c
             if (a.count[x] == 0 || a.qlen_before[x] > 0 || a.running[x] == 0) continue;
-            if (a.first_row[x] < fcr) {
+            if (first_row[x] < fcr) {
               u = fmin(u, a.ufc[x]);
               r = fmin(r, a.rfc[x]);
               k = fmin(k, a.counter[x]);
@@ -286,6 +298,18 @@ __device__ void lift_epilogue(const DrainArgs& a) {
     }
   }
   for (int c = tid; c < C; c += blockDim.x) a.backlogged[c] = (a.qlen_before[c] + a.count[c]) > 0 ? 1 : 0;
+}
+
+__device__ void lift_epilogue(const DrainArgs& a) {
+  // counts and first arrival rows from the segment offsets / perm
+  for (int c = threadIdx.x; c < a.C; c += blockDim.x) {
+    const int32_t s0 = __ldcg(a.seg_off + c), s1 = __ldcg(a.seg_off + c + 1);
+    a.count[c] = s1 - s0;
+    a.first_row[c] = s1 > s0 ? static_cast<int32_t>(__ldcg(a.perm + s0)) : 0x7fffffff;
+  }
+  __syncthreads();
+  const LiftIn l{a.C, a.counter_lift, a.count, a.qlen_before, a.running, a.ufc, a.rfc, a.counter, a.backlogged};
+  lift_core<int32_t>(l, a.first_row);
 }
 
 // Stable scatter of row indices into per-client FIFO segments.  Each CTA owns one tile; each
@@ -594,8 +618,24 @@ __device__ __forceinline__ WinEntry make_entry(const A& a, const ModelTables& M,
   return e;
 }
 
-// Head at FIFO position j beyond the cached window (rejection streams): scored from HBM.
-__device__ __noinline__ WinEntry deep_entry(const SelectArgs& a, const ModelTables& M, int32_t c, int32_t j, double w) {
+// Head at FIFO position j (window index k) beyond the shared-memory window: scored from HBM
+// (rejection streams), or, in a client-sharded step, read from the gathered windows.  A head
+// beyond the gathered depth flags DevState::underflow: the host re-runs the step from its
+// checkpoint with deeper windows, so a flagged step's picks are never used.  The sentinel
+// always fits alone, so the loop still terminates (admissions are bounded by max_batch).
+__device__ __noinline__ WinEntry deep_entry(const SelectArgs& a, const ModelTables& M, int32_t c, int32_t j,
+                                            int32_t k, double w) {
+  if (a.gW > 0) {
+    if (k < a.gW) return a.win_g[static_cast<int64_t>(c) * a.gW + k];
+    a.st->underflow = 1;
+    WinEntry e;
+    e.ufc_inc = e.rfc_inc = 0.0;
+    e.abits = ~0ull;
+    e.in = e.pred = 0;
+    e.row = -1;
+    e.alone = 1;
+    return e;
+  }
   return make_entry(a, M, static_cast<int32_t>(a.perm[a.seg_off[c] + j]), w);
 }
 
@@ -603,7 +643,7 @@ __device__ __forceinline__ WinEntry get_entry(const SelectArgs& a, const ModelTa
                                               const ClientWork& cw, int32_t c, int32_t j) {
   const int32_t k = j - cw.pos0[c];
   if (k < a.W) return win[static_cast<int64_t>(c) * a.W + k];
-  return deep_entry(a, M, c, j, cw.w[c]);
+  return deep_entry(a, M, c, j, k, cw.w[c]);
 }
 
 // First W queued entries of every client (C*W items, one per thread across many CTAs).
@@ -1205,7 +1245,7 @@ __device__ void seq_reg_phase(const SelectArgs& a, const ModelTables& M, const W
   double mu = S.max_u, mr = S.max_r;
   auto entry = [&](int32_t c, int32_t j, int32_t pos0) -> WinEntry {
     const int32_t k = j - pos0;
-    return k < W ? win[static_cast<int64_t>(c) * W + k] : deep_entry(a, M, c, j, cw.w[c]);
+    return k < W ? win[static_cast<int64_t>(c) * W + k] : deep_entry(a, M, c, j, k, cw.w[c]);
   };
   // (re)generate the lookahead stream of slot s under the current maxima
   auto gen = [&](int s, int depth) {
@@ -1517,7 +1557,17 @@ __global__ void __launch_bounds__(kSelectMaxThreads, 1) select_kernel(const Sele
     cw.flags[c] = a.backlogged[c] ? kBacklogged : 0;
     cw.adm[c] = 0;
   }
-  {
+  if (a.gW > 0 && a.gW != a.W) {  // gathered [C][gW] windows: the first W of every client
+    constexpr int kWords = sizeof(WinEntry) / 8;
+    const int64_t per = static_cast<int64_t>(a.W) * kWords;
+    const int64_t words = static_cast<int64_t>(C) * per;
+    const uint2* src = reinterpret_cast<const uint2*>(a.win_g);
+    uint2* dst = reinterpret_cast<uint2*>(win);
+    for (int64_t i = tid; i < words; i += NT) {
+      const int64_t c = i / per;
+      dst[i] = __ldcg(src + c * a.gW * kWords + (i - c * per));
+    }
+  } else {
     const int64_t words = static_cast<int64_t>(C) * a.W * (sizeof(WinEntry) / 8);
     const uint2* src = reinterpret_cast<const uint2*>(a.win_g);
     uint2* dst = reinterpret_cast<uint2*>(win);
@@ -1619,7 +1669,131 @@ __global__ void event_fill_kernel(const EventFillArgs a) {
 __global__ void gather_ids_kernel(const int32_t* __restrict__ rows, int64_t n, const int64_t* __restrict__ id,
                                   int64_t id_base, int64_t* __restrict__ out) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n) out[i] = id ? id[rows[i]] : id_base + rows[i];
+  if (i < n) {
+    const int32_t r = rows[i];
+    out[i] = r < 0 ? -1 : (id ? id[r] : id_base + r);
+  }
+}
+
+// ================================ client-sharded step =====================================
+// the queue shards by client over ranks; every rank scores its own queue and
+// exports its clients' head windows (shard_export_kernel), the records are all-gathered
+// (NCCL), and every rank runs the identical exact selection over the gathered windows with a
+// replicated ledger (shard_ingest_kernel applies the drain's backlog flags and counter lift
+// with global arrival order, shard_unpack_kernel lays the windows out as [C][W]).
+
+__device__ __forceinline__ int32_t rank_of(const ShardMap& m, int32_t c) {
+  int32_t r = 0;
+  while (r + 1 < m.world && m.off[r + 1] <= c) ++r;
+  return r;
+}
+
+__global__ void __launch_bounds__(256) shard_export_kernel(const WindowArgs a, int32_t cmax, unsigned char* rec) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  stage_model(a.model, a.model_words, smem);
+  __syncthreads();
+  const ModelTables& M = *reinterpret_cast<const ModelTables*>(smem);
+  const RecLayout L = rec_layout(cmax, a.W);
+  int32_t* r_count = reinterpret_cast<int32_t*>(rec + L.count);
+  int64_t* r_first = reinterpret_cast<int64_t*>(rec + L.first);
+  WinEntry* r_win = reinterpret_cast<WinEntry*>(rec + L.win);
+  int64_t* r_id = reinterpret_cast<int64_t*>(rec + L.id);
+  const int64_t items = static_cast<int64_t>(cmax) * a.W;
+  for (int64_t it = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; it < items;
+       it += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t c = static_cast<int32_t>(it / a.W);
+    const int32_t k = static_cast<int32_t>(it % a.W);
+    const bool mine = c < a.C;
+    const int32_t h = mine ? a.head[c] : 0, cnt = mine ? a.count[c] : 0;
+    if (k == 0) {
+      r_count[c] = cnt - h;
+      int64_t f = 0x7fffffffffffffffLL;
+      if (cnt > 0) {
+        const int32_t row0 = static_cast<int32_t>(a.perm[a.seg_off[c]]);
+        f = a.id ? a.id[row0] : a.id_base + row0;
+      }
+      r_first[c] = f;
+    }
+    if (h + k < cnt) {
+      const int32_t row = static_cast<int32_t>(a.perm[a.seg_off[c] + h + k]);
+      WinEntry e = make_entry(a, M, row, a.weight[c]);
+      e.row = -1;
+      r_win[it] = e;
+      r_id[it] = a.id ? a.id[row] : a.id_base + row;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(1024) shard_ingest_kernel(const ShardMap m, const ShardSelectBufs b) {
+  const RecLayout L = rec_layout(m.cmax, m.W);
+  for (int32_t c = threadIdx.x; c < m.C; c += blockDim.x) {
+    const int32_t r = rank_of(m, c), l = c - m.off[r];
+    const unsigned char* base = m.recs + static_cast<int64_t>(r) * m.stride;
+    b.count[c] = reinterpret_cast<const int32_t*>(base + L.count)[l];
+    b.first[c] = reinterpret_cast<const int64_t*>(base + L.first)[l];
+    b.head[c] = 0;
+    b.qlen_before[c] = 0;
+  }
+  __shared__ unsigned long long total;
+  if (threadIdx.x == 0) {
+    b.st->underflow = 0;
+    total = 0;
+  }
+  __syncthreads();
+  unsigned long long mine = 0;
+  for (int32_t c = threadIdx.x; c < m.C; c += blockDim.x) mine += static_cast<unsigned long long>(b.count[c]);
+  atomicAdd(&total, mine);
+  __syncthreads();
+  if (threadIdx.x == 0) b.st->n_queued = static_cast<int64_t>(total);
+  const LiftIn li{m.C, b.counter_lift, b.count, b.qlen_before, b.running, b.ufc, b.rfc, b.counter, b.backlogged};
+  lift_core<int64_t>(li, b.first);
+}
+
+__global__ void __launch_bounds__(256) shard_unpack_kernel(const ShardMap m, const ShardSelectBufs b) {
+  const RecLayout L = rec_layout(m.cmax, m.W);
+  const int64_t items = static_cast<int64_t>(m.C) * m.W;
+  for (int64_t it = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; it < items;
+       it += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t c = static_cast<int32_t>(it / m.W);
+    const int32_t k = static_cast<int32_t>(it % m.W);
+    const int32_t r = rank_of(m, c), l = c - m.off[r];
+    const unsigned char* base = m.recs + static_cast<int64_t>(r) * m.stride;
+    const int64_t src = static_cast<int64_t>(l) * m.W + k;
+    WinEntry e = reinterpret_cast<const WinEntry*>(base + L.win)[src];
+    e.row = static_cast<int32_t>(it);
+    b.win[it] = e;
+    b.gid[it] = reinterpret_cast<const int64_t*>(base + L.id)[src];
+  }
+}
+
+// event_fill_kernel over the gathered windows (row = c * W + k indexes b.win).
+__global__ void shard_event_fill_kernel(const EventFillArgs a, const WinEntry* __restrict__ win) {
+  const int64_t n = *a.n_events;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n && i < a.ev_cap;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t row = a.ev_row[i];
+    const bool adm = a.ev_kind[i] == 1 && row >= 0;
+    WinEntry e;
+    if (row >= 0) {
+      e = win[row];
+    } else {
+      e.ufc_inc = e.rfc_inc = 0.0;
+      e.abits = 0;
+      e.in = e.pred = 0;
+    }
+    a.ev_pred[i] = e.pred;
+    a.ev_ufc[i] = adm ? e.ufc_inc : 0.0;
+    a.ev_rfc[i] = adm ? e.rfc_inc : 0.0;
+    double v = 0.0;
+    if (adm && a.pol.kind == kVtc) {  // scheduler.cpp:169-181
+      const double w = a.weight[a.ev_client[i]];
+      v = a.pol.vtc_use_prediction
+              ? __dmul_rn(w, __dadd_rn(static_cast<double>(e.in), __dmul_rn(a.pol.ow, static_cast<double>(e.pred))))
+              : __dmul_rn(w, static_cast<double>(e.in));
+    }
+    a.ev_vtc[i] = v;
+    a.ev_wait[i] = adm ? __dsub_rn(a.now, from_ordered_bits(e.abits)) : 0.0;  // engine.cpp:257
+  }
 }
 
 }  // namespace eqx

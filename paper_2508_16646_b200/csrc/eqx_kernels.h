@@ -124,7 +124,9 @@ struct SelectArgs {
   int32_t* head;
   int32_t C;
   int32_t W;             // head-window depth cached in shared memory per client
-  const WinEntry* win_g; // [C][W] windows produced by window_kernel
+  const WinEntry* win_g; // [C][W] windows produced by window_kernel ([C][gW] when gathered)
+  int32_t gW;            // > 0: client-sharded step; win_g holds the gathered [C][gW] windows and
+                         // a head beyond them raises DevState::underflow instead of reading HBM
   int32_t D;             // batch lookahead per client (0 = sequential picks only)
   int32_t Tn;            // batch sort size (power of two >= C * D)
   int32_t sel_threads;   // threads in the selection loop (multiple of 32)
@@ -178,6 +180,60 @@ struct EventFillArgs {
   Policy pol;
   double now;
 };
+
+// ---- client-sharded step ------------------------------------------------
+// One rank's exchange record: for cmax client slots (the rank's clients, padded to the largest
+// shard so every rank contributes the same byte count to the all-gather) the drained queue
+// length, the trace position (id) of the client's first arrival in the drain, and the first W
+// queued requests scored at the step's `now`, with their ids.  16-byte aligned sections.
+struct RecLayout {
+  int64_t count, first, win, id, bytes;
+};
+__host__ __device__ inline RecLayout rec_layout(int64_t cmax, int64_t W) {
+  auto a16 = [](int64_t x) { return (x + 15) & ~int64_t(15); };
+  RecLayout L;
+  L.count = 0;
+  L.first = a16(4 * cmax);
+  L.win = L.first + a16(8 * cmax);
+  L.id = L.win + a16(static_cast<int64_t>(sizeof(WinEntry)) * cmax * W);
+  L.bytes = L.id + a16(8 * cmax * W);
+  return L;
+}
+
+constexpr int kMaxWorld = 64;
+
+// The gathered records of `world` ranks: rank r's record at recs + r * stride covers global
+// clients [off[r], off[r+1]) (contiguous client_id-rank blocks).
+struct ShardMap {
+  const unsigned char* recs;
+  int64_t stride;
+  int32_t world;
+  int32_t cmax;
+  int32_t W;
+  int32_t C;
+  int32_t off[kMaxWorld + 1];
+};
+
+struct ShardSelectBufs {
+  int32_t* count;        // [C]
+  int64_t* first;        // [C] trace position of the first arrival
+  int32_t* head;         // [C] reset to 0 (cold step)
+  int32_t* qlen_before;  // [C] reset to 0 (the drain replaces the queue)
+  const int32_t* running;
+  double* ufc;
+  double* rfc;
+  double* counter;
+  int32_t* backlogged;
+  int32_t counter_lift;
+  WinEntry* win;         // [C][W] gathered windows, row = c * W + k
+  int64_t* gid;          // [C][W] request ids
+  DevState* st;
+};
+
+__global__ void shard_export_kernel(WindowArgs a, int32_t cmax, unsigned char* rec);
+__global__ void shard_ingest_kernel(ShardMap m, ShardSelectBufs b);
+__global__ void shard_unpack_kernel(ShardMap m, ShardSelectBufs b);
+__global__ void shard_event_fill_kernel(EventFillArgs a, const WinEntry* win);
 
 __global__ void drain_hist_kernel(DrainArgs a);
 __global__ void event_fill_kernel(EventFillArgs a);

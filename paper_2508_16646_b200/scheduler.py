@@ -228,6 +228,8 @@ class StepResult:
     noisy_near_ties: int
     batch_members: int
     batch_reserved_kv_tokens: int
+    queued: int = 0
+    window_underflow: int = 0
 
     @property
     def admitted(self) -> np.ndarray:
@@ -443,7 +445,7 @@ class GpuScheduler:
         return self._result(s, with_events)
 
     def _result(self, s: L.StepSummary, with_events: bool) -> StepResult:
-        n = int(s.n_events) if with_events else 0
+        n = int(s.n_events) if with_events and not s.window_underflow else 0
         ids = np.zeros(n, np.int64)
         kinds, cl, pr = (np.zeros(n, np.int32) for _ in range(3))
         ui, ri, vi, wt = (np.zeros(n) for _ in range(4))
@@ -455,7 +457,27 @@ class GpuScheduler:
                                                   wt.ctypes.data_as(L._dp)))
         return StepResult(ids, kinds, cl, pr, ui, ri, vi, wt, int(s.n_admitted), int(s.n_rejected),
                           int(s.new_prefill_tokens), int(s.length_fallbacks), int(s.noisy_near_ties),
-                          int(s.batch_members), int(s.batch_reserved_kv_tokens))
+                          int(s.batch_members), int(s.batch_reserved_kv_tokens), int(s.queued),
+                          int(s.window_underflow))
+
+    # -- client-sharded step (include/eqx.h; driven by sharded.ShardedScheduler) --
+    def set_stream(self, stream_ptr: int) -> None:
+        """Launch on the caller's CUDA stream (e.g. torch's current stream, where the NCCL
+        all-gather of the sharded step is ordered)."""
+        self._check(self._lib.eqx_ctx_set_stream(self._ctx, C.c_void_p(int(stream_ptr))))
+
+    def shard_export_async(self, now: float, cmax: int, window: int, rec) -> None:
+        """Score the local queue and write this rank's exchange record into ``rec`` (a CUDA
+        uint8 tensor of at least eqx_shard_record_bytes(cmax, window) bytes)."""
+        self._check(self._lib.eqx_shard_export_async(self._ctx, float(now), int(cmax), int(window),
+                                                     C.c_void_p(rec.data_ptr())))
+
+    def shard_select_async(self, recs, world: int, stride: int, client_off, cmax: int, window: int,
+                           now: float) -> None:
+        off = np.ascontiguousarray(client_off, np.int32)
+        self._check(self._lib.eqx_shard_select_async(self._ctx, C.c_void_p(recs.data_ptr()), int(world),
+                                                     int(stride), off.ctypes.data_as(L._i32p), int(cmax),
+                                                     int(window), float(now)))
 
     def kernel_times_ms(self) -> dict:
         """CUDA-event durations of the last (non-graph) step's kernels."""

@@ -50,11 +50,15 @@ def default_profile() -> dict:
         return {k: np.asarray(v) for k, v in json.load(f).items()}
 
 
-def gpu_run(case: H.StepCase, device_columns: bool = False):
-    """Run one StepCase through the product (GpuScheduler over libeqx_b200.so)."""
+def case_clients(case: H.StepCase) -> list:
     case.finalize()
-    clients = [S.ClientState(n, weight=float(w), ufc=float(u), rfc=float(r), counter=float(k))
-               for n, w, u, r, k in zip(case.client_names, case.weight, case.ufc0, case.rfc0, case.counter0)]
+    return [S.ClientState(n, weight=float(w), ufc=float(u), rfc=float(r), counter=float(k))
+            for n, w, u, r, k in zip(case.client_names, case.weight, case.ufc0, case.rfc0, case.counter0)]
+
+
+def case_kwargs(case: H.StepCase) -> dict:
+    """GpuScheduler keyword arguments (policy, perf, profile, predictor) of a StepCase."""
+    case.finalize()
     pol = S.PolicySpec(kind=KIND_NAMES[case.kind],
                        equinox=S.EquinoxParams(case.alpha, case.delta, case.output_weight,
                                                "none" if case.norm_mode == H.NORM_NONE else "max_over_clients"),
@@ -64,16 +68,29 @@ def gpu_run(case: H.StepCase, device_columns: bool = False):
     p = case.profile
     prof = S.GpuProfile.from_arrays(p["upper"], p["lat"], p["util"], p["tps"])
     model = S.MopeModel.from_json(case.model) if case.model is not None else None
-    sch = S.GpuScheduler(clients, policy=pol, perf=perf, profile=prof, predictor=PRED_NAMES[case.pred_kind],
-                         model=model, tag_names=case.tag_names, noisy_l1=case.noisy_l1,
-                         noisy_seed=case.noisy_seed, backfill=bool(case.backfill), running=case.running)
+    return dict(policy=pol, perf=perf, profile=prof, predictor=PRED_NAMES[case.pred_kind], model=model,
+                tag_names=case.tag_names, noisy_l1=case.noisy_l1, noisy_seed=case.noisy_seed,
+                backfill=bool(case.backfill))
+
+
+def case_batch(case: H.StepCase) -> tuple:
     reserved = int(np.sum(case.mem_in.astype(np.int64) +
                           np.maximum(case.mem_reserved, case.mem_generated).astype(np.int64)))
-    sch.set_batch(len(case.mem_in), reserved)
+    return len(case.mem_in), reserved
+
+
+def case_columns(case: H.StepCase) -> dict:
     tag = np.where(np.asarray(case.tag) < 0, 0, np.asarray(case.tag) + 1).astype(np.uint8)
-    cols = dict(client=np.asarray(case.client, np.int32), arrival_s=np.asarray(case.arrival, np.float64),
+    return dict(client=np.asarray(case.client, np.int32), arrival_s=np.asarray(case.arrival, np.float64),
                 input_tokens=np.asarray(case.in_tokens, np.int32), tag=tag,
                 true_output_tokens=np.asarray(case.true_out, np.int32), ids=np.asarray(case.id, np.int64))
+
+
+def gpu_run(case: H.StepCase, device_columns: bool = False):
+    """Run one StepCase through the product (GpuScheduler over libeqx_b200.so)."""
+    sch = S.GpuScheduler(case_clients(case), running=case.running, **case_kwargs(case))
+    sch.set_batch(*case_batch(case))
+    cols = case_columns(case)
     if device_columns:
         import torch
         cols = {k: torch.from_numpy(v).cuda() for k, v in cols.items()}
