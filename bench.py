@@ -6,8 +6,10 @@ A "step" is one cold scheduling step over a resident queue: dra
 the whole queue (client-grouped FIFO index + counter lift) followed by admit_requests with
 whole-queue scoring (MoPE predict -> map_metrics -> ufc/rfc increments -> HF selection under
 the slot/KV budget).  N=1 runs BASELINE configs[1] (1M LMSYS-shaped requests, 64 clients).
-Under torchrun each rank holds its own 1M-request / 64-client shard (weak scaling, no
-data-path collective in this round: see DESIGN.md "Multi-GPU").
+Under torchrun (N>1) the queue is client-sharded: each rank holds a
+1M-request / 64-client shard of one global trace (weak scaling; --config cfg4: 2M / 1,250 per
+rank = 16M / 10k clients at N=8), scores it locally, and the ranks all-gather their clients'
+head-window records over NCCL before every rank runs the identical exact selection.
 
 Timing: every timed step is bracketed by CUDA events on the context stream; the L2 (126 MB)
 is flushed with a 256 MiB memset between steps, outside the events.  `e2e` repeats the step
@@ -156,14 +158,154 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def shard_inputs(cfg: str, rank: int, world: int):
+    """Rank `rank`'s shard of a client-sharded global trace (SURVEY.md 8(e)): per GPU the cfg's
+    queue shape (cfg2: 1M requests / 64 clients; cfg4: 2M / 1,250 = 16M / 10k over 8 GPUs).
+    Global client g = rank * C_r + local, named client%06d so rank blocks are client_id-byte
+    blocks; the rank's i-th request has trace position i * world + rank and arrival
+    position / (n_r * world) s, so the union over ranks is one arrival-ordered trace."""
+    from paper_2508_16646_b200 import workload as W
+    from paper_2508_16646_b200 import scheduler as S
+    data = os.path.join(ROOT, "paper_2508_16646_b200", "data")
+    model = S.MopeModel.load(os.path.join(data, "mope_builtin_c10000_s7_e3.json"))
+    prof = S.GpuProfile.load_json(os.path.join(data, "profile_default.json"))
+    n_r, c_r = (2_000_000, 1250) if cfg == "cfg4" else (1_000_000, 64)
+    q = W.lmsys_queue(n_r, c_r, seed=1 + 100 * rank)
+    pos = np.arange(n_r, dtype=np.int64) * world + rank
+    q["id"] = pos
+    q["arrival"] = pos.astype(np.float64) / float(n_r * world)
+    led = W.warm_ledger(c_r * world, seed=2)
+    names = [f"client{g:06d}" for g in range(c_r * world)]
+    desc = (f"{cfg} per GPU: {n_r} queued requests / {c_r} clients per rank, client-sharded over {world} "
+            f"GPU(s) ({n_r * world} requests, {c_r * world} clients), warm ledger, max_batch 64")
+    return q, led, names, c_r, S.PerfParams(max_batch=64), model, prof, desc
+
+
+def run_sharded(args, rank, world):
+    """N GPUs: one process per GPU, client-sharded queue, exact replicated selection after one
+    NCCL all-gather of the ranks' head-window records per step."""
+    import torch
+    from paper_2508_16646_b200 import scheduler as S
+    from paper_2508_16646_b200.sharded import ShardedScheduler
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = "cfg4" if args.config == "cfg4" else "cfg2"
+    q, led, names, c_r, perf, model, prof, desc = shard_inputs(cfg, rank, world)
+    n = len(q["client"])
+    clients = [S.ClientState(nm, ufc=float(u), rfc=float(r), counter=float(c))
+               for nm, u, r, c in zip(names, led["ufc"], led["rfc"], led["counter"])]
+    owner = np.repeat(np.arange(world, dtype=np.int32), c_r)
+    sch = ShardedScheduler(clients, rank, world, owner=owner, device=local, policy=S.PolicySpec(), perf=perf,
+                           profile=prof, predictor="mope", model=model, tag_names=q["tag_names"])
+    stream = sch.stream
+    with torch.cuda.stream(stream):
+        cols = dict(client=torch.from_numpy(q["client"]).to(dev), arrival_s=torch.from_numpy(q["arrival"]).to(dev),
+                    input_tokens=torch.from_numpy(q["in_tokens"]).to(dev), tag=torch.from_numpy(tag_ids(q)).to(dev),
+                    ids=torch.from_numpy(q["id"]).to(dev))
+        flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    torch.cuda.synchronize()
+    sch.set_batch(0, 0)
+    window = perf.max_batch + 1  # free slots + 1: exact without rejections (underflow is checked)
+    sch.sel.checkpoint()
+
+    def enqueue_step():
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            sch.sel.restore_async()
+            flush.zero_()
+            e0.record(stream)
+            sch.drain(local=True, **cols)
+            sch.step_async(1.0, window)
+            e1.record(stream)
+        return e0, e1
+
+    for _ in range(args.warmup):
+        enqueue_step()
+    res = sch.sel.collect(with_events=False)
+    if res.window_underflow:
+        raise RuntimeError("head windows underflowed on the bench workload")
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        recs = [enqueue_step() for _ in range(args.steps)]
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    res = sch.sel.collect(with_events=False)
+    step_ms = np.array([a.elapsed_time(b) for a, b in recs])
+    total_ms = float(step_ms.sum())
+    p50 = float(np.median(step_ms))
+    if dist:
+        t = torch.tensor([total_ms, p50], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, p50 = float(t[0].item()), float(t[1].item())
+    value = world * n * args.steps / (total_ms * 1e-3)
+
+    # e2e: the public sharded API with this rank's pinned host columns (H2D inside), events D2H
+    host = {k: torch.from_numpy(v).pin_memory() for k, v in
+            dict(client=q["client"], arrival_s=q["arrival"], input_tokens=q["in_tokens"], tag=tag_ids(q),
+                 ids=q["id"]).items()}
+    e2e_t, d2h = [], 0
+    for i in range(args.warmup + max(3, args.steps // 4)):
+        sch.sel.restore_async()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        sch.drain(local=True, **host)
+        r = sch.step(1.0, window=window)
+        t1 = time.perf_counter()
+        if i >= args.warmup:
+            e2e_t.append(t1 - t0)
+        d2h = r.ids.nbytes + r.kinds.nbytes + r.clients.nbytes + r.preds.nbytes + 4 * r.ufc_inc.nbytes + 80
+    e2e_med = float(np.median(e2e_t))
+    if dist:
+        t = torch.tensor([e2e_med], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_med = float(t.item())
+    h2d = sum(v.numel() * v.element_size() for v in host.values())
+    if rank == 0:
+        from paper_2508_16646_b200.sharded import record_bytes
+        rec = record_bytes(c_r, window)
+        line = {
+            "metric": "requests scored+scheduled/sec", "value": value, "unit": "requests/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "p50_ms": p50,
+            "p99_ms": float(np.percentile(step_ms, 99)), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": desc, "policy": "equinox (alpha 0.7, delta 0.1, max_over_clients)",
+                       "predictor": "mope(3) trained by the reference on its builtin corpus (seed 7)",
+                       "queue_per_gpu": n, "l2": "flushed between steps (256 MiB memset outside the events)",
+                       "parallelism": f"client-sharded x{world}: local drain+score+window export, NCCL all-gather "
+                                      f"of {rec} B/rank, replicated exact selection"},
+            "admitted": res.n_admitted,
+            "exchange_bytes_per_rank": rec,
+            "e2e": {"value": world * n / e2e_med, "unit": "requests/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "p50_ms": e2e_med * 1e3},
+            # drain_hist, drain_rank, score, shard_export, shard_ingest, shard_unpack, select, event_fill
+            "gpu_launches": 8 * args.steps,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def run_ours(args, rank, world):
+    if world > 1 or args.sharded or args.config == "cfg4":
+        return run_sharded(args, rank, world)
     import torch
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl")
     q, led, perf, model, prof, desc = load_inputs(args.config, rank)
     n = len(q["client"])
     sch, clients = make_scheduler(q, led, perf, model, prof, local)
@@ -313,7 +455,8 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3"])
+    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3", "cfg4"])
+    ap.add_argument("--sharded", action="store_true", help="client-sharded pipeline even at N=1")
     ap.add_argument("--cpu-reps", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no e2e / cpu legs")
