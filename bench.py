@@ -375,24 +375,53 @@ def run_ours(args, rank, world):
     value = world * n * args.steps / (total_ms * 1e-3)
 
     # ---- e2e through the public API with pinned host buffers ----
-    host = {k: torch.from_numpy(v).pin_memory() for k, v in
-            dict(client=q["client"], arrival_s=q["arrival"], input_tokens=q["in_tokens"], tag=tag_ids(q)).items()}
-    e2e_t = []
+    # Every step copies its batch H2D from pinned memory and reads its events + ledger back.
+    # The batch of step i+1 is staged (eqx_stage_async, copy stream, two staging buffers) while
+    # step i computes, so the steady-state step costs max(H2D, compute) -- what a serving loop
+    # pays.  Two alternating pinned host batches (same content) keep the copies distinct.
+    hosts = [{k: torch.from_numpy(v.copy()).pin_memory() for k, v in
+              dict(client=q["client"], arrival_s=q["arrival"], input_tokens=q["in_tokens"],
+                   tag=tag_ids(q)).items()} for _ in range(2)]
+    e2e_steps = 0 if args.profile else max(8, args.steps)
     d2h = 0
-    for i in range(0 if args.profile else args.warmup + max(3, args.steps // 4)):
-        sch.restore_async()
+
+    def e2e_loop(steps):
+        nonlocal d2h
+        adm = []
+        sch.stage_async(**hosts[0])
+        for i in range(steps):
+            if i + 1 < steps:
+                sch.stage_async(**hosts[(i + 1) % 2])
+            sch.restore_async()
+            sch.drain(**hosts[i % 2])
+            r = sch.step(1.0, with_events=True)
+            led_out = sch.ledger()
+            adm.append(r.n_admitted)
+            d2h = r.ids.nbytes + r.kinds.nbytes + r.clients.nbytes + r.preds.nbytes + 4 * r.ufc_inc.nbytes + \
+                sum(v.nbytes for v in led_out.values()) + 80
+        return adm
+
+    e2e_val, e2e_step_ms, single_ms = None, None, None
+    if e2e_steps:
+        e2e_loop(args.warmup)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        sch.drain(**host)
-        r = sch.step(1.0, with_events=True)
-        led_out = sch.ledger()
+        adm = e2e_loop(e2e_steps)
         t1 = time.perf_counter()
-        if i >= args.warmup:
-            e2e_t.append(t1 - t0)
-        d2h = r.ids.nbytes + r.kinds.nbytes + r.clients.nbytes + r.preds.nbytes + 4 * r.ufc_inc.nbytes + \
-            sum(v.nbytes for v in led_out.values()) + 80
-    h2d = sum(v.numel() * v.element_size() for v in host.values())
-    e2e_val = world * n / float(np.median(e2e_t)) if e2e_t else None
+        assert all(a == res.n_admitted for a in adm)
+        e2e_step_ms = (t1 - t0) * 1e3 / e2e_steps
+        e2e_val = world * n / (e2e_step_ms * 1e-3)
+        single = []
+        for _ in range(5):  # unpipelined latency of one step through the same API
+            sch.restore_async()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            sch.drain(**hosts[0])
+            sch.step(1.0, with_events=True)
+            sch.ledger()
+            single.append(time.perf_counter() - t0)
+        single_ms = float(np.median(single) * 1e3)
+    h2d = sum(v.numel() * v.element_size() for v in hosts[0].values())
 
     if rank != 0:
         if dist:
@@ -432,7 +461,9 @@ def run_ours(args, rank, world):
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "algo_bytes_per_request": ALGO_BYTES_K1, "peak_source": peak_src},
         "e2e": {"value": e2e_val, "unit": "requests/s", "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": int(d2h), "p50_ms": float(np.median(e2e_t) * 1e3) if e2e_t else None},
+                "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_step_ms, "steps": e2e_steps,
+                "single_step_latency_ms": single_ms,
+                "note": "wall clock over consecutive steps; step i+1's H2D (copy stream) overlaps step i"},
         # per step: drain_hist, drain_rank, score, window, select, event_fill
         "gpu_launches": 6 * args.steps,
         "clocks": clk.summary(),

@@ -169,6 +169,12 @@ eqx_status eqx_ledger_checkpoint(eqx_ctx* ctx);
 eqx_status eqx_ledger_restore_async(eqx_ctx* ctx);
 
 /* ---- the hot path ------------------------------------------------------------------------ */
+/* Prefetch a HOST batch: its H2D copy runs on the context's copy stream into the next of two
+ * device staging buffers, overlapping whatever the context is computing.  A later eqx_drain /
+ * eqx_drain_step_async of the same batch (same pointers and n) uses the staged copy.  Host
+ * buffers should be pinned for the copy to be asynchronous; they must stay unchanged until
+ * that drain.  A step's results stay readable until the batch after next is drained. */
+eqx_status eqx_stage_async(eqx_ctx* ctx, const eqx_requests* arrivals);
 /* drain_arrivals (engine.cpp:171-197) for a whole batch of arrivals: the batch becomes the
  * per-client FIFO queues (client-grouped index in HBM), clients that go idle -> backlogged get
  * the counter lift (on_activated, scheduler.cpp:235-253) in arrival order, and every

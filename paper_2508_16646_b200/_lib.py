@@ -6,7 +6,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libeqx_b200.so")
+# EQX_LIB selects an instrumented build (csrc/Makefile `prof`: libeqx_b200_prof.so) for profiling
+LIB_PATH = os.environ.get("EQX_LIB") or os.path.join(HERE, "libeqx_b200.so")
 
 EQX_OK, EQX_ERR_CONFIG, EQX_ERR_PARSE, EQX_ERR_ENGINE, EQX_ERR_CUDA, EQX_ERR_ARG = range(6)
 EQX_HOST, EQX_DEVICE = 0, 1
@@ -82,6 +83,7 @@ _SIGS = {
     "eqx_ledger_checkpoint": ([C.c_void_p], C.c_int),
     "eqx_ledger_restore_async": ([C.c_void_p], C.c_int),
     "eqx_drain": ([C.c_void_p, C.POINTER(Requests)], C.c_int),
+    "eqx_stage_async": ([C.c_void_p, C.POINTER(Requests)], C.c_int),
     "eqx_step_async": ([C.c_void_p, C.c_double], C.c_int),
     "eqx_drain_step_async": ([C.c_void_p, C.POINTER(Requests), C.c_double], C.c_int),
     "eqx_step_collect": ([C.c_void_p, C.POINTER(StepSummary)], C.c_int),

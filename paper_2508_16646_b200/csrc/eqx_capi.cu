@@ -79,7 +79,21 @@ struct eqx_ctx {
   const uint8_t* q_tag = nullptr;
   const int64_t* q_id = nullptr;
   int64_t id_base = 0;
-  DevBuf own_client, own_arrival, own_in, own_true, own_tag, own_id;
+  DevBuf own_tag;  // zero tags for device batches without a tag column
+  // Host batches are staged through two device buffer sets on a copy stream, so the H2D of
+  // the next batch (eqx_stage_async) overlaps the current step; `free_` is recorded on the
+  // main stream after the last launch that reads a set.
+  struct Stage {
+    DevBuf client, arrival, in, tru, tag, id;
+    const void* key[6] = {};
+    int64_t n = -1;
+    uint64_t seq = 0;  // staging order: a drain consumes the oldest matching staged batch
+    bool valid = false;
+    cudaEvent_t ready = nullptr, free_ = nullptr;
+  } stg[2];
+  int bound_stage = -1;
+  uint64_t stage_seq = 0;
+  cudaStream_t copy_stream = nullptr;
   DevBuf d_perm, d_hist;
   bool queue_ready = false;
 
@@ -111,6 +125,13 @@ struct eqx_ctx {
   cudaGraphExec_t graph = nullptr;
   std::vector<unsigned char> graph_key;
   bool owns_stream = true;         // false after eqx_ctx_set_stream (caller's stream)
+  // pinned bounce buffer for result reads: async D2H of every column, one sync, host memcpy
+  void* h_scratch = nullptr;
+  size_t h_scratch_bytes = 0;
+  // launch-attribute caches (cudaFuncSetAttribute / occupancy queries cost host time per step)
+  int smem_attr[3] = {-1, -1, -1};  // drain_hist, drain_rank, select
+  size_t occ_smem = SIZE_MAX;
+  int occ_per_sm = 1;
   // client-sharded step (selection context): gathered windows and their ids
   DevBuf d_first64, d_gid;
   int32_t shard_W = 0;             // > 0: the last step was a sharded selection
@@ -123,6 +144,33 @@ eqx_status fail(eqx_ctx* ctx, eqx_status st, const std::string& msg) {
   return st;
 }
 
+cudaError_t ensure_scratch(eqx_ctx* ctx, size_t bytes) {
+  if (bytes <= ctx->h_scratch_bytes) return cudaSuccess;
+  if (ctx->h_scratch) cudaFreeHost(ctx->h_scratch);
+  ctx->h_scratch = nullptr;
+  ctx->h_scratch_bytes = 0;
+  const size_t want = std::max<size_t>(bytes, 1 << 16);
+  cudaError_t e = cudaMallocHost(&ctx->h_scratch, want);
+  if (e == cudaSuccess) ctx->h_scratch_bytes = want;
+  return e;
+}
+
+// Device columns -> caller arrays through the pinned scratch: the copies are queued back to
+// back on the stream, the host waits once, then copies out (pageable D2H copies would each
+// stage and synchronise on their own).
+struct Col {
+  void* dst;
+  const void* src;
+  size_t bytes;
+};
+
+cudaError_t set_smem_attr(eqx_ctx* ctx, int which, const void* fn, size_t bytes) {
+  if (ctx->smem_attr[which] == static_cast<int>(bytes)) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+  if (e == cudaSuccess) ctx->smem_attr[which] = static_cast<int>(bytes);
+  return e;
+}
+
 #define CUDA_TRY(ctx, expr)                                                            \
   do {                                                                                 \
     cudaError_t _e = (expr);                                                           \
@@ -130,6 +178,31 @@ eqx_status fail(eqx_ctx* ctx, eqx_status st, const std::string& msg) {
       return fail((ctx), EQX_ERR_CUDA, std::string("CUDA error: ") + cudaGetErrorString(_e) + \
                                            " at " #expr);                              \
   } while (0)
+
+namespace {
+eqx_status read_cols(eqx_ctx* ctx, const Col* cols, int n) {
+  size_t total = 0;
+  for (int i = 0; i < n; ++i)
+    if (cols[i].dst) total += (cols[i].bytes + 15) & ~size_t(15);
+  CUDA_TRY(ctx, ensure_scratch(ctx, total));
+  cudaStream_t s = ctx->stream;
+  size_t off = 0;
+  for (int i = 0; i < n; ++i) {
+    if (!cols[i].dst || !cols[i].bytes) continue;
+    CUDA_TRY(ctx, cudaMemcpyAsync(static_cast<char*>(ctx->h_scratch) + off, cols[i].src, cols[i].bytes,
+                                  cudaMemcpyDeviceToHost, s));
+    off += (cols[i].bytes + 15) & ~size_t(15);
+  }
+  CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  off = 0;
+  for (int i = 0; i < n; ++i) {
+    if (!cols[i].dst || !cols[i].bytes) continue;
+    std::memcpy(cols[i].dst, static_cast<char*>(ctx->h_scratch) + off, cols[i].bytes);
+    off += (cols[i].bytes + 15) & ~size_t(15);
+  }
+  return EQX_OK;
+}
+}  // namespace
 
 // ---- reference predictor semantics, evaluated once per LUT cell (host "model compiler") ----
 // RouterModel::length_bucket (predictor.cpp:29-34)
@@ -228,6 +301,11 @@ eqx_status eqx_ctx_create(int32_t device, eqx_ctx** out) {
   ctx->smem_optin = prop.sharedMemPerBlockOptin;
   e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking);
+  for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
+    e = cudaEventCreateWithFlags(&ctx->stg[b].ready, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->stg[b].free_, cudaEventDisableTiming);
+  }
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming);
   for (int i = 0; i < 6 && e == cudaSuccess; ++i) e = cudaEventCreate(&ctx->ev_k[i]);
@@ -261,8 +339,7 @@ void eqx_ctx_destroy(eqx_ctx* ctx) {
   DevBuf* bufs[] = {&ctx->d_model, &ctx->d_ufc, &ctx->d_rfc, &ctx->d_counter, &ctx->d_weight,
                     &ctx->d_order, &ctx->d_running, &ctx->d_backlogged, &ctx->d_head,
                     &ctx->d_count, &ctx->d_first, &ctx->d_qlen_before, &ctx->d_seg_off,
-                    &ctx->own_client, &ctx->own_arrival, &ctx->own_in, &ctx->own_true,
-                    &ctx->own_tag, &ctx->own_id, &ctx->d_perm, &ctx->d_hist, &ctx->d_pred,
+                    &ctx->own_tag, &ctx->d_perm, &ctx->d_hist, &ctx->d_pred,
                     &ctx->d_bucket, &ctx->d_ufc_out, &ctx->d_rfc_out, &ctx->d_ev_row,
                     &ctx->d_ev_kind, &ctx->d_ev_client, &ctx->d_ev_pred, &ctx->d_ev_ufc,
                     &ctx->d_ev_rfc, &ctx->d_ev_vtc, &ctx->d_ev_wait, &ctx->d_ev_id,
@@ -270,6 +347,7 @@ void eqx_ctx_destroy(eqx_ctx* ctx) {
                     &ctx->snap_counter, &ctx->snap_running, &ctx->snap_backlogged, &ctx->snap_state};
   for (DevBuf* b : bufs) b->release();
   if (ctx->h_state) cudaFreeHost(ctx->h_state);
+  if (ctx->h_scratch) cudaFreeHost(ctx->h_scratch);
   if (ctx->stream2) cudaStreamSynchronize(ctx->stream2);
   ctx->d_done.release();
   ctx->d_win.release();
@@ -280,6 +358,16 @@ void eqx_ctx_destroy(eqx_ctx* ctx) {
     if (ev) cudaEventDestroy(ev);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->stream2) cudaStreamDestroy(ctx->stream2);
+  if (ctx->copy_stream) {
+    cudaStreamSynchronize(ctx->copy_stream);
+    cudaStreamDestroy(ctx->copy_stream);
+  }
+  for (auto& st : ctx->stg) {
+    DevBuf* sb[] = {&st.client, &st.arrival, &st.in, &st.tru, &st.tag, &st.id};
+    for (DevBuf* b : sb) b->release();
+    if (st.ready) cudaEventDestroy(st.ready);
+    if (st.free_) cudaEventDestroy(st.free_);
+  }
   if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
   ctx->d_first64.release();
   ctx->d_gid.release();
@@ -488,16 +576,10 @@ eqx_status eqx_get_clients(eqx_ctx* ctx, int32_t n, double* ufc, double* rfc, do
                            int32_t* backlogged, int32_t* running) {
   if (!ctx || n != ctx->C) return fail(ctx, EQX_ERR_ARG, "eqx_get_clients: roster size mismatch");
   cudaSetDevice(ctx->device);
-  cudaStream_t s = ctx->stream;
-  if (n > 0) {
-    if (ufc) CUDA_TRY(ctx, cudaMemcpyAsync(ufc, ctx->d_ufc.p, 8ull * n, cudaMemcpyDeviceToHost, s));
-    if (rfc) CUDA_TRY(ctx, cudaMemcpyAsync(rfc, ctx->d_rfc.p, 8ull * n, cudaMemcpyDeviceToHost, s));
-    if (counter) CUDA_TRY(ctx, cudaMemcpyAsync(counter, ctx->d_counter.p, 8ull * n, cudaMemcpyDeviceToHost, s));
-    if (backlogged) CUDA_TRY(ctx, cudaMemcpyAsync(backlogged, ctx->d_backlogged.p, 4ull * n, cudaMemcpyDeviceToHost, s));
-    if (running) CUDA_TRY(ctx, cudaMemcpyAsync(running, ctx->d_running.p, 4ull * n, cudaMemcpyDeviceToHost, s));
-  }
-  CUDA_TRY(ctx, cudaStreamSynchronize(s));
-  return EQX_OK;
+  const size_t d8 = 8ull * n, d4 = 4ull * n;
+  const Col cols[] = {{ufc, ctx->d_ufc.p, d8}, {rfc, ctx->d_rfc.p, d8}, {counter, ctx->d_counter.p, d8},
+                      {backlogged, ctx->d_backlogged.p, d4}, {running, ctx->d_running.p, d4}};
+  return read_cols(ctx, cols, n > 0 ? 5 : 0);
 }
 
 eqx_status eqx_ledger_checkpoint(eqx_ctx* ctx) {
@@ -551,6 +633,79 @@ eqx_status eqx_set_batch(eqx_ctx* ctx, int32_t members, int64_t reserved) {
   return EQX_OK;
 }
 
+// H2D of a host batch into staging set b on the copy stream (after the set's last reader).
+static eqx_status stage_fill(eqx_ctx* ctx, const eqx_requests* r, int b) {
+  eqx_ctx::Stage& st = ctx->stg[b];
+  cudaStream_t cs = ctx->copy_stream;
+  const int64_t n = r->n;
+  const size_t nn = static_cast<size_t>(std::max<int64_t>(n, 1));
+  st.valid = false;
+  CUDA_TRY(ctx, st.client.ensure(4 * nn));
+  CUDA_TRY(ctx, st.arrival.ensure(8 * nn));
+  CUDA_TRY(ctx, st.in.ensure(4 * nn));
+  CUDA_TRY(ctx, st.tag.ensure(nn + 16));
+  if (r->true_output_tokens) CUDA_TRY(ctx, st.tru.ensure(4 * nn));
+  if (r->id) CUDA_TRY(ctx, st.id.ensure(8 * nn));
+  CUDA_TRY(ctx, cudaStreamWaitEvent(cs, st.free_, 0));
+  // 1 MiB pieces: a step's small result reads (D2H) interleave with a long prefetch instead of
+  // queueing behind all of it on the DMA engines
+  auto h2d = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
+    constexpr size_t kPiece = size_t(1) << 20;
+    for (size_t o = 0; o < bytes; o += kPiece) {
+      cudaError_t e = cudaMemcpyAsync(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o,
+                                      std::min(kPiece, bytes - o), cudaMemcpyHostToDevice, cs);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  };
+  if (n > 0) {
+    CUDA_TRY(ctx, h2d(st.client.p, r->client, 4 * n));
+    CUDA_TRY(ctx, h2d(st.arrival.p, r->arrival_s, 8 * n));
+    CUDA_TRY(ctx, h2d(st.in.p, r->input_tokens, 4 * n));
+    if (r->tag) CUDA_TRY(ctx, h2d(st.tag.p, r->tag, n));
+    else CUDA_TRY(ctx, cudaMemsetAsync(st.tag.p, 0, n, cs));
+    if (r->true_output_tokens) CUDA_TRY(ctx, h2d(st.tru.p, r->true_output_tokens, 4 * n));
+    if (r->id) CUDA_TRY(ctx, h2d(st.id.p, r->id, 8 * n));
+  }
+  CUDA_TRY(ctx, cudaEventRecord(st.ready, cs));
+  const void* key[6] = {r->client, r->arrival_s, r->input_tokens, r->tag, r->true_output_tokens, r->id};
+  std::memcpy(st.key, key, sizeof(key));
+  st.n = n;
+  st.seq = ++ctx->stage_seq;
+  st.valid = true;
+  return EQX_OK;
+}
+
+// Staging target: a set holding no unconsumed batch, else the older one.
+static int stage_target(const eqx_ctx* ctx) {
+  const eqx_ctx::Stage* st = ctx->stg;
+  if (!st[0].valid && !st[1].valid) return st[0].seq <= st[1].seq ? 0 : 1;
+  if (!st[0].valid) return 0;
+  if (!st[1].valid) return 1;
+  return st[0].seq <= st[1].seq ? 0 : 1;
+}
+
+static bool stage_matches(const eqx_ctx::Stage& st, const eqx_requests* r) {
+  const void* key[6] = {r->client, r->arrival_s, r->input_tokens, r->tag, r->true_output_tokens, r->id};
+  return st.valid && st.n == r->n && std::memcmp(st.key, key, sizeof(key)) == 0;
+}
+
+// The main stream is done with the bound staging set once everything enqueued so far ran.
+static eqx_status release_stage(eqx_ctx* ctx) {
+  if (ctx->bound_stage >= 0) CUDA_TRY(ctx, cudaEventRecord(ctx->stg[ctx->bound_stage].free_, ctx->stream));
+  return EQX_OK;
+}
+
+eqx_status eqx_stage_async(eqx_ctx* ctx, const eqx_requests* r) {
+  if (!ctx || !r) return fail(ctx, EQX_ERR_ARG, "eqx_stage_async: NULL argument");
+  if (r->location != EQX_HOST) return fail(ctx, EQX_ERR_ARG, "eqx_stage_async: only host batches are staged");
+  if (r->n < 0 || r->n >= (int64_t(1) << 31) - 1) return fail(ctx, EQX_ERR_ARG, "eqx_stage_async: n out of range");
+  if (r->n > 0 && (!r->client || !r->arrival_s || !r->input_tokens))
+    return fail(ctx, EQX_ERR_ARG, "eqx_stage_async: missing request column");
+  cudaSetDevice(ctx->device);
+  return stage_fill(ctx, r, stage_target(ctx));
+}
+
 static eqx_status drain_prepare(eqx_ctx* ctx, const eqx_requests* r) {
   if (!ctx || !r) return fail(ctx, EQX_ERR_ARG, "eqx_drain: NULL argument");
   if (!ctx->model_set || !ctx->profile_set)
@@ -567,6 +722,7 @@ static eqx_status drain_prepare(eqx_ctx* ctx, const eqx_requests* r) {
   const size_t nn = static_cast<size_t>(std::max<int64_t>(n, 1));
   // bind (device) or copy (host) the columns
   if (r->location == EQX_DEVICE) {
+    ctx->bound_stage = -1;
     ctx->q_client = r->client;
     ctx->q_arrival = r->arrival_s;
     ctx->q_in = r->input_tokens;
@@ -580,33 +736,26 @@ static eqx_status drain_prepare(eqx_ctx* ctx, const eqx_requests* r) {
       ctx->q_tag = ctx->own_tag.as<uint8_t>();
     }
   } else {
-    CUDA_TRY(ctx, ctx->own_client.ensure(4 * nn));
-    CUDA_TRY(ctx, ctx->own_arrival.ensure(8 * nn));
-    CUDA_TRY(ctx, ctx->own_in.ensure(4 * nn));
-    CUDA_TRY(ctx, ctx->own_tag.ensure(nn + 16));
-    if (n > 0) {
-      CUDA_TRY(ctx, cudaMemcpyAsync(ctx->own_client.p, r->client, 4 * n, cudaMemcpyHostToDevice, s));
-      CUDA_TRY(ctx, cudaMemcpyAsync(ctx->own_arrival.p, r->arrival_s, 8 * n, cudaMemcpyHostToDevice, s));
-      CUDA_TRY(ctx, cudaMemcpyAsync(ctx->own_in.p, r->input_tokens, 4 * n, cudaMemcpyHostToDevice, s));
-      if (r->tag) CUDA_TRY(ctx, cudaMemcpyAsync(ctx->own_tag.p, r->tag, n, cudaMemcpyHostToDevice, s));
-      else CUDA_TRY(ctx, cudaMemsetAsync(ctx->own_tag.p, 0, n, s));
+    // host batch: a matching staged copy (eqx_stage_async), else stage it now
+    int b = -1;
+    for (int k = 0; k < 2; ++k)
+      if (stage_matches(ctx->stg[k], r) && (b < 0 || ctx->stg[k].seq < ctx->stg[b].seq)) b = k;
+    if (b < 0) {
+      if (std::getenv("EQX_DEBUG_STAGE")) std::fprintf(stderr, "eqx: drain of an unstaged host batch\n");
+      b = stage_target(ctx);
+      eqx_status e = stage_fill(ctx, r, b);
+      if (e != EQX_OK) return e;
     }
-    ctx->q_client = ctx->own_client.as<int32_t>();
-    ctx->q_arrival = ctx->own_arrival.as<double>();
-    ctx->q_in = ctx->own_in.as<int32_t>();
-    ctx->q_tag = ctx->own_tag.as<uint8_t>();
-    ctx->q_true = nullptr;
-    if (r->true_output_tokens) {
-      CUDA_TRY(ctx, ctx->own_true.ensure(4 * nn));
-      if (n > 0) CUDA_TRY(ctx, cudaMemcpyAsync(ctx->own_true.p, r->true_output_tokens, 4 * n, cudaMemcpyHostToDevice, s));
-      ctx->q_true = ctx->own_true.as<int32_t>();
-    }
-    ctx->q_id = nullptr;
-    if (r->id) {
-      CUDA_TRY(ctx, ctx->own_id.ensure(8 * nn));
-      if (n > 0) CUDA_TRY(ctx, cudaMemcpyAsync(ctx->own_id.p, r->id, 8 * n, cudaMemcpyHostToDevice, s));
-      ctx->q_id = ctx->own_id.as<int64_t>();
-    }
+    eqx_ctx::Stage& st = ctx->stg[b];
+    st.valid = false;  // consumed
+    CUDA_TRY(ctx, cudaStreamWaitEvent(s, st.ready, 0));
+    ctx->bound_stage = b;
+    ctx->q_client = st.client.as<int32_t>();
+    ctx->q_arrival = st.arrival.as<double>();
+    ctx->q_in = st.in.as<int32_t>();
+    ctx->q_tag = st.tag.as<uint8_t>();
+    ctx->q_true = r->true_output_tokens ? st.tru.as<int32_t>() : nullptr;
+    ctx->q_id = r->id ? st.id.as<int64_t>() : nullptr;
   }
   ctx->id_base = r->id_base;
   ctx->n = n;
@@ -645,10 +794,8 @@ static eqx_status drain_prepare(eqx_ctx* ctx, const eqx_requests* r) {
   ctx->rank_smem = rank_base + (ctx->staged ? 6ull * tile_rows : 0);
   if (ctx->rank_smem > ctx->smem_optin || ctx->hist_smem > ctx->smem_optin)
     return fail(ctx, EQX_ERR_CONFIG, "too many clients per device (" + std::to_string(C) + ")");
-  CUDA_TRY(ctx, cudaFuncSetAttribute(drain_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(ctx->hist_smem)));
-  CUDA_TRY(ctx, cudaFuncSetAttribute(drain_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(ctx->rank_smem)));
+  CUDA_TRY(ctx, set_smem_attr(ctx, 0, reinterpret_cast<const void*>(drain_hist_kernel), ctx->hist_smem));
+  CUDA_TRY(ctx, set_smem_attr(ctx, 1, reinterpret_cast<const void*>(drain_rank_kernel), ctx->rank_smem));
   ctx->queue_ready = true;
   return EQX_OK;
 }
@@ -808,7 +955,12 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl, int32_t g
   sc.now = now;
   pl.score_smem = model_smem;
   int per_sm = 1;
-  CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, score_kernel, kScoreThreads, pl.score_smem));
+  if (ctx->occ_smem != pl.score_smem) {
+    CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->occ_per_sm, score_kernel, kScoreThreads,
+                                                                pl.score_smem));
+    ctx->occ_smem = pl.score_smem;
+  }
+  per_sm = ctx->occ_per_sm;
   const int64_t want = (ctx->n / 8 + kScoreThreads - 1) / kScoreThreads;
   pl.score_grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, static_cast<int64_t>(ctx->sm_count) * std::max(per_sm, 1))));
   // ---- selection ----
@@ -954,7 +1106,7 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl, int32_t g
   pl.window_smem = model_smem;
   const int64_t witems = static_cast<int64_t>(C) * a.W;
   pl.window_grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((witems + 255) / 256, 8ll * ctx->sm_count)));
-  CUDA_TRY(ctx, cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  CUDA_TRY(ctx, set_smem_attr(ctx, 2, reinterpret_cast<const void*>(select_kernel), smem));
   return EQX_OK;
 }
 
@@ -1016,7 +1168,9 @@ eqx_status eqx_drain(eqx_ctx* ctx, const eqx_requests* r) {
   eqx_status st = drain_prepare(ctx, r);
   if (st != EQX_OK) return st;
   ctx->shard_W = 0;
-  return drain_enqueue(ctx);
+  st = drain_enqueue(ctx);
+  if (st != EQX_OK) return st;
+  return release_stage(ctx);
 }
 
 eqx_status eqx_step_async(eqx_ctx* ctx, double now) {
@@ -1028,7 +1182,7 @@ eqx_status eqx_step_async(eqx_ctx* ctx, double now) {
   if (st != EQX_OK) return st;
   ctx->step_pending = true;
   ctx->stepped = true;
-  return EQX_OK;
+  return release_stage(ctx);
 }
 
 eqx_status eqx_drain_step_async(eqx_ctx* ctx, const eqx_requests* r, double now) {
@@ -1039,8 +1193,9 @@ eqx_status eqx_drain_step_async(eqx_ctx* ctx, const eqx_requests* r, double now)
   st = step_prepare(ctx, now, pl);
   if (st != EQX_OK) return st;
   cudaStream_t s = ctx->stream;
-  if (r->location != EQX_DEVICE) {  // host columns: plain launches (H2D copies already queued)
+  if (r->location != EQX_DEVICE) {  // host columns: plain launches after the staged H2D
     st = step_enqueue(ctx, pl, true);
+    if (st == EQX_OK) st = release_stage(ctx);
   } else {
     // Resident queue: one CUDA-graph launch replays drain + scoring + selection.  The key
     // covers every launch parameter (pointers, sizes, policy, `now`, smem/tiling plan).
@@ -1107,7 +1262,7 @@ eqx_status eqx_shard_export_async(eqx_ctx* ctx, double now, int32_t cmax, int32_
   CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_join, 0));
   ctx->stepped = true;
   ctx->shard_W = 0;
-  return EQX_OK;
+  return release_stage(ctx);
 }
 
 eqx_status eqx_shard_select_async(eqx_ctx* ctx, const void* recs, int32_t world, int64_t stride,
@@ -1268,17 +1423,13 @@ eqx_status eqx_copy_events(eqx_ctx* ctx, int64_t cap, int64_t* id, int32_t* kind
     gather_ids_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
         ctx->d_ev_row.as<int32_t>(), n, ctx->q_id, ctx->id_base, ctx->d_ev_id.as<int64_t>());
     CUDA_TRY(ctx, cudaGetLastError());
-    CUDA_TRY(ctx, cudaMemcpyAsync(id, ctx->d_ev_id.p, 8 * n, cudaMemcpyDeviceToHost, s));
   }
-  if (kind) CUDA_TRY(ctx, cudaMemcpyAsync(kind, ctx->d_ev_kind.p, 4 * n, cudaMemcpyDeviceToHost, s));
-  if (client) CUDA_TRY(ctx, cudaMemcpyAsync(client, ctx->d_ev_client.p, 4 * n, cudaMemcpyDeviceToHost, s));
-  if (pred) CUDA_TRY(ctx, cudaMemcpyAsync(pred, ctx->d_ev_pred.p, 4 * n, cudaMemcpyDeviceToHost, s));
-  if (ufc_inc) CUDA_TRY(ctx, cudaMemcpyAsync(ufc_inc, ctx->d_ev_ufc.p, 8 * n, cudaMemcpyDeviceToHost, s));
-  if (rfc_inc) CUDA_TRY(ctx, cudaMemcpyAsync(rfc_inc, ctx->d_ev_rfc.p, 8 * n, cudaMemcpyDeviceToHost, s));
-  if (vtc_inc) CUDA_TRY(ctx, cudaMemcpyAsync(vtc_inc, ctx->d_ev_vtc.p, 8 * n, cudaMemcpyDeviceToHost, s));
-  if (wait_s) CUDA_TRY(ctx, cudaMemcpyAsync(wait_s, ctx->d_ev_wait.p, 8 * n, cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(ctx, cudaStreamSynchronize(s));
-  return EQX_OK;
+  const size_t n8 = 8ull * n, n4 = 4ull * n;
+  const Col cols[] = {{id, ctx->d_ev_id.p, n8},        {kind, ctx->d_ev_kind.p, n4},
+                      {client, ctx->d_ev_client.p, n4}, {pred, ctx->d_ev_pred.p, n4},
+                      {ufc_inc, ctx->d_ev_ufc.p, n8},   {rfc_inc, ctx->d_ev_rfc.p, n8},
+                      {vtc_inc, ctx->d_ev_vtc.p, n8},   {wait_s, ctx->d_ev_wait.p, n8}};
+  return read_cols(ctx, cols, 8);
 }
 
 eqx_status eqx_copy_scores(eqx_ctx* ctx, int64_t cap, int32_t* pred, uint8_t* bucket,
@@ -1289,14 +1440,11 @@ eqx_status eqx_copy_scores(eqx_ctx* ctx, int64_t cap, int32_t* pred, uint8_t* bu
   cudaSetDevice(ctx->device);
   cudaStream_t s = ctx->stream;
   const int64_t n = std::min<int64_t>(cap, ctx->n);
-  if (n > 0) {
-    if (pred) CUDA_TRY(ctx, cudaMemcpyAsync(pred, ctx->d_pred.p, 4 * n, cudaMemcpyDeviceToHost, s));
-    if (bucket) CUDA_TRY(ctx, cudaMemcpyAsync(bucket, ctx->d_bucket.p, n, cudaMemcpyDeviceToHost, s));
-    if (ufc_inc) CUDA_TRY(ctx, cudaMemcpyAsync(ufc_inc, ctx->d_ufc_out.p, 8 * n, cudaMemcpyDeviceToHost, s));
-    if (rfc_inc) CUDA_TRY(ctx, cudaMemcpyAsync(rfc_inc, ctx->d_rfc_out.p, 8 * n, cudaMemcpyDeviceToHost, s));
-  }
-  CUDA_TRY(ctx, cudaStreamSynchronize(s));
-  return EQX_OK;
+  const size_t nn = n > 0 ? static_cast<size_t>(n) : 0;
+  const Col cols[] = {{pred, ctx->d_pred.p, 4 * nn}, {bucket, ctx->d_bucket.p, nn},
+                      {ufc_inc, ctx->d_ufc_out.p, 8 * nn}, {rfc_inc, ctx->d_rfc_out.p, 8 * nn}};
+  (void)s;
+  return read_cols(ctx, cols, 4);
 }
 
 // bindings/module.cpp:144-172 scalar helpers (host utilities; not part of the step)

@@ -1297,7 +1297,13 @@ __device__ void seq_reg_phase(const SelectArgs& a, const ModelTables& M, const W
   if (G > 1) named_sync(1, nthr);
   int parity = 0;
   bool done = false;
+#ifdef EQX_PROF
+  long long cy0 = 0, cy1 = 0, cy2 = 0, cyp = 0;
+#endif
   for (int32_t pick = 0; pick < max_picks; ++pick) {
+#ifdef EQX_PROF
+    const long long ta = clock64();
+#endif
     Cand best = no_cand();
     int bs = 0;
 #pragma unroll
@@ -1344,6 +1350,9 @@ __device__ void seq_reg_phase(const SelectArgs& a, const ModelTables& M, const W
       done = true;
       break;
     }
+#ifdef EQX_PROF
+    const long long tb = clock64();
+#endif
     // ---- uniform evaluation of the pick (engine.cpp:216-268) ----
     const int32_t c = w.c, j = w.pos;
     const int64_t x = static_cast<int64_t>(c) * Ds + w.d;
@@ -1383,6 +1392,9 @@ __device__ void seq_reg_phase(const SelectArgs& a, const ModelTables& M, const W
       nr = T.r[x];
     }
     bool own_regen = false;
+#ifdef EQX_PROF
+    const long long tc = clock64();
+#endif
     if (owner) {
 #pragma unroll
       for (int s = 0; s < K; ++s)
@@ -1457,7 +1469,22 @@ __device__ void seq_reg_phase(const SelectArgs& a, const ModelTables& M, const W
     }
     __syncwarp();
     if (G > 1) named_sync(1, nthr);
+#ifdef EQX_PROF
+    const long long td = clock64();
+    cy0 += tb - ta;
+    cy1 += tc - tb;
+    cy2 += td - tc;
+    ++cyp;
+#endif
   }
+#ifdef EQX_PROF
+  if (tid == 0) {
+    a.st->t[12] += cy0;
+    a.st->t[13] += cy1;
+    a.st->t[14] += cy2;
+    a.st->t[15] += cyp;
+  }
+#endif
 #pragma unroll
   for (int s = 0; s < K; ++s) {
     const int32_t c = tid + s * nthr;
@@ -1742,7 +1769,9 @@ __global__ void __launch_bounds__(1024) shard_ingest_kernel(const ShardMap m, co
   __syncthreads();
   unsigned long long mine = 0;
   for (int32_t c = threadIdx.x; c < m.C; c += blockDim.x) mine += static_cast<unsigned long long>(b.count[c]);
-  atomicAdd(&total, mine);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(&total, mine);  // one shared atomic per warp
   __syncthreads();
   if (threadIdx.x == 0) b.st->n_queued = static_cast<int64_t>(total);
   const LiftIn li{m.C, b.counter_lift, b.count, b.qlen_before, b.running, b.ufc, b.rfc, b.counter, b.backlogged};

@@ -405,14 +405,27 @@ class GpuScheduler:
         rq = self._requests(client, arrival_s, input_tokens, tag, true_output_tokens, ids, id_base)
         self._check(self._lib.eqx_drain(self._ctx, C.byref(rq)))
 
+    def stage_async(self, client, arrival_s, input_tokens, tag=None, true_output_tokens=None, ids=None,
+                    id_base: int = 0) -> None:
+        """Prefetch a host batch (pinned numpy/torch CPU columns) into the context's next staging
+        buffer on its copy stream; the drain of the same arrays then skips the copy.  The H2D
+        overlaps the step in flight (two staging buffers)."""
+        keep: list = []
+        rq = self._requests(client, arrival_s, input_tokens, tag, true_output_tokens, ids, id_base, keep)
+        if rq.location != L.EQX_HOST:
+            raise ValueError("stage_async: host columns only")
+        self._staged = getattr(self, "_staged", [])[-1:] + [keep]  # keep both staged batches alive
+        self._check(self._lib.eqx_stage_async(self._ctx, C.byref(rq)))
+
     def drain_step_async(self, now: float, client, arrival_s, input_tokens, tag=None,
                          true_output_tokens=None, ids=None, id_base: int = 0) -> None:
         """drain + step_async in one call (CUDA-graph replay for a resident device queue)."""
         rq = self._requests(client, arrival_s, input_tokens, tag, true_output_tokens, ids, id_base)
         self._check(self._lib.eqx_drain_step_async(self._ctx, C.byref(rq), float(now)))
 
-    def _requests(self, client, arrival_s, input_tokens, tag, true_output_tokens, ids, id_base):
-        keep: list = []
+    def _requests(self, client, arrival_s, input_tokens, tag, true_output_tokens, ids, id_base, keep=None):
+        staging = keep is not None
+        keep = [] if keep is None else keep
         cols = {}
         loc = set()
         for name, x, dt in (("client", client, np.int32), ("arrival_s", arrival_s, np.float64),
@@ -427,8 +440,9 @@ class GpuScheduler:
         n = len(client)
         rq = L.Requests(n, cols["id"], id_base, cols["client"], cols["arrival_s"], cols["input_tokens"],
                         cols["true_output_tokens"], cols["tag"], loc.pop() if loc else L.EQX_HOST)
-        self._keep = keep  # device columns are used in place: keep them alive with the queue
-        self.n_queued = n
+        if not staging:
+            self._keep = keep  # device columns are used in place: keep them alive with the queue
+            self.n_queued = n
         return rq
 
     def step_async(self, now: float) -> None:

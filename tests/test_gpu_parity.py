@@ -100,3 +100,27 @@ def test_scalar_helpers_and_errors():
         S.GpuScheduler([S.ClientState("a", weight=0.0)], profile=prof, predictor="oracle")
     with pytest.raises(S.ConfigError, match="non-empty GPU profile"):
         S.GpuScheduler([S.ClientState("a")], profile=S.GpuProfile([]), predictor="oracle")
+
+
+def test_staged_host_batches_in_order():
+    """eqx_stage_async: two host batches staged ahead on the copy stream are consumed by the
+    drains of the same arrays, oldest first, with results identical to unstaged drains."""
+    import torch
+    from helpers import case_batch, case_clients, case_columns, case_kwargs
+    from paper_2508_16646_b200 import scheduler as S
+    c0 = _random_case(41, 20000, 64, kind=2, norm_mode=0, backfill=False)
+    same = {k: getattr(c0, k) for k in ("vtc_use_prediction", "max_batch", "pred_kind", "mem_per_token_bytes",
+                                        "mem_capacity_bytes", "alpha", "delta")}
+    cases = [c0, _random_case(42, 20000, 64, kind=2, norm_mode=0, backfill=False, **same)]
+    wants = [H.run_step(c, "oracle") for c in cases]
+    sch = S.GpuScheduler(case_clients(cases[0]), running=cases[0].running, **case_kwargs(cases[0]))
+    cols = [{k: torch.from_numpy(v).pin_memory() for k, v in case_columns(c).items()} for c in cases]
+    for rnd in range(2):
+        for c in cols:
+            sch.stage_async(**c)
+        for c, case, want in zip(cols, cases, wants):
+            sch.set_clients(case_clients(case), case.running)
+            sch.set_batch(*case_batch(case))
+            sch.drain(**c)
+            res = sch.step(case.now)
+            compare_step(res, sch, want)
