@@ -129,7 +129,7 @@ struct eqx_ctx {
   void* h_scratch = nullptr;
   size_t h_scratch_bytes = 0;
   // launch-attribute caches (cudaFuncSetAttribute / occupancy queries cost host time per step)
-  int smem_attr[3] = {-1, -1, -1};  // drain_hist, drain_rank, select
+  int smem_attr[8] = {-1, -1, -1, -1, -1, -1, -1, -1};  // drain_hist, drain_rank, select kernels (select_fn)
   size_t occ_smem = SIZE_MAX;
   int occ_per_sm = 1;
   // client-sharded step (selection context): gathered windows and their ids
@@ -163,6 +163,18 @@ struct Col {
   const void* src;
   size_t bytes;
 };
+
+// warp_sel: 0 multi-mode select_kernel; 1 single-warp (shared-memory slots); 2/3/4 single-warp
+// with 1/2/4 register slots per lane
+const void* select_fn(int warp_sel) {
+  switch (warp_sel) {
+    case 1: return reinterpret_cast<const void*>(select_warp_kernel<0>);
+    case 2: return reinterpret_cast<const void*>(select_warp_kernel<1>);
+    case 3: return reinterpret_cast<const void*>(select_warp_kernel<2>);
+    case 4: return reinterpret_cast<const void*>(select_warp_kernel<4>);
+    default: return reinterpret_cast<const void*>(select_kernel);
+  }
+}
 
 cudaError_t set_smem_attr(eqx_ctx* ctx, int which, const void* fn, size_t bytes) {
   if (ctx->smem_attr[which] == static_cast<int>(bytes)) return cudaSuccess;
@@ -1044,6 +1056,7 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl, int32_t g
     return static_cast<size_t>(tn * (sizeof(BatchItem) + 1) + 16 * 3 + 4ll * C);
   };
   int64_t D = std::min<int64_t>(8, std::max<int64_t>(2, 2 * static_cast<int64_t>(ctx->perf.max_batch) / std::max(C, 1) + 2));
+  if (const char* bd = std::getenv("EQX_BATCH_D")) D = std::max<int64_t>(2, std::atoi(bd));  // experiments
   while (D >= 2 && (static_cast<int64_t>(C) * D > 8192 ||
                     batch_bytes(D) + static_cast<size_t>(D) * C * sizeof(WinEntry) > left0))
     --D;
@@ -1053,6 +1066,7 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl, int32_t g
   {
     const char* m = std::getenv("EQX_SELECT_MODE");
     if (!(m && std::string(m) == "batch") && K > 0) D = 0;
+    a.warp_sel = !(m && (std::string(m) == "batch" || std::string(m) == "reg"));
   }
   a.D = static_cast<int32_t>(D);
   a.Tn = D ? static_cast<int32_t>(pow2(std::max<int64_t>(C * D, 2))) : 0;
@@ -1060,9 +1074,13 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl, int32_t g
   // key streams of the register loop: up to 16 lookahead items (33 B each) per client, using
   // at most a third of what is left (the head windows get the rest)
   int64_t Ds = 0;
+  auto stream_bytes = [&](int64_t d) {
+    return 4 * ((8ull * C * d + 15) & ~15ull) + ((1ull * C * d + 15) & ~15ull) + 2 * ((4ull * C + 15) & ~15ull);
+  };
   if (K > 0 && C > 0) {
     const size_t left_s = ctx->smem_optin - static_smem - smem;
-    Ds = std::min<int64_t>(16, static_cast<int64_t>(left_s / 3 / (33ull * C + 5 * 16)));
+    Ds = 16;
+    while (Ds >= 1 && stream_bytes(Ds) > left_s / 3) --Ds;
     if (Ds < 1) {
       Ds = 0;
       K = 0;  // no room: shared-memory loop
@@ -1070,7 +1088,7 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl, int32_t g
     a.K = K;
   }
   a.Ds = static_cast<int32_t>(Ds);
-  if (Ds) smem += 4 * ((8ull * C * Ds + 15) & ~15ull) + ((1ull * C * Ds + 15) & ~15ull);
+  if (Ds) smem += stream_bytes(Ds);
   const size_t left = ctx->smem_optin - static_smem - smem;
   // A client is picked at most max_batch times before the slots run out (+1 for the next
   // head's arrival); deeper heads (rejection streams) are scored on demand from HBM.
@@ -1106,7 +1124,15 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl, int32_t g
   pl.window_smem = model_smem;
   const int64_t witems = static_cast<int64_t>(C) * a.W;
   pl.window_grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((witems + 255) / 256, 8ll * ctx->sm_count)));
-  CUDA_TRY(ctx, set_smem_attr(ctx, 2, reinterpret_cast<const void*>(select_kernel), smem));
+  a.warp_sel = a.warp_sel && a.D == 0 && a.K > 0 && a.Ds > 0;
+  // kernel variant (select_fn): register slots up to 128 clients; larger rosters keep the
+  // multi-warp register loop (measured faster than the shared-memory single-warp variant,
+  // which stays selectable with EQX_SELECT_MODE=warp)
+  if (a.warp_sel) {
+    const char* m = std::getenv("EQX_SELECT_MODE");
+    a.warp_sel = C <= 32 ? 2 : C <= 64 ? 3 : C <= 128 ? 4 : (m && std::string(m) == "warp") ? 1 : 0;
+  }
+  CUDA_TRY(ctx, set_smem_attr(ctx, a.warp_sel + 2, select_fn(a.warp_sel), smem));
   return EQX_OK;
 }
 
@@ -1134,7 +1160,10 @@ static eqx_status step_enqueue(eqx_ctx* ctx, const StepPlan& pl, bool with_drain
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[5], s));
   window_kernel<<<pl.window_grid, 256, pl.window_smem, s>>>(pl.wi);
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[2], s));
-  select_kernel<<<1, pl.select_threads, pl.select_smem, s>>>(pl.se);
+  {
+    void* args[] = {const_cast<SelectArgs*>(&pl.se)};
+    CUDA_TRY(ctx, cudaLaunchKernel(select_fn(pl.se.warp_sel), dim3(1), dim3(pl.select_threads), args, pl.select_smem, s));
+  }
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[3], s));
   CUDA_TRY(ctx, cudaGetLastError());
   CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_join, 0));
@@ -1329,7 +1358,10 @@ eqx_status eqx_shard_select_async(eqx_ctx* ctx, const void* recs, int32_t world,
     CUDA_TRY(ctx, cudaGetLastError());
   }
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[2], s));
-  select_kernel<<<1, pl.select_threads, pl.select_smem, s>>>(pl.se);
+  {
+    void* args[] = {const_cast<SelectArgs*>(&pl.se)};
+    CUDA_TRY(ctx, cudaLaunchKernel(select_fn(pl.se.warp_sel), dim3(1), dim3(pl.select_threads), args, pl.select_smem, s));
+  }
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[3], s));
   CUDA_TRY(ctx, cudaGetLastError());
   EventFillArgs ef;

@@ -1198,6 +1198,8 @@ struct StreamScratch {
   double* r;
   double* cn;   // VTC counter after item d
   uint8_t* fl;  // [C][Ds] kFlAlone | kFlMaxChg | kFlHolder
+  int32_t* sd;  // [C] stream cursor (item of the current head)
+  int32_t* sdl; // [C] items generated
   int32_t Ds;
 };
 
@@ -1510,7 +1512,553 @@ __device__ void seq_reg_phase(const SelectArgs& a, const ModelTables& M, const W
   }
 }
 
-__global__ void __launch_bounds__(kSelectMaxThreads, 1) select_kernel(const SelectArgs a) {
+// ---- single-warp selection with winner-lane updates -------------------------------------
+// Warp 0 runs the exact admit_requests loop; lane L owns clients L, L+32, ...  Every client's
+// next Ds keys (and the ledger after each of those requests) are generated ahead under the
+// current maxima (same sequential FP64 adds/divisions as on_admit + holistic_score), so
+// cw.kb/cw.ab hold each client's current head tuple (~0 = not a candidate).  Each lane keeps
+// its best candidate and that candidate's pick outcome (reject / admit / skip / stop, from the
+// replicated batch counters) in registers; a pick is a warp argmin (redux) plus one broadcast
+// of the winner's outcome, after which only the winning lane touches shared memory (advance
+// the client's stream, rescan its own clients).  A maximum moving (an admission above it, or a
+// max holder leaving the backlog) regenerates every stream with the whole CTA: the other
+// warps wait at a barrier for such commands.
+enum : int32_t { kCmdRegen = 1, kCmdMaxRegen = 2, kCmdExit = 3 };
+enum : int32_t { kOutNone = 0, kOutRej = 1, kOutAdm = 2, kOutSkip = 3, kOutStop = 4 };
+
+struct WarpSelShared {
+  int32_t cmd, depth;
+};
+
+// (Re)generate client c's stream from its current head under the maxima (mu, mr).
+__device__ __forceinline__ void gen_stream(const SelectArgs& a, const ModelTables& M, const WinEntry* win,
+                                           const ClientWork& cw, const StreamScratch& T, int32_t c, int depth,
+                                           double mu, double mr) {
+  const Policy& P = a.pol;
+  const bool maxmode = P.kind == kEquinox && P.norm_mode == 0;
+  const int32_t pos = cw.pos[c], end = cw.end[c], pos0 = cw.pos0[c];
+  T.sd[c] = 0;
+  if (!(pos < end) || (cw.flags[c] & kSkipped)) {
+    T.sdl[c] = 0;
+    cw.kb[c] = ~0ull;
+    return;
+  }
+  double u = cw.ufc[c], r = cw.rfc[c], k = cw.cnt[c];
+  const double w = cw.w[c];
+  const int64_t base = static_cast<int64_t>(c) * T.Ds;
+  int d = 0;
+  for (; d < depth && pos + d < end; ++d) {
+    const int32_t j = pos + d, kk = j - pos0;
+    const WinEntry e = kk < a.W ? win[static_cast<int64_t>(c) * a.W + kk] : deep_entry(a, M, c, j, kk, w);
+    if (d == 0) cw.ab[c] = e.abits;
+    uint8_t f = 0;
+    double nu = u, nr = r, nk = k;
+    if (e.alone) {
+      f |= kFlAlone;
+      nu = __dadd_rn(u, e.ufc_inc);
+      nr = __dadd_rn(r, e.rfc_inc);
+      if (P.kind == kVtc) nk = __dadd_rn(k, vtc_inc(P, e, w));
+    }
+    if (j + 1 == end) {
+      if (maxmode && (u == mu || r == mr)) f |= kFlHolder;  // a max holder leaves the backlog
+    } else if (e.alone && maxmode && (mu < nu || mr < nr)) {
+      f |= kFlMaxChg;  // this admission raises a maximum
+    }
+    T.k[base + d] = ordered_bits(hf_key(P, u, r, mu, mr, k));
+    T.u[base + d] = nu;
+    T.r[base + d] = nr;
+    T.cn[base + d] = nk;
+    T.fl[base + d] = f;
+    u = nu;
+    r = nr;
+    k = nk;
+  }
+  T.sdl[c] = d;
+  cw.kb[c] = T.k[base];
+}
+
+__device__ __forceinline__ void warp_select_phase(const SelectArgs& a, const ModelTables& M, const WinEntry* win,
+                                                  const ClientWork& cw, SelShared& S, const StreamScratch& T) {
+  __shared__ WarpSelShared X;
+  const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31;
+  const int32_t C = a.C, Ds = T.Ds, W = a.W;
+  const Policy P = a.pol;
+  auto regen_all = [&](int depth) {
+    for (int32_t c = tid; c < C; c += NT) gen_stream(a, M, win, cw, T, c, depth, S.max_u, S.max_r);
+  };
+  // initial streams (maxima from cta_maxima)
+  regen_all(Ds);
+  __syncthreads();
+  if (tid >= 32) {  // helper warps: CTA-wide stream regeneration on command
+    for (;;) {
+      __syncthreads();
+      const int32_t cmd = X.cmd;
+      if (cmd == kCmdExit) break;
+      if (cmd == kCmdMaxRegen) cta_maxima(cw, C, S);
+      regen_all(X.depth);
+      __syncthreads();
+    }
+    return;
+  }
+  // ---------------- selection warp ----------------
+  uint64_t* const kb = cw.kb;
+  uint64_t* const ab = cw.ab;
+  const uint32_t* const order = cw.order;
+  int32_t* const posv = cw.pos;
+  const int32_t* const pos0v = cw.pos0;
+  const int32_t* const endv = cw.end;
+  const int32_t K = (C + 31) >> 5;  // clients per lane
+  const int64_t tmax = a.tmax;
+  int32_t members = S.members;
+  int64_t reserved = S.reserved, n_ev = S.n_ev, n_adm = S.n_adm, n_rej = S.n_rej, prefill = S.prefill;
+  // The lane's best candidate and everything a pick of it needs, prefetched so that the
+  // winning lane's update is stores only.
+  uint64_t bk = ~0ull, ba = ~0ull, bnk = ~0ull, bna = ~0ull;
+  uint32_t bo = 0xffffffffu;
+  int32_t bc = -1, bin = 0, brow = 0, bflags = 0, bpos = 0, bd = 0;
+  int64_t bneed = 0;
+  double bnu = 0.0, bnr = 0.0, bncn = 0.0;
+  auto head_entry = [&](int32_t c, int32_t j) -> WinEntry {
+    const int32_t kk = j - pos0v[c];
+    return kk < W ? win[static_cast<int64_t>(c) * W + kk] : deep_entry(a, M, c, j, kk, cw.w[c]);
+  };
+  auto lane_best = [&]() {
+    bk = ~0ull;
+    ba = ~0ull;
+    bo = 0xffffffffu;
+    bc = -1;
+    for (int32_t i = 0; i < K; ++i) {
+      const int32_t c = lane + 32 * i;
+      if (c >= C) break;
+      const uint64_t k = kb[c];
+      if (k == ~0ull) continue;
+      const uint64_t av = ab[c];
+      const uint32_t o = order[c];
+      const bool lt = (k < bk) | ((k == bk) & ((av < ba) | ((av == ba) & (o < bo))));
+      if (bc < 0 || lt) {
+        bk = k;
+        ba = av;
+        bo = o;
+        bc = c;
+      }
+    }
+    if (bc >= 0) {
+      const int32_t c = bc, j = posv[c], d = T.sd[c], dl = T.sdl[c], end = endv[c];
+      const int64_t x = static_cast<int64_t>(c) * Ds + d;
+      const WinEntry e = head_entry(c, j);
+      const uint8_t f = T.fl[x];
+      bpos = j;
+      bd = d;
+      bin = e.in;
+      brow = e.row;
+      bneed = static_cast<int64_t>(e.in) + e.pred;
+      bnu = T.u[x];
+      bnr = T.r[x];
+      bncn = T.cn[x];
+      const bool leaving = j + 1 == end, more = d + 1 < dl;
+      bflags = (e.alone ? 1 : 0) | ((f & kFlMaxChg) ? 2 : 0) | ((f & kFlHolder) ? 4 : 0) | (leaving ? 8 : 0) |
+               (more ? 16 : 0);
+      if (!leaving && more) {
+        bnk = T.k[x + 1];
+        bna = head_entry(c, j + 1).abits;
+      }
+    }
+  };
+  auto command = [&](int32_t cmd, int depth) {  // CTA-wide regeneration (all warps)
+    if (lane == 0) {
+      X.cmd = cmd;
+      X.depth = depth;
+    }
+    __syncthreads();
+    if (cmd == kCmdMaxRegen) cta_maxima(cw, C, S);
+    regen_all(depth);
+    __syncthreads();
+  };
+  lane_best();
+  int since_regen = 1 << 30;
+#ifdef EQX_PROF
+  long long cy0 = 0, cy1 = 0, cy2 = 0, cyp = 0;
+#endif
+  for (;;) {
+#ifdef EQX_PROF
+    const long long ta = clock64();
+#endif
+    // outcome of picking this lane's best (engine.cpp:216-268 with can_fit/fits_alone)
+    int32_t out = kOutNone;
+    if (bc >= 0) {
+      if (!(bflags & 1)) out = kOutRej;
+      else if ((members + 1 <= P.max_batch) && (reserved + bneed <= tmax)) out = kOutAdm;
+      else out = P.backfill ? kOutSkip : kOutStop;
+    }
+    const int src = warp_argmin_lane(Cand{bk, ba, bo});
+    const uint64_t pk = __shfl_sync(0xffffffffu, static_cast<uint64_t>(static_cast<uint32_t>(out | (bflags << 4))) |
+                                                      (static_cast<uint64_t>(static_cast<uint32_t>(bin)) << 32), src);
+    const int64_t need = __shfl_sync(0xffffffffu, bneed, src);
+    const int32_t o = static_cast<int32_t>(pk & 15), fl = static_cast<int32_t>((pk >> 4) & 31);
+    if (o == kOutNone || o == kOutStop) break;  // no candidates (engine.cpp:217) / batch full (:239)
+    const int64_t ev = n_ev;
+    if (o == kOutRej) {
+      ++n_rej;
+      ++n_ev;
+    } else if (o == kOutAdm) {
+      members += 1;
+      reserved += need;
+      prefill += static_cast<int32_t>(pk >> 32);
+      ++n_adm;
+      ++n_ev;
+    }
+    const bool maxchg = o == kOutAdm && (fl & 2);
+    const bool holder = o != kOutSkip && (fl & 4) && (fl & 8);
+    ++since_regen;
+#ifdef EQX_PROF
+    const long long tb = clock64();
+#endif
+    bool rescan = false;
+    if (lane == src) {  // the winning lane applies the pick to its client (stores only)
+      const int32_t c = bc;
+      rescan = true;
+      if (o == kOutSkip) {
+        cw.flags[c] = kBacklogged | kSkipped;  // engine.cpp:236-238 (a candidate is backlogged)
+        kb[c] = ~0ull;
+      } else {
+        if (ev < a.ev_cap) {
+          a.ev_row[ev] = brow;
+          a.ev_kind[ev] = o == kOutAdm ? 1 : 2;
+          a.ev_client[ev] = c;
+        }
+        posv[c] = bpos + 1;
+        cw.ufc[c] = bnu;
+        cw.rfc[c] = bnr;
+        cw.cnt[c] = bncn;
+        if (o == kOutAdm) cw.adm[c] += 1;
+        if (fl & 8) {  // pop_head emptied the queue: set_backlogged(false)
+          cw.flags[c] = 0;
+          kb[c] = ~0ull;
+        } else if (maxchg) {
+          if (S.max_u < bnu) S.max_u = bnu;
+          if (S.max_r < bnr) S.max_r = bnr;
+        } else if (fl & 16) {
+          T.sd[c] = bd + 1;
+          kb[c] = bnk;
+          ab[c] = bna;
+        } else {
+          gen_stream(a, M, win, cw, T, c, Ds, S.max_u, S.max_r);  // its lookahead ran out
+        }
+      }
+    }
+#ifdef EQX_PROF
+    const long long tc = clock64();
+#endif
+    if (maxchg || holder) {
+      __syncwarp();
+      // maxima moving every few picks (cold ledgers): short lookahead; otherwise the full one
+      const int depth = since_regen < 4 ? min(2, Ds) : Ds;
+      since_regen = 0;
+      command(holder ? kCmdMaxRegen : kCmdRegen, depth);
+      lane_best();
+    } else if (rescan) {
+      lane_best();
+    }
+#ifdef EQX_PROF
+    __syncwarp();
+    const long long td = clock64();
+    cy0 += tb - ta;
+    cy1 += tc - tb;
+    cy2 += td - tc;
+    ++cyp;
+#endif
+  }
+#ifdef EQX_PROF
+  if (lane == 0) {
+    a.st->t[12] += cy0;
+    a.st->t[13] += cy1;
+    a.st->t[14] += cy2;
+    a.st->t[15] += cyp;
+  }
+#endif
+  if (lane == 0) {
+    S.members = members;
+    S.reserved = reserved;
+    S.n_ev = n_ev;
+    S.n_adm = n_adm;
+    S.n_rej = n_rej;
+    S.prefill = prefill;
+    S.flags |= kDone;
+    X.cmd = kCmdExit;
+  }
+  __syncthreads();  // releases the helper warps
+}
+
+// Register-slot variant of warp_select_phase for rosters of up to 32*K clients (K <= 4): each
+// lane keeps its clients' current head item *and* the next stream item in registers, so a pick
+// is a slot compare, a warp argmin and a broadcast; the winning lane promotes its prefetched
+// next item and issues the loads of the one after, whose latency hides behind later picks.
+struct RegItem {  // raw loads only: nothing is computed from them until the item is promoted
+  uint64_t k, a;
+  double nu, nr, ncn;
+  int32_t in, pred, row, alone;
+  uint32_t fl;      // T.fl byte (kFlMaxChg / kFlHolder)
+};
+
+template <int K>
+__device__ __forceinline__ void warp_select_reg(const SelectArgs& a, const ModelTables& M, const WinEntry* win,
+                                                const ClientWork& cw, SelShared& S, const StreamScratch& T) {
+  __shared__ WarpSelShared X;
+  const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31;
+  const int32_t C = a.C, Ds = T.Ds, W = a.W;
+  const Policy P = a.pol;
+  auto regen_all = [&](int depth) {
+    for (int32_t c = tid; c < C; c += NT) gen_stream(a, M, win, cw, T, c, depth, S.max_u, S.max_r);
+  };
+  regen_all(Ds);
+  __syncthreads();
+  if (tid >= 32) {  // helper warps: CTA-wide stream regeneration on command
+    for (;;) {
+      __syncthreads();
+      const int32_t cmd = X.cmd;
+      if (cmd == kCmdExit) break;
+      if (cmd == kCmdMaxRegen) cta_maxima(cw, C, S);
+      regen_all(X.depth);
+      __syncthreads();
+    }
+    return;
+  }
+  const int64_t tmax = a.tmax;
+  // per-slot registers
+  RegItem cur[K], nxt[K];
+  int32_t spos[K], spos0[K], send[K], sd[K], sdl[K], sadm[K], sfl[K];
+  uint32_t so[K];
+  double su[K], sr[K], scn[K];
+  auto load_item = [&](int s, int32_t c, int32_t d, int32_t j) -> RegItem {
+    RegItem it;
+    const int64_t x = static_cast<int64_t>(c) * Ds + d;
+    const int32_t kk = j - spos0[s];
+    const WinEntry e = kk < W ? win[static_cast<int64_t>(c) * W + kk] : deep_entry(a, M, c, j, kk, cw.w[c]);
+    it.k = T.k[x];
+    it.a = e.abits;
+    it.nu = T.u[x];
+    it.nr = T.r[x];
+    it.ncn = T.cn[x];
+    it.in = e.in;
+    it.pred = e.pred;
+    it.row = e.row;
+    it.alone = e.alone;
+    it.fl = T.fl[x];
+    return it;
+  };
+  auto load_slot = [&](int s) {  // after (re)generation: current head and the item after it
+    const int32_t c = lane + 32 * s;
+    cur[s].k = ~0ull;
+    if (c >= C) return;
+    spos[s] = cw.pos[c];
+    spos0[s] = cw.pos0[c];
+    send[s] = cw.end[c];
+    sfl[s] = cw.flags[c];
+    su[s] = cw.ufc[c];
+    sr[s] = cw.rfc[c];
+    scn[s] = cw.cnt[c];
+    sd[s] = 0;
+    sdl[s] = T.sdl[c];
+    if (sdl[s] == 0) return;  // not a candidate
+    cur[s] = load_item(s, c, 0, spos[s]);
+    if (1 < sdl[s]) nxt[s] = load_item(s, c, 1, spos[s] + 1);
+  };
+#pragma unroll
+  for (int s = 0; s < K; ++s) {
+    so[s] = lane + 32 * s < C ? cw.order[lane + 32 * s] : 0xffffffffu;
+    sadm[s] = lane + 32 * s < C ? cw.adm[lane + 32 * s] : 0;
+    load_slot(s);
+  }
+  int32_t members = S.members;
+  int64_t reserved = S.reserved, n_ev = S.n_ev, n_adm = S.n_adm, n_rej = S.n_rej, prefill = S.prefill;
+  int since_regen = 1 << 30;
+  auto command = [&](int32_t cmd, int depth) {
+#pragma unroll
+    for (int s = 0; s < K; ++s) {  // publish the slots' state for the regeneration
+      const int32_t c = lane + 32 * s;
+      if (c < C) {
+        cw.pos[c] = spos[s];
+        cw.flags[c] = sfl[s];
+        cw.ufc[c] = su[s];
+        cw.rfc[c] = sr[s];
+        cw.cnt[c] = scn[s];
+      }
+    }
+    if (lane == 0) {
+      X.cmd = cmd;
+      X.depth = depth;
+    }
+    __syncthreads();
+    if (cmd == kCmdMaxRegen) cta_maxima(cw, C, S);
+    regen_all(depth);
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < K; ++s) load_slot(s);
+  };
+#ifdef EQX_PROF
+  long long cy0 = 0, cy1 = 0, cy2 = 0, cyp = 0;
+#endif
+  for (;;) {
+#ifdef EQX_PROF
+    const long long ta = clock64();
+#endif
+    // the lane's best slot (select_next order: key, head arrival, client_id rank)
+    int bs = -1;
+    uint64_t bk = ~0ull, ba = ~0ull;
+    uint32_t bo = 0xffffffffu;
+#pragma unroll
+    for (int s = 0; s < K; ++s) {
+      if (cur[s].k == ~0ull) continue;
+      const bool lt = (cur[s].k < bk) | ((cur[s].k == bk) & ((cur[s].a < ba) | ((cur[s].a == ba) & (so[s] < bo))));
+      if (bs < 0 || lt) {
+        bs = s;
+        bk = cur[s].k;
+        ba = cur[s].a;
+        bo = so[s];
+      }
+    }
+    int32_t out = kOutNone, bflags = 0, bin = 0;
+    int64_t bneed = 0;
+#pragma unroll
+    for (int s = 0; s < K; ++s)
+      if (s == bs) {
+        bflags = (cur[s].alone ? 1 : 0) | ((cur[s].fl & kFlMaxChg) ? 2 : 0) | ((cur[s].fl & kFlHolder) ? 4 : 0) |
+                 ((spos[s] + 1 == send[s]) ? 8 : 0) | ((sd[s] + 1 < sdl[s]) ? 16 : 0);
+        bin = cur[s].in;
+        bneed = static_cast<int64_t>(cur[s].in) + cur[s].pred;
+      }
+    if (bs >= 0) {
+      if (!(bflags & 1)) out = kOutRej;
+      else if ((members + 1 <= P.max_batch) && (reserved + bneed <= tmax)) out = kOutAdm;
+      else out = P.backfill ? kOutSkip : kOutStop;
+    }
+    const int src = warp_argmin_lane(Cand{bk, ba, bo});
+    const uint64_t pk = __shfl_sync(0xffffffffu, static_cast<uint64_t>(static_cast<uint32_t>(out | (bflags << 4))) |
+                                                      (static_cast<uint64_t>(static_cast<uint32_t>(bin)) << 32), src);
+    const int64_t need = __shfl_sync(0xffffffffu, bneed, src);
+    const int32_t o = static_cast<int32_t>(pk & 15), fl = static_cast<int32_t>((pk >> 4) & 31);
+    if (o == kOutNone || o == kOutStop) break;  // no candidates (engine.cpp:217) / batch full (:239)
+    const int64_t ev = n_ev;
+    if (o == kOutRej) {
+      ++n_rej;
+      ++n_ev;
+    } else if (o == kOutAdm) {
+      members += 1;
+      reserved += need;
+      prefill += static_cast<int32_t>(pk >> 32);
+      ++n_adm;
+      ++n_ev;
+    }
+    const bool maxchg = o == kOutAdm && (fl & 2);
+    const bool holder = o != kOutSkip && (fl & 4) && (fl & 8);
+    ++since_regen;
+#ifdef EQX_PROF
+    const long long tb = clock64();
+#endif
+    bool own_regen = false;
+    if (lane == src) {
+#pragma unroll
+      for (int s = 0; s < K; ++s) {
+        if (s != bs) continue;
+        const int32_t c = lane + 32 * s;
+        if (o == kOutSkip) {
+          sfl[s] |= kSkipped;  // engine.cpp:236-238
+          cur[s].k = ~0ull;
+          continue;
+        }
+        if (ev < a.ev_cap) {
+          a.ev_row[ev] = cur[s].row;
+          a.ev_kind[ev] = o == kOutAdm ? 1 : 2;
+          a.ev_client[ev] = c;
+        }
+        spos[s] += 1;
+        su[s] = cur[s].nu;
+        sr[s] = cur[s].nr;
+        scn[s] = cur[s].ncn;
+        if (o == kOutAdm) sadm[s] += 1;
+        if (fl & 8) {  // pop_head emptied the queue: set_backlogged(false)
+          sfl[s] &= ~kBacklogged;
+          cur[s].k = ~0ull;
+        } else if (maxchg) {
+          if (S.max_u < su[s]) S.max_u = su[s];
+          if (S.max_r < sr[s]) S.max_r = sr[s];
+        } else if (fl & 16) {  // promote the prefetched item, prefetch the one after
+          cur[s] = nxt[s];
+          sd[s] += 1;
+          if (sd[s] + 1 < sdl[s]) nxt[s] = load_item(s, c, sd[s] + 1, spos[s] + 1);
+        } else {
+          own_regen = true;
+        }
+      }
+    }
+    if (own_regen) {  // the winner's lookahead ran out: regenerate its stream alone
+#pragma unroll
+      for (int s = 0; s < K; ++s) {
+        if (s != bs) continue;
+        const int32_t c = lane + 32 * s;
+        cw.pos[c] = spos[s];
+        cw.ufc[c] = su[s];
+        cw.rfc[c] = sr[s];
+        cw.cnt[c] = scn[s];
+        gen_stream(a, M, win, cw, T, c, Ds, S.max_u, S.max_r);
+        load_slot(s);
+      }
+    }
+#ifdef EQX_PROF
+    const long long tc = clock64();
+#endif
+    if (maxchg || holder) {
+      __syncwarp();
+      const int depth = since_regen < 4 ? min(2, Ds) : Ds;
+      since_regen = 0;
+      command(holder ? kCmdMaxRegen : kCmdRegen, depth);
+    }
+#ifdef EQX_PROF
+    __syncwarp();
+    const long long td = clock64();
+    cy0 += tb - ta;
+    cy1 += tc - tb;
+    cy2 += td - tc;
+    ++cyp;
+#endif
+  }
+#ifdef EQX_PROF
+  if (lane == 0) {
+    a.st->t[12] += cy0;
+    a.st->t[13] += cy1;
+    a.st->t[14] += cy2;
+    a.st->t[15] += cyp;
+  }
+#endif
+#pragma unroll
+  for (int s = 0; s < K; ++s) {
+    const int32_t c = lane + 32 * s;
+    if (c < C) {
+      cw.pos[c] = spos[s];
+      cw.flags[c] = sfl[s];
+      cw.ufc[c] = su[s];
+      cw.rfc[c] = sr[s];
+      cw.cnt[c] = scn[s];
+      cw.adm[c] = sadm[s];
+    }
+  }
+  if (lane == 0) {
+    S.members = members;
+    S.reserved = reserved;
+    S.n_ev = n_ev;
+    S.n_adm = n_adm;
+    S.n_rej = n_rej;
+    S.prefill = prefill;
+    S.flags |= kDone;
+    X.cmd = kCmdExit;
+  }
+  __syncthreads();  // releases the helper warps
+}
+
+// kMode: -1 multi-mode loops (select_kernel); 0 warp_select_phase; 1/2/4 warp_select_reg<kMode>
+template <int kMode>
+__device__ __forceinline__ void select_body(const SelectArgs& a) {
+  constexpr bool kWarp = kMode >= 0;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ SelShared S;
   const int32_t C = a.C;
@@ -1564,6 +2112,8 @@ __global__ void __launch_bounds__(kSelectMaxThreads, 1) select_kernel(const Sele
     T.r = reinterpret_cast<double*>(carve(8 * items));
     T.cn = reinterpret_cast<double*>(carve(8 * items));
     T.fl = reinterpret_cast<uint8_t*>(carve(items));
+    T.sd = reinterpret_cast<int32_t*>(carve(4ull * C));
+    T.sdl = reinterpret_cast<int32_t*>(carve(4ull * C));
   }
   WinEntry* win = reinterpret_cast<WinEntry*>(p);
   __syncthreads();
@@ -1622,7 +2172,14 @@ __global__ void __launch_bounds__(kSelectMaxThreads, 1) select_kernel(const Sele
 
   // ---- batches; short batches (maxima moving every pick) fall back to sequential picks ----
   unsigned long long nb = 0, ns = 0;
-  for (;;) {
+  if constexpr (kMode == 0) {  // default: single-warp selection
+    warp_select_phase(a, M, win, cw, S, T);
+    ns = 1;
+  } else if constexpr (kMode > 0) {
+    warp_select_reg<kMode>(a, M, win, cw, S, T);
+    ns = 1;
+  }
+  for (; !kWarp && !(S.flags & kDone);) {
     if (a.D > 0) {
       int32_t acc = 0;
       const int32_t bf = batch_phase(a, win, cw, S, B, &acc);
@@ -1667,6 +2224,16 @@ __global__ void __launch_bounds__(kSelectMaxThreads, 1) select_kernel(const Sele
     a.st->new_prefill = S.prefill;
   }
 }
+
+// Multi-mode selection (register slots / shared-memory loop / speculative batches) and the
+// default single-warp selection, as separate kernels so each gets its own register budget.
+__global__ void __launch_bounds__(kSelectMaxThreads, 1) select_kernel(const SelectArgs a) { select_body<-1>(a); }
+template <int kMode>
+__global__ void __launch_bounds__(kSelectMaxThreads, 1) select_warp_kernel(const SelectArgs a) { select_body<kMode>(a); }
+template __global__ void select_warp_kernel<0>(SelectArgs);
+template __global__ void select_warp_kernel<1>(SelectArgs);
+template __global__ void select_warp_kernel<2>(SelectArgs);
+template __global__ void select_warp_kernel<4>(SelectArgs);
 
 // Event payloads (scheduler.hpp:131-138 PendingContribution) from the per-request scores the
 // scoring kernel wrote: predicted tokens, ufc/rfc increments, the VTC charge and wait_s.

@@ -131,6 +131,7 @@ struct SelectArgs {
   int32_t Tn;            // batch sort size (power of two >= C * D)
   int32_t sel_threads;   // threads in the selection loop (multiple of 32)
   int32_t K;             // register client slots per selection thread (1/2/4/8; 0 = smem loop)
+  int32_t warp_sel;      // 1: single-warp selection (warp_select_phase), the default
   int32_t Ds;            // key-stream lookahead per client for the register loop
   int32_t cw_in_smem;
   void* cw_global;       // per-client work arrays when they do not fit in smem
@@ -241,6 +242,8 @@ __global__ void drain_rank_kernel(DrainArgs a);
 __global__ void score_kernel(ScoreArgs a);
 __global__ void window_kernel(WindowArgs a);
 __global__ void select_kernel(SelectArgs a);
+template <int kMode>
+__global__ void select_warp_kernel(SelectArgs a);  // kMode 0: smem slots; 1/2/4: register slots
 __global__ void gather_ids_kernel(const int32_t* rows, int64_t n, const int64_t* id, int64_t id_base,
                                   int64_t* out);
 
