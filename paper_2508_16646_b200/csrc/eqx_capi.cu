@@ -172,6 +172,7 @@ const void* select_fn(int warp_sel) {
     case 2: return reinterpret_cast<const void*>(select_warp_kernel<1>);
     case 3: return reinterpret_cast<const void*>(select_warp_kernel<2>);
     case 4: return reinterpret_cast<const void*>(select_warp_kernel<4>);
+    case 5: return reinterpret_cast<const void*>(select_warp_kernel<8>);
     default: return reinterpret_cast<const void*>(select_kernel);
   }
 }
@@ -801,7 +802,7 @@ static eqx_status drain_prepare(eqx_ctx* ctx, const eqx_requests* r) {
   ctx->hist_L = L;
   const size_t rank_base = (8ull + 2ull * kDrainWarps) * C + 64;
   ctx->staged = rank_base + 6ull * tile_rows <= ctx->smem_optin;
-  ctx->hist_smem = std::max<size_t>(2ull * kDrainWarps * C, 16);
+  ctx->hist_smem = 2ull * kDrainWarps * C + 4ull * C + 16;  // per-warp counts + per-client first rows
   CUDA_TRY(ctx, ctx->d_wcnt.ensure(std::max<size_t>(2ull * kDrainWarps * C * n_tiles, 64)));
   ctx->rank_smem = rank_base + (ctx->staged ? 6ull * tile_rows : 0);
   if (ctx->rank_smem > ctx->smem_optin || ctx->hist_smem > ctx->smem_optin)
@@ -818,6 +819,8 @@ static DrainArgs drain_args(eqx_ctx* ctx) {
   d.client = ctx->q_client;
   d.n = static_cast<int32_t>(ctx->n);
   d.C = ctx->C;
+  d.cbits = 1;
+  while ((1 << d.cbits) <= d.C) ++d.cbits;
   d.tile_rows = static_cast<int32_t>(ctx->tile_rows);
   d.n_tiles = ctx->n_tiles;
   d.staged = ctx->staged ? 1 : 0;
@@ -841,15 +844,27 @@ static DrainArgs drain_args(eqx_ctx* ctx) {
 }
 
 // Pure stream work of a drain (2 memsets + 2 kernels); capturable into a CUDA graph.
-static eqx_status drain_enqueue(eqx_ctx* ctx) {
+// lift: also apply on_activated / set_backlogged now (a standalone drain); a drain fused into a
+// step leaves that to the selection kernel's prologue (SelectArgs::do_lift).
+static eqx_status drain_enqueue(eqx_ctx* ctx, bool lift) {
   cudaStream_t s = ctx->stream;
   const int32_t C = ctx->C;
   if (C == 0) return EQX_OK;
   CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_head.p, 0, 4ull * C, s));
   CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_qlen_before.p, 0, 4ull * C, s));
+  CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_first.p, 0xff, 4ull * C, s));  // atomicMin target
+#ifdef EQX_PROF
+  {
+    char* dt = reinterpret_cast<char*>(ctx->d_state.p) + offsetof(DevState, dt);
+    CUDA_TRY(ctx, cudaMemsetAsync(dt, 0, 8 * 8, s));
+    CUDA_TRY(ctx, cudaMemsetAsync(dt, 0xff, 8, s));
+    CUDA_TRY(ctx, cudaMemsetAsync(dt + 24, 0xff, 8, s));
+  }
+#endif
   const DrainArgs d = drain_args(ctx);
   drain_hist_kernel<<<ctx->n_tiles, kDrainThreads, ctx->hist_smem, s>>>(d);
   drain_rank_kernel<<<ctx->n_tiles, kDrainThreads, ctx->rank_smem, s>>>(d);
+  if (lift) lift_kernel<<<1, 1024, 0, s>>>(d);
   CUDA_TRY(ctx, cudaGetLastError());
   return EQX_OK;
 }
@@ -1009,6 +1024,10 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl, int32_t g
   a.model = ctx->d_model.as<ModelTables>();
   a.model_words = model_words;
   a.tmax = kv_threshold(ctx->perf.mem_per_token_bytes, ctx->perf.mem_capacity_bytes);
+  a.do_lift = 0;
+  a.first_row = ctx->d_first.as<int32_t>();
+  a.qlen_before = ctx->d_qlen_before.as<int32_t>();
+  a.counter_lift = ctx->counter_lift;
   a.pol = ctx->pol;
   a.now = now;
   pl.select_threads = kSelectMaxThreads;
@@ -1061,12 +1080,14 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl, int32_t g
                     batch_bytes(D) + static_cast<size_t>(D) * C * sizeof(WinEntry) > left0))
     --D;
   if (D < 2 || C == 0) D = 0;
+  bool batch_kernel = false;
   // Default: register-resident sequential picks (measured faster than speculative batches on
   // cfg2/cfg3, profiles/); EQX_SELECT_MODE=batch enables the batch path for experiments.
   {
     const char* m = std::getenv("EQX_SELECT_MODE");
     if (!(m && std::string(m) == "batch") && K > 0) D = 0;
     a.warp_sel = !(m && (std::string(m) == "batch" || std::string(m) == "reg"));
+    batch_kernel = m && std::string(m) == "batch";
   }
   a.D = static_cast<int32_t>(D);
   a.Tn = D ? static_cast<int32_t>(pow2(std::max<int64_t>(C * D, 2))) : 0;
@@ -1125,10 +1146,11 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl, int32_t g
   const int64_t witems = static_cast<int64_t>(C) * a.W;
   pl.window_grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((witems + 255) / 256, 8ll * ctx->sm_count)));
   a.warp_sel = a.warp_sel && a.D == 0 && a.K > 0 && a.Ds > 0;
+  if (batch_kernel && a.D > 0) a.warp_sel = 5;  // batch kernel variant (select_fn)
   // kernel variant (select_fn): register slots up to 128 clients; larger rosters keep the
   // multi-warp register loop (measured faster than the shared-memory single-warp variant,
   // which stays selectable with EQX_SELECT_MODE=warp)
-  if (a.warp_sel) {
+  if (a.warp_sel && a.warp_sel != 5) {
     const char* m = std::getenv("EQX_SELECT_MODE");
     a.warp_sel = C <= 32 ? 2 : C <= 64 ? 3 : C <= 128 ? 4 : (m && std::string(m) == "warp") ? 1 : 0;
   }
@@ -1154,7 +1176,7 @@ static eqx_status step_enqueue(eqx_ctx* ctx, const StepPlan& pl, bool with_drain
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_join, s2));
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[4], s));
   if (with_drain) {
-    eqx_status e = drain_enqueue(ctx);
+    eqx_status e = drain_enqueue(ctx, false);
     if (e != EQX_OK) return e;
   }
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[5], s));
@@ -1197,7 +1219,7 @@ eqx_status eqx_drain(eqx_ctx* ctx, const eqx_requests* r) {
   eqx_status st = drain_prepare(ctx, r);
   if (st != EQX_OK) return st;
   ctx->shard_W = 0;
-  st = drain_enqueue(ctx);
+  st = drain_enqueue(ctx, true);
   if (st != EQX_OK) return st;
   return release_stage(ctx);
 }
@@ -1221,6 +1243,7 @@ eqx_status eqx_drain_step_async(eqx_ctx* ctx, const eqx_requests* r, double now)
   StepPlan pl;
   st = step_prepare(ctx, now, pl);
   if (st != EQX_OK) return st;
+  pl.se.do_lift = 1;  // the fused drain leaves on_activated to the selection prologue
   cudaStream_t s = ctx->stream;
   if (r->location != EQX_DEVICE) {  // host columns: plain launches after the staged H2D
     st = step_enqueue(ctx, pl, true);
@@ -1423,6 +1446,8 @@ eqx_status eqx_phase_times(eqx_ctx* ctx, double* out_us, int32_t n) {
   const double base = static_cast<double>(t[0]);
   for (int i = 0; i < n && i < 6; ++i) out_us[i] = (static_cast<double>(t[i]) - base) * 1e-3;
   for (int i = 6; i < n && i < 16; ++i) out_us[i] = static_cast<double>(t[i]);  // counts / cycles
+  const unsigned long long* dt = ctx->h_state->dt;  // EQX_PROF drain timeline (us from hist start)
+  for (int i = 16; i < n && i < 22; ++i) out_us[i] = (static_cast<double>(dt[i - 16]) - static_cast<double>(dt[0])) * 1e-3;
   return EQX_OK;
 }
 

@@ -65,6 +65,9 @@ struct DevState {
   // [8..11] batch cycles: stream generation, sort, verify, commit
   unsigned long long t[16];
   int64_t n_queued;       // client-sharded step: queued requests over all ranks at step start
+  // EQX_PROF builds: drain timeline (%globaltimer ns): hist start (min) / walk end (max) /
+  // epilogue end, rank start (min) / walk end (max) / epilogue end
+  unsigned long long dt[8];
 };
 
 // Order-preserving map double -> uint64 (IEEE total order on non-NaN values, with -0.0 and

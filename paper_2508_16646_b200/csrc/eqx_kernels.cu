@@ -3,7 +3,7 @@
 //   drain_arrivals (engine.cpp:171-197), two launches:
 //     drain_hist_kernel  per-tile client histogram; the last CTA to finish scans the
 //                        [client][tile] table into FIFO segment offsets
-//     drain_rank_kernel  stable per-client rank inside each tile (warp __match_any_sync walk),
+//     drain_rank_kernel  stable per-client rank inside each tile (warp ballot peer walk),
 //                        staged in shared memory and written out as contiguous per-client runs
 //                        -> perm (row indices grouped by client, arrival order kept); the last
 //                        CTA applies the on_activated counter lift (scheduler.cpp:235-253)
@@ -14,6 +14,7 @@
 //                        16-byte coalesced loads, streaming stores (HBM-bound stream)
 //   gather_ids_kernel    event rows -> request ids for the caller.
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 #include <cstdio>
 
@@ -75,6 +76,19 @@ __device__ __forceinline__ bool last_cta(unsigned int* done) {
   return s_last != 0;
 }
 
+// Lanes holding the same key (the __match_any_sync result) from nbits ballots: MATCH.ANY
+// serialises on sm_100, a ballot per key bit does not.  Keys must be < 2^nbits.
+__device__ __forceinline__ unsigned peer_mask(uint32_t key, int nbits) {
+  unsigned m = 0xffffffffu;
+#pragma unroll 4
+  for (int b = 0; b < nbits; ++b) {
+    const bool bit = (key >> b) & 1u;
+    const unsigned bb = __ballot_sync(0xffffffffu, bit);
+    m &= bit ? bb : ~bb;
+  }
+  return m;
+}
+
 // Block-wide exclusive scan of one uint32 per thread (blockDim.x <= 1024); returns the total.
 __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* out, uint32_t* warp_buf) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
@@ -105,83 +119,6 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* o
 }  // namespace
 
 // ===================================== drain =============================================
-
-__global__ void __launch_bounds__(kDrainThreads) drain_hist_kernel(const DrainArgs a) {
-  extern __shared__ __align__(16) uint32_t sh[];
-  const int32_t C = a.C;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  uint16_t* wc = reinterpret_cast<uint16_t*>(sh);  // [kDrainWarps][C]
-  for (int i = tid; i < kDrainWarps * C; i += blockDim.x) wc[i] = 0;
-  __syncthreads();
-  const int32_t tile = blockIdx.x;
-  const int32_t sub = a.tile_rows / kDrainWarps;
-  const int32_t r0 = tile * a.tile_rows + warp * sub;
-  const int32_t r1 = min(a.n, r0 + sub);
-  uint16_t* my = wc + warp * C;
-  bool bad = false;
-  for (int32_t rb = r0; rb < r1; rb += 32 * 8) {  // 8 loads in flight per lane, then walk
-    int32_t cv[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int32_t row = rb + 32 * u + lane;
-      cv[u] = row < r1 ? a.client[row] : -1;
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {  // per-warp counts: one writer per (warp, client)
-      const int32_t row = rb + 32 * u + lane;
-      const int32_t c = cv[u];
-      const bool ok = static_cast<uint32_t>(c) < static_cast<uint32_t>(C);
-      bad |= row < r1 && !ok;
-      const unsigned peers = __match_any_sync(0xffffffffu, ok ? c : -1);
-      if (ok && lane == __ffs(peers) - 1) my[c] = static_cast<uint16_t>(my[c] + __popc(peers));
-      __syncwarp();
-    }
-  }
-  if (bad) a.st->bad_client = 1;
-  __syncthreads();
-  uint16_t* g = a.wcnt + static_cast<int64_t>(tile) * kDrainWarps * C;
-  for (int i = tid; i < kDrainWarps * C; i += blockDim.x) g[i] = wc[i];
-  for (int c = tid; c < C; c += blockDim.x) {
-    uint32_t t = 0;
-#pragma unroll 8
-    for (int w = 0; w < kDrainWarps; ++w) t += wc[w * C + c];
-    a.hist[static_cast<int64_t>(c) * a.n_tiles + tile] = t;
-  }
-  if (!last_cta(&a.done[0])) return;
-  // ---- epilogue (one CTA): exclusive scan of hist in [client][tile] order ----
-  __shared__ uint32_t warp_buf[32];
-  const int64_t L = a.hist_L;
-  const int64_t per = (L + blockDim.x - 1) / blockDim.x;
-  const int64_t b0 = ::min(L, per * static_cast<int64_t>(threadIdx.x)), b1 = ::min(L, b0 + per);
-  uint32_t sum = 0;
-  for (int64_t i0 = b0; i0 < b1; i0 += 8) {  // 8 independent L2 loads in flight
-    uint32_t v[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) v[k] = (i0 + k < b1) ? __ldcg(a.hist + i0 + k) : 0u;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) sum += v[k];
-  }
-  uint32_t run;
-  const uint32_t total = block_exclusive_scan(sum, &run, warp_buf);
-  for (int64_t i0 = b0; i0 < b1; i0 += 8) {
-    uint32_t v[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) v[k] = (i0 + k < b1) ? __ldcg(a.hist + i0 + k) : 0u;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int64_t i = i0 + k;
-      if (i < b1) {
-        __stcg(a.hist + i, run);
-        if (i % a.n_tiles == 0) a.seg_off[i / a.n_tiles] = static_cast<int32_t>(run);
-        run += v[k];
-      }
-    }
-  }
-  if (threadIdx.x == 0) {
-    a.seg_off[C] = static_cast<int32_t>(total);
-    a.done[0] = 0;
-  }
-}
 
 // on_activated in arrival order for every client that goes idle -> backlogged in this drain.
 // The lift target is the componentwise min over *other* backlogged clients at that moment.
@@ -300,25 +237,83 @@ __device__ void lift_core(const LiftIn& a, const Key* first_row) {
   for (int c = tid; c < C; c += blockDim.x) a.backlogged[c] = (a.qlen_before[c] + a.count[c]) > 0 ? 1 : 0;
 }
 
-__device__ void lift_epilogue(const DrainArgs& a) {
-  // counts and first arrival rows from the segment offsets / perm
-  for (int c = threadIdx.x; c < a.C; c += blockDim.x) {
-    const int32_t s0 = __ldcg(a.seg_off + c), s1 = __ldcg(a.seg_off + c + 1);
-    a.count[c] = s1 - s0;
-    a.first_row[c] = s1 > s0 ? static_cast<int32_t>(__ldcg(a.perm + s0)) : 0x7fffffff;
-  }
-  __syncthreads();
+// on_activated / set_backlogged for a drained queue (counts from drain_rank_kernel, first
+// rows from drain_hist_kernel): a standalone eqx_drain, or the selection kernel's prologue.
+__global__ void __launch_bounds__(1024) lift_kernel(const DrainArgs a) {
   const LiftIn l{a.C, a.counter_lift, a.count, a.qlen_before, a.running, a.ufc, a.rfc, a.counter, a.backlogged};
   lift_core<int32_t>(l, a.first_row);
 }
 
+#ifdef EQX_PROF
+#define EQX_DT_MIN(i) do { if (threadIdx.x == 0) atomicMin(&a.st->dt[i], global_ns()); } while (0)
+#define EQX_DT_MAX(i) do { if (threadIdx.x == 0) atomicMax(&a.st->dt[i], global_ns()); } while (0)
+#else
+#define EQX_DT_MIN(i) do {} while (0)
+#define EQX_DT_MAX(i) do {} while (0)
+#endif
+
+__global__ void __launch_bounds__(kDrainThreads) drain_hist_kernel(const DrainArgs a) {
+  extern __shared__ __align__(16) uint32_t sh[];
+  EQX_DT_MIN(0);
+  const int32_t C = a.C;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint16_t* wc = reinterpret_cast<uint16_t*>(sh);  // [kDrainWarps][C]
+  uint32_t* fr = sh + (kDrainWarps * C + 1) / 2;    // [C] first row of each client in the tile
+  for (int i = tid; i < kDrainWarps * C; i += blockDim.x) wc[i] = 0;
+  for (int c = tid; c < C; c += blockDim.x) fr[c] = 0xffffffffu;
+  __syncthreads();
+  const int32_t tile = blockIdx.x;
+  const int32_t sub = a.tile_rows / kDrainWarps;
+  const int32_t r0 = tile * a.tile_rows + warp * sub;
+  const int32_t r1 = min(a.n, r0 + sub);
+  uint16_t* my = wc + warp * C;
+  bool bad = false;
+  for (int32_t rb = r0; rb < r1; rb += 32 * 8) {  // 8 loads in flight per lane, then walk
+    int32_t cv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int32_t row = rb + 32 * u + lane;
+      cv[u] = row < r1 ? a.client[row] : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {  // per-warp counts: one writer per (warp, client)
+      const int32_t row = rb + 32 * u + lane;
+      const int32_t c = cv[u];
+      const bool ok = static_cast<uint32_t>(c) < static_cast<uint32_t>(C);
+      bad |= row < r1 && !ok;
+      const unsigned peers = peer_mask(ok ? static_cast<uint32_t>(c) : static_cast<uint32_t>(C), a.cbits);
+      if (ok && lane == __ffs(peers) - 1) {  // the earliest row of the client in these 32
+        if (my[c] == 0) atomicMin(&fr[c], static_cast<uint32_t>(row));
+        my[c] = static_cast<uint16_t>(my[c] + __popc(peers));
+      }
+      __syncwarp();
+    }
+  }
+  if (bad) a.st->bad_client = 1;
+  __syncthreads();
+  for (int c = tid; c < C; c += blockDim.x)
+    if (fr[c] != 0xffffffffu) atomicMin(reinterpret_cast<unsigned int*>(a.first_row) + c, fr[c]);
+  uint16_t* g = a.wcnt + static_cast<int64_t>(tile) * kDrainWarps * C;
+  for (int i = tid; i < kDrainWarps * C; i += blockDim.x) g[i] = wc[i];
+  for (int c = tid; c < C; c += blockDim.x) {
+    uint32_t t = 0;
+#pragma unroll 8
+    for (int w = 0; w < kDrainWarps; ++w) t += wc[w * C + c];
+    a.hist[static_cast<int64_t>(tile) * C + c] = t;  // [tile][client]
+  }
+  EQX_DT_MAX(1);
+}
+
+
+
 // Stable scatter of row indices into per-client FIFO segments.  Each CTA owns one tile; each
 // of its 8 warps walks a contiguous sub-tile 32 rows at a time in row order, ranking rows of
-// the same client with __match_any_sync.  Walk 1 counts per (warp, client); scans over warps
+// the same client (ballot peer masks).  Walk 1 counts per (warp, client); scans over warps
 // and clients give every row its slot in a client-sorted copy of the tile in shared memory
 // (walk 2), which is then written to perm as contiguous per-client runs (coalesced).
 __global__ void __launch_bounds__(kDrainThreads) drain_rank_kernel(const DrainArgs a) {
   extern __shared__ __align__(16) uint32_t sh[];
+  EQX_DT_MIN(3);
   const int32_t C = a.C;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int32_t tile = blockIdx.x;
@@ -331,10 +326,72 @@ __global__ void __launch_bounds__(kDrainThreads) drain_rank_kernel(const DrainAr
   uint32_t* base = sh;                                     // [C] global start of this tile's run
   uint32_t* toff = sh + C;                                 // [C] tile-local start / totals
   uint16_t* wc = reinterpret_cast<uint16_t*>(sh + 2 * C);  // [kDrainWarps][C]
-  for (int c = tid; c < C; c += blockDim.x) base[c] = a.hist[static_cast<int64_t>(c) * a.n_tiles + tile];
   {  // per-warp client counts from drain_hist_kernel's walk
     const uint16_t* g = a.wcnt + static_cast<int64_t>(tile) * kDrainWarps * C;
     for (int i = tid; i < kDrainWarps * C; i += blockDim.x) wc[i] = g[i];
+  }
+  // Every CTA derives its own global offsets from the [tile][client] histogram (no serial
+  // scan): base[c] = sum_{c' < c} total[c'] + sum_{t < tile} hist[t][c].  G threads per
+  // client split the tiles; the rows are read coalesced across clients.
+  for (int c = tid; c < C; c += blockDim.x) base[c] = toff[c] = 0;
+  __syncthreads();
+  {
+    const int NT = blockDim.x;
+    int G = 1;  // threads per client: a power of two, so client groups never straddle warps
+    while (G * 2 * C <= NT) G *= 2;
+    const int32_t nt = a.n_tiles;
+    for (int c0 = 0; c0 < C; c0 += NT / G) {
+      const int c = c0 + tid / G, g = tid % G;
+      uint32_t pre = 0, tot = 0;
+      if (tid / G < NT / G && c < C) {
+        for (int32_t t0 = g; t0 < nt; t0 += 8 * G) {  // 8 independent L2 loads in flight
+          uint32_t h[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int32_t t = t0 + u * G;
+            h[u] = t < nt ? __ldcg(a.hist + static_cast<int64_t>(t) * C + c) : 0u;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            tot += h[u];
+            pre += t0 + u * G < tile ? h[u] : 0u;
+          }
+        }
+      }
+      for (int o = 1; o < G && o < 32; o <<= 1) {  // segment sums (lane g == 0 of each group)
+        pre += __shfl_down_sync(0xffffffffu, pre, o);
+        tot += __shfl_down_sync(0xffffffffu, tot, o);
+      }
+      if (G > 32) {  // combine the warps of one client through shared memory
+        if (lane == 0 && c < C) {
+          atomicAdd(&base[c], pre);
+          atomicAdd(&toff[c], tot);
+        }
+      } else if (g == 0 && c < C) {
+        base[c] = pre;
+        toff[c] = tot;
+      }
+    }
+  }
+  __syncthreads();
+  {  // segment starts: exclusive scan of the per-client totals
+    __shared__ uint32_t warp_buf[32];
+    const int per = (C + blockDim.x - 1) / blockDim.x;
+    const int c0 = min(C, per * tid), c1 = min(C, c0 + per);
+    uint32_t s = 0;
+    for (int c = c0; c < c1; ++c) s += toff[c];
+    uint32_t run;
+    const uint32_t total = block_exclusive_scan(s, &run, warp_buf);
+    for (int c = c0; c < c1; ++c) {
+      const uint32_t t = toff[c];
+      if (tile == 0) {
+        a.seg_off[c] = static_cast<int32_t>(run);
+        a.count[c] = static_cast<int32_t>(t);
+      }
+      base[c] += run;
+      run += t;
+    }
+    if (tile == 0 && tid == 0) a.seg_off[C] = static_cast<int32_t>(total);
   }
   __syncthreads();
   uint16_t* my = wc + warp * C;
@@ -378,7 +435,7 @@ __global__ void __launch_bounds__(kDrainThreads) drain_rank_kernel(const DrainAr
         const int32_t row = rb + 32 * u + lane;
         const int32_t c = cv[u];
         const bool ok = static_cast<uint32_t>(c) < static_cast<uint32_t>(C);
-        const unsigned peers = __match_any_sync(0xffffffffu, ok ? c : -1);
+        const unsigned peers = peer_mask(ok ? static_cast<uint32_t>(c) : static_cast<uint32_t>(C), a.cbits);
         const int leader = __ffs(peers) - 1;
         uint32_t start = 0;
         if (ok && lane == leader) {
@@ -404,10 +461,10 @@ __global__ void __launch_bounds__(kDrainThreads) drain_rank_kernel(const DrainAr
     for (int32_t r = r0; r < r1; r += 32) {  // walk 2: direct scatter (large rosters)
       const int32_t row = r + lane;
       const int32_t c = row < r1 ? a.client[row] : -1;
-      const unsigned peers = __match_any_sync(0xffffffffu, c);
+      const bool ok = static_cast<uint32_t>(c) < static_cast<uint32_t>(C);
+      const unsigned peers = peer_mask(ok ? static_cast<uint32_t>(c) : static_cast<uint32_t>(C), a.cbits);
       const int leader = __ffs(peers) - 1;
       uint32_t start = 0;
-      const bool ok = static_cast<uint32_t>(c) < static_cast<uint32_t>(C);
       if (ok && lane == leader) {
         start = my[c];
         my[c] = static_cast<uint16_t>(start + __popc(peers));
@@ -417,9 +474,7 @@ __global__ void __launch_bounds__(kDrainThreads) drain_rank_kernel(const DrainAr
       __syncwarp();
     }
   }
-  if (!last_cta(&a.done[1])) return;
-  lift_epilogue(a);
-  if (threadIdx.x == 0) a.done[1] = 0;
+  EQX_DT_MAX(4);
 }
 
 // ===================================== scoring ===========================================
@@ -875,6 +930,82 @@ struct BatchScratch {
   int32_t* evx;      // [Tn] event index of accepted items
 };
 
+// Bitonic sort of NT*P tuples held P per thread in registers (blocked: thread t owns items
+// t*P .. t*P+P-1): partners inside a thread are compare-exchanged in registers, partners in
+// another lane of the warp through shuffles, and only strides of 32*P and more go through
+// shared memory.  Same network (and result) as the plain shared-memory loop.
+__device__ __forceinline__ BatchItem shfl_item(const BatchItem& x, int m) {
+  BatchItem y;
+  y.k = __shfl_xor_sync(0xffffffffu, x.k, m);
+  y.a = __shfl_xor_sync(0xffffffffu, x.a, m);
+  y.o = __shfl_xor_sync(0xffffffffu, x.o, m);
+  y.meta = __shfl_xor_sync(0xffffffffu, x.meta, m);
+  return y;
+}
+
+template <int P>
+__device__ __noinline__ void bitonic_sort_reg(BatchItem* items, int32_t Tn) {
+  const int tid = threadIdx.x;
+  BatchItem x[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) x[p] = items[tid * P + p];
+  for (int32_t k = 2; k <= Tn; k <<= 1) {
+    for (int32_t j = k >> 1; j > 0; j >>= 1) {
+      if (j < P) {  // compile-time partner indices keep x[] in registers
+        auto cx = [&](auto J) {
+          constexpr int jj = decltype(J)::value;
+#pragma unroll
+          for (int p = 0; p < P; ++p) {
+            const int q = p ^ jj;
+            if (q > p) {
+              const int32_t i = tid * P + p;
+              const bool up = (i & k) == 0;
+              if (up ? item_better(x[q], x[p]) : item_better(x[p], x[q])) {
+                const BatchItem t = x[p];
+                x[p] = x[q];
+                x[q] = t;
+              }
+            }
+          }
+        };
+        if (j == 1) cx(std::integral_constant<int, 1>{});
+        if constexpr (P > 2) if (j == 2) cx(std::integral_constant<int, 2>{});
+        if constexpr (P > 4) if (j == 4) cx(std::integral_constant<int, 4>{});
+      } else if (j < 32 * P) {
+        const int m = j / P;  // partner lane distance
+        const bool lower = ((tid & 31) & m) == 0;
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          const BatchItem y = shfl_item(x[p], m);
+          const int32_t i = tid * P + p;
+          const bool up = (i & k) == 0;
+          const bool want_min = lower == up;
+          const bool take = want_min ? item_better(y, x[p]) : item_better(x[p], y);
+          if (take) x[p] = y;
+        }
+      } else {
+        __syncthreads();
+#pragma unroll
+        for (int p = 0; p < P; ++p) items[tid * P + p] = x[p];
+        __syncthreads();
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          const int32_t i = tid * P + p, ixj = i ^ j;
+          const BatchItem y = items[ixj];
+          const bool up = (i & k) == 0;
+          const bool want_min = (i < ixj) == up;
+          const bool take = want_min ? item_better(y, x[p]) : item_better(x[p], y);
+          if (take) x[p] = y;
+        }
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int p = 0; p < P; ++p) items[tid * P + p] = x[p];
+  __syncthreads();
+}
+
 // One batch by the whole CTA.  Returns kBatchDone / kBatchNeedMax; *accepted = events emitted.
 __device__ int32_t batch_phase(const SelectArgs& a, const WinEntry* win, const ClientWork& cw, SelShared& S,
                                const BatchScratch& B, int32_t* accepted) {
@@ -924,6 +1055,13 @@ __device__ int32_t batch_phase(const SelectArgs& a, const WinEntry* win, const C
   __syncthreads();
   long long c1 = clock64();
   // 2. bitonic sort of the Tn tuples
+  if (NT == 256 && Tn == 512) {
+    bitonic_sort_reg<2>(B.items, Tn);
+  } else if (NT == 256 && Tn == 1024) {
+    bitonic_sort_reg<4>(B.items, Tn);
+  } else if (NT == 256 && Tn == 2048) {
+    bitonic_sort_reg<8>(B.items, Tn);
+  } else
   for (int32_t kk = 2; kk <= Tn; kk <<= 1) {
     for (int32_t j = kk >> 1; j > 0; j >>= 1) {
       for (int32_t i = tid; i < Tn; i += NT) {
@@ -2058,7 +2196,7 @@ __device__ __forceinline__ void warp_select_reg(const SelectArgs& a, const Model
 // kMode: -1 multi-mode loops (select_kernel); 0 warp_select_phase; 1/2/4 warp_select_reg<kMode>
 template <int kMode>
 __device__ __forceinline__ void select_body(const SelectArgs& a) {
-  constexpr bool kWarp = kMode >= 0;
+  constexpr bool kWarp = kMode >= 0 && kMode != 8;  // 8: speculative batches + shared-memory picks
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ SelShared S;
   const int32_t C = a.C;
@@ -2119,6 +2257,11 @@ __device__ __forceinline__ void select_body(const SelectArgs& a) {
   __syncthreads();
   const ModelTables& M = *reinterpret_cast<const ModelTables*>(smem);
 
+  if (a.do_lift) {  // on_activated / set_backlogged of the drain that preceded this step
+    const LiftIn l{C, a.counter_lift, a.count, a.qlen_before, a.running, a.ufc, a.rfc, a.counter, a.backlogged};
+    lift_core<int32_t>(l, a.first_row);
+    __syncthreads();
+  }
   // ---- ledger in, head windows (bulk copy of window_kernel's [C][W] entries) ----
   for (int32_t c = tid; c < C; c += NT) {
     cw.ufc[c] = a.ufc[c];
@@ -2175,7 +2318,7 @@ __device__ __forceinline__ void select_body(const SelectArgs& a) {
   if constexpr (kMode == 0) {  // default: single-warp selection
     warp_select_phase(a, M, win, cw, S, T);
     ns = 1;
-  } else if constexpr (kMode > 0) {
+  } else if constexpr (kWarp && kMode > 0) {
     warp_select_reg<kMode>(a, M, win, cw, S, T);
     ns = 1;
   }
@@ -2189,12 +2332,16 @@ __device__ __forceinline__ void select_body(const SelectArgs& a) {
       if (acc >= 4) continue;
     }
     const int32_t picks = a.D > 0 ? 8 : 0x7fffffff;
-    switch (a.K) {  // register-resident slots per thread (selection threads = a.sel_threads)
-      case 1: seq_reg_phase<1>(a, M, win, cw, S, picks, T); break;
-      case 2: seq_reg_phase<2>(a, M, win, cw, S, picks, T); break;
-      case 4: seq_reg_phase<4>(a, M, win, cw, S, picks, T); break;
-      case 8: seq_reg_phase<8>(a, M, win, cw, S, picks, T); break;
-      default: seq_phase(a, M, win, cw, S, picks); break;
+    if constexpr (kMode == 8) {
+      seq_phase(a, M, win, cw, S, picks);
+    } else {
+      switch (a.K) {  // register-resident slots per thread (selection threads = a.sel_threads)
+        case 1: seq_reg_phase<1>(a, M, win, cw, S, picks, T); break;
+        case 2: seq_reg_phase<2>(a, M, win, cw, S, picks, T); break;
+        case 4: seq_reg_phase<4>(a, M, win, cw, S, picks, T); break;
+        case 8: seq_reg_phase<8>(a, M, win, cw, S, picks, T); break;
+        default: seq_phase(a, M, win, cw, S, picks); break;
+      }
     }
     ++ns;
     __syncthreads();
@@ -2234,6 +2381,7 @@ template __global__ void select_warp_kernel<0>(SelectArgs);
 template __global__ void select_warp_kernel<1>(SelectArgs);
 template __global__ void select_warp_kernel<2>(SelectArgs);
 template __global__ void select_warp_kernel<4>(SelectArgs);
+template __global__ void select_warp_kernel<8>(SelectArgs);
 
 // Event payloads (scheduler.hpp:131-138 PendingContribution) from the per-request scores the
 // scoring kernel wrote: predicted tokens, ufc/rfc increments, the VTC charge and wait_s.

@@ -36,6 +36,7 @@ struct DrainArgs {
   const int32_t* client;
   int32_t n;
   int32_t C;
+  int32_t cbits;        // bits of a client key (keys 0..C; C marks rows outside the roster)
   int32_t tile_rows;
   int32_t n_tiles;
   int32_t staged;       // 1: smem-staged coalesced scatter (when the tile fits in smem)
@@ -131,7 +132,11 @@ struct SelectArgs {
   int32_t Tn;            // batch sort size (power of two >= C * D)
   int32_t sel_threads;   // threads in the selection loop (multiple of 32)
   int32_t K;             // register client slots per selection thread (1/2/4/8; 0 = smem loop)
-  int32_t warp_sel;      // 1: single-warp selection (warp_select_phase), the default
+  int32_t warp_sel;      // selection kernel variant (eqx_capi.cu select_fn)
+  int32_t do_lift;       // run the drain's counter lift / backlog flags first (drain + step)
+  const int32_t* first_row;
+  const int32_t* qlen_before;
+  int32_t counter_lift;
   int32_t Ds;            // key-stream lookahead per client for the register loop
   int32_t cw_in_smem;
   void* cw_global;       // per-client work arrays when they do not fit in smem
@@ -237,6 +242,7 @@ __global__ void shard_unpack_kernel(ShardMap m, ShardSelectBufs b);
 __global__ void shard_event_fill_kernel(EventFillArgs a, const WinEntry* win);
 
 __global__ void drain_hist_kernel(DrainArgs a);
+__global__ void lift_kernel(DrainArgs a);
 __global__ void event_fill_kernel(EventFillArgs a);
 __global__ void drain_rank_kernel(DrainArgs a);
 __global__ void score_kernel(ScoreArgs a);

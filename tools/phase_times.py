@@ -12,6 +12,6 @@ flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
 for i in range(5):
     sch.restore_async(); flush.zero_(); torch.cuda.synchronize()
     sch.drain(**cols); sch.step_async(1.0); r = sch.collect(with_events=False)
-    out = (C.c_double * 16)()
-    L.load().eqx_phase_times(sch._ctx, out, 16)
-    print(r.n_admitted, [round(x, 2) for x in out[:6]], 'batches', out[6], 'seq', out[7], 'cyc gen/sort/verify/commit', list(out[8:12]), 'seq cyc arg/proc/tail/picks', list(out[12:16]))
+    out = (C.c_double * 22)()
+    L.load().eqx_phase_times(sch._ctx, out, 22)
+    print(r.n_admitted, [round(x, 2) for x in out[:6]], 'batches', out[6], 'seq', out[7], 'cyc gen/sort/verify/commit', list(out[8:12]), 'seq cyc arg/proc/tail/picks', list(out[12:16]), 'drain hist walk/epi rank start/walk/epi us', [round(x,2) for x in out[17:22]])
