@@ -894,6 +894,7 @@ struct StepPlan {
   SelectArgs se;
   size_t score_smem, select_smem, window_smem;
   int score_grid, select_threads, window_grid;
+  int score_tma;  // 1: score_tma_kernel (bulk-copy tiles), 0: score_kernel
 };
 
 // gW > 0 plans the selection of a client-sharded step over gathered [C][gW] head windows
@@ -988,8 +989,29 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl, int32_t g
     ctx->occ_smem = pl.score_smem;
   }
   per_sm = ctx->occ_per_sm;
-  const int64_t want = (ctx->n / 8 + kScoreThreads - 1) / kScoreThreads;
+  const int64_t want = (ctx->n / 8 + kScoreThreads - 1) / kScoreThreads;  // two 4-request vectors per thread
   pl.score_grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, static_cast<int64_t>(ctx->sm_count) * std::max(per_sm, 1))));
+  {  // TMA-pipelined variant: 16-byte aligned columns (bulk copies) and at least one full tile
+    const char* m = std::getenv("EQX_SCORE");
+    // opt-in (EQX_SCORE=tma): measured slower than the register-streaming kernel (profiles/)
+    const bool tma_ok = sc.vec_ok && (reinterpret_cast<uintptr_t>(sc.tag) % 16 == 0) && ctx->n >= kScoreTile &&
+                        (m && std::string(m) == "tma");
+    pl.score_tma = tma_ok ? 1 : 0;
+    if (tma_ok) {
+      // ring | model | direct table (staged in shared memory when it fits two CTAs per SM)
+      const int32_t dwords = ctx->direct_n ? (ctx->model.pred_kind == kPredOracle ? ctx->direct_n
+                                                                                  : ctx->direct_n * ctx->model.n_tag_states)
+                                           : 0;
+      size_t tsmem = static_cast<size_t>(kScoreStages) * kScoreStageBytes +
+                     ((static_cast<size_t>(model_words) * 4 + 127) & ~size_t(127));
+      sc.direct_words = (tsmem + 4ull * dwords) * 2 <= ctx->smem_optin ? dwords : 0;
+      tsmem += 4ull * sc.direct_words;
+      pl.score_smem = tsmem;
+      CUDA_TRY(ctx, set_smem_attr(ctx, 7, reinterpret_cast<const void*>(score_tma_kernel), tsmem));
+      const int64_t tiles = ctx->n / kScoreTile;
+      pl.score_grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(tiles, 2ll * ctx->sm_count)));
+    }
+  }
   // ---- selection ----
   SelectArgs& a = pl.se;
   a.client = ctx->q_client;
@@ -1170,7 +1192,10 @@ static eqx_status step_enqueue(eqx_ctx* ctx, const StepPlan& pl, bool with_drain
   CUDA_TRY(ctx, cudaStreamWaitEvent(s2, ctx->ev_fork, 0));
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[0], s2));
   if (ctx->n > 0)
-    score_kernel<<<pl.score_grid, kScoreThreads, pl.score_smem, s2>>>(pl.sc);
+    {
+    if (pl.score_tma) score_tma_kernel<<<pl.score_grid, kScoreTmaThreads, pl.score_smem, s2>>>(pl.sc);
+    else score_kernel<<<pl.score_grid, kScoreThreads, pl.score_smem, s2>>>(pl.sc);
+  }
   CUDA_TRY(ctx, cudaGetLastError());
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[1], s2));
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_join, s2));
@@ -1299,7 +1324,10 @@ eqx_status eqx_shard_export_async(eqx_ctx* ctx, double now, int32_t cmax, int32_
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fork, s));
   CUDA_TRY(ctx, cudaStreamWaitEvent(s2, ctx->ev_fork, 0));
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[0], s2));
-  if (ctx->n > 0) score_kernel<<<pl.score_grid, kScoreThreads, pl.score_smem, s2>>>(pl.sc);
+  if (ctx->n > 0) {
+    if (pl.score_tma) score_tma_kernel<<<pl.score_grid, kScoreTmaThreads, pl.score_smem, s2>>>(pl.sc);
+    else score_kernel<<<pl.score_grid, kScoreThreads, pl.score_smem, s2>>>(pl.sc);
+  }
   CUDA_TRY(ctx, cudaGetLastError());
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[1], s2));
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_join, s2));

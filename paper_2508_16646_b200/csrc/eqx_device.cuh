@@ -177,7 +177,7 @@ __device__ __forceinline__ Scored score_request_direct(const ModelTables& M, con
   if constexpr (KIND == kPredMope) {
     const uint32_t t = tag < static_cast<uint32_t>(M.n_tag_states) ? tag : 0u;
     if (static_cast<uint32_t>(in) < static_cast<uint32_t>(direct_n)) {
-      const uint32_t e = __ldg(direct + t * static_cast<uint32_t>(direct_n) + static_cast<uint32_t>(in));
+      const uint32_t e = direct[t * static_cast<uint32_t>(direct_n) + static_cast<uint32_t>(in)];
       pred = static_cast<int32_t>(e & 0xffffu);
       b = static_cast<int32_t>((e >> 16) & 0xffu);
       s.fallback = e >> 24;
@@ -187,7 +187,7 @@ __device__ __forceinline__ Scored score_request_direct(const ModelTables& M, con
   } else if constexpr (KIND == kPredOracle) {
     pred = true_out > 1 ? true_out : 1;
     if (pred < direct_n) {
-      b = static_cast<int32_t>(__ldg(direct + pred));
+      b = static_cast<int32_t>(direct[pred]);
     } else {
       return score_request_t<KIND>(M, P, now, in, tag, true_out, id, arrival, w);
     }

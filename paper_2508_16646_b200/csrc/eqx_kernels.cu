@@ -553,6 +553,164 @@ __global__ void __launch_bounds__(kScoreThreads, 4) score_kernel(const ScoreArgs
   if (threadIdx.x == 0) atomicMax(&a.st->t[5], global_ns());
 }
 
+// ---- TMA-pipelined whole-queue scoring ---------------------------------------------------
+// Persistent CTAs (2 per SM) stream tiles of kScoreTile requests: one elected thread arms an
+// mbarrier and issues 1-D bulk copies (cp.async.bulk, the TMA engine) of the tile's columns
+// into a kScoreStages-deep shared-memory ring, so several tiles per SM are in flight without
+// any thread holding registers for them; all threads score the landed tile from shared memory
+// and write the outputs with coalesced 16-byte streaming stores.  Rows past the last full tile
+// take the register path (score_body).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n EQX_WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra EQX_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// PHASE 0: issue the first kScoreStages tiles (thread 0); PHASE 1: consume all tiles.
+template <int KIND, int PHASE>
+__device__ __forceinline__ void score_tma_body(const ScoreArgs& a, const ModelTables& M, unsigned char* ring,
+                                               uint64_t* bars) {
+  constexpr bool oracle_like = KIND == kPredOracle || KIND == kPredNoisy;
+  constexpr int R = kScoreTile;
+  constexpr uint32_t kBytes = R * (4 + 8 + 4 + 1) + (oracle_like ? 4 * R : 0);
+  const int tid = threadIdx.x;
+  const int64_t n_full = a.n / R;
+  auto stage_ptr = [&](int st) { return ring + static_cast<size_t>(st) * kScoreStageBytes; };
+  auto issue = [&](int64_t tile, int st) {  // one thread: arm the stage barrier, copy the columns
+    unsigned char* b = stage_ptr(st);
+    const int64_t r0 = tile * R;
+    mbar_expect_tx(&bars[st], kBytes);
+    bulk_g2s(b, a.client + r0, 4 * R, &bars[st]);
+    bulk_g2s(b + 4 * R, a.arrival + r0, 8 * R, &bars[st]);
+    bulk_g2s(b + 12 * R, a.in_tok + r0, 4 * R, &bars[st]);
+    bulk_g2s(b + 16 * R, a.tag + r0, R, &bars[st]);
+    if constexpr (oracle_like) bulk_g2s(b + 17 * R, a.true_out + r0, 4 * R, &bars[st]);
+  };
+  if constexpr (PHASE == 0) {
+    if (tid == 0) {
+      int64_t t = blockIdx.x;
+      for (int st = 0; st < kScoreStages && t < n_full; ++st, t += gridDim.x) issue(t, st);
+    }
+    return;
+  }
+  uint32_t fb = 0, nt = 0;
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < n_full; tile += gridDim.x, ++it) {
+    const int st = it % kScoreStages;
+    mbar_wait(&bars[st], static_cast<uint32_t>((it / kScoreStages) & 1));
+    const unsigned char* b = stage_ptr(st);
+    const int64_t r0 = tile * R;
+#pragma unroll
+    for (int q = 0; q < R / (4 * kScoreTmaThreads); ++q) {
+      const int j = 4 * (tid + q * kScoreTmaThreads);  // tile-local row of this thread's 4 requests
+      const int4 cl = *reinterpret_cast<const int4*>(b + 4 * j);
+      const double2 a01 = *reinterpret_cast<const double2*>(b + 4 * R + 8 * j);
+      const double2 a23 = *reinterpret_cast<const double2*>(b + 4 * R + 8 * j + 16);
+      const int4 in4 = *reinterpret_cast<const int4*>(b + 12 * R + 4 * j);
+      const uint32_t tg = *reinterpret_cast<const uint32_t*>(b + 16 * R + j);
+      int4 to = make_int4(1, 1, 1, 1);
+      if constexpr (oracle_like) to = *reinterpret_cast<const int4*>(b + 17 * R + 4 * j);
+      const int cs[4] = {cl.x, cl.y, cl.z, cl.w};
+      const int ins[4] = {in4.x, in4.y, in4.z, in4.w};
+      const int tos[4] = {to.x, to.y, to.z, to.w};
+      const double arr[4] = {a01.x, a01.y, a23.x, a23.y};
+      const int64_t r = r0 + j;
+      Scored sc[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int64_t id = (KIND == kPredNoisy && a.id) ? a.id[r + k] : a.id_base + r + k;
+        const double w = __ldg(a.weight + cs[k]);
+        sc[k] = score_request_direct<KIND>(M, a.pol, a.direct, a.direct_n, a.now, ins[k], (tg >> (8 * k)) & 0xffu,
+                                           tos[k], id, arr[k], w);
+        fb += sc[k].fallback;
+        nt += sc[k].near_tie;
+      }
+      const int64_t v = r / 4;
+      stg_stream(reinterpret_cast<int4*>(a.pred_out) + v, make_int4(sc[0].pred, sc[1].pred, sc[2].pred, sc[3].pred));
+      stg_stream(reinterpret_cast<uint32_t*>(a.bucket_out) + v,
+                 static_cast<uint32_t>(sc[0].bucket) | (static_cast<uint32_t>(sc[1].bucket) << 8) |
+                     (static_cast<uint32_t>(sc[2].bucket) << 16) | (static_cast<uint32_t>(sc[3].bucket) << 24));
+      stg_stream(reinterpret_cast<double2*>(a.ufc_out) + 2 * v, make_double2(sc[0].ufc_inc, sc[1].ufc_inc));
+      stg_stream(reinterpret_cast<double2*>(a.ufc_out) + 2 * v + 1, make_double2(sc[2].ufc_inc, sc[3].ufc_inc));
+      stg_stream(reinterpret_cast<double2*>(a.rfc_out) + 2 * v, make_double2(sc[0].rfc_inc, sc[1].rfc_inc));
+      stg_stream(reinterpret_cast<double2*>(a.rfc_out) + 2 * v + 1, make_double2(sc[2].rfc_inc, sc[3].rfc_inc));
+    }
+    __syncthreads();  // every thread is done with this stage
+    const int64_t next = tile + static_cast<int64_t>(kScoreStages) * gridDim.x;
+    if (tid == 0 && next < n_full) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before async writes
+      issue(next, st);
+    }
+  }
+  // rows after the last full tile
+  for (int64_t r = n_full * R + static_cast<int64_t>(blockIdx.x) * blockDim.x + tid; r < a.n;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t c = a.client[r];
+    const int64_t id = a.id ? a.id[r] : a.id_base + r;
+    const Scored sc = score_request_direct<KIND>(M, a.pol, a.direct, a.direct_n, a.now, a.in_tok[r], a.tag[r],
+                                                 oracle_like ? a.true_out[r] : 1, id, a.arrival[r], a.weight[c]);
+    a.pred_out[r] = sc.pred;
+    a.bucket_out[r] = static_cast<uint8_t>(sc.bucket);
+    a.ufc_out[r] = sc.ufc_inc;
+    a.rfc_out[r] = sc.rfc_inc;
+    fb += sc.fallback;
+    nt += sc.near_tie;
+  }
+  fb = __reduce_add_sync(0xffffffffu, fb);
+  nt = __reduce_add_sync(0xffffffffu, nt);
+  if ((tid & 31) == 0) {
+    if (fb) atomicAdd(&a.st->fallbacks, static_cast<unsigned long long>(fb));
+    if (nt) atomicAdd(&a.st->near_ties, static_cast<unsigned long long>(nt));
+  }
+}
+
+__global__ void __launch_bounds__(kScoreTmaThreads, 2) score_tma_kernel(const ScoreArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bars[kScoreStages];
+  // layout: tile ring | compiled model | direct predict/map table
+  unsigned char* ring = smem;
+  unsigned char* msm = smem + static_cast<size_t>(kScoreStages) * kScoreStageBytes;
+  uint32_t* dsm = reinterpret_cast<uint32_t*>(msm + ((a.model_words * 4 + 127) & ~127));
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kScoreStages; ++st) mbar_init(&bars[st], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  ScoreArgs b = a;
+  b.direct = a.direct_words > 0 ? dsm : a.direct;
+  const int kind = __ldg(&a.model->pred_kind);
+  // the first tiles' bulk copies start before the tables are staged
+  if (kind == kPredOracle) score_tma_body<kPredOracle, 0>(b, *a.model, ring, bars);
+  else if (kind == kPredNoisy) score_tma_body<kPredNoisy, 0>(b, *a.model, ring, bars);
+  else score_tma_body<kPredMope, 0>(b, *a.model, ring, bars);
+  stage_model(a.model, a.model_words, msm);
+  for (int i = threadIdx.x; i < a.direct_words; i += blockDim.x) dsm[i] = __ldg(a.direct + i);
+  __syncthreads();
+  const ModelTables& M = *reinterpret_cast<const ModelTables*>(msm);
+  if (threadIdx.x == 0) atomicMin(&a.st->t[4], global_ns());
+  if (kind == kPredOracle) score_tma_body<kPredOracle, 1>(b, M, ring, bars);
+  else if (kind == kPredNoisy) score_tma_body<kPredNoisy, 1>(b, M, ring, bars);
+  else score_tma_body<kPredMope, 1>(b, M, ring, bars);
+  __syncthreads();
+  if (threadIdx.x == 0) atomicMax(&a.st->t[5], global_ns());
+}
+
 // ===================================== selection =========================================
 
 // Candidate tuple of select_next (scheduler.cpp:139-153): (key, head arrival, client_id rank),

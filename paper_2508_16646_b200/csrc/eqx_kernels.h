@@ -11,6 +11,10 @@ namespace eqx {
 constexpr int kDrainThreads = 1024;  // 32 warps per tile
 constexpr int kDrainWarps = kDrainThreads / 32;
 constexpr int kScoreThreads = 256;
+constexpr int kScoreTmaThreads = 256;                        // score_tma_kernel block
+constexpr int kScoreTile = 1024;                             // requests per bulk-copied tile
+constexpr int kScoreStages = 3;                              // tiles in flight per CTA
+constexpr int kScoreStageBytes = kScoreTile * (4 + 8 + 4 + 1 + 4);  // columns (+ true_out)
 constexpr int kSelectMaxThreads = 256;
 
 // One head-of-queue entry as the selection loop consumes it (40 B, shared memory).
@@ -81,6 +85,7 @@ struct ScoreArgs {
   // Inputs outside [0, direct_n) take the interval/profile search.
   const uint32_t* direct;
   int32_t direct_n;
+  int32_t direct_words;  // uint32 words of `direct` (staged in shared memory by score_tma_kernel)
   int32_t vec_ok;
   Policy pol;
   double now;
@@ -246,6 +251,7 @@ __global__ void lift_kernel(DrainArgs a);
 __global__ void event_fill_kernel(EventFillArgs a);
 __global__ void drain_rank_kernel(DrainArgs a);
 __global__ void score_kernel(ScoreArgs a);
+__global__ void score_tma_kernel(ScoreArgs a);
 __global__ void window_kernel(WindowArgs a);
 __global__ void select_kernel(SelectArgs a);
 template <int kMode>
