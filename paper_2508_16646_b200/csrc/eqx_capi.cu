@@ -11,6 +11,7 @@
 #include <cstring>
 #include <numeric>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -175,6 +176,24 @@ const void* select_fn(int warp_sel) {
     case 5: return reinterpret_cast<const void*>(select_warp_kernel<8>);
     default: return reinterpret_cast<const void*>(select_kernel);
   }
+}
+
+// Programmatic dependent launch: the kernel may be scheduled while its predecessor on the
+// stream is still finishing; it executes griddepcontrol.wait before touching the predecessor's
+// results (pdl_wait in eqx_kernels.cu), so only launch latency and the prologue overlap.
+template <class... KArgs, class... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 cudaError_t set_smem_attr(eqx_ctx* ctx, int which, const void* fn, size_t bytes) {
@@ -863,7 +882,7 @@ static eqx_status drain_enqueue(eqx_ctx* ctx, bool lift) {
 #endif
   const DrainArgs d = drain_args(ctx);
   drain_hist_kernel<<<ctx->n_tiles, kDrainThreads, ctx->hist_smem, s>>>(d);
-  drain_rank_kernel<<<ctx->n_tiles, kDrainThreads, ctx->rank_smem, s>>>(d);
+  CUDA_TRY(ctx, launch_pdl(drain_rank_kernel, dim3(ctx->n_tiles), dim3(kDrainThreads), ctx->rank_smem, s, d));
   if (lift) lift_kernel<<<1, 1024, 0, s>>>(d);
   CUDA_TRY(ctx, cudaGetLastError());
   return EQX_OK;
@@ -1205,7 +1224,7 @@ static eqx_status step_enqueue(eqx_ctx* ctx, const StepPlan& pl, bool with_drain
     if (e != EQX_OK) return e;
   }
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[5], s));
-  window_kernel<<<pl.window_grid, 256, pl.window_smem, s>>>(pl.wi);
+  CUDA_TRY(ctx, launch_pdl(window_kernel, dim3(pl.window_grid), dim3(256), pl.window_smem, s, pl.wi));
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[2], s));
   {
     void* args[] = {const_cast<SelectArgs*>(&pl.se)};

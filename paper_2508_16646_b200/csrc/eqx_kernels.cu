@@ -57,6 +57,11 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+// Programmatic dependent launch (sm_90+): wait for the predecessor grid's results / let the
+// successor grid get scheduled early.  No-ops for kernels launched without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // Copy the compiled model (header + the LUT words in use) into shared memory.
 __device__ __forceinline__ void stage_model(const ModelTables* g, int words, unsigned char* smem) {
   const uint32_t* src = reinterpret_cast<const uint32_t*>(g);
@@ -255,6 +260,7 @@ __global__ void __launch_bounds__(1024) lift_kernel(const DrainArgs a) {
 __global__ void __launch_bounds__(kDrainThreads) drain_hist_kernel(const DrainArgs a) {
   extern __shared__ __align__(16) uint32_t sh[];
   EQX_DT_MIN(0);
+  pdl_trigger();
   const int32_t C = a.C;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint16_t* wc = reinterpret_cast<uint16_t*>(sh);  // [kDrainWarps][C]
@@ -326,6 +332,8 @@ __global__ void __launch_bounds__(kDrainThreads) drain_rank_kernel(const DrainAr
   uint32_t* base = sh;                                     // [C] global start of this tile's run
   uint32_t* toff = sh + C;                                 // [C] tile-local start / totals
   uint16_t* wc = reinterpret_cast<uint16_t*>(sh + 2 * C);  // [kDrainWarps][C]
+  pdl_wait();     // drain_hist_kernel's counts, histogram and first rows are complete
+  pdl_trigger();  // the window kernel may get scheduled
   {  // per-warp client counts from drain_hist_kernel's walk
     const uint16_t* g = a.wcnt + static_cast<int64_t>(tile) * kDrainWarps * C;
     for (int i = tid; i < kDrainWarps * C; i += blockDim.x) wc[i] = g[i];
@@ -862,7 +870,8 @@ __device__ __forceinline__ WinEntry get_entry(const SelectArgs& a, const ModelTa
 // First W queued entries of every client (C*W items, one per thread across many CTAs).
 __global__ void __launch_bounds__(256) window_kernel(const WindowArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
-  stage_model(a.model, a.model_words, smem);
+  stage_model(a.model, a.model_words, smem);  // overlaps the drain's tail (programmatic launch)
+  pdl_wait();
   __syncthreads();
   const ModelTables& M = *reinterpret_cast<const ModelTables*>(smem);
   const int64_t items = static_cast<int64_t>(a.C) * a.W;

@@ -38,7 +38,7 @@ def launches(path):
     ki, vi = h.index("Kernel Name"), h.index("Metric Value")
     out = []
     for r in rows[i + 1:]:
-        out.append((r[ki].split("(")[0].replace("eqx::", ""), float(r[vi].replace(",", ""))))
+        out.append((r[ki].split("(")[0].replace("eqx::", "").replace("void ", ""), float(r[vi].replace(",", ""))))
     return out
 
 
@@ -46,12 +46,11 @@ def main():
     lpath, rep, prefix = sys.argv[1:4]
     L = launches(lpath)
     # the last complete step: from the last flush memset onwards
-    ours = [x for x in L if not x[0].startswith("void at::")]
+    ours = [x for x in L if not x[0].startswith("at::")]  # drop the L2-flush memset
     per = defaultdict(list)
     for name, ns in ours:
         per[name].append(ns)
-    step_names = ["drain_hist_kernel", "drain_rank_kernel", "score_kernel", "window_kernel", "select_kernel",
-                  "event_fill_kernel"]
+    step_names = list(dict.fromkeys(name for name, _ in ours))  # our kernels, launch order
     lines = ["# Launch list (ncu --metrics gpu__time_duration.sum --clock-control none)", "",
              "Serialised, cold-cache per-launch device times of one cold scheduling step (cfg2: 1M requests,",
              "64 clients).  Inside a real step score_kernel overlaps drain+window+select (side stream), so the",
@@ -71,8 +70,9 @@ def main():
     kn = h.index("Kernel Name")
     seen = {}
     for r in rows[2:]:
-        name = r[kn].split("(")[0].replace("eqx::", "")
-        seen.setdefault(name, r)
+        name = r[kn].split("(")[0].replace("eqx::", "").replace("void ", "")
+        if not name.startswith("at::"):
+            seen.setdefault(name, r)
     out = ["# ncu --set full (clock-control none), one launch per kernel, cfg2 step", "",
            "| metric | " + " | ".join(seen) + " |", "|---|" + "---|" * len(seen)]
     for m, label in METRICS:
