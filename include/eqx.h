@@ -193,6 +193,36 @@ eqx_status eqx_step_collect(eqx_ctx* ctx, eqx_step_summary* out);
 /* Convenience: eqx_step_async + eqx_step_collect. */
 eqx_status eqx_step(eqx_ctx* ctx, double now, eqx_step_summary* out);
 
+/* ---- completion / feedback -------------------------------------------
+ * A batch of completed requests, in the engine's completion order (complete_finished,
+ * engine.cpp:327-375): RequestActuals (scheduler.hpp:89-95) plus the PendingContribution the
+ * admission registered (scheduler.hpp:131-138; the event payloads of eqx_copy_events). */
+typedef struct {
+  int64_t n;
+  const int32_t* client;          /* roster index */
+  const int32_t* input_tokens;
+  const int32_t* output_tokens;   /* RequestActuals::output_tokens */
+  const double* latency_s;
+  const double* tps;
+  const double* gpu_util;
+  const double* pending_ufc;
+  const double* pending_rfc;
+  const double* pending_vtc;      /* VTC with predictions only; may be NULL otherwise */
+  int32_t location;               /* EQX_HOST / EQX_DEVICE */
+} eqx_completions;
+
+/* One engine iteration's feedback, in the reference's order: on_tokens for every client with
+ * tokens[c] > 0 (scheduler.cpp:185-190; tokens may be NULL), then for each completion
+ * on_complete (scheduler.cpp:192-233), the running-count decrement (engine.cpp:368) and
+ * update_map with ema_alpha (predictor.cpp:372-383) on the context's profile, which later
+ * drains map against.  done may be NULL. */
+eqx_status eqx_feedback(eqx_ctx* ctx, const int64_t* tokens, const eqx_completions* done, double ema_alpha);
+/* ClientState::accumulated_service per client and SchedulerPolicy::counter_clamps(). */
+eqx_status eqx_get_service(eqx_ctx* ctx, int32_t n, double* service, int64_t* counter_clamps);
+eqx_status eqx_set_service(eqx_ctx* ctx, int32_t n, const double* service);
+/* The profile metrics as update_map left them (GpuProfile entries in roster order). */
+eqx_status eqx_get_profile(eqx_ctx* ctx, int32_t n, double* latency_ms, double* gpu_util, double* tps);
+
 /* ---- client-sharded step over several GPUs ------------------------------
  * The queue shards by client: rank r owns the contiguous client_id-rank block
  * [client_off[r], client_off[r+1]) of the global roster and every queued request of those

@@ -353,3 +353,47 @@ int eqxo_noisy_predict(double l1, uint64_t seed, int64_t id, int true_out) {
   return noisy_predict(l1, seed, id, true_out);
 }
 int eqxo_route(const eqxo_mope* m, int in, int row, int* fallback) { return route(m, in, row, fallback); }
+
+/* ---- completion / feedback (restatement of scheduler.cpp:185-233, predictor.cpp:372-383,
+ *      engine.cpp:287-293 and 327-375) ---- */
+static int entry_for_idx(int n, const int32_t* upper, int out) { /* gpu_model.cpp:74-80 */
+  for (int e = 0; e < n; ++e)
+    if (out <= upper[e]) return e;
+  return n - 1;
+}
+
+int eqxo_feedback_run(eqxo_feedback* f) {
+  if (f->ema_alpha <= 0.0 || f->ema_alpha > 1.0) return 1; /* ConfigError (predictor.cpp:374-376) */
+  const double ow = f->output_weight;
+  f->clamps = 0;
+  /* run_iteration: on_tokens per client in index order (engine.cpp:289-293) */
+  if (f->tokens && f->kind == EQXO_VTC && !f->vtc_use_prediction) {
+    for (int c = 0; c < f->n_clients; ++c)
+      if (f->tokens[c] > 0) f->counter[c] += f->weight[c] * ow * (double)f->tokens[c];
+  }
+  /* complete_finished: completions in order */
+  for (int64_t i = 0; i < f->n_done; ++i) {
+    const int c = f->client[i];
+    const double w = f->weight[c];
+    const double wt = (double)f->in_tokens[i] + ow * (double)f->out_tokens[i];
+    const double actual_ufc = w * wt / (1.0 + f->delta * f->latency_s[i]);
+    const double actual_rfc = w * f->tps[i] * f->util[i];
+    f->ufc[c] += actual_ufc - f->pend_ufc[i];
+    if (f->ufc[c] < 0.0) { f->ufc[c] = 0.0; ++f->clamps; }
+    f->rfc[c] += actual_rfc - f->pend_rfc[i];
+    if (f->rfc[c] < 0.0) { f->rfc[c] = 0.0; ++f->clamps; }
+    if (f->kind == EQXO_VTC && f->vtc_use_prediction) {
+      f->counter[c] += w * wt - f->pend_vtc[i];
+      if (f->counter[c] < 0.0) { f->counter[c] = 0.0; ++f->clamps; }
+    }
+    f->service[c] += w * wt;
+    if (f->running) f->running[c] -= 1;
+    /* update_map with ObservedMetrics{out, latency_s * 1000, util, tps} */
+    const int e = entry_for_idx(f->n_profile, f->prof_upper, f->out_tokens[i]);
+    const double a = f->ema_alpha;
+    f->prof_lat[e] = (1.0 - a) * f->prof_lat[e] + a * (f->latency_s[i] * 1000.0);
+    f->prof_util[e] = (1.0 - a) * f->prof_util[e] + a * f->util[i];
+    f->prof_tps[e] = (1.0 - a) * f->prof_tps[e] + a * f->tps[i];
+  }
+  return 0;
+}

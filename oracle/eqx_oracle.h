@@ -106,6 +106,33 @@ typedef struct {
 /* 0 on success; nonzero + message in err on invalid configuration. */
 int eqxo_step(const eqxo_step_in* in, eqxo_step_out* out, char* err, int err_len);
 
+/* ---- completion / feedback path ------------------------------------
+ * One engine iteration's feedback, in engine order (engine.cpp:273-375): on_tokens for every
+ * client with generated tokens (scheduler.cpp:185-190), then for each completion in order
+ * on_complete (scheduler.cpp:192-233), running_count decrement (engine.cpp:368) and update_map
+ * (predictor.cpp:372-383).  Ledger and profile arrays are updated in place. */
+typedef struct {
+  int32_t kind;
+  double alpha, delta, output_weight;
+  int32_t vtc_use_prediction;
+  int32_t n_clients;
+  const double* weight;
+  double *ufc, *rfc, *counter, *service;  /* ClientState::accumulated_service */
+  int32_t* running;
+  int32_t n_profile;
+  const int32_t* prof_upper;
+  double *prof_lat, *prof_util, *prof_tps;
+  double ema_alpha;
+  const int64_t* tokens;                  /* [n_clients] decode tokens of the iteration */
+  int64_t n_done;
+  const int32_t *client, *in_tokens, *out_tokens;
+  const double *latency_s, *tps, *util;
+  const double *pend_ufc, *pend_rfc, *pend_vtc; /* PendingContribution of each completion */
+  int64_t clamps;                         /* out: counter_clamps() increments */
+} eqxo_feedback;
+
+int eqxo_feedback_run(eqxo_feedback* f);
+
 #ifdef __cplusplus
 }
 #endif

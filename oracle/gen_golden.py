@@ -172,7 +172,42 @@ def main() -> None:
                         arrival=qr["arrival"], in_tokens=qr["in_tokens"], true_out=qr["true_out"],
                         tag=qr["tag"])
     print("replay events", len(ev_id))
+    gen_feedback(prof)
+
+
+def gen_feedback(profile: dict) -> None:
+    """Feedback goldens from the reference objects: the scenario, the
+    pending increments on_admit registered, the ledger after the admissions, and the ledger,
+    accumulated service, clamp count and profile after on_tokens + on_complete + update_map."""
+    cases = {"fb_equinox": dict(seed=1), "fb_vtc_bare": dict(seed=2, kind=1),
+             "fb_vtc_pred": dict(seed=3, kind=1, vtc_use_prediction=1), "fb_fcfs": dict(seed=4, kind=0),
+             "fb_cold_many": dict(seed=5, n_clients=40, n_adm=300, n_done=250, ledger_scale=0.0),
+             "fb_alpha1": dict(seed=6, ema_alpha=1.0)}
+    for name, kw in cases.items():
+        fb = H.feedback_case(profile=profile, **kw)
+        r = H.run_feedback(fb, "ref")
+        flat = {"meta": json.dumps({k: fb[k] for k in ("kind", "alpha", "delta", "output_weight",
+                                                        "vtc_use_prediction", "ema_alpha", "now", "names")})}
+        for k in ("weight", "ufc0", "rfc0", "counter0", "service0", "tokens"):
+            flat["in_" + k] = np.asarray(fb[k])
+        for k, v in fb["profile"].items():
+            flat["prof_" + k] = np.asarray(v)
+        for k, v in fb["adm"].items():
+            flat["adm_" + k] = np.asarray(v)
+        for k, v in fb["done"].items():
+            flat["done_" + k] = np.asarray(v)
+        flat["out_pend"] = r["pend"]
+        flat["out_mid"] = r["mid"]
+        for k in H.FEEDBACK_KEYS:
+            flat["out_" + k] = r[k]
+        flat["out_clamps"] = np.asarray(r["clamps"])
+        np.savez_compressed(os.path.join(GOLDEN, f"{name}.npz"), **flat)
+        print(name, "clamps", r["clamps"])
 
 
 if __name__ == "__main__":
-    main()
+    if "--feedback" in sys.argv:  # only the feedback goldens, with the committed profile
+        with open(os.path.join(DATA, "profile_default.json")) as f:
+            gen_feedback({k: np.asarray(v) for k, v in json.load(f).items()})
+    else:
+        main()

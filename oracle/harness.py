@@ -339,3 +339,128 @@ def ref_replay(case: StepCase, max_sim_time_s=3600.0, ema_alpha=0.2, cap=None):
         raise ValueError(err.value.decode())
     n = min(int(n), cap)
     return ev_id[:n], ev_kind[:n], ev_time[:n], u, r, c
+
+
+# ---- completion / feedback path ---------------------------------------
+class Feedback(C.Structure):
+    _fields_ = [
+        ("kind", C.c_int32), ("alpha", C.c_double), ("delta", C.c_double), ("output_weight", C.c_double),
+        ("vtc_use_prediction", C.c_int32), ("n_clients", C.c_int32), ("weight", _dp),
+        ("ufc", _dp), ("rfc", _dp), ("counter", _dp), ("service", _dp), ("running", _i32p),
+        ("n_profile", C.c_int32), ("prof_upper", _i32p), ("prof_lat", _dp), ("prof_util", _dp),
+        ("prof_tps", _dp), ("ema_alpha", C.c_double), ("tokens", _i64p), ("n_done", C.c_int64),
+        ("client", _i32p), ("in_tokens", _i32p), ("out_tokens", _i32p), ("latency_s", _dp), ("tps", _dp),
+        ("util", _dp), ("pend_ufc", _dp), ("pend_rfc", _dp), ("pend_vtc", _dp), ("clamps", C.c_int64),
+    ]
+
+
+def _feedback_struct(fb: dict, ledger: dict, done_client, pend, keep: list) -> Feedback:
+    def arr(x, dt):
+        a = np.ascontiguousarray(x, dt)
+        keep.append(a)
+        return a
+    f = Feedback()
+    f.kind, f.alpha, f.delta, f.output_weight = fb["kind"], fb["alpha"], fb["delta"], fb["output_weight"]
+    f.vtc_use_prediction = int(fb["vtc_use_prediction"])
+    f.n_clients = len(fb["weight"])
+    f.weight = _ptr(arr(fb["weight"], np.float64), C.c_double)
+    for k in ("ufc", "rfc", "counter", "service"):
+        setattr(f, k, _ptr(ledger[k], C.c_double))
+    f.running = _ptr(ledger["running"], C.c_int32)
+    prof = fb["profile"]
+    f.n_profile = len(prof["upper"])
+    f.prof_upper = _ptr(arr(prof["upper"], np.int32), C.c_int32)
+    for k, src in (("prof_lat", "lat"), ("prof_util", "util"), ("prof_tps", "tps")):
+        setattr(f, k, _ptr(ledger[k], C.c_double))
+    f.ema_alpha = fb["ema_alpha"]
+    f.tokens = _ptr(arr(fb["tokens"], np.int64), C.c_int64)
+    d = fb["done"]
+    f.n_done = len(d["adm"])
+    f.client = _ptr(arr(done_client, np.int32), C.c_int32)
+    f.in_tokens = _ptr(arr(np.asarray(fb["adm"]["in"])[np.asarray(d["adm"], np.int64)], np.int32), C.c_int32)
+    f.out_tokens = _ptr(arr(d["out"], np.int32), C.c_int32)
+    f.latency_s = _ptr(arr(d["latency_s"], np.float64), C.c_double)
+    f.tps = _ptr(arr(d["tps"], np.float64), C.c_double)
+    f.util = _ptr(arr(d["util"], np.float64), C.c_double)
+    f.pend_ufc = _ptr(arr(pend[0], np.float64), C.c_double)
+    f.pend_rfc = _ptr(arr(pend[1], np.float64), C.c_double)
+    f.pend_vtc = _ptr(arr(pend[2], np.float64), C.c_double)
+    return f
+
+
+def run_feedback(fb: dict, which: str = "ref", pend=None, mid=None) -> dict:
+    """One iteration's feedback (on_admit registrations, on_tokens, on_complete + update_map).
+
+    ``ref``: through the reference objects (admissions included); returns the registered
+    pending increments and the ledger after the admissions too.  ``oracle``: the C restatement,
+    starting from ``mid`` (ledger after admissions) with the given ``pend`` increments."""
+    keep: list = []
+    nc = len(fb["weight"])
+    done_adm = np.asarray(fb["done"]["adm"], np.int64)
+    adm_client = np.asarray(fb["adm"]["client"], np.int32)
+    done_client = adm_client[done_adm] if len(done_adm) else np.zeros(0, np.int32)
+    led = {k: np.array(fb[k + "0"], np.float64) for k in ("ufc", "rfc", "counter", "service")}
+    led["running"] = np.array(fb.get("running0", np.zeros(nc)), np.int32)
+    for k, src in (("prof_lat", "lat"), ("prof_util", "util"), ("prof_tps", "tps")):
+        led[k] = np.array(fb["profile"][src], np.float64)
+    n_adm = len(adm_client)
+    if which == "ref":
+        pend_out = np.zeros(3 * max(n_adm, 1))
+        mid_out = np.zeros(3 * max(nc, 1))
+        pend_in = pend_out.reshape(3, -1)[:, done_adm] if n_adm else np.zeros((3, 0))
+        f = _feedback_struct(fb, led, done_client, np.zeros((3, len(done_adm))), keep)
+        lib = C.CDLL(LIB_REF)
+        fn = lib.ref_feedback
+        fn.restype = C.c_int
+        names = b"".join(n.encode() + b"\0" for n in fb["names"])
+        a = {k: np.ascontiguousarray(fb["adm"][k], dt) for k, dt in
+             (("id", np.int64), ("client", np.int32), ("in", np.int32), ("pred", np.int32), ("wait", np.float64))}
+        err = C.create_string_buffer(512)
+        rc = fn(C.byref(f), C.c_char_p(names), C.c_double(fb["now"]), C.c_int64(n_adm),
+                _ptr(a["id"], C.c_int64), _ptr(a["client"], C.c_int32), _ptr(a["in"], C.c_int32), _ptr(a["pred"], C.c_int32),
+                _ptr(a["wait"], C.c_double), _ptr(np.ascontiguousarray(done_adm.astype(np.int32)), C.c_int32),
+                _ptr(pend_out, C.c_double), _ptr(mid_out, C.c_double), err, 512)
+        if rc:
+            raise RuntimeError(err.value.decode())
+        pend = pend_out[:3 * n_adm].reshape(3, n_adm) if n_adm else np.zeros((3, 0))
+        mid = mid_out[:3 * nc].reshape(3, nc)
+        del pend_in
+    else:
+        for i, k in enumerate(("ufc", "rfc", "counter")):
+            led[k][:] = mid[i]
+        f = _feedback_struct(fb, led, done_client, np.asarray(pend)[:, done_adm], keep)
+        lib = _lib("oracle")[0]
+        lib.eqxo_feedback_run.restype = C.c_int
+        if lib.eqxo_feedback_run(C.byref(f)):
+            raise ValueError("ema_alpha must lie in (0, 1]")
+    out = {k: led[k].copy() for k in ("ufc", "rfc", "counter", "service", "running", "prof_lat", "prof_util",
+                                        "prof_tps")}
+    out["clamps"] = int(f.clamps)
+    out["pend"] = pend
+    out["mid"] = mid
+    return out
+
+
+def feedback_case(seed: int, kind: int = 2, vtc_use_prediction: int = 0, n_clients: int = 5, n_adm: int = 12,
+                  n_done: int = 8, ledger_scale: float = 1.0, ema_alpha: float = 0.2, profile: dict | None = None,
+                  weights=None) -> dict:
+    """A seeded feedback scenario: n_adm admissions (registered through on_admit), one
+    iteration's decode tokens, and n_done of the admitted requests completing in a random order."""
+    rng = np.random.default_rng(seed)
+    C = n_clients
+    w = np.asarray(weights, np.float64) if weights is not None else rng.choice([0.5, 1.0, 2.0], C)
+    return dict(kind=kind, alpha=0.7, delta=0.1, output_weight=4.0, vtc_use_prediction=vtc_use_prediction,
+                names=[f"client{i}" for i in range(C)], weight=w,
+                ufc0=rng.uniform(0, 1e4, C) * ledger_scale, rfc0=rng.uniform(0, 1e3, C) * ledger_scale,
+                counter0=rng.uniform(0, 1e4, C) * ledger_scale, service0=rng.uniform(0, 1e5, C) * ledger_scale,
+                profile={k: np.asarray(v) for k, v in profile.items()}, ema_alpha=ema_alpha, now=3.0,
+                adm={"id": np.arange(100, 100 + n_adm, dtype=np.int64), "client": rng.integers(0, C, n_adm),
+                     "in": rng.integers(8, 1000, n_adm), "pred": rng.integers(1, 1500, n_adm),
+                     "wait": rng.uniform(0, 2, n_adm)},
+                tokens=rng.integers(0, 5, C),
+                done={"adm": rng.permutation(n_adm)[:n_done], "out": rng.integers(1, 5000, n_done),
+                      "latency_s": rng.uniform(0.1, 30, n_done), "tps": rng.uniform(10, 5000, n_done),
+                      "util": rng.uniform(0.2, 1, n_done)})
+
+
+FEEDBACK_KEYS = ("ufc", "rfc", "counter", "service", "running", "prof_lat", "prof_util", "prof_tps")

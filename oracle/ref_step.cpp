@@ -455,3 +455,96 @@ int64_t ref_replay(const eqxo_step_in* in, double max_sim_time_s, double ema_alp
 }
 
 }  // extern "C"
+
+// ref_feedback -- the completion / feedback path through the reference objects: every
+// admission registers its PendingContribution with SchedulerPolicy::on_admit (the prediction
+// record from map_metrics against the profile), then one iteration's on_tokens in client order
+// (engine.cpp:289-293), then for each completion in order SchedulerPolicy::on_complete and
+// update_map (engine.cpp:327-375).  `f` carries the pre-admission ledger and profile in and the
+// final state out; pend_out[3][n_adm] = the registered pending (ufc, rfc, vtc) increments and
+// mid_out[3][C] = the ledger (ufc, rfc, counter) after the admissions.
+extern "C" int ref_feedback(eqxo_feedback* f, const char* client_names, double now, int64_t n_adm,
+                            const int64_t* adm_id, const int32_t* adm_client, const int32_t* adm_in,
+                            const int32_t* adm_pred, const double* adm_wait, const int32_t* done_adm,
+                            double* pend_out, double* mid_out, char* err, int err_len) {
+  try {
+    const auto names = split_names(client_names, f->n_clients);
+    PolicySpec spec;
+    spec.kind = static_cast<PolicyKind>(f->kind);
+    spec.equinox.alpha = f->alpha;
+    spec.equinox.delta = f->delta;
+    spec.equinox.output_weight = f->output_weight;
+    spec.vtc_use_prediction = f->vtc_use_prediction != 0;
+    std::vector<ClientState> roster(static_cast<std::size_t>(f->n_clients));
+    for (int c = 0; c < f->n_clients; ++c) {
+      roster[c].client_id = names[c];
+      roster[c].weight = f->weight[c];
+      roster[c].ufc = f->ufc[c];
+      roster[c].rfc = f->rfc[c];
+      roster[c].counter = f->counter[c];
+      roster[c].accumulated_service = f->service[c];
+    }
+    SchedulerPolicy policy(spec, roster);
+    GpuProfile profile;
+    for (int e = 0; e < f->n_profile; ++e)
+      profile.entries.push_back({f->prof_upper[e], f->prof_lat[e], f->prof_util[e], f->prof_tps[e]});
+    std::vector<Request> reqs(static_cast<std::size_t>(n_adm));
+    for (int64_t a = 0; a < n_adm; ++a) {
+      Request& r = reqs[static_cast<std::size_t>(a)];
+      r.id = adm_id[a];
+      r.client_id = names[adm_client[a]];
+      r.input_tokens = adm_in[a];
+      ScheduleContext ctx;
+      ctx.now_s = now;
+      ctx.wait_s = adm_wait[a];
+      ctx.prediction = map_metrics(adm_pred[a], profile);
+      const ClientState before = policy.clients()[static_cast<std::size_t>(adm_client[a])];
+      policy.on_admit(static_cast<std::size_t>(adm_client[a]), r, ctx);
+      const ClientState& after = policy.clients()[static_cast<std::size_t>(adm_client[a])];
+      pend_out[a] = ufc_increment(r, ctx, before.weight, spec.equinox);
+      pend_out[n_adm + a] = rfc_increment(ctx.prediction, before.weight);
+      pend_out[2 * n_adm + a] = after.counter - before.counter;  // vtc_inc (0 unless VTC)
+    }
+    for (int c = 0; c < f->n_clients; ++c) {
+      const ClientState& s = policy.clients()[static_cast<std::size_t>(c)];
+      mid_out[c] = s.ufc;
+      mid_out[f->n_clients + c] = s.rfc;
+      mid_out[2 * f->n_clients + c] = s.counter;
+    }
+    if (f->tokens)
+      for (int c = 0; c < f->n_clients; ++c)
+        if (f->tokens[c] > 0) policy.on_tokens(static_cast<std::size_t>(c), f->tokens[c]);
+    for (int64_t i = 0; i < f->n_done; ++i) {
+      const int64_t a = done_adm[i];
+      RequestActuals act;
+      act.output_tokens = f->out_tokens[i];
+      act.latency_s = f->latency_s[i];
+      act.tps = f->tps[i];
+      act.gpu_util = f->util[i];
+      policy.on_complete(static_cast<std::size_t>(adm_client[a]), reqs[static_cast<std::size_t>(a)], act);
+      ObservedMetrics obs;
+      obs.output_tokens = act.output_tokens;
+      obs.latency_ms = act.latency_s * 1000.0;
+      obs.gpu_util = act.gpu_util;
+      obs.tps = act.tps;
+      update_map(profile, obs, f->ema_alpha);
+    }
+    for (int c = 0; c < f->n_clients; ++c) {
+      const ClientState& s = policy.clients()[static_cast<std::size_t>(c)];
+      f->ufc[c] = s.ufc;
+      f->rfc[c] = s.rfc;
+      f->counter[c] = s.counter;
+      f->service[c] = s.accumulated_service;
+    }
+    for (int e = 0; e < f->n_profile; ++e) {
+      f->prof_lat[e] = profile.entries[static_cast<std::size_t>(e)].latency_ms;
+      f->prof_util[e] = profile.entries[static_cast<std::size_t>(e)].gpu_util;
+      f->prof_tps[e] = profile.entries[static_cast<std::size_t>(e)].tps;
+    }
+    f->clamps = policy.counter_clamps();
+    return 0;
+  } catch (const std::exception& e) {
+    set_err(err, err_len, e.what());
+    return 1;
+  }
+}

@@ -62,6 +62,13 @@ class StepSummary(C.Structure):
                 ("window_underflow", C.c_int32)]
 
 
+class Completions(C.Structure):
+    _fields_ = [("n", C.c_int64), ("client", C.c_void_p), ("input_tokens", C.c_void_p),
+                ("output_tokens", C.c_void_p), ("latency_s", C.c_void_p), ("tps", C.c_void_p),
+                ("gpu_util", C.c_void_p), ("pending_ufc", C.c_void_p), ("pending_rfc", C.c_void_p),
+                ("pending_vtc", C.c_void_p), ("location", C.c_int32)]
+
+
 _SIGS = {
     "eqx_abi_version": ([], C.c_int32),
     "eqx_ctx_create": ([C.c_int32, C.POINTER(C.c_void_p)], C.c_int),
@@ -73,6 +80,10 @@ _SIGS = {
     "eqx_shard_export_async": ([C.c_void_p, C.c_double, C.c_int32, C.c_int32, C.c_void_p], C.c_int),
     "eqx_shard_select_async": ([C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, _i32p, C.c_int32, C.c_int32,
                                 C.c_double], C.c_int),
+    "eqx_feedback": ([C.c_void_p, _i64p, C.POINTER(Completions), C.c_double], C.c_int),
+    "eqx_get_service": ([C.c_void_p, C.c_int32, _dp, _i64p], C.c_int),
+    "eqx_set_service": ([C.c_void_p, C.c_int32, _dp], C.c_int),
+    "eqx_get_profile": ([C.c_void_p, C.c_int32, _dp, _dp, _dp], C.c_int),
     "eqx_set_policy": ([C.c_void_p, C.POINTER(Policy)], C.c_int),
     "eqx_set_perf": ([C.c_void_p, C.POINTER(Perf)], C.c_int),
     "eqx_set_profile": ([C.c_void_p, C.POINTER(Profile)], C.c_int),

@@ -135,6 +135,8 @@ struct eqx_ctx {
   int occ_per_sm = 1;
   // client-sharded step (selection context): gathered windows and their ids
   DevBuf d_first64, d_gid;
+  DevBuf d_service;                // ClientState::accumulated_service
+  DevBuf d_fb;                     // staged completion batch / token counts
   int32_t shard_W = 0;             // > 0: the last step was a sharded selection
 };
 
@@ -403,6 +405,8 @@ void eqx_ctx_destroy(eqx_ctx* ctx) {
   if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
   ctx->d_first64.release();
   ctx->d_gid.release();
+  ctx->d_service.release();
+  ctx->d_fb.release();
   if (ctx->stream && ctx->owns_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -585,7 +589,9 @@ eqx_status eqx_set_clients(eqx_ctx* ctx, int32_t n, const char* names, const dou
   CUDA_TRY(ctx, ctx->d_first.ensure(d4));
   CUDA_TRY(ctx, ctx->d_qlen_before.ensure(d4));
   CUDA_TRY(ctx, ctx->d_seg_off.ensure(4ull * (n + 1)));
+  CUDA_TRY(ctx, ctx->d_service.ensure(d8));
   cudaStream_t s = ctx->stream;
+  CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_service.p, 0, d8, s));
   if (n > 0) {
     CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_ufc.p, ufc ? ufc : zeros.data(), 8ull * n, cudaMemcpyHostToDevice, s));
     CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_rfc.p, rfc ? rfc : zeros.data(), 8ull * n, cudaMemcpyHostToDevice, s));
@@ -1323,6 +1329,136 @@ eqx_status eqx_drain_step_async(eqx_ctx* ctx, const eqx_requests* r, double now)
   ctx->step_pending = true;
   ctx->stepped = true;
   return EQX_OK;
+}
+
+// ---- completion / feedback ------------------------------------------
+eqx_status eqx_feedback(eqx_ctx* ctx, const int64_t* tokens, const eqx_completions* done, double ema_alpha) {
+  if (!ctx) return fail(ctx, EQX_ERR_ARG, "eqx_feedback: NULL context");
+  if (!ctx->policy_set || !ctx->profile_set) return fail(ctx, EQX_ERR_CONFIG, "eqx_feedback: policy and profile must be set first");
+  const int64_t n = done ? done->n : 0;
+  if (n < 0) return fail(ctx, EQX_ERR_ARG, "eqx_feedback: negative completion count");
+  if (n > 0 && (ema_alpha <= 0.0 || ema_alpha > 1.0))
+    return fail(ctx, EQX_ERR_CONFIG, "ema_alpha must lie in (0, 1]");  // predictor.cpp:374-376
+  if (n > 0 && (!done->client || !done->input_tokens || !done->output_tokens || !done->latency_s || !done->tps ||
+                !done->gpu_util || !done->pending_ufc || !done->pending_rfc))
+    return fail(ctx, EQX_ERR_ARG, "eqx_feedback: missing completion column");
+  const int32_t C = ctx->C;
+  if (n > 0 && done->location == EQX_HOST)
+    for (int64_t i = 0; i < n; ++i)
+      if (done->client[i] < 0 || done->client[i] >= C)
+        return fail(ctx, EQX_ERR_ENGINE, "completion for unknown client index " + std::to_string(done->client[i]));
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = ctx->stream;
+  FeedbackArgs f;
+  std::memset(&f, 0, sizeof(f));
+  f.n = n;
+  // host columns: one staging block [tokens C][client, in, out n][latency, tps, util, pending x3 n]
+  const size_t nn = static_cast<size_t>(n);
+  const size_t need = 8ull * C + 12 * nn + 48 * nn + 64;
+  CUDA_TRY(ctx, ctx->d_fb.ensure(need));
+  char* base = static_cast<char*>(ctx->d_fb.p);
+  if (tokens) {
+    CUDA_TRY(ctx, cudaMemcpyAsync(base, tokens, 8ull * C, cudaMemcpyHostToDevice, s));
+    f.tokens = reinterpret_cast<const int64_t*>(base);
+  }
+  if (n > 0) {
+    if (done->location == EQX_DEVICE) {
+      f.client = done->client;
+      f.in_tok = done->input_tokens;
+      f.out_tok = done->output_tokens;
+      f.latency_s = done->latency_s;
+      f.tps = done->tps;
+      f.util = done->gpu_util;
+      f.pend_ufc = done->pending_ufc;
+      f.pend_rfc = done->pending_rfc;
+      f.pend_vtc = done->pending_vtc;
+    } else {
+      char* p = base + ((8ull * C + 15) & ~size_t(15));
+      auto put = [&](const void* src, size_t bytes) -> const void* {
+        if (!src) return nullptr;
+        char* d = p;
+        p += (bytes + 15) & ~size_t(15);
+        return cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, s) == cudaSuccess ? d : nullptr;
+      };
+      f.client = static_cast<const int32_t*>(put(done->client, 4 * nn));
+      f.in_tok = static_cast<const int32_t*>(put(done->input_tokens, 4 * nn));
+      f.out_tok = static_cast<const int32_t*>(put(done->output_tokens, 4 * nn));
+      f.latency_s = static_cast<const double*>(put(done->latency_s, 8 * nn));
+      f.tps = static_cast<const double*>(put(done->tps, 8 * nn));
+      f.util = static_cast<const double*>(put(done->gpu_util, 8 * nn));
+      f.pend_ufc = static_cast<const double*>(put(done->pending_ufc, 8 * nn));
+      f.pend_rfc = static_cast<const double*>(put(done->pending_rfc, 8 * nn));
+      f.pend_vtc = static_cast<const double*>(put(done->pending_vtc, 8 * nn));
+      if (!f.client || !f.in_tok || !f.out_tok || !f.latency_s || !f.tps || !f.util || !f.pend_ufc || !f.pend_rfc)
+        return fail(ctx, EQX_ERR_CUDA, "eqx_feedback: completion upload failed");
+    }
+    if (!f.pend_vtc) {  // only VTC with predictions reads it
+      if (ctx->pol.kind == kVtc && ctx->pol.vtc_use_prediction)
+        return fail(ctx, EQX_ERR_ARG, "eqx_feedback: pending_vtc is required for vtc+pred");
+      f.pend_vtc = f.pend_ufc;
+    }
+  }
+  f.C = C;
+  f.ema_alpha = n > 0 ? ema_alpha : 0.0;
+  f.weight = ctx->d_weight.as<double>();
+  f.ufc = ctx->d_ufc.as<double>();
+  f.rfc = ctx->d_rfc.as<double>();
+  f.counter = ctx->d_counter.as<double>();
+  f.service = ctx->d_service.as<double>();
+  f.running = ctx->d_running.as<int32_t>();
+  f.model = ctx->d_model.as<ModelTables>();
+  f.st = ctx->d_state.as<DevState>();
+  f.pol = ctx->pol;
+  if (ctx->model_dirty) {  // the device profile must exist before update_map edits it
+    StepPlan pl;
+    const bool qr = ctx->queue_ready;
+    ctx->queue_ready = true;  // step_prepare only uploads the tables here
+    const int64_t n0 = ctx->n;
+    eqx_status st = step_prepare(ctx, 0.0, pl);
+    ctx->queue_ready = qr;
+    ctx->n = n0;
+    if (st != EQX_OK) return st;
+  }
+  if (C > 0 || n > 0) feedback_kernel<<<1, 1024, 0, s>>>(f);
+  CUDA_TRY(ctx, cudaGetLastError());
+  CUDA_TRY(ctx, cudaStreamSynchronize(s));  // host columns may go away
+  return EQX_OK;
+}
+
+eqx_status eqx_get_service(eqx_ctx* ctx, int32_t n, double* service, int64_t* counter_clamps) {
+  if (!ctx || n != ctx->C) return fail(ctx, EQX_ERR_ARG, "eqx_get_service: roster size mismatch");
+  cudaSetDevice(ctx->device);
+  const Col cols[] = {{service, ctx->d_service.p, 8ull * n},
+                      {counter_clamps, reinterpret_cast<char*>(ctx->d_state.p) + offsetof(DevState, clamps), 8}};
+  return read_cols(ctx, cols, 2);
+}
+
+eqx_status eqx_set_service(eqx_ctx* ctx, int32_t n, const double* service) {
+  if (!ctx || n != ctx->C || (n > 0 && !service)) return fail(ctx, EQX_ERR_ARG, "eqx_set_service: roster size mismatch");
+  cudaSetDevice(ctx->device);
+  if (n > 0) CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_service.p, service, 8ull * n, cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return EQX_OK;
+}
+
+eqx_status eqx_get_profile(eqx_ctx* ctx, int32_t n, double* latency_ms, double* gpu_util, double* tps) {
+  if (!ctx || !ctx->profile_set || n != ctx->model.n_prof)
+    return fail(ctx, EQX_ERR_ARG, "eqx_get_profile: profile size mismatch");
+  cudaSetDevice(ctx->device);
+  if (ctx->model_dirty) {  // not uploaded yet: the host copy is current
+    for (int e = 0; e < n; ++e) {
+      if (latency_ms) latency_ms[e] = ctx->model.prof_lat[e];
+      if (gpu_util) gpu_util[e] = ctx->model.prof_util[e];
+      if (tps) tps[e] = ctx->model.prof_tps[e];
+    }
+    return EQX_OK;
+  }
+  char* m = static_cast<char*>(ctx->d_model.p);
+  const size_t b = 8ull * n;
+  const Col cols[] = {{latency_ms, m + offsetof(ModelTables, prof_lat), b},
+                      {gpu_util, m + offsetof(ModelTables, prof_util), b},
+                      {tps, m + offsetof(ModelTables, prof_tps), b}};
+  return read_cols(ctx, cols, 3);
 }
 
 // ---- client-sharded step ---------------------------------------------------

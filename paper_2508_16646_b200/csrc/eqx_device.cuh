@@ -68,6 +68,7 @@ struct DevState {
   // EQX_PROF builds: drain timeline (%globaltimer ns): hist start (min) / walk end (max) /
   // epilogue end, rank start (min) / walk end (max) / epilogue end
   unsigned long long dt[8];
+  int64_t clamps;          // SchedulerPolicy::counter_clamps() (on_complete clamps at 0)
 };
 
 // Order-preserving map double -> uint64 (IEEE total order on non-NaN values, with -0.0 and

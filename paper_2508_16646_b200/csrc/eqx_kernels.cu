@@ -2584,6 +2584,93 @@ __global__ void gather_ids_kernel(const int32_t* __restrict__ rows, int64_t n, c
   }
 }
 
+// ============================== completion / feedback =====================================
+// One engine iteration's feedback (engine.cpp:273-375) in the reference's order: on_tokens for
+// every client with decode tokens (scheduler.cpp:185-190), then each completion in order:
+// on_complete (scheduler.cpp:192-233: actual minus pending increments, clamped at 0), the
+// running-count decrement (engine.cpp:368) and update_map's EMA of the profile entry of the
+// observed output length (predictor.cpp:372-383).  Per-client and per-entry chains are
+// sequential in completion order (the FP64 rounding and clamps depend on it); different
+// clients / entries are independent, so one thread owns each.
+__global__ void __launch_bounds__(1024) feedback_kernel(const FeedbackArgs a) {
+  const Policy& P = a.pol;
+  const int tid = threadIdx.x;
+  __shared__ unsigned long long s_clamps;
+  if (tid == 0) s_clamps = 0;
+  __syncthreads();
+  unsigned long long clamps = 0;
+  for (int32_t c = tid; c < a.C; c += blockDim.x) {
+    const double w = a.weight[c];
+    double k = a.counter[c];
+    if (a.tokens && P.kind == kVtc && !P.vtc_use_prediction && a.tokens[c] > 0)  // on_tokens
+      k = __dadd_rn(k, __dmul_rn(__dmul_rn(w, P.ow), static_cast<double>(a.tokens[c])));
+    double u = a.ufc[c], r = a.rfc[c], sv = a.service[c];
+    int32_t run = a.running[c];
+    for (int64_t i = 0; i < a.n; ++i) {
+      if (a.client[i] != c) continue;
+      const double wt = __dadd_rn(static_cast<double>(a.in_tok[i]), __dmul_rn(P.ow, static_cast<double>(a.out_tok[i])));
+      const double wwt = __dmul_rn(w, wt);
+      const double au = __ddiv_rn(wwt, __dadd_rn(1.0, __dmul_rn(P.delta, a.latency_s[i])));
+      const double ar = __dmul_rn(__dmul_rn(w, a.tps[i]), a.util[i]);
+      u = __dadd_rn(u, __dsub_rn(au, a.pend_ufc[i]));
+      if (u < 0.0) {
+        u = 0.0;
+        ++clamps;
+      }
+      r = __dadd_rn(r, __dsub_rn(ar, a.pend_rfc[i]));
+      if (r < 0.0) {
+        r = 0.0;
+        ++clamps;
+      }
+      if (P.kind == kVtc && P.vtc_use_prediction) {
+        k = __dadd_rn(k, __dsub_rn(wwt, a.pend_vtc[i]));
+        if (k < 0.0) {
+          k = 0.0;
+          ++clamps;
+        }
+      }
+      sv = __dadd_rn(sv, wwt);
+      --run;
+    }
+    a.ufc[c] = u;
+    a.rfc[c] = r;
+    a.counter[c] = k;
+    a.service[c] = sv;
+    a.running[c] = run;
+  }
+  if (clamps) atomicAdd(&s_clamps, clamps);
+  // update_map: lane e of warp 1 owns profile entry e
+  if (a.ema_alpha > 0.0 && (tid >> 5) == (blockDim.x > 32 ? 1 : 0)) {
+    const int e = tid & 31;
+    ModelTables* M = a.model;
+    const int np = M->n_prof;
+    if (e < np) {
+      double lat = M->prof_lat[e], ut = M->prof_util[e], tp = M->prof_tps[e];
+      const double al = a.ema_alpha, bl = __dsub_rn(1.0, a.ema_alpha);
+      bool hit = false;
+      for (int64_t i = 0; i < a.n; ++i) {
+        const int32_t out = a.out_tok[i];
+        int b = np - 1;  // entry_for (gpu_model.cpp:74-80): first entry with out <= upper
+        for (int x = np - 1; x >= 0; --x)
+          if (out <= M->prof_upper[x]) b = x;
+        if (b != e) continue;
+        hit = true;
+        lat = __dadd_rn(__dmul_rn(bl, lat), __dmul_rn(al, __dmul_rn(a.latency_s[i], 1000.0)));
+        ut = __dadd_rn(__dmul_rn(bl, ut), __dmul_rn(al, a.util[i]));
+        tp = __dadd_rn(__dmul_rn(bl, tp), __dmul_rn(al, a.tps[i]));
+      }
+      if (hit) {
+        M->prof_lat[e] = lat;
+        M->prof_util[e] = ut;
+        M->prof_tps[e] = tp;
+        M->prof_pred_s[e] = __ddiv_rn(lat, 1000.0);  // scheduler.cpp:23 reads latency_ms / 1000
+      }
+    }
+  }
+  __syncthreads();
+  if (tid == 0 && s_clamps) a.st->clamps += static_cast<int64_t>(s_clamps);
+}
+
 // ================================ client-sharded step =====================================
 // the queue shards by client over ranks; every rank scores its own queue and
 // exports its clients' head windows (shard_export_kernel), the records are all-gathered

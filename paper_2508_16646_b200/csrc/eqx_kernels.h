@@ -246,6 +246,33 @@ __global__ void shard_ingest_kernel(ShardMap m, ShardSelectBufs b);
 __global__ void shard_unpack_kernel(ShardMap m, ShardSelectBufs b);
 __global__ void shard_event_fill_kernel(EventFillArgs a, const WinEntry* win);
 
+// ---- completion / feedback ------------------------------------------
+struct FeedbackArgs {
+  int64_t n;               // completions, in engine order (complete_finished)
+  const int32_t* client;
+  const int32_t* in_tok;
+  const int32_t* out_tok;
+  const double* latency_s;
+  const double* tps;
+  const double* util;
+  const double* pend_ufc;
+  const double* pend_rfc;
+  const double* pend_vtc;
+  const int64_t* tokens;   // [C] on_tokens of one iteration (nullptr: none)
+  int32_t C;
+  double ema_alpha;        // update_map; <= 0: skip
+  const double* weight;
+  double* ufc;
+  double* rfc;
+  double* counter;
+  double* service;         // ClientState::accumulated_service
+  int32_t* running;
+  ModelTables* model;      // the device copy: update_map edits its profile metrics
+  DevState* st;
+  Policy pol;
+};
+__global__ void feedback_kernel(FeedbackArgs a);
+
 __global__ void drain_hist_kernel(DrainArgs a);
 __global__ void lift_kernel(DrainArgs a);
 __global__ void event_fill_kernel(EventFillArgs a);

@@ -307,6 +307,7 @@ class GpuScheduler:
         lat = np.array([x.latency_ms for x in e], np.float64)
         ut = np.array([x.gpu_util for x in e], np.float64)
         tp = np.array([x.tps for x in e], np.float64)
+        self._n_profile = len(e)
         pr = L.Profile(len(e), up.ctypes.data_as(L._i32p), lat.ctypes.data_as(L._dp),
                        ut.ctypes.data_as(L._dp), tp.ctypes.data_as(L._dp))
         self._check(self._lib.eqx_set_profile(self._ctx, C.byref(pr)))
@@ -473,6 +474,62 @@ class GpuScheduler:
                           int(s.new_prefill_tokens), int(s.length_fallbacks), int(s.noisy_near_ties),
                           int(s.batch_members), int(s.batch_reserved_kv_tokens), int(s.queued),
                           int(s.window_underflow))
+
+    # -- completion / feedback (engine.cpp:273-375) --
+    def feedback(self, tokens=None, completions: dict | None = None, ema_alpha: float = 0.2) -> None:
+        """One iteration's feedback in the engine's order: on_tokens(c, tokens[c]) for every
+        client with tokens, then per completion (in order) on_complete + running-count
+        decrement + update_map(profile, observed, ema_alpha).  ``completions`` holds columns
+        client, input_tokens, output_tokens, latency_s, tps, gpu_util, pending_ufc, pending_rfc
+        and (VTC with predictions) pending_vtc: the admission's PendingContribution, i.e. the
+        StepResult fields ufc_inc / rfc_inc / vtc_inc of its event."""
+        keep: list = []
+        tok = None
+        if tokens is not None:
+            t = np.ascontiguousarray(tokens, np.int64)
+            if t.shape != (len(self.client_ids),):
+                raise ValueError("tokens must hold one count per client")
+            keep.append(t)
+            tok = t.ctypes.data_as(L._i64p)
+        cp = None
+        if completions is not None:
+            cols = {}
+            loc = set()
+            n = len(completions["client"])
+            for name, dt in (("client", np.int32), ("input_tokens", np.int32), ("output_tokens", np.int32),
+                             ("latency_s", np.float64), ("tps", np.float64), ("gpu_util", np.float64),
+                             ("pending_ufc", np.float64), ("pending_rfc", np.float64), ("pending_vtc", np.float64)):
+                ptr, where = _as_col(completions.get(name), dt, keep)
+                cols[name] = ptr
+                if where is not None:
+                    loc.add(where)
+            if len(loc) > 1:
+                raise ValueError("feedback: mix of host and device columns")
+            cp = L.Completions(n, cols["client"], cols["input_tokens"], cols["output_tokens"], cols["latency_s"],
+                               cols["tps"], cols["gpu_util"], cols["pending_ufc"], cols["pending_rfc"],
+                               cols["pending_vtc"], loc.pop() if loc else L.EQX_HOST)
+        self._check(self._lib.eqx_feedback(self._ctx, tok, C.byref(cp) if cp is not None else None,
+                                           float(ema_alpha)))
+
+    def service(self) -> tuple:
+        """(ClientState::accumulated_service per client, SchedulerPolicy::counter_clamps())."""
+        n = len(self.client_ids)
+        out = np.zeros(n)
+        cl = np.zeros(1, np.int64)
+        self._check(self._lib.eqx_get_service(self._ctx, n, out.ctypes.data_as(L._dp), cl.ctypes.data_as(L._i64p)))
+        return out, int(cl[0])
+
+    def set_service(self, service) -> None:
+        sv = np.ascontiguousarray(service, np.float64)
+        self._check(self._lib.eqx_set_service(self._ctx, len(self.client_ids), sv.ctypes.data_as(L._dp)))
+
+    def profile_metrics(self) -> dict:
+        """The profile entries' latency_ms / gpu_util / tps as update_map left them."""
+        n = self._n_profile
+        out = {k: np.zeros(n) for k in ("lat", "util", "tps")}
+        self._check(self._lib.eqx_get_profile(self._ctx, n, out["lat"].ctypes.data_as(L._dp),
+                                              out["util"].ctypes.data_as(L._dp), out["tps"].ctypes.data_as(L._dp)))
+        return out
 
     # -- client-sharded step (include/eqx.h; driven by sharded.ShardedScheduler) --
     def set_stream(self, stream_ptr: int) -> None:
