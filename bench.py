@@ -393,8 +393,8 @@ def run_ours(args, rank, world):
             if i + 1 < steps:
                 sch.stage_async(**hosts[(i + 1) % 2])
             sch.restore_async()
-            sch.drain(**hosts[i % 2])
-            r = sch.step(1.0, with_events=True)
+            sch.drain_step_async(1.0, **hosts[i % 2])  # staged batch -> one graph launch
+            r = sch.collect(with_events=True)
             led_out = sch.ledger()
             adm.append(r.n_admitted)
             d2h = r.ids.nbytes + r.kinds.nbytes + r.clients.nbytes + r.preds.nbytes + 4 * r.ufc_inc.nbytes + \
@@ -416,8 +416,8 @@ def run_ours(args, rank, world):
             sch.restore_async()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            sch.drain(**hosts[0])
-            sch.step(1.0, with_events=True)
+            sch.drain_step_async(1.0, **hosts[0])
+            sch.collect(with_events=True)
             sch.ledger()
             single.append(time.perf_counter() - t0)
         single_ms = float(np.median(single) * 1e3)

@@ -142,6 +142,8 @@ void eqx_ctx_destroy(eqx_ctx* ctx);
 const char* eqx_last_error(const eqx_ctx* ctx);
 /* The cudaStream_t the context launches on (as void*), for event timing by the caller. */
 void* eqx_ctx_stream(eqx_ctx* ctx);
+/* The stream host batches are staged on (eqx_stage_async), for timing by the caller. */
+void* eqx_ctx_copy_stream(eqx_ctx* ctx);
 /* Launch on the caller's cudaStream_t from now on (e.g. the stream a torch.distributed / NCCL
  * collective runs on), so contexts and collectives order without host synchronisation.  The
  * context no longer owns (or destroys) a stream. */

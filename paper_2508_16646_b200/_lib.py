@@ -75,6 +75,7 @@ _SIGS = {
     "eqx_ctx_destroy": ([C.c_void_p], None),
     "eqx_last_error": ([C.c_void_p], C.c_char_p),
     "eqx_ctx_stream": ([C.c_void_p], C.c_void_p),
+    "eqx_ctx_copy_stream": ([C.c_void_p], C.c_void_p),
     "eqx_ctx_set_stream": ([C.c_void_p, C.c_void_p], C.c_int),
     "eqx_shard_record_bytes": ([C.c_int32, C.c_int32], C.c_int64),
     "eqx_shard_export_async": ([C.c_void_p, C.c_double, C.c_int32, C.c_int32, C.c_void_p], C.c_int),

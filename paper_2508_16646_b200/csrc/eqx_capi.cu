@@ -123,12 +123,16 @@ struct eqx_ctx {
   DevBuf d_direct;                 // direct predict/map table (see ScoreArgs::direct)
   int32_t direct_n = 0;
   // cached CUDA graph of drain + step for a resident (device) queue
-  cudaGraphExec_t graph = nullptr;
-  std::vector<unsigned char> graph_key;
+  // cached CUDA graphs of drain + step (two: a resident queue, or the two staging buffers)
+  cudaGraphExec_t graphs[2] = {nullptr, nullptr};
+  std::vector<unsigned char> graph_keys[2];
+  int graph_lru = 0;
   bool owns_stream = true;         // false after eqx_ctx_set_stream (caller's stream)
   // pinned bounce buffer for result reads: async D2H of every column, one sync, host memcpy
-  void* h_scratch = nullptr;
+  void* h_scratch = nullptr;       // mapped pinned memory
+  void* h_scratch_dev = nullptr;   // its device alias
   size_t h_scratch_bytes = 0;
+  DevState* h_state_dev = nullptr; // device alias of the mapped h_state
   // launch-attribute caches (cudaFuncSetAttribute / occupancy queries cost host time per step)
   int smem_attr[8] = {-1, -1, -1, -1, -1, -1, -1, -1};  // drain_hist, drain_rank, select kernels (select_fn)
   size_t occ_smem = SIZE_MAX;
@@ -153,7 +157,8 @@ cudaError_t ensure_scratch(eqx_ctx* ctx, size_t bytes) {
   ctx->h_scratch = nullptr;
   ctx->h_scratch_bytes = 0;
   const size_t want = std::max<size_t>(bytes, 1 << 16);
-  cudaError_t e = cudaMallocHost(&ctx->h_scratch, want);
+  cudaError_t e = cudaHostAlloc(&ctx->h_scratch, want, cudaHostAllocMapped);
+  if (e == cudaSuccess) e = cudaHostGetDevicePointer(&ctx->h_scratch_dev, ctx->h_scratch, 0);
   if (e == cudaSuccess) ctx->h_scratch_bytes = want;
   return e;
 }
@@ -198,6 +203,18 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
+// DevState -> the mapped host copy by a kernel (no copy-engine dependency; capturable).
+cudaError_t state_to_host(eqx_ctx* ctx, cudaStream_t s) {
+  PackCols pc;
+  std::memset(&pc, 0, sizeof(pc));
+  pc.src[0] = ctx->d_state.p;
+  pc.dst[0] = ctx->h_state_dev;
+  pc.bytes[0] = sizeof(DevState);
+  pc.n = 1;
+  pack_cols_kernel<<<1, 64, 0, s>>>(pc);
+  return cudaGetLastError();
+}
+
 cudaError_t set_smem_attr(eqx_ctx* ctx, int which, const void* fn, size_t bytes) {
   if (ctx->smem_attr[which] == static_cast<int>(bytes)) return cudaSuccess;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
@@ -221,11 +238,21 @@ eqx_status read_cols(eqx_ctx* ctx, const Col* cols, int n) {
   CUDA_TRY(ctx, ensure_scratch(ctx, total));
   cudaStream_t s = ctx->stream;
   size_t off = 0;
+  PackCols pc;
+  std::memset(&pc, 0, sizeof(pc));
   for (int i = 0; i < n; ++i) {
     if (!cols[i].dst || !cols[i].bytes) continue;
-    CUDA_TRY(ctx, cudaMemcpyAsync(static_cast<char*>(ctx->h_scratch) + off, cols[i].src, cols[i].bytes,
-                                  cudaMemcpyDeviceToHost, s));
+    pc.src[pc.n] = cols[i].src;
+    pc.dst[pc.n] = static_cast<char*>(ctx->h_scratch_dev) + off;
+    pc.bytes[pc.n] = static_cast<int64_t>(cols[i].bytes);
+    ++pc.n;
     off += (cols[i].bytes + 15) & ~size_t(15);
+  }
+  if (pc.n > 0) {
+    pack_cols_kernel<<<dim3(std::max<unsigned>(1, std::min<unsigned>(64, static_cast<unsigned>(total / 4096 + 1))),
+                            static_cast<unsigned>(pc.n)),
+                       256, 0, s>>>(pc);
+    CUDA_TRY(ctx, cudaGetLastError());
   }
   CUDA_TRY(ctx, cudaStreamSynchronize(s));
   off = 0;
@@ -347,7 +374,8 @@ eqx_status eqx_ctx_create(int32_t device, eqx_ctx** out) {
   if (e == cudaSuccess) e = cudaMemset(ctx->d_done.p, 0, 64);
   if (e == cudaSuccess) e = ctx->d_state.ensure(sizeof(DevState));
   if (e == cudaSuccess) e = cudaMemset(ctx->d_state.p, 0, sizeof(DevState));
-  if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_state, sizeof(DevState));
+  if (e == cudaSuccess) e = cudaHostAlloc(&ctx->h_state, sizeof(DevState), cudaHostAllocMapped);
+  if (e == cudaSuccess) e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->h_state_dev), ctx->h_state, 0);
   if (e == cudaSuccess) e = ctx->d_model.ensure(sizeof(ModelTables));
   if (e != cudaSuccess) {
     g_create_error = cudaGetErrorString(e);
@@ -402,7 +430,8 @@ void eqx_ctx_destroy(eqx_ctx* ctx) {
     if (st.ready) cudaEventDestroy(st.ready);
     if (st.free_) cudaEventDestroy(st.free_);
   }
-  if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
+  for (auto& g : ctx->graphs)
+    if (g) cudaGraphExecDestroy(g);
   ctx->d_first64.release();
   ctx->d_gid.release();
   ctx->d_service.release();
@@ -412,6 +441,7 @@ void eqx_ctx_destroy(eqx_ctx* ctx) {
 }
 
 void* eqx_ctx_stream(eqx_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+void* eqx_ctx_copy_stream(eqx_ctx* ctx) { return ctx ? static_cast<void*>(ctx->copy_stream) : nullptr; }
 
 eqx_status eqx_ctx_set_stream(eqx_ctx* ctx, void* stream) {
   if (!ctx) return fail(ctx, EQX_ERR_ARG, "eqx_ctx_set_stream: NULL context");  // stream 0 = legacy default
@@ -420,9 +450,11 @@ eqx_status eqx_ctx_set_stream(eqx_ctx* ctx, void* stream) {
   if (ctx->owns_stream) CUDA_TRY(ctx, cudaStreamDestroy(ctx->stream));
   ctx->stream = static_cast<cudaStream_t>(stream);
   ctx->owns_stream = false;
-  if (ctx->graph) cudaGraphExecDestroy(ctx->graph);  // captured on the old stream's plan
-  ctx->graph = nullptr;
-  ctx->graph_key.clear();
+  for (int i = 0; i < 2; ++i) {  // captured on the old stream's plan
+    if (ctx->graphs[i]) cudaGraphExecDestroy(ctx->graphs[i]);
+    ctx->graphs[i] = nullptr;
+    ctx->graph_keys[i].clear();
+  }
   return EQX_OK;
 }
 
@@ -685,16 +717,8 @@ static eqx_status stage_fill(eqx_ctx* ctx, const eqx_requests* r, int b) {
   if (r->true_output_tokens) CUDA_TRY(ctx, st.tru.ensure(4 * nn));
   if (r->id) CUDA_TRY(ctx, st.id.ensure(8 * nn));
   CUDA_TRY(ctx, cudaStreamWaitEvent(cs, st.free_, 0));
-  // 1 MiB pieces: a step's small result reads (D2H) interleave with a long prefetch instead of
-  // queueing behind all of it on the DMA engines
-  auto h2d = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
-    constexpr size_t kPiece = size_t(1) << 20;
-    for (size_t o = 0; o < bytes; o += kPiece) {
-      cudaError_t e = cudaMemcpyAsync(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o,
-                                      std::min(kPiece, bytes - o), cudaMemcpyHostToDevice, cs);
-      if (e != cudaSuccess) return e;
-    }
-    return cudaSuccess;
+  auto h2d = [&](void* dst, const void* src, size_t bytes) {
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, cs);
   };
   if (n > 0) {
     CUDA_TRY(ctx, h2d(st.client.p, r->client, 4 * n));
@@ -1261,7 +1285,7 @@ static eqx_status step_enqueue(eqx_ctx* ctx, const StepPlan& pl, bool with_drain
   ef.now = pl.se.now;
   if (ctx->n > 0) event_fill_kernel<<<ctx->sm_count, 256, 0, s>>>(ef);
   CUDA_TRY(ctx, cudaGetLastError());
-  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_state, ctx->d_state.p, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(ctx, state_to_host(ctx, s));
   return EQX_OK;
 }
 
@@ -1295,36 +1319,39 @@ eqx_status eqx_drain_step_async(eqx_ctx* ctx, const eqx_requests* r, double now)
   if (st != EQX_OK) return st;
   pl.se.do_lift = 1;  // the fused drain leaves on_activated to the selection prologue
   cudaStream_t s = ctx->stream;
-  if (r->location != EQX_DEVICE) {  // host columns: plain launches after the staged H2D
+  // One CUDA-graph launch replays drain + scoring + selection.  The key covers every launch
+  // parameter (pointers, sizes, policy, `now`, smem/tiling plan); two graphs are cached, for a
+  // resident queue or the two staging buffers of host batches (whose H2D and release events
+  // stay outside the graph).
+  std::vector<unsigned char> key(sizeof(StepPlan) + 6 * sizeof(int64_t));
+  std::memcpy(key.data(), &pl, sizeof(StepPlan));
+  const int64_t extra[6] = {ctx->tile_rows, ctx->n_tiles, ctx->counter_lift, static_cast<int64_t>(ctx->hist_smem),
+                            static_cast<int64_t>(ctx->rank_smem), ctx->staged};
+  std::memcpy(key.data() + sizeof(StepPlan), extra, sizeof(extra));
+  int slot = -1;
+  for (int i = 0; i < 2; ++i)
+    if (ctx->graphs[i] && ctx->graph_keys[i] == key) slot = i;
+  if (slot < 0) {
+    slot = ctx->graph_lru;
+    if (ctx->graphs[slot]) cudaGraphExecDestroy(ctx->graphs[slot]);
+    ctx->graphs[slot] = nullptr;
+    cudaGraph_t g = nullptr;
+    CUDA_TRY(ctx, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     st = step_enqueue(ctx, pl, true);
-    if (st == EQX_OK) st = release_stage(ctx);
-  } else {
-    // Resident queue: one CUDA-graph launch replays drain + scoring + selection.  The key
-    // covers every launch parameter (pointers, sizes, policy, `now`, smem/tiling plan).
-    std::vector<unsigned char> key(sizeof(StepPlan) + 6 * sizeof(int64_t));
-    std::memcpy(key.data(), &pl, sizeof(StepPlan));
-    const int64_t extra[6] = {ctx->tile_rows, ctx->n_tiles, ctx->counter_lift, static_cast<int64_t>(ctx->hist_smem),
-                              static_cast<int64_t>(ctx->rank_smem), ctx->staged};
-    std::memcpy(key.data() + sizeof(StepPlan), extra, sizeof(extra));
-    if (!ctx->graph || key != ctx->graph_key) {
-      if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
-      ctx->graph = nullptr;
-      cudaGraph_t g = nullptr;
-      CUDA_TRY(ctx, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-      st = step_enqueue(ctx, pl, true);
-      cudaError_t ce = cudaStreamEndCapture(s, &g);
-      if (st != EQX_OK) {
-        if (g) cudaGraphDestroy(g);
-        return st;
-      }
-      CUDA_TRY(ctx, ce);
-      cudaError_t ie = cudaGraphInstantiate(&ctx->graph, g, 0);
-      cudaGraphDestroy(g);
-      CUDA_TRY(ctx, ie);
-      ctx->graph_key = key;
+    cudaError_t ce = cudaStreamEndCapture(s, &g);
+    if (st != EQX_OK) {
+      if (g) cudaGraphDestroy(g);
+      return st;
     }
-    CUDA_TRY(ctx, cudaGraphLaunch(ctx->graph, s));
+    CUDA_TRY(ctx, ce);
+    cudaError_t ie = cudaGraphInstantiate(&ctx->graphs[slot], g, 0);
+    cudaGraphDestroy(g);
+    CUDA_TRY(ctx, ie);
+    ctx->graph_keys[slot] = key;
   }
+  ctx->graph_lru = slot ^ 1;
+  CUDA_TRY(ctx, cudaGraphLaunch(ctx->graphs[slot], s));
+  if (r->location != EQX_DEVICE) st = release_stage(ctx);
   if (st != EQX_OK) return st;
   ctx->step_pending = true;
   ctx->stepped = true;
@@ -1587,7 +1614,7 @@ eqx_status eqx_shard_select_async(eqx_ctx* ctx, const void* recs, int32_t world,
   ef.now = now;
   shard_event_fill_kernel<<<std::max(1, ctx->sm_count / 4), 256, 0, s>>>(ef, ctx->d_win.as<WinEntry>());
   CUDA_TRY(ctx, cudaGetLastError());
-  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_state, ctx->d_state.p, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(ctx, state_to_host(ctx, s));
   ctx->q_id = ctx->d_gid.as<int64_t>();
   ctx->id_base = 0;
   ctx->shard_W = W;

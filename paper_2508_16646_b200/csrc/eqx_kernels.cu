@@ -2584,6 +2584,25 @@ __global__ void gather_ids_kernel(const int32_t* __restrict__ rows, int64_t n, c
   }
 }
 
+// Columns -> mapped host memory by SM stores over PCIe (16-byte words when aligned).
+__global__ void pack_cols_kernel(const PackCols p) {
+  for (int c = blockIdx.y; c < p.n; c += gridDim.y) {
+    const int64_t b = p.bytes[c];
+    const unsigned char* src = static_cast<const unsigned char*>(p.src[c]);
+    unsigned char* dst = static_cast<unsigned char*>(p.dst[c]);
+    const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t nt = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+      const int64_t w = b / 16;
+      for (int64_t i = tid; i < w; i += nt)
+        reinterpret_cast<int4*>(dst)[i] = __ldcg(reinterpret_cast<const int4*>(src) + i);
+      for (int64_t i = 16 * w + tid; i < b; i += nt) dst[i] = src[i];
+    } else {
+      for (int64_t i = tid; i < b; i += nt) dst[i] = src[i];
+    }
+  }
+}
+
 // ============================== completion / feedback =====================================
 // One engine iteration's feedback (engine.cpp:273-375) in the reference's order: on_tokens for
 // every client with decode tokens (scheduler.cpp:185-190), then each completion in order:

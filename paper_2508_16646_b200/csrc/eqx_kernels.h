@@ -273,6 +273,17 @@ struct FeedbackArgs {
 };
 __global__ void feedback_kernel(FeedbackArgs a);
 
+// Device -> mapped pinned host memory without the DMA engines (a step's results must not
+// queue behind the next batch's H2D prefetch on the copy engines).
+constexpr int kMaxPackCols = 8;
+struct PackCols {
+  const void* src[kMaxPackCols];
+  void* dst[kMaxPackCols];  // device-side aliases of mapped host memory
+  int64_t bytes[kMaxPackCols];
+  int32_t n;
+};
+__global__ void pack_cols_kernel(PackCols p);
+
 __global__ void drain_hist_kernel(DrainArgs a);
 __global__ void lift_kernel(DrainArgs a);
 __global__ void event_fill_kernel(EventFillArgs a);

@@ -30,7 +30,7 @@ print("serial step", tm(serial))
 st = {"i": 0}
 def piped():
     i = st["i"]; st["i"] += 1
-    sch.stage_async(**hosts[(i + 1) % 2]); sch.restore_async(); sch.drain(**hosts[i % 2]); sch.step(1.0); sch.ledger()
+    sch.stage_async(**hosts[(i + 1) % 2]); sch.restore_async(); sch.drain_step_async(1.0, **hosts[i % 2]); sch.collect(); sch.ledger()
 sch.stage_async(**hosts[0])
 print("pipelined step", tm(piped))
 # per-call wall times inside the pipelined loop
