@@ -195,6 +195,15 @@ eqx_status eqx_step_collect(eqx_ctx* ctx, eqx_step_summary* out);
 /* Convenience: eqx_step_async + eqx_step_collect. */
 eqx_status eqx_step(eqx_ctx* ctx, double now, eqx_step_summary* out);
 
+/* ---- live queues ------------------------------------------------------
+ * drain_arrivals (engine.cpp:171-197) for a batch of arrivals that joins the requests still
+ * queued (unlike eqx_drain, which replaces the queue): each arrival's prediction record is made
+ * now against the current profile and frozen with it (update_map later does not change it),
+ * clients idle before the batch (empty queue, no running requests) get on_activated in arrival
+ * order, every arriving client becomes backlogged.  Then eqx_step_async / eqx_step schedule
+ * from the live queue, repeatedly; eqx_feedback between steps.  ids default to id_base + i. */
+eqx_status eqx_append(eqx_ctx* ctx, const eqx_requests* arrivals);
+
 /* ---- completion / feedback -------------------------------------------
  * A batch of completed requests, in the engine's completion order (complete_finished,
  * engine.cpp:327-375): RequestActuals (scheduler.hpp:89-95) plus the PendingContribution the

@@ -464,3 +464,37 @@ def feedback_case(seed: int, kind: int = 2, vtc_use_prediction: int = 0, n_clien
 
 
 FEEDBACK_KEYS = ("ufc", "rfc", "counter", "service", "running", "prof_lat", "prof_util", "prof_tps")
+
+
+def ref_multi(case: "StepCase", step_end, step_now, act_extra, act_tps, act_util, ema_alpha=0.2, complete_mod=3):
+    """Several engine steps on live queues through the reference objects (oracle/ref_step.cpp
+    ref_multi): events (id, kind, step, ufc_inc, rfc_inc), final ledger and profile."""
+    lib, _ = _lib("ref")
+    keep: list = []
+    s = _build_in(case, keep)
+    cap = max(1, 2 * int(s.n_req))
+    out = {k: np.zeros(cap, dt) for k, dt in (("ev_id", np.int64), ("ev_kind", np.int32), ("ev_step", np.int32),
+                                               ("ev_ufc", np.float64), ("ev_rfc", np.float64))}
+    nc, npf = int(s.n_clients), int(s.n_profile)
+    led = {k: np.zeros(nc) for k in ("ufc", "rfc", "counter")}
+    prof = {k: np.zeros(npf) for k in ("lat", "util", "tps")}
+    arr = {k: np.ascontiguousarray(v, np.float64) for k, v in (("now", step_now), ("extra", act_extra),
+                                                                ("tps", act_tps), ("util", act_util))}
+    end = np.ascontiguousarray(step_end, np.int64)
+    err = C.create_string_buffer(512)
+    f = lib.ref_multi
+    f.restype = C.c_int64
+    n = f(C.byref(s), C.c_int32(len(end)), _ptr(end, C.c_int64), _ptr(arr["now"], C.c_double),
+          _ptr(arr["extra"], C.c_double), _ptr(arr["tps"], C.c_double), _ptr(arr["util"], C.c_double),
+          C.c_double(ema_alpha), C.c_int32(complete_mod), _ptr(out["ev_id"], C.c_int64),
+          _ptr(out["ev_kind"], C.c_int32), _ptr(out["ev_step"], C.c_int32), _ptr(out["ev_ufc"], C.c_double),
+          _ptr(out["ev_rfc"], C.c_double), C.c_int64(cap), _ptr(led["ufc"], C.c_double), _ptr(led["rfc"], C.c_double),
+          _ptr(led["counter"], C.c_double), _ptr(prof["lat"], C.c_double), _ptr(prof["util"], C.c_double),
+          _ptr(prof["tps"], C.c_double), err, 512)
+    if n < 0:
+        raise ValueError(err.value.decode())
+    n = min(int(n), cap)
+    res = {k: v[:n] for k, v in out.items()}
+    res.update(led)
+    res.update({"prof_" + k: v for k, v in prof.items()})
+    return res

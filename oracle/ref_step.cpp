@@ -548,3 +548,185 @@ extern "C" int ref_feedback(eqxo_feedback* f, const char* client_names, double n
     return 1;
   }
 }
+
+// ref_multi -- several engine steps on live queues through the reference objects: at step k
+// the arrivals in rows [step_end[k-1], step_end[k]) are drained (engine.cpp:171-197: predict,
+// map_metrics against the *current* profile, on_activated for idle clients, push,
+// set_backlogged), admit_requests runs at step_now[k] (engine.cpp:207-271) on the queues left
+// by earlier steps plus the new arrivals, and then every batch member whose
+// (request_id * 7 + k) % complete_mod == 0 completes in batch order (engine.cpp:327-375:
+// on_complete, update_map, running count, member erase) with actuals
+// {true_output_tokens, step_now[k] - arrival + act_extra, act_tps, act_util} (row-indexed).
+// ids must be the row indices.  Events go to ev_* with their step in ev_step; returns the
+// event count, or -1 on error.
+extern "C" int64_t ref_multi(const eqxo_step_in* in, int32_t n_steps, const int64_t* step_end,
+                             const double* step_now, const double* act_extra, const double* act_tps,
+                             const double* act_util, double ema_alpha, int32_t complete_mod, int64_t* ev_id,
+                             int32_t* ev_kind, int32_t* ev_step, double* ev_ufc, double* ev_rfc, int64_t cap,
+                             double* ufc, double* rfc, double* counter, double* prof_lat, double* prof_util,
+                             double* prof_tps, char* err, int err_len) {
+  try {
+    const auto names = split_names(in->client_names, in->n_clients);
+    const auto tags = split_names(in->tag_names, in->n_tags);
+    PolicySpec spec;
+    spec.kind = static_cast<PolicyKind>(in->kind);
+    spec.equinox.alpha = in->alpha;
+    spec.equinox.delta = in->delta;
+    spec.equinox.output_weight = in->output_weight;
+    spec.equinox.norm_mode = in->norm_mode == EQXO_NORM_NONE ? NormMode::None : NormMode::MaxOverClients;
+    spec.vtc_use_prediction = in->vtc_use_prediction != 0;
+    spec.counter_lift = in->counter_lift != 0;
+    std::vector<ClientState> roster(static_cast<std::size_t>(in->n_clients));
+    for (int c = 0; c < in->n_clients; ++c) {
+      roster[c].client_id = names[c];
+      roster[c].weight = in->weight[c];
+      roster[c].ufc = in->ufc0[c];
+      roster[c].rfc = in->rfc0[c];
+      roster[c].counter = in->counter0[c];
+    }
+    SchedulerPolicy policy(spec, roster);
+    PerfParams perf;
+    perf.max_batch = in->max_batch;
+    perf.mem_per_token_bytes = in->mem_per_token_bytes;
+    perf.mem_capacity_bytes = in->mem_capacity_bytes;
+    GpuProfile profile;
+    for (int e = 0; e < in->n_profile; ++e)
+      profile.entries.push_back({in->prof_upper[e], in->prof_lat[e], in->prof_util[e], in->prof_tps[e]});
+    std::unique_ptr<Predictor> predictor;
+    switch (in->pred_kind) {
+      case EQXO_PRED_ORACLE: predictor = std::make_unique<OraclePredictor>(); break;
+      case EQXO_PRED_NOISY: predictor = std::make_unique<NoisyOraclePredictor>(in->noisy_l1, in->noisy_seed); break;
+      case EQXO_PRED_MOPE:
+        predictor = std::make_unique<MopePredictor>(model_from(in->mope, tags, in->tag_row, in->n_tags));
+        break;
+      case EQXO_PRED_SINGLE: {
+        MopeModel m = model_from(in->mope, tags, in->tag_row, in->n_tags);
+        predictor = std::make_unique<SingleProxyPredictor>(m.experts.at(0));
+        break;
+      }
+      default: throw ConfigError("unknown predictor kind");
+    }
+    std::vector<Request> reqs(static_cast<std::size_t>(in->n_req));
+    for (int64_t r = 0; r < in->n_req; ++r) {
+      Request& q = reqs[static_cast<std::size_t>(r)];
+      q.id = in->id[r];
+      q.client_id = names[static_cast<std::size_t>(in->client[r])];
+      q.arrival_time_s = in->arrival[r];
+      q.input_tokens = in->in_tokens[r];
+      q.true_output_tokens = in->true_out[r];
+      if (in->tag[r] >= 0) q.category_tag = tags[static_cast<std::size_t>(in->tag[r])];
+    }
+    std::vector<std::deque<Queued>> queues(static_cast<std::size_t>(in->n_clients));
+    std::vector<int> running(static_cast<std::size_t>(in->n_clients), 0);
+    BatchState batch;
+    std::vector<std::size_t> member_client;
+    int64_t n_ev = 0, row = 0;
+    for (int32_t k = 0; k < n_steps; ++k) {
+      const double now = step_now[k];
+      for (; row < step_end[k]; ++row) {  // drain_arrivals
+        const Request& req = reqs[static_cast<std::size_t>(row)];
+        const std::size_t ci = static_cast<std::size_t>(in->client[row]);
+        const int predicted = std::max(1, predictor->predict(req));
+        Queued queued{req, map_metrics(predicted, profile)};
+        if (queues[ci].empty() && running[ci] == 0) policy.on_activated(ci);
+        queues[ci].push_back(std::move(queued));
+        policy.set_backlogged(ci, true);
+      }
+      auto pop_head = [&](std::size_t ci) {
+        queues[ci].pop_front();
+        if (queues[ci].empty()) policy.set_backlogged(ci, false);
+      };
+      std::set<std::size_t> skipped;
+      while (true) {  // admit_requests
+        std::vector<HeadCandidate> candidates;
+        for (std::size_t i = 0; i < queues.size(); ++i) {
+          if (queues[i].empty() || skipped.count(i) != 0) continue;
+          candidates.push_back({i, queues[i].front().req.arrival_time_s});
+        }
+        const auto choice = policy.select_next(candidates);
+        if (!choice) break;
+        const std::size_t ci = *choice;
+        const Queued head = queues[ci].front();
+        const int tin = head.req.input_tokens;
+        const int predicted = head.prediction.predicted_output_tokens;
+        if (!fits_alone(tin, predicted, perf)) {
+          if (n_ev < cap) {
+            ev_id[n_ev] = head.req.id;
+            ev_kind[n_ev] = EQXO_EV_REJECT;
+            ev_step[n_ev] = k;
+            ev_ufc[n_ev] = ev_rfc[n_ev] = 0.0;
+          }
+          ++n_ev;
+          pop_head(ci);
+          continue;
+        }
+        if (!can_fit(batch, tin, predicted, perf)) {
+          if (in->backfill) {
+            skipped.insert(ci);
+            continue;
+          }
+          break;
+        }
+        pop_head(ci);
+        batch.members.push_back({head.req.id, tin, 0, predicted});
+        member_client.push_back(ci);
+        ++running[ci];
+        ScheduleContext ctx;
+        ctx.now_s = now;
+        ctx.wait_s = now - head.req.arrival_time_s;
+        ctx.prediction = head.prediction;
+        const double w = policy.clients()[ci].weight;
+        policy.on_admit(ci, head.req, ctx);
+        if (n_ev < cap) {
+          ev_id[n_ev] = head.req.id;
+          ev_kind[n_ev] = EQXO_EV_ADMIT;
+          ev_step[n_ev] = k;
+          ev_ufc[n_ev] = ufc_increment(head.req, ctx, w, spec.equinox);
+          ev_rfc[n_ev] = rfc_increment(ctx.prediction, w);
+        }
+        ++n_ev;
+      }
+      // completions, in batch order
+      std::size_t i = 0;
+      while (i < batch.members.size()) {
+        const int64_t id = batch.members[i].request_id;
+        if ((id * 7 + k) % complete_mod != 0) {
+          ++i;
+          continue;
+        }
+        const Request& req = reqs[static_cast<std::size_t>(id)];
+        const std::size_t ci = member_client[i];
+        RequestActuals act;
+        act.output_tokens = req.true_output_tokens;
+        act.latency_s = now - req.arrival_time_s + act_extra[id];
+        act.tps = act_tps[id];
+        act.gpu_util = act_util[id];
+        policy.on_complete(ci, req, act);
+        ObservedMetrics obs;
+        obs.output_tokens = act.output_tokens;
+        obs.latency_ms = act.latency_s * 1000.0;
+        obs.gpu_util = act.gpu_util;
+        obs.tps = act.tps;
+        update_map(profile, obs, ema_alpha);
+        --running[ci];
+        batch.members.erase(batch.members.begin() + static_cast<std::ptrdiff_t>(i));
+        member_client.erase(member_client.begin() + static_cast<std::ptrdiff_t>(i));
+      }
+    }
+    for (int c = 0; c < in->n_clients; ++c) {
+      const ClientState& s = policy.clients()[static_cast<std::size_t>(c)];
+      ufc[c] = s.ufc;
+      rfc[c] = s.rfc;
+      counter[c] = s.counter;
+    }
+    for (int e = 0; e < in->n_profile; ++e) {
+      prof_lat[e] = profile.entries[static_cast<std::size_t>(e)].latency_ms;
+      prof_util[e] = profile.entries[static_cast<std::size_t>(e)].gpu_util;
+      prof_tps[e] = profile.entries[static_cast<std::size_t>(e)].tps;
+    }
+    return n_ev;
+  } catch (const std::exception& e) {
+    set_err(err, err_len, e.what());
+    return -1;
+  }
+}

@@ -96,6 +96,7 @@ _SIGS = {
     "eqx_ledger_restore_async": ([C.c_void_p], C.c_int),
     "eqx_drain": ([C.c_void_p, C.POINTER(Requests)], C.c_int),
     "eqx_stage_async": ([C.c_void_p, C.POINTER(Requests)], C.c_int),
+    "eqx_append": ([C.c_void_p, C.POINTER(Requests)], C.c_int),
     "eqx_step_async": ([C.c_void_p, C.c_double], C.c_int),
     "eqx_drain_step_async": ([C.c_void_p, C.POINTER(Requests), C.c_double], C.c_int),
     "eqx_step_collect": ([C.c_void_p, C.POINTER(StepSummary)], C.c_int),

@@ -140,6 +140,15 @@ struct eqx_ctx {
   // client-sharded step (selection context): gathered windows and their ids
   DevBuf d_first64, d_gid;
   DevBuf d_service;                // ClientState::accumulated_service
+  // live queue (eqx_append): two column stores with frozen prediction records, swapped per append
+  struct Live {
+    DevBuf client, arrival, in, tag, tru, id, pred, bucket, preds, rfc;
+  } live[2];
+  int live_cur = -1;
+  bool live_mode = false;
+  int64_t popped = 0;  // requests popped (admitted / rejected) since the queue was (re)built
+  Frozen frozen{};
+  DevBuf d_live_off, d_nlive;
   DevBuf d_fb;                     // staged completion batch / token counts
   int32_t shard_W = 0;             // > 0: the last step was a sharded selection
 };
@@ -435,6 +444,12 @@ void eqx_ctx_destroy(eqx_ctx* ctx) {
   ctx->d_first64.release();
   ctx->d_gid.release();
   ctx->d_service.release();
+  for (auto& L : ctx->live) {
+    DevBuf* lb[] = {&L.client, &L.arrival, &L.in, &L.tag, &L.tru, &L.id, &L.pred, &L.bucket, &L.preds, &L.rfc};
+    for (DevBuf* b : lb) b->release();
+  }
+  ctx->d_live_off.release();
+  ctx->d_nlive.release();
   ctx->d_fb.release();
   if (ctx->stream && ctx->owns_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -821,6 +836,7 @@ static eqx_status drain_prepare(eqx_ctx* ctx, const eqx_requests* r) {
   }
   ctx->id_base = r->id_base;
   ctx->n = n;
+  ctx->popped = 0;
   // scores + events sized to the queue
   CUDA_TRY(ctx, ctx->d_pred.ensure(4 * nn + 16));
   CUDA_TRY(ctx, ctx->d_bucket.ensure(nn + 16));
@@ -895,12 +911,12 @@ static DrainArgs drain_args(eqx_ctx* ctx) {
 // Pure stream work of a drain (2 memsets + 2 kernels); capturable into a CUDA graph.
 // lift: also apply on_activated / set_backlogged now (a standalone drain); a drain fused into a
 // step leaves that to the selection kernel's prologue (SelectArgs::do_lift).
-static eqx_status drain_enqueue(eqx_ctx* ctx, bool lift) {
+static eqx_status drain_enqueue(eqx_ctx* ctx, bool lift, bool keep_qlen = false) {
   cudaStream_t s = ctx->stream;
   const int32_t C = ctx->C;
   if (C == 0) return EQX_OK;
   CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_head.p, 0, 4ull * C, s));
-  CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_qlen_before.p, 0, 4ull * C, s));
+  if (!keep_qlen) CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_qlen_before.p, 0, 4ull * C, s));
   CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_first.p, 0xff, 4ull * C, s));  // atomicMin target
 #ifdef EQX_PROF
   {
@@ -1029,6 +1045,7 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl, int32_t g
   sc.vec_ok = aligned16(sc.client) && aligned16(sc.arrival) && aligned16(sc.in_tok) &&
               (reinterpret_cast<uintptr_t>(sc.tag) % 8 == 0) && (!sc.true_out || aligned16(sc.true_out));
   sc.pol = ctx->pol;
+  sc.frozen = ctx->live_mode ? ctx->frozen : Frozen{};
   sc.now = now;
   pl.score_smem = model_smem;
   int per_sm = 1;
@@ -1100,6 +1117,7 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl, int32_t g
   a.qlen_before = ctx->d_qlen_before.as<int32_t>();
   a.counter_lift = ctx->counter_lift;
   a.pol = ctx->pol;
+  a.frozen = ctx->live_mode ? ctx->frozen : Frozen{};
   a.now = now;
   pl.select_threads = kSelectMaxThreads;
   // selection threads: one warp holding up to 8 clients per lane when C <= 256 (no barriers),
@@ -1212,6 +1230,7 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl, int32_t g
   wi.model_words = model_words;
   wi.tmax = a.tmax;
   wi.pol = ctx->pol;
+  wi.frozen = ctx->live_mode ? ctx->frozen : Frozen{};
   wi.now = now;
   pl.window_smem = model_smem;
   const int64_t witems = static_cast<int64_t>(C) * a.W;
@@ -1292,6 +1311,7 @@ static eqx_status step_enqueue(eqx_ctx* ctx, const StepPlan& pl, bool with_drain
 eqx_status eqx_drain(eqx_ctx* ctx, const eqx_requests* r) {
   eqx_status st = drain_prepare(ctx, r);
   if (st != EQX_OK) return st;
+  ctx->live_mode = false;  // replaces the queue
   ctx->shard_W = 0;
   st = drain_enqueue(ctx, true);
   if (st != EQX_OK) return st;
@@ -1313,6 +1333,7 @@ eqx_status eqx_step_async(eqx_ctx* ctx, double now) {
 eqx_status eqx_drain_step_async(eqx_ctx* ctx, const eqx_requests* r, double now) {
   eqx_status st = drain_prepare(ctx, r);
   if (st != EQX_OK) return st;
+  ctx->live_mode = false;  // replaces the queue
   ctx->shard_W = 0;
   StepPlan pl;
   st = step_prepare(ctx, now, pl);
@@ -1358,6 +1379,133 @@ eqx_status eqx_drain_step_async(eqx_ctx* ctx, const eqx_requests* r, double now)
   return EQX_OK;
 }
 
+// ---- live queues -----------------------------------------------------
+eqx_status eqx_append(eqx_ctx* ctx, const eqx_requests* r) {
+  if (!ctx || !r) return fail(ctx, EQX_ERR_ARG, "eqx_append: NULL argument");
+  if (!ctx->model_set || !ctx->profile_set)
+    return fail(ctx, EQX_ERR_CONFIG, "eqx_append: predictor and GPU profile must be set first");
+  if (ctx->queue_ready && !ctx->live_mode)
+    return fail(ctx, EQX_ERR_CONFIG, "eqx_append: the context holds a queue from eqx_drain (which replaces queues)");
+  const int64_t m = r->n;
+  if (m < 0) return fail(ctx, EQX_ERR_ARG, "eqx_append: negative batch size");
+  const int32_t C = ctx->C;
+  if (m > 0 && C == 0) return fail(ctx, EQX_ERR_CONFIG, "eqx_append: requests but no clients");
+  const bool needs_true = ctx->model.pred_kind == kPredOracle || ctx->model.pred_kind == kPredNoisy;
+  if (m > 0 && (!r->client || !r->arrival_s || !r->input_tokens || (needs_true && !r->true_output_tokens)))
+    return fail(ctx, EQX_ERR_ARG, "eqx_append: missing request column");
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = ctx->stream;
+  // 1. remaining rows of the live queue (client-grouped FIFO order)
+  const int old = ctx->live_cur;
+  const bool have_old = ctx->live_mode && old >= 0;
+  LiveArgs L;
+  std::memset(&L, 0, sizeof(L));
+  L.C = C;
+  int64_t n_live = 0;
+  CUDA_TRY(ctx, ctx->d_live_off.ensure(4ull * (C + 1)));
+  CUDA_TRY(ctx, ctx->d_nlive.ensure(64));
+  L.live_off = ctx->d_live_off.as<int32_t>();
+  L.qlen_before = ctx->d_qlen_before.as<int32_t>();
+  L.n_live = ctx->d_nlive.as<int64_t>();
+  if (have_old && C > 0) {
+    L.perm = ctx->d_perm.as<uint32_t>();
+    L.seg_off = ctx->d_seg_off.as<int32_t>();
+    L.count = ctx->d_count.as<int32_t>();
+    L.head = ctx->d_head.as<int32_t>();
+    live_offsets_kernel<<<1, 1024, 0, s>>>(L);
+    CUDA_TRY(ctx, cudaGetLastError());
+    CUDA_TRY(ctx, cudaMemcpyAsync(&n_live, L.n_live, 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  } else if (C > 0) {
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_qlen_before.p, 0, 4ull * C, s));
+  }
+  // 2. the new column store: remaining rows, then the arrivals
+  const int nb = have_old ? (old ^ 1) : 0;
+  eqx_ctx::Live& N = ctx->live[nb];
+  const int64_t total = n_live + m;
+  if (total >= (int64_t(1) << 31) - 1) return fail(ctx, EQX_ERR_ARG, "eqx_append: live queue too long");
+  const size_t tt = static_cast<size_t>(std::max<int64_t>(total, 1));
+  CUDA_TRY(ctx, N.client.ensure(4 * tt + 16));
+  CUDA_TRY(ctx, N.arrival.ensure(8 * tt + 16));
+  CUDA_TRY(ctx, N.in.ensure(4 * tt + 16));
+  CUDA_TRY(ctx, N.tag.ensure(tt + 16));
+  CUDA_TRY(ctx, N.id.ensure(8 * tt + 16));
+  CUDA_TRY(ctx, N.pred.ensure(4 * tt + 16));
+  CUDA_TRY(ctx, N.bucket.ensure(tt + 16));
+  CUDA_TRY(ctx, N.preds.ensure(8 * tt + 16));
+  CUDA_TRY(ctx, N.rfc.ensure(8 * tt + 16));
+  if (needs_true) CUDA_TRY(ctx, N.tru.ensure(4 * tt + 16));
+  L.n_client = N.client.as<int32_t>();
+  L.n_arrival = N.arrival.as<double>();
+  L.n_in = N.in.as<int32_t>();
+  L.n_tag = N.tag.as<uint8_t>();
+  L.n_true = needs_true ? N.tru.as<int32_t>() : nullptr;
+  L.n_id = N.id.as<int64_t>();
+  L.n_pred = N.pred.as<int32_t>();
+  L.n_bucket = N.bucket.as<uint8_t>();
+  L.n_preds = N.preds.as<double>();
+  L.n_rfc = N.rfc.as<double>();
+  if (n_live > 0) {
+    eqx_ctx::Live& O = ctx->live[old];
+    L.o_client = O.client.as<int32_t>();
+    L.o_arrival = O.arrival.as<double>();
+    L.o_in = O.in.as<int32_t>();
+    L.o_tag = O.tag.as<uint8_t>();
+    L.o_true = needs_true ? O.tru.as<int32_t>() : nullptr;
+    L.o_id = O.id.as<int64_t>();
+    L.o_pred = O.pred.as<int32_t>();
+    L.o_bucket = O.bucket.as<uint8_t>();
+    L.o_preds = O.preds.as<double>();
+    L.o_rfc = O.rfc.as<double>();
+    const int grid = static_cast<int>(std::min<int64_t>((n_live + 255) / 256, 8ll * ctx->sm_count));
+    gather_live_kernel<<<grid, 256, 0, s>>>(L);
+    CUDA_TRY(ctx, cudaGetLastError());
+  }
+  if (m > 0) {
+    const cudaMemcpyKind k = r->location == EQX_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    CUDA_TRY(ctx, cudaMemcpyAsync(L.n_client + n_live, r->client, 4 * m, k, s));
+    CUDA_TRY(ctx, cudaMemcpyAsync(L.n_arrival + n_live, r->arrival_s, 8 * m, k, s));
+    CUDA_TRY(ctx, cudaMemcpyAsync(L.n_in + n_live, r->input_tokens, 4 * m, k, s));
+    if (r->tag) CUDA_TRY(ctx, cudaMemcpyAsync(L.n_tag + n_live, r->tag, m, k, s));
+    else CUDA_TRY(ctx, cudaMemsetAsync(L.n_tag + n_live, 0, m, s));
+    if (needs_true) CUDA_TRY(ctx, cudaMemcpyAsync(L.n_true + n_live, r->true_output_tokens, 4 * m, k, s));
+    if (r->id) CUDA_TRY(ctx, cudaMemcpyAsync(L.n_id + n_live, r->id, 8 * m, k, s));
+    // 3. prediction records against the current profile (drain_arrivals: predict + map_metrics)
+    StepPlan pl;
+    const bool qr = ctx->queue_ready;
+    const int64_t n0 = ctx->n;
+    ctx->queue_ready = true;  // plan only: uploads the model tables if they changed
+    eqx_status st = step_prepare(ctx, 0.0, pl);
+    ctx->queue_ready = qr;
+    ctx->n = n0;
+    if (st != EQX_OK) return st;
+    ScoreArgs sc = pl.sc;
+    sc.frozen = Frozen{};
+    sc.id_base = r->id_base;
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, 8ll * ctx->sm_count)));
+    predict_rows_kernel<<<grid, 256, pl.window_smem, s>>>(sc, n_live, total, L, r->id ? 0 : 1);
+    CUDA_TRY(ctx, cudaGetLastError());
+  }
+  ctx->live_cur = nb;
+  ctx->live_mode = true;
+  ctx->frozen = Frozen{L.n_pred, L.n_bucket, L.n_preds, L.n_rfc};
+  // 4. per-client FIFOs over the new store; the lift treats the remaining counts as non-empty
+  //    queues (on_activated only for clients idle before the batch, engine.cpp:182)
+  eqx_requests q{};
+  q.n = total;
+  q.id = L.n_id;
+  q.client = L.n_client;
+  q.arrival_s = L.n_arrival;
+  q.input_tokens = L.n_in;
+  q.true_output_tokens = L.n_true;
+  q.tag = L.n_tag;
+  q.location = EQX_DEVICE;
+  eqx_status st = drain_prepare(ctx, &q);
+  if (st != EQX_OK) return st;
+  ctx->shard_W = 0;
+  return drain_enqueue(ctx, true, true);
+}
+
 // ---- completion / feedback ------------------------------------------
 eqx_status eqx_feedback(eqx_ctx* ctx, const int64_t* tokens, const eqx_completions* done, double ema_alpha) {
   if (!ctx) return fail(ctx, EQX_ERR_ARG, "eqx_feedback: NULL context");
@@ -1381,7 +1529,7 @@ eqx_status eqx_feedback(eqx_ctx* ctx, const int64_t* tokens, const eqx_completio
   f.n = n;
   // host columns: one staging block [tokens C][client, in, out n][latency, tps, util, pending x3 n]
   const size_t nn = static_cast<size_t>(n);
-  const size_t need = 8ull * C + 12 * nn + 48 * nn + 64;
+  const size_t need = 8ull * C + 12 * nn + 48 * nn + 16 * 12;  // + 16-byte alignment of 10 sections
   CUDA_TRY(ctx, ctx->d_fb.ensure(need));
   char* base = static_cast<char*>(ctx->d_fb.p);
   if (tokens) {
@@ -1416,7 +1564,8 @@ eqx_status eqx_feedback(eqx_ctx* ctx, const int64_t* tokens, const eqx_completio
       f.pend_ufc = static_cast<const double*>(put(done->pending_ufc, 8 * nn));
       f.pend_rfc = static_cast<const double*>(put(done->pending_rfc, 8 * nn));
       f.pend_vtc = static_cast<const double*>(put(done->pending_vtc, 8 * nn));
-      if (!f.client || !f.in_tok || !f.out_tok || !f.latency_s || !f.tps || !f.util || !f.pend_ufc || !f.pend_rfc)
+      if (!f.client || !f.in_tok || !f.out_tok || !f.latency_s || !f.tps || !f.util || !f.pend_ufc || !f.pend_rfc ||
+          (done->pending_vtc && !f.pend_vtc))
         return fail(ctx, EQX_ERR_CUDA, "eqx_feedback: completion upload failed");
     }
     if (!f.pend_vtc) {  // only VTC with predictions reads it
@@ -1638,8 +1787,12 @@ eqx_status eqx_step_collect(eqx_ctx* ctx, eqx_step_summary* out) {
     out->noisy_near_ties = static_cast<int64_t>(h.near_ties - ctx->last_near_ties);
     out->batch_members = h.members;
     out->batch_reserved_kv_tokens = h.reserved;
-    // cold-step accounting: one drain, one step
-    out->queued = (ctx->shard_W > 0 ? h.n_queued : ctx->n) - h.n_events;
+    if (ctx->shard_W > 0) {
+      out->queued = h.n_queued - h.n_events;
+    } else {
+      ctx->popped += h.n_events;
+      out->queued = ctx->n - ctx->popped;
+    }
     out->window_underflow = ctx->shard_W > 0 ? h.underflow : 0;
   }
   ctx->last_fallbacks = h.fallbacks;

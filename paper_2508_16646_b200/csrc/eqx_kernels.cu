@@ -57,6 +57,21 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+// ufc/rfc increments of a queued request from its frozen prediction record (live queues).
+__device__ __forceinline__ Scored score_frozen(const Frozen& F, int64_t row, const Policy& P, double now, int32_t in,
+                                              double arrival, double w) {
+  Scored s;
+  s.fallback = 0;
+  s.near_tie = 0;
+  s.pred = F.pred[row];
+  s.bucket = F.bucket[row];
+  const double tokens = __dadd_rn(static_cast<double>(in), __dmul_rn(P.ow, static_cast<double>(s.pred)));
+  const double denom = __dadd_rn(1.0, __dmul_rn(P.delta, __dadd_rn(__dsub_rn(now, arrival), F.pred_s[row])));
+  s.ufc_inc = __ddiv_rn(__dmul_rn(w, tokens), denom);  // scheduler.cpp:21-26
+  s.rfc_inc = F.rfc[row];
+  return s;
+}
+
 // Programmatic dependent launch (sm_90+): wait for the predecessor grid's results / let the
 // successor grid get scheduled early.  No-ops for kernels launched without the attribute.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
@@ -548,8 +563,24 @@ __device__ __forceinline__ void score_body(const ScoreArgs& a, const ModelTables
   }
 }
 
+// Live queue: increments at `now` from the frozen prediction records.
+__device__ __forceinline__ void score_frozen_body(const ScoreArgs& a) {
+  for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < a.n;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const Scored s = score_frozen(a.frozen, r, a.pol, a.now, a.in_tok[r], a.arrival[r], __ldg(a.weight + a.client[r]));
+    a.pred_out[r] = s.pred;
+    a.bucket_out[r] = static_cast<uint8_t>(s.bucket);
+    a.ufc_out[r] = s.ufc_inc;
+    a.rfc_out[r] = s.rfc_inc;
+  }
+}
+
 __global__ void __launch_bounds__(kScoreThreads, 4) score_kernel(const ScoreArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
+  if (a.frozen.pred) {
+    score_frozen_body(a);
+    return;
+  }
   stage_model(a.model, a.model_words, smem);
   __syncthreads();
   const ModelTables& M = *reinterpret_cast<const ModelTables*>(smem);
@@ -826,7 +857,9 @@ __device__ __forceinline__ WinEntry make_entry(const A& a, const ModelTables& M,
   const int64_t id = a.id ? a.id[row] : a.id_base + row;
   const double arr = a.arrival[row];
   const int32_t in = a.in_tok[row];
-  const Scored s = score_request(M, a.pol, a.now, in, a.tag[row], a.true_out ? a.true_out[row] : 1, id, arr, w);
+  const Scored s = a.frozen.pred ? score_frozen(a.frozen, row, a.pol, a.now, in, arr, w)
+                                 : score_request(M, a.pol, a.now, in, a.tag[row], a.true_out ? a.true_out[row] : 1,
+                                                 id, arr, w);
   WinEntry e;
   e.ufc_inc = s.ufc_inc;
   e.rfc_inc = s.rfc_inc;
@@ -2600,6 +2633,86 @@ __global__ void pack_cols_kernel(const PackCols p) {
     } else {
       for (int64_t i = tid; i < b; i += nt) dst[i] = src[i];
     }
+  }
+}
+
+// =================================== live queues ==========================================
+// arrivals are appended to the requests still queued.  The new column
+// store holds the remaining rows client-grouped in FIFO order (straight from perm/head) followed
+// by the arrivals in arrival order, so a drain over it rebuilds every client's FIFO (old rows
+// first) and the counter lift sees the remaining counts as drain_arrivals' non-empty queues.
+__global__ void __launch_bounds__(1024) live_offsets_kernel(const LiveArgs a) {
+  __shared__ uint32_t warp_buf[32];
+  const int per = (a.C + blockDim.x - 1) / blockDim.x;
+  const int c0 = min(a.C, per * static_cast<int>(threadIdx.x)), c1 = min(a.C, c0 + per);
+  uint32_t s = 0;
+  for (int c = c0; c < c1; ++c) s += static_cast<uint32_t>(a.count[c] - a.head[c]);
+  uint32_t run;
+  const uint32_t total = block_exclusive_scan(s, &run, warp_buf);
+  for (int c = c0; c < c1; ++c) {
+    const int32_t rem = a.count[c] - a.head[c];
+    a.live_off[c] = static_cast<int32_t>(run);
+    a.qlen_before[c] = rem;
+    run += static_cast<uint32_t>(rem);
+  }
+  if (threadIdx.x == 0) {
+    a.live_off[a.C] = static_cast<int32_t>(total);
+    *a.n_live = total;
+  }
+}
+
+__global__ void __launch_bounds__(256) gather_live_kernel(const LiveArgs a) {
+  const int64_t n = a.live_off[a.C];
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int32_t lo = 0, hi = a.C;  // client: last c with live_off[c] <= i
+    while (hi - lo > 1) {
+      const int32_t mid = (lo + hi) >> 1;
+      if (a.live_off[mid] <= i) lo = mid;
+      else hi = mid;
+    }
+    const int32_t c = lo;
+    const int64_t row = a.perm[a.seg_off[c] + a.head[c] + (i - a.live_off[c])];
+    a.n_client[i] = a.o_client[row];
+    a.n_arrival[i] = a.o_arrival[row];
+    a.n_in[i] = a.o_in[row];
+    a.n_tag[i] = a.o_tag[row];
+    if (a.n_true) a.n_true[i] = a.o_true ? a.o_true[row] : 1;
+    a.n_id[i] = a.o_id[row];
+    a.n_pred[i] = a.o_pred[row];
+    a.n_bucket[i] = a.o_bucket[row];
+    a.n_preds[i] = a.o_preds[row];
+    a.n_rfc[i] = a.o_rfc[row];
+  }
+}
+
+__global__ void __launch_bounds__(256) predict_rows_kernel(const ScoreArgs a, int64_t r0, int64_t r1,
+                                                           const LiveArgs L, int32_t fill_id) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  stage_model(a.model, a.model_words, smem);
+  __syncthreads();
+  const ModelTables& M = *reinterpret_cast<const ModelTables*>(smem);
+  uint32_t fb = 0, nt = 0;
+  for (int64_t r = r0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < r1;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (fill_id) L.n_id[r] = a.id_base + (r - r0);
+    const int32_t c = L.n_client[r];
+    if (static_cast<uint32_t>(c) >= static_cast<uint32_t>(L.C)) continue;  // the drain flags it
+    const double w = a.weight[c];
+    // the prediction record of map_metrics at arrival (now / arrival do not enter it)
+    const Scored s = score_request(M, a.pol, 0.0, L.n_in[r], L.n_tag[r], L.n_true ? L.n_true[r] : 1, L.n_id[r], 0.0, w);
+    L.n_pred[r] = s.pred;
+    L.n_bucket[r] = static_cast<uint8_t>(s.bucket);
+    L.n_preds[r] = M.prof_pred_s[s.bucket];
+    L.n_rfc[r] = s.rfc_inc;
+    fb += s.fallback;
+    nt += s.near_tie;
+  }
+  fb = __reduce_add_sync(0xffffffffu, fb);
+  nt = __reduce_add_sync(0xffffffffu, nt);
+  if ((threadIdx.x & 31) == 0) {
+    if (fb) atomicAdd(&a.st->fallbacks, static_cast<unsigned long long>(fb));
+    if (nt) atomicAdd(&a.st->near_ties, static_cast<unsigned long long>(nt));
   }
 }
 

@@ -17,6 +17,16 @@ constexpr int kScoreStages = 3;                              // tiles in flight 
 constexpr int kScoreStageBytes = kScoreTile * (4 + 8 + 4 + 1 + 4);  // columns (+ true_out)
 constexpr int kSelectMaxThreads = 256;
 
+// Prediction records frozen when a request joined a live queue (drain_arrivals stores
+// map_metrics' PredictionRecord with the request, engine.cpp:178-180): later update_map EMA
+// steps do not change them.  pred == nullptr: no live queue (predict at step time).
+struct Frozen {
+  const int32_t* pred;    // predicted output tokens (after the engine's max(1, .))
+  const uint8_t* bucket;  // profile entry
+  const double* pred_s;   // predicted_latency_ms / 1000.0 (scheduler.cpp:23)
+  const double* rfc;      // rfc_increment(prediction, weight) = (w * tps) * util
+};
+
 // One head-of-queue entry as the selection loop consumes it (40 B, shared memory).
 struct WinEntry {
   double ufc_inc;
@@ -63,6 +73,7 @@ struct DrainArgs {
 };
 
 struct ScoreArgs {
+  Frozen frozen;         // live queue: frozen prediction records (see Frozen)
   int64_t n;
   const int32_t* client;
   const double* arrival;
@@ -94,6 +105,7 @@ struct ScoreArgs {
 // Head windows: the first W queued entries of every client, scored once per step by many
 // CTAs (window_kernel) and bulk-loaded into the selection CTA's shared memory.
 struct WindowArgs {
+  Frozen frozen;         // live queue: frozen prediction records (see Frozen)
   const double* arrival;
   const int32_t* in_tok;
   const int32_t* true_out;
@@ -116,6 +128,7 @@ struct WindowArgs {
 };
 
 struct SelectArgs {
+  Frozen frozen;         // live queue: frozen prediction records (see Frozen)
   // queue columns (head entries are scored in-kernel with the same device function)
   const int32_t* client;
   const double* arrival;
@@ -283,6 +296,30 @@ struct PackCols {
   int32_t n;
 };
 __global__ void pack_cols_kernel(PackCols p);
+
+// ---- live queues: append arrivals to the remaining queue ------------
+struct LiveArgs {
+  // remaining rows of the current queue, per client FIFO through perm/seg_off/head/count
+  const uint32_t* perm;
+  const int32_t* seg_off;
+  const int32_t* count;
+  const int32_t* head;
+  int32_t C;
+  int32_t* live_off;      // [C+1] exclusive scan of the remaining counts
+  int32_t* qlen_before;   // [C] remaining count (drain_arrivals' "queue non-empty")
+  int64_t* n_live;        // total remaining
+  // old columns -> new columns (client-grouped remaining rows first)
+  const int32_t* o_client; const double* o_arrival; const int32_t* o_in; const uint8_t* o_tag;
+  const int32_t* o_true; const int64_t* o_id;
+  const int32_t* o_pred; const uint8_t* o_bucket; const double* o_preds; const double* o_rfc;
+  int32_t* n_client; double* n_arrival; int32_t* n_in; uint8_t* n_tag; int32_t* n_true; int64_t* n_id;
+  int32_t* n_pred; uint8_t* n_bucket; double* n_preds; double* n_rfc;
+};
+__global__ void live_offsets_kernel(LiveArgs a);
+__global__ void gather_live_kernel(LiveArgs a);
+// Prediction records of rows [r0, r1) of the new columns (drain_arrivals' predict + map_metrics
+// against the current profile); ids default to id_base + (row - r0) when `fill_id`.
+__global__ void predict_rows_kernel(ScoreArgs a, int64_t r0, int64_t r1, LiveArgs L, int32_t fill_id);
 
 __global__ void drain_hist_kernel(DrainArgs a);
 __global__ void lift_kernel(DrainArgs a);

@@ -406,6 +406,15 @@ class GpuScheduler:
         rq = self._requests(client, arrival_s, input_tokens, tag, true_output_tokens, ids, id_base)
         self._check(self._lib.eqx_drain(self._ctx, C.byref(rq)))
 
+    def append(self, client, arrival_s, input_tokens, tag=None, true_output_tokens=None, ids=None,
+               id_base: int = 0) -> None:
+        """drain_arrivals for a batch that joins the requests still queued (live queue): the
+        arrivals' prediction records are frozen against the current profile; step() then
+        schedules from the whole live queue."""
+        keep: list = []
+        rq = self._requests(client, arrival_s, input_tokens, tag, true_output_tokens, ids, id_base, keep)
+        self._check(self._lib.eqx_append(self._ctx, C.byref(rq)))
+
     def stage_async(self, client, arrival_s, input_tokens, tag=None, true_output_tokens=None, ids=None,
                     id_base: int = 0) -> None:
         """Prefetch a host batch (pinned numpy/torch CPU columns) into the context's next staging
