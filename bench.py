@@ -188,12 +188,20 @@ def run_sharded(args, rank, world):
     from paper_2508_16646_b200 import scheduler as S
     from paper_2508_16646_b200.sharded import ShardedScheduler
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # EQX_BENCH_SAME_DEVICE=1 + EQX_BENCH_BACKEND=gloo: every rank on cuda:0 with a CPU-staged
+    # exchange, to exercise the multi-rank path on a one-GPU box (never for reported numbers)
+    if os.environ.get("EQX_BENCH_SAME_DEVICE") == "1":
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("EQX_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     cfg = "cfg4" if args.config == "cfg4" else "cfg2"
     q, led, names, c_r, perf, model, prof, desc = shard_inputs(cfg, rank, world)
     n = len(q["client"])

@@ -1005,7 +1005,7 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl, int32_t g
                                                   (static_cast<uint32_t>(e < 0 ? 1 : 0) << 24);
         }
       }
-      if (ok) ctx->direct_n = dn;
+      if (ok && !std::getenv("EQX_NO_DIRECT")) ctx->direct_n = dn;  // EQX_NO_DIRECT: experiments
     } else if (M.pred_kind == kPredOracle) {
       const int dn = 8192;
       tab.resize(dn);

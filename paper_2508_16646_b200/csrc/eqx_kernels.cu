@@ -512,13 +512,31 @@ __device__ __forceinline__ void score_body(const ScoreArgs& a, const ModelTables
   constexpr bool oracle_like = KIND == kPredOracle || KIND == kPredNoisy;
   const int64_t nvec = a.vec_ok ? n / 4 : 0;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t v = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < nvec; v += stride) {
-    const int4 cl = ldg_stream(reinterpret_cast<const int4*>(a.client) + v);
-    const int4 in4 = ldg_stream(reinterpret_cast<const int4*>(a.in_tok) + v);
-    const double2 a01 = ldg_stream(reinterpret_cast<const double2*>(a.arrival) + 2 * v);
-    const double2 a23 = ldg_stream(reinterpret_cast<const double2*>(a.arrival) + 2 * v + 1);
-    const uint32_t tg = ldg_stream(reinterpret_cast<const uint32_t*>(a.tag) + v);
-    const int4 to = oracle_like ? ldg_stream(reinterpret_cast<const int4*>(a.true_out) + v) : make_int4(1, 1, 1, 1);
+  // software-pipelined: the next vector's loads are in flight while this one is scored
+  struct Vec {
+    int4 cl, in4, to;
+    double2 a01, a23;
+    uint32_t tg;
+  };
+  auto load = [&](int64_t v) {
+    Vec x;
+    x.cl = ldg_stream(reinterpret_cast<const int4*>(a.client) + v);
+    x.in4 = ldg_stream(reinterpret_cast<const int4*>(a.in_tok) + v);
+    x.a01 = ldg_stream(reinterpret_cast<const double2*>(a.arrival) + 2 * v);
+    x.a23 = ldg_stream(reinterpret_cast<const double2*>(a.arrival) + 2 * v + 1);
+    x.tg = ldg_stream(reinterpret_cast<const uint32_t*>(a.tag) + v);
+    x.to = oracle_like ? ldg_stream(reinterpret_cast<const int4*>(a.true_out) + v) : make_int4(1, 1, 1, 1);
+    return x;
+  };
+  int64_t v = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  Vec nx{};
+  if (v < nvec) nx = load(v);
+  for (; v < nvec; v += stride) {
+    const Vec x = nx;
+    if (v + stride < nvec) nx = load(v + stride);
+    const int4 cl = x.cl, in4 = x.in4, to = x.to;
+    const double2 a01 = x.a01, a23 = x.a23;
+    const uint32_t tg = x.tg;
     const int64_t r0 = 4 * v;
     const int cs[4] = {cl.x, cl.y, cl.z, cl.w};
     const int ins[4] = {in4.x, in4.y, in4.z, in4.w};

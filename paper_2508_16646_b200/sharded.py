@@ -124,6 +124,10 @@ def all_gather_records(send, world: int, group=None):
     recv = torch.empty(world * send.numel(), dtype=send.dtype, device=send.device)
     if world == 1:
         recv.copy_(send)
+    elif send.is_cuda and dist.get_backend(group) == "gloo":  # CPU-staged (single-GPU tests)
+        host = torch.empty(world * send.numel(), dtype=send.dtype)
+        dist.all_gather_into_tensor(host, send.cpu(), group=group)
+        recv.copy_(host)
     else:
         dist.all_gather_into_tensor(recv, send, group=group)
     return recv
