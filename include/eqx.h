@@ -195,6 +195,43 @@ eqx_status eqx_step_collect(eqx_ctx* ctx, eqx_step_summary* out);
 /* Convenience: eqx_step_async + eqx_step_collect. */
 eqx_status eqx_step(eqx_ctx* ctx, double now, eqx_step_summary* out);
 
+/* ---- batched engine replays (config 5, the alpha sweep) ---------------
+ * run_simulation (engine.cpp:119-146) for many independent traces at once, one replay per
+ * GPU thread, with the context's policy / perf / timing / profile / predictor / roster and a
+ * per-replay EquinoxParams::alpha.  Each replay starts from zero ledgers (engine.cpp:148-157)
+ * and its own copy of the profile; prediction_overhead_ms is 0 (EngineConfig default). */
+typedef struct {
+  int32_t n_replays;
+  const int64_t* row_off;            /* [n_replays + 1], row_off[0] = 0: rows of replay r */
+  const int32_t* client;             /* concatenated traces, each in arrival order */
+  const double* arrival_s;
+  const int32_t* input_tokens;
+  const int32_t* true_output_tokens;
+  const uint8_t* tag;                /* may be NULL (untagged) */
+  const int64_t* id;                 /* may be NULL: trace positions within each replay */
+  const double* alpha;               /* [n_replays] */
+  double max_sim_time_s;             /* <= 0: each trace's last arrival */
+  double ema_alpha;                  /* EngineConfig::ema_alpha (update_map) */
+  int64_t ev_cap;                    /* admitted / rejected events kept per replay */
+} eqx_replays;
+
+typedef struct {                     /* host arrays; any may be NULL */
+  int64_t* n_events;                 /* [n_replays] (may exceed ev_cap) */
+  int64_t* ev_id;                    /* [n_replays][ev_cap] */
+  int32_t* ev_kind;                  /* EQX_EV_* */
+  double* ev_time;                   /* LogEntry::time_s */
+  double *ufc, *rfc, *counter;       /* [n_replays][C] SimResult::final_clients */
+  int64_t* completed;                /* SimResult::completed */
+  double* sim_end;                   /* SimResult::sim_end_s */
+  int64_t* counter_clamps;
+  int32_t* status;                   /* 0 ok; 2: KV memory bound violated (EngineError) */
+} eqx_replay_out;
+
+/* PerfParams timing fields (gpu_model.hpp:14-28) used by replays. */
+eqx_status eqx_set_timing(eqx_ctx* ctx, double prefill_linear_ms, double prefill_quad_ms, double decode_base_ms,
+                          double decode_per_ctx_ms, double refresh_ms);
+eqx_status eqx_replay(eqx_ctx* ctx, const eqx_replays* replays, eqx_replay_out* out);
+
 /* ---- live queues ------------------------------------------------------
  * drain_arrivals (engine.cpp:171-197) for a batch of arrivals that joins the requests still
  * queued (unlike eqx_drain, which replaces the queue): each arrival's prediction record is made

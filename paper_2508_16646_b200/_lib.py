@@ -69,6 +69,19 @@ class Completions(C.Structure):
                 ("pending_vtc", C.c_void_p), ("location", C.c_int32)]
 
 
+class Replays(C.Structure):
+    _fields_ = [("n_replays", C.c_int32), ("row_off", C.c_void_p), ("client", C.c_void_p),
+                ("arrival_s", C.c_void_p), ("input_tokens", C.c_void_p), ("true_output_tokens", C.c_void_p),
+                ("tag", C.c_void_p), ("id", C.c_void_p), ("alpha", C.c_void_p), ("max_sim_time_s", C.c_double),
+                ("ema_alpha", C.c_double), ("ev_cap", C.c_int64)]
+
+
+class ReplayOut(C.Structure):
+    _fields_ = [("n_events", C.c_void_p), ("ev_id", C.c_void_p), ("ev_kind", C.c_void_p), ("ev_time", C.c_void_p),
+                ("ufc", C.c_void_p), ("rfc", C.c_void_p), ("counter", C.c_void_p), ("completed", C.c_void_p),
+                ("sim_end", C.c_void_p), ("counter_clamps", C.c_void_p), ("status", C.c_void_p)]
+
+
 _SIGS = {
     "eqx_abi_version": ([], C.c_int32),
     "eqx_ctx_create": ([C.c_int32, C.POINTER(C.c_void_p)], C.c_int),
@@ -82,6 +95,8 @@ _SIGS = {
     "eqx_shard_select_async": ([C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, _i32p, C.c_int32, C.c_int32,
                                 C.c_double], C.c_int),
     "eqx_feedback": ([C.c_void_p, _i64p, C.POINTER(Completions), C.c_double], C.c_int),
+    "eqx_set_timing": ([C.c_void_p, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double], C.c_int),
+    "eqx_replay": ([C.c_void_p, C.POINTER(Replays), C.POINTER(ReplayOut)], C.c_int),
     "eqx_get_service": ([C.c_void_p, C.c_int32, _dp, _i64p], C.c_int),
     "eqx_set_service": ([C.c_void_p, C.c_int32, _dp], C.c_int),
     "eqx_get_profile": ([C.c_void_p, C.c_int32, _dp, _dp, _dp], C.c_int),

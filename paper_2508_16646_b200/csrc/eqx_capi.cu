@@ -140,6 +140,9 @@ struct eqx_ctx {
   // client-sharded step (selection context): gathered windows and their ids
   DevBuf d_first64, d_gid;
   DevBuf d_service;                // ClientState::accumulated_service
+  // engine timing (PerfParams, gpu_model.hpp:14-28) for replays
+  double prefill_linear_ms = 0.05, prefill_quad_ms = 1e-6, decode_base_ms = 5.0, decode_per_ctx_ms = 0.002,
+         refresh_ms = 15.0;
   // live queue (eqx_append): two column stores with frozen prediction records, swapped per append
   struct Live {
     DevBuf client, arrival, in, tag, tru, id, pred, bucket, preds, rfc;
@@ -1377,6 +1380,147 @@ eqx_status eqx_drain_step_async(eqx_ctx* ctx, const eqx_requests* r, double now)
   ctx->step_pending = true;
   ctx->stepped = true;
   return EQX_OK;
+}
+
+// ---- batched engine replays -------------------------------------------
+eqx_status eqx_set_timing(eqx_ctx* ctx, double prefill_linear_ms, double prefill_quad_ms, double decode_base_ms,
+                          double decode_per_ctx_ms, double refresh_ms) {
+  if (!ctx) return fail(ctx, EQX_ERR_ARG, "eqx_set_timing: NULL context");
+  // PerfParams::validate (gpu_model.cpp:9-24)
+  if (prefill_linear_ms < 0.0 || prefill_quad_ms < 0.0 || decode_base_ms < 0.0 || decode_per_ctx_ms < 0.0 ||
+      refresh_ms < 0.0)
+    return fail(ctx, EQX_ERR_CONFIG, "perf timing parameters must be >= 0");
+  ctx->prefill_linear_ms = prefill_linear_ms;
+  ctx->prefill_quad_ms = prefill_quad_ms;
+  ctx->decode_base_ms = decode_base_ms;
+  ctx->decode_per_ctx_ms = decode_per_ctx_ms;
+  ctx->refresh_ms = refresh_ms;
+  return EQX_OK;
+}
+
+eqx_status eqx_replay(eqx_ctx* ctx, const eqx_replays* R, eqx_replay_out* O) {
+  if (!ctx || !R || !O) return fail(ctx, EQX_ERR_ARG, "eqx_replay: NULL argument");
+  if (!ctx->policy_set || !ctx->model_set || !ctx->profile_set)
+    return fail(ctx, EQX_ERR_CONFIG, "eqx_replay: policy, predictor and GPU profile must be set first");
+  const int32_t nr = R->n_replays, C = ctx->C;
+  if (nr < 0 || !R->row_off || (nr > 0 && (!R->alpha || !R->client || !R->arrival_s || !R->input_tokens ||
+                                           !R->true_output_tokens)))
+    return fail(ctx, EQX_ERR_ARG, "eqx_replay: missing replay columns");
+  if (C < 1 || C > 64) return fail(ctx, EQX_ERR_CONFIG, "eqx_replay: rosters of 1..64 clients");
+  if (R->ema_alpha <= 0.0 || R->ema_alpha > 1.0) return fail(ctx, EQX_ERR_CONFIG, "ema_alpha must lie in (0, 1]");
+  for (int32_t i = 0; i < nr; ++i) {
+    if (R->alpha[i] < 0.0 || R->alpha[i] > 1.0) return fail(ctx, EQX_ERR_CONFIG, "alpha must lie in [0, 1]");
+    if (R->row_off[i + 1] < R->row_off[i]) return fail(ctx, EQX_ERR_ARG, "eqx_replay: row offsets must be ordered");
+  }
+  if (nr == 0) return EQX_OK;
+  const int64_t rows = R->row_off[nr] - R->row_off[0];
+  if (R->row_off[0] != 0) return fail(ctx, EQX_ERR_ARG, "eqx_replay: row_off[0] must be 0");
+  for (int64_t i = 0; i < rows; ++i)
+    if (R->client[i] < 0 || R->client[i] >= C) return fail(ctx, EQX_ERR_CONFIG, "request references unknown client");
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = ctx->stream;
+  if (ctx->model_dirty) {  // upload the compiled model tables
+    StepPlan pl;
+    const bool qr = ctx->queue_ready;
+    const int64_t n0 = ctx->n;
+    ctx->queue_ready = true;
+    eqx_status st = step_prepare(ctx, 0.0, pl);
+    ctx->queue_ready = qr;
+    ctx->n = n0;
+    if (st != EQX_OK) return st;
+  }
+  const int64_t cap = std::max<int64_t>(R->ev_cap, 1);
+  const size_t rr = static_cast<size_t>(std::max<int64_t>(rows, 1)), n8 = static_cast<size_t>(nr);
+  // one device block: inputs | scratch | outputs
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off += (bytes + 15) & ~size_t(15);
+    return o;
+  };
+  const size_t o_off = take(8 * (n8 + 1)), o_client = take(4 * rr), o_arr = take(8 * rr), o_in = take(4 * rr),
+               o_true = take(4 * rr), o_tag = take(rr), o_id = take(8 * rr), o_alpha = take(8 * n8),
+               o_crow = take(4 * rr), o_fpred = take(4 * rr), o_fpreds = take(8 * rr), o_frfc = take(8 * rr),
+               o_cl = take(sizeof(ReplayClient) * n8 * C), o_mb = take(sizeof(ReplayMember) * n8 * ctx->perf.max_batch),
+               o_prof = take(8 * n8 * 4 * kMaxProfile), o_evid = take(8 * n8 * cap), o_evk = take(4 * n8 * cap),
+               o_evt = take(8 * n8 * cap), o_nev = take(8 * n8), o_comp = take(8 * n8), o_end = take(8 * n8),
+               o_clamp = take(8 * n8), o_stat = take(4 * n8), o_u = take(8 * n8 * C), o_r = take(8 * n8 * C),
+               o_k = take(8 * n8 * C);
+  CUDA_TRY(ctx, ctx->d_fb.ensure(off));
+  char* b = static_cast<char*>(ctx->d_fb.p);
+  auto up = [&](size_t o, const void* src, size_t bytes) {
+    return src ? cudaMemcpyAsync(b + o, src, bytes, cudaMemcpyHostToDevice, s) : cudaMemsetAsync(b + o, 0, bytes, s);
+  };
+  CUDA_TRY(ctx, up(o_off, R->row_off, 8 * (n8 + 1)));
+  CUDA_TRY(ctx, up(o_client, R->client, 4 * rows));
+  CUDA_TRY(ctx, up(o_arr, R->arrival_s, 8 * rows));
+  CUDA_TRY(ctx, up(o_in, R->input_tokens, 4 * rows));
+  CUDA_TRY(ctx, up(o_true, R->true_output_tokens, 4 * rows));
+  CUDA_TRY(ctx, up(o_tag, R->tag, rows));
+  CUDA_TRY(ctx, up(o_alpha, R->alpha, 8 * n8));
+  std::vector<int64_t> ids;
+  if (!R->id) {  // trace positions within each replay
+    ids.resize(rr);
+    for (int32_t i = 0; i < nr; ++i)
+      for (int64_t k = R->row_off[i]; k < R->row_off[i + 1]; ++k) ids[k] = k - R->row_off[i];
+  }
+  CUDA_TRY(ctx, up(o_id, R->id ? static_cast<const void*>(R->id) : ids.data(), 8 * rows));
+  ReplayArgs A;
+  std::memset(&A, 0, sizeof(A));
+  A.n_replays = nr;
+  A.C = C;
+  A.row_off = reinterpret_cast<const int64_t*>(b + o_off);
+  A.client = reinterpret_cast<const int32_t*>(b + o_client);
+  A.arrival = reinterpret_cast<const double*>(b + o_arr);
+  A.in_tok = reinterpret_cast<const int32_t*>(b + o_in);
+  A.true_out = reinterpret_cast<const int32_t*>(b + o_true);
+  A.tag = reinterpret_cast<const uint8_t*>(b + o_tag);
+  A.id = reinterpret_cast<const int64_t*>(b + o_id);
+  A.alpha = reinterpret_cast<const double*>(b + o_alpha);
+  A.weight = ctx->d_weight.as<double>();
+  A.order = ctx->d_order.as<uint32_t>();
+  A.model = ctx->d_model.as<ModelTables>();
+  A.pol = ctx->pol;
+  A.counter_lift = ctx->counter_lift;
+  A.max_sim_time_s = R->max_sim_time_s;
+  A.ema_alpha = R->ema_alpha;
+  A.prefill_linear_ms = ctx->prefill_linear_ms;
+  A.prefill_quad_ms = ctx->prefill_quad_ms;
+  A.decode_base_ms = ctx->decode_base_ms;
+  A.decode_per_ctx_ms = ctx->decode_per_ctx_ms;
+  A.refresh_ms = ctx->refresh_ms;
+  A.crow = reinterpret_cast<int32_t*>(b + o_crow);
+  A.f_pred = reinterpret_cast<int32_t*>(b + o_fpred);
+  A.f_preds = reinterpret_cast<double*>(b + o_fpreds);
+  A.f_rfc = reinterpret_cast<double*>(b + o_frfc);
+  A.cl = reinterpret_cast<ReplayClient*>(b + o_cl);
+  A.mb = reinterpret_cast<ReplayMember*>(b + o_mb);
+  A.prof = reinterpret_cast<double*>(b + o_prof);
+  A.ev_cap = cap;
+  A.ev_id = reinterpret_cast<int64_t*>(b + o_evid);
+  A.ev_kind = reinterpret_cast<int32_t*>(b + o_evk);
+  A.ev_time = reinterpret_cast<double*>(b + o_evt);
+  A.n_events = reinterpret_cast<int64_t*>(b + o_nev);
+  A.completed = reinterpret_cast<int64_t*>(b + o_comp);
+  A.sim_end = reinterpret_cast<double*>(b + o_end);
+  A.clamps = reinterpret_cast<int64_t*>(b + o_clamp);
+  A.status = reinterpret_cast<int32_t*>(b + o_stat);
+  A.out_ufc = reinterpret_cast<double*>(b + o_u);
+  A.out_rfc = reinterpret_cast<double*>(b + o_r);
+  A.out_counter = reinterpret_cast<double*>(b + o_k);
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[2], s));
+  replay_kernel<<<(nr + 63) / 64, 64, 0, s>>>(A);
+  CUDA_TRY(ctx, cudaGetLastError());
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[3], s));
+  const Col cols[] = {{O->n_events, b + o_nev, 8 * n8},       {O->ev_id, b + o_evid, 8 * n8 * cap},
+                      {O->ev_kind, b + o_evk, 4 * n8 * cap},    {O->ev_time, b + o_evt, 8 * n8 * cap},
+                      {O->ufc, b + o_u, 8 * n8 * C},           {O->rfc, b + o_r, 8 * n8 * C},
+                      {O->counter, b + o_k, 8 * n8 * C},       {O->completed, b + o_comp, 8 * n8}};
+  eqx_status st = read_cols(ctx, cols, 8);
+  if (st != EQX_OK) return st;
+  const Col cols2[] = {{O->sim_end, b + o_end, 8 * n8}, {O->counter_clamps, b + o_clamp, 8 * n8},
+                       {O->status, b + o_stat, 4 * n8}};
+  return read_cols(ctx, cols2, 3);
 }
 
 // ---- live queues -----------------------------------------------------

@@ -321,6 +321,60 @@ __global__ void gather_live_kernel(LiveArgs a);
 // against the current profile); ids default to id_base + (row - r0) when `fill_id`.
 __global__ void predict_rows_kernel(ScoreArgs a, int64_t r0, int64_t r1, LiveArgs L, int32_t fill_id);
 
+// ---- batched engine replays (eqx_replay.cu) ---------------------------
+struct ReplayClient {
+  double ufc, rfc, counter, weight;
+  int32_t running, backlogged;
+  uint32_t order;            // rank of client_id (select_next tie-break)
+  int32_t qbase, qhead, qend;  // FIFO over the client's rows: [qhead, qend) of crow
+};
+struct ReplayMember {
+  int32_t row, client, in, generated, reserved_out, pad;
+  double admit_s, busy_at, ovh_at;
+  double p_ufc, p_rfc, p_vtc;  // PendingContribution
+};
+struct ReplayArgs {
+  int32_t n_replays;
+  int32_t C;
+  const int64_t* row_off;     // [n_replays + 1] into the concatenated traces
+  const int32_t* client;
+  const double* arrival;
+  const int32_t* in_tok;
+  const int32_t* true_out;
+  const uint8_t* tag;
+  const int64_t* id;
+  const double* alpha;        // [n_replays]
+  const double* weight;       // [C]
+  const uint32_t* order;      // [C]
+  const ModelTables* model;
+  Policy pol;
+  int32_t counter_lift;
+  double max_sim_time_s, ema_alpha;
+  double prefill_linear_ms, prefill_quad_ms, decode_base_ms, decode_per_ctx_ms, refresh_ms;
+  // scratch
+  int32_t* crow;
+  int32_t* f_pred;
+  double* f_preds;
+  double* f_rfc;
+  ReplayClient* cl;           // [n_replays][C]
+  ReplayMember* mb;           // [n_replays][max_batch]
+  double* prof;               // [n_replays][4][kMaxProfile]
+  // outputs
+  int64_t ev_cap;             // per replay
+  int64_t* ev_id;
+  int32_t* ev_kind;
+  double* ev_time;
+  int64_t* n_events;
+  int64_t* completed;
+  double* sim_end;
+  int64_t* clamps;
+  int32_t* status;            // 0 ok, 2 KV memory bound violated (EngineError)
+  double* out_ufc;            // [n_replays][C]
+  double* out_rfc;
+  double* out_counter;
+};
+__global__ void replay_kernel(ReplayArgs a);
+
 __global__ void drain_hist_kernel(DrainArgs a);
 __global__ void lift_kernel(DrainArgs a);
 __global__ void event_fill_kernel(EventFillArgs a);

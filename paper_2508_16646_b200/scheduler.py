@@ -484,6 +484,39 @@ class GpuScheduler:
                           int(s.batch_members), int(s.batch_reserved_kv_tokens), int(s.queued),
                           int(s.window_underflow))
 
+    # -- batched engine replays --
+    def replay(self, row_off, client, arrival_s, input_tokens, true_output_tokens, alpha, tag=None, ids=None,
+               max_sim_time_s: float = 0.0, ema_alpha: float = 0.2, ev_cap: int = 4096) -> dict:
+        """run_simulation (engine.cpp:119-146) for many traces at once on the GPU, one replay per
+        thread: traces concatenated (row_off[r]..row_off[r+1]), per-replay alpha, the
+        scheduler's policy / perf / profile / predictor / roster otherwise.  Returns the
+        admitted/rejected event logs (id, kind, time), final ledgers and run statistics."""
+        n = len(alpha)
+        nc = len(self.client_ids)
+        cols = {"row_off": np.ascontiguousarray(row_off, np.int64), "client": np.ascontiguousarray(client, np.int32),
+                "arrival_s": np.ascontiguousarray(arrival_s, np.float64),
+                "input_tokens": np.ascontiguousarray(input_tokens, np.int32),
+                "true_output_tokens": np.ascontiguousarray(true_output_tokens, np.int32),
+                "alpha": np.ascontiguousarray(alpha, np.float64),
+                "tag": None if tag is None else np.ascontiguousarray(tag, np.uint8),
+                "id": None if ids is None else np.ascontiguousarray(ids, np.int64)}
+        ptr = {k: (v.ctypes.data if v is not None else None) for k, v in cols.items()}
+        rq = L.Replays(n, ptr["row_off"], ptr["client"], ptr["arrival_s"], ptr["input_tokens"],
+                       ptr["true_output_tokens"], ptr["tag"], ptr["id"], ptr["alpha"], float(max_sim_time_s),
+                       float(ema_alpha), int(ev_cap))
+        out = {"n_events": np.zeros(n, np.int64), "ev_id": np.zeros((n, ev_cap), np.int64),
+               "ev_kind": np.zeros((n, ev_cap), np.int32), "ev_time": np.zeros((n, ev_cap)),
+               "ufc": np.zeros((n, nc)), "rfc": np.zeros((n, nc)), "counter": np.zeros((n, nc)),
+               "completed": np.zeros(n, np.int64), "sim_end": np.zeros(n), "counter_clamps": np.zeros(n, np.int64),
+               "status": np.zeros(n, np.int32)}
+        ro = L.ReplayOut(*(out[k].ctypes.data for k in ("n_events", "ev_id", "ev_kind", "ev_time", "ufc", "rfc",
+                                                          "counter", "completed", "sim_end", "counter_clamps",
+                                                          "status")))
+        self._check(self._lib.eqx_replay(self._ctx, C.byref(rq), C.byref(ro)))
+        if np.any(out["status"] == 2):
+            raise EngineError("KV memory bound violated in replay(s) " + str(np.nonzero(out["status"] == 2)[0][:8]))
+        return out
+
     # -- completion / feedback (engine.cpp:273-375; SURVEY.md 8f row 1) --
     def feedback(self, tokens=None, completions: dict | None = None, ema_alpha: float = 0.2) -> None:
         """One iteration's feedback in the engine's order: on_tokens(c, tokens[c]) for every

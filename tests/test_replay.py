@@ -1,0 +1,103 @@
+"""Batched engine replays (BASELINE configs[0] and configs[4]).
+
+eqx_replay runs run_simulation (engine.cpp:119-146) for many traces in one launch, one replay
+per GPU thread.  Oracle: the reference's own run_simulation through oracle/_ref (ref_replay),
+replay by replay.  Bit-exact: the admitted / rejected event sequence with its simulated times
+and the final FP64 ledgers.
+"""
+import numpy as np
+import pytest
+
+import harness as H
+from helpers import case_clients, case_kwargs, default_model, default_profile
+from paper_2508_16646_b200 import workload as W
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not H.available("ref"), reason="reference build not present")]
+
+
+def poisson_trace(seed, n_clients=8, rate=400.0, duration=6.0):
+    """cfg1-shaped: Poisson arrivals over n_clients, corpus-mixture lengths (workload.lmsys_queue)."""
+    rng = np.random.default_rng(seed)
+    n = int(rng.poisson(rate * duration))
+    q = W.lmsys_queue(n, n_clients, seed=seed, tag_noise=0.2)
+    q["arrival"] = np.sort(rng.uniform(0.0, duration, n))
+    return q
+
+
+def preset_trace(seed, duration=20.0):
+    """The reference's poisson preset shape (workload.cpp:254-260): client1 16 req/s 512 in /
+    32 out, client2 3 req/s 32 in / 512 out (configs/sweep_alpha.json)."""
+    rng = np.random.default_rng(seed)
+    parts = []
+    for c, (rate, tin, tout) in enumerate(((16.0, 512, 32), (3.0, 32, 512))):
+        t = np.cumsum(rng.exponential(1.0 / rate, int(rate * duration * 2)))
+        t = t[t < duration]
+        parts.append((t, np.full(len(t), c), np.full(len(t), tin), np.full(len(t), tout)))
+    arr = np.concatenate([p[0] for p in parts])
+    order = np.argsort(arr, kind="stable")
+    q = {"arrival": arr[order], "client": np.concatenate([p[1] for p in parts])[order].astype(np.int32),
+         "in_tokens": np.concatenate([p[2] for p in parts])[order].astype(np.int32),
+         "true_out": np.concatenate([p[3] for p in parts])[order].astype(np.int32)}
+    q["tag"] = np.full(len(arr), -1, np.int32)
+    q["client_names"] = ["client1", "client2"]
+    q["tag_names"] = list(W.TAG_NAMES)
+    return q
+
+
+def run_both(traces, alphas, **kw):
+    from paper_2508_16646_b200 import scheduler as S
+    base = dict(model=default_model(), profile=default_profile())
+    base.update(kw)
+    ref = []
+    for q, a in zip(traces, alphas):
+        case = H.StepCase(client=q["client"], arrival=q["arrival"], in_tokens=q["in_tokens"], true_out=q["true_out"],
+                          tag=q["tag"], client_names=q["client_names"], alpha=float(a), **base)
+        ref.append(H.ref_replay(case, max_sim_time_s=0.0, ema_alpha=0.2, cap=1 << 20))
+    case0 = H.StepCase(client=traces[0]["client"], arrival=traces[0]["arrival"], in_tokens=traces[0]["in_tokens"],
+                       true_out=traces[0]["true_out"], tag=traces[0]["tag"], client_names=traces[0]["client_names"],
+                       alpha=float(alphas[0]), **base)
+    sch = S.GpuScheduler(case_clients(case0), running=np.zeros(len(case0.client_names), np.int32), **case_kwargs(case0))
+    row_off = np.concatenate([[0], np.cumsum([len(q["client"]) for q in traces])])
+    cat = {k: np.concatenate([np.asarray(q[k]) for q in traces]) for k in ("client", "arrival", "in_tokens", "true_out")}
+    tag = np.concatenate([np.where(np.asarray(q["tag"]) < 0, 0, np.asarray(q["tag"]) + 1) for q in traces])
+    cap = max(len(r[0]) for r in ref) + 1
+    got = sch.replay(row_off, cat["client"], cat["arrival"], cat["in_tokens"], cat["true_out"], alphas,
+                     tag=tag.astype(np.uint8), ema_alpha=0.2, ev_cap=cap)
+    return ref, got
+
+
+def check(ref, got):
+    for i, (ev_id, ev_kind, ev_time, u, r, c) in enumerate(ref):
+        n = int(got["n_events"][i])
+        assert n == len(ev_id), f"replay {i}: {n} events vs {len(ev_id)}"
+        np.testing.assert_array_equal(got["ev_id"][i, :n], ev_id, err_msg=f"replay {i} ids")
+        np.testing.assert_array_equal(got["ev_kind"][i, :n], ev_kind, err_msg=f"replay {i} kinds")
+        np.testing.assert_array_equal(got["ev_time"][i, :n], ev_time, err_msg=f"replay {i} times")
+        np.testing.assert_array_equal(got["ufc"][i], u, err_msg=f"replay {i} ufc")
+        np.testing.assert_array_equal(got["rfc"][i], r, err_msg=f"replay {i} rfc")
+        np.testing.assert_array_equal(got["counter"][i], c, err_msg=f"replay {i} counter")
+
+
+@pytest.mark.parametrize("pred_kind", [0, 1])
+def test_cfg1_shaped_replays_match_reference(pred_kind):
+    traces = [poisson_trace(s) for s in range(4)]
+    ref, got = run_both(traces, [0.5, 0.6, 0.7, 0.85], pred_kind=pred_kind)
+    check(ref, got)
+    assert all(len(r[0]) > 30 for r in ref), [len(r[0]) for r in ref]
+
+
+@pytest.mark.parametrize("over", [{"kind": 1}, {"kind": 1, "vtc_use_prediction": True}, {"kind": 0},
+                                  {"backfill": True, "max_batch": 8}, {"norm_mode": 1},
+                                  {"mem_per_token_bytes": 1.0, "mem_capacity_bytes": 40000.0}])
+def test_replay_policies_match_reference(over):
+    traces = [poisson_trace(10 + s, rate=300.0, duration=4.0) for s in range(3)]
+    ref, got = run_both(traces, [0.3, 0.7, 1.0], pred_kind=0, **over)
+    check(ref, got)
+
+
+def test_alpha_sweep_preset_replays_match_reference():
+    """configs[4]'s shape: the poisson preset under an alpha grid, many replays in one launch."""
+    alphas = np.repeat(np.arange(0.5, 0.86, 0.05), 4)
+    traces = [preset_trace(100 + i) for i in range(len(alphas))]
+    ref, got = run_both(traces, alphas, pred_kind=0)
+    check(ref, got)
