@@ -307,7 +307,110 @@ def run_sharded(args, rank, world):
         dist.destroy_process_group()
 
 
+def preset_traces(n_replays: int, duration: float, seed0: int = 1):
+    """The reference's poisson preset (workload.cpp:254-260: client1 Poisson 16/s, 512 in / 32
+    out; client2 Poisson 3/s, 32 in / 512 out), one seeded trace per replay, concatenated."""
+    traces = []
+    for i in range(n_replays):
+        rng = np.random.default_rng(seed0 + i)
+        parts = []
+        for c, (rate, tin, tout) in enumerate(((16.0, 512, 32), (3.0, 32, 512))):
+            t = np.cumsum(rng.exponential(1.0 / rate, int(rate * duration * 2) + 16))
+            t = t[t < duration]
+            parts.append((t, np.full(len(t), c, np.int32), np.full(len(t), tin, np.int32),
+                          np.full(len(t), tout, np.int32)))
+        arr = np.concatenate([p[0] for p in parts])
+        o = np.argsort(arr, kind="stable")
+        traces.append({"arrival": arr[o], "client": np.concatenate([p[1] for p in parts])[o],
+                       "in_tokens": np.concatenate([p[2] for p in parts])[o],
+                       "true_out": np.concatenate([p[3] for p in parts])[o]})
+    row_off = np.concatenate([[0], np.cumsum([len(t["client"]) for t in traces])]).astype(np.int64)
+    cat = {k: np.concatenate([t[k] for t in traces]) for k in ("client", "arrival", "in_tokens", "true_out")}
+    return traces, row_off, cat
+
+
+def cfg5_setup(n_seeds: int):
+    alphas = np.round(np.arange(0.5, 0.86, 0.05), 2)              # 8 values
+    alpha = np.tile(alphas, n_seeds)                             # replay r: alpha[r % 8], seed r // 8
+    traces, row_off, cat = preset_traces(len(alpha), 60.0)
+    return alpha, traces, row_off, cat
+
+
+def ref_replay_one(args_):
+    """One reference run_simulation (oracle/_ref) of a preset trace (the reference arm)."""
+    q, a = args_
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import harness as H
+    with open(os.path.join(ROOT, "paper_2508_16646_b200", "data", "profile_default.json")) as f:
+        prof = {k: np.asarray(v) for k, v in json.load(f).items()}
+    case = H.StepCase(client=q["client"], arrival=q["arrival"], in_tokens=q["in_tokens"], true_out=q["true_out"],
+                      tag=np.full(len(q["client"]), -1, np.int32), client_names=["client1", "client2"],
+                      alpha=float(a), pred_kind=0, profile=prof)
+    t0 = time.perf_counter()
+    H.ref_replay(case, max_sim_time_s=0.0, ema_alpha=0.2, cap=1 << 20)
+    return time.perf_counter() - t0
+
+
+def run_cfg5(args, rank, world):
+    """configs[4]: the Holistic-Fairness alpha sweep as 1024 independent engine replays (8 alpha
+    values x 128 seeds of the poisson preset, 60 s each) in one eqx_replay launch per step."""
+    if rank != 0:
+        return
+    alpha, traces, row_off, cat = cfg5_setup(128)
+    n = len(alpha)
+    if args.impl == "reference":
+        import multiprocessing as mp
+        cores = os.cpu_count() or 1
+        sample = min(n, 4 * cores)
+        with mp.Pool(cores) as pool:
+            pool.map(ref_replay_one, [(traces[i], alpha[i]) for i in range(cores)])  # warm
+            t0 = time.perf_counter()
+            pool.map(ref_replay_one, [(traces[i], alpha[i]) for i in range(sample)])
+            dt = time.perf_counter() - t0
+        val = sample / dt
+        print(json.dumps({"impl": "reference", "metric": "engine replays/sec (alpha sweep)", "value": val,
+                          "unit": "replays/s", "n_gpus": world, "higher_is_better": True,
+                          "config": {"workload": "cfg5: 1024 replays = 8 alpha x 128 seeds, poisson preset, 60 s"},
+                          "cpu_baseline": {"value": val, "unit": "replays/s", "cores": cores, "kind": "reference",
+                                           "sample": f"{sample} replays (run_simulation, oracle/_ref) on a {cores}-process pool"},
+                          "e2e": {"value": val, "unit": "replays/s", "h2d_bytes_per_step": 0,
+                                  "d2h_bytes_per_step": 0}}), flush=True)
+        return
+    import torch
+    from paper_2508_16646_b200 import scheduler as S
+    data = os.path.join(ROOT, "paper_2508_16646_b200", "data")
+    prof = S.GpuProfile.load_json(os.path.join(data, "profile_default.json"))
+    sch = S.GpuScheduler([S.ClientState("client1"), S.ClientState("client2")], policy=S.PolicySpec(),
+                         perf=S.PerfParams(), profile=prof, predictor="oracle")
+    cap = 2048
+    times, kms = [], []
+    for i in range(args.warmup + args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        out = sch.replay(row_off, cat["client"], cat["arrival"], cat["in_tokens"], cat["true_out"], alpha,
+                         ema_alpha=0.2, ev_cap=cap)
+        t1 = time.perf_counter()
+        if i >= args.warmup:
+            times.append(t1 - t0)
+            kms.append(sch.kernel_times_ms()["select_kernel"])
+    k = float(np.median(kms))
+    h2d = int(sum(v.nbytes for v in cat.values()) + row_off.nbytes + alpha.nbytes)
+    line = {"metric": "engine replays/sec (alpha sweep)", "value": n / (k * 1e-3), "unit": "replays/s",
+            "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": k, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "cfg5: 1024 replays = 8 alpha x 128 seeds of the poisson preset (60 s), "
+                                   "one replay per GPU thread", "requests": int(row_off[-1]),
+                       "completed": int(out["completed"].sum()), "admissions": int(out["n_events"].sum())},
+            "e2e": {"value": n / float(np.median(times)), "unit": "replays/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": int(sum(v.nbytes for v in out.values())),
+                    "ms_per_step": float(np.median(times)) * 1e3},
+            "gpu_launches": args.steps}
+    print(json.dumps(line), flush=True)
+
+
 def run_ours(args, rank, world):
+    if args.config == "cfg5":
+        return run_cfg5(args, rank, world)
     if world > 1 or args.sharded or args.config == "cfg4":
         return run_sharded(args, rank, world)
     import torch
@@ -494,7 +597,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3", "cfg4"])
+    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--sharded", action="store_true", help="client-sharded pipeline even at N=1")
     ap.add_argument("--cpu-reps", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -503,7 +606,9 @@ def main():
     args.warmup = max(3, args.warmup)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if args.impl == "reference":
+    if args.impl == "reference" and args.config == "cfg5":
+        run_cfg5(args, rank, world)
+    elif args.impl == "reference":
         run_reference(args, rank, world)
     else:
         run_ours(args, rank, world)

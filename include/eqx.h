@@ -314,7 +314,8 @@ eqx_status eqx_copy_scores(eqx_ctx* ctx, int64_t cap, int32_t* pred, uint8_t* bu
 eqx_status eqx_phase_times(eqx_ctx* ctx, double* out_us, int32_t n);
 
 /* Profiling: CUDA-event durations (ms) of the last non-graph step: [0] score_kernel (side
- * stream), [1] select_kernel, [2] drain launched inside eqx_drain_step_async (0 otherwise). */
+ * stream), [1] select_kernel (or the last eqx_replay's replay_kernel), [2] drain launched
+ * inside eqx_drain_step_async; -1 for a pair never recorded. */
 eqx_status eqx_kernel_times(eqx_ctx* ctx, float* out_ms);
 
 /* ---- host scalar utilities (bindings/module.cpp:144-172 `ufc_increment`/`rfc_increment`) - */

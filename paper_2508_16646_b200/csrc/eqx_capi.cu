@@ -1406,7 +1406,7 @@ eqx_status eqx_replay(eqx_ctx* ctx, const eqx_replays* R, eqx_replay_out* O) {
   if (nr < 0 || !R->row_off || (nr > 0 && (!R->alpha || !R->client || !R->arrival_s || !R->input_tokens ||
                                            !R->true_output_tokens)))
     return fail(ctx, EQX_ERR_ARG, "eqx_replay: missing replay columns");
-  if (C < 1 || C > 64) return fail(ctx, EQX_ERR_CONFIG, "eqx_replay: rosters of 1..64 clients");
+  if (C < 1 || C > kMaxReplayClients) return fail(ctx, EQX_ERR_CONFIG, "eqx_replay: rosters of 1..16 clients");
   if (R->ema_alpha <= 0.0 || R->ema_alpha > 1.0) return fail(ctx, EQX_ERR_CONFIG, "ema_alpha must lie in (0, 1]");
   for (int32_t i = 0; i < nr; ++i) {
     if (R->alpha[i] < 0.0 || R->alpha[i] > 1.0) return fail(ctx, EQX_ERR_CONFIG, "alpha must lie in [0, 1]");
@@ -1509,7 +1509,7 @@ eqx_status eqx_replay(eqx_ctx* ctx, const eqx_replays* R, eqx_replay_out* O) {
   A.out_rfc = reinterpret_cast<double*>(b + o_r);
   A.out_counter = reinterpret_cast<double*>(b + o_k);
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[2], s));
-  replay_kernel<<<(nr + 63) / 64, 64, 0, s>>>(A);
+  replay_kernel<<<(nr + 3) / 4, 128, 0, s>>>(A);  // one warp per replay
   CUDA_TRY(ctx, cudaGetLastError());
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[3], s));
   const Col cols[] = {{O->n_events, b + o_nev, 8 * n8},       {O->ev_id, b + o_evid, 8 * n8 * cap},
@@ -1962,9 +1962,10 @@ eqx_status eqx_kernel_times(eqx_ctx* ctx, float* out_ms) {
   if (!ctx || !out_ms) return fail(ctx, EQX_ERR_ARG, "eqx_kernel_times: NULL argument");
   cudaSetDevice(ctx->device);
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-  CUDA_TRY(ctx, cudaEventElapsedTime(&out_ms[0], ctx->ev_k[0], ctx->ev_k[1]));  // score_kernel
-  CUDA_TRY(ctx, cudaEventElapsedTime(&out_ms[1], ctx->ev_k[2], ctx->ev_k[3]));  // select_kernel
-  CUDA_TRY(ctx, cudaEventElapsedTime(&out_ms[2], ctx->ev_k[4], ctx->ev_k[5]));  // drain (in-step)
+  // pairs never recorded (e.g. a replay-only context) read as -1
+  for (int i = 0; i < 3; ++i)
+    if (cudaEventElapsedTime(&out_ms[i], ctx->ev_k[2 * i], ctx->ev_k[2 * i + 1]) != cudaSuccess) out_ms[i] = -1.0f;
+  cudaGetLastError();
   return EQX_OK;
 }
 

@@ -322,6 +322,7 @@ __global__ void gather_live_kernel(LiveArgs a);
 __global__ void predict_rows_kernel(ScoreArgs a, int64_t r0, int64_t r1, LiveArgs L, int32_t fill_id);
 
 // ---- batched engine replays (eqx_replay.cu) ---------------------------
+constexpr int kMaxReplayClients = 16;
 struct ReplayClient {
   double ufc, rfc, counter, weight;
   int32_t running, backlogged;

@@ -1,12 +1,15 @@
 // eqx_replay.cu -- many independent engine replays per launch (SURVEY.md 8f row 3, config 5:
 // the Holistic-Fairness alpha sweep, 1024 replays).
 //
-// One thread runs one whole replay: the reference's SimulationRun::run loop (engine.cpp:
+// One warp runs one whole replay: the reference's SimulationRun::run loop (engine.cpp:
 // 119-146) with drain_arrivals (:171-197), admit_requests (:207-271), run_iteration
 // (:273-325) and complete_finished (:327-375), and the SchedulerPolicy / GpuProfile
 // operations they call, in the reference's order and FP64 operation order.  Replays are
 // independent, so the GPU runs them side by side (148 SMs x many warps); each replay keeps its
 // ledger, profile copy, per-client FIFO cursors and batch in its own slice of global scratch.
+// The scalar engine logic runs uniformly on all 32 lanes (identical values, identical stores:
+// no divergence between replays of a warp, as one-thread-per-replay had), and the loops over
+// batch members (reservations, decode step, completion scan and erase) are split across lanes.
 // Reporting windows (advance_clock's samples) do not change the schedule and are not produced.
 #include <cstdint>
 
@@ -28,9 +31,16 @@ __device__ __forceinline__ bool key_better(double k, double a, uint32_t o, doubl
 
 }  // namespace
 
-__global__ void __launch_bounds__(64) replay_kernel(const ReplayArgs A) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= A.n_replays) return;
+__device__ __forceinline__ int64_t warp_sum64(int64_t v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= A.n_replays) return;  // warp-uniform
   const ModelTables& M = *A.model;
   const Policy P = A.pol;
   const int32_t C = A.C;
@@ -46,9 +56,12 @@ __global__ void __launch_bounds__(64) replay_kernel(const ReplayArgs A) {
   int32_t* f_pred = A.f_pred + t0;                      // frozen prediction records
   double* f_preds = A.f_preds + t0;
   double* f_rfc = A.f_rfc + t0;
-  ReplayClient* cl = A.cl + static_cast<int64_t>(r) * C;
+  // Ledger, FIFO cursors and profile are private per lane (identical copies, updated uniformly),
+  // so the read-modify-write engine steps need no intra-warp synchronisation; the batch lives
+  // in global scratch, split across lanes.
+  ReplayClient cl[kMaxReplayClients];
+  double prof[4 * kMaxProfile];  // lat | util | tps | pred_s
   ReplayMember* mb = A.mb + static_cast<int64_t>(r) * P.max_batch;
-  double* prof = A.prof + static_cast<int64_t>(r) * 4 * kMaxProfile;  // lat | util | tps | pred_s
   const int np = M.n_prof;
   for (int e = 0; e < np; ++e) {
     prof[e] = M.prof_lat[e];
@@ -187,7 +200,9 @@ __global__ void __launch_bounds__(64) replay_kernel(const ReplayArgs A) {
         continue;
       }
       int64_t reserved = 0;  // BatchState::reserved_kv_tokens (gpu_model.cpp:40-46)
-      for (int j = 0; j < members; ++j) reserved += mb[j].in + (mb[j].reserved_out > mb[j].generated ? mb[j].reserved_out : mb[j].generated);
+      for (int j = lane; j < members; j += 32)
+        reserved += mb[j].in + (mb[j].reserved_out > mb[j].generated ? mb[j].reserved_out : mb[j].generated);
+      reserved = warp_sum64(reserved);
       if (!((members + 1 <= P.max_batch) &&
             __dmul_rn(static_cast<double>(reserved + in + pred), P.m) <= P.M)) {  // can_fit
         if (P.backfill) {
@@ -240,7 +255,8 @@ __global__ void __launch_bounds__(64) replay_kernel(const ReplayArgs A) {
     if (members == 0) continue;
     // ---- run_iteration (engine.cpp:273-325) ----
     int64_t resident = 0;
-    for (int j = 0; j < members; ++j) resident += mb[j].in + mb[j].generated;
+    for (int j = lane; j < members; j += 32) resident += mb[j].in + mb[j].generated;
+    resident = warp_sum64(resident);
     const double p = static_cast<double>(new_prefill);
     double iter_ms = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(A.prefill_linear_ms, p), __dmul_rn(__dmul_rn(A.prefill_quad_ms, p), p)),
                                          A.decode_base_ms),
@@ -253,75 +269,95 @@ __global__ void __launch_bounds__(64) replay_kernel(const ReplayArgs A) {
     ovh_cum = __dadd_rn(ovh_cum, overhead_ms);
     now = t_end;
     comp_changed = false;
-    for (int j = 0; j < members; ++j) mb[j].generated += 1;
+    for (int j = lane; j < members; j += 32) mb[j].generated += 1;
+    __syncwarp();
     if (P.kind == kVtc && !P.vtc_use_prediction) {  // on_tokens per client (scheduler.cpp:185-190)
       for (int c = 0; c < C; ++c) {
         int64_t t = 0;
-        for (int j = 0; j < members; ++j) t += mb[j].client == c ? 1 : 0;
+        for (int j = lane; j < members; j += 32) t += mb[j].client == c ? 1 : 0;
+        t = warp_sum64(t);
         if (t > 0) cl[c].counter = __dadd_rn(cl[c].counter, __dmul_rn(__dmul_rn(cl[c].weight, P.ow), static_cast<double>(t)));
       }
     }
-    int64_t res2 = 0;
-    for (int j = 0; j < members; ++j) res2 += mb[j].in + mb[j].generated;
+    const int64_t res2 = resident + members;  // every resident request generated one token
     if (__dmul_rn(static_cast<double>(res2), P.m) > P.M) {  // KV memory bound violated
       status = 2;
       break;
     }
     drain(now);
     // ---- complete_finished (engine.cpp:327-375) ----
-    int j = 0;
-    while (j < members) {
-      const ReplayMember m = mb[j];
-      if (m.generated < true_out[m.row]) {
-        ++j;
-        continue;
+    // finished members are processed in batch order (ledger and update_map chains), then the
+    // survivors are compacted in order (members.erase keeps the relative order)
+    int32_t kept = 0;
+    for (int base = 0; base < members; base += 32) {
+      const int j = base + lane;
+      ReplayMember mine{};
+      bool fin = false;
+      if (j < members) {
+        mine = mb[j];
+        fin = mine.generated >= true_out[mine.row];
       }
-      const int c = m.client;
-      const double w = cl[c].weight;
-      const int32_t out = m.generated;
-      const double latency_s = __dsub_rn(now, arrival[m.row]);
-      const double exec_s = __dsub_rn(now, m.admit_s);
-      const double tps = __ddiv_rn(__dadd_rn(static_cast<double>(m.in), static_cast<double>(out)), exec_s);
-      const double busy_span = __dsub_rn(busy_cum, m.busy_at);
-      const double ovh_span = __dsub_rn(ovh_cum, m.ovh_at);
-      const double util = __ddiv_rn(busy_span, __dadd_rn(busy_span, ovh_span));
-      ++completed;
-      // on_complete (scheduler.cpp:192-233)
-      const double wt = __dadd_rn(static_cast<double>(m.in), __dmul_rn(P.ow, static_cast<double>(out)));
-      const double wwt = __dmul_rn(w, wt);
-      const double au = __ddiv_rn(wwt, __dadd_rn(1.0, __dmul_rn(P.delta, latency_s)));
-      const double ar = __dmul_rn(__dmul_rn(w, tps), util);
-      cl[c].ufc = __dadd_rn(cl[c].ufc, __dsub_rn(au, m.p_ufc));
-      if (cl[c].ufc < 0.0) {
-        cl[c].ufc = 0.0;
-        ++clamps;
-      }
-      cl[c].rfc = __dadd_rn(cl[c].rfc, __dsub_rn(ar, m.p_rfc));
-      if (cl[c].rfc < 0.0) {
-        cl[c].rfc = 0.0;
-        ++clamps;
-      }
-      if (P.kind == kVtc && P.vtc_use_prediction) {
-        cl[c].counter = __dadd_rn(cl[c].counter, __dsub_rn(wwt, m.p_vtc));
-        if (cl[c].counter < 0.0) {
-          cl[c].counter = 0.0;
+      unsigned fm = __ballot_sync(0xffffffffu, fin);
+      while (fm) {
+        const int src = __ffs(fm) - 1;
+        fm &= fm - 1;
+        const ReplayMember m = mb[base + src];
+        const int c = m.client;
+        const double w = cl[c].weight;
+        const int32_t out = m.generated;
+        const double latency_s = __dsub_rn(now, arrival[m.row]);
+        const double exec_s = __dsub_rn(now, m.admit_s);
+        const double tps = __ddiv_rn(__dadd_rn(static_cast<double>(m.in), static_cast<double>(out)), exec_s);
+        const double busy_span = __dsub_rn(busy_cum, m.busy_at);
+        const double ovh_span = __dsub_rn(ovh_cum, m.ovh_at);
+        const double util = __ddiv_rn(busy_span, __dadd_rn(busy_span, ovh_span));
+        ++completed;
+        // on_complete (scheduler.cpp:192-233)
+        const double wt = __dadd_rn(static_cast<double>(m.in), __dmul_rn(P.ow, static_cast<double>(out)));
+        const double wwt = __dmul_rn(w, wt);
+        const double au = __ddiv_rn(wwt, __dadd_rn(1.0, __dmul_rn(P.delta, latency_s)));
+        const double ar = __dmul_rn(__dmul_rn(w, tps), util);
+        double u = __dadd_rn(cl[c].ufc, __dsub_rn(au, m.p_ufc));
+        if (u < 0.0) {
+          u = 0.0;
           ++clamps;
         }
-      }
-      // update_map (predictor.cpp:372-383) with ObservedMetrics{out, latency_s * 1000, util, tps}
-      {
+        double v = __dadd_rn(cl[c].rfc, __dsub_rn(ar, m.p_rfc));
+        if (v < 0.0) {
+          v = 0.0;
+          ++clamps;
+        }
+        cl[c].ufc = u;
+        cl[c].rfc = v;
+        if (P.kind == kVtc && P.vtc_use_prediction) {
+          double k = __dadd_rn(cl[c].counter, __dsub_rn(wwt, m.p_vtc));
+          if (k < 0.0) {
+            k = 0.0;
+            ++clamps;
+          }
+          cl[c].counter = k;
+        }
+        // update_map (predictor.cpp:372-383) with ObservedMetrics{out, latency_s * 1000, util, tps}
         const int e = entry_for(out);
         const double al = A.ema_alpha, bl = __dsub_rn(1.0, A.ema_alpha);
-        prof[e] = __dadd_rn(__dmul_rn(bl, prof[e]), __dmul_rn(al, __dmul_rn(latency_s, 1000.0)));
-        prof[kMaxProfile + e] = __dadd_rn(__dmul_rn(bl, prof[kMaxProfile + e]), __dmul_rn(al, util));
-        prof[2 * kMaxProfile + e] = __dadd_rn(__dmul_rn(bl, prof[2 * kMaxProfile + e]), __dmul_rn(al, tps));
-        prof[3 * kMaxProfile + e] = __ddiv_rn(prof[e], 1000.0);
+        const double nl = __dadd_rn(__dmul_rn(bl, prof[e]), __dmul_rn(al, __dmul_rn(latency_s, 1000.0)));
+        const double nu = __dadd_rn(__dmul_rn(bl, prof[kMaxProfile + e]), __dmul_rn(al, util));
+        const double nt = __dadd_rn(__dmul_rn(bl, prof[2 * kMaxProfile + e]), __dmul_rn(al, tps));
+        prof[e] = nl;
+        prof[kMaxProfile + e] = nu;
+        prof[2 * kMaxProfile + e] = nt;
+        prof[3 * kMaxProfile + e] = __ddiv_rn(nl, 1000.0);
+        cl[c].running -= 1;
+        comp_changed = true;
+        __syncwarp();
       }
-      cl[c].running -= 1;
-      for (int k = j; k + 1 < members; ++k) mb[k] = mb[k + 1];  // members.erase
-      --members;
-      comp_changed = true;
+      // stable compaction of this chunk's survivors
+      const unsigned keep = __ballot_sync(0xffffffffu, j < members && !fin);
+      if (j < members && !fin) mb[kept + __popc(keep & ((1u << lane) - 1u))] = mine;
+      kept += __popc(keep);
+      __syncwarp();
     }
+    members = kept;
   }
   A.n_events[r] = n_ev;
   A.completed[r] = completed;
