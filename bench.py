@@ -422,7 +422,7 @@ def run_cfg5(args, rank, world):
     n = n_total
     line = {"metric": "engine replays/sec (alpha sweep)", "value": n / (k * 1e-3), "unit": "replays/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": k, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "cfg5: 1024 replays = 8 alpha x 128 seeds of the poisson preset (60 s), "
                                    "one replay per GPU thread", "requests": int(row_off[-1]),
                        "completed": int(out["completed"].sum()), "admissions": int(out["n_events"].sum())},
