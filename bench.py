@@ -541,13 +541,16 @@ def run_ours(args, rank, world):
 
     e2e_val, e2e_step_ms, single_ms = None, None, None
     if e2e_steps:
-        e2e_loop(args.warmup)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        adm = e2e_loop(e2e_steps)
-        t1 = time.perf_counter()
-        assert all(a == res.n_admitted for a in adm)
-        e2e_step_ms = (t1 - t0) * 1e3 / e2e_steps
+        e2e_loop(max(10, args.warmup))  # first touches of the pinned batches and staging graphs
+        passes = []
+        for _ in range(3):  # median of three timed passes
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            adm = e2e_loop(e2e_steps)
+            t1 = time.perf_counter()
+            assert all(a == res.n_admitted for a in adm)
+            passes.append((t1 - t0) * 1e3 / e2e_steps)
+        e2e_step_ms = float(np.median(passes))
         e2e_val = world * n / (e2e_step_ms * 1e-3)
         single = []
         for _ in range(5):  # unpipelined latency of one step through the same API
@@ -600,6 +603,7 @@ def run_ours(args, rank, world):
                      "traffic": traffic, "algo_bytes_per_request": ALGO_BYTES_K1, "peak_source": peak_src},
         "e2e": {"value": e2e_val, "unit": "requests/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_step_ms, "steps": e2e_steps,
+                "passes": 3,
                 "single_step_latency_ms": single_ms,
                 "note": "wall clock over consecutive steps; step i+1's H2D (copy stream) overlaps step i"},
         # per step: drain_hist, drain_rank, score, window, select, event_fill

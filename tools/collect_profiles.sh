@@ -12,3 +12,7 @@ timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --cs
 timeout 600 ncu --set full --clock-control none --import-source on -s 14 -c 8 -o gpurun_out/prof/full \
   python bench.py --steps 2 --warmup 3 --profile --no-cpu-baseline > /dev/null 2>&1
 ls -la gpurun_out/prof
+timeout 300 python bench.py --config cfg5 --steps 5 --warmup 2 > gpurun_out/prof/bench_cfg5.json 2>&1
+timeout 300 python bench.py --config cfg5 --impl reference > gpurun_out/prof/bench_cfg5_reference.json 2>&1
+timeout 300 ncu --set full --clock-control none -k regex:replay -c 1 -o gpurun_out/prof/replay python bench.py --config cfg5 --steps 1 --warmup 0 > /dev/null 2>&1
+ls -la gpurun_out/prof
