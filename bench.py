@@ -430,6 +430,13 @@ def run_cfg5(args, rank, world):
                     "d2h_bytes_per_step": int(sum(v.nbytes for v in out.values())),
                     "ms_per_step": e2e_s * 1e3},
             "gpu_launches": args.steps}
+    if world == 1:  # the sweep points run_sweep_alpha reports (per alpha, mean over seeds)
+        pts = []
+        for a in np.unique(alpha):
+            sel = np.nonzero(alpha == a)[0]
+            pts.append({"alpha": float(a), "jain_ttft_p90": float(np.mean(out["jain_ttft_p90"][sel])),
+                        "throughput_tps": float(np.mean(out["throughput_tps"][sel]))})
+        line["sweep"] = pts
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

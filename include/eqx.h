@@ -225,6 +225,8 @@ typedef struct {                     /* host arrays; any may be NULL */
   double* sim_end;                   /* SimResult::sim_end_s */
   int64_t* counter_clamps;
   int32_t* status;                   /* 0 ok; 2: KV memory bound violated (EngineError) */
+  double* jain_ttft_p90;             /* build_report: Jain index of per-client p90 TTFT */
+  double* throughput_tps;            /* build_report: completed (in + out) tokens per second */
 } eqx_replay_out;
 
 /* PerfParams timing fields (gpu_model.hpp:14-28) used by replays. */

@@ -498,3 +498,19 @@ def ref_multi(case: "StepCase", step_end, step_now, act_extra, act_tps, act_util
     res.update(led)
     res.update({"prof_" + k: v for k, v in prof.items()})
     return res
+
+
+def ref_replay_report(case: "StepCase", max_sim_time_s=0.0, ema_alpha=0.2) -> dict:
+    """run_simulation + build_report: jain_ttft_p90, throughput_tps, completed, sim_end_s."""
+    lib, _ = _lib("ref")
+    keep: list = []
+    s = _build_in(case, keep)
+    j, t, e = C.c_double(), C.c_double(), C.c_double()
+    n = C.c_int64()
+    err = C.create_string_buffer(512)
+    f = lib.ref_replay_report
+    f.restype = C.c_int
+    if f(C.byref(s), C.c_double(max_sim_time_s), C.c_double(ema_alpha), C.byref(j), C.byref(t), C.byref(n),
+         C.byref(e), err, 512):
+        raise ValueError(err.value.decode())
+    return {"jain_ttft_p90": j.value, "throughput_tps": t.value, "completed": n.value, "sim_end": e.value}

@@ -25,6 +25,7 @@
 #include "equinox/engine.hpp"
 #include "equinox/errors.hpp"
 #include "equinox/gpu_model.hpp"
+#include "equinox/metrics.hpp"
 #include "equinox/predictor.hpp"
 #include "equinox/rng.hpp"
 #include "equinox/scheduler.hpp"
@@ -728,5 +729,73 @@ extern "C" int64_t ref_multi(const eqxo_step_in* in, int32_t n_steps, const int6
   } catch (const std::exception& e) {
     set_err(err, err_len, e.what());
     return -1;
+  }
+}
+
+// ref_replay_report -- run_simulation as ref_replay does, then build_report (metrics.cpp:155-229)
+// for the two numbers run_sweep_alpha aggregates (experiments.cpp:354-360): the Jain index of
+// the per-client p90 TTFT and the completed-token throughput.
+extern "C" int ref_replay_report(const eqxo_step_in* in, double max_sim_time_s, double ema_alpha,
+                                 double* jain_ttft_p90, double* throughput_tps, int64_t* completed,
+                                 double* sim_end, char* err, int err_len) {
+  try {
+    const auto names = split_names(in->client_names, in->n_clients);
+    const auto tags = split_names(in->tag_names, in->n_tags);
+    Trace trace;
+    for (int c = 0; c < in->n_clients; ++c) {
+      ClientSpec cs;
+      cs.client_id = names[c];
+      cs.weight = in->weight[c];
+      cs.arrivals.kind = ArrivalKind::Replay;
+      trace.clients.push_back(cs);
+    }
+    double last = 0.0;
+    for (int64_t r = 0; r < in->n_req; ++r) {
+      Request q;
+      q.id = in->id[r];
+      q.client_id = names[static_cast<std::size_t>(in->client[r])];
+      q.arrival_time_s = in->arrival[r];
+      q.input_tokens = in->in_tokens[r];
+      q.true_output_tokens = in->true_out[r];
+      if (in->tag[r] >= 0) q.category_tag = tags[static_cast<std::size_t>(in->tag[r])];
+      last = q.arrival_time_s;
+      trace.requests.push_back(q);
+    }
+    trace.duration_s = last;
+    EngineConfig cfg;
+    cfg.policy.kind = static_cast<PolicyKind>(in->kind);
+    cfg.policy.equinox.alpha = in->alpha;
+    cfg.policy.equinox.delta = in->delta;
+    cfg.policy.equinox.output_weight = in->output_weight;
+    cfg.policy.equinox.norm_mode = in->norm_mode == EQXO_NORM_NONE ? NormMode::None : NormMode::MaxOverClients;
+    cfg.policy.vtc_use_prediction = in->vtc_use_prediction != 0;
+    cfg.policy.counter_lift = in->counter_lift != 0;
+    cfg.perf.max_batch = in->max_batch;
+    cfg.perf.mem_per_token_bytes = in->mem_per_token_bytes;
+    cfg.perf.mem_capacity_bytes = in->mem_capacity_bytes;
+    cfg.backfill = in->backfill != 0;
+    cfg.max_sim_time_s = max_sim_time_s;
+    cfg.ema_alpha = ema_alpha;
+    GpuProfile profile;
+    for (int e = 0; e < in->n_profile; ++e)
+      profile.entries.push_back({in->prof_upper[e], in->prof_lat[e], in->prof_util[e], in->prof_tps[e]});
+    std::unique_ptr<Predictor> predictor;
+    if (in->pred_kind == EQXO_PRED_MOPE) {
+      predictor = std::make_unique<MopePredictor>(model_from(in->mope, tags, in->tag_row, in->n_tags));
+    } else if (in->pred_kind == EQXO_PRED_NOISY) {
+      predictor = std::make_unique<NoisyOraclePredictor>(in->noisy_l1, in->noisy_seed);
+    } else {
+      predictor = std::make_unique<OraclePredictor>();
+    }
+    const SimResult res = run_simulation(trace, cfg, *predictor, profile);
+    const SimReport rep = build_report(trace, res, cfg.policy.equinox.output_weight, cfg.report_window_s);
+    *jain_ttft_p90 = rep.jain_ttft_p90;
+    *throughput_tps = rep.throughput_tps;
+    *completed = rep.completed;
+    *sim_end = rep.sim_end_s;
+    return 0;
+  } catch (const std::exception& e) {
+    set_err(err, err_len, e.what());
+    return 1;
   }
 }

@@ -79,7 +79,8 @@ class Replays(C.Structure):
 class ReplayOut(C.Structure):
     _fields_ = [("n_events", C.c_void_p), ("ev_id", C.c_void_p), ("ev_kind", C.c_void_p), ("ev_time", C.c_void_p),
                 ("ufc", C.c_void_p), ("rfc", C.c_void_p), ("counter", C.c_void_p), ("completed", C.c_void_p),
-                ("sim_end", C.c_void_p), ("counter_clamps", C.c_void_p), ("status", C.c_void_p)]
+                ("sim_end", C.c_void_p), ("counter_clamps", C.c_void_p), ("status", C.c_void_p),
+                ("jain_ttft_p90", C.c_void_p), ("throughput_tps", C.c_void_p)]
 
 
 _SIGS = {

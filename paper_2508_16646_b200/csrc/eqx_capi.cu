@@ -1445,7 +1445,7 @@ eqx_status eqx_replay(eqx_ctx* ctx, const eqx_replays* R, eqx_replay_out* O) {
                o_prof = take(8 * n8 * 4 * kMaxProfile), o_evid = take(8 * n8 * cap), o_evk = take(4 * n8 * cap),
                o_evt = take(8 * n8 * cap), o_nev = take(8 * n8), o_comp = take(8 * n8), o_end = take(8 * n8),
                o_clamp = take(8 * n8), o_stat = take(4 * n8), o_u = take(8 * n8 * C), o_r = take(8 * n8 * C),
-               o_k = take(8 * n8 * C);
+               o_k = take(8 * n8 * C), o_ttft = take(8 * rr), o_jain = take(8 * n8), o_tput = take(8 * n8);
   CUDA_TRY(ctx, ctx->d_fb.ensure(off));
   char* b = static_cast<char*>(ctx->d_fb.p);
   auto up = [&](size_t o, const void* src, size_t bytes) {
@@ -1508,6 +1508,9 @@ eqx_status eqx_replay(eqx_ctx* ctx, const eqx_replays* R, eqx_replay_out* O) {
   A.out_ufc = reinterpret_cast<double*>(b + o_u);
   A.out_rfc = reinterpret_cast<double*>(b + o_r);
   A.out_counter = reinterpret_cast<double*>(b + o_k);
+  A.f_ttft = reinterpret_cast<double*>(b + o_ttft);
+  A.jain_ttft_p90 = reinterpret_cast<double*>(b + o_jain);
+  A.throughput_tps = reinterpret_cast<double*>(b + o_tput);
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[2], s));
   replay_kernel<<<(nr + 3) / 4, 128, 0, s>>>(A);  // one warp per replay
   CUDA_TRY(ctx, cudaGetLastError());
@@ -1519,8 +1522,9 @@ eqx_status eqx_replay(eqx_ctx* ctx, const eqx_replays* R, eqx_replay_out* O) {
   eqx_status st = read_cols(ctx, cols, 8);
   if (st != EQX_OK) return st;
   const Col cols2[] = {{O->sim_end, b + o_end, 8 * n8}, {O->counter_clamps, b + o_clamp, 8 * n8},
-                       {O->status, b + o_stat, 4 * n8}};
-  return read_cols(ctx, cols2, 3);
+                       {O->status, b + o_stat, 4 * n8}, {O->jain_ttft_p90, b + o_jain, 8 * n8},
+                       {O->throughput_tps, b + o_tput, 8 * n8}};
+  return read_cols(ctx, cols2, 5);
 }
 
 // ---- live queues -----------------------------------------------------

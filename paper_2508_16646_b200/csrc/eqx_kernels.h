@@ -373,6 +373,10 @@ struct ReplayArgs {
   double* out_ufc;            // [n_replays][C]
   double* out_rfc;
   double* out_counter;
+  // build_report's sweep metrics (metrics.cpp:155-229; experiments.cpp:354-360)
+  double* f_ttft;             // [rows] first-token latency per request (-1: none)
+  double* jain_ttft_p90;      // [n_replays]
+  double* throughput_tps;     // [n_replays]
 };
 __global__ void replay_kernel(ReplayArgs a);
 

@@ -56,6 +56,9 @@ __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
   int32_t* f_pred = A.f_pred + t0;                      // frozen prediction records
   double* f_preds = A.f_preds + t0;
   double* f_rfc = A.f_rfc + t0;
+  double* f_ttft = A.f_ttft + t0;
+  for (int64_t i = lane; i < n; i += 32) f_ttft[i] = -1.0;
+  int64_t completed_tokens = 0;
   // Ledger, FIFO cursors and profile are private per lane (identical copies, updated uniformly),
   // so the read-modify-write engine steps need no intra-warp synchronisation; the batch lives
   // in global scratch, split across lanes.
@@ -269,7 +272,10 @@ __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
     ovh_cum = __dadd_rn(ovh_cum, overhead_ms);
     now = t_end;
     comp_changed = false;
-    for (int j = lane; j < members; j += 32) mb[j].generated += 1;
+    for (int j = lane; j < members; j += 32) {
+      mb[j].generated += 1;
+      if (mb[j].generated == 1) f_ttft[mb[j].row] = __dsub_rn(now, arrival[mb[j].row]);  // FirstToken
+    }
     __syncwarp();
     if (P.kind == kVtc && !P.vtc_use_prediction) {  // on_tokens per client (scheduler.cpp:185-190)
       for (int c = 0; c < C; ++c) {
@@ -312,6 +318,7 @@ __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
         const double ovh_span = __dsub_rn(ovh_cum, m.ovh_at);
         const double util = __ddiv_rn(busy_span, __dadd_rn(busy_span, ovh_span));
         ++completed;
+        completed_tokens += static_cast<int64_t>(m.in) + out;
         // on_complete (scheduler.cpp:192-233)
         const double wt = __dadd_rn(static_cast<double>(m.in), __dmul_rn(P.ow, static_cast<double>(out)));
         const double wwt = __dmul_rn(w, wt);
@@ -358,6 +365,53 @@ __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
       __syncwarp();
     }
     members = kept;
+  }
+  // ---- build_report's sweep metrics (metrics.cpp:76-105,170-189) ----
+  {
+    // per-client p90 TTFT (percentile_stats: nearest rank ceil(0.9 n)), clients in client_id
+    // order (the std::map of ttft_stats), Jain index over those with any first token
+    double sum = 0.0, sum_sq = 0.0;
+    int32_t m_clients = 0;
+    for (uint32_t rank = 0; rank < static_cast<uint32_t>(C); ++rank) {
+      int c = -1;
+      for (int i = 0; i < C; ++i)
+        if (cl[i].order == rank) c = i;
+      if (c < 0) continue;
+      // rows of client c: crow[qbase[c] .. qbase[c + 1])
+      int64_t cnt = 0;
+      const int32_t c_rows = (c + 1 < C ? cl[c + 1].qbase : static_cast<int32_t>(n)) - cl[c].qbase;
+      for (int32_t j = lane; j < c_rows; j += 32) cnt += f_ttft[crow[cl[c].qbase + j]] >= 0.0 ? 1 : 0;
+      cnt = warp_sum64(cnt);
+      if (cnt == 0) continue;
+      int64_t k = static_cast<int64_t>(ceil(__dmul_rn(__ddiv_rn(90.0, 100.0), static_cast<double>(cnt))));
+      k = k < 1 ? 1 : (k > cnt ? cnt : k);
+      uint64_t prefix = 0, mask = 0;  // k-th smallest by MSB-first radix select on the bits
+      for (int bit = 63; bit >= 0; --bit) {
+        const uint64_t b = 1ull << bit;
+        int64_t zeros = 0;
+        for (int32_t j = lane; j < c_rows; j += 32) {
+          const double v = f_ttft[crow[cl[c].qbase + j]];
+          if (v < 0.0) continue;
+          const uint64_t u = static_cast<uint64_t>(__double_as_longlong(v));
+          zeros += ((u & mask) == prefix && !(u & b)) ? 1 : 0;
+        }
+        zeros = warp_sum64(zeros);
+        if (zeros < k) {
+          k -= zeros;
+          prefix |= b;
+        }
+        mask |= b;
+      }
+      const double p90 = __longlong_as_double(static_cast<long long>(prefix));
+      sum = __dadd_rn(sum, p90);
+      sum_sq = __dadd_rn(sum_sq, __dmul_rn(p90, p90));
+      ++m_clients;
+    }
+    double jain = 1.0;  // no first tokens: 1.0 (metrics.cpp:176); jain_index: all-zero -> 1.0
+    if (m_clients > 0 && sum_sq != 0.0)
+      jain = __ddiv_rn(__dmul_rn(sum, sum), __dmul_rn(static_cast<double>(m_clients), sum_sq));
+    A.jain_ttft_p90[r] = jain;
+    A.throughput_tps[r] = now > 0.0 ? __ddiv_rn(static_cast<double>(completed_tokens), now) : 0.0;
   }
   A.n_events[r] = n_ev;
   A.completed[r] = completed;

@@ -508,14 +508,40 @@ class GpuScheduler:
                "ev_kind": np.zeros((n, ev_cap), np.int32), "ev_time": np.zeros((n, ev_cap)),
                "ufc": np.zeros((n, nc)), "rfc": np.zeros((n, nc)), "counter": np.zeros((n, nc)),
                "completed": np.zeros(n, np.int64), "sim_end": np.zeros(n), "counter_clamps": np.zeros(n, np.int64),
-               "status": np.zeros(n, np.int32)}
+               "status": np.zeros(n, np.int32), "jain_ttft_p90": np.zeros(n), "throughput_tps": np.zeros(n)}
         ro = L.ReplayOut(*(out[k].ctypes.data for k in ("n_events", "ev_id", "ev_kind", "ev_time", "ufc", "rfc",
                                                           "counter", "completed", "sim_end", "counter_clamps",
-                                                          "status")))
+                                                          "status", "jain_ttft_p90", "throughput_tps")))
         self._check(self._lib.eqx_replay(self._ctx, C.byref(rq), C.byref(ro)))
         if np.any(out["status"] == 2):
             raise EngineError("KV memory bound violated in replay(s) " + str(np.nonzero(out["status"] == 2)[0][:8]))
         return out
+
+    def sweep_alpha(self, alphas, traces: list, ema_alpha: float = 0.2) -> list:
+        """run_sweep_alpha (experiments.cpp:331-373): every (alpha, trace) pair replayed on the
+        GPU in one launch; per alpha the mean jain_ttft_p90 and throughput_tps over the traces
+        and both normalised by their maximum over alphas (SweepPoint)."""
+        alphas = list(alphas)
+        pairs = [(a, t) for a in alphas for t in traces]
+        row_off = np.concatenate([[0], np.cumsum([len(t["client"]) for _, t in pairs])]).astype(np.int64)
+        cat = {k: np.concatenate([np.asarray(t[k]) for _, t in pairs]) for k in
+               ("client", "arrival", "in_tokens", "true_out")}
+        out = self.replay(row_off, cat["client"], cat["arrival"], cat["in_tokens"], cat["true_out"],
+                          np.array([a for a, _ in pairs]), ema_alpha=ema_alpha, ev_cap=1)
+        k = len(traces)
+        points = []
+        for i, a in enumerate(alphas):  # the reference's accumulation order (seeds in order)
+            j = t = 0.0
+            for s in range(k):
+                j += out["jain_ttft_p90"][i * k + s]
+                t += out["throughput_tps"][i * k + s]
+            points.append({"alpha": a, "jain_ttft_p90": j / float(k), "throughput_tps": t / float(k)})
+        mj = max([0.0] + [p["jain_ttft_p90"] for p in points])
+        mt = max([0.0] + [p["throughput_tps"] for p in points])
+        for p in points:
+            p["jain_norm"] = p["jain_ttft_p90"] / mj if mj > 0.0 else 0.0
+            p["throughput_norm"] = p["throughput_tps"] / mt if mt > 0.0 else 0.0
+        return points
 
     # -- completion / feedback (engine.cpp:273-375; SURVEY.md 8f row 1) --
     def feedback(self, tokens=None, completions: dict | None = None, ema_alpha: float = 0.2) -> None:

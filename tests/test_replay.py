@@ -101,3 +101,29 @@ def test_alpha_sweep_preset_replays_match_reference():
     traces = [preset_trace(100 + i) for i in range(len(alphas))]
     ref, got = run_both(traces, alphas, pred_kind=0)
     check(ref, got)
+
+
+def test_sweep_metrics_match_reference_build_report():
+    """build_report's jain_ttft_p90 and throughput_tps per replay (what run_sweep_alpha averages)."""
+    alphas = [0.5, 0.7, 0.85]
+    traces = [preset_trace(200 + i) for i in range(3)] + [poisson_trace(300, n_clients=5, rate=200.0, duration=5.0)]
+    want = []
+    for a in alphas:
+        for q in traces[:3]:
+            case = H.StepCase(client=q["client"], arrival=q["arrival"], in_tokens=q["in_tokens"],
+                              true_out=q["true_out"], tag=q["tag"], client_names=q["client_names"], alpha=a,
+                              pred_kind=0, profile=default_profile())
+            want.append(H.ref_replay_report(case))
+    ref, got = run_both(traces[:3] * 3, np.repeat(alphas, 3), pred_kind=0)
+    check(ref, got)
+    np.testing.assert_array_equal(got["jain_ttft_p90"], [w["jain_ttft_p90"] for w in want])
+    np.testing.assert_array_equal(got["throughput_tps"], [w["throughput_tps"] for w in want])
+    np.testing.assert_array_equal(got["completed"], [w["completed"] for w in want])
+    np.testing.assert_array_equal(got["sim_end"], [w["sim_end"] for w in want])
+    # the 5-client trace exercises the client_id-ordered Jain sum
+    q = traces[3]
+    case = H.StepCase(client=q["client"], arrival=q["arrival"], in_tokens=q["in_tokens"], true_out=q["true_out"],
+                      tag=q["tag"], client_names=q["client_names"], alpha=0.6, pred_kind=0, profile=default_profile())
+    w5 = H.ref_replay_report(case)
+    _, g5 = run_both([q], [0.6], pred_kind=0)
+    assert g5["jain_ttft_p90"][0] == w5["jain_ttft_p90"] and g5["throughput_tps"][0] == w5["throughput_tps"]
