@@ -85,6 +85,8 @@ class ReplayOut(C.Structure):
 
 _SIGS = {
     "eqx_abi_version": ([], C.c_int32),
+    "eqx_host_alloc": ([C.c_int64], C.c_void_p),
+    "eqx_host_free": ([C.c_void_p], C.c_int),
     "eqx_ctx_create": ([C.c_int32, C.POINTER(C.c_void_p)], C.c_int),
     "eqx_ctx_destroy": ([C.c_void_p], None),
     "eqx_last_error": ([C.c_void_p], C.c_char_p),

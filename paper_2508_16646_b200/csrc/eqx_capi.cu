@@ -15,6 +15,9 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <map>
+#include <mutex>
+#include <sys/mman.h>
 
 #include "../../include/eqx.h"
 #include "eqx_device.cuh"
@@ -335,6 +338,46 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 extern "C" {
 
 int32_t eqx_abi_version(void) { return EQX_ABI_VERSION; }
+
+namespace {
+std::mutex g_host_mu;
+std::map<void*, std::pair<void*, size_t>> g_host_maps;  // aligned pointer -> (mapping, length)
+constexpr size_t kHuge = size_t(2) << 20;
+}  // namespace
+
+void* eqx_host_alloc(int64_t bytes) {
+  if (bytes <= 0) return nullptr;
+  const size_t size = (size_t(bytes) + kHuge - 1) / kHuge * kHuge;
+  const size_t len = size + kHuge;
+  void* m = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+  if (m == MAP_FAILED) return nullptr;
+  char* al = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(m) + kHuge - 1) & ~(uintptr_t(kHuge) - 1));
+  madvise(al, size, MADV_HUGEPAGE);  // advisory: a kernel without THP still gets a working arena
+  memset(al, 0, size);               // fault the pages in (huge where THP allows) before pinning
+  if (cudaHostRegister(al, size, cudaHostRegisterDefault) != cudaSuccess) {
+    cudaGetLastError();
+    munmap(m, len);
+    return nullptr;
+  }
+  std::lock_guard<std::mutex> g(g_host_mu);
+  g_host_maps[al] = {m, len};
+  return al;
+}
+
+eqx_status eqx_host_free(void* p) {
+  if (!p) return EQX_OK;
+  std::pair<void*, size_t> mp;
+  {
+    std::lock_guard<std::mutex> g(g_host_mu);
+    auto it = g_host_maps.find(p);
+    if (it == g_host_maps.end()) return EQX_ERR_CONFIG;
+    mp = it->second;
+    g_host_maps.erase(it);
+  }
+  cudaHostUnregister(p);
+  munmap(mp.first, mp.second);
+  return EQX_OK;
+}
 
 const char* eqx_last_error(const eqx_ctx* ctx) {
   return ctx ? ctx->err.c_str() : g_create_error.c_str();

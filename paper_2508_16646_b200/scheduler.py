@@ -190,6 +190,30 @@ def rfc_increment(weight: float, tps: float, gpu_util: float) -> float:
 
 
 # ---- the request batch -------------------------------------------------------------------------
+def pinned_empty(shape, dtype) -> np.ndarray:
+    """numpy array in the library's pinned host arena (eqx_host_alloc: 2 MiB-aligned, huge-page
+    backed, driver-registered), for request columns a serving loop refills and stages every step.
+    The arena is released when the array (and every view of it) is garbage."""
+    import weakref
+    dt = np.dtype(dtype)
+    count = int(np.prod(shape, dtype=np.int64))
+    nbytes = max(count * dt.itemsize, 1)
+    lib = L.load()
+    ptr = lib.eqx_host_alloc(nbytes)
+    if not ptr:
+        raise MemoryError(f"eqx_host_alloc({nbytes}) failed")
+    buf = (C.c_uint8 * nbytes).from_address(ptr)
+    weakref.finalize(buf, lib.eqx_host_free, C.c_void_p(ptr))
+    return np.frombuffer(buf, dtype=dt, count=count).reshape(shape)
+
+
+def pinned_copy(x) -> np.ndarray:
+    a = np.ascontiguousarray(x)
+    out = pinned_empty(a.shape, a.dtype)
+    out[...] = a
+    return out
+
+
 def _as_col(x, dtype, keep: list):
     """numpy -> (host ptr, HOST); torch CUDA tensor -> (device ptr, DEVICE)."""
     if x is None:

@@ -4,6 +4,7 @@ import os
 import re
 import subprocess
 
+import numpy as np
 import pytest
 
 from paper_2508_16646_b200 import _lib as L
@@ -46,3 +47,20 @@ def test_scalar_helpers_match_reference_known_answers():
     assert lib.eqx_ufc_increment(1.0, 100, 400, 0.0, 0.0, 0.1, 4.0) == 1700.0
     assert lib.eqx_ufc_increment(1.0, 100, 400, 5.0, 5000.0, 0.1, 4.0) == 850.0
     assert lib.eqx_rfc_increment(1.0, 1000.0, 0.9) == 900.0
+
+
+@pytest.mark.gpu
+def test_pinned_host_arena():
+    import torch
+    from paper_2508_16646_b200 import scheduler as S
+    a = S.pinned_empty((3, 1000), np.float64)
+    a[...] = np.arange(3000).reshape(3, 1000)
+    t = torch.from_numpy(a)
+    d = t.to("cuda", non_blocking=True)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(d.cpu().numpy(), a)
+    b = S.pinned_copy(np.arange(5, dtype=np.int32))
+    assert b.dtype == np.int32 and list(b) == [0, 1, 2, 3, 4]
+    lib = S.L.load()
+    assert lib.eqx_host_free(None) == 0
+    assert lib.eqx_host_alloc(0) is None

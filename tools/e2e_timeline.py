@@ -5,7 +5,8 @@ import numpy as np, torch
 import bench
 q, led, perf, model, prof, desc = bench.load_inputs("cfg2", 0)
 sch, clients = bench.make_scheduler(q, led, perf, model, prof, 0)
-hosts = [{k: torch.from_numpy(v.copy()).pin_memory() for k, v in
+from paper_2508_16646_b200 import scheduler as S
+hosts = [{k: S.pinned_copy(v) for k, v in
           dict(client=q["client"], arrival_s=q["arrival"], input_tokens=q["in_tokens"],
                tag=bench.tag_ids(q)).items()} for _ in range(2)]
 sch.set_batch(0, 0); sch.checkpoint()
