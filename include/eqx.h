@@ -178,8 +178,9 @@ void* eqx_host_alloc(int64_t bytes);
 eqx_status eqx_host_free(void* p);
 
 /* ---- the hot path ------------------------------------------------------------------------ */
-/* Prefetch a HOST batch: its H2D copy runs on the context's copy stream into the next of two
- * device staging buffers, overlapping whatever the context is computing.  A later eqx_drain /
+/* Prefetch a HOST batch: its H2D copy runs on the context's copy stream into the next of three
+ * device staging buffers, overlapping whatever the context is computing (a serving loop keeps
+ * up to two batches staged ahead of the step it collects).  A later eqx_drain /
  * eqx_drain_step_async of the same batch (same pointers and n) uses the staged copy.  Host
  * buffers should be pinned for the copy to be asynchronous; they must stay unchanged until
  * that drain.  A step's results stay readable until the batch after next is drained. */

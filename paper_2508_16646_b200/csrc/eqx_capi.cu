@@ -84,9 +84,11 @@ struct eqx_ctx {
   const int64_t* q_id = nullptr;
   int64_t id_base = 0;
   DevBuf own_tag;  // zero tags for device batches without a tag column
-  // Host batches are staged through two device buffer sets on a copy stream, so the H2D of
-  // the next batch (eqx_stage_async) overlaps the current step; `free_` is recorded on the
-  // main stream after the last launch that reads a set.
+  // Host batches are staged through kStages device buffer sets on a copy stream, so the H2D
+  // of the next batches (eqx_stage_async) overlaps the current step: with three sets a caller
+  // can keep two batches in flight, so the copy engine never idles while the host collects a
+  // step.  `free_` is recorded on the main stream after the last launch that reads a set.
+  static constexpr int kStages = 3;
   struct Stage {
     DevBuf client, arrival, in, tru, tag, id;
     const void* key[6] = {};
@@ -94,7 +96,7 @@ struct eqx_ctx {
     uint64_t seq = 0;  // staging order: a drain consumes the oldest matching staged batch
     bool valid = false;
     cudaEvent_t ready = nullptr, free_ = nullptr;
-  } stg[2];
+  } stg[kStages];
   int bound_stage = -1;
   uint64_t stage_seq = 0;
   cudaStream_t copy_stream = nullptr;
@@ -125,11 +127,13 @@ struct eqx_ctx {
   DevBuf d_wcnt;                   // per-(tile, warp, client) counts of the drain walk
   DevBuf d_direct;                 // direct predict/map table (see ScoreArgs::direct)
   int32_t direct_n = 0;
-  // cached CUDA graph of drain + step for a resident (device) queue
-  // cached CUDA graphs of drain + step (two: a resident queue, or the two staging buffers)
-  cudaGraphExec_t graphs[2] = {nullptr, nullptr};
-  std::vector<unsigned char> graph_keys[2];
-  int graph_lru = 0;
+  // cached CUDA graphs of drain + step, least recently used evicted (a resident queue, or
+  // one per staging buffer set)
+  static constexpr int kGraphs = kStages + 1;
+  cudaGraphExec_t graphs[kGraphs] = {};
+  std::vector<unsigned char> graph_keys[kGraphs];
+  uint64_t graph_used[kGraphs] = {};
+  uint64_t graph_clock = 0;
   bool owns_stream = true;         // false after eqx_ctx_set_stream (caller's stream)
   // pinned bounce buffer for result reads: async D2H of every column, one sync, host memcpy
   void* h_scratch = nullptr;       // mapped pinned memory
@@ -418,7 +422,7 @@ eqx_status eqx_ctx_create(int32_t device, eqx_ctx** out) {
   e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking);
-  for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
+  for (int b = 0; b < eqx_ctx::kStages && e == cudaSuccess; ++b) {
     e = cudaEventCreateWithFlags(&ctx->stg[b].ready, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->stg[b].free_, cudaEventDisableTiming);
   }
@@ -511,7 +515,7 @@ eqx_status eqx_ctx_set_stream(eqx_ctx* ctx, void* stream) {
   if (ctx->owns_stream) CUDA_TRY(ctx, cudaStreamDestroy(ctx->stream));
   ctx->stream = static_cast<cudaStream_t>(stream);
   ctx->owns_stream = false;
-  for (int i = 0; i < 2; ++i) {  // captured on the old stream's plan
+  for (int i = 0; i < eqx_ctx::kGraphs; ++i) {  // captured on the old stream's plan
     if (ctx->graphs[i]) cudaGraphExecDestroy(ctx->graphs[i]);
     ctx->graphs[i] = nullptr;
     ctx->graph_keys[i].clear();
@@ -799,13 +803,20 @@ static eqx_status stage_fill(eqx_ctx* ctx, const eqx_requests* r, int b) {
   return EQX_OK;
 }
 
-// Staging target: a set holding no unconsumed batch, else the older one.
+// Staging target: the least recently filled set holding no unconsumed batch, preferring one
+// the live queue is not bound to (its copy then need not wait for the step in flight); with
+// every set unconsumed, the oldest.
 static int stage_target(const eqx_ctx* ctx) {
-  const eqx_ctx::Stage* st = ctx->stg;
-  if (!st[0].valid && !st[1].valid) return st[0].seq <= st[1].seq ? 0 : 1;
-  if (!st[0].valid) return 0;
-  if (!st[1].valid) return 1;
-  return st[0].seq <= st[1].seq ? 0 : 1;
+  int best = -1, rank_best = 0;
+  for (int k = 0; k < eqx_ctx::kStages; ++k) {
+    const eqx_ctx::Stage& st = ctx->stg[k];
+    const int rank = st.valid ? 2 : (k == ctx->bound_stage ? 1 : 0);
+    if (best < 0 || rank < rank_best || (rank == rank_best && st.seq < ctx->stg[best].seq)) {
+      best = k;
+      rank_best = rank;
+    }
+  }
+  return best;
 }
 
 static bool stage_matches(const eqx_ctx::Stage& st, const eqx_requests* r) {
@@ -861,7 +872,7 @@ static eqx_status drain_prepare(eqx_ctx* ctx, const eqx_requests* r) {
   } else {
     // host batch: a matching staged copy (eqx_stage_async), else stage it now
     int b = -1;
-    for (int k = 0; k < 2; ++k)
+    for (int k = 0; k < eqx_ctx::kStages; ++k)
       if (stage_matches(ctx->stg[k], r) && (b < 0 || ctx->stg[k].seq < ctx->stg[b].seq)) b = k;
     if (b < 0) {
       if (std::getenv("EQX_DEBUG_STAGE")) std::fprintf(stderr, "eqx: drain of an unstaged host batch\n");
@@ -1388,7 +1399,7 @@ eqx_status eqx_drain_step_async(eqx_ctx* ctx, const eqx_requests* r, double now)
   cudaStream_t s = ctx->stream;
   // One CUDA-graph launch replays drain + scoring + selection.  The key covers every launch
   // parameter (pointers, sizes, policy, `now`, smem/tiling plan); two graphs are cached, for a
-  // resident queue or the two staging buffers of host batches (whose H2D and release events
+  // resident queue or the staging buffer sets of host batches (whose H2D and release events
   // stay outside the graph).
   std::vector<unsigned char> key(sizeof(StepPlan) + 6 * sizeof(int64_t));
   std::memcpy(key.data(), &pl, sizeof(StepPlan));
@@ -1396,10 +1407,12 @@ eqx_status eqx_drain_step_async(eqx_ctx* ctx, const eqx_requests* r, double now)
                             static_cast<int64_t>(ctx->rank_smem), ctx->staged};
   std::memcpy(key.data() + sizeof(StepPlan), extra, sizeof(extra));
   int slot = -1;
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < eqx_ctx::kGraphs; ++i)
     if (ctx->graphs[i] && ctx->graph_keys[i] == key) slot = i;
   if (slot < 0) {
-    slot = ctx->graph_lru;
+    slot = 0;
+    for (int i = 1; i < eqx_ctx::kGraphs; ++i)
+      if (ctx->graph_used[i] < ctx->graph_used[slot]) slot = i;
     if (ctx->graphs[slot]) cudaGraphExecDestroy(ctx->graphs[slot]);
     ctx->graphs[slot] = nullptr;
     cudaGraph_t g = nullptr;
@@ -1416,7 +1429,7 @@ eqx_status eqx_drain_step_async(eqx_ctx* ctx, const eqx_requests* r, double now)
     CUDA_TRY(ctx, ie);
     ctx->graph_keys[slot] = key;
   }
-  ctx->graph_lru = slot ^ 1;
+  ctx->graph_used[slot] = ++ctx->graph_clock;
   CUDA_TRY(ctx, cudaGraphLaunch(ctx->graphs[slot], s));
   if (r->location != EQX_DEVICE) st = release_stage(ctx);
   if (st != EQX_OK) return st;

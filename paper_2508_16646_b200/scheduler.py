@@ -443,12 +443,12 @@ class GpuScheduler:
                     id_base: int = 0) -> None:
         """Prefetch a host batch (pinned numpy/torch CPU columns) into the context's next staging
         buffer on its copy stream; the drain of the same arrays then skips the copy.  The H2D
-        overlaps the step in flight (two staging buffers)."""
+        overlaps the steps in flight (three staging buffers: up to two batches ahead)."""
         keep: list = []
         rq = self._requests(client, arrival_s, input_tokens, tag, true_output_tokens, ids, id_base, keep)
         if rq.location != L.EQX_HOST:
             raise ValueError("stage_async: host columns only")
-        self._staged = getattr(self, "_staged", [])[-1:] + [keep]  # keep both staged batches alive
+        self._staged = getattr(self, "_staged", [])[-2:] + [keep]  # keep every staged batch alive (3 sets)
         self._check(self._lib.eqx_stage_async(self._ctx, C.byref(rq)))
 
     def drain_step_async(self, now: float, client, arrival_s, input_tokens, tag=None,
