@@ -425,7 +425,7 @@ def run_cfg5(args, rank, world):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": k, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "cfg5: 1024 replays = 8 alpha x 128 seeds of the poisson preset (60 s), "
-                                   "one replay per GPU thread", "requests": int(row_off[-1]),
+                                   "one replay per GPU warp, build_report + window samples on the device", "requests": int(row_off[-1]),
                        "completed": int(out["completed"].sum()), "admissions": int(out["n_events"].sum())},
             "e2e": {"value": n / e2e_s, "unit": "replays/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": int(sum(v.nbytes for v in out.values())),

@@ -205,9 +205,12 @@ eqx_status eqx_step(eqx_ctx* ctx, double now, eqx_step_summary* out);
 
 /* ---- batched engine replays (config 5, the alpha sweep) ---------------
  * run_simulation (engine.cpp:119-146) for many independent traces at once, one replay per
- * GPU thread, with the context's policy / perf / timing / profile / predictor / roster and a
+ * GPU warp, with the context's policy / perf / timing / profile / predictor / roster and a
  * per-replay EquinoxParams::alpha.  Each replay starts from zero ledgers (engine.cpp:148-157)
- * and its own copy of the profile; prediction_overhead_ms is 0 (EngineConfig default). */
+ * and its own copy of the profile; prediction_overhead_ms is 0 (EngineConfig default).  The
+ * reporting side runs on the device too: the engine's window samples (advance_clock /
+ * emit_window_samples, engine.cpp:379-430) and build_report (metrics.cpp:151-229) with the
+ * policy's output_weight and report_window_s as its window. */
 typedef struct {
   int32_t n_replays;
   const int64_t* row_off;            /* [n_replays + 1], row_off[0] = 0: rows of replay r */
@@ -221,7 +224,35 @@ typedef struct {
   double max_sim_time_s;             /* <= 0: each trace's last arrival */
   double ema_alpha;                  /* EngineConfig::ema_alpha (update_map) */
   int64_t ev_cap;                    /* admitted / rejected events kept per replay */
+  double report_window_s;            /* EngineConfig::report_window_s; <= 0: 1.0 (default) */
+  int64_t win_cap;                   /* window samples kept per replay in the series outputs */
 } eqx_replays;
+
+/* build_report's SimReport summary (metrics.hpp:63-81) + the SimResult totals of one replay. */
+typedef struct {
+  double max_diff, avg_diff, var_diff; /* service_difference over report windows (C >= 2) */
+  double jain_hf;                      /* Jain index of final_hf (metric_hf over all clients) */
+  double jain_ttft_p90;                /* Jain index of the per-client p90 TTFT */
+  double throughput_tps;               /* completed (in + out) tokens per second */
+  double mean_gpu_util;                /* busy_ms_total / (sim_end_s * 1000) */
+  double ttft_p50, ttft_p90;           /* nearest-rank percentiles over all first tokens */
+  double latency_p50, latency_p90;     /* ... over completed requests' end-to-end latency */
+  int64_t ttft_count, latency_count;
+  double sim_end_s, busy_ms_total, overhead_ms_total;
+  int64_t completed, rejected, total_completed_tokens;
+  int64_t n_windows;                   /* engine window samples (gpu_series / counter_series) */
+  int64_t n_diff;                      /* service-difference samples (diff_series) */
+  int64_t n_rate;                      /* service-rate windows per client */
+} eqx_replay_report;
+
+/* ClientReport (metrics.hpp:55-60) + the final reporting HF of one client of one replay. */
+typedef struct {
+  double final_hf;
+  double accumulated_service;
+  double mean_service_rate;
+  double ttft_p50, ttft_p90;
+  int64_t ttft_count;
+} eqx_replay_client;
 
 typedef struct {                     /* host arrays; any may be NULL */
   int64_t* n_events;                 /* [n_replays] (may exceed ev_cap) */
@@ -235,6 +266,13 @@ typedef struct {                     /* host arrays; any may be NULL */
   int32_t* status;                   /* 0 ok; 2: KV memory bound violated (EngineError) */
   double* jain_ttft_p90;             /* build_report: Jain index of per-client p90 TTFT */
   double* throughput_tps;            /* build_report: completed (in + out) tokens per second */
+  eqx_replay_report* report;         /* [n_replays] */
+  eqx_replay_client* clients;        /* [n_replays][C], roster order */
+  double* win;                       /* [n_replays][win_cap][4] time, busy_ms, overhead_ms, gpu_util */
+  double* win_clients;               /* [n_replays][win_cap][C][4] ufc, rfc, hf, service_cum */
+  double* diff;                      /* [n_replays][win_cap][2] time, max-min service */
+  double* rate;                      /* [n_replays][C][win_cap] service rate of window w
+                                        (time = window_s * (w + 1)) */
 } eqx_replay_out;
 
 /* PerfParams timing fields (gpu_model.hpp:14-28) used by replays. */

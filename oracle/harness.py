@@ -500,6 +500,35 @@ def ref_multi(case: "StepCase", step_end, step_now, act_extra, act_tps, act_util
     return res
 
 
+REPORT_FIELDS = ("max_diff", "avg_diff", "var_diff", "jain_hf", "jain_ttft_p90", "throughput_tps", "mean_gpu_util",
+                 "ttft_p50", "ttft_p90", "latency_p50", "latency_p90", "ttft_count", "latency_count", "sim_end_s",
+                 "busy_ms_total", "overhead_ms_total", "completed", "rejected", "total_completed_tokens",
+                 "n_windows", "n_diff", "n_rate")
+CLIENT_FIELDS = ("final_hf", "accumulated_service", "mean_service_rate", "ttft_p50", "ttft_p90", "ttft_count")
+
+
+def ref_replay_full(case: "StepCase", max_sim_time_s=0.0, ema_alpha=0.2, window_s=1.0, win_cap=256) -> dict:
+    """run_simulation + build_report through the reference objects (oracle/ref_step.cpp
+    ref_replay_full): the SimReport summary, per-client reports (roster order) and the series
+    (gpu_series, counter_series, diff_series, service_rate_series), cut at win_cap windows."""
+    lib, _ = _lib("ref")
+    keep: list = []
+    s = _build_in(case, keep)
+    nc = len(case.client_names)
+    rep, cli = np.zeros(len(REPORT_FIELDS)), np.zeros((nc, len(CLIENT_FIELDS)))
+    win, winc = np.zeros((win_cap, 4)), np.zeros((win_cap, nc, 4))
+    diff, rate = np.zeros((win_cap, 2)), np.zeros((nc, win_cap))
+    err = C.create_string_buffer(512)
+    f = lib.ref_replay_full
+    f.restype = C.c_int
+    dp = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))
+    if f(C.byref(s), C.c_double(max_sim_time_s), C.c_double(ema_alpha), C.c_double(window_s), C.c_int64(win_cap),
+         dp(rep), dp(cli), dp(win), dp(winc), dp(diff), dp(rate), err, 512):
+        raise ValueError(err.value.decode())
+    return {"report": dict(zip(REPORT_FIELDS, rep)), "clients": {k: cli[:, i] for i, k in enumerate(CLIENT_FIELDS)},
+            "win": win, "win_clients": winc, "diff": diff, "rate": rate}
+
+
 def ref_replay_report(case: "StepCase", max_sim_time_s=0.0, ema_alpha=0.2) -> dict:
     """run_simulation + build_report: jain_ttft_p90, throughput_tps, completed, sim_end_s."""
     lib, _ = _lib("ref")

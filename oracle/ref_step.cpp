@@ -799,3 +799,130 @@ extern "C" int ref_replay_report(const eqxo_step_in* in, double max_sim_time_s, 
     return 1;
   }
 }
+
+// ref_replay_full -- run_simulation + build_report (metrics.cpp:151-229) with every reported
+// quantity the device replay produces: the SimReport summary (rep[22], the field order of
+// eqx_replay_report, integers as doubles), per-client reports (cli[C][6], roster order:
+// final_hf, accumulated_service, mean_service_rate, ttft p50, p90, count), and the series,
+// each cut at win_cap windows: gpu_series (win[w][4]), counter_series (winc[w][C][4]),
+// diff_series (diff[w][2]) and service_rate_series values (rate[C][win_cap]).
+extern "C" int ref_replay_full(const eqxo_step_in* in, double max_sim_time_s, double ema_alpha, double window_s,
+                               int64_t win_cap, double* rep, double* cli, double* win, double* winc, double* diff,
+                               double* rate, char* err, int err_len) {
+  try {
+    const auto names = split_names(in->client_names, in->n_clients);
+    const auto tags = split_names(in->tag_names, in->n_tags);
+    Trace trace;
+    for (int c = 0; c < in->n_clients; ++c) {
+      ClientSpec cs;
+      cs.client_id = names[c];
+      cs.weight = in->weight[c];
+      cs.arrivals.kind = ArrivalKind::Replay;
+      trace.clients.push_back(cs);
+    }
+    double last = 0.0;
+    for (int64_t r = 0; r < in->n_req; ++r) {
+      Request q;
+      q.id = in->id[r];
+      q.client_id = names[static_cast<std::size_t>(in->client[r])];
+      q.arrival_time_s = in->arrival[r];
+      q.input_tokens = in->in_tokens[r];
+      q.true_output_tokens = in->true_out[r];
+      if (in->tag[r] >= 0) q.category_tag = tags[static_cast<std::size_t>(in->tag[r])];
+      last = q.arrival_time_s;
+      trace.requests.push_back(q);
+    }
+    trace.duration_s = last;
+    EngineConfig cfg;
+    cfg.policy.kind = static_cast<PolicyKind>(in->kind);
+    cfg.policy.equinox.alpha = in->alpha;
+    cfg.policy.equinox.delta = in->delta;
+    cfg.policy.equinox.output_weight = in->output_weight;
+    cfg.policy.equinox.norm_mode = in->norm_mode == EQXO_NORM_NONE ? NormMode::None : NormMode::MaxOverClients;
+    cfg.policy.vtc_use_prediction = in->vtc_use_prediction != 0;
+    cfg.policy.counter_lift = in->counter_lift != 0;
+    cfg.perf.max_batch = in->max_batch;
+    cfg.perf.mem_per_token_bytes = in->mem_per_token_bytes;
+    cfg.perf.mem_capacity_bytes = in->mem_capacity_bytes;
+    cfg.backfill = in->backfill != 0;
+    cfg.max_sim_time_s = max_sim_time_s;
+    cfg.ema_alpha = ema_alpha;
+    cfg.report_window_s = window_s;
+    GpuProfile profile;
+    for (int e = 0; e < in->n_profile; ++e)
+      profile.entries.push_back({in->prof_upper[e], in->prof_lat[e], in->prof_util[e], in->prof_tps[e]});
+    std::unique_ptr<Predictor> predictor;
+    if (in->pred_kind == EQXO_PRED_MOPE) {
+      predictor = std::make_unique<MopePredictor>(model_from(in->mope, tags, in->tag_row, in->n_tags));
+    } else if (in->pred_kind == EQXO_PRED_NOISY) {
+      predictor = std::make_unique<NoisyOraclePredictor>(in->noisy_l1, in->noisy_seed);
+    } else {
+      predictor = std::make_unique<OraclePredictor>();
+    }
+    const SimResult res = run_simulation(trace, cfg, *predictor, profile);
+    const SimReport r = build_report(trace, res, cfg.policy.equinox.output_weight, cfg.report_window_s);
+    const std::size_t C = trace.clients.size();
+    std::size_t n_rate = 0;
+    for (const auto& kv : r.per_client) n_rate = std::max(n_rate, kv.second.service_rate_series.size());
+    const double v[22] = {r.max_diff,
+                          r.avg_diff,
+                          r.var_diff,
+                          r.jain_hf,
+                          r.jain_ttft_p90,
+                          r.throughput_tps,
+                          r.mean_gpu_util,
+                          r.ttft_overall.p50,
+                          r.ttft_overall.p90,
+                          r.latency_overall.p50,
+                          r.latency_overall.p90,
+                          static_cast<double>(r.ttft_overall.count),
+                          static_cast<double>(r.latency_overall.count),
+                          r.sim_end_s,
+                          res.busy_ms_total,
+                          res.overhead_ms_total,
+                          static_cast<double>(r.completed),
+                          static_cast<double>(r.rejected),
+                          static_cast<double>(r.total_completed_tokens),
+                          static_cast<double>(res.gpu_series.size()),
+                          static_cast<double>(r.diff_series.size()),
+                          static_cast<double>(n_rate)};
+    std::memcpy(rep, v, sizeof(v));
+    for (std::size_t c = 0; c < C; ++c) {
+      const ClientReport& pc = r.per_client.at(names[c]);
+      double* o = cli + 6 * c;
+      o[0] = res.final_hf[c];
+      o[1] = pc.accumulated_service;
+      o[2] = pc.mean_service_rate;
+      o[3] = pc.ttft.p50;
+      o[4] = pc.ttft.p90;
+      o[5] = static_cast<double>(pc.ttft.count);
+      for (std::size_t w = 0; w < pc.service_rate_series.size() && static_cast<int64_t>(w) < win_cap; ++w)
+        rate[c * static_cast<std::size_t>(win_cap) + w] = pc.service_rate_series[w].value;
+    }
+    for (std::size_t w = 0; w < res.gpu_series.size() && static_cast<int64_t>(w) < win_cap; ++w) {
+      const GpuWindowSample& g = res.gpu_series[w];
+      win[4 * w + 0] = g.time_s;
+      win[4 * w + 1] = g.busy_ms;
+      win[4 * w + 2] = g.overhead_ms;
+      win[4 * w + 3] = g.gpu_util;
+    }
+    for (std::size_t k = 0; k < res.counter_series.size(); ++k) {
+      const std::size_t w = k / C;
+      if (static_cast<int64_t>(w) >= win_cap) break;
+      const CounterSample& cs = res.counter_series[k];
+      double* o = winc + 4 * (w * C + cs.client_index);
+      o[0] = cs.ufc;
+      o[1] = cs.rfc;
+      o[2] = cs.hf;
+      o[3] = cs.service_cum;
+    }
+    for (std::size_t w = 0; w < r.diff_series.size() && static_cast<int64_t>(w) < win_cap; ++w) {
+      diff[2 * w] = r.diff_series[w].time_s;
+      diff[2 * w + 1] = r.diff_series[w].value;
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    set_err(err, err_len, e.what());
+    return 1;
+  }
+}

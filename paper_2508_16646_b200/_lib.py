@@ -5,6 +5,8 @@ from __future__ import annotations
 import ctypes as C
 import os
 
+import numpy as np
+
 HERE = os.path.dirname(os.path.abspath(__file__))
 # EQX_LIB selects an instrumented build (csrc/Makefile `prof`: libeqx_b200_prof.so) for profiling
 LIB_PATH = os.environ.get("EQX_LIB") or os.path.join(HERE, "libeqx_b200.so")
@@ -73,14 +75,28 @@ class Replays(C.Structure):
     _fields_ = [("n_replays", C.c_int32), ("row_off", C.c_void_p), ("client", C.c_void_p),
                 ("arrival_s", C.c_void_p), ("input_tokens", C.c_void_p), ("true_output_tokens", C.c_void_p),
                 ("tag", C.c_void_p), ("id", C.c_void_p), ("alpha", C.c_void_p), ("max_sim_time_s", C.c_double),
-                ("ema_alpha", C.c_double), ("ev_cap", C.c_int64)]
+                ("ema_alpha", C.c_double), ("ev_cap", C.c_int64), ("report_window_s", C.c_double),
+                ("win_cap", C.c_int64)]
+
+
+REPORT_FIELDS = ("max_diff", "avg_diff", "var_diff", "jain_hf", "jain_ttft_p90", "throughput_tps", "mean_gpu_util",
+                 "ttft_p50", "ttft_p90", "latency_p50", "latency_p90", "ttft_count", "latency_count", "sim_end_s",
+                 "busy_ms_total", "overhead_ms_total", "completed", "rejected", "total_completed_tokens",
+                 "n_windows", "n_diff", "n_rate")
+REPORT_INT = {"ttft_count", "latency_count", "completed", "rejected", "total_completed_tokens", "n_windows", "n_diff",
+              "n_rate"}
+REPORT_DTYPE = np.dtype([(f, np.int64 if f in REPORT_INT else np.float64) for f in REPORT_FIELDS])
+CLIENT_FIELDS = ("final_hf", "accumulated_service", "mean_service_rate", "ttft_p50", "ttft_p90", "ttft_count")
+CLIENT_DTYPE = np.dtype([(f, np.int64 if f == "ttft_count" else np.float64) for f in CLIENT_FIELDS])
 
 
 class ReplayOut(C.Structure):
     _fields_ = [("n_events", C.c_void_p), ("ev_id", C.c_void_p), ("ev_kind", C.c_void_p), ("ev_time", C.c_void_p),
                 ("ufc", C.c_void_p), ("rfc", C.c_void_p), ("counter", C.c_void_p), ("completed", C.c_void_p),
                 ("sim_end", C.c_void_p), ("counter_clamps", C.c_void_p), ("status", C.c_void_p),
-                ("jain_ttft_p90", C.c_void_p), ("throughput_tps", C.c_void_p)]
+                ("jain_ttft_p90", C.c_void_p), ("throughput_tps", C.c_void_p), ("report", C.c_void_p),
+                ("clients", C.c_void_p), ("win", C.c_void_p), ("win_clients", C.c_void_p), ("diff", C.c_void_p),
+                ("rate", C.c_void_p)]
 
 
 _SIGS = {

@@ -1502,6 +1502,11 @@ eqx_status eqx_replay(eqx_ctx* ctx, const eqx_replays* R, eqx_replay_out* O) {
                o_evt = take(8 * n8 * cap), o_nev = take(8 * n8), o_comp = take(8 * n8), o_end = take(8 * n8),
                o_clamp = take(8 * n8), o_stat = take(4 * n8), o_u = take(8 * n8 * C), o_r = take(8 * n8 * C),
                o_k = take(8 * n8 * C), o_ttft = take(8 * rr), o_jain = take(8 * n8), o_tput = take(8 * n8);
+  const int64_t wcap = std::max<int64_t>(R->win_cap, 0);
+  const size_t w8 = static_cast<size_t>(wcap), c8 = static_cast<size_t>(C);
+  const size_t o_lat = take(8 * rr), o_rep = take(sizeof(eqx_replay_report) * n8),
+               o_rcl = take(sizeof(eqx_replay_client) * n8 * c8), o_win = take(8 * 4 * n8 * w8),
+               o_winc = take(8 * 4 * n8 * w8 * c8), o_diff = take(8 * 2 * n8 * w8), o_rate = take(8 * n8 * c8 * w8);
   CUDA_TRY(ctx, ctx->d_fb.ensure(off));
   char* b = static_cast<char*>(ctx->d_fb.p);
   auto up = [&](size_t o, const void* src, size_t bytes) {
@@ -1521,6 +1526,7 @@ eqx_status eqx_replay(eqx_ctx* ctx, const eqx_replays* R, eqx_replay_out* O) {
       for (int64_t k = R->row_off[i]; k < R->row_off[i + 1]; ++k) ids[k] = k - R->row_off[i];
   }
   CUDA_TRY(ctx, up(o_id, R->id ? static_cast<const void*>(R->id) : ids.data(), 8 * rows));
+  if (O->rate && wcap > 0) CUDA_TRY(ctx, cudaMemsetAsync(b + o_rate, 0, 8 * n8 * c8 * w8, s));
   ReplayArgs A;
   std::memset(&A, 0, sizeof(A));
   A.n_replays = nr;
@@ -1567,6 +1573,15 @@ eqx_status eqx_replay(eqx_ctx* ctx, const eqx_replays* R, eqx_replay_out* O) {
   A.f_ttft = reinterpret_cast<double*>(b + o_ttft);
   A.jain_ttft_p90 = reinterpret_cast<double*>(b + o_jain);
   A.throughput_tps = reinterpret_cast<double*>(b + o_tput);
+  A.window_s = R->report_window_s > 0.0 ? R->report_window_s : 1.0;  // EngineConfig default
+  A.win_cap = wcap;
+  A.f_lat = reinterpret_cast<double*>(b + o_lat);
+  A.report = reinterpret_cast<eqx_replay_report*>(b + o_rep);
+  A.rclients = reinterpret_cast<eqx_replay_client*>(b + o_rcl);
+  A.win = O->win && wcap > 0 ? reinterpret_cast<double*>(b + o_win) : nullptr;
+  A.win_clients = O->win_clients && wcap > 0 ? reinterpret_cast<double*>(b + o_winc) : nullptr;
+  A.diff = O->diff && wcap > 0 ? reinterpret_cast<double*>(b + o_diff) : nullptr;
+  A.rate = O->rate && wcap > 0 ? reinterpret_cast<double*>(b + o_rate) : nullptr;
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[2], s));
   replay_kernel<<<(nr + 3) / 4, 128, 0, s>>>(A);  // one warp per replay
   CUDA_TRY(ctx, cudaGetLastError());
@@ -1577,10 +1592,20 @@ eqx_status eqx_replay(eqx_ctx* ctx, const eqx_replays* R, eqx_replay_out* O) {
                       {O->counter, b + o_k, 8 * n8 * C},       {O->completed, b + o_comp, 8 * n8}};
   eqx_status st = read_cols(ctx, cols, 8);
   if (st != EQX_OK) return st;
-  const Col cols2[] = {{O->sim_end, b + o_end, 8 * n8}, {O->counter_clamps, b + o_clamp, 8 * n8},
-                       {O->status, b + o_stat, 4 * n8}, {O->jain_ttft_p90, b + o_jain, 8 * n8},
-                       {O->throughput_tps, b + o_tput, 8 * n8}};
-  return read_cols(ctx, cols2, 5);
+  const Col cols2[] = {{O->sim_end, b + o_end, 8 * n8},
+                       {O->counter_clamps, b + o_clamp, 8 * n8},
+                       {O->status, b + o_stat, 4 * n8},
+                       {O->jain_ttft_p90, b + o_jain, 8 * n8},
+                       {O->throughput_tps, b + o_tput, 8 * n8},
+                       {O->report, b + o_rep, sizeof(eqx_replay_report) * n8},
+                       {O->clients, b + o_rcl, sizeof(eqx_replay_client) * n8 * c8},
+                       {wcap > 0 ? O->win : nullptr, b + o_win, 8 * 4 * n8 * w8}};
+  st = read_cols(ctx, cols2, 8);
+  if (st != EQX_OK) return st;
+  const Col cols3[] = {{wcap > 0 ? O->win_clients : nullptr, b + o_winc, 8 * 4 * n8 * w8 * c8},
+                       {wcap > 0 ? O->diff : nullptr, b + o_diff, 8 * 2 * n8 * w8},
+                       {wcap > 0 ? O->rate : nullptr, b + o_rate, 8 * n8 * c8 * w8}};
+  return read_cols(ctx, cols3, 3);
 }
 
 // ---- live queues -----------------------------------------------------

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include "eqx_device.cuh"
+#include "../../include/eqx.h"
 
 namespace eqx {
 
@@ -325,6 +326,8 @@ __global__ void predict_rows_kernel(ScoreArgs a, int64_t r0, int64_t r1, LiveArg
 constexpr int kMaxReplayClients = 16;
 struct ReplayClient {
   double ufc, rfc, counter, weight;
+  double service;            // ClientState::accumulated_service
+  double bucket, merged;     // service of the current rate window; previous + current window
   int32_t running, backlogged;
   uint32_t order;            // rank of client_id (select_next tie-break)
   int32_t qbase, qhead, qend;  // FIFO over the client's rows: [qhead, qend) of crow
@@ -377,6 +380,16 @@ struct ReplayArgs {
   double* f_ttft;             // [rows] first-token latency per request (-1: none)
   double* jain_ttft_p90;      // [n_replays]
   double* throughput_tps;     // [n_replays]
+  // reporting (engine.cpp:379-430, metrics.cpp:151-229)
+  double window_s;
+  int64_t win_cap;
+  double* f_lat;              // [rows] end-to-end latency of completed requests (-1: none)
+  eqx_replay_report* report;  // [n_replays]
+  eqx_replay_client* rclients;  // [n_replays][C]
+  double* win;                // [n_replays][win_cap][4]
+  double* win_clients;        // [n_replays][win_cap][C][4]
+  double* diff;               // [n_replays][win_cap][2]
+  double* rate;               // [n_replays][C][win_cap] (zeroed by the host)
 };
 __global__ void replay_kernel(ReplayArgs a);
 

@@ -10,7 +10,12 @@
 // The scalar engine logic runs uniformly on all 32 lanes (identical values, identical stores:
 // no divergence between replays of a warp, as one-thread-per-replay had), and the loops over
 // batch members (reservations, decode step, completion scan and erase) are split across lanes.
-// Reporting windows (advance_clock's samples) do not change the schedule and are not produced.
+// The reporting side follows the run on the same warp: the engine's window samples
+// (advance_clock / emit_window_samples, engine.cpp:379-430) at every clock advance, the
+// service-difference samples and per-client service-rate windows of build_report (metrics.cpp:
+// 21-69,199-226) online at each completion (the event log is in time order, so a sample at
+// window end t sees exactly the completions logged at or before t), and the percentile /
+// Jain reductions at the end by radix selection over the per-request TTFT and latency.
 #include <cstdint>
 
 #include "eqx_device.cuh"
@@ -37,10 +42,200 @@ __device__ __forceinline__ int64_t warp_sum64(int64_t v) {
   return v;
 }
 
+// k-th smallest (1-based) of the non-negative values get(j), j in [0, m) (negative = absent):
+// MSB-first radix select on the FP64 bit patterns (monotone for values >= 0), one byte per
+// pass through a warp-private 256-bin shared-memory histogram (8 passes over the values).
+template <class Get>
+__device__ double warp_kth(Get get, int64_t m, int64_t k, uint32_t* hist) {
+  const int lane = threadIdx.x & 31;
+  uint64_t prefix = 0;
+  uint32_t kk = static_cast<uint32_t>(k);
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int b = lane; b < 256; b += 32) hist[b] = 0;
+    __syncwarp();
+    const uint64_t hmask = shift == 56 ? 0ull : (~0ull << (shift + 8));
+    for (int64_t j = lane; j < m; j += 32) {
+      const double v = get(j);
+      if (v < 0.0) continue;
+      const uint64_t u = static_cast<uint64_t>(__double_as_longlong(v));
+      if ((u & hmask) == prefix) atomicAdd(&hist[(u >> shift) & 255u], 1u);
+    }
+    __syncwarp();
+    uint32_t c[8], sum = 0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      c[t] = hist[8 * lane + t];
+      sum += c[t];
+    }
+    uint32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t x = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += x;
+    }
+    const uint32_t excl = incl - sum;
+    const bool mine = excl < kk && kk <= incl;
+    uint32_t digit = 0, rest = 0;
+    if (mine) {
+      uint32_t acc = excl;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        if (acc + c[t] >= kk && digit == 0 && rest == 0) {
+          digit = 8 * lane + t + 1;  // +1: found marker
+          rest = kk - acc;
+        }
+        acc += c[t];
+      }
+    }
+    const int src = __ffs(__ballot_sync(0xffffffffu, mine)) - 1;
+    digit = __shfl_sync(0xffffffffu, digit, src) - 1;
+    kk = __shfl_sync(0xffffffffu, rest, src);
+    prefix |= static_cast<uint64_t>(digit) << shift;
+    __syncwarp();
+  }
+  return __longlong_as_double(static_cast<long long>(prefix));
+}
+
+// percentile_stats (metrics.cpp:76-91): nearest rank ceil(pct / 100 * count), clamped to [1, count]
+template <class Get>
+__device__ void warp_percentiles(Get get, int64_t m, double* p50, double* p90, int64_t* count, uint32_t* hist) {
+  int64_t cnt = 0;
+  for (int64_t j = threadIdx.x & 31; j < m; j += 32) cnt += get(j) >= 0.0 ? 1 : 0;
+  cnt = warp_sum64(cnt);
+  *count = cnt;
+  *p50 = 0.0;
+  *p90 = 0.0;
+  if (cnt == 0) return;
+  auto rank = [&](double pct) {
+    int64_t r = static_cast<int64_t>(ceil(__dmul_rn(__ddiv_rn(pct, 100.0), static_cast<double>(cnt))));
+    return r < 1 ? int64_t(1) : (r > cnt ? cnt : r);
+  };
+  *p50 = warp_kth(get, m, rank(50.0), hist);
+  *p90 = warp_kth(get, m, rank(90.0), hist);
+}
+
+// Reporting state of one replay (uniform across the warp's lanes, like the engine state).
+struct Reporter {
+  int r, C, norm_mode;
+  double alpha, beta, ws;
+  int64_t wcap;
+  double *win, *win_clients, *diff, *rate;
+  double window_start, win_busy, win_ovh;  // advance_clock's open window
+  int64_t n_win;
+  double sd_t, sd_sum, sd_sq, sd_max;      // service_difference
+  int64_t n_diff;
+  int64_t rate_w;                          // current service-rate window (-1: none yet)
+};
+
+__device__ __forceinline__ void all_maxima(const ReplayClient* cl, int C, double& mu, double& mr) {
+  mu = 0.0;  // metric_hf's Normalizers over all clients (std::max keeps the first on ties)
+  mr = 0.0;
+  for (int i = 0; i < C; ++i) {
+    if (mu < cl[i].ufc) mu = cl[i].ufc;
+    if (mr < cl[i].rfc) mr = cl[i].rfc;
+  }
+}
+
+// metric_hf (scheduler.cpp:68-81) for one client, combine() in the reference's order
+__device__ __forceinline__ double metric_hf(const Reporter& R, const ReplayClient& c, double mu, double mr) {
+  if (R.norm_mode == 1) return __dadd_rn(__dmul_rn(R.alpha, c.ufc), __dmul_rn(R.beta, c.rfc));
+  const double u = mu > 0.0 ? __ddiv_rn(c.ufc, mu) : 0.0;
+  const double v = mr > 0.0 ? __ddiv_rn(c.rfc, mr) : 0.0;
+  return __dadd_rn(__dmul_rn(R.alpha, u), __dmul_rn(R.beta, v));
+}
+
+// emit_window_samples (engine.cpp:409-430): the GPU sample and one counter sample per client
+__device__ __noinline__ void rep_emit(Reporter& R, const ReplayClient* cl, double time_s, double len_s) {
+  const int lane = threadIdx.x & 31;
+  if (R.n_win < R.wcap) {
+    if (R.win && lane == 0) {
+      double* w = R.win + (static_cast<int64_t>(R.r) * R.wcap + R.n_win) * 4;
+      w[0] = time_s;
+      w[1] = R.win_busy;
+      w[2] = R.win_ovh;
+      w[3] = len_s > 0.0 ? __ddiv_rn(R.win_busy, __dmul_rn(len_s, 1000.0)) : 0.0;
+    }
+    if (R.win_clients) {
+      double mu, mr;
+      all_maxima(cl, R.C, mu, mr);
+      double* w = R.win_clients + (static_cast<int64_t>(R.r) * R.wcap + R.n_win) * R.C * 4;
+      for (int c = lane; c < R.C; c += 32) {
+        w[4 * c + 0] = cl[c].ufc;
+        w[4 * c + 1] = cl[c].rfc;
+        w[4 * c + 2] = metric_hf(R, cl[c], mu, mr);
+        w[4 * c + 3] = cl[c].service;
+      }
+    }
+  }
+  ++R.n_win;
+  R.win_busy = 0.0;
+  R.win_ovh = 0.0;
+}
+
+// advance_clock's general path (engine.cpp:379-399): the span split pro rata over the windows
+// it crosses, one sample per closed window
+__device__ __noinline__ void rep_clock_cross(Reporter& R, const ReplayClient* cl, double t_from, double t_to,
+                                             double busy_ms, double ovh_ms) {
+  const double span = __dsub_rn(t_to, t_from);
+  double t = t_from;
+  while (t < t_to) {
+    const double window_end = __dadd_rn(R.window_start, R.ws);
+    const double cut = window_end < t_to ? window_end : t_to;
+    const double frac = __ddiv_rn(__dsub_rn(cut, t), span);
+    R.win_busy = __dadd_rn(R.win_busy, __dmul_rn(busy_ms, frac));
+    R.win_ovh = __dadd_rn(R.win_ovh, __dmul_rn(ovh_ms, frac));
+    if (cut == window_end) {
+      rep_emit(R, cl, window_end, R.ws);
+      R.window_start = window_end;
+    }
+    t = cut;
+  }
+}
+
+// service_difference's sample_diff (metrics.cpp:39-46): max - min accumulated service
+__device__ __noinline__ void rep_sample_diff(Reporter& R, const ReplayClient* cl, double t) {
+  double lo = cl[0].service, hi = cl[0].service;
+  for (int c = 1; c < R.C; ++c) {
+    if (cl[c].service < lo) lo = cl[c].service;
+    if (!(cl[c].service < hi)) hi = cl[c].service;
+  }
+  const double d = __dsub_rn(hi, lo);
+  if (R.diff && R.n_diff < R.wcap && (threadIdx.x & 31) == 0) {
+    R.diff[(static_cast<int64_t>(R.r) * R.wcap + R.n_diff) * 2] = t;
+    R.diff[(static_cast<int64_t>(R.r) * R.wcap + R.n_diff) * 2 + 1] = d;
+  }
+  if (R.sd_max < d) R.sd_max = d;
+  R.sd_sum = __dadd_rn(R.sd_sum, d);
+  R.sd_sq = __dadd_rn(R.sd_sq, __dmul_rn(d, d));
+  ++R.n_diff;
+}
+
+// the samples at window ends t < now (they precede a completion logged at now)
+__device__ __noinline__ void rep_diff_until(Reporter& R, const ReplayClient* cl, double now) {
+  while (R.sd_t < now) {
+    rep_sample_diff(R, cl, R.sd_t);
+    R.sd_t = __dadd_rn(R.sd_t, R.ws);
+  }
+}
+
+// a completion opened service-rate window w > the current one: close the current window and
+// restart the previous + current sums (the last window absorbs completions at the very end)
+__device__ __noinline__ void rep_rate_advance(Reporter& R, ReplayClient* cl, int64_t w) {
+  for (int k = 0; k < R.C; ++k) {
+    if (R.rate && R.rate_w >= 0 && R.rate_w < R.wcap && (threadIdx.x & 31) == 0)
+      R.rate[static_cast<int64_t>(k) * R.wcap + R.rate_w] = cl[k].bucket;
+    cl[k].merged = (R.rate_w >= 0 && w == R.rate_w + 1) ? cl[k].bucket : 0.0;
+    cl[k].bucket = 0.0;
+  }
+  R.rate_w = w;
+}
+
 __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
+  __shared__ uint32_t s_hist[4][256];  // radix-select histograms, one per warp
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (r >= A.n_replays) return;  // warp-uniform
+  uint32_t* hist = s_hist[threadIdx.x >> 5];
   const ModelTables& M = *A.model;
   const Policy P = A.pol;
   const int32_t C = A.C;
@@ -57,8 +252,12 @@ __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
   double* f_preds = A.f_preds + t0;
   double* f_rfc = A.f_rfc + t0;
   double* f_ttft = A.f_ttft + t0;
-  for (int64_t i = lane; i < n; i += 32) f_ttft[i] = -1.0;
-  int64_t completed_tokens = 0;
+  double* f_lat = A.f_lat + t0;
+  for (int64_t i = lane; i < n; i += 32) {
+    f_ttft[i] = -1.0;
+    f_lat[i] = -1.0;
+  }
+  int64_t completed_tokens = 0, rejected = 0;
   // Ledger, FIFO cursors and profile are private per lane (identical copies, updated uniformly),
   // so the read-modify-write engine steps need no intra-warp synchronisation; the batch lives
   // in global scratch, split across lanes.
@@ -104,6 +303,47 @@ __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
   int32_t members = 0;
   bool comp_changed = false;
   int32_t status = 0;
+  // ---- reporting state (the rare paths are out-of-line: the hot loop's code stays small) ----
+  const double ws = A.window_s;
+  const int64_t wcap = A.win_cap;
+  Reporter R;
+  R.r = r;
+  R.C = C;
+  R.norm_mode = P.norm_mode;
+  R.alpha = eq.alpha;
+  R.beta = eq.beta;
+  R.ws = ws;
+  R.wcap = wcap;
+  R.win = A.win;
+  R.win_clients = A.win_clients;
+  R.diff = A.diff;
+  R.rate = A.rate ? A.rate + static_cast<int64_t>(r) * C * wcap : nullptr;
+  R.window_start = R.win_busy = R.win_ovh = 0.0;
+  R.n_win = 0;
+  R.sd_t = ws;
+  R.sd_sum = R.sd_sq = R.sd_max = 0.0;
+  R.n_diff = 0;
+  R.rate_w = -1;
+  // advance_clock (engine.cpp:379-399).  Within one window the single segment's fraction is
+  // span / span = 1 exactly, so busy / overhead add as they are; crossings take the general
+  // pro-rata loop with its window samples.
+  double w_end = ws, w_busy = 0.0, w_ovh = 0.0;  // register copies of the open window
+  auto advance_clock = [&](double t_from, double t_to, double busy_ms, double ovh_ms) {
+    busy_cum = __dadd_rn(busy_cum, busy_ms);
+    ovh_cum = __dadd_rn(ovh_cum, ovh_ms);
+    if (t_to <= t_from) return;
+    if (w_end > t_to) {
+      w_busy = __dadd_rn(w_busy, busy_ms);
+      w_ovh = __dadd_rn(w_ovh, ovh_ms);
+      return;
+    }
+    R.win_busy = w_busy;
+    R.win_ovh = w_ovh;
+    rep_clock_cross(R, cl, t_from, t_to, busy_ms, ovh_ms);
+    w_busy = R.win_busy;
+    w_ovh = R.win_ovh;
+    w_end = __dadd_rn(R.window_start, ws);
+  };
   int64_t* ev_id = A.ev_id + static_cast<int64_t>(r) * A.ev_cap;
   int32_t* ev_kind = A.ev_kind + static_cast<int64_t>(r) * A.ev_cap;
   double* ev_time = A.ev_time + static_cast<int64_t>(r) * A.ev_cap;
@@ -199,6 +439,7 @@ __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
       // fits_alone (gpu_model.cpp:69-72): the can_fit test on an empty batch
       if (!((1 <= P.max_batch) && __dmul_rn(static_cast<double>(static_cast<int64_t>(in) + pred), P.m) <= P.M)) {
         log_ev(id[row], 2);
+        ++rejected;
         pop_head(c);
         continue;
       }
@@ -251,7 +492,8 @@ __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
       if (arrival_idx >= n) break;
       const double next_t = __dadd_rn(arrival[arrival_idx], 0.0);
       if (next_t >= max_sim) break;
-      now = next_t;  // advance_clock(now, next_t, 0, 0)
+      advance_clock(now, next_t, 0.0, 0.0);
+      now = next_t;
       drain(now);
     }
     const int64_t new_prefill = admit();
@@ -268,8 +510,7 @@ __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
     const double overhead_ms = comp_changed ? A.refresh_ms : 0.0;
     const double busy_ms = __dsub_rn(iter_ms, overhead_ms);
     const double t_end = __dadd_rn(now, __ddiv_rn(iter_ms, 1000.0));
-    busy_cum = __dadd_rn(busy_cum, busy_ms);
-    ovh_cum = __dadd_rn(ovh_cum, overhead_ms);
+    advance_clock(now, t_end, busy_ms, overhead_ms);
     now = t_end;
     comp_changed = false;
     for (int j = lane; j < members; j += 32) {
@@ -319,6 +560,8 @@ __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
         const double util = __ddiv_rn(busy_span, __dadd_rn(busy_span, ovh_span));
         ++completed;
         completed_tokens += static_cast<int64_t>(m.in) + out;
+        if (lane == 0) f_lat[m.row] = latency_s;
+        if (C >= 2 && R.sd_t < now) rep_diff_until(R, cl, now);  // windows closed before this completion
         // on_complete (scheduler.cpp:192-233)
         const double wt = __dadd_rn(static_cast<double>(m.in), __dmul_rn(P.ow, static_cast<double>(out)));
         const double wwt = __dmul_rn(w, wt);
@@ -336,6 +579,13 @@ __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
         }
         cl[c].ufc = u;
         cl[c].rfc = v;
+        cl[c].service = __dadd_rn(cl[c].service, wwt);  // accumulated_service (scheduler.cpp:232)
+        {  // build_report's service-rate window of this completion: weight * (in + ow * out), same value
+          const int64_t w = static_cast<int64_t>(__ddiv_rn(now, ws));
+          if (w > R.rate_w) rep_rate_advance(R, cl, w);
+          cl[c].bucket = __dadd_rn(cl[c].bucket, wwt);
+          cl[c].merged = __dadd_rn(cl[c].merged, wwt);
+        }
         if (P.kind == kVtc && P.vtc_use_prediction) {
           double k = __dadd_rn(cl[c].counter, __dsub_rn(wwt, m.p_vtc));
           if (k < 0.0) {
@@ -366,10 +616,68 @@ __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
     }
     members = kept;
   }
-  // ---- build_report's sweep metrics (metrics.cpp:76-105,170-189) ----
+  // ---- end of run (engine.cpp:137-145): flush_window, then build_report (metrics.cpp:151-229) ----
+  R.win_busy = w_busy;
+  R.win_ovh = w_ovh;
+  if (now > R.window_start) rep_emit(R, cl, now, __dsub_rn(now, R.window_start));  // flush_window
+  __syncwarp();
+  eqx_replay_report rep{};
+  rep.sim_end_s = now;
+  rep.busy_ms_total = busy_cum;
+  rep.overhead_ms_total = ovh_cum;
+  rep.completed = completed;
+  rep.rejected = rejected;
+  rep.total_completed_tokens = completed_tokens;
+  rep.n_windows = R.n_win;
+  if (C >= 2) {  // service_difference: the remaining windows up to the end, then the moments
+    const double lim = __dadd_rn(now, 1e-12);
+    while (R.sd_t <= lim) {
+      rep_sample_diff(R, cl, R.sd_t);
+      R.sd_t = __dadd_rn(R.sd_t, ws);
+    }
+    if (R.n_diff == 0) rep_sample_diff(R, cl, now);
+    const double nd = static_cast<double>(R.n_diff);
+    rep.max_diff = R.sd_max;
+    rep.avg_diff = __ddiv_rn(R.sd_sum, nd);
+    rep.var_diff = __dsub_rn(__ddiv_rn(R.sd_sq, nd), __dmul_rn(rep.avg_diff, rep.avg_diff));
+    if (rep.var_diff < 0.0) rep.var_diff = 0.0;
+    rep.n_diff = R.n_diff;
+  }
+  {  // jain_hf over final_hf = metric_hf(final_clients), roster order
+    double mu, mr, sum = 0.0, sum_sq = 0.0;
+    all_maxima(cl, C, mu, mr);
+    for (int c = 0; c < C; ++c) {
+      const double h = metric_hf(R, cl[c], mu, mr);
+      if (A.rclients && lane == 0) A.rclients[static_cast<int64_t>(r) * C + c].final_hf = h;
+      sum = __dadd_rn(sum, h);
+      sum_sq = __dadd_rn(sum_sq, __dmul_rn(h, h));
+    }
+    rep.jain_hf = sum_sq == 0.0 ? 1.0 : __ddiv_rn(__dmul_rn(sum, sum), __dmul_rn(static_cast<double>(C), sum_sq));
+  }
+  // per-client service-rate windows: n_windows = max(1, ceil(sim_end / ws - 1e-12))
+  const int64_t n_rate = static_cast<int64_t>(fmax(1.0, ceil(__dsub_rn(__ddiv_rn(now, ws), 1e-12))));
+  rep.n_rate = n_rate;
+  if (double* rate = R.rate) {
+    const int64_t rate_w = R.rate_w;
+    if (rate_w >= 0 && lane == 0)
+      for (int k = 0; k < C; ++k) {
+        if (rate_w < n_rate) {
+          if (rate_w < wcap) rate[static_cast<int64_t>(k) * wcap + rate_w] = cl[k].bucket;
+        } else if (n_rate - 1 < wcap) {  // completions at the very end fell past the last window
+          rate[static_cast<int64_t>(k) * wcap + n_rate - 1] = cl[k].merged;
+          if (rate_w < wcap) rate[static_cast<int64_t>(k) * wcap + rate_w] = 0.0;
+        }
+      }
+    __syncwarp();
+    const int64_t kept = n_rate < wcap ? n_rate : wcap;
+    for (int64_t j = lane; j < static_cast<int64_t>(C) * kept; j += 32) {
+      double* x = rate + (j / kept) * wcap + (j % kept);
+      *x = __ddiv_rn(*x, ws);
+    }
+  }
   {
-    // per-client p90 TTFT (percentile_stats: nearest rank ceil(0.9 n)), clients in client_id
-    // order (the std::map of ttft_stats), Jain index over those with any first token
+    // per-client TTFT percentiles (ttft_stats' per_client map); jain_ttft_p90 over the clients
+    // with any first token, in client_id order
     double sum = 0.0, sum_sq = 0.0;
     int32_t m_clients = 0;
     for (uint32_t rank = 0; rank < static_cast<uint32_t>(C); ++rank) {
@@ -377,32 +685,20 @@ __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
       for (int i = 0; i < C; ++i)
         if (cl[i].order == rank) c = i;
       if (c < 0) continue;
-      // rows of client c: crow[qbase[c] .. qbase[c + 1])
-      int64_t cnt = 0;
       const int32_t c_rows = (c + 1 < C ? cl[c + 1].qbase : static_cast<int32_t>(n)) - cl[c].qbase;
-      for (int32_t j = lane; j < c_rows; j += 32) cnt += f_ttft[crow[cl[c].qbase + j]] >= 0.0 ? 1 : 0;
-      cnt = warp_sum64(cnt);
-      if (cnt == 0) continue;
-      int64_t k = static_cast<int64_t>(ceil(__dmul_rn(__ddiv_rn(90.0, 100.0), static_cast<double>(cnt))));
-      k = k < 1 ? 1 : (k > cnt ? cnt : k);
-      uint64_t prefix = 0, mask = 0;  // k-th smallest by MSB-first radix select on the bits
-      for (int bit = 63; bit >= 0; --bit) {
-        const uint64_t b = 1ull << bit;
-        int64_t zeros = 0;
-        for (int32_t j = lane; j < c_rows; j += 32) {
-          const double v = f_ttft[crow[cl[c].qbase + j]];
-          if (v < 0.0) continue;
-          const uint64_t u = static_cast<uint64_t>(__double_as_longlong(v));
-          zeros += ((u & mask) == prefix && !(u & b)) ? 1 : 0;
-        }
-        zeros = warp_sum64(zeros);
-        if (zeros < k) {
-          k -= zeros;
-          prefix |= b;
-        }
-        mask |= b;
+      const int32_t* rows_c = crow + cl[c].qbase;
+      double p50, p90;
+      int64_t cnt;
+      warp_percentiles([&](int64_t j) { return f_ttft[rows_c[j]]; }, c_rows, &p50, &p90, &cnt, hist);
+      if (A.rclients && lane == 0) {
+        eqx_replay_client& o = A.rclients[static_cast<int64_t>(r) * C + c];
+        o.accumulated_service = cl[c].service;
+        o.mean_service_rate = now > 0.0 ? __ddiv_rn(cl[c].service, now) : 0.0;
+        o.ttft_p50 = p50;
+        o.ttft_p90 = p90;
+        o.ttft_count = cnt;
       }
-      const double p90 = __longlong_as_double(static_cast<long long>(prefix));
+      if (cnt == 0) continue;
       sum = __dadd_rn(sum, p90);
       sum_sq = __dadd_rn(sum_sq, __dmul_rn(p90, p90));
       ++m_clients;
@@ -410,8 +706,16 @@ __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
     double jain = 1.0;  // no first tokens: 1.0 (metrics.cpp:176); jain_index: all-zero -> 1.0
     if (m_clients > 0 && sum_sq != 0.0)
       jain = __ddiv_rn(__dmul_rn(sum, sum), __dmul_rn(static_cast<double>(m_clients), sum_sq));
+    rep.jain_ttft_p90 = jain;
+    rep.throughput_tps = now > 0.0 ? __ddiv_rn(static_cast<double>(completed_tokens), now) : 0.0;
+    rep.mean_gpu_util = now > 0.0 ? __ddiv_rn(busy_cum, __dmul_rn(now, 1000.0)) : 0.0;
     A.jain_ttft_p90[r] = jain;
-    A.throughput_tps[r] = now > 0.0 ? __ddiv_rn(static_cast<double>(completed_tokens), now) : 0.0;
+    A.throughput_tps[r] = rep.throughput_tps;
+  }
+  if (A.report) {
+    warp_percentiles([&](int64_t j) { return f_ttft[j]; }, n, &rep.ttft_p50, &rep.ttft_p90, &rep.ttft_count, hist);
+    warp_percentiles([&](int64_t j) { return f_lat[j]; }, n, &rep.latency_p50, &rep.latency_p90, &rep.latency_count, hist);
+    if (lane == 0) A.report[r] = rep;
   }
   A.n_events[r] = n_ev;
   A.completed[r] = completed;

@@ -510,11 +510,18 @@ class GpuScheduler:
 
     # -- batched engine replays --
     def replay(self, row_off, client, arrival_s, input_tokens, true_output_tokens, alpha, tag=None, ids=None,
-               max_sim_time_s: float = 0.0, ema_alpha: float = 0.2, ev_cap: int = 4096) -> dict:
+               max_sim_time_s: float = 0.0, ema_alpha: float = 0.2, ev_cap: int = 4096,
+               report_window_s: float = 1.0, win_cap: int = 0) -> dict:
         """run_simulation (engine.cpp:119-146) for many traces at once on the GPU, one replay per
-        thread: traces concatenated (row_off[r]..row_off[r+1]), per-replay alpha, the
+        warp: traces concatenated (row_off[r]..row_off[r+1]), per-replay alpha, the
         scheduler's policy / perf / profile / predictor / roster otherwise.  Returns the
-        admitted/rejected event logs (id, kind, time), final ledgers and run statistics."""
+        admitted/rejected event logs (id, kind, time), final ledgers and run statistics, and
+        build_report's SimReport per replay ("report": a structured array with the fields of
+        eqx_replay_report; "clients": [replay][client] ClientReport fields, roster order).
+        With win_cap > 0 also the series, each cut at win_cap windows: "win" [r][w][4] (time,
+        busy_ms, overhead_ms, gpu_util: SimResult::gpu_series), "win_clients" [r][w][C][4] (ufc,
+        rfc, hf, service_cum: counter_series), "diff" [r][w][2] (diff_series) and "rate"
+        [r][C][w] (service_rate_series values; window w ends at report_window_s * (w + 1))."""
         n = len(alpha)
         nc = len(self.client_ids)
         cols = {"row_off": np.ascontiguousarray(row_off, np.int64), "client": np.ascontiguousarray(client, np.int32),
@@ -525,17 +532,25 @@ class GpuScheduler:
                 "tag": None if tag is None else np.ascontiguousarray(tag, np.uint8),
                 "id": None if ids is None else np.ascontiguousarray(ids, np.int64)}
         ptr = {k: (v.ctypes.data if v is not None else None) for k, v in cols.items()}
+        if report_window_s <= 0.0:
+            raise ConfigError("'engine.report_window_s' must be > 0")
+        wc = max(int(win_cap), 0)
         rq = L.Replays(n, ptr["row_off"], ptr["client"], ptr["arrival_s"], ptr["input_tokens"],
                        ptr["true_output_tokens"], ptr["tag"], ptr["id"], ptr["alpha"], float(max_sim_time_s),
-                       float(ema_alpha), int(ev_cap))
+                       float(ema_alpha), int(ev_cap), float(report_window_s), wc)
         out = {"n_events": np.zeros(n, np.int64), "ev_id": np.zeros((n, ev_cap), np.int64),
                "ev_kind": np.zeros((n, ev_cap), np.int32), "ev_time": np.zeros((n, ev_cap)),
                "ufc": np.zeros((n, nc)), "rfc": np.zeros((n, nc)), "counter": np.zeros((n, nc)),
                "completed": np.zeros(n, np.int64), "sim_end": np.zeros(n), "counter_clamps": np.zeros(n, np.int64),
-               "status": np.zeros(n, np.int32), "jain_ttft_p90": np.zeros(n), "throughput_tps": np.zeros(n)}
-        ro = L.ReplayOut(*(out[k].ctypes.data for k in ("n_events", "ev_id", "ev_kind", "ev_time", "ufc", "rfc",
-                                                          "counter", "completed", "sim_end", "counter_clamps",
-                                                          "status", "jain_ttft_p90", "throughput_tps")))
+               "status": np.zeros(n, np.int32), "jain_ttft_p90": np.zeros(n), "throughput_tps": np.zeros(n),
+               "report": np.zeros(n, L.REPORT_DTYPE), "clients": np.zeros((n, nc), L.CLIENT_DTYPE)}
+        if wc:
+            out.update(win=np.zeros((n, wc, 4)), win_clients=np.zeros((n, wc, nc, 4)), diff=np.zeros((n, wc, 2)),
+                       rate=np.zeros((n, nc, wc)))
+        names = ("n_events", "ev_id", "ev_kind", "ev_time", "ufc", "rfc", "counter", "completed", "sim_end",
+                 "counter_clamps", "status", "jain_ttft_p90", "throughput_tps", "report", "clients", "win",
+                 "win_clients", "diff", "rate")
+        ro = L.ReplayOut(*((out[k].ctypes.data if k in out else None) for k in names))
         self._check(self._lib.eqx_replay(self._ctx, C.byref(rq), C.byref(ro)))
         if np.any(out["status"] == 2):
             raise EngineError("KV memory bound violated in replay(s) " + str(np.nonzero(out["status"] == 2)[0][:8]))

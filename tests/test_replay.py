@@ -127,3 +127,74 @@ def test_sweep_metrics_match_reference_build_report():
     w5 = H.ref_replay_report(case)
     _, g5 = run_both([q], [0.6], pred_kind=0)
     assert g5["jain_ttft_p90"][0] == w5["jain_ttft_p90"] and g5["throughput_tps"][0] == w5["throughput_tps"]
+
+
+def run_full(traces, alphas, window_s=1.0, win_cap=128, max_sim=0.0, **kw):
+    from paper_2508_16646_b200 import scheduler as S
+    base = dict(model=default_model(), profile=default_profile())
+    base.update(kw)
+    cases = [H.StepCase(client=q["client"], arrival=q["arrival"], in_tokens=q["in_tokens"], true_out=q["true_out"],
+                        tag=q["tag"], client_names=q["client_names"], alpha=float(a), **base)
+             for q, a in zip(traces, alphas)]
+    want = [H.ref_replay_full(c, max_sim_time_s=max_sim, window_s=window_s, win_cap=win_cap) for c in cases]
+    sch = S.GpuScheduler(case_clients(cases[0]), running=np.zeros(len(cases[0].client_names), np.int32),
+                         **case_kwargs(cases[0]))
+    row_off = np.concatenate([[0], np.cumsum([len(q["client"]) for q in traces])])
+    cat = {k: np.concatenate([np.asarray(q[k]) for q in traces]) for k in ("client", "arrival", "in_tokens", "true_out")}
+    tag = np.concatenate([np.where(np.asarray(q["tag"]) < 0, 0, np.asarray(q["tag"]) + 1) for q in traces])
+    got = sch.replay(row_off, cat["client"], cat["arrival"], cat["in_tokens"], cat["true_out"], alphas,
+                     tag=tag.astype(np.uint8), ema_alpha=0.2, ev_cap=1, max_sim_time_s=max_sim,
+                     report_window_s=window_s, win_cap=win_cap)
+    return want, got
+
+
+def check_full(want, got, win_cap):
+    for i, w in enumerate(want):
+        rep = got["report"][i]
+        for k, v in w["report"].items():
+            assert rep[k] == v, f"replay {i} report.{k}: {rep[k]!r} vs {v!r}"
+        for k, v in w["clients"].items():
+            np.testing.assert_array_equal(got["clients"][k][i], v, err_msg=f"replay {i} clients.{k}")
+        nw, nd, nr = (min(int(rep[k]), win_cap) for k in ("n_windows", "n_diff", "n_rate"))
+        np.testing.assert_array_equal(got["win"][i, :nw], w["win"][:nw], err_msg=f"replay {i} gpu_series")
+        np.testing.assert_array_equal(got["win_clients"][i, :nw], w["win_clients"][:nw],
+                                      err_msg=f"replay {i} counter_series")
+        np.testing.assert_array_equal(got["diff"][i, :nd], w["diff"][:nd], err_msg=f"replay {i} diff_series")
+        np.testing.assert_array_equal(got["rate"][i, :, :nr], w["rate"][:, :nr], err_msg=f"replay {i} service rates")
+
+
+@pytest.mark.parametrize("window_s", [1.0, 0.25, 0.7])
+def test_full_report_preset_sweep(window_s):
+    """build_report (metrics.cpp:151-229) and the engine's window samples (engine.cpp:379-430),
+    every field and series bit-exact against the reference objects, over an alpha grid."""
+    alphas = [0.5, 0.65, 0.85]
+    traces = [preset_trace(400 + i, duration=12.0) for i in range(3)]
+    want, got = run_full(traces, alphas, window_s=window_s, win_cap=128, pred_kind=0)
+    check_full(want, got, 128)
+    assert all(w["report"]["n_diff"] >= 10 for w in want)
+
+
+@pytest.mark.parametrize("over", [{}, {"kind": 1}, {"kind": 0, "max_batch": 8}, {"norm_mode": 1},
+                                  {"pred_kind": 1}, {"backfill": True, "max_batch": 6}])
+def test_full_report_policies(over):
+    kw = dict(pred_kind=0)
+    kw.update(over)
+    traces = [poisson_trace(500 + s, n_clients=5, rate=250.0, duration=4.0) for s in range(2)]
+    want, got = run_full(traces, [0.4, 0.8], window_s=0.5, win_cap=64, **kw)
+    check_full(want, got, 64)
+
+
+def test_full_report_cutoff_caps_and_single_client():
+    # max_sim_time_s cuts the run mid-window; a small win_cap truncates the series only
+    traces = [poisson_trace(600, n_clients=4, rate=300.0, duration=5.0)]
+    want, got = run_full(traces, [0.7], window_s=0.3, win_cap=5, max_sim=3.3, pred_kind=0)
+    check_full(want, got, 5)
+    assert want[0]["report"]["n_windows"] > 5
+    # one client: service_difference is undefined, the report keeps zeros there
+    q = preset_trace(601, duration=8.0)
+    keep = q["client"] == 0
+    one = {k: (np.asarray(v)[keep] if isinstance(v, np.ndarray) else v) for k, v in q.items()}
+    one["client_names"] = ["client1"]
+    want, got = run_full([one], [0.7], window_s=1.0, win_cap=32, pred_kind=0)
+    check_full(want, got, 32)
+    assert got["report"]["n_diff"][0] == 0 and got["report"]["max_diff"][0] == 0.0
