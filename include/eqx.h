@@ -280,6 +280,41 @@ eqx_status eqx_set_timing(eqx_ctx* ctx, double prefill_linear_ms, double prefill
                           double decode_per_ctx_ms, double refresh_ms);
 eqx_status eqx_replay(eqx_ctx* ctx, const eqx_replays* replays, eqx_replay_out* out);
 
+/* ---- request traces (the trace formats) --------------------------------
+ * load_trace (workload.cpp:312-400) -- the reference's CSV format with its validation and
+ * ParseError messages ("trace line N: ..."), stable re-sort of out-of-order rows (one warning),
+ * client roster in first-appearance order -- plus write_trace_csv / trace_hash (FNV-1a of the
+ * canonical CSV, 16 hex digits; workload.cpp:405-428) and a binary struct-of-arrays format that
+ * records the hash and loads straight into the pinned host arena (eqx_host_alloc).  Columns are
+ * the eqx_requests layout: pass them to eqx_stage_async / eqx_drain as EQX_HOST columns.
+ * Errors: EQX_ERR_PARSE with the reference's message in err (ParseError). */
+typedef struct eqx_trace eqx_trace;
+typedef struct {
+  int64_t n;
+  int32_t n_clients, n_tags, n_warnings;
+  int32_t pinned;                    /* columns live in the pinned host arena */
+  double duration_s;                 /* last arrival (Trace::duration_s) */
+  const int32_t* client;             /* roster index, arrival order */
+  const double* arrival_s;
+  const int32_t* input_tokens;
+  const int32_t* output_tokens;      /* true_output_tokens */
+  const int32_t* tag;                /* index into tag_names; -1 = untagged */
+  const char* client_names;          /* n_clients NUL-terminated client_id strings */
+  const char* tag_names;             /* n_tags NUL-terminated category_tag strings */
+  const char* warnings;              /* n_warnings NUL-terminated strings */
+  char stored_hash[17];              /* hash recorded in a binary trace ("" for CSV) */
+} eqx_trace_view;
+eqx_status eqx_trace_load_csv(const char* path, eqx_trace** out, char* err, int32_t err_len);
+eqx_status eqx_trace_load_bin(const char* path, eqx_trace** out, char* err, int32_t err_len);
+eqx_status eqx_trace_create(int64_t n, const int32_t* client, const double* arrival_s, const int32_t* input_tokens,
+                            const int32_t* output_tokens, const int32_t* tag, int32_t n_clients,
+                            const char* client_names, int32_t n_tags, const char* tag_names, eqx_trace** out);
+eqx_status eqx_trace_view_get(eqx_trace* t, eqx_trace_view* v);
+eqx_status eqx_trace_hash(eqx_trace* t, char out[17]);
+eqx_status eqx_trace_save_csv(eqx_trace* t, const char* path);
+eqx_status eqx_trace_save_bin(eqx_trace* t, const char* path);
+void eqx_trace_free(eqx_trace* t);
+
 /* ---- live queues ------------------------------------------------------
  * drain_arrivals (engine.cpp:171-197) for a batch of arrivals that joins the requests still
  * queued (unlike eqx_drain, which replaces the queue): each arrival's prediction record is made

@@ -232,6 +232,10 @@ def _lib(which: str):
         path = LIB_REF if which == "ref" else LIB_ORACLE
         if not os.path.exists(path):
             raise FileNotFoundError(f"{path} not built (run __graft_entry__.build())")
+        if which == "ref":
+            # the reference objects use iostreams / locale state of the system libstdc++; load it
+            # globally first so it is not resolved against a copy a wheel loaded privately
+            C.CDLL("libstdc++.so.6", mode=C.RTLD_GLOBAL)
         lib = C.CDLL(path)
         fn = lib.ref_step if which == "ref" else lib.eqxo_step
         fn.argtypes = [C.POINTER(StepIn), C.POINTER(StepOut), C.c_char_p, C.c_int]
@@ -409,7 +413,7 @@ def run_feedback(fb: dict, which: str = "ref", pend=None, mid=None) -> dict:
         mid_out = np.zeros(3 * max(nc, 1))
         pend_in = pend_out.reshape(3, -1)[:, done_adm] if n_adm else np.zeros((3, 0))
         f = _feedback_struct(fb, led, done_client, np.zeros((3, len(done_adm))), keep)
-        lib = C.CDLL(LIB_REF)
+        lib, _ = _lib("ref")
         fn = lib.ref_feedback
         fn.restype = C.c_int
         names = b"".join(n.encode() + b"\0" for n in fb["names"])
@@ -543,3 +547,42 @@ def ref_replay_report(case: "StepCase", max_sim_time_s=0.0, ema_alpha=0.2) -> di
          C.byref(e), err, 512):
         raise ValueError(err.value.decode())
     return {"jain_ttft_p90": j.value, "throughput_tps": t.value, "completed": n.value, "sim_end": e.value}
+
+
+# ---- traces -----------------------------------------------------------------
+def ref_trace_load(path: str, cap: int = 1 << 18) -> dict:
+    """The reference's load_trace + trace_hash (oracle/ref_step.cpp ref_trace_load); raises
+    ValueError with the reference's ParseError message."""
+    lib, _ = _lib("ref")
+    n, nc, nw = C.c_int64(), C.c_int32(), C.c_int32()
+    dur = C.c_double()
+    client, arrival = np.zeros(cap, np.int32), np.zeros(cap)
+    tin, tout = np.zeros(cap, np.int32), np.zeros(cap, np.int32)
+    tags, names = C.create_string_buffer(32 * cap + 1), C.create_string_buffer(1 << 16)
+    h, err = C.create_string_buffer(17), C.create_string_buffer(1024)
+    f = lib.ref_trace_load
+    f.restype = C.c_int
+    vp = C.c_void_p
+    f.argtypes = [C.c_char_p, C.c_int64, vp, vp, vp, vp, vp, C.c_char_p, C.c_int64, C.c_char_p, C.c_int64, vp, vp, vp,
+                  C.c_char_p, C.c_char_p, C.c_int]
+    if f(str(path).encode(), cap, C.addressof(n), client.ctypes.data, arrival.ctypes.data, tin.ctypes.data,
+         tout.ctypes.data, tags, len(tags), names, len(names), C.addressof(nc), C.addressof(nw), C.addressof(dur), h,
+         err, 1024):
+        raise ValueError(err.value.decode())
+    k = int(n.value)
+    return {"n": k, "client": client[:k], "arrival": arrival[:k], "in_tokens": tin[:k], "out_tokens": tout[:k],
+            "tags": tags.raw.split(b"\0")[:k] if k else [],
+            "client_names": [x.decode() for x in names.raw.split(b"\0")[:nc.value]],
+            "n_warnings": nw.value, "duration": dur.value, "hash": h.value.decode()}
+
+
+def ref_scenario_csv(preset: str, seed: int, duration_s: float, path: str) -> str:
+    """generate_scenario written by the reference's write_trace_csv; returns its trace_hash."""
+    lib, _ = _lib("ref")
+    h, err = C.create_string_buffer(17), C.create_string_buffer(1024)
+    f = lib.ref_scenario_csv
+    f.restype = C.c_int
+    f.argtypes = [C.c_char_p, C.c_uint64, C.c_double, C.c_char_p, C.c_char_p, C.c_char_p, C.c_int]
+    if f(preset.encode(), seed, duration_s, str(path).encode(), h, err, 1024):
+        raise ValueError(err.value.decode())
+    return h.value.decode()

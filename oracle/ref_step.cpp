@@ -17,6 +17,7 @@
 #include <cstring>
 #include <deque>
 #include <exception>
+#include <fstream>
 #include <memory>
 #include <set>
 #include <string>
@@ -920,6 +921,63 @@ extern "C" int ref_replay_full(const eqxo_step_in* in, double max_sim_time_s, do
       diff[2 * w] = r.diff_series[w].time_s;
       diff[2 * w + 1] = r.diff_series[w].value;
     }
+    return 0;
+  } catch (const std::exception& e) {
+    set_err(err, err_len, e.what());
+    return 1;
+  }
+}
+
+// ---- traces ------------------------------------------------------------
+// ref_trace_load -- load_trace (workload.cpp:312-400) + trace_hash; columns into caller arrays
+// of capacity cap (n returned even when larger), roster / tag strings NUL-packed.  Returns 0, or
+// 1 with the ParseError / ConfigError message in err.
+extern "C" int ref_trace_load(const char* path, int64_t cap, int64_t* n, int32_t* client, double* arrival,
+                              int32_t* in_tokens, int32_t* out_tokens, char* tags, int64_t tags_cap,
+                              char* names, int64_t names_cap, int32_t* n_clients, int32_t* n_warnings,
+                              double* duration, char* hash, char* err, int err_len) {
+  try {
+    const Trace t = load_trace(path);
+    *n = static_cast<int64_t>(t.requests.size());
+    *n_clients = static_cast<int32_t>(t.clients.size());
+    *n_warnings = static_cast<int32_t>(t.warnings.size());
+    *duration = t.duration_s;
+    std::string nb, tb;
+    for (const auto& c : t.clients) nb += c.client_id + std::string(1, '\0');
+    for (int64_t i = 0; i < *n && i < cap; ++i) {
+      const Request& r = t.requests[static_cast<std::size_t>(i)];
+      if (r.id != i) throw EngineError("load_trace ids are not positions");
+      int32_t ci = -1;
+      for (std::size_t c = 0; c < t.clients.size(); ++c)
+        if (t.clients[c].client_id == r.client_id) ci = static_cast<int32_t>(c);
+      client[i] = ci;
+      arrival[i] = r.arrival_time_s;
+      in_tokens[i] = r.input_tokens;
+      out_tokens[i] = r.true_output_tokens;
+      tb += r.category_tag + std::string(1, '\0');
+    }
+    std::memcpy(names, nb.data(), std::min<std::size_t>(nb.size(), static_cast<std::size_t>(names_cap)));
+    std::memcpy(tags, tb.data(), std::min<std::size_t>(tb.size(), static_cast<std::size_t>(tags_cap)));
+    const std::string h = trace_hash(t);
+    std::memcpy(hash, h.c_str(), 17);
+    return 0;
+  } catch (const std::exception& e) {
+    set_err(err, err_len, e.what());
+    return 1;
+  }
+}
+
+// ref_scenario_csv -- generate_scenario (workload.cpp:254-298) written with write_trace_csv to
+// path; hash = trace_hash of the generated trace.
+extern "C" int ref_scenario_csv(const char* preset, uint64_t seed, double duration_s, const char* path, char* hash,
+                                char* err, int err_len) {
+  try {
+    const Trace t = generate_scenario(std::string_view(preset), seed, duration_s);
+    std::ofstream out(path, std::ios::binary);
+    write_trace_csv(t, out);
+    out.close();
+    const std::string h = trace_hash(t);
+    std::memcpy(hash, h.c_str(), 17);
     return 0;
   } catch (const std::exception& e) {
     set_err(err, err_len, e.what());

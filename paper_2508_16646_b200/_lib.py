@@ -99,7 +99,24 @@ class ReplayOut(C.Structure):
                 ("rate", C.c_void_p)]
 
 
+class TraceView(C.Structure):
+    _fields_ = [("n", C.c_int64), ("n_clients", C.c_int32), ("n_tags", C.c_int32), ("n_warnings", C.c_int32),
+                ("pinned", C.c_int32), ("duration_s", C.c_double), ("client", C.c_void_p), ("arrival_s", C.c_void_p),
+                ("input_tokens", C.c_void_p), ("output_tokens", C.c_void_p), ("tag", C.c_void_p),
+                ("client_names", C.c_void_p), ("tag_names", C.c_void_p), ("warnings", C.c_void_p),
+                ("stored_hash", C.c_char * 17)]
+
+
 _SIGS = {
+    "eqx_trace_load_csv": ([C.c_char_p, C.POINTER(C.c_void_p), C.c_char_p, C.c_int32], C.c_int),
+    "eqx_trace_load_bin": ([C.c_char_p, C.POINTER(C.c_void_p), C.c_char_p, C.c_int32], C.c_int),
+    "eqx_trace_create": ([C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
+                          C.c_char_p, C.c_int32, C.c_char_p, C.POINTER(C.c_void_p)], C.c_int),
+    "eqx_trace_view_get": ([C.c_void_p, C.c_void_p], C.c_int),
+    "eqx_trace_hash": ([C.c_void_p, C.c_char_p], C.c_int),
+    "eqx_trace_save_csv": ([C.c_void_p, C.c_char_p], C.c_int),
+    "eqx_trace_save_bin": ([C.c_void_p, C.c_char_p], C.c_int),
+    "eqx_trace_free": ([C.c_void_p], None),
     "eqx_abi_version": ([], C.c_int32),
     "eqx_host_alloc": ([C.c_int64], C.c_void_p),
     "eqx_host_free": ([C.c_void_p], C.c_int),
