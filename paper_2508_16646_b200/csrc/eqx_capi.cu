@@ -2040,6 +2040,7 @@ eqx_status eqx_phase_times(eqx_ctx* ctx, double* out_us, int32_t n) {
   for (int i = 6; i < n && i < 16; ++i) out_us[i] = static_cast<double>(t[i]);  // counts / cycles
   const unsigned long long* dt = ctx->h_state->dt;  // EQX_PROF drain timeline (us from hist start)
   for (int i = 16; i < n && i < 22; ++i) out_us[i] = (static_cast<double>(dt[i - 16]) - static_cast<double>(dt[0])) * 1e-3;
+  if (n > 22) out_us[22] = (base - static_cast<double>(dt[0])) * 1e-3;  // selection start after drain start
   return EQX_OK;
 }
 
