@@ -1329,12 +1329,24 @@ static eqx_status step_enqueue(eqx_ctx* ctx, const StepPlan& pl, bool with_drain
     eqx_status e = drain_enqueue(ctx, false);
     if (e != EQX_OK) return e;
   }
-  CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[5], s));
+  // Split launches record the per-kernel timing events; the graph path (with_drain) leaves the
+  // drain -> window -> selection chain bare so its programmatic (PDL) edges survive capture.
+  if (!with_drain) CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[5], s));
   CUDA_TRY(ctx, launch_pdl(window_kernel, dim3(pl.window_grid), dim3(256), pl.window_smem, s, pl.wi));
-  CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[2], s));
-  {
+  if (!with_drain) CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[2], s));
+  {  // PDL: the selection CTA stages its model, lifts and loads the ledger while the windows fill
     void* args[] = {const_cast<SelectArgs*>(&pl.se)};
-    CUDA_TRY(ctx, cudaLaunchKernel(select_fn(pl.se.warp_sel), dim3(1), dim3(pl.select_threads), args, pl.select_smem, s));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(pl.select_threads);
+    cfg.dynamicSmemBytes = pl.select_smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CUDA_TRY(ctx, cudaLaunchKernelExC(&cfg, select_fn(pl.se.warp_sel), args));
   }
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[3], s));
   CUDA_TRY(ctx, cudaGetLastError());

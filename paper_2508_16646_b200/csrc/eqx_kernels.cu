@@ -923,6 +923,7 @@ __global__ void __launch_bounds__(256) window_kernel(const WindowArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   stage_model(a.model, a.model_words, smem);  // overlaps the drain's tail (programmatic launch)
   pdl_wait();
+  pdl_trigger();  // the drain is complete: the selection CTA may start its prologue
   __syncthreads();
   const ModelTables& M = *reinterpret_cast<const ModelTables*>(smem);
   const int64_t items = static_cast<int64_t>(a.C) * a.W;
@@ -2495,6 +2496,7 @@ __device__ __forceinline__ void select_body(const SelectArgs& a) {
     cw.flags[c] = a.backlogged[c] ? kBacklogged : 0;
     cw.adm[c] = 0;
   }
+  pdl_wait();  // window_kernel's [C][W] entries (programmatic launch: the prologue above overlapped it)
   if (a.gW > 0 && a.gW != a.W) {  // gathered [C][gW] windows: the first W of every client
     constexpr int kWords = sizeof(WinEntry) / 8;
     const int64_t per = static_cast<int64_t>(a.W) * kWords;
@@ -2505,6 +2507,23 @@ __device__ __forceinline__ void select_body(const SelectArgs& a) {
       const int64_t c = i / per;
       dst[i] = __ldcg(src + c * a.gW * kWords + (i - c * per));
     }
+  } else if (const uint64_t wbytes = static_cast<uint64_t>(C) * a.W * sizeof(WinEntry);
+             wbytes > 0 && wbytes < (1u << 20) && wbytes % 16 == 0 && (reinterpret_cast<uintptr_t>(a.win_g) & 15) == 0) {
+    // one elected thread moves the whole [C][W] block with 1-D bulk copies (TMA engine)
+    __shared__ uint64_t wbar;
+    if (tid == 0) {
+      mbar_init(&wbar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0) {
+      mbar_expect_tx(&wbar, static_cast<uint32_t>(wbytes));
+      const unsigned char* src = reinterpret_cast<const unsigned char*>(a.win_g);
+      unsigned char* dst = reinterpret_cast<unsigned char*>(win);
+      for (uint32_t off = 0; off < wbytes; off += 32768u)
+        bulk_g2s(dst + off, src + off, min(32768u, static_cast<uint32_t>(wbytes) - off), &wbar);
+    }
+    mbar_wait(&wbar, 0);
   } else {
     const int64_t words = static_cast<int64_t>(C) * a.W * (sizeof(WinEntry) / 8);
     const uint2* src = reinterpret_cast<const uint2*>(a.win_g);
