@@ -53,8 +53,10 @@ def main():
     step_names = list(dict.fromkeys(name for name, _ in ours))  # our kernels, launch order
     lines = ["# Launch list (ncu --metrics gpu__time_duration.sum --clock-control none)", "",
              "Serialised, cold-cache per-launch device times of one cold scheduling step (cfg2: 1M requests,",
-             "64 clients).  Inside a real step score_kernel overlaps drain+window+select (side stream), so the",
-             "shares below are of the serial sum, not of the step's wall time.", "",
+             "64 clients).  Inside a real (graph-replayed) step score_kernel runs on a side stream beside the",
+             "one-CTA selection loop, lift_kernel is the selection prologue, and drain_rank / window / selection",
+             "are chained with programmatic launches, so the shares below are of the serial sum, not of the",
+             "step's wall time (tools/graph_timeline.py measures that).", "",
              "| kernel | launches | median us | share of serial step |", "|---|---:|---:|---:|"]
     med = {k: sorted(v)[len(v) // 2] / 1000.0 for k, v in per.items()}
     tot = sum(med.get(k, 0.0) for k in step_names)
