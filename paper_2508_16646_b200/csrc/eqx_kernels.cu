@@ -109,6 +109,24 @@ __device__ __forceinline__ unsigned peer_mask(uint32_t key, int nbits) {
   return m;
 }
 
+// peer_mask with the key width fixed at compile time (NB > 0): fully unrolled ballots; NB = 0
+// keeps the runtime loop.
+template <int NB>
+__device__ __forceinline__ unsigned peer_mask_nb(uint32_t key, int nbits) {
+  if constexpr (NB == 0) {
+    return peer_mask(key, nbits);
+  } else {
+    unsigned m = 0xffffffffu;
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const unsigned bit = (key >> b) & 1u;
+      const unsigned bb = __ballot_sync(0xffffffffu, bit);
+      m &= bb ^ (bit - 1u);  // bit ? bb : ~bb
+    }
+    return m;
+  }
+}
+
 // Block-wide exclusive scan of one uint32 per thread (blockDim.x <= 1024); returns the total.
 __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* out, uint32_t* warp_buf) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
@@ -272,7 +290,8 @@ __global__ void __launch_bounds__(1024) lift_kernel(const DrainArgs a) {
 #define EQX_DT_MAX(i) do {} while (0)
 #endif
 
-__global__ void __launch_bounds__(kDrainThreads) drain_hist_kernel(const DrainArgs a) {
+template <int NB>
+__device__ __forceinline__ void drain_hist_body(const DrainArgs& a) {
   extern __shared__ __align__(16) uint32_t sh[];
   EQX_DT_MIN(0);
   pdl_trigger();
@@ -302,7 +321,7 @@ __global__ void __launch_bounds__(kDrainThreads) drain_hist_kernel(const DrainAr
       const int32_t c = cv[u];
       const bool ok = static_cast<uint32_t>(c) < static_cast<uint32_t>(C);
       bad |= row < r1 && !ok;
-      const unsigned peers = peer_mask(ok ? static_cast<uint32_t>(c) : static_cast<uint32_t>(C), a.cbits);
+      const unsigned peers = peer_mask_nb<NB>(ok ? static_cast<uint32_t>(c) : static_cast<uint32_t>(C), a.cbits);
       if (ok && lane == __ffs(peers) - 1) {  // the earliest row of the client in these 32
         if (my[c] == 0) atomicMin(&fr[c], static_cast<uint32_t>(row));
         my[c] = static_cast<uint16_t>(my[c] + __popc(peers));
@@ -325,6 +344,23 @@ __global__ void __launch_bounds__(kDrainThreads) drain_hist_kernel(const DrainAr
   EQX_DT_MAX(1);
 }
 
+// The client-key width selects an unrolled peer-mask instantiation (rosters up to 255 clients),
+// else the runtime loop.
+#define EQX_NB_DISPATCH(BODY)                     \
+  switch (a.cbits) {                              \
+    case 1: BODY<1>(a); break;                    \
+    case 2: BODY<2>(a); break;                    \
+    case 3: BODY<3>(a); break;                    \
+    case 4: BODY<4>(a); break;                    \
+    case 5: BODY<5>(a); break;                    \
+    case 6: BODY<6>(a); break;                    \
+    case 7: BODY<7>(a); break;                    \
+    case 8: BODY<8>(a); break;                    \
+    default: BODY<0>(a); break;                   \
+  }
+
+__global__ void __launch_bounds__(kDrainThreads) drain_hist_kernel(const DrainArgs a) { EQX_NB_DISPATCH(drain_hist_body) }
+
 
 
 // Stable scatter of row indices into per-client FIFO segments.  Each CTA owns one tile; each
@@ -332,7 +368,8 @@ __global__ void __launch_bounds__(kDrainThreads) drain_hist_kernel(const DrainAr
 // the same client (ballot peer masks).  Walk 1 counts per (warp, client); scans over warps
 // and clients give every row its slot in a client-sorted copy of the tile in shared memory
 // (walk 2), which is then written to perm as contiguous per-client runs (coalesced).
-__global__ void __launch_bounds__(kDrainThreads) drain_rank_kernel(const DrainArgs a) {
+template <int NB>
+__device__ __forceinline__ void drain_rank_body(const DrainArgs& a) {
   extern __shared__ __align__(16) uint32_t sh[];
   EQX_DT_MIN(3);
   const int32_t C = a.C;
@@ -458,7 +495,7 @@ __global__ void __launch_bounds__(kDrainThreads) drain_rank_kernel(const DrainAr
         const int32_t row = rb + 32 * u + lane;
         const int32_t c = cv[u];
         const bool ok = static_cast<uint32_t>(c) < static_cast<uint32_t>(C);
-        const unsigned peers = peer_mask(ok ? static_cast<uint32_t>(c) : static_cast<uint32_t>(C), a.cbits);
+        const unsigned peers = peer_mask_nb<NB>(ok ? static_cast<uint32_t>(c) : static_cast<uint32_t>(C), a.cbits);
         const int leader = __ffs(peers) - 1;
         uint32_t start = 0;
         if (ok && lane == leader) {
@@ -485,7 +522,7 @@ __global__ void __launch_bounds__(kDrainThreads) drain_rank_kernel(const DrainAr
       const int32_t row = r + lane;
       const int32_t c = row < r1 ? a.client[row] : -1;
       const bool ok = static_cast<uint32_t>(c) < static_cast<uint32_t>(C);
-      const unsigned peers = peer_mask(ok ? static_cast<uint32_t>(c) : static_cast<uint32_t>(C), a.cbits);
+      const unsigned peers = peer_mask_nb<NB>(ok ? static_cast<uint32_t>(c) : static_cast<uint32_t>(C), a.cbits);
       const int leader = __ffs(peers) - 1;
       uint32_t start = 0;
       if (ok && lane == leader) {
@@ -499,6 +536,8 @@ __global__ void __launch_bounds__(kDrainThreads) drain_rank_kernel(const DrainAr
   }
   EQX_DT_MAX(4);
 }
+
+__global__ void __launch_bounds__(kDrainThreads) drain_rank_kernel(const DrainArgs a) { EQX_NB_DISPATCH(drain_rank_body) }
 
 // ===================================== scoring ===========================================
 
