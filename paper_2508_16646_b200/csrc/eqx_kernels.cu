@@ -386,9 +386,17 @@ __device__ __forceinline__ void drain_rank_body(const DrainArgs& a) {
   uint16_t* wc = reinterpret_cast<uint16_t*>(sh + 2 * C);  // [kDrainWarps][C]
   pdl_wait();     // drain_hist_kernel's counts, histogram and first rows are complete
   pdl_trigger();  // the window kernel may get scheduled
-  {  // per-warp client counts from drain_hist_kernel's walk
+  {  // per-warp client counts from drain_hist_kernel's walk (4 independent L2 loads in flight)
     const uint16_t* g = a.wcnt + static_cast<int64_t>(tile) * kDrainWarps * C;
-    for (int i = tid; i < kDrainWarps * C; i += blockDim.x) wc[i] = g[i];
+    const int nwc = kDrainWarps * C, NT = blockDim.x;
+    for (int i0 = tid; i0 < nwc; i0 += 4 * NT) {
+      uint16_t v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = i0 + u * NT < nwc ? __ldcg(g + i0 + u * NT) : uint16_t(0);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (i0 + u * NT < nwc) wc[i0 + u * NT] = v[u];
+    }
   }
   // Every CTA derives its own global offsets from the [tile][client] histogram (no serial
   // scan): base[c] = sum_{c' < c} total[c'] + sum_{t < tile} hist[t][c].  G threads per
@@ -398,21 +406,21 @@ __device__ __forceinline__ void drain_rank_body(const DrainArgs& a) {
   {
     const int NT = blockDim.x;
     int G = 1;  // threads per client: a power of two, so client groups never straddle warps
-    while (G * 2 * C <= NT) G *= 2;
+    while (G * 2 * C <= NT) G *= 2;  // every thread takes part (G * C <= NT)
     const int32_t nt = a.n_tiles;
     for (int c0 = 0; c0 < C; c0 += NT / G) {
       const int c = c0 + tid / G, g = tid % G;
       uint32_t pre = 0, tot = 0;
       if (tid / G < NT / G && c < C) {
-        for (int32_t t0 = g; t0 < nt; t0 += 8 * G) {  // 8 independent L2 loads in flight
-          uint32_t h[8];
+        for (int32_t t0 = g; t0 < nt; t0 += 16 * G) {  // 16 independent L2 loads in flight
+          uint32_t h[16];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
+          for (int u = 0; u < 16; ++u) {
             const int32_t t = t0 + u * G;
             h[u] = t < nt ? __ldcg(a.hist + static_cast<int64_t>(t) * C + c) : 0u;
           }
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
+          for (int u = 0; u < 16; ++u) {
             tot += h[u];
             pre += t0 + u * G < tile ? h[u] : 0u;
           }
