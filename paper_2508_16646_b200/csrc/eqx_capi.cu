@@ -1311,31 +1311,41 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl, int32_t g
 static eqx_status step_enqueue(eqx_ctx* ctx, const StepPlan& pl, bool with_drain) {
   cudaStream_t s = ctx->stream, s2 = ctx->stream2;
   char* st = reinterpret_cast<char*>(ctx->d_state.p);
-  CUDA_TRY(ctx, cudaMemsetAsync(st + offsetof(DevState, t) + 4 * 8, 0xff, 8, s));
-  CUDA_TRY(ctx, cudaMemsetAsync(st + offsetof(DevState, t) + 5 * 8, 0, 8, s));
-  CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[4], s));
+  // Timing (events, the scoring-CTA stamps of eqx_phase_times) belongs to split launches and the
+  // instrumented build; a captured graph carries only the work.
+  const bool timing = !with_drain;
+#ifndef EQX_PROF
+  const bool stamps = timing;
+#else
+  const bool stamps = true;
+#endif
+  if (stamps) {
+    CUDA_TRY(ctx, cudaMemsetAsync(st + offsetof(DevState, t) + 4 * 8, 0xff, 8, s));
+    CUDA_TRY(ctx, cudaMemsetAsync(st + offsetof(DevState, t) + 5 * 8, 0, 8, s));
+  }
+  if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[4], s));
   if (with_drain) {
     eqx_status e = drain_enqueue(ctx, false);
     if (e != EQX_OK) return e;
   }
   // Split launches record the per-kernel timing events; the graph path (with_drain) leaves the
   // drain -> window -> selection chain bare so its programmatic (PDL) edges survive capture.
-  if (!with_drain) CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[5], s));
+  if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[5], s));
   CUDA_TRY(ctx, launch_pdl(window_kernel, dim3(pl.window_grid), dim3(256), pl.window_smem, s, pl.wi));
   // Whole-queue scoring forks off after the windows: the selection CTA (PDL) is resident by
   // then, so the scoring grid fills the other SMs while the one-warp selection loop runs
   // (nothing in the selection reads the per-request scores; event_fill joins them).
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fork, s));
   CUDA_TRY(ctx, cudaStreamWaitEvent(s2, ctx->ev_fork, 0));
-  CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[0], s2));
+  if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[0], s2));
   if (ctx->n > 0) {
     if (pl.score_tma) score_tma_kernel<<<pl.score_grid, kScoreTmaThreads, pl.score_smem, s2>>>(pl.sc);
     else score_kernel<<<pl.score_grid, kScoreThreads, pl.score_smem, s2>>>(pl.sc);
   }
   CUDA_TRY(ctx, cudaGetLastError());
-  CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[1], s2));
+  if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[1], s2));
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_join, s2));
-  if (!with_drain) CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[2], s));
+  if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[2], s));
   {  // PDL: the selection CTA stages its model, lifts and loads the ledger while the windows fill
     void* args[] = {const_cast<SelectArgs*>(&pl.se)};
     cudaLaunchConfig_t cfg = {};
@@ -1350,7 +1360,7 @@ static eqx_status step_enqueue(eqx_ctx* ctx, const StepPlan& pl, bool with_drain
     cfg.numAttrs = 1;
     CUDA_TRY(ctx, cudaLaunchKernelExC(&cfg, select_fn(pl.se.warp_sel), args));
   }
-  CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[3], s));
+  if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[3], s));
   CUDA_TRY(ctx, cudaGetLastError());
   CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_join, 0));
   EventFillArgs ef;
