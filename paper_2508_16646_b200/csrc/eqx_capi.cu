@@ -223,13 +223,15 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 }
 
 // DevState -> the mapped host copy by a kernel (no copy-engine dependency; capturable).
-cudaError_t state_to_host(eqx_ctx* ctx, cudaStream_t s) {
+// pdl: launched programmatically after the kernel that last wrote the state (it waits).
+cudaError_t state_to_host(eqx_ctx* ctx, cudaStream_t s, bool pdl = false) {
   PackCols pc;
   std::memset(&pc, 0, sizeof(pc));
   pc.src[0] = ctx->d_state.p;
   pc.dst[0] = ctx->h_state_dev;
   pc.bytes[0] = sizeof(DevState);
   pc.n = 1;
+  if (pdl) return launch_pdl(pack_cols_kernel, dim3(1), dim3(64), 0, s, pc);
   pack_cols_kernel<<<1, 64, 0, s>>>(pc);
   return cudaGetLastError();
 }
@@ -1383,9 +1385,12 @@ static eqx_status step_enqueue(eqx_ctx* ctx, const StepPlan& pl, bool with_drain
   ef.weight = ctx->d_weight.as<double>();
   ef.pol = ctx->pol;
   ef.now = pl.se.now;
-  if (ctx->n > 0) event_fill_kernel<<<ctx->sm_count, 256, 0, s>>>(ef);
+  if (ctx->n > 0) {
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ctx->sm_count, (ctx->ev_cap + 255) / 256)));
+    CUDA_TRY(ctx, launch_pdl(event_fill_kernel, dim3(grid), dim3(256), 0, s, ef));
+  }
   CUDA_TRY(ctx, cudaGetLastError());
-  CUDA_TRY(ctx, state_to_host(ctx, s));
+  CUDA_TRY(ctx, state_to_host(ctx, s, true));
   return EQX_OK;
 }
 

@@ -2637,6 +2637,7 @@ __device__ __forceinline__ void select_body(const SelectArgs& a) {
     a.st->t[6] = nb;
     a.st->t[7] = ns;
   }
+  pdl_trigger();  // the event fill may get scheduled while the ledger is written back
   // ---- write back ledger, heads, batch, summary ----
   for (int32_t c = tid; c < C; c += NT) {
     a.ufc[c] = cw.ufc[c];
@@ -2670,6 +2671,7 @@ template __global__ void select_warp_kernel<8>(SelectArgs);
 // Event payloads (scheduler.hpp:131-138 PendingContribution) from the per-request scores the
 // scoring kernel wrote: predicted tokens, ufc/rfc increments, the VTC charge and wait_s.
 __global__ void event_fill_kernel(const EventFillArgs a) {
+  pdl_wait();  // programmatic launch: the selection's events are complete
   const int64_t n = *a.n_events;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n && i < a.ev_cap;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -2703,6 +2705,8 @@ __global__ void gather_ids_kernel(const int32_t* __restrict__ rows, int64_t n, c
 
 // Columns -> mapped host memory by SM stores over PCIe (16-byte words when aligned).
 __global__ void pack_cols_kernel(const PackCols p) {
+  pdl_wait();  // no-op unless launched programmatically after the kernel producing the columns
+  pdl_trigger();
   for (int c = blockIdx.y; c < p.n; c += gridDim.y) {
     const int64_t b = p.bytes[c];
     const unsigned char* src = static_cast<const unsigned char*>(p.src[c]);
