@@ -2459,6 +2459,223 @@ __device__ __forceinline__ void warp_select_reg(const SelectArgs& a, const Model
   __syncthreads();  // releases the helper warps
 }
 
+// Two-warp variant of warp_select_reg<1> for rosters of 33..64 clients: lane L of selection
+// warp w owns client 32 w + L alone, so no lane compares or predicates over slots.  A pick is a
+// warp argmin in each selection warp, the two warp winners exchanged through double-buffered
+// shared memory behind one 64-thread named barrier, and the same select_next comparison on the
+// two; the winning lane alone updates its client.  Both warps keep identical copies of the batch
+// counters and issue the same regeneration commands.
+struct Warp2Cand {
+  uint64_t k, a, pk;
+  int64_t need;
+  uint32_t o;
+  int32_t lane;
+};
+
+__device__ __forceinline__ void warp2_select(const SelectArgs& a, const ModelTables& M, const WinEntry* win,
+                                             const ClientWork& cw, SelShared& S, const StreamScratch& T) {
+  __shared__ WarpSelShared X;
+  __shared__ Warp2Cand xw[2][2];  // [pick parity][selection warp]
+  const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  const int32_t C = a.C, Ds = T.Ds, W = a.W;
+  const Policy P = a.pol;
+  auto regen_all = [&](int depth) {
+    for (int32_t c = tid; c < C; c += NT) gen_stream(a, M, win, cw, T, c, depth, S.max_u, S.max_r);
+  };
+  regen_all(Ds);
+  __syncthreads();
+  if (tid >= 64) {  // helper warps: CTA-wide stream regeneration on command
+    for (;;) {
+      __syncthreads();
+      const int32_t cmd = X.cmd;
+      if (cmd == kCmdExit) break;
+      if (cmd == kCmdMaxRegen) cta_maxima(cw, C, S);
+      regen_all(X.depth);
+      __syncthreads();
+    }
+    return;
+  }
+  const int64_t tmax = a.tmax;
+  const int32_t c = warp * 32 + lane;  // this lane's client
+  RegItem cur, nxt;
+  int32_t spos = 0, spos0 = 0, send = 0, sd = 0, sdl = 0, sadm = 0, sfl = 0;
+  double su = 0.0, sr = 0.0, scn = 0.0;
+  const uint32_t so = c < C ? cw.order[c] : 0xffffffffu;
+  auto load_item = [&](int32_t d, int32_t j) -> RegItem {
+    RegItem it;
+    const int64_t x = static_cast<int64_t>(c) * Ds + d;
+    const int32_t kk = j - spos0;
+    const WinEntry e = kk < W ? win[static_cast<int64_t>(c) * W + kk] : deep_entry(a, M, c, j, kk, cw.w[c]);
+    it.k = T.k[x];
+    it.a = e.abits;
+    it.nu = T.u[x];
+    it.nr = T.r[x];
+    it.ncn = T.cn[x];
+    it.in = e.in;
+    it.pred = e.pred;
+    it.row = e.row;
+    it.alone = e.alone;
+    it.fl = T.fl[x];
+    return it;
+  };
+  auto load_slot = [&]() {  // after (re)generation: current head and the item after it
+    cur.k = ~0ull;
+    if (c >= C) return;
+    spos = cw.pos[c];
+    spos0 = cw.pos0[c];
+    send = cw.end[c];
+    sfl = cw.flags[c];
+    su = cw.ufc[c];
+    sr = cw.rfc[c];
+    scn = cw.cnt[c];
+    sd = 0;
+    sdl = T.sdl[c];
+    if (sdl == 0) return;  // not a candidate
+    cur = load_item(0, spos);
+    if (1 < sdl) nxt = load_item(1, spos + 1);
+  };
+  sadm = c < C ? cw.adm[c] : 0;
+  load_slot();
+  int32_t members = S.members;
+  int64_t reserved = S.reserved, n_ev = S.n_ev, n_adm = S.n_adm, n_rej = S.n_rej, prefill = S.prefill;
+  int since_regen = 1 << 30;
+  int par = 0;
+  auto publish = [&]() {
+    if (c < C) {
+      cw.pos[c] = spos;
+      cw.flags[c] = sfl;
+      cw.ufc[c] = su;
+      cw.rfc[c] = sr;
+      cw.cnt[c] = scn;
+    }
+  };
+  auto command = [&](int32_t cmd, int depth) {
+    publish();
+    if (tid == 0) {
+      X.cmd = cmd;
+      X.depth = depth;
+    }
+    __syncthreads();
+    if (cmd == kCmdMaxRegen) cta_maxima(cw, C, S);
+    regen_all(depth);
+    __syncthreads();
+    load_slot();
+  };
+  for (;;) {
+    const bool has = cur.k != ~0ull;
+    int32_t out = kOutNone, bflags = 0;
+    int64_t bneed = 0;
+    if (has) {
+      bflags = (cur.alone ? 1 : 0) | ((cur.fl & kFlMaxChg) ? 2 : 0) | ((cur.fl & kFlHolder) ? 4 : 0) |
+               ((spos + 1 == send) ? 8 : 0) | ((sd + 1 < sdl) ? 16 : 0);
+      bneed = static_cast<int64_t>(cur.in) + cur.pred;
+      if (!(bflags & 1)) out = kOutRej;
+      else if ((members + 1 <= P.max_batch) && (reserved + bneed <= tmax)) out = kOutAdm;
+      else out = P.backfill ? kOutSkip : kOutStop;
+    }
+    const Cand mine = has ? Cand{cur.k, cur.a, so} : no_cand();
+    const int wsrc = warp_argmin_lane(mine);
+    if (lane == wsrc) {
+      Warp2Cand& x = xw[par][warp];
+      x.k = mine.k;
+      x.a = mine.a;
+      x.o = mine.o;
+      x.lane = lane;
+      x.pk = static_cast<uint64_t>(static_cast<uint32_t>(out | (bflags << 4))) |
+             (static_cast<uint64_t>(static_cast<uint32_t>(has ? cur.in : 0)) << 32);
+      x.need = bneed;
+    }
+    asm volatile("bar.sync 1, 64;" ::: "memory");
+    const Warp2Cand x0 = xw[par][0], x1 = xw[par][1];
+    par ^= 1;
+    const bool w1 = better(Cand{x1.k, x1.a, x1.o}, Cand{x0.k, x0.a, x0.o});
+    const int win_warp = w1 ? 1 : 0;
+    const Warp2Cand& xb = w1 ? x1 : x0;
+    const uint64_t pk = xb.pk;
+    const int64_t need = xb.need;
+    const int32_t o = static_cast<int32_t>(pk & 15), fl = static_cast<int32_t>((pk >> 4) & 31);
+    if (o == kOutNone || o == kOutStop) break;  // no candidates (engine.cpp:217) / batch full (:239)
+    const int64_t ev = n_ev;
+    if (o == kOutRej) {
+      ++n_rej;
+      ++n_ev;
+    } else if (o == kOutAdm) {
+      members += 1;
+      reserved += need;
+      prefill += static_cast<int32_t>(pk >> 32);
+      ++n_adm;
+      ++n_ev;
+    }
+    const bool maxchg = o == kOutAdm && (fl & 2);
+    const bool holder = o != kOutSkip && (fl & 4) && (fl & 8);
+    ++since_regen;
+    if (warp == win_warp && lane == xb.lane) {
+      bool own_regen = false;
+      if (o == kOutSkip) {
+        sfl |= kSkipped;  // engine.cpp:236-238
+        cur.k = ~0ull;
+      } else {
+        if (ev < a.ev_cap) {
+          a.ev_row[ev] = cur.row;
+          a.ev_kind[ev] = o == kOutAdm ? 1 : 2;
+          a.ev_client[ev] = c;
+        }
+        spos += 1;
+        su = cur.nu;
+        sr = cur.nr;
+        scn = cur.ncn;
+        if (o == kOutAdm) sadm += 1;
+        if (fl & 8) {  // pop_head emptied the queue: set_backlogged(false)
+          sfl &= ~kBacklogged;
+          cur.k = ~0ull;
+        } else if (maxchg) {
+          if (S.max_u < su) S.max_u = su;
+          if (S.max_r < sr) S.max_r = sr;
+        } else if (fl & 16) {  // promote the prefetched item, prefetch the one after
+          cur = nxt;
+          sd += 1;
+          if (sd + 1 < sdl) nxt = load_item(sd + 1, spos + 1);
+        } else {
+          own_regen = true;
+        }
+      }
+      if (own_regen) {  // the winner's lookahead ran out: regenerate its stream alone
+        cw.pos[c] = spos;
+        cw.ufc[c] = su;
+        cw.rfc[c] = sr;
+        cw.cnt[c] = scn;
+        gen_stream(a, M, win, cw, T, c, Ds, S.max_u, S.max_r);
+        load_slot();
+      }
+    }
+    if (maxchg || holder) {
+      __syncwarp();
+      const int depth = since_regen < 4 ? min(2, Ds) : Ds;
+      since_regen = 0;
+      command(holder ? kCmdMaxRegen : kCmdRegen, depth);
+    }
+  }
+  if (c < C) {
+    cw.pos[c] = spos;
+    cw.flags[c] = sfl;
+    cw.ufc[c] = su;
+    cw.rfc[c] = sr;
+    cw.cnt[c] = scn;
+    cw.adm[c] = sadm;
+  }
+  if (tid == 0) {
+    S.members = members;
+    S.reserved = reserved;
+    S.n_ev = n_ev;
+    S.n_adm = n_adm;
+    S.n_rej = n_rej;
+    S.prefill = prefill;
+    S.flags |= kDone;
+    X.cmd = kCmdExit;
+  }
+  __syncthreads();  // releases the helper warps
+}
+
 // kMode: -1 multi-mode loops (select_kernel); 0 warp_select_phase; 1/2/4 warp_select_reg<kMode>
 template <int kMode>
 __device__ __forceinline__ void select_body(const SelectArgs& a) {
@@ -2602,6 +2819,9 @@ __device__ __forceinline__ void select_body(const SelectArgs& a) {
   if constexpr (kMode == 0) {  // default: single-warp selection
     warp_select_phase(a, M, win, cw, S, T);
     ns = 1;
+  } else if constexpr (kMode == 16) {  // two selection warps, one client per lane
+    warp2_select(a, M, win, cw, S, T);
+    ns = 1;
   } else if constexpr (kWarp && kMode > 0) {
     warp_select_reg<kMode>(a, M, win, cw, S, T);
     ns = 1;
@@ -2667,6 +2887,7 @@ template __global__ void select_warp_kernel<1>(SelectArgs);
 template __global__ void select_warp_kernel<2>(SelectArgs);
 template __global__ void select_warp_kernel<4>(SelectArgs);
 template __global__ void select_warp_kernel<8>(SelectArgs);
+template __global__ void select_warp_kernel<16>(SelectArgs);
 
 // Event payloads (scheduler.hpp:131-138 PendingContribution) from the per-request scores the
 // scoring kernel wrote: predicted tokens, ufc/rfc increments, the VTC charge and wait_s.

@@ -402,7 +402,8 @@ __global__ void score_tma_kernel(ScoreArgs a);
 __global__ void window_kernel(WindowArgs a);
 __global__ void select_kernel(SelectArgs a);
 template <int kMode>
-__global__ void select_warp_kernel(SelectArgs a);  // kMode 0: smem slots; 1/2/4: register slots
+__global__ void select_warp_kernel(SelectArgs a);  // kMode 0: smem slots; 1/2/4: register slots;
+                                                   // 16: two selection warps, one client per lane
 __global__ void gather_ids_kernel(const int32_t* rows, int64_t n, const int64_t* id, int64_t id_base,
                                   int64_t* out);
 
