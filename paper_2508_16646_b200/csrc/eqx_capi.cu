@@ -141,7 +141,7 @@ struct eqx_ctx {
   size_t h_scratch_bytes = 0;
   DevState* h_state_dev = nullptr; // device alias of the mapped h_state
   // launch-attribute caches (cudaFuncSetAttribute / occupancy queries cost host time per step)
-  int smem_attr[10] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1};  // drain_hist, drain_rank, select kernels (select_fn)
+  int smem_attr[12] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};  // drain_hist, drain_rank, select kernels (select_fn)
   size_t occ_smem = SIZE_MAX;
   int occ_per_sm = 1;
   // client-sharded step (selection context): gathered windows and their ids
@@ -192,7 +192,8 @@ struct Col {
 };
 
 // warp_sel: 0 multi-mode select_kernel; 1 single-warp (shared-memory slots); 2/3/4 single-warp
-// with 1/2/4 register slots per lane; 5 speculative batches; 6 two selection warps (33..64 clients)
+// with 1/2/4 register slots per lane; 5 speculative batches; 6 / 7 two / four selection warps
+// with one client per lane (33..64 / 65..128 clients)
 const void* select_fn(int warp_sel) {
   switch (warp_sel) {
     case 1: return reinterpret_cast<const void*>(select_warp_kernel<0>);
@@ -201,6 +202,7 @@ const void* select_fn(int warp_sel) {
     case 4: return reinterpret_cast<const void*>(select_warp_kernel<4>);
     case 5: return reinterpret_cast<const void*>(select_warp_kernel<8>);
     case 6: return reinterpret_cast<const void*>(select_warp_kernel<16>);
+    case 7: return reinterpret_cast<const void*>(select_warp_kernel<32>);
     default: return reinterpret_cast<const void*>(select_kernel);
   }
 }
@@ -1302,8 +1304,9 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl, int32_t g
   // which stays selectable with EQX_SELECT_MODE=warp)
   if (a.warp_sel && a.warp_sel != 5) {
     const char* m = std::getenv("EQX_SELECT_MODE");
-    const bool k2 = m && std::string(m) == "k2";  // 33..64 clients on one warp, two slots per lane
-    a.warp_sel = C <= 32 ? 2 : C <= 64 ? (k2 ? 3 : 6) : C <= 128 ? 4 : (m && std::string(m) == "warp") ? 1 : 0;
+    const bool slots = m && std::string(m) == "slots";  // one warp, 2 / 4 register slots per lane
+    a.warp_sel = C <= 32 ? 2 : C <= 64 ? (slots ? 3 : 6) : C <= 128 ? (slots ? 4 : 7)
+                                                                  : (m && std::string(m) == "warp") ? 1 : 0;
   }
   CUDA_TRY(ctx, set_smem_attr(ctx, a.warp_sel + 2, select_fn(a.warp_sel), smem));
   return EQX_OK;

@@ -2459,12 +2459,12 @@ __device__ __forceinline__ void warp_select_reg(const SelectArgs& a, const Model
   __syncthreads();  // releases the helper warps
 }
 
-// Two-warp variant of warp_select_reg<1> for rosters of 33..64 clients: lane L of selection
+// Multi-warp variant of warp_select_reg<1> for rosters of 33..32*NW clients: lane L of selection
 // warp w owns client 32 w + L alone, so no lane compares or predicates over slots.  A pick is a
-// warp argmin in each selection warp, the two warp winners exchanged through double-buffered
-// shared memory behind one 64-thread named barrier, and the same select_next comparison on the
-// two; the winning lane alone updates its client.  Both warps keep identical copies of the batch
-// counters and issue the same regeneration commands.
+// warp argmin in each selection warp, the NW warp winners exchanged through double-buffered
+// shared memory behind one named barrier of the selection warps, and the same select_next
+// comparison over them; the winning lane alone updates its client.  All selection warps keep
+// identical copies of the batch counters and issue the same regeneration commands.
 struct Warp2Cand {
   uint64_t k, a, pk;
   int64_t need;
@@ -2472,10 +2472,11 @@ struct Warp2Cand {
   int32_t lane;
 };
 
-__device__ __forceinline__ void warp2_select(const SelectArgs& a, const ModelTables& M, const WinEntry* win,
+template <int NW>
+__device__ __forceinline__ void warpn_select(const SelectArgs& a, const ModelTables& M, const WinEntry* win,
                                              const ClientWork& cw, SelShared& S, const StreamScratch& T) {
   __shared__ WarpSelShared X;
-  __shared__ Warp2Cand xw[2][2];  // [pick parity][selection warp]
+  __shared__ Warp2Cand xw[2][NW];  // [pick parity][selection warp]
   const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5;
   const int32_t C = a.C, Ds = T.Ds, W = a.W;
   const Policy P = a.pol;
@@ -2484,7 +2485,7 @@ __device__ __forceinline__ void warp2_select(const SelectArgs& a, const ModelTab
   };
   regen_all(Ds);
   __syncthreads();
-  if (tid >= 64) {  // helper warps: CTA-wide stream regeneration on command
+  if (tid >= 32 * NW) {  // helper warps: CTA-wide stream regeneration on command
     for (;;) {
       __syncthreads();
       const int32_t cmd = X.cmd;
@@ -2585,12 +2586,18 @@ __device__ __forceinline__ void warp2_select(const SelectArgs& a, const ModelTab
              (static_cast<uint64_t>(static_cast<uint32_t>(has ? cur.in : 0)) << 32);
       x.need = bneed;
     }
-    asm volatile("bar.sync 1, 64;" ::: "memory");
-    const Warp2Cand x0 = xw[par][0], x1 = xw[par][1];
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * NW) : "memory");
+    Warp2Cand xb = xw[par][0];
+    int win_warp = 0;
+#pragma unroll
+    for (int w = 1; w < NW; ++w) {
+      const Warp2Cand xo = xw[par][w];
+      if (better(Cand{xo.k, xo.a, xo.o}, Cand{xb.k, xb.a, xb.o})) {
+        xb = xo;
+        win_warp = w;
+      }
+    }
     par ^= 1;
-    const bool w1 = better(Cand{x1.k, x1.a, x1.o}, Cand{x0.k, x0.a, x0.o});
-    const int win_warp = w1 ? 1 : 0;
-    const Warp2Cand& xb = w1 ? x1 : x0;
     const uint64_t pk = xb.pk;
     const int64_t need = xb.need;
     const int32_t o = static_cast<int32_t>(pk & 15), fl = static_cast<int32_t>((pk >> 4) & 31);
@@ -2819,8 +2826,8 @@ __device__ __forceinline__ void select_body(const SelectArgs& a) {
   if constexpr (kMode == 0) {  // default: single-warp selection
     warp_select_phase(a, M, win, cw, S, T);
     ns = 1;
-  } else if constexpr (kMode == 16) {  // two selection warps, one client per lane
-    warp2_select(a, M, win, cw, S, T);
+  } else if constexpr (kMode == 16 || kMode == 32) {  // 2 / 4 selection warps, one client per lane
+    warpn_select<kMode / 8>(a, M, win, cw, S, T);
     ns = 1;
   } else if constexpr (kWarp && kMode > 0) {
     warp_select_reg<kMode>(a, M, win, cw, S, T);
@@ -2888,6 +2895,7 @@ template __global__ void select_warp_kernel<2>(SelectArgs);
 template __global__ void select_warp_kernel<4>(SelectArgs);
 template __global__ void select_warp_kernel<8>(SelectArgs);
 template __global__ void select_warp_kernel<16>(SelectArgs);
+template __global__ void select_warp_kernel<32>(SelectArgs);
 
 // Event payloads (scheduler.hpp:131-138 PendingContribution) from the per-request scores the
 // scoring kernel wrote: predicted tokens, ufc/rfc increments, the VTC charge and wait_s.

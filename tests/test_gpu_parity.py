@@ -58,6 +58,18 @@ def test_random_steps_vs_oracle(seed):
     compare_step(res, sch, want)
 
 
+@pytest.mark.parametrize("C", [33, 48, 64, 65, 100, 128])
+@pytest.mark.parametrize("seed", range(3))
+def test_multiwarp_selection_rosters_vs_oracle(C, seed):
+    """Rosters of 33..128 clients take the multi-warp selection (one client per lane, warp winners
+    exchanged through shared memory); every policy mix of _random_case, bit-exact."""
+    rng = np.random.default_rng(5000 + 10 * C + seed)
+    case = _random_case(7000 + 10 * C + seed, int(rng.integers(2000, 40000)), C)
+    want = H.run_step(case, "oracle")
+    sch, res = gpu_run(case)
+    compare_step(res, sch, want)
+
+
 @pytest.mark.slow
 def test_cfg2_full_size_vs_oracle():
     """BASELINE configs[1]: 1M queued requests, 64 clients, MoPE, warm ledger, max_batch 64."""
