@@ -620,8 +620,8 @@ def run_ours(args, rank, world):
                 "bound": "pcie h2d (17 B/request; ~54.5 GB/s measured pinned H2D on the box, tools/pin_probe.py)",
                 "note": "wall clock over consecutive steps; the H2D of steps i+1, i+2 (copy stream) "
                         "overlaps step i"},
-        # per step: drain_hist, drain_rank, score, window, select, event_fill
-        "gpu_launches": 6 * args.steps,
+        # per step: drain_hist, drain_rank, window, score, select, event_fill, pack_cols (state copy)
+        "gpu_launches": 7 * args.steps,
         "clocks": clk.summary(),
     }
     if not (args.no_cpu_baseline or args.profile):
