@@ -339,7 +339,7 @@ __device__ __forceinline__ void drain_hist_body(const DrainArgs& a) {
     uint32_t t = 0;
 #pragma unroll 8
     for (int w = 0; w < kDrainWarps; ++w) t += wc[w * C + c];
-    a.hist[static_cast<int64_t>(tile) * C + c] = t;  // [tile][client]
+    a.hist[static_cast<int64_t>(c) * a.n_tiles + tile] = t;  // [client][tile]: the rank prologue reads tile runs
   }
   EQX_DT_MAX(1);
 }
@@ -398,9 +398,9 @@ __device__ __forceinline__ void drain_rank_body(const DrainArgs& a) {
         if (i0 + u * NT < nwc) wc[i0 + u * NT] = v[u];
     }
   }
-  // Every CTA derives its own global offsets from the [tile][client] histogram (no serial
-  // scan): base[c] = sum_{c' < c} total[c'] + sum_{t < tile} hist[t][c].  G threads per
-  // client split the tiles; the rows are read coalesced across clients.
+  // Every CTA derives its own global offsets from the [client][tile] histogram (no serial
+  // scan): base[c] = sum_{c' < c} total[c'] + sum_{t < tile} hist[c][t].  G threads per
+  // client split the tiles; each client's run of tile counts is read coalesced.
   for (int c = tid; c < C; c += blockDim.x) base[c] = toff[c] = 0;
   __syncthreads();
   {
@@ -417,7 +417,7 @@ __device__ __forceinline__ void drain_rank_body(const DrainArgs& a) {
 #pragma unroll
           for (int u = 0; u < 16; ++u) {
             const int32_t t = t0 + u * G;
-            h[u] = t < nt ? __ldcg(a.hist + static_cast<int64_t>(t) * C + c) : 0u;
+            h[u] = t < nt ? __ldcg(a.hist + static_cast<int64_t>(c) * nt + t) : 0u;  // coalesced over g
           }
 #pragma unroll
           for (int u = 0; u < 16; ++u) {

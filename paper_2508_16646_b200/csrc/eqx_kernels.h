@@ -55,7 +55,7 @@ struct DrainArgs {
   int32_t tile_rows;
   int32_t n_tiles;
   int32_t staged;       // 1: smem-staged coalesced scatter (when the tile fits in smem)
-  uint32_t* hist;       // [C][n_tiles] counts -> exclusive offsets
+  uint32_t* hist;       // [C][n_tiles] per-tile client counts
   int64_t hist_L;
   int32_t* seg_off;     // [C+1]
   uint32_t* perm;       // [n] row indices grouped by client, FIFO order
