@@ -986,6 +986,7 @@ static eqx_status drain_enqueue(eqx_ctx* ctx, bool lift, bool keep_qlen = false)
     CUDA_TRY(ctx, cudaMemsetAsync(dt, 0, 8 * 8, s));
     CUDA_TRY(ctx, cudaMemsetAsync(dt, 0xff, 8, s));
     CUDA_TRY(ctx, cudaMemsetAsync(dt + 24, 0xff, 8, s));
+    CUDA_TRY(ctx, cudaMemsetAsync(dt + 40, 0xff, 8, s));
   }
 #endif
   const DrainArgs d = drain_args(ctx);
@@ -1289,6 +1290,7 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl, int32_t g
   wi.W = a.W;
   wi.win = ctx->d_win.as<WinEntry>();
   wi.model = ctx->d_model.as<ModelTables>();
+  wi.st = ctx->d_state.as<DevState>();
   wi.model_words = model_words;
   wi.tmax = a.tmax;
   wi.pol = ctx->pol;
@@ -2075,6 +2077,10 @@ eqx_status eqx_phase_times(eqx_ctx* ctx, double* out_us, int32_t n) {
   const unsigned long long* dt = ctx->h_state->dt;  // EQX_PROF drain timeline (us from hist start)
   for (int i = 16; i < n && i < 22; ++i) out_us[i] = (static_cast<double>(dt[i - 16]) - static_cast<double>(dt[0])) * 1e-3;
   if (n > 22) out_us[22] = (base - static_cast<double>(dt[0])) * 1e-3;  // selection start after drain start
+  if (n > 24) {  // window kernel first CTA past its wait / last CTA done, after drain start
+    out_us[23] = (static_cast<double>(dt[5]) - static_cast<double>(dt[0])) * 1e-3;
+    out_us[24] = (static_cast<double>(dt[6]) - static_cast<double>(dt[0])) * 1e-3;
+  }
   return EQX_OK;
 }
 

@@ -971,6 +971,9 @@ __global__ void __launch_bounds__(256) window_kernel(const WindowArgs a) {
   stage_model(a.model, a.model_words, smem);  // overlaps the drain's tail (programmatic launch)
   pdl_wait();
   pdl_trigger();  // the drain is complete: the selection CTA may start its prologue
+#ifdef EQX_PROF
+  if (threadIdx.x == 0) atomicMin(&a.st->dt[5], global_ns());
+#endif
   __syncthreads();
   const ModelTables& M = *reinterpret_cast<const ModelTables*>(smem);
   const int64_t items = static_cast<int64_t>(a.C) * a.W;
@@ -980,6 +983,10 @@ __global__ void __launch_bounds__(256) window_kernel(const WindowArgs a) {
     const int32_t j = a.head[c] + static_cast<int32_t>(it % a.W);
     if (j < a.count[c]) a.win[it] = make_entry(a, M, static_cast<int32_t>(a.perm[a.seg_off[c] + j]), a.weight[c]);
   }
+#ifdef EQX_PROF
+  __syncthreads();
+  if (threadIdx.x == 0) atomicMax(&a.st->dt[6], global_ns());
+#endif
 }
 
 __device__ __forceinline__ Cand cand_of(const ClientWork& cw, int32_t c) {
@@ -2752,6 +2759,9 @@ __device__ __forceinline__ void select_body(const SelectArgs& a) {
     lift_core<int32_t>(l, a.first_row);
     __syncthreads();
   }
+#ifdef EQX_PROF
+  if (tid == 0) a.st->t[8] = global_ns() - a.st->t[0];  // ns after the selection start
+#endif
   // ---- ledger in, head windows (bulk copy of window_kernel's [C][W] entries) ----
   for (int32_t c = tid; c < C; c += NT) {
     cw.ufc[c] = a.ufc[c];
@@ -2767,7 +2777,13 @@ __device__ __forceinline__ void select_body(const SelectArgs& a) {
     cw.flags[c] = a.backlogged[c] ? kBacklogged : 0;
     cw.adm[c] = 0;
   }
+#ifdef EQX_PROF
+  if (tid == 0) a.st->t[9] = global_ns() - a.st->t[0];
+#endif
   pdl_wait();  // window_kernel's [C][W] entries (programmatic launch: the prologue above overlapped it)
+#ifdef EQX_PROF
+  if (tid == 0) a.st->t[10] = global_ns() - a.st->t[0];
+#endif
   if (a.gW > 0 && a.gW != a.W) {  // gathered [C][gW] windows: the first W of every client
     constexpr int kWords = sizeof(WinEntry) / 8;
     const int64_t per = static_cast<int64_t>(a.W) * kWords;

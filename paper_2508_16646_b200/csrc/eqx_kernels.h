@@ -126,6 +126,7 @@ struct WindowArgs {
   int64_t tmax;
   Policy pol;
   double now;
+  DevState* st;          // EQX_PROF timeline stamps (dt[5] window start, dt[6] window end)
 };
 
 struct SelectArgs {
