@@ -1296,6 +1296,15 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl, int32_t g
   wi.pol = ctx->pol;
   wi.frozen = ctx->live_mode ? ctx->frozen : Frozen{};
   wi.now = now;
+  wi.do_lift = 0;  // eqx_drain_step_async moves the lift here
+  wi.counter_lift = ctx->counter_lift;
+  wi.qlen_before = ctx->d_qlen_before.as<int32_t>();
+  wi.running = ctx->d_running.as<int32_t>();
+  wi.first_row = ctx->d_first.as<int32_t>();
+  wi.ufc = ctx->d_ufc.as<double>();
+  wi.rfc = ctx->d_rfc.as<double>();
+  wi.counter = ctx->d_counter.as<double>();
+  wi.backlogged = ctx->d_backlogged.as<int32_t>();
   pl.window_smem = model_smem;
   const int64_t witems = static_cast<int64_t>(C) * a.W;
   pl.window_grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((witems + 255) / 256, 8ll * ctx->sm_count)));
@@ -1431,7 +1440,12 @@ eqx_status eqx_drain_step_async(eqx_ctx* ctx, const eqx_requests* r, double now)
   StepPlan pl;
   st = step_prepare(ctx, now, pl);
   if (st != EQX_OK) return st;
-  pl.se.do_lift = 1;  // the fused drain leaves on_activated to the selection prologue
+  // the fused drain leaves on_activated / set_backlogged to an extra CTA of the window kernel
+  // (the selection CTA, launched programmatically behind it, reads the ledger after its wait)
+  pl.wi.do_lift = 1;
+  pl.window_grid += 1;
+  pl.se.do_lift = 0;
+  pl.se.ledger_after_wait = 1;
   cudaStream_t s = ctx->stream;
   // One CUDA-graph launch replays drain + scoring + selection.  The key covers every launch
   // parameter (pointers, sizes, policy, `now`, smem/tiling plan); two graphs are cached, for a

@@ -976,9 +976,15 @@ __global__ void __launch_bounds__(256) window_kernel(const WindowArgs a) {
 #endif
   __syncthreads();
   const ModelTables& M = *reinterpret_cast<const ModelTables*>(smem);
+  const int entry_ctas = gridDim.x - (a.do_lift ? 1 : 0);
+  if (static_cast<int>(blockIdx.x) >= entry_ctas) {  // the extra CTA: the drain's counter lift
+    const LiftIn l{a.C, a.counter_lift, a.count, a.qlen_before, a.running, a.ufc, a.rfc, a.counter, a.backlogged};
+    lift_core<int32_t>(l, a.first_row);
+    return;
+  }
   const int64_t items = static_cast<int64_t>(a.C) * a.W;
   for (int64_t it = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; it < items;
-       it += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+       it += static_cast<int64_t>(entry_ctas) * blockDim.x) {
     const int32_t c = static_cast<int32_t>(it / a.W);
     const int32_t j = a.head[c] + static_cast<int32_t>(it % a.W);
     if (j < a.count[c]) a.win[it] = make_entry(a, M, static_cast<int32_t>(a.perm[a.seg_off[c] + j]), a.weight[c]);
@@ -2763,24 +2769,28 @@ __device__ __forceinline__ void select_body(const SelectArgs& a) {
   if (tid == 0) a.st->t[8] = global_ns() - a.st->t[0];  // ns after the selection start
 #endif
   // ---- ledger in, head windows (bulk copy of window_kernel's [C][W] entries) ----
-  for (int32_t c = tid; c < C; c += NT) {
-    cw.ufc[c] = a.ufc[c];
-    cw.rfc[c] = a.rfc[c];
-    cw.cnt[c] = a.counter[c];
-    cw.w[c] = a.weight[c];
-    cw.pos[c] = a.head[c];
-    cw.pos0[c] = a.head[c];
-    cw.end[c] = a.count[c];
-    const uint32_t o = a.order[c];
-    cw.order[c] = o;
-    cw.by_order[o] = c;
-    cw.flags[c] = a.backlogged[c] ? kBacklogged : 0;
-    cw.adm[c] = 0;
-  }
+  auto ledger_in = [&]() {
+    for (int32_t c = tid; c < C; c += NT) {
+      cw.ufc[c] = a.ufc[c];
+      cw.rfc[c] = a.rfc[c];
+      cw.cnt[c] = a.counter[c];
+      cw.w[c] = a.weight[c];
+      cw.pos[c] = a.head[c];
+      cw.pos0[c] = a.head[c];
+      cw.end[c] = a.count[c];
+      const uint32_t o = a.order[c];
+      cw.order[c] = o;
+      cw.by_order[o] = c;
+      cw.flags[c] = a.backlogged[c] ? kBacklogged : 0;
+      cw.adm[c] = 0;
+    }
+  };
+  if (!a.ledger_after_wait) ledger_in();
 #ifdef EQX_PROF
   if (tid == 0) a.st->t[9] = global_ns() - a.st->t[0];
 #endif
   pdl_wait();  // window_kernel's [C][W] entries (programmatic launch: the prologue above overlapped it)
+  if (a.ledger_after_wait) ledger_in();  // lifted by the window kernel's extra CTA
 #ifdef EQX_PROF
   if (tid == 0) a.st->t[10] = global_ns() - a.st->t[0];
 #endif

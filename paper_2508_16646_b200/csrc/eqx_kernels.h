@@ -127,6 +127,16 @@ struct WindowArgs {
   Policy pol;
   double now;
   DevState* st;          // EQX_PROF timeline stamps (dt[5] window start, dt[6] window end)
+  // drain + step: the last CTA runs the drain's counter lift (on_activated / set_backlogged)
+  // beside the window entries, off the selection CTA's critical path
+  int32_t do_lift, counter_lift;
+  const int32_t* qlen_before;
+  const int32_t* running;
+  const int32_t* first_row;
+  double* ufc;
+  double* rfc;
+  double* counter;
+  int32_t* backlogged;
 };
 
 struct SelectArgs {
@@ -154,6 +164,8 @@ struct SelectArgs {
   int32_t K;             // register client slots per selection thread (1/2/4/8; 0 = smem loop)
   int32_t warp_sel;      // selection kernel variant (eqx_capi.cu select_fn)
   int32_t do_lift;       // run the drain's counter lift / backlog flags first (drain + step)
+  int32_t ledger_after_wait;  // the preceding window kernel lifted the ledger: load it after the
+                              // programmatic wait
   const int32_t* first_row;
   const int32_t* qlen_before;
   int32_t counter_lift;
