@@ -339,7 +339,9 @@ __device__ __forceinline__ void drain_hist_body(const DrainArgs& a) {
     uint32_t t = 0;
 #pragma unroll 8
     for (int w = 0; w < kDrainWarps; ++w) t += wc[w * C + c];
-    a.hist[static_cast<int64_t>(c) * a.n_tiles + tile] = t;  // [client][tile]: the rank prologue reads tile runs
+    // small rosters: [client][tile] (the rank prologue's thread groups read tile runs);
+    // large rosters (one thread per client): [tile][client] (a warp reads adjacent clients)
+    a.hist[C <= kHistClientMajor ? static_cast<int64_t>(c) * a.n_tiles + tile : static_cast<int64_t>(tile) * C + c] = t;
   }
   EQX_DT_MAX(1);
 }
@@ -398,9 +400,9 @@ __device__ __forceinline__ void drain_rank_body(const DrainArgs& a) {
         if (i0 + u * NT < nwc) wc[i0 + u * NT] = v[u];
     }
   }
-  // Every CTA derives its own global offsets from the [client][tile] histogram (no serial
-  // scan): base[c] = sum_{c' < c} total[c'] + sum_{t < tile} hist[c][t].  G threads per
-  // client split the tiles; each client's run of tile counts is read coalesced.
+  // Every CTA derives its own global offsets from the histogram (no serial scan):
+  // base[c] = sum_{c' < c} total[c'] + sum_{t < tile} hist(c, t).  G threads per client split
+  // the tiles; the layout (kHistClientMajor) keeps either layout's reads coalesced.
   for (int c = tid; c < C; c += blockDim.x) base[c] = toff[c] = 0;
   __syncthreads();
   {
@@ -417,7 +419,9 @@ __device__ __forceinline__ void drain_rank_body(const DrainArgs& a) {
 #pragma unroll
           for (int u = 0; u < 16; ++u) {
             const int32_t t = t0 + u * G;
-            h[u] = t < nt ? __ldcg(a.hist + static_cast<int64_t>(c) * nt + t) : 0u;  // coalesced over g
+            h[u] = t < nt ? __ldcg(a.hist + (C <= kHistClientMajor ? static_cast<int64_t>(c) * nt + t
+                                                                   : static_cast<int64_t>(t) * C + c))
+                          : 0u;
           }
 #pragma unroll
           for (int u = 0; u < 16; ++u) {

@@ -11,6 +11,7 @@ namespace eqx {
 
 constexpr int kDrainThreads = 1024;  // 32 warps per tile
 constexpr int kDrainWarps = kDrainThreads / 32;
+constexpr int kHistClientMajor = 128;  // rosters up to this size store the drain histogram [client][tile]
 constexpr int kScoreThreads = 256;
 constexpr int kScoreTmaThreads = 256;                        // score_tma_kernel block
 constexpr int kScoreTile = 1024;                             // requests per bulk-copied tile
@@ -55,7 +56,7 @@ struct DrainArgs {
   int32_t tile_rows;
   int32_t n_tiles;
   int32_t staged;       // 1: smem-staged coalesced scatter (when the tile fits in smem)
-  uint32_t* hist;       // [C][n_tiles] per-tile client counts
+  uint32_t* hist;       // per-tile client counts: [C][n_tiles] (C <= kHistClientMajor) or [n_tiles][C]
   int64_t hist_L;
   int32_t* seg_off;     // [C+1]
   uint32_t* perm;       // [n] row indices grouped by client, FIFO order
