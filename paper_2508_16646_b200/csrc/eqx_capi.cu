@@ -1383,6 +1383,7 @@ static eqx_status step_enqueue(eqx_ctx* ctx, const StepPlan& pl, bool with_drain
   CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_join, 0));
   EventFillArgs ef;
   std::memset(&ef, 0, sizeof(ef));
+  ef.st = ctx->d_state.as<DevState>();
   ef.n_events = &ctx->d_state.as<DevState>()->n_events;
   ef.ev_cap = ctx->ev_cap;
   ef.ev_row = ctx->d_ev_row.as<int32_t>();
@@ -2027,6 +2028,7 @@ eqx_status eqx_shard_select_async(eqx_ctx* ctx, const void* recs, int32_t world,
   CUDA_TRY(ctx, cudaGetLastError());
   EventFillArgs ef;
   std::memset(&ef, 0, sizeof(ef));
+  ef.st = ctx->d_state.as<DevState>();
   ef.n_events = &ctx->d_state.as<DevState>()->n_events;
   ef.ev_cap = ctx->ev_cap;
   ef.ev_row = ctx->d_ev_row.as<int32_t>();
@@ -2094,6 +2096,10 @@ eqx_status eqx_phase_times(eqx_ctx* ctx, double* out_us, int32_t n) {
   if (n > 24) {  // window kernel first CTA past its wait / last CTA done, after drain start
     out_us[23] = (static_cast<double>(dt[5]) - static_cast<double>(dt[0])) * 1e-3;
     out_us[24] = (static_cast<double>(dt[6]) - static_cast<double>(dt[0])) * 1e-3;
+  }
+  if (n > 26) {  // selection epilogue done / last event-fill CTA done, after drain start
+    out_us[25] = (static_cast<double>(t[12]) - static_cast<double>(dt[0])) * 1e-3;
+    out_us[26] = (static_cast<double>(dt[7]) - static_cast<double>(dt[0])) * 1e-3;
   }
   return EQX_OK;
 }

@@ -2911,6 +2911,9 @@ __device__ __forceinline__ void select_body(const SelectArgs& a) {
     a.st->n_admitted = S.n_adm;
     a.st->n_rejected = S.n_rej;
     a.st->new_prefill = S.prefill;
+#ifdef EQX_PROF
+    if (kMode == 16 || kMode == 32) a.st->t[12] = global_ns();  // selection epilogue done
+#endif
   }
 }
 
@@ -2951,6 +2954,10 @@ __global__ void event_fill_kernel(const EventFillArgs a) {
     a.ev_vtc[i] = v;
     a.ev_wait[i] = adm ? __dsub_rn(a.now, a.arrival[row]) : 0.0;  // engine.cpp:257
   }
+#ifdef EQX_PROF
+  __syncthreads();
+  if (threadIdx.x == 0) atomicMax(&a.st->dt[7], global_ns());
+#endif
 }
 
 __global__ void gather_ids_kernel(const int32_t* __restrict__ rows, int64_t n, const int64_t* __restrict__ id,

@@ -200,6 +200,7 @@ struct SelectArgs {
 };
 
 struct EventFillArgs {
+  DevState* st;             // EQX_PROF stamp (dt[7]: last event-fill CTA done)
   const int64_t* n_events;  // &DevState::n_events
   int64_t ev_cap;
   const int32_t* ev_row;

@@ -16,12 +16,12 @@ rows = []
 for i in range(12):
     sch.restore_async(); flush.zero_(); torch.cuda.synchronize()
     sch.drain_step_async(1.0, **cols); r = sch.collect(with_events=False)
-    out = (C.c_double * 25)()
-    L.load().eqx_phase_times(sch._ctx, out, 25)
+    out = (C.c_double * 27)()
+    L.load().eqx_phase_times(sch._ctx, out, 27)
     s0 = out[22]
     rows.append([out[17], out[19], out[20], out[23], out[24], s0, s0 + out[1], s0 + out[2], s0 + out[3], s0 + out[4],
-                 s0 + out[5], s0 + out[8] * 1e-3, s0 + out[9] * 1e-3, s0 + out[10] * 1e-3])
+                 s0 + out[5], s0 + out[8] * 1e-3, s0 + out[9] * 1e-3, s0 + out[10] * 1e-3, out[25], out[26]])
 a = np.median(np.array(rows[2:]), axis=0)
 names = ["hist_end", "rank_start", "rank_end", "window_start", "window_end", "select_start", "windows_filled",
-         "loop_start", "loop_end", "score_start", "score_end", "sel_lift_done", "sel_ledger_in", "sel_wait_done"]
+         "loop_start", "loop_end", "score_start", "score_end", "sel_lift_done", "sel_ledger_in", "sel_wait_done", "select_done", "event_fill_done"]
 print(" ".join(f"{n}={v:.1f}" for n, v in zip(names, a)))
