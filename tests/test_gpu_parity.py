@@ -136,3 +136,54 @@ def test_staged_host_batches_in_order():
             sch.drain(**c)
             res = sch.step(case.now)
             compare_step(res, sch, want)
+
+
+def _graph_step(case, device_columns: bool, staged: bool = False, reps: int = 2):
+    """The path bench.py times: eqx_drain_step_async (one CUDA-graph replay of drain, windows
+    with the counter lift, scoring and selection), repeated on the restored ledger so the cached
+    graph is replayed, then eqx_step_collect."""
+    import torch
+    from helpers import case_batch, case_clients, case_columns, case_kwargs
+    from paper_2508_16646_b200 import scheduler as S
+    sch = S.GpuScheduler(case_clients(case), running=case.running, **case_kwargs(case))
+    sch.set_batch(*case_batch(case))
+    sch.checkpoint()
+    cols = case_columns(case)
+    if device_columns:
+        cols = {k: torch.from_numpy(v).cuda() for k, v in cols.items()}
+    elif staged:
+        cols = {k: S.pinned_copy(v) for k, v in cols.items()}
+    res = None
+    for _ in range(reps):
+        sch.restore_async()
+        if staged:
+            sch.stage_async(**cols)
+        sch.drain_step_async(case.now, **cols)
+        res = sch.collect(with_events=True)
+    return sch, res
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_golden_graph_step(name):
+    """Every golden through the graph path with resident device columns."""
+    meta, ins, outs = load_golden(name)
+    case = case_from_golden(meta, ins)
+    sch, res = _graph_step(case, device_columns=True)
+    if res.noisy_near_ties:
+        pytest.skip(f"{res.noisy_near_ties} flagged near-ties (log1p ulp) -- allowed by the north star")
+    compare_step(res, sch, outs)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_graph_steps_vs_oracle(seed):
+    """Random policies / rosters (with running clients and warm ledgers, so the counter lift in
+    the window kernel's extra CTA has work) through the graph path, host columns staged from the
+    pinned arena on even seeds, device columns on odd ones."""
+    rng = np.random.default_rng(9000 + seed)
+    C = int(rng.choice([5, 31, 64, 100, 200, 777]))
+    case = _random_case(9100 + seed, int(rng.integers(1000, 50000)), C)
+    case.finalize()
+    case.running = (rng.random(C) < 0.3).astype(np.int32) * rng.integers(0, 3, C).astype(np.int32)
+    want = H.run_step(case, "oracle")
+    sch, res = _graph_step(case, device_columns=bool(seed % 2), staged=not seed % 2)
+    compare_step(res, sch, want)
