@@ -1634,7 +1634,13 @@ eqx_status eqx_replay(eqx_ctx* ctx, const eqx_replays* R, eqx_replay_out* O) {
   A.diff = O->diff && wcap > 0 ? reinterpret_cast<double*>(b + o_diff) : nullptr;
   A.rate = O->rate && wcap > 0 ? reinterpret_cast<double*>(b + o_rate) : nullptr;
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[2], s));
-  replay_kernel<<<(nr + 3) / 4, 128, 0, s>>>(A);  // one warp per replay
+  {  // one warp per replay; the instantiation of the context's policy (explicit in eqx_replay.cu)
+    const void* rk = ctx->pol.kind == kFcfs  ? reinterpret_cast<const void*>(replay_kernel<kFcfs>)
+                     : ctx->pol.kind == kVtc ? reinterpret_cast<const void*>(replay_kernel<kVtc>)
+                                             : reinterpret_cast<const void*>(replay_kernel<kEquinox>);
+    void* args[] = {&A};
+    CUDA_TRY(ctx, cudaLaunchKernel(rk, dim3((nr + 3) / 4), dim3(128), args, 0, s));
+  }
   CUDA_TRY(ctx, cudaGetLastError());
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[3], s));
   const Col cols[] = {{O->n_events, b + o_nev, 8 * n8},       {O->ev_id, b + o_evid, 8 * n8 * cap},

@@ -406,7 +406,8 @@ struct ReplayArgs {
   double* diff;               // [n_replays][win_cap][2]
   double* rate;               // [n_replays][C][win_cap] (zeroed by the host)
 };
-__global__ void replay_kernel(ReplayArgs a);
+template <int KIND>
+__global__ void replay_kernel(ReplayArgs a);  // KIND: kFcfs / kVtc / kEquinox
 
 __global__ void drain_hist_kernel(DrainArgs a);
 __global__ void lift_kernel(DrainArgs a);

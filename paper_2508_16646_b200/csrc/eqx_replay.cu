@@ -230,6 +230,9 @@ __device__ __noinline__ void rep_rate_advance(Reporter& R, ReplayClient* cl, int
   R.rate_w = w;
 }
 
+// KIND: the policy kind, fixed per instantiation so a replay carries only its policy's code
+// (the kernel is long scalar code; its instruction footprint is what its single warps stall on).
+template <int KIND>
 __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
   __shared__ uint32_t s_hist[4][256];  // radix-select histograms, one per warp
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -403,7 +406,7 @@ __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
     uint64_t skipped = 0;
     for (;;) {
       double mu = 0.0, mr = 0.0;  // backlogged_maxima (scheduler.cpp:40-48)
-      const bool maxmode = P.kind == kEquinox && P.norm_mode == 0;
+      const bool maxmode = KIND == kEquinox && P.norm_mode == 0;
       if (maxmode)
         for (int i = 0; i < C; ++i)
           if (cl[i].backlogged) {
@@ -416,8 +419,8 @@ __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
       for (int i = 0; i < C; ++i) {
         if (cl[i].qhead == cl[i].qend || ((skipped >> (i & 63)) & 1u)) continue;
         double k;
-        if (P.kind == kFcfs) k = 0.0;
-        else if (P.kind == kVtc) k = cl[i].counter;
+        if (KIND == kFcfs) k = 0.0;
+        else if (KIND == kVtc) k = cl[i].counter;
         else if (P.norm_mode == 1) k = __dadd_rn(__dmul_rn(eq.alpha, cl[i].ufc), __dmul_rn(eq.beta, cl[i].rfc));
         else {
           const double u = mu > 0.0 ? __ddiv_rn(cl[i].ufc, mu) : 0.0;
@@ -477,7 +480,7 @@ __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
       m.p_vtc = 0.0;
       cl[c].ufc = __dadd_rn(cl[c].ufc, m.p_ufc);
       cl[c].rfc = __dadd_rn(cl[c].rfc, m.p_rfc);
-      if (P.kind == kVtc) {
+      if (KIND == kVtc) {
         m.p_vtc = P.vtc_use_prediction ? __dmul_rn(w, tokens) : __dmul_rn(w, static_cast<double>(in));
         cl[c].counter = __dadd_rn(cl[c].counter, m.p_vtc);
       }
@@ -518,7 +521,7 @@ __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
       if (mb[j].generated == 1) f_ttft[mb[j].row] = __dsub_rn(now, arrival[mb[j].row]);  // FirstToken
     }
     __syncwarp();
-    if (P.kind == kVtc && !P.vtc_use_prediction) {  // on_tokens per client (scheduler.cpp:185-190)
+    if (KIND == kVtc && !P.vtc_use_prediction) {  // on_tokens per client (scheduler.cpp:185-190)
       for (int c = 0; c < C; ++c) {
         int64_t t = 0;
         for (int j = lane; j < members; j += 32) t += mb[j].client == c ? 1 : 0;
@@ -586,7 +589,7 @@ __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
           cl[c].bucket = __dadd_rn(cl[c].bucket, wwt);
           cl[c].merged = __dadd_rn(cl[c].merged, wwt);
         }
-        if (P.kind == kVtc && P.vtc_use_prediction) {
+        if (KIND == kVtc && P.vtc_use_prediction) {
           double k = __dadd_rn(cl[c].counter, __dsub_rn(wwt, m.p_vtc));
           if (k < 0.0) {
             k = 0.0;
@@ -728,5 +731,9 @@ __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
     A.out_counter[static_cast<int64_t>(r) * C + c] = cl[c].counter;
   }
 }
+
+template __global__ void replay_kernel<kFcfs>(ReplayArgs);
+template __global__ void replay_kernel<kVtc>(ReplayArgs);
+template __global__ void replay_kernel<kEquinox>(ReplayArgs);
 
 }  // namespace eqx
