@@ -147,6 +147,7 @@ struct eqx_ctx {
   // client-sharded step (selection context): gathered windows and their ids
   DevBuf d_first64, d_gid;
   DevBuf d_service;                // ClientState::accumulated_service
+  DevBuf d_tk, d_tkh;              // top-K selection: items beyond shared memory, head tuples
   // engine timing (PerfParams, gpu_model.hpp:14-28) for replays
   double prefill_linear_ms = 0.05, prefill_quad_ms = 1e-6, decode_base_ms = 5.0, decode_per_ctx_ms = 0.002,
          refresh_ms = 15.0;
@@ -203,6 +204,7 @@ const void* select_fn(int warp_sel) {
     case 5: return reinterpret_cast<const void*>(select_warp_kernel<8>);
     case 6: return reinterpret_cast<const void*>(select_warp_kernel<16>);
     case 7: return reinterpret_cast<const void*>(select_warp_kernel<32>);
+    case 8: return reinterpret_cast<const void*>(select_topk_kernel);
     default: return reinterpret_cast<const void*>(select_kernel);
   }
 }
@@ -1183,6 +1185,67 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl, int32_t g
   a.frozen = ctx->live_mode ? ctx->frozen : Frozen{};
   a.now = now;
   pl.select_threads = kSelectMaxThreads;
+  // Default: rounds of block-radix top-K over per-client key streams (select_topk_kernel,
+  // eqx_topk.cuh).  EQX_SELECT_MODE=seq keeps the sequential pick loops below (the reference
+  // loop one pick at a time; the -m gpu suite runs both).
+  const char* sel_mode = std::getenv("EQX_SELECT_MODE");
+  const bool topk = !(sel_mode && std::string(sel_mode) == "seq");
+  bool batch_kernel = false;
+  if (topk) {
+    const size_t static_smem = 12288;
+    const int32_t kcap = kTopkThreads;
+    const size_t cw_bytes = 13ull * 16 + static_cast<size_t>(C) * (6 * 8 + 7 * 4);
+    const size_t k_bytes = static_cast<size_t>(kcap) * (6 * 4 + 3 * 8 + 3 * 4 + sizeof(WinEntry)) + 15 * 16 + 4 * 256 +
+                           8 * 160 * (kTopkThreads / 32);
+    const size_t heads_bytes = C > kcap ? 17 * static_cast<size_t>((C + 1) & ~1) + 16 : 0;
+    const size_t per_item = 5 * 8 + 2 + 4;  // k, a, u, r, cn, fl, st, sd
+    const size_t min_items = 1024;
+    // shared memory: model | per-client work | ranked list | head tuples | stream items (the
+    // rest); per-client work and head tuples fall back to global scratch on huge rosters
+    const size_t fixed = static_smem + model_smem + k_bytes + min_items * per_item + 8 * 16;
+    size_t smem = model_smem + k_bytes;
+    a.cw_in_smem = fixed + cw_bytes + heads_bytes <= ctx->smem_optin ||
+                   (heads_bytes > 0 && fixed + cw_bytes <= ctx->smem_optin && cw_bytes >= heads_bytes);
+    if (a.cw_in_smem) {
+      a.cw_global = nullptr;
+      smem += cw_bytes;
+    } else {
+      CUDA_TRY(ctx, ctx->d_cw.ensure(cw_bytes));
+      a.cw_global = ctx->d_cw.p;
+    }
+    a.tk_heads = nullptr;
+    if (heads_bytes > 0) {
+      if (static_smem + smem + heads_bytes + min_items * per_item + 8 * 16 <= ctx->smem_optin) {
+        smem += heads_bytes;
+      } else {
+        CUDA_TRY(ctx, ctx->d_tkh.ensure(heads_bytes));
+        a.tk_heads = ctx->d_tkh.p;
+      }
+    }
+    // head windows stay in HBM/L2 (window_kernel output): deep enough for a client taking every
+    // free slot on small rosters, a few entries per client on huge ones
+    int64_t W = std::min<int64_t>(static_cast<int64_t>(ctx->perf.max_batch) + 2,
+                                  std::max<int64_t>(4, (1 << 16) / std::max(C, 1)));
+    if (gW > 0) W = std::min<int64_t>(W, gW);
+    a.W = static_cast<int32_t>(W);
+    a.gW = gW;
+    // stream items per round: the rest of shared memory, at most 4096; the depth per client (a
+    // power of two <= 64) is fitted per round on the device
+    const int64_t cap = std::min<int64_t>(4096, static_cast<int64_t>((ctx->smem_optin - static_smem - smem - 8 * 16) / per_item));
+    smem += static_cast<size_t>(cap) * per_item + 8 * 16;
+    a.tk_cap = static_cast<int32_t>(cap);
+    a.tk_dsh = 6;
+    a.tk_kcap = kcap;
+    a.K = 0;
+    a.D = 0;
+    a.Ds = 0;
+    a.sel_threads = kTopkThreads;
+    a.warp_sel = 8;
+    pl.select_threads = kTopkThreads;
+    pl.select_smem = smem;
+    CUDA_TRY(ctx, ctx->d_win.ensure(std::max<size_t>(static_cast<size_t>(gW > 0 ? gW : a.W) * C * sizeof(WinEntry), 64)));
+    a.win_g = ctx->d_win.as<WinEntry>();
+  } else {
   // selection threads: one warp holding up to 8 clients per lane when C <= 256 (no barriers),
   // otherwise up to 8 warps with 1/2/4/8 register slots per thread; beyond 2048 clients the
   // shared-memory loop (seq_phase) takes over.
@@ -1232,7 +1295,6 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl, int32_t g
                     batch_bytes(D) + static_cast<size_t>(D) * C * sizeof(WinEntry) > left0))
     --D;
   if (D < 2 || C == 0) D = 0;
-  bool batch_kernel = false;
   // Default: register-resident sequential picks (measured faster than speculative batches on
   // cfg2/cfg3, profiles/); EQX_SELECT_MODE=batch enables the batch path for experiments.
   {
@@ -1274,6 +1336,7 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl, int32_t g
   pl.select_smem = smem;
   CUDA_TRY(ctx, ctx->d_win.ensure(std::max<size_t>(static_cast<size_t>(gW > 0 ? gW : a.W) * C * sizeof(WinEntry), 64)));
   a.win_g = ctx->d_win.as<WinEntry>();
+  }  // sequential pick loops
   WindowArgs& wi = pl.wi;
   wi.arrival = ctx->q_arrival;
   wi.in_tok = ctx->q_in;
@@ -1308,6 +1371,10 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl, int32_t g
   pl.window_smem = model_smem;
   const int64_t witems = static_cast<int64_t>(C) * a.W;
   pl.window_grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((witems + 255) / 256, 8ll * ctx->sm_count)));
+  if (topk) {
+    CUDA_TRY(ctx, set_smem_attr(ctx, 10, select_fn(a.warp_sel), pl.select_smem));
+    return EQX_OK;
+  }
   a.warp_sel = a.warp_sel && a.D == 0 && a.K > 0 && a.Ds > 0;
   if (batch_kernel && a.D > 0) a.warp_sel = 5;  // batch kernel variant (select_fn)
   // kernel variant (select_fn): register slots up to 128 clients; larger rosters keep the
@@ -1319,7 +1386,7 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl, int32_t g
     a.warp_sel = C <= 32 ? 2 : C <= 64 ? (slots ? 3 : 6) : C <= 128 ? (slots ? 4 : 7)
                                                                   : (m && std::string(m) == "warp") ? 1 : 0;
   }
-  CUDA_TRY(ctx, set_smem_attr(ctx, a.warp_sel + 2, select_fn(a.warp_sel), smem));
+  CUDA_TRY(ctx, set_smem_attr(ctx, a.warp_sel + 2, select_fn(a.warp_sel), pl.select_smem));
   return EQX_OK;
 }
 

@@ -2700,7 +2700,10 @@ __device__ __forceinline__ void warpn_select(const SelectArgs& a, const ModelTab
   __syncthreads();  // releases the helper warps
 }
 
-// kMode: -1 multi-mode loops (select_kernel); 0 warp_select_phase; 1/2/4 warp_select_reg<kMode>
+#include "eqx_topk.cuh"
+
+// kMode: -1 multi-mode loops (select_kernel); 0 warp_select_phase; 1/2/4 warp_select_reg<kMode>;
+// 64: rounds of block-radix top-K (topk_select)
 template <int kMode>
 __device__ __forceinline__ void select_body(const SelectArgs& a) {
   constexpr bool kWarp = kMode >= 0 && kMode != 8;  // 8: speculative batches + shared-memory picks
@@ -2760,6 +2763,44 @@ __device__ __forceinline__ void select_body(const SelectArgs& a) {
     T.sd = reinterpret_cast<int32_t*>(carve(4ull * C));
     T.sdl = reinterpret_cast<int32_t*>(carve(4ull * C));
   }
+  TopkScratch TK;
+  if constexpr (kMode == 64) {
+    const size_t items = static_cast<size_t>(a.tk_cap);
+    const size_t kc = static_cast<size_t>(a.tk_kcap);
+    TK.dsh_max = a.tk_dsh;
+    TK.Kcap = a.tk_kcap;
+    TK.cap = a.tk_cap;
+    TK.k = reinterpret_cast<uint64_t*>(carve(8 * items));  // stream items: always shared memory
+    TK.a = reinterpret_cast<uint64_t*>(carve(8 * items));
+    TK.u = reinterpret_cast<double*>(carve(8 * items));
+    TK.r = reinterpret_cast<double*>(carve(8 * items));
+    TK.cn = reinterpret_cast<double*>(carve(8 * items));
+    TK.fl = reinterpret_cast<uint8_t*>(carve(items));
+    TK.st = reinterpret_cast<uint8_t*>(carve(items));
+    TK.sd = reinterpret_cast<uint32_t*>(carve(4 * items));
+    TK.sc = reinterpret_cast<int32_t*>(carve(4 * kc));
+    TK.snd = reinterpret_cast<int32_t*>(carve(4 * kc));
+    TK.spos = reinterpret_cast<int32_t*>(carve(4 * kc));
+    TK.sk0 = reinterpret_cast<int32_t*>(carve(4 * kc));
+    TK.off = reinterpret_cast<int32_t*>(carve(4 * kc));
+    TK.cut = reinterpret_cast<int32_t*>(carve(4 * kc));
+    TK.gk = reinterpret_cast<uint64_t*>(carve(8 * kc));
+    TK.ga = reinterpret_cast<uint64_t*>(carve(8 * kc));
+    TK.go = reinterpret_cast<uint64_t*>(carve(8 * kc));
+    TK.gx = reinterpret_cast<int32_t*>(carve(4 * kc));
+    TK.rank = reinterpret_cast<int32_t*>(carve(4 * kc));
+    TK.srt = reinterpret_cast<int32_t*>(carve(4 * kc));
+    TK.ent = reinterpret_cast<WinEntry*>(carve(sizeof(WinEntry) * kc));
+    TK.hist = reinterpret_cast<uint32_t*>(carve(4 * 256));
+    TK.stage = reinterpret_cast<uint64_t*>(carve(8 * 160 * (kTopkThreads / 32)));
+    // head tuples (rosters beyond tk_kcap): shared memory when they fit, else global scratch
+    unsigned char* hp = nullptr;
+    const size_t cc = static_cast<size_t>((C + 1) & ~1);
+    if (C > a.tk_kcap) hp = a.tk_heads ? reinterpret_cast<unsigned char*>(a.tk_heads) : carve(17 * cc + 16);
+    TK.hk = reinterpret_cast<uint64_t*>(hp);
+    TK.ha = hp ? reinterpret_cast<uint64_t*>(hp + 8 * cc) : nullptr;
+    TK.hst = hp ? hp + 16 * cc : nullptr;
+  }
   WinEntry* win = reinterpret_cast<WinEntry*>(p);
   __syncthreads();
   const ModelTables& M = *reinterpret_cast<const ModelTables*>(smem);
@@ -2798,7 +2839,9 @@ __device__ __forceinline__ void select_body(const SelectArgs& a) {
 #ifdef EQX_PROF
   if (tid == 0) a.st->t[10] = global_ns() - a.st->t[0];
 #endif
-  if (a.gW > 0 && a.gW != a.W) {  // gathered [C][gW] windows: the first W of every client
+  if (kMode == 64) {
+    // top-K rounds read the head windows from L2 (topk_entry)
+  } else if (a.gW > 0 && a.gW != a.W) {  // gathered [C][gW] windows: the first W of every client
     constexpr int kWords = sizeof(WinEntry) / 8;
     const int64_t per = static_cast<int64_t>(a.W) * kWords;
     const int64_t words = static_cast<int64_t>(C) * per;
@@ -2853,7 +2896,9 @@ __device__ __forceinline__ void select_body(const SelectArgs& a) {
 
   // ---- batches; short batches (maxima moving every pick) fall back to sequential picks ----
   unsigned long long nb = 0, ns = 0;
-  if constexpr (kMode == 0) {  // default: single-warp selection
+  if constexpr (kMode == 64) {
+    topk_select(a, M, cw, S, TK);
+  } else if constexpr (kMode == 0) {  // single-warp selection
     warp_select_phase(a, M, win, cw, S, T);
     ns = 1;
   } else if constexpr (kMode == 16 || kMode == 32) {  // 2 / 4 selection warps, one client per lane
@@ -2863,7 +2908,7 @@ __device__ __forceinline__ void select_body(const SelectArgs& a) {
     warp_select_reg<kMode>(a, M, win, cw, S, T);
     ns = 1;
   }
-  for (; !kWarp && !(S.flags & kDone);) {
+  for (; !kWarp && kMode != 64 && !(S.flags & kDone);) {
     if (a.D > 0) {
       int32_t acc = 0;
       const int32_t bf = batch_phase(a, win, cw, S, B, &acc);
@@ -2891,8 +2936,10 @@ __device__ __forceinline__ void select_body(const SelectArgs& a) {
   }
   if (tid == 0) {
     a.st->t[3] = global_ns();
-    a.st->t[6] = nb;
-    a.st->t[7] = ns;
+    if (kMode != 64) {  // topk_select stamps its own round count / phase cycles
+      a.st->t[6] = nb;
+      a.st->t[7] = ns;
+    }
   }
   pdl_trigger();  // the event fill may get scheduled while the ledger is written back
   // ---- write back ledger, heads, batch, summary ----
@@ -2922,6 +2969,7 @@ __device__ __forceinline__ void select_body(const SelectArgs& a) {
 __global__ void __launch_bounds__(kSelectMaxThreads, 1) select_kernel(const SelectArgs a) { select_body<-1>(a); }
 template <int kMode>
 __global__ void __launch_bounds__(kSelectMaxThreads, 1) select_warp_kernel(const SelectArgs a) { select_body<kMode>(a); }
+__global__ void __launch_bounds__(kTopkThreads, 1) select_topk_kernel(const SelectArgs a) { select_body<64>(a); }
 template __global__ void select_warp_kernel<0>(SelectArgs);
 template __global__ void select_warp_kernel<1>(SelectArgs);
 template __global__ void select_warp_kernel<2>(SelectArgs);

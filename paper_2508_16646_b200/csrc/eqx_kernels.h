@@ -18,6 +18,7 @@ constexpr int kScoreTile = 1024;                             // requests per bul
 constexpr int kScoreStages = 3;                              // tiles in flight per CTA
 constexpr int kScoreStageBytes = kScoreTile * (4 + 8 + 4 + 1 + 4);  // columns (+ true_out)
 constexpr int kSelectMaxThreads = 256;
+constexpr int kTopkThreads = 512;                           // select_topk_kernel block
 
 // Prediction records frozen when a request joined a live queue (drain_arrivals stores
 // map_metrics' PredictionRecord with the request, engine.cpp:178-180): later update_map EMA
@@ -173,6 +174,12 @@ struct SelectArgs {
   int32_t Ds;            // key-stream lookahead per client for the register loop
   int32_t cw_in_smem;
   void* cw_global;       // per-client work arrays when they do not fit in smem
+  // top-K rounds (select_topk_kernel, eqx_topk.cuh)
+  int32_t tk_dsh;        // log2 of the largest key-stream depth per client
+  int32_t tk_kcap;       // largest K of one round (<= threads)
+  int32_t tk_cap;        // stream items per round
+  void* tk_heads;        // [C] head tuples in global scratch (rosters beyond tk_kcap clients whose
+                         // tuples do not fit in shared memory; nullptr: shared memory)
   // ledger
   double* ufc;
   double* rfc;
@@ -417,6 +424,7 @@ __global__ void score_kernel(ScoreArgs a);
 __global__ void score_tma_kernel(ScoreArgs a);
 __global__ void window_kernel(WindowArgs a);
 __global__ void select_kernel(SelectArgs a);
+__global__ void select_topk_kernel(SelectArgs a);  // rounds of block-radix top-K (eqx_topk.cuh)
 template <int kMode>
 __global__ void select_warp_kernel(SelectArgs a);  // kMode 0: smem slots; 1/2/4: register slots;
                                                    // 16: two selection warps, one client per lane

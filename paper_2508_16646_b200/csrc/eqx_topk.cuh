@@ -1,0 +1,797 @@
+// eqx_topk.cuh -- the admission loop of admit_requests (engine.cpp:207-271) as rounds of a
+// block-radix top-K selection over per-client key streams (included by eqx_kernels.cu).
+//
+// Why a round is exact.  select_next (scheduler.cpp:131-156) takes the argmin of
+// (selection_key, head arrival, client_id) over the non-empty, non-skipped queues.  Under fixed
+// maxima (scheduler.cpp:40-48) a client's key only depends on its own ledger, and on_admit only
+// adds non-negative increments (scheduler.cpp:158-183), so along one client's FIFO the tuples
+// (key, arrival) never decrease: the greedy argmin sequence is the merge of the per-client
+// streams, i.e. their sorted order.  A round therefore
+//   0. (rosters larger than the block) radix-selects the K clients with the smallest heads: the
+//      K smallest tuples of all streams come from them;
+//   1. generates those clients' next D tuples under the current maxima: the head entries are
+//      gathered in parallel, the ledger chain of on_admit runs in the reference's FP64 order by
+//      one thread per client, the keys of all items in parallel;
+//   2. selects the K smallest tuples with an MSB-first radix select over the composite
+//      (key, arrival, client_id rank, stream index) -- the stream index keeps equal tuples of one
+//      client in FIFO order;
+//   3. ranks them (pairwise counting) into admission order;
+//   4. applies the exact loop body (reject / break / backfill skip / admit) to the ranked items:
+//      slot and KV budgets are prefix sums, so the walk is a block scan up to the first item that
+//      does not fit or that ends the round (an admission raising a maximum, a max holder leaving
+//      the backlog, a client whose generated stream ran out); backfill skips continue one item at
+//      a time.  The next round regenerates from there.
+// Every round makes at least one pick (its first item is the true argmin of the current heads),
+// so the result is the reference's sequence, for every policy and norm mode.  A stream also ends
+// early at a negative increment or an arrival going backwards (inputs outside the engine's
+// invariants), which keeps the merge argument valid.
+
+struct TopkScratch {
+  // items: slot-major runs, stream item d of slot s at x = off[s] + d (capacity `cap`)
+  uint64_t* k;    // ordered key bits
+  uint64_t* a;    // ordered head-arrival bits
+  double* u;      // gathered: ufc increment -> ufc before the item
+  double* r;      // gathered: rfc increment -> rfc before the item
+  double* cn;     // gathered: VTC charge -> counter before the item
+  uint8_t* fl;    // kTkValid | kFlAlone | kFlMaxChg | kFlHolder | kFlExh
+  uint8_t* st;    // radix state: 0 out, 1 in play, 2 selected, 3 consumed
+  uint32_t* sd;   // slot << 8 | d
+  int32_t cap;
+  // slots (clients whose streams a round generates)
+  int32_t* sc;    // [max(C, Kcap)] client of slot s
+  int32_t* snd;   // items generated for slot s
+  int32_t* spos;  // FIFO position of slot s's head
+  int32_t* sk0;   // its head-window index (pos - pos0)
+  int32_t* off;   // first item of slot s
+  int32_t* cut;   // stream length after the order / sign checks
+  // ranked list
+  uint64_t* gk;   // [Kcap] composites of the selected items
+  uint64_t* ga;
+  uint64_t* go;
+  int32_t* gx;    // [Kcap] selected item
+  int32_t* rank;  // [Kcap]
+  int32_t* srt;   // [Kcap] items in admission order
+  WinEntry* ent;  // [Kcap] their head entries
+  // heads (rosters beyond Kcap): one tuple per client
+  uint64_t* hk;   // [C]
+  uint64_t* ha;   // [C]
+  uint8_t* hst;   // [C]
+  uint32_t* hist; // [256]
+  uint64_t* stage;  // [warps][160] coalesced head-window words in flight
+  int32_t Kcap, dsh_max;
+};
+
+enum : uint32_t { kTkValid = 16 };
+
+struct TopkShared {
+  unsigned long long orv[3], andv[3];
+  int32_t nvalid, nsel, nslot, bin, below, inbin, stop, fn, fs;
+  int32_t wm[32];
+  long long wr[32], wp[32];
+};
+
+// Head entry j of client c: the head windows of window_kernel (L2), or scored on demand beyond
+// them (deep_entry; a client-sharded step reads the gathered windows and flags underflow).
+__device__ __forceinline__ WinEntry topk_entry(const SelectArgs& a, const ModelTables& M, const ClientWork& cw,
+                                               int32_t c, int32_t j) {
+  const int32_t k = j - cw.pos0[c];
+  const int32_t depth = a.gW > 0 ? a.gW : a.W;
+  if (k < depth) {
+    // 40-byte entries are 8-byte aligned: five 64-bit L2 loads
+    const unsigned long long* p =
+        reinterpret_cast<const unsigned long long*>(a.win_g + static_cast<int64_t>(c) * depth + k);
+    const uint64_t v0 = __ldcg(p), v1 = __ldcg(p + 1), v2 = __ldcg(p + 2), v3 = __ldcg(p + 3), v4 = __ldcg(p + 4);
+    WinEntry e;
+    e.ufc_inc = __longlong_as_double(static_cast<long long>(v0));
+    e.rfc_inc = __longlong_as_double(static_cast<long long>(v1));
+    e.abits = v2;
+    e.in = static_cast<int32_t>(v3);
+    e.pred = static_cast<int32_t>(v3 >> 32);
+    e.row = static_cast<int32_t>(v4);
+    e.alone = static_cast<int32_t>(v4 >> 32);
+    return e;
+  }
+  return deep_entry(a, M, c, j, k, cw.w[c]);
+}
+
+// Radix-select views: the composite of entry x is (field 0, field 1, field 2).
+struct ItemView {
+  const TopkScratch& T;
+  const ClientWork& cw;
+  int64_t n;
+  __device__ __forceinline__ uint8_t* st() const { return T.st; }
+  __device__ __forceinline__ uint64_t field(int64_t x, int f) const {
+    if (f == 0) return T.k[x];
+    if (f == 1) return T.a[x];
+    const uint32_t sd = T.sd[x];
+    return (static_cast<uint64_t>(cw.order[T.sc[sd >> 8]]) << 32) | (sd & 255u);
+  }
+};
+struct HeadView {
+  const TopkScratch& T;
+  const ClientWork& cw;
+  int64_t n;
+  __device__ __forceinline__ uint8_t* st() const { return T.hst; }
+  __device__ __forceinline__ uint64_t field(int64_t x, int f) const {
+    if (f == 0) return T.hk[x];
+    if (f == 1) return T.ha[x];
+    return static_cast<uint64_t>(cw.order[x]) << 32;
+  }
+};
+
+__device__ __forceinline__ void topk_or_and_commit(uint64_t o, uint64_t an, TopkShared& X, int b) {
+  const uint32_t ohi = __reduce_or_sync(0xffffffffu, static_cast<uint32_t>(o >> 32));
+  const uint32_t olo = __reduce_or_sync(0xffffffffu, static_cast<uint32_t>(o));
+  const uint32_t ahi = __reduce_and_sync(0xffffffffu, static_cast<uint32_t>(an >> 32));
+  const uint32_t alo = __reduce_and_sync(0xffffffffu, static_cast<uint32_t>(an));
+  if ((threadIdx.x & 31) == 0) {
+    atomicOr(&X.orv[b], (static_cast<unsigned long long>(ohi) << 32) | olo);
+    atomicAnd(&X.andv[b], (static_cast<unsigned long long>(ahi) << 32) | alo);
+  }
+}
+
+// OR and AND of field f over the in-play entries (st == 1), optionally below bit `lo` only.
+template <class V>
+__device__ __forceinline__ uint64_t topk_diff(const V& v, int f, TopkShared& X) {
+  const int tid = threadIdx.x, NT = blockDim.x;
+  if (tid == 0) {
+    X.orv[2] = 0;
+    X.andv[2] = ~0ull;
+  }
+  __syncthreads();
+  uint64_t o = 0, an = ~0ull;
+  for (int64_t x = tid; x < v.n; x += NT) {
+    if (v.st()[x] != 1) continue;
+    const uint64_t w = v.field(x, f);
+    o |= w;
+    an &= w;
+  }
+  topk_or_and_commit(o, an, X, 2);
+  __syncthreads();
+  const uint64_t d = X.orv[2] ^ X.andv[2];
+  __syncthreads();  // X.orv[2] / X.andv[2] are reset by the next call
+  return d;
+}
+
+// MSB-first radix select of the `need` smallest composites among the in-play entries (st == 1):
+// they end with st == 2, the others with st == 0.  Composites are unique (client rank, stream
+// index), so exactly `need` are selected.  Each pass histograms the next (up to) 8 bits below
+// the leading bits every in-play entry shares: the pass that keeps a bin also reduces the OR /
+// AND of that bin's remaining bits, so runs of common bits (and whole common fields, e.g. the
+// zero keys of a cold ledger) cost no pass.
+template <class V>
+__device__ void topk_radix_select(const V& v, int32_t need, uint32_t* hist, TopkShared& X) {
+  const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31;
+  uint8_t* st = v.st();
+  const int64_t n = v.n;
+  int f = 0;
+  uint64_t diff = topk_diff(v, 0, X);
+  int hi = diff ? 63 - __clzll(static_cast<long long>(diff)) : -1;
+  int par = 0;
+#pragma unroll 1
+  for (;;) {
+    while (hi < 0) {  // every in-play entry agrees on the rest of this field
+      if (++f == 3) return;
+      diff = topk_diff(v, f, X);
+      hi = diff ? 63 - __clzll(static_cast<long long>(diff)) : -1;
+    }
+    const int lo = hi >= 7 ? hi - 7 : 0;
+    const uint32_t mask = (1u << (hi - lo + 1)) - 1u;
+    for (int i = tid; i < 256; i += NT) hist[i] = 0;
+    if (tid == 0) {
+      X.orv[par] = 0;
+      X.andv[par] = ~0ull;
+    }
+    __syncthreads();
+    // warp-uniform trip count so the peer-mask ballots see all 32 lanes
+    for (int64_t base = tid - lane; base < n; base += NT) {
+      const int64_t x = base + lane;
+      uint32_t dg = 256;
+      if (x < n && st[x] == 1) dg = static_cast<uint32_t>(v.field(x, f) >> lo) & mask;
+      if (!__ballot_sync(0xffffffffu, dg != 256)) continue;
+      const unsigned m = peer_mask(dg, 9);
+      if (dg != 256 && lane == __ffs(m) - 1) atomicAdd(&hist[dg], static_cast<uint32_t>(__popc(m)));
+    }
+    __syncthreads();
+    if (tid < 32) {  // the bin where the running count reaches need
+      uint32_t h[8], sum = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        h[i] = hist[lane * 8 + i];
+        sum += h[i];
+      }
+      uint32_t incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const uint32_t excl = incl - sum;
+      const unsigned hit =
+          __ballot_sync(0xffffffffu, excl < static_cast<uint32_t>(need) && static_cast<uint32_t>(need) <= incl);
+      if (lane == __ffs(hit) - 1) {
+        uint32_t cum = excl;
+        int b = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (cum + h[i] >= static_cast<uint32_t>(need)) {
+            b = i;
+            break;
+          }
+          cum += h[i];
+        }
+        X.bin = lane * 8 + b;
+        X.below = static_cast<int32_t>(cum);
+        X.inbin = static_cast<int32_t>(h[b]);
+      }
+    }
+    __syncthreads();
+    const uint32_t bin = static_cast<uint32_t>(X.bin);
+    need -= X.below;
+    const bool all_in = X.inbin == need;
+    const uint64_t low = lo > 0 ? (1ull << lo) - 1 : 0;
+    uint64_t o = 0, an = ~0ull;
+    for (int64_t x = tid; x < n; x += NT) {
+      if (st[x] != 1) continue;
+      const uint64_t w = v.field(x, f);
+      const uint32_t dg = static_cast<uint32_t>(w >> lo) & mask;
+      if (dg < bin || (dg == bin && all_in)) {
+        st[x] = 2;
+      } else if (dg > bin) {
+        st[x] = 0;
+      } else {
+        o |= w & low;
+        an &= w | ~low;
+      }
+    }
+    if (all_in) {
+      __syncthreads();
+      return;
+    }
+    topk_or_and_commit(o, an, X, par);
+    __syncthreads();
+    diff = (X.orv[par] ^ X.andv[par]) & low;
+    hi = diff ? 63 - __clzll(static_cast<long long>(diff)) : -1;
+    par ^= 1;
+  }
+}
+
+// Block-wide exclusive scan of (count, tokens, prefill) over list positions (one per thread).
+__device__ __forceinline__ void topk_scan(int32_t m, long long rv, long long pv, int32_t& mx, long long& rx,
+                                          long long& px, TopkShared& X) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int32_t mi = m;
+  long long ri = rv, pi = pv;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t a = __shfl_up_sync(0xffffffffu, mi, o);
+    const long long b = __shfl_up_sync(0xffffffffu, ri, o), c = __shfl_up_sync(0xffffffffu, pi, o);
+    if (lane >= o) {
+      mi += a;
+      ri += b;
+      pi += c;
+    }
+  }
+  if (lane == 31) {
+    X.wm[warp] = mi;
+    X.wr[warp] = ri;
+    X.wp[warp] = pi;
+  }
+  __syncthreads();
+  int32_t mb = 0;
+  long long rb = 0, pb = 0;
+  for (int w = 0; w < warp; ++w) {
+    mb += X.wm[w];
+    rb += X.wr[w];
+    pb += X.wp[w];
+  }
+  mx = mb + mi - m;
+  rx = rb + ri - rv;
+  px = pb + pi - pv;
+}
+
+// The rounds (see the file comment).  Runs on the whole CTA after select_body's prologue.
+__device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTables& M, const ClientWork& cw, SelShared& S,
+                            const TopkScratch& T) {
+  __shared__ TopkShared X;
+  const int tid = threadIdx.x, NT = blockDim.x;
+  const int32_t C = a.C;
+  const Policy P = a.pol;
+  const bool maxmode = P.kind == kEquinox && P.norm_mode == 0;
+  const int64_t tmax = a.tmax;
+  const bool big = C > T.Kcap;  // rosters beyond one slot per thread: pre-select the K best heads
+  if (!big)
+    for (int32_t s = tid; s < C; s += NT) T.sc[s] = s;
+  // K of a round: the free slots (+ a margin for rejections), grown while lists run out
+  const int32_t want = P.backfill ? T.Kcap : max(32, min(T.Kcap, P.max_batch - S.members + 8));
+  int32_t K = min(want, 128);
+#ifdef EQX_PROF
+  unsigned long long rounds = 0, cy[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long t0 = clock64(), t1;
+#define TK_STAMP(i) \
+  t1 = clock64();   \
+  cy[i] += t1 - t0; \
+  t0 = t1;
+#else
+#define TK_STAMP(i)
+#endif
+  __syncthreads();
+  for (;;) {
+    const double mu = S.max_u, mr = S.max_r;
+    if (tid == 0) {
+      X.nvalid = 0;
+      X.nsel = 0;
+      X.nslot = 0;
+      X.stop = 0;
+      X.fn = 0x7fffffff;
+      X.fs = 0x7fffffff;
+    }
+    __syncthreads();
+    // ---- 0. slots: every client, or the K clients with the smallest heads ----
+    int32_t nslot = C;
+    if (big) {
+      int32_t nc = 0;
+      for (int32_t c = tid; c < C; c += NT) {
+        const bool cand = cw.pos[c] < cw.end[c] && !(cw.flags[c] & kSkipped);
+        if (cand) {
+          T.ha[c] = topk_entry(a, M, cw, c, cw.pos[c]).abits;
+          T.hk[c] = ordered_bits(hf_key(P, cw.ufc[c], cw.rfc[c], mu, mr, cw.cnt[c]));
+        }
+        T.hst[c] = cand ? 1 : 0;
+        nc += cand;
+      }
+      nc = __reduce_add_sync(0xffffffffu, nc);
+      if ((tid & 31) == 0 && nc) atomicAdd(&X.nvalid, nc);
+      __syncthreads();
+      const int32_t ncand = X.nvalid;
+      if (ncand == 0) break;  // no candidates (engine.cpp:217)
+      if (ncand > K) topk_radix_select(HeadView{T, cw, C}, K, T.hist, X);
+      for (int32_t c = tid; c < C; c += NT)
+        if (T.hst[c] == (ncand > K ? 2 : 1)) T.sc[atomicAdd(&X.nslot, 1)] = c;
+      __syncthreads();
+      nslot = X.nslot;
+      if (tid == 0) X.nvalid = 0;
+    }
+    TK_STAMP(0)
+    // ---- 1. key streams ----
+    // 1a. per slot: FIFO position, window index, head tuple, longest useful stream
+    for (int32_t s = tid; s < nslot; s += NT) {
+      const int32_t c = T.sc[s], pos = cw.pos[c], end = cw.end[c], k0 = pos - cw.pos0[c];
+      int32_t lim = 0;
+      uint64_t hkv = ~0ull, hav = ~0ull, hov = ~0ull;
+      if (pos < end && !(cw.flags[c] & kSkipped)) {
+        lim = min(64, end - pos);
+        if (a.gW > 0) lim = min(lim, max(a.gW - k0, 1));  // stay inside the gathered windows
+        hkv = big ? T.hk[c] : ordered_bits(hf_key(P, cw.ufc[c], cw.rfc[c], mu, mr, cw.cnt[c]));
+        hav = big ? T.ha[c] : topk_entry(a, M, cw, c, pos).abits;
+        hov = static_cast<uint64_t>(cw.order[c]) << 32;
+      }
+      T.spos[s] = pos;
+      T.sk0[s] = k0;
+      T.snd[s] = lim;
+      T.gk[s] = hkv;
+      T.ga[s] = hav;
+      T.go[s] = hov;
+      T.rank[s] = 0;
+    }
+    __syncthreads();
+    // 1b. depth budget: the client with the r-th smallest head gets about K / (r + 1) items
+    //     (a client's items sit below the K-th smallest tuple only while its key climbs past
+    //     the others'), large slot sets one to a few each
+    const bool harmonic = nslot <= 128;
+    if (harmonic) {
+      const int parts = max(1, NT / nslot);
+      if (tid < nslot * parts) {
+        const int32_t i = tid % nslot, part = tid / nslot;
+        const uint64_t k = T.gk[i], av = T.ga[i], o = T.go[i];
+        int32_t rk = 0;
+        for (int32_t j = part; j < nslot; j += parts) {
+          const uint64_t kj = T.gk[j], aj = T.ga[j], oj = T.go[j];
+          rk += (kj < k) | ((kj == k) & ((aj < av) | ((aj == av) & (oj < o))));
+        }
+        if (rk) atomicAdd(&T.rank[i], rk);
+      }
+      __syncthreads();
+    }
+    int64_t n;
+    {
+      const int32_t room = T.cap - nslot;  // one item per slot, the rest shared out
+      int32_t extra = 0;
+      if (tid < nslot && T.snd[tid] > 0) {
+        const int32_t w = harmonic ? (K + T.rank[tid]) / (T.rank[tid] + 1) : max(1, room / max(nslot, 1));
+        extra = min(w, T.snd[tid]) - 1;
+      }
+      int32_t ex;
+      long long e1, e2;
+      topk_scan(extra, 0, 0, ex, e1, e2, X);
+      if (tid < nslot) {
+        const int32_t take = max(0, min(extra, room - ex));
+        const int32_t o = tid + min(ex, room);
+        T.off[tid] = o;
+        const int32_t len = T.snd[tid] > 0 ? 1 + take : 0;
+        T.snd[tid] = len;
+        T.cut[tid] = len;
+        for (int32_t d = 0; d < max(len, 1); ++d) T.sd[o + d] = (static_cast<uint32_t>(tid) << 8) | d;
+        if (tid == nslot - 1) X.nvalid = o + max(len, 1);  // items this round
+      }
+      __syncthreads();
+      n = X.nvalid;
+      __syncthreads();
+      if (tid == 0) X.nvalid = 0;
+    }
+    {  // 1c. head entries: a warp moves 32 consecutive items (mostly one client's contiguous
+       //     window run) as 160 coalesced 64-bit words through shared memory
+      const int32_t depth = a.gW > 0 ? a.gW : a.W;
+      const int lane = tid & 31;
+      uint64_t* stg = T.stage + (tid >> 5) * 160;
+      for (int64_t base = tid - lane; base < n; base += NT) {
+        const int64_t li = base + lane;
+        const uint32_t sdv = li < n ? T.sd[li] : 0u;
+        const int32_t s = static_cast<int32_t>(sdv >> 8), d = static_cast<int32_t>(sdv & 255u);
+        const bool valid = li < n && d < T.snd[s];
+        int32_t c = 0, k = 0;
+        unsigned long long p = 0;
+        if (valid) {
+          c = T.sc[s];
+          k = T.sk0[s] + d;
+          if (k < depth) p = reinterpret_cast<unsigned long long>(a.win_g + static_cast<int64_t>(c) * depth + k);
+        }
+#pragma unroll
+        for (int j = 0; j < 5; ++j) {
+          const int w = j * 32 + lane, e = w / 5;
+          const unsigned long long pe = __shfl_sync(0xffffffffu, p, e);
+          if (pe) stg[w] = __ldcg(reinterpret_cast<const unsigned long long*>(pe) + (w - 5 * e));
+        }
+        __syncwarp();
+        if (li < n) {
+          uint8_t f = 0;
+          if (valid) {
+            WinEntry e;
+            if (p) {
+              e.ufc_inc = __longlong_as_double(static_cast<long long>(stg[5 * lane]));
+              e.rfc_inc = __longlong_as_double(static_cast<long long>(stg[5 * lane + 1]));
+              e.abits = stg[5 * lane + 2];
+              const uint64_t ip = stg[5 * lane + 3];
+              e.in = static_cast<int32_t>(ip);
+              e.pred = static_cast<int32_t>(ip >> 32);
+              e.alone = static_cast<int32_t>(stg[5 * lane + 4] >> 32);
+            } else {
+              e = deep_entry(a, M, c, T.spos[s] + d, k, cw.w[c]);  // beyond the head window
+            }
+            T.a[li] = e.abits;
+            T.u[li] = e.ufc_inc;
+            T.r[li] = e.rfc_inc;
+            T.cn[li] = vtc_inc(P, e, cw.w[c]);
+            f = kTkValid | (e.alone ? kFlAlone : 0);
+          }
+          T.fl[li] = f;
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    // 1d. stream ends: an arrival going backwards (the stream stops before it) or a negative
+    //     increment (the stream stops after it)
+    for (int64_t x = tid; x < n; x += NT) {
+      const uint8_t f = T.fl[x];
+      if (!(f & kTkValid)) continue;
+      const uint32_t sdv = T.sd[x];
+      const int32_t s = static_cast<int32_t>(sdv >> 8), d = static_cast<int32_t>(sdv & 255u);
+      if (d > 0 && T.a[x] < T.a[x - 1]) atomicMin(&T.cut[s], d);
+      if ((f & kFlAlone) && d + 1 < T.snd[s] &&
+          (!(T.u[x] >= 0.0) || !(T.r[x] >= 0.0) || (P.kind == kVtc && !(T.cn[x] >= 0.0))))
+        atomicMin(&T.cut[s], d + 1);
+    }
+    __syncthreads();
+    TK_STAMP(1)
+    // 1e. ledger chains (on_admit's adds in FIFO order): a warp per slot, 32 items at a time in
+    //     the lanes; the increments are broadcast by shuffles, so only the adds are serial
+    {
+      const int lane = tid & 31, nw = NT >> 5;
+      for (int32_t s = tid >> 5; s < nslot; s += nw) {
+        const int32_t c = T.sc[s], pos = T.spos[s], end = cw.end[c], x0 = T.off[s];
+        const int32_t nd = T.cut[s];
+        double u = cw.ufc[c], r = cw.rfc[c], cn = cw.cnt[c];
+        for (int32_t base = 0; base < nd; base += 32) {
+          const int32_t d = base + lane, x = x0 + d;
+          const bool in = d < nd;
+          uint8_t f = in ? T.fl[x] : 0;
+          const double iu = in ? T.u[x] : 0.0, ir = in ? T.r[x] : 0.0, ic = in ? T.cn[x] : 0.0;
+          double ub = 0.0, rb = 0.0, cb = 0.0;
+          const int32_t m = min(32, nd - base);
+          if (P.kind == kVtc) {
+#pragma unroll 4
+            for (int32_t j = 0; j < m; ++j) {
+              if (lane == j) {
+                ub = u;
+                rb = r;
+                cb = cn;
+              }
+              const bool al = __shfl_sync(0xffffffffu, f, j) & kFlAlone;
+              const double iuj = __shfl_sync(0xffffffffu, iu, j), irj = __shfl_sync(0xffffffffu, ir, j),
+                           icj = __shfl_sync(0xffffffffu, ic, j);
+              const double nu = __dadd_rn(u, iuj), nr = __dadd_rn(r, irj), nc = __dadd_rn(cn, icj);
+              u = al ? nu : u;
+              r = al ? nr : r;
+              cn = al ? nc : cn;
+            }
+          } else {
+#pragma unroll 4
+            for (int32_t j = 0; j < m; ++j) {
+              if (lane == j) {
+                ub = u;
+                rb = r;
+              }
+              const bool al = __shfl_sync(0xffffffffu, f, j) & kFlAlone;
+              const double iuj = __shfl_sync(0xffffffffu, iu, j), irj = __shfl_sync(0xffffffffu, ir, j);
+              const double nu = __dadd_rn(u, iuj), nr = __dadd_rn(r, irj);
+              u = al ? nu : u;
+              r = al ? nr : r;
+            }
+            cb = cn;
+          }
+          if (in) {
+            T.u[x] = ub;
+            T.r[x] = rb;
+            T.cn[x] = cb;
+            if (pos + d + 1 == end) {
+              if (maxmode && (ub == mu || rb == mr)) f |= kFlHolder;  // a max holder leaves the backlog
+            } else if ((f & kFlAlone) && maxmode && (mu < __dadd_rn(ub, iu) || mr < __dadd_rn(rb, ir))) {
+              f |= kFlMaxChg;  // this admission raises a maximum
+            }
+            if (d + 1 == nd && pos + nd < end) f |= kFlExh;  // later items were not generated
+            T.fl[x] = f;
+          }
+        }
+        for (int32_t d = nd + lane; d < T.snd[s]; d += 32) T.fl[x0 + d] = 0;
+        __syncwarp();
+        if (lane == 0) T.snd[s] = nd;
+      }
+    }
+    __syncthreads();
+    TK_STAMP(2)
+    {
+      int32_t nv = 0;
+      for (int64_t x = tid; x < n; x += NT) {
+        const bool v = T.fl[x] & kTkValid;
+        if (v) T.k[x] = ordered_bits(hf_key(P, T.u[x], T.r[x], mu, mr, T.cn[x]));
+        T.st[x] = v ? 1 : 0;
+        nv += v;
+      }
+      nv = __reduce_add_sync(0xffffffffu, nv);
+      if ((tid & 31) == 0 && nv) atomicAdd(&X.nvalid, nv);
+    }
+    __syncthreads();
+    const int32_t nvalid = X.nvalid;
+    TK_STAMP(3)
+    if (nvalid == 0) break;  // no candidates (engine.cpp:217)
+    // ---- 2. the K smallest tuples ----
+    const int32_t ks = min(nvalid, K);
+    const ItemView iv{T, cw, n};
+    if (ks < nvalid) {
+      topk_radix_select(iv, ks, T.hist, X);
+    } else {
+      for (int64_t x = tid; x < n; x += NT)
+        if (T.st[x] == 1) T.st[x] = 2;
+      __syncthreads();
+    }
+    TK_STAMP(4)
+    // ---- 3. admission order: gather, rank by pairwise counting ----
+    for (int64_t x = tid; x < n; x += NT) {
+      if (T.st[x] != 2) continue;
+      const int32_t i = atomicAdd(&X.nsel, 1);
+      T.gx[i] = static_cast<int32_t>(x);
+      T.gk[i] = T.k[x];
+      T.ga[i] = T.a[x];
+      T.go[i] = iv.field(x, 2);
+      T.rank[i] = 0;
+    }
+    __syncthreads();
+    const int32_t ns = X.nsel;
+    {
+      const int parts = max(1, NT / ns);
+      if (tid < ns * parts) {
+        const int32_t i = tid % ns, part = tid / ns;
+        const uint64_t k = T.gk[i], av = T.ga[i], o = T.go[i];
+        int32_t rk = 0;
+        for (int32_t j = part; j < ns; j += parts) {
+          const uint64_t kj = T.gk[j], aj = T.ga[j], oj = T.go[j];
+          rk += (kj < k) | ((kj == k) & ((aj < av) | ((aj == av) & (oj < o))));
+        }
+        if (rk) atomicAdd(&T.rank[i], rk);
+      }
+      __syncthreads();
+      for (int32_t i = tid; i < ns; i += NT) {
+        const int32_t x = T.gx[i], rk = T.rank[i];
+        T.srt[rk] = x;
+        const uint32_t sdv = T.sd[x];
+        const int32_t c = T.sc[sdv >> 8];
+        T.ent[rk] = topk_entry(a, M, cw, c, cw.pos[c] + static_cast<int32_t>(sdv & 255u));
+      }
+      __syncthreads();
+    }
+    TK_STAMP(5)
+    // ---- 4. the loop body over the ranked items (engine.cpp:216-268) ----
+    // 4a. block scan: slot / KV budgets as prefix sums, up to the first item that does not fit
+    //     or ends the round
+    const int32_t members0 = S.members;
+    const int64_t reserved0 = S.reserved;
+    {
+      int32_t m = 0;
+      long long rv = 0, pv = 0;
+      bool alone = false, flag = false;
+      if (tid < ns) {
+        const int32_t x = T.srt[tid];
+        const int32_t c = T.sc[T.sd[x] >> 8], d = static_cast<int32_t>(T.sd[x] & 255u);
+        const WinEntry& e = T.ent[tid];
+        const uint8_t f = T.fl[x];
+        const bool last = cw.pos[c] + d + 1 == cw.end[c];
+        alone = e.alone;
+        m = alone ? 1 : 0;
+        rv = alone ? static_cast<long long>(e.in) + e.pred : 0;
+        pv = alone ? e.in : 0;
+        flag = last ? (f & kFlHolder) : ((f & kFlExh) || (alone && (f & kFlMaxChg)));
+      }
+      int32_t mx;
+      long long rx, px;
+      topk_scan(m, rv, pv, mx, rx, px, X);
+      if (tid < ns) {
+        const bool nofit = alone && !((members0 + mx + 1 <= P.max_batch) && (reserved0 + rx + rv <= tmax));
+        if (nofit) atomicMin(&X.fn, tid);
+        if (flag) atomicMin(&X.fs, tid);
+      }
+      __syncthreads();
+      const int32_t fn = X.fn, fs = X.fs;
+      const int32_t cend = fn <= fs ? min(fn, ns) : fs + 1;  // items [0, cend) are consumed
+      // 4b. commit: events, admissions, per-client ledgers after the client's last consumed item
+      if (tid < cend) {
+        const int32_t x = T.srt[tid];
+        const int32_t c = T.sc[T.sd[x] >> 8];
+        const WinEntry& e = T.ent[tid];
+        const int64_t ev = S.n_ev + tid;
+        if (ev < a.ev_cap) {
+          a.ev_row[ev] = e.row;
+          a.ev_kind[ev] = alone ? 1 : 2;
+          a.ev_client[ev] = c;
+        }
+        if (alone) atomicAdd(&cw.adm[c], 1);
+        T.st[x] = 3;
+      }
+      __syncthreads();
+      if (tid == cend - 1) {  // round totals
+        S.members = members0 + mx + m;
+        S.reserved = reserved0 + rx + rv;
+        S.prefill += px + pv;
+        S.n_adm += mx + m;
+        S.n_rej += cend - (mx + m);
+        S.n_ev += cend;
+      }
+      if (tid < cend) {
+        const int32_t x = T.srt[tid];
+        const int32_t s = static_cast<int32_t>(T.sd[x] >> 8), c = T.sc[s], d = static_cast<int32_t>(T.sd[x] & 255u);
+        if (d + 1 >= T.snd[s] || T.st[x + 1] != 3) {  // the client's last consumed item
+          const WinEntry& e = T.ent[tid];
+          double nu = T.u[x], nr = T.r[x], ncn = T.cn[x];
+          if (alone) {
+            nu = __dadd_rn(nu, e.ufc_inc);
+            nr = __dadd_rn(nr, e.rfc_inc);
+            if (P.kind == kVtc) ncn = __dadd_rn(ncn, vtc_inc(P, e, cw.w[c]));
+          }
+          cw.ufc[c] = nu;
+          cw.rfc[c] = nr;
+          cw.cnt[c] = ncn;
+          const int32_t np = cw.pos[c] + d + 1;
+          if (np == cw.end[c]) cw.flags[c] &= ~kBacklogged;  // pop_head emptied the queue
+          cw.pos[c] = np;
+          if (tid == fs && fs < fn) {  // the item that ends the round
+            const uint8_t f = T.fl[x];
+            if (np == cw.end[c]) {
+              if (f & kFlHolder) X.stop = 4;  // maxima need a rescan
+            } else if (alone && (f & kFlMaxChg)) {
+              if (S.max_u < nu) S.max_u = nu;
+              if (S.max_r < nr) S.max_r = nr;
+            }
+          }
+        }
+      }
+      if (tid == 0 && fn < ns && fn <= fs) {
+        if (!P.backfill) X.stop = 2;  // engine.cpp:239: the head does not fit, the step is over
+        else X.stop = 8;              // backfill: skip its client, continue item by item
+      }
+      __syncthreads();
+    }
+    TK_STAMP(6)
+    // 4c. backfill after a head that did not fit: the exact loop body, one item at a time
+    if (X.stop == 8 && tid == 0) {
+      int32_t stop = 0;
+      int32_t members = S.members;
+      int64_t reserved = S.reserved, n_ev = S.n_ev, n_adm = S.n_adm, n_rej = S.n_rej, prefill = S.prefill;
+      double max_u = S.max_u, max_r = S.max_r;
+      for (int32_t i = X.fn; i < ns && !stop; ++i) {
+        const int32_t x = T.srt[i];
+        const int32_t c = T.sc[T.sd[x] >> 8];
+        const int32_t fc = cw.flags[c];
+        if (fc & kSkipped) continue;  // skipped earlier in the round
+        const WinEntry& e = T.ent[i];
+        const uint8_t fl = T.fl[x];
+        const int32_t j = cw.pos[c];
+        const bool last = j + 1 == cw.end[c];
+        if (!e.alone) {  // engine.cpp:223-234: Rejected, pop_head, no counter change
+          if (n_ev < a.ev_cap) {
+            a.ev_row[n_ev] = e.row;
+            a.ev_kind[n_ev] = 2;
+            a.ev_client[n_ev] = c;
+          }
+          ++n_ev;
+          ++n_rej;
+          cw.pos[c] = j + 1;
+          if (last) {
+            cw.flags[c] = fc & ~kBacklogged;
+            if (fl & kFlHolder) stop = 4;
+          } else if (fl & kFlExh) {
+            stop = 1;
+          }
+          continue;
+        }
+        if (!((members + 1 <= P.max_batch) && (reserved + e.in + e.pred <= tmax))) {
+          cw.flags[c] = fc | kSkipped;  // engine.cpp:236-238
+          continue;
+        }
+        members += 1;
+        reserved += static_cast<int64_t>(e.in) + e.pred;
+        prefill += e.in;
+        const double nu = __dadd_rn(cw.ufc[c], e.ufc_inc), nr = __dadd_rn(cw.rfc[c], e.rfc_inc);
+        cw.ufc[c] = nu;
+        cw.rfc[c] = nr;
+        if (P.kind == kVtc) cw.cnt[c] = __dadd_rn(cw.cnt[c], vtc_inc(P, e, cw.w[c]));
+        cw.adm[c] += 1;
+        if (n_ev < a.ev_cap) {
+          a.ev_row[n_ev] = e.row;
+          a.ev_kind[n_ev] = 1;
+          a.ev_client[n_ev] = c;
+        }
+        ++n_ev;
+        ++n_adm;
+        cw.pos[c] = j + 1;
+        if (last) {
+          cw.flags[c] = fc & ~kBacklogged;
+          if (fl & kFlHolder) stop = 4;
+        } else if (fl & kFlMaxChg) {
+          if (max_u < nu) max_u = nu;
+          if (max_r < nr) max_r = nr;
+          stop = 1;
+        } else if (fl & kFlExh) {
+          stop = 1;
+        }
+      }
+      S.members = members;
+      S.reserved = reserved;
+      S.n_ev = n_ev;
+      S.n_adm = n_adm;
+      S.n_rej = n_rej;
+      S.prefill = prefill;
+      S.max_u = max_u;
+      S.max_r = max_r;
+      X.stop = stop;
+    }
+    __syncthreads();
+    TK_STAMP(7)
+#ifdef EQX_PROF
+    ++rounds;
+#endif
+    const int32_t stop = X.stop, consumed = X.fn <= X.fs ? min(X.fn, ns) : X.fs + 1;
+    if (stop == 2) break;
+    if (stop & 4) cta_maxima(cw, C, S);  // max over the backlogged clients (scheduler.cpp:40-48)
+    // next K: double it when the list ran out, else about twice what this round consumed
+    K = (X.fn >= ns && X.fs >= ns) ? min(want, 2 * K) : min(want, max(32, 2 * consumed));
+    __syncthreads();
+  }
+#ifdef EQX_PROF
+  if (tid == 0) {
+    a.st->t[7] = rounds;
+    for (int i = 0; i < 8; ++i) a.st->t[8 + i] = cy[i];
+  }
+#endif
+#undef TK_STAMP
+  if (tid == 0) S.flags = kDone;
+}
