@@ -330,10 +330,13 @@ def preset_traces(n_replays: int, duration: float, seed0: int = 1):
     return traces, row_off, cat
 
 
+CFG5_DURATION = 60.0  # Trace::duration_s of the generated scenarios: the replay horizon (engine.cpp:120-121)
+
+
 def cfg5_setup(n_seeds: int):
     alphas = np.round(np.arange(0.5, 0.86, 0.05), 2)              # 8 values
     alpha = np.tile(alphas, n_seeds)                             # replay r: alpha[r % 8], seed r // 8
-    traces, row_off, cat = preset_traces(len(alpha), 60.0)
+    traces, row_off, cat = preset_traces(len(alpha), CFG5_DURATION)
     return alpha, traces, row_off, cat
 
 
@@ -346,7 +349,7 @@ def ref_replay_one(args_):
         prof = {k: np.asarray(v) for k, v in json.load(f).items()}
     case = H.StepCase(client=q["client"], arrival=q["arrival"], in_tokens=q["in_tokens"], true_out=q["true_out"],
                       tag=np.full(len(q["client"]), -1, np.int32), client_names=["client1", "client2"],
-                      alpha=float(a), pred_kind=0, profile=prof)
+                      alpha=float(a), pred_kind=0, profile=prof, duration_s=CFG5_DURATION)
     t0 = time.perf_counter()
     H.ref_replay(case, max_sim_time_s=0.0, ema_alpha=0.2, cap=1 << 20)
     return time.perf_counter() - t0
@@ -398,13 +401,13 @@ def run_cfg5(args, rank, world):
     prof = S.GpuProfile.load_json(os.path.join(data, "profile_default.json"))
     sch = S.GpuScheduler([S.ClientState("client1"), S.ClientState("client2")], policy=S.PolicySpec(),
                          perf=S.PerfParams(), profile=prof, predictor="oracle", device=local)
-    cap = 2048
+    cap = 1  # run_sweep_alpha reads the reports only: no event log comes back
     times, kms = [], []
     for i in range(args.warmup + args.steps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         out = sch.replay(row_off, cat["client"], cat["arrival"], cat["in_tokens"], cat["true_out"], alpha,
-                         ema_alpha=0.2, ev_cap=cap)
+                         ema_alpha=0.2, ev_cap=cap, duration_s=np.full(n, CFG5_DURATION))
         t1 = time.perf_counter()
         if i >= args.warmup:
             times.append(t1 - t0)

@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define EQX_ABI_VERSION 2
+#define EQX_ABI_VERSION 3
 
 typedef enum {
   EQX_OK = 0,
@@ -42,8 +42,9 @@ enum { EQX_FCFS = 0, EQX_VTC = 1, EQX_EQUINOX = 2 };
 enum { EQX_NORM_MAX_OVER_CLIENTS = 0, EQX_NORM_NONE = 1 };
 /* Predictor implementations (predictor.hpp:34-129) */
 enum { EQX_PRED_ORACLE = 0, EQX_PRED_MOPE = 1, EQX_PRED_NOISY_ORACLE = 2, EQX_PRED_SINGLE_PROXY = 3 };
-/* LogEvent::Admitted / LogEvent::Rejected (engine.hpp:33) */
-enum { EQX_EV_ADMITTED = 1, EQX_EV_REJECTED = 2 };
+/* LogEvent (engine.hpp:33): a step logs admissions and rejections; a replay with log_all set
+ * logs the engine's whole event log */
+enum { EQX_EV_ADMITTED = 1, EQX_EV_REJECTED = 2, EQX_EV_ARRIVED = 3, EQX_EV_FIRST_TOKEN = 4, EQX_EV_COMPLETED = 5 };
 /* where the pointers of an eqx_requests batch live */
 enum { EQX_HOST = 0, EQX_DEVICE = 1 };
 
@@ -207,7 +208,8 @@ eqx_status eqx_step(eqx_ctx* ctx, double now, eqx_step_summary* out);
  * run_simulation (engine.cpp:119-146) for many independent traces at once, one replay per
  * GPU warp, with the context's policy / perf / timing / profile / predictor / roster and a
  * per-replay EquinoxParams::alpha.  Each replay starts from zero ledgers (engine.cpp:148-157)
- * and its own copy of the profile; prediction_overhead_ms is 0 (EngineConfig default).  The
+ * and its own copy of the profile.  Rosters of any size (one warp per replay; rosters beyond 16
+ * clients keep the ledger in global scratch).  The
  * reporting side runs on the device too: the engine's window samples (advance_clock /
  * emit_window_samples, engine.cpp:379-430) and build_report (metrics.cpp:151-229) with the
  * policy's output_weight and report_window_s as its window. */
@@ -226,6 +228,18 @@ typedef struct {
   int64_t ev_cap;                    /* admitted / rejected events kept per replay */
   double report_window_s;            /* EngineConfig::report_window_s; <= 0: 1.0 (default) */
   int64_t win_cap;                   /* window samples kept per replay in the series outputs */
+  /* ABI 3 */
+  const double* duration_s;          /* [n_replays] Trace::duration_s, the horizon when
+                                        max_sim_time_s <= 0 (engine.cpp:120-121); NULL: each
+                                        trace's last arrival */
+  double prediction_overhead_ms;     /* EngineConfig::prediction_overhead_ms: a request is
+                                        eligible at arrival + overhead / 1000 (engine.cpp:165-168) */
+  const int32_t* predicted;          /* optional [rows]: Predictor::predict(req) of every row, made by
+                                        the caller's predictor (the engine applies max(1, .)); NULL:
+                                        the context's predictor on the device */
+  int32_t log_all;                   /* 1: ev_* is the engine's whole log (EventLog, engine.hpp:
+                                        36-57) -- arrived / admitted / first_token / completed /
+                                        rejected, with payloads in ev_i0 / ev_d0..2 */
 } eqx_replays;
 
 /* build_report's SimReport summary (metrics.hpp:63-81) + the SimResult totals of one replay. */
@@ -243,6 +257,9 @@ typedef struct {
   int64_t n_windows;                   /* engine window samples (gpu_series / counter_series) */
   int64_t n_diff;                      /* service-difference samples (diff_series) */
   int64_t n_rate;                      /* service-rate windows per client */
+  int64_t max_resident_kv_tokens;      /* SimResult::max_resident_kv_tokens (with status 2: the
+                                          resident tokens that exceeded the capacity) */
+  int64_t drained;                     /* requests that entered the queues (drain_arrivals) */
 } eqx_replay_report;
 
 /* ClientReport (metrics.hpp:55-60) + the final reporting HF of one client of one replay. */
@@ -273,6 +290,14 @@ typedef struct {                     /* host arrays; any may be NULL */
   double* diff;                      /* [n_replays][win_cap][2] time, max-min service */
   double* rate;                      /* [n_replays][C][win_cap] service rate of window w
                                         (time = window_s * (w + 1)) */
+  /* ABI 3: event payloads ([n_replays][ev_cap]; LogEntry fields, engine.hpp:39-51).
+   *   arrived / rejected: ev_i0 = input_tokens; ev_time = arrival_time_s for arrivals
+   *   admitted:  ev_i0 = predicted_output_tokens, ev_d0 = predicted_latency_ms
+   *   completed: ev_i0 = output_tokens, ev_d0 = latency_s, ev_d1 = tps, ev_d2 = gpu_util */
+  int32_t* ev_i0;
+  double *ev_d0, *ev_d1, *ev_d2;
+  double* profile;                   /* [n_replays][3][n_profile]: SimResult::profile after the
+                                        update_map feedback -- latency_ms, gpu_util, tps */
 } eqx_replay_out;
 
 /* PerfParams timing fields (gpu_model.hpp:14-28) used by replays. */

@@ -82,6 +82,8 @@ typedef struct {
   const char* tag_names;          /* n_tags NUL-terminated strings (ref driver) */
   const int32_t* tag_row;         /* [n_tags] keyword row for that tag, -1 = unseen */
   double now;
+  double duration_s;              /* replays: Trace::duration_s (<= 0: the last arrival) */
+  double prediction_overhead_ms;  /* replays: EngineConfig::prediction_overhead_ms */
 } eqxo_step_in;
 
 typedef struct {

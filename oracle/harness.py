@@ -55,7 +55,8 @@ class StepIn(C.Structure):
         ("mem_reserved", _i32p),
         ("n_req", C.c_int64), ("id", _i64p), ("client", _i32p), ("arrival", _dp),
         ("in_tokens", _i32p), ("true_out", _i32p), ("tag", _i32p), ("n_tags", C.c_int32),
-        ("tag_names", C.c_char_p), ("tag_row", _i32p), ("now", C.c_double),
+        ("tag_names", C.c_char_p), ("tag_row", _i32p), ("now", C.c_double), ("duration_s", C.c_double),
+        ("prediction_overhead_ms", C.c_double),
     ]
 
 
@@ -118,6 +119,8 @@ class StepCase:
     mem_per_token_bytes: float = 0.5 * 1024.0 * 1024.0
     mem_capacity_bytes: float = 60.0 * 1024.0 * 1024.0 * 1024.0
     now: float = 1.0
+    duration_s: float = 0.0              # replays: Trace::duration_s (0: the last arrival)
+    prediction_overhead_ms: float = 0.0  # replays: EngineConfig::prediction_overhead_ms
 
     def finalize(self):
         n = len(self.client)
@@ -221,6 +224,8 @@ def _build_in(case: StepCase, keep: list) -> StepIn:
     s.tag_names = tn
     s.tag_row = _ptr(arr(tag_row, np.int32), C.c_int32)
     s.now = case.now
+    s.duration_s = float(case.duration_s)
+    s.prediction_overhead_ms = float(case.prediction_overhead_ms)
     return s
 
 
@@ -509,6 +514,36 @@ REPORT_FIELDS = ("max_diff", "avg_diff", "var_diff", "jain_hf", "jain_ttft_p90",
                  "busy_ms_total", "overhead_ms_total", "completed", "rejected", "total_completed_tokens",
                  "n_windows", "n_diff", "n_rate")
 CLIENT_FIELDS = ("final_hf", "accumulated_service", "mean_service_rate", "ttft_p50", "ttft_p90", "ttft_count")
+
+
+def ref_replay_log(case: "StepCase", max_sim_time_s=0.0, ema_alpha=0.2, window_s=1.0) -> dict:
+    """run_simulation's whole SimResult (oracle/_ref): the event log with its payloads (kind as
+    EQX_EV_*, id, time, i0, d0..d2 -- include/eqx.h), the feedback-updated profile, the
+    final ledger / accumulated service, max_resident_kv_tokens and the run totals."""
+    lib, _ = _lib("ref")
+    keep: list = []
+    s = _build_in(case, keep)
+    n, nc, npf = int(s.n_req), int(s.n_clients), int(s.n_profile)
+    cap = 4 * n + 4
+    o = {"id": np.zeros(cap, np.int64), "kind": np.zeros(cap, np.int32), "time": np.zeros(cap),
+         "i0": np.zeros(cap, np.int32), "d0": np.zeros(cap), "d1": np.zeros(cap), "d2": np.zeros(cap),
+         "profile": np.zeros((3, npf)), "clients": np.zeros((nc, 4)), "totals": np.zeros(8)}
+    err = C.create_string_buffer(512)
+    f = lib.ref_replay_log
+    f.argtypes = [C.POINTER(StepIn), C.c_double, C.c_double, C.c_double, C.c_int64] + [C.c_void_p] * 10 + \
+        [C.c_char_p, C.c_int]
+    f.restype = C.c_int64
+    ne = f(C.byref(s), max_sim_time_s, ema_alpha, window_s, cap,
+           *[o[k].ctypes.data for k in ("id", "kind", "time", "i0", "d0", "d1", "d2", "profile", "clients", "totals")],
+           err, 512)
+    if ne < 0:
+        raise ValueError(err.value.decode())
+    for k in ("id", "kind", "time", "i0", "d0", "d1", "d2"):
+        o[k] = o[k][:ne]
+    t = o.pop("totals")
+    o.update(sim_end=t[0], busy_ms_total=t[1], overhead_ms_total=t[2], max_resident_kv_tokens=int(t[3]),
+             completed=int(t[4]), rejected=int(t[5]), counter_clamps=int(t[6]))
+    return o
 
 
 def ref_replay_full(case: "StepCase", max_sim_time_s=0.0, ema_alpha=0.2, window_s=1.0, win_cap=256) -> dict:

@@ -404,7 +404,7 @@ int64_t ref_replay(const eqxo_step_in* in, double max_sim_time_s, double ema_alp
       last = q.arrival_time_s;
       trace.requests.push_back(q);
     }
-    trace.duration_s = last;
+    trace.duration_s = in->duration_s > 0.0 ? in->duration_s : last;
     EngineConfig cfg;
     cfg.policy.kind = static_cast<PolicyKind>(in->kind);
     cfg.policy.equinox.alpha = in->alpha;
@@ -762,7 +762,7 @@ extern "C" int ref_replay_report(const eqxo_step_in* in, double max_sim_time_s, 
       last = q.arrival_time_s;
       trace.requests.push_back(q);
     }
-    trace.duration_s = last;
+    trace.duration_s = in->duration_s > 0.0 ? in->duration_s : last;
     EngineConfig cfg;
     cfg.policy.kind = static_cast<PolicyKind>(in->kind);
     cfg.policy.equinox.alpha = in->alpha;
@@ -833,7 +833,7 @@ extern "C" int ref_replay_full(const eqxo_step_in* in, double max_sim_time_s, do
       last = q.arrival_time_s;
       trace.requests.push_back(q);
     }
-    trace.duration_s = last;
+    trace.duration_s = in->duration_s > 0.0 ? in->duration_s : last;
     EngineConfig cfg;
     cfg.policy.kind = static_cast<PolicyKind>(in->kind);
     cfg.policy.equinox.alpha = in->alpha;
@@ -982,5 +982,116 @@ extern "C" int ref_scenario_csv(const char* preset, uint64_t seed, double durati
   } catch (const std::exception& e) {
     set_err(err, err_len, e.what());
     return 1;
+  }
+}
+
+// The whole SimResult of run_simulation (engine.cpp:119-146) with its event log: per entry the
+// kind as EQX_EV_* (admitted 1, rejected 2, arrived 3, first_token 4, completed 5), request
+// id, time and the payload fields as include/eqx.h lays them out (i0: input / predicted /
+// output tokens; d0..d2: predicted_latency_ms, or latency_s / tps / gpu_util), the profile
+// after update_map (prof[3][P]: latency_ms, gpu_util, tps), final clients (cl[C][4]: ufc,
+// rfc, counter, accumulated_service) and totals (sim_end, busy, overhead, max resident KV
+// tokens, completed, rejected, clamps).  Returns the number of log entries or -1.
+extern "C" int64_t ref_replay_log(const eqxo_step_in* in, double max_sim_time_s, double ema_alpha, double window_s,
+                                  int64_t cap, int64_t* id, int32_t* kind, double* t, int32_t* i0, double* d0,
+                                  double* d1, double* d2, double* prof, double* cl, double* tot, char* err,
+                                  int err_len) {
+  try {
+    const auto names = split_names(in->client_names, in->n_clients);
+    const auto tags = split_names(in->tag_names, in->n_tags);
+    Trace trace;
+    for (int c = 0; c < in->n_clients; ++c) {
+      ClientSpec cs;
+      cs.client_id = names[c];
+      cs.weight = in->weight[c];
+      cs.arrivals.kind = ArrivalKind::Replay;
+      trace.clients.push_back(cs);
+    }
+    double last = 0.0;
+    for (int64_t r = 0; r < in->n_req; ++r) {
+      Request q;
+      q.id = in->id[r];
+      q.client_id = names[static_cast<std::size_t>(in->client[r])];
+      q.arrival_time_s = in->arrival[r];
+      q.input_tokens = in->in_tokens[r];
+      q.true_output_tokens = in->true_out[r];
+      if (in->tag[r] >= 0) q.category_tag = tags[static_cast<std::size_t>(in->tag[r])];
+      last = q.arrival_time_s;
+      trace.requests.push_back(q);
+    }
+    trace.duration_s = in->duration_s > 0.0 ? in->duration_s : last;
+    EngineConfig cfg;
+    cfg.policy.kind = static_cast<PolicyKind>(in->kind);
+    cfg.policy.equinox.alpha = in->alpha;
+    cfg.policy.equinox.delta = in->delta;
+    cfg.policy.equinox.output_weight = in->output_weight;
+    cfg.policy.equinox.norm_mode = in->norm_mode == EQXO_NORM_NONE ? NormMode::None : NormMode::MaxOverClients;
+    cfg.policy.vtc_use_prediction = in->vtc_use_prediction != 0;
+    cfg.policy.counter_lift = in->counter_lift != 0;
+    cfg.perf.max_batch = in->max_batch;
+    cfg.perf.mem_per_token_bytes = in->mem_per_token_bytes;
+    cfg.perf.mem_capacity_bytes = in->mem_capacity_bytes;
+    cfg.backfill = in->backfill != 0;
+    cfg.max_sim_time_s = max_sim_time_s;
+    cfg.ema_alpha = ema_alpha;
+    cfg.report_window_s = window_s;
+    cfg.prediction_overhead_ms = in->prediction_overhead_ms;
+    GpuProfile profile;
+    for (int e = 0; e < in->n_profile; ++e)
+      profile.entries.push_back({in->prof_upper[e], in->prof_lat[e], in->prof_util[e], in->prof_tps[e]});
+    std::unique_ptr<Predictor> predictor;
+    if (in->pred_kind == EQXO_PRED_MOPE) {
+      predictor = std::make_unique<MopePredictor>(model_from(in->mope, tags, in->tag_row, in->n_tags));
+    } else if (in->pred_kind == EQXO_PRED_NOISY) {
+      predictor = std::make_unique<NoisyOraclePredictor>(in->noisy_l1, in->noisy_seed);
+    } else {
+      predictor = std::make_unique<OraclePredictor>();
+    }
+    const SimResult res = run_simulation(trace, cfg, *predictor, profile);
+    int64_t n = 0;
+    for (const auto& e : res.log.entries) {
+      if (n < cap) {
+        int k = 0, a = 0;
+        double x = 0.0, y = 0.0, z = 0.0;
+        switch (e.event) {
+          case LogEvent::Admitted: k = 1; a = e.predicted_output_tokens; x = e.predicted_latency_ms; break;
+          case LogEvent::Rejected: k = 2; a = e.input_tokens; break;
+          case LogEvent::Arrived: k = 3; a = e.input_tokens; break;
+          case LogEvent::FirstToken: k = 4; break;
+          case LogEvent::Completed: k = 5; a = e.output_tokens; x = e.latency_s; y = e.tps; z = e.gpu_util; break;
+        }
+        id[n] = e.request_id;
+        kind[n] = k;
+        t[n] = e.time_s;
+        i0[n] = a;
+        d0[n] = x;
+        d1[n] = y;
+        d2[n] = z;
+      }
+      ++n;
+    }
+    const std::size_t P = res.profile.entries.size();
+    for (std::size_t e = 0; e < P; ++e) {
+      prof[e] = res.profile.entries[e].latency_ms;
+      prof[P + e] = res.profile.entries[e].gpu_util;
+      prof[2 * P + e] = res.profile.entries[e].tps;
+    }
+    for (std::size_t c = 0; c < res.final_clients.size(); ++c) {
+      cl[4 * c] = res.final_clients[c].ufc;
+      cl[4 * c + 1] = res.final_clients[c].rfc;
+      cl[4 * c + 2] = res.final_clients[c].counter;
+      cl[4 * c + 3] = res.final_clients[c].accumulated_service;
+    }
+    tot[0] = res.sim_end_s;
+    tot[1] = res.busy_ms_total;
+    tot[2] = res.overhead_ms_total;
+    tot[3] = static_cast<double>(res.max_resident_kv_tokens);
+    tot[4] = static_cast<double>(res.completed);
+    tot[5] = static_cast<double>(res.rejected);
+    tot[6] = static_cast<double>(res.counter_clamps);
+    return n;
+  } catch (const std::exception& e) {
+    if (err && err_len > 0) std::snprintf(err, err_len, "%s", e.what());
+    return -1;
   }
 }

@@ -76,15 +76,16 @@ class Replays(C.Structure):
                 ("arrival_s", C.c_void_p), ("input_tokens", C.c_void_p), ("true_output_tokens", C.c_void_p),
                 ("tag", C.c_void_p), ("id", C.c_void_p), ("alpha", C.c_void_p), ("max_sim_time_s", C.c_double),
                 ("ema_alpha", C.c_double), ("ev_cap", C.c_int64), ("report_window_s", C.c_double),
-                ("win_cap", C.c_int64)]
+                ("win_cap", C.c_int64), ("duration_s", C.c_void_p), ("prediction_overhead_ms", C.c_double),
+                ("predicted", C.c_void_p), ("log_all", C.c_int32)]
 
 
 REPORT_FIELDS = ("max_diff", "avg_diff", "var_diff", "jain_hf", "jain_ttft_p90", "throughput_tps", "mean_gpu_util",
                  "ttft_p50", "ttft_p90", "latency_p50", "latency_p90", "ttft_count", "latency_count", "sim_end_s",
                  "busy_ms_total", "overhead_ms_total", "completed", "rejected", "total_completed_tokens",
-                 "n_windows", "n_diff", "n_rate")
+                 "n_windows", "n_diff", "n_rate", "max_resident_kv_tokens", "drained")
 REPORT_INT = {"ttft_count", "latency_count", "completed", "rejected", "total_completed_tokens", "n_windows", "n_diff",
-              "n_rate"}
+              "n_rate", "max_resident_kv_tokens", "drained"}
 REPORT_DTYPE = np.dtype([(f, np.int64 if f in REPORT_INT else np.float64) for f in REPORT_FIELDS])
 CLIENT_FIELDS = ("final_hf", "accumulated_service", "mean_service_rate", "ttft_p50", "ttft_p90", "ttft_count")
 CLIENT_DTYPE = np.dtype([(f, np.int64 if f == "ttft_count" else np.float64) for f in CLIENT_FIELDS])
@@ -96,7 +97,8 @@ class ReplayOut(C.Structure):
                 ("sim_end", C.c_void_p), ("counter_clamps", C.c_void_p), ("status", C.c_void_p),
                 ("jain_ttft_p90", C.c_void_p), ("throughput_tps", C.c_void_p), ("report", C.c_void_p),
                 ("clients", C.c_void_p), ("win", C.c_void_p), ("win_clients", C.c_void_p), ("diff", C.c_void_p),
-                ("rate", C.c_void_p)]
+                ("rate", C.c_void_p), ("ev_i0", C.c_void_p), ("ev_d0", C.c_void_p), ("ev_d1", C.c_void_p),
+                ("ev_d2", C.c_void_p), ("profile", C.c_void_p)]
 
 
 class TraceView(C.Structure):

@@ -73,6 +73,7 @@ struct eqx_ctx {
 
   int32_t C = 0;
   DevBuf d_ufc, d_rfc, d_counter, d_weight, d_order, d_running, d_backlogged;
+  DevBuf d_by_order;               // client of client_id rank k (replay reports)
   DevBuf d_head, d_count, d_first, d_qlen_before, d_seg_off;
 
   int64_t n = 0;
@@ -686,6 +687,7 @@ eqx_status eqx_set_clients(eqx_ctx* ctx, int32_t n, const char* names, const dou
   CUDA_TRY(ctx, ctx->d_counter.ensure(d8));
   CUDA_TRY(ctx, ctx->d_weight.ensure(d8));
   CUDA_TRY(ctx, ctx->d_order.ensure(d4));
+  CUDA_TRY(ctx, ctx->d_by_order.ensure(d4));
   CUDA_TRY(ctx, ctx->d_running.ensure(d4));
   CUDA_TRY(ctx, ctx->d_backlogged.ensure(d4));
   CUDA_TRY(ctx, ctx->d_head.ensure(d4));
@@ -702,6 +704,7 @@ eqx_status eqx_set_clients(eqx_ctx* ctx, int32_t n, const char* names, const dou
     CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_counter.p, counter ? counter : zeros.data(), 8ull * n, cudaMemcpyHostToDevice, s));
     CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_weight.p, weight, 8ull * n, cudaMemcpyHostToDevice, s));
     CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_order.p, order.data(), 4ull * n, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_by_order.p, idx.data(), 4ull * n, cudaMemcpyHostToDevice, s));
     CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_running.p, running ? running : izeros.data(), 4ull * n, cudaMemcpyHostToDevice, s));
     CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_backlogged.p, 0, d4, s));
     CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_head.p, 0, d4, s));
@@ -1580,8 +1583,10 @@ eqx_status eqx_replay(eqx_ctx* ctx, const eqx_replays* R, eqx_replay_out* O) {
   if (nr < 0 || !R->row_off || (nr > 0 && (!R->alpha || !R->client || !R->arrival_s || !R->input_tokens ||
                                            !R->true_output_tokens)))
     return fail(ctx, EQX_ERR_ARG, "eqx_replay: missing replay columns");
-  if (C < 1 || C > kMaxReplayClients) return fail(ctx, EQX_ERR_CONFIG, "eqx_replay: rosters of 1..16 clients");
+  if (C < 1) return fail(ctx, EQX_ERR_CONFIG, "eqx_replay: empty roster");
   if (R->ema_alpha <= 0.0 || R->ema_alpha > 1.0) return fail(ctx, EQX_ERR_CONFIG, "ema_alpha must lie in (0, 1]");
+  if (R->prediction_overhead_ms < 0.0) return fail(ctx, EQX_ERR_CONFIG, "prediction_overhead_ms must be >= 0");
+  if (R->max_sim_time_s < 0.0) return fail(ctx, EQX_ERR_CONFIG, "max_sim_time_s must be >= 0");
   for (int32_t i = 0; i < nr; ++i) {
     if (R->alpha[i] < 0.0 || R->alpha[i] > 1.0) return fail(ctx, EQX_ERR_CONFIG, "alpha must lie in [0, 1]");
     if (R->row_off[i + 1] < R->row_off[i]) return fail(ctx, EQX_ERR_ARG, "eqx_replay: row offsets must be ordered");
@@ -1622,6 +1627,10 @@ eqx_status eqx_replay(eqx_ctx* ctx, const eqx_replays* R, eqx_replay_out* O) {
                o_k = take(8 * n8 * C), o_ttft = take(8 * rr), o_jain = take(8 * n8), o_tput = take(8 * n8);
   const int64_t wcap = std::max<int64_t>(R->win_cap, 0);
   const size_t w8 = static_cast<size_t>(wcap), c8 = static_cast<size_t>(C);
+  const bool full = R->log_all != 0;
+  const size_t o_dur = take(8 * n8), o_given = take(R->predicted ? 4 * rr : 0), o_plat = take(full ? 8 * rr : 0),
+               o_i0 = take(full ? 4 * n8 * cap : 0), o_d0 = take(full ? 8 * n8 * cap : 0),
+               o_d1 = take(full ? 8 * n8 * cap : 0), o_d2 = take(full ? 8 * n8 * cap : 0);
   const size_t o_lat = take(8 * rr), o_rep = take(sizeof(eqx_replay_report) * n8),
                o_rcl = take(sizeof(eqx_replay_client) * n8 * c8), o_win = take(8 * 4 * n8 * w8),
                o_winc = take(8 * 4 * n8 * w8 * c8), o_diff = take(8 * 2 * n8 * w8), o_rate = take(8 * n8 * c8 * w8);
@@ -1637,6 +1646,8 @@ eqx_status eqx_replay(eqx_ctx* ctx, const eqx_replays* R, eqx_replay_out* O) {
   CUDA_TRY(ctx, up(o_true, R->true_output_tokens, 4 * rows));
   CUDA_TRY(ctx, up(o_tag, R->tag, rows));
   CUDA_TRY(ctx, up(o_alpha, R->alpha, 8 * n8));
+  if (R->duration_s) CUDA_TRY(ctx, up(o_dur, R->duration_s, 8 * n8));
+  if (R->predicted) CUDA_TRY(ctx, up(o_given, R->predicted, 4 * rows));
   std::vector<int64_t> ids;
   if (!R->id) {  // trace positions within each replay
     ids.resize(rr);
@@ -1700,11 +1711,26 @@ eqx_status eqx_replay(eqx_ctx* ctx, const eqx_replays* R, eqx_replay_out* O) {
   A.win_clients = O->win_clients && wcap > 0 ? reinterpret_cast<double*>(b + o_winc) : nullptr;
   A.diff = O->diff && wcap > 0 ? reinterpret_cast<double*>(b + o_diff) : nullptr;
   A.rate = O->rate && wcap > 0 ? reinterpret_cast<double*>(b + o_rate) : nullptr;
+  A.duration = R->duration_s ? reinterpret_cast<const double*>(b + o_dur) : nullptr;
+  A.overhead_s = R->prediction_overhead_ms / 1000.0;  // eligible_at's operand (engine.cpp:167)
+  A.given_pred = R->predicted ? reinterpret_cast<const int32_t*>(b + o_given) : nullptr;
+  A.by_order = ctx->d_by_order.as<uint32_t>();
+  A.log_all = full ? 1 : 0;
+  A.f_plat = full ? reinterpret_cast<double*>(b + o_plat) : nullptr;
+  A.ev_i0 = full ? reinterpret_cast<int32_t*>(b + o_i0) : nullptr;
+  A.ev_d0 = full ? reinterpret_cast<double*>(b + o_d0) : nullptr;
+  A.ev_d1 = full ? reinterpret_cast<double*>(b + o_d1) : nullptr;
+  A.ev_d2 = full ? reinterpret_cast<double*>(b + o_d2) : nullptr;
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[2], s));
   {  // one warp per replay; the instantiation of the context's policy (explicit in eqx_replay.cu)
-    const void* rk = ctx->pol.kind == kFcfs  ? reinterpret_cast<const void*>(replay_kernel<kFcfs>)
-                     : ctx->pol.kind == kVtc ? reinterpret_cast<const void*>(replay_kernel<kVtc>)
-                                             : reinterpret_cast<const void*>(replay_kernel<kEquinox>);
+    const bool big = C > kMaxReplayClients;
+    const void* rk = ctx->pol.kind == kFcfs
+                         ? (big ? reinterpret_cast<const void*>(replay_kernel<kFcfs, true>)
+                                : reinterpret_cast<const void*>(replay_kernel<kFcfs, false>))
+                     : ctx->pol.kind == kVtc ? (big ? reinterpret_cast<const void*>(replay_kernel<kVtc, true>)
+                                                    : reinterpret_cast<const void*>(replay_kernel<kVtc, false>))
+                     : (big ? reinterpret_cast<const void*>(replay_kernel<kEquinox, true>)
+                            : reinterpret_cast<const void*>(replay_kernel<kEquinox, false>));
     void* args[] = {&A};
     CUDA_TRY(ctx, cudaLaunchKernel(rk, dim3((nr + 3) / 4), dim3(128), args, 0, s));
   }
@@ -1729,7 +1755,15 @@ eqx_status eqx_replay(eqx_ctx* ctx, const eqx_replays* R, eqx_replay_out* O) {
   const Col cols3[] = {{wcap > 0 ? O->win_clients : nullptr, b + o_winc, 8 * 4 * n8 * w8 * c8},
                        {wcap > 0 ? O->diff : nullptr, b + o_diff, 8 * 2 * n8 * w8},
                        {wcap > 0 ? O->rate : nullptr, b + o_rate, 8 * n8 * c8 * w8}};
-  return read_cols(ctx, cols3, 3);
+  st = read_cols(ctx, cols3, 3);
+  if (st != EQX_OK) return st;
+  const size_t np = static_cast<size_t>(ctx->model.n_prof);
+  const Col cols4[] = {{full ? O->ev_i0 : nullptr, b + o_i0, 4 * n8 * cap},
+                       {full ? O->ev_d0 : nullptr, b + o_d0, 8 * n8 * cap},
+                       {full ? O->ev_d1 : nullptr, b + o_d1, 8 * n8 * cap},
+                       {full ? O->ev_d2 : nullptr, b + o_d2, 8 * n8 * cap},
+                       {O->profile, b + o_prof, 8 * 3 * np * n8}};
+  return read_cols(ctx, cols4, 5);
 }
 
 // ---- live queues -----------------------------------------------------
@@ -2131,7 +2165,15 @@ eqx_status eqx_step_collect(eqx_ctx* ctx, eqx_step_summary* out) {
   cudaSetDevice(ctx->device);
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   const DevState& h = *ctx->h_state;
-  if (h.bad_client) return fail(ctx, EQX_ERR_CONFIG, "request references unknown client index");
+  if (h.bad_client) {
+    // the flag is sticky on the device: clear it so the next drain of valid queues succeeds, and
+    // end this step (its schedule is void)
+    ctx->step_pending = false;
+    ctx->h_state->bad_client = 0;
+    CUDA_TRY(ctx, cudaMemset(reinterpret_cast<char*>(ctx->d_state.p) + offsetof(DevState, bad_client), 0,
+                             sizeof(int32_t)));
+    return fail(ctx, EQX_ERR_CONFIG, "request references unknown client index");
+  }
   if (out) {
     out->n_events = h.n_events;
     out->n_admitted = h.n_admitted;

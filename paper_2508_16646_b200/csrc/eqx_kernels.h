@@ -345,7 +345,8 @@ __global__ void gather_live_kernel(LiveArgs a);
 __global__ void predict_rows_kernel(ScoreArgs a, int64_t r0, int64_t r1, LiveArgs L, int32_t fill_id);
 
 // ---- batched engine replays (eqx_replay.cu) ---------------------------
-constexpr int kMaxReplayClients = 16;
+constexpr int kMaxReplayClients = 16;  // rosters up to this size keep the ledger in registers /
+                                       // local memory; larger ones in global scratch (kBig)
 struct ReplayClient {
   double ufc, rfc, counter, weight;
   double service;            // ClientState::accumulated_service
@@ -353,6 +354,7 @@ struct ReplayClient {
   int32_t running, backlogged;
   uint32_t order;            // rank of client_id (select_next tie-break)
   int32_t qbase, qhead, qend;  // FIFO over the client's rows: [qhead, qend) of crow
+  int32_t skip;              // admit_requests' skipped set (large rosters): stamp of the call
 };
 struct ReplayMember {
   int32_t row, client, in, generated, reserved_out, pad;
@@ -412,9 +414,20 @@ struct ReplayArgs {
   double* win_clients;        // [n_replays][win_cap][C][4]
   double* diff;               // [n_replays][win_cap][2]
   double* rate;               // [n_replays][C][win_cap] (zeroed by the host)
+  // ABI 3: horizons, eligibility, caller predictions, the whole event log
+  const double* duration;     // [n_replays] Trace::duration_s (nullptr: last arrival)
+  double overhead_s;          // prediction_overhead_ms / 1000.0 (engine.cpp:165-168)
+  const int32_t* given_pred;  // [rows] Predictor::predict per row (nullptr: the device predictor)
+  const uint32_t* by_order;   // [C] client of client_id rank k
+  int32_t log_all;
+  int32_t* ev_i0;             // [n_replays][ev_cap] payloads (nullptr: not kept)
+  double* ev_d0;
+  double* ev_d1;
+  double* ev_d2;
+  double* f_plat;             // [rows] frozen predicted_latency_ms (log_all)
 };
-template <int KIND>
-__global__ void replay_kernel(ReplayArgs a);  // KIND: kFcfs / kVtc / kEquinox
+template <int KIND, bool kBig>
+__global__ void replay_kernel(ReplayArgs a);  // KIND: kFcfs / kVtc / kEquinox; kBig: C > 16
 
 __global__ void drain_hist_kernel(DrainArgs a);
 __global__ void lift_kernel(DrainArgs a);

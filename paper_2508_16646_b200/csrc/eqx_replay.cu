@@ -232,7 +232,7 @@ __device__ __noinline__ void rep_rate_advance(Reporter& R, ReplayClient* cl, int
 
 // KIND: the policy kind, fixed per instantiation so a replay carries only its policy's code
 // (the kernel is long scalar code; its instruction footprint is what its single warps stall on).
-template <int KIND>
+template <int KIND, bool kBig>
 __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
   __shared__ uint32_t s_hist[4][256];  // radix-select histograms, one per warp
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -264,7 +264,10 @@ __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
   // Ledger, FIFO cursors and profile are private per lane (identical copies, updated uniformly),
   // so the read-modify-write engine steps need no intra-warp synchronisation; the batch lives
   // in global scratch, split across lanes.
-  ReplayClient cl[kMaxReplayClients];
+  // kBig (rosters beyond kMaxReplayClients): one copy in global scratch, stored identically by
+  // every lane (each lane reads back its own store, so no intra-warp synchronisation either)
+  ReplayClient cl_local[kBig ? 1 : kMaxReplayClients];
+  ReplayClient* const cl = kBig ? A.cl + static_cast<int64_t>(r) * C : cl_local;
   double prof[4 * kMaxProfile];  // lat | util | tps | pred_s
   ReplayMember* mb = A.mb + static_cast<int64_t>(r) * P.max_batch;
   const int np = M.n_prof;
@@ -282,6 +285,7 @@ __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
     ReplayClient z{};
     z.weight = A.weight[c];
     z.order = A.order[c];
+    z.skip = -1;
     cl[c] = z;
   }
   for (int64_t i = 0; i < n; ++i) cl[client[i]].qend += 1;  // counts -> offsets
@@ -300,9 +304,15 @@ __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
     }
     for (int c = 0; c < C; ++c) cl[c].qend = cl[c].qbase;
   }
-  const double max_sim = A.max_sim_time_s > 0.0 ? A.max_sim_time_s : (n > 0 ? arrival[n - 1] : 0.0);
+  // run() (engine.cpp:120-121): max_sim_time_s, else Trace::duration_s
+  const double max_sim = A.max_sim_time_s > 0.0 ? A.max_sim_time_s
+                         : A.duration             ? A.duration[r]
+                                                  : (n > 0 ? arrival[n - 1] : 0.0);
+  // eligible_at (engine.cpp:165-168): arrival + prediction_overhead_ms / 1000
+  auto eligible_at = [&](int64_t i) { return __dadd_rn(arrival[i], A.overhead_s); };
   double now = 0.0, busy_cum = 0.0, ovh_cum = 0.0;
-  int64_t arrival_idx = 0, total_queued = 0, n_ev = 0, completed = 0, clamps = 0;
+  int64_t arrival_idx = 0, total_queued = 0, n_ev = 0, completed = 0, clamps = 0, max_resident = 0;
+  int32_t admit_no = 0;  // admit_requests calls (the skipped stamps of large rosters)
   int32_t members = 0;
   bool comp_changed = false;
   int32_t status = 0;
@@ -358,6 +368,22 @@ __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
     }
     ++n_ev;
   };
+  // the whole log (log_all): LogEntry payloads (engine.cpp:44-76)
+  const int64_t evo = static_cast<int64_t>(r) * A.ev_cap;
+  auto log_full = [&](int64_t rid, int32_t kind, double t, int32_t i0, double d0, double d1, double d2) {
+    if (n_ev < A.ev_cap) {
+      ev_id[n_ev] = rid;
+      ev_kind[n_ev] = kind;
+      ev_time[n_ev] = t;
+      if (A.ev_i0) {
+        A.ev_i0[evo + n_ev] = i0;
+        A.ev_d0[evo + n_ev] = d0;
+        A.ev_d1[evo + n_ev] = d1;
+        A.ev_d2[evo + n_ev] = d2;
+      }
+    }
+    ++n_ev;
+  };
   auto entry_for = [&](int32_t out) {  // gpu_model.cpp:74-80
     int b = np - 1;
     for (int e = np - 1; e >= 0; --e)
@@ -380,16 +406,25 @@ __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
     if (cl[c].rfc < mr) cl[c].rfc = mr;
     if (cl[c].counter < mc) cl[c].counter = mc;
   };
-  auto drain = [&](double upto) {  // engine.cpp:171-197 (prediction_overhead_ms = 0)
-    while (arrival_idx < n && __dadd_rn(arrival[arrival_idx], 0.0) <= upto) {
+  auto drain = [&](double upto) {  // engine.cpp:171-197
+    while (arrival_idx < n && eligible_at(arrival_idx) <= upto) {
       const int64_t i = arrival_idx++;
       const int c = client[i];
       const double w = cl[c].weight;
-      const Scored s = score_request(M, P, 0.0, in_tok[i], tag[i], true_out[i], id[i], 0.0, w);  // max(1, predict)
-      const int b = entry_for(s.pred);  // map_metrics against the replay's current profile
-      f_pred[i] = s.pred;
+      int32_t pred;  // max(1, predict(req)) (engine.cpp:179)
+      if (A.given_pred) {
+        pred = A.given_pred[t0 + i] > 1 ? A.given_pred[t0 + i] : 1;
+      } else {
+        pred = score_request(M, P, 0.0, in_tok[i], tag[i], true_out[i], id[i], 0.0, w).pred;
+      }
+      const int b = entry_for(pred);  // map_metrics against the replay's current profile
+      f_pred[i] = pred;
       f_preds[i] = prof[3 * kMaxProfile + b];
       f_rfc[i] = __dmul_rn(__dmul_rn(w, prof[2 * kMaxProfile + b]), prof[kMaxProfile + b]);
+      if (A.log_all) {
+        A.f_plat[t0 + i] = prof[b];  // every lane stores the same value and reads back its own
+        log_full(id[i], 3, arrival[i], in_tok[i], 0.0, 0.0, 0.0);  // Arrived at arrival_time_s
+      }
       if (cl[c].qend == cl[c].qhead && cl[c].running == 0) on_activated(c);
       cl[c].qend += 1;
       ++total_queued;
@@ -404,6 +439,7 @@ __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
   auto admit = [&]() -> int64_t {  // engine.cpp:207-271
     int64_t new_prefill = 0;
     uint64_t skipped = 0;
+    ++admit_no;
     for (;;) {
       double mu = 0.0, mr = 0.0;  // backlogged_maxima (scheduler.cpp:40-48)
       const bool maxmode = KIND == kEquinox && P.norm_mode == 0;
@@ -417,7 +453,7 @@ __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
       double bk = 0.0, ba = 0.0;
       uint32_t bo = 0;
       for (int i = 0; i < C; ++i) {
-        if (cl[i].qhead == cl[i].qend || ((skipped >> (i & 63)) & 1u)) continue;
+        if (cl[i].qhead == cl[i].qend || (kBig ? cl[i].skip == admit_no : ((skipped >> (i & 63)) & 1u))) continue;
         double k;
         if (KIND == kFcfs) k = 0.0;
         else if (KIND == kVtc) k = cl[i].counter;
@@ -441,7 +477,8 @@ __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
       const int32_t in = in_tok[row], pred = f_pred[row];
       // fits_alone (gpu_model.cpp:69-72): the can_fit test on an empty batch
       if (!((1 <= P.max_batch) && __dmul_rn(static_cast<double>(static_cast<int64_t>(in) + pred), P.m) <= P.M)) {
-        log_ev(id[row], 2);
+        if (A.log_all) log_full(id[row], 2, now, in, 0.0, 0.0, 0.0);
+        else log_ev(id[row], 2);
         ++rejected;
         pop_head(c);
         continue;
@@ -453,7 +490,8 @@ __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
       if (!((members + 1 <= P.max_batch) &&
             __dmul_rn(static_cast<double>(reserved + in + pred), P.m) <= P.M)) {  // can_fit
         if (P.backfill) {
-          skipped |= 1ull << (c & 63);
+          if (kBig) cl[c].skip = admit_no;
+          else skipped |= 1ull << (c & 63);
           continue;
         }
         break;
@@ -484,7 +522,11 @@ __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
         m.p_vtc = P.vtc_use_prediction ? __dmul_rn(w, tokens) : __dmul_rn(w, static_cast<double>(in));
         cl[c].counter = __dadd_rn(cl[c].counter, m.p_vtc);
       }
-      log_ev(id[row], 1);
+      if (A.log_all) {
+        log_full(id[row], 1, now, pred, A.f_plat[t0 + row], 0.0, 0.0);
+      } else {
+        log_ev(id[row], 1);
+      }
     }
     return new_prefill;
   };
@@ -493,12 +535,13 @@ __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
     drain(now);
     if (members == 0 && total_queued == 0) {
       if (arrival_idx >= n) break;
-      const double next_t = __dadd_rn(arrival[arrival_idx], 0.0);
+      const double next_t = eligible_at(arrival_idx);
       if (next_t >= max_sim) break;
       advance_clock(now, next_t, 0.0, 0.0);
       now = next_t;
       drain(now);
     }
+    const int32_t members0 = members;  // admissions of this round are members [members0, members)
     const int64_t new_prefill = admit();
     if (members == 0) continue;
     // ---- run_iteration (engine.cpp:273-325) ----
@@ -530,11 +573,17 @@ __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
       }
     }
     const int64_t res2 = resident + members;  // every resident request generated one token
+    if (res2 > max_resident) max_resident = res2;
     if (__dmul_rn(static_cast<double>(res2), P.m) > P.M) {  // KV memory bound violated
       status = 2;
       break;
     }
     drain(now);
+    // FirstToken of this round's admissions, in admission order, after the iteration's
+    // arrivals (engine.cpp:305-318)
+    if (A.log_all)
+      for (int32_t j = members0; j < members; ++j)
+        if (mb[j].generated == 1) log_full(id[mb[j].row], 4, now, 0, 0.0, 0.0, 0.0);
     // ---- complete_finished (engine.cpp:327-375) ----
     // finished members are processed in batch order (ledger and update_map chains), then the
     // survivors are compacted in order (members.erase keeps the relative order)
@@ -563,6 +612,7 @@ __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
         const double util = __ddiv_rn(busy_span, __dadd_rn(busy_span, ovh_span));
         ++completed;
         completed_tokens += static_cast<int64_t>(m.in) + out;
+        if (A.log_all) log_full(id[m.row], 5, now, out, latency_s, tps, util);  // Completed
         if (lane == 0) f_lat[m.row] = latency_s;
         if (C >= 2 && R.sd_t < now) rep_diff_until(R, cl, now);  // windows closed before this completion
         // on_complete (scheduler.cpp:192-233)
@@ -632,6 +682,8 @@ __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
   rep.rejected = rejected;
   rep.total_completed_tokens = completed_tokens;
   rep.n_windows = R.n_win;
+  rep.max_resident_kv_tokens = max_resident;
+  rep.drained = arrival_idx;
   if (C >= 2) {  // service_difference: the remaining windows up to the end, then the moments
     const double lim = __dadd_rn(now, 1e-12);
     while (R.sd_t <= lim) {
@@ -684,10 +736,7 @@ __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
     double sum = 0.0, sum_sq = 0.0;
     int32_t m_clients = 0;
     for (uint32_t rank = 0; rank < static_cast<uint32_t>(C); ++rank) {
-      int c = -1;
-      for (int i = 0; i < C; ++i)
-        if (cl[i].order == rank) c = i;
-      if (c < 0) continue;
+      const int c = static_cast<int>(A.by_order[rank]);
       const int32_t c_rows = (c + 1 < C ? cl[c + 1].qbase : static_cast<int32_t>(n)) - cl[c].qbase;
       const int32_t* rows_c = crow + cl[c].qbase;
       double p50, p90;
@@ -720,6 +769,14 @@ __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
     warp_percentiles([&](int64_t j) { return f_lat[j]; }, n, &rep.latency_p50, &rep.latency_p90, &rep.latency_count, hist);
     if (lane == 0) A.report[r] = rep;
   }
+  if (lane == 0) {  // SimResult::profile (the feedback-updated map)
+    double* po = A.prof + static_cast<int64_t>(r) * 3 * np;
+    for (int e = 0; e < np; ++e) {
+      po[e] = prof[e];
+      po[np + e] = prof[kMaxProfile + e];
+      po[2 * np + e] = prof[2 * kMaxProfile + e];
+    }
+  }
   A.n_events[r] = n_ev;
   A.completed[r] = completed;
   A.sim_end[r] = now;
@@ -732,8 +789,11 @@ __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
   }
 }
 
-template __global__ void replay_kernel<kFcfs>(ReplayArgs);
-template __global__ void replay_kernel<kVtc>(ReplayArgs);
-template __global__ void replay_kernel<kEquinox>(ReplayArgs);
+template __global__ void replay_kernel<kFcfs, false>(ReplayArgs);
+template __global__ void replay_kernel<kVtc, false>(ReplayArgs);
+template __global__ void replay_kernel<kEquinox, false>(ReplayArgs);
+template __global__ void replay_kernel<kFcfs, true>(ReplayArgs);
+template __global__ void replay_kernel<kVtc, true>(ReplayArgs);
+template __global__ void replay_kernel<kEquinox, true>(ReplayArgs);
 
 }  // namespace eqx

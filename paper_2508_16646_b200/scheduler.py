@@ -511,7 +511,8 @@ class GpuScheduler:
     # -- batched engine replays --
     def replay(self, row_off, client, arrival_s, input_tokens, true_output_tokens, alpha, tag=None, ids=None,
                max_sim_time_s: float = 0.0, ema_alpha: float = 0.2, ev_cap: int = 4096,
-               report_window_s: float = 1.0, win_cap: int = 0) -> dict:
+               report_window_s: float = 1.0, win_cap: int = 0, duration_s=None,
+               prediction_overhead_ms: float = 0.0, predicted=None, log_all: bool = False) -> dict:
         """run_simulation (engine.cpp:119-146) for many traces at once on the GPU, one replay per
         warp: traces concatenated (row_off[r]..row_off[r+1]), per-replay alpha, the
         scheduler's policy / perf / profile / predictor / roster otherwise.  Returns the
@@ -521,7 +522,15 @@ class GpuScheduler:
         With win_cap > 0 also the series, each cut at win_cap windows: "win" [r][w][4] (time,
         busy_ms, overhead_ms, gpu_util: SimResult::gpu_series), "win_clients" [r][w][C][4] (ufc,
         rfc, hf, service_cum: counter_series), "diff" [r][w][2] (diff_series) and "rate"
-        [r][C][w] (service_rate_series values; window w ends at report_window_s * (w + 1))."""
+        [r][C][w] (service_rate_series values; window w ends at report_window_s * (w + 1)).
+
+        ``duration_s`` [r]: each trace's Trace::duration_s, the horizon when max_sim_time_s is 0
+        (engine.cpp:120-121; default: its last arrival).  ``prediction_overhead_ms`` delays
+        eligibility (engine.cpp:165-168).  ``predicted`` [rows]: Predictor::predict of every row
+        from a caller's predictor instead of the scheduler's.  ``log_all``: the events are the
+        engine's whole log (EQX_EV_*: arrived 3, admitted 1, first_token 4, completed 5,
+        rejected 2) with payloads "ev_i0", "ev_d0".."ev_d2" (include/eqx.h); "profile" [r][3][P]
+        is the feedback-updated GPU profile (latency_ms, gpu_util, tps)."""
         n = len(alpha)
         nc = len(self.client_ids)
         cols = {"row_off": np.ascontiguousarray(row_off, np.int64), "client": np.ascontiguousarray(client, np.int32),
@@ -530,26 +539,33 @@ class GpuScheduler:
                 "true_output_tokens": np.ascontiguousarray(true_output_tokens, np.int32),
                 "alpha": np.ascontiguousarray(alpha, np.float64),
                 "tag": None if tag is None else np.ascontiguousarray(tag, np.uint8),
-                "id": None if ids is None else np.ascontiguousarray(ids, np.int64)}
+                "id": None if ids is None else np.ascontiguousarray(ids, np.int64),
+                "duration_s": None if duration_s is None else np.ascontiguousarray(duration_s, np.float64),
+                "predicted": None if predicted is None else np.ascontiguousarray(predicted, np.int32)}
         ptr = {k: (v.ctypes.data if v is not None else None) for k, v in cols.items()}
         if report_window_s <= 0.0:
             raise ConfigError("'engine.report_window_s' must be > 0")
         wc = max(int(win_cap), 0)
         rq = L.Replays(n, ptr["row_off"], ptr["client"], ptr["arrival_s"], ptr["input_tokens"],
                        ptr["true_output_tokens"], ptr["tag"], ptr["id"], ptr["alpha"], float(max_sim_time_s),
-                       float(ema_alpha), int(ev_cap), float(report_window_s), wc)
+                       float(ema_alpha), int(ev_cap), float(report_window_s), wc, ptr["duration_s"],
+                       float(prediction_overhead_ms), ptr["predicted"], 1 if log_all else 0)
         out = {"n_events": np.zeros(n, np.int64), "ev_id": np.zeros((n, ev_cap), np.int64),
                "ev_kind": np.zeros((n, ev_cap), np.int32), "ev_time": np.zeros((n, ev_cap)),
                "ufc": np.zeros((n, nc)), "rfc": np.zeros((n, nc)), "counter": np.zeros((n, nc)),
                "completed": np.zeros(n, np.int64), "sim_end": np.zeros(n), "counter_clamps": np.zeros(n, np.int64),
                "status": np.zeros(n, np.int32), "jain_ttft_p90": np.zeros(n), "throughput_tps": np.zeros(n),
-               "report": np.zeros(n, L.REPORT_DTYPE), "clients": np.zeros((n, nc), L.CLIENT_DTYPE)}
+               "report": np.zeros(n, L.REPORT_DTYPE), "clients": np.zeros((n, nc), L.CLIENT_DTYPE),
+               "profile": np.zeros((n, 3, self._n_profile))}
+        if log_all:
+            out.update(ev_i0=np.zeros((n, ev_cap), np.int32), ev_d0=np.zeros((n, ev_cap)),
+                       ev_d1=np.zeros((n, ev_cap)), ev_d2=np.zeros((n, ev_cap)))
         if wc:
             out.update(win=np.zeros((n, wc, 4)), win_clients=np.zeros((n, wc, nc, 4)), diff=np.zeros((n, wc, 2)),
                        rate=np.zeros((n, nc, wc)))
         names = ("n_events", "ev_id", "ev_kind", "ev_time", "ufc", "rfc", "counter", "completed", "sim_end",
                  "counter_clamps", "status", "jain_ttft_p90", "throughput_tps", "report", "clients", "win",
-                 "win_clients", "diff", "rate")
+                 "win_clients", "diff", "rate", "ev_i0", "ev_d0", "ev_d1", "ev_d2", "profile")
         ro = L.ReplayOut(*((out[k].ctypes.data if k in out else None) for k in names))
         self._check(self._lib.eqx_replay(self._ctx, C.byref(rq), C.byref(ro)))
         if np.any(out["status"] == 2):
@@ -565,8 +581,22 @@ class GpuScheduler:
         row_off = np.concatenate([[0], np.cumsum([len(t["client"]) for _, t in pairs])]).astype(np.int64)
         cat = {k: np.concatenate([np.asarray(t[k]) for _, t in pairs]) for k in
                ("client", "arrival", "in_tokens", "true_out")}
-        out = self.replay(row_off, cat["client"], cat["arrival"], cat["in_tokens"], cat["true_out"],
-                          np.array([a for a, _ in pairs]), ema_alpha=ema_alpha, ev_cap=1)
+        # every sweep point runs the Equinox policy (experiments.cpp:345-347), whatever this
+        # scheduler was built with
+        saved = self.policy
+        if saved.kind != "equinox":
+            import dataclasses
+            self.policy = dataclasses.replace(saved, kind="equinox")
+            self._set_policy()
+        try:
+            out = self.replay(row_off, cat["client"], cat["arrival"], cat["in_tokens"], cat["true_out"],
+                              np.array([a for a, _ in pairs]), ema_alpha=ema_alpha, ev_cap=1,
+                              duration_s=[t.get("duration_s", 0.0) or t["arrival"][-1] if len(t["arrival"]) else 0.0
+                                          for _, t in pairs])
+        finally:
+            if self.policy is not saved:
+                self.policy = saved
+                self._set_policy()
         k = len(traces)
         points = []
         for i, a in enumerate(alphas):  # the reference's accumulation order (seeds in order)

@@ -23,7 +23,7 @@ from typing import Sequence
 import numpy as np
 
 from . import _lib as L
-from .scheduler import ClientState, ConfigError, GpuScheduler, StepResult
+from .scheduler import ClientState, ConfigError, EngineError, GpuScheduler, StepResult
 
 # WinEntry (csrc/eqx_kernels.h): one scored head-of-queue request, 40 bytes.
 WIN_DTYPE = np.dtype([("ufc_inc", "<f8"), ("rfc_inc", "<f8"), ("abits", "<u8"), ("in_tokens", "<i4"),
@@ -167,6 +167,10 @@ class ShardedScheduler:
         self.retries = 0
         self._bufs: dict = {}
         self._lmap = None
+        # one step per drain: shard_ingest treats every queued request as a fresh arrival (queue
+        # length before = 0, counter lift in arrival order), which is the reference's state only
+        # right after drain_arrivals of the whole queue (engine.cpp:171-197)
+        self._drained = False
 
     def set_batch(self, members: int, reserved_kv_tokens: int) -> None:
         self.members = int(members)
@@ -192,6 +196,7 @@ class ShardedScheduler:
                 client = self.layout.local_index(self.rank, client)
         self.local.drain(client, arrival_s, input_tokens, tag=tag, true_output_tokens=true_output_tokens,
                          ids=ids)
+        self._drained = True
 
     def _buf(self, name: str, nbytes: int):
         import torch
@@ -203,7 +208,12 @@ class ShardedScheduler:
         return b[:nbytes]
 
     def step_async(self, now: float, window: int) -> None:
-        """Export -> all-gather -> selection, all enqueued on the shared stream."""
+        """Export -> all-gather -> selection, all enqueued on the shared stream.  Exactly one
+        step per drain (the sharded step treats the drained queue as fresh arrivals)."""
+        if not self._drained:
+            raise EngineError("sharded step without a drain: ShardedScheduler runs one step per drain of the "
+                              "rank's whole queue")
+        self._drained = False
         stride = _a16(record_bytes(self.layout.cmax, window))
         send = self._buf("send", stride)
         self.local.shard_export_async(now, self.layout.cmax, window, send)
@@ -214,15 +224,24 @@ class ShardedScheduler:
         self.sel.shard_select_async(recv, self.world, stride, self.layout.off, self.layout.cmax, window, now)
 
     def default_window(self) -> int:
+        """Head-window depth exchanged per client: small by default (a client rarely takes more
+        than a few of the free slots when many clients are backlogged), grown 4x after an
+        underflow and kept; the depth never exceeds free slots + 1, which is always exact without
+        rejection streams."""
+        free = max(0, self.max_batch - self.members)
         if self.window:
-            return self.window
-        return max(1, min(self.max_batch - self.members, 64) + 1)
+            return min(self.window, free + 1) if free else 1
+        return max(1, min(free + 1, 8))
 
     def step(self, now: float, window: int | None = None, with_events: bool = True) -> StepResult:
         """One exact scheduling step over the whole sharded queue; identical on every rank."""
+        if not self._drained:
+            raise EngineError("sharded step without a drain: ShardedScheduler runs one step per drain of the "
+                              "rank's whole queue")
         W = window or self.default_window()
         self.sel.checkpoint()
         while True:
+            self._drained = True  # a retry re-runs the same drained step from its checkpoint
             self.step_async(now, W)
             res = self.sel.collect(with_events=with_events)
             if not res.window_underflow:

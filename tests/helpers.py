@@ -99,8 +99,16 @@ def gpu_run(case: H.StepCase, device_columns: bool = False):
     return sch, res
 
 
-def compare_step(res, sch, want: dict, flagged_near_ties: int = 0) -> None:
-    """Bit-exact parity of events, ledger and per-request scores against an oracle output."""
+def compare_step(res, sch, want: dict, flagged_near_ties: int = 0, row_ids=None) -> None:
+    """Bit-exact parity of events, ledger and per-request scores against an oracle output.
+
+    ``flagged_near_ties`` > 0 (noisy-oracle predictions within 1e-9 of a .5 rounding boundary,
+    where the device's log1p and glibc's may round apart -- the only differences the north
+    star allows): every unflagged row must still match bit-exactly; a flagged row may differ
+    by one token.  The schedule is compared in full when no prediction differs, else only up to
+    the first event that a differing prediction could have influenced."""
+    if flagged_near_ties and compare_flagged(res, sch.scores(), want, flagged_near_ties, row_ids):
+        return
     np.testing.assert_array_equal(res.ids, want["ev_id"], err_msg="event ids / order")
     np.testing.assert_array_equal(res.kinds, want["ev_kind"], err_msg="event kinds")
     np.testing.assert_array_equal(res.clients, want["ev_client"])
@@ -122,3 +130,26 @@ def compare_step(res, sch, want: dict, flagged_near_ties: int = 0) -> None:
     np.testing.assert_array_equal(sc["ufc_inc"], want["ufc_inc"], err_msg="ufc_inc")
     np.testing.assert_array_equal(sc["rfc_inc"], want["rfc_inc"], err_msg="rfc_inc")
     assert res.length_fallbacks == want["length_fallbacks"]
+
+
+def compare_flagged(res, sc: dict, want: dict, flagged: int, row_ids=None) -> bool:
+    """Noisy-oracle near-ties (see compare_step): unflagged rows bit-exact, flagged rows within
+    one token.  Returns True when a prediction differs -- the event prefix before the first
+    event of a differing row was compared and the rest of the step may legitimately differ."""
+    diff = np.nonzero(sc["pred"] != want["pred"])[0]
+    assert len(diff) <= flagged, f"{len(diff)} predictions differ, {flagged} flagged"
+    assert np.all(np.abs(sc["pred"][diff].astype(np.int64) - want["pred"][diff]) == 1)
+    ok = np.ones(len(sc["pred"]), bool)
+    ok[diff] = False
+    for k in ("pred", "ufc_inc", "rfc_inc"):
+        np.testing.assert_array_equal(sc[k][ok], want[k][ok], err_msg=k + " (unflagged rows)")
+    np.testing.assert_array_equal(np.asarray(sc["bucket"]).astype(np.int32)[ok], want["bucket"][ok])
+    if not len(diff):
+        return False
+    # the schedule agrees up to the first event of a request whose prediction differs (its
+    # increments enter the ledger there); compare that prefix
+    bad = set((np.arange(len(sc["pred"])) if row_ids is None else np.asarray(row_ids))[diff].tolist())
+    n = min(len(res.ids), len(want["ev_id"]))
+    stop = next((i for i in range(n) if int(want["ev_id"][i]) in bad or int(res.ids[i]) in bad), n)
+    np.testing.assert_array_equal(res.ids[:stop], want["ev_id"][:stop], err_msg="event prefix")
+    return True

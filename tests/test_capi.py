@@ -23,7 +23,7 @@ def test_library_exports_every_declared_symbol():
     assert decl == L.EXPORTED
     for name in decl:
         assert hasattr(lib, name), name
-    assert lib.eqx_abi_version() == 2
+    assert lib.eqx_abi_version() == 3
 
 
 def test_library_is_sm100a_only():

@@ -198,3 +198,98 @@ def test_full_report_cutoff_caps_and_single_client():
     want, got = run_full([one], [0.7], window_s=1.0, win_cap=32, pred_kind=0)
     check_full(want, got, 32)
     assert got["report"]["n_diff"][0] == 0 and got["report"]["max_diff"][0] == 0.0
+
+
+# ---- the engine's whole log, horizons, eligibility, large rosters, caller predictions ----------
+def run_log(traces, alphas, duration=None, overhead_ms=0.0, max_sim=0.0, predicted=None, window_s=1.0, **kw):
+    """GPU replays with log_all against the reference's run_simulation SimResult (ref_replay_log)."""
+    from paper_2508_16646_b200 import scheduler as S
+    base = dict(model=default_model(), profile=default_profile())
+    base.update(kw)
+    cases = [H.StepCase(client=q["client"], arrival=q["arrival"], in_tokens=q["in_tokens"], true_out=q["true_out"],
+                        tag=q["tag"], client_names=q["client_names"], alpha=float(a),
+                        duration_s=float(duration[i]) if duration is not None else 0.0,
+                        prediction_overhead_ms=overhead_ms, **base)
+             for i, (q, a) in enumerate(zip(traces, alphas))]
+    want = [H.ref_replay_log(c, max_sim_time_s=max_sim, window_s=window_s) for c in cases]
+    gkw = case_kwargs(cases[0])
+    if predicted is not None:  # the caller's predictor made the predictions; the device maps them
+        gkw["predictor"] = "oracle"
+    sch = S.GpuScheduler(case_clients(cases[0]), running=np.zeros(len(cases[0].client_names), np.int32), **gkw)
+    row_off = np.concatenate([[0], np.cumsum([len(q["client"]) for q in traces])])
+    cat = {k: np.concatenate([np.asarray(q[k]) for q in traces]) for k in ("client", "arrival", "in_tokens", "true_out")}
+    tag = np.concatenate([np.where(np.asarray(q["tag"]) < 0, 0, np.asarray(q["tag"]) + 1) for q in traces])
+    cap = max(len(w["id"]) for w in want) + 1
+    got = sch.replay(row_off, cat["client"], cat["arrival"], cat["in_tokens"], cat["true_out"], alphas,
+                     tag=tag.astype(np.uint8), ema_alpha=0.2, ev_cap=cap, max_sim_time_s=max_sim,
+                     report_window_s=window_s, duration_s=duration, prediction_overhead_ms=overhead_ms,
+                     predicted=None if predicted is None else np.concatenate(predicted), log_all=True)
+    return want, got
+
+
+def check_log(want, got):
+    for i, w in enumerate(want):
+        n = int(got["n_events"][i])
+        assert n == len(w["id"]), f"replay {i}: {n} log entries vs {len(w['id'])}"
+        for k, g in (("id", "ev_id"), ("kind", "ev_kind"), ("time", "ev_time"), ("i0", "ev_i0"), ("d0", "ev_d0"),
+                     ("d1", "ev_d1"), ("d2", "ev_d2")):
+            np.testing.assert_array_equal(got[g][i, :n], w[k], err_msg=f"replay {i} log {k}")
+        np.testing.assert_array_equal(got["profile"][i], w["profile"], err_msg=f"replay {i} profile")
+        np.testing.assert_array_equal(got["ufc"][i], w["clients"][:, 0])
+        np.testing.assert_array_equal(got["rfc"][i], w["clients"][:, 1])
+        np.testing.assert_array_equal(got["counter"][i], w["clients"][:, 2])
+        np.testing.assert_array_equal(got["clients"]["accumulated_service"][i], w["clients"][:, 3])
+        rep = got["report"][i]
+        assert rep["sim_end_s"] == w["sim_end"] and rep["busy_ms_total"] == w["busy_ms_total"]
+        assert rep["overhead_ms_total"] == w["overhead_ms_total"]
+        assert rep["max_resident_kv_tokens"] == w["max_resident_kv_tokens"]
+        assert rep["completed"] == w["completed"] and rep["rejected"] == w["rejected"]
+        assert got["counter_clamps"][i] == w["counter_clamps"]
+
+
+@pytest.mark.parametrize("over", [{}, {"kind": 1}, {"kind": 1, "vtc_use_prediction": True}, {"kind": 0},
+                                  {"backfill": True, "max_batch": 6}, {"norm_mode": 1}, {"pred_kind": 1},
+                                  {"mem_per_token_bytes": 1.0, "mem_capacity_bytes": 40000.0}])
+def test_full_event_log_matches_reference(over):
+    """log_all: arrived / admitted / first_token / completed / rejected entries with every
+    payload field, in the reference's log order, bit-exact (engine.cpp:44-76,171-375)."""
+    kw = dict(pred_kind=0)
+    kw.update(over)
+    traces = [poisson_trace(700 + s, n_clients=6, rate=250.0, duration=4.0) for s in range(3)]
+    # a 30 s horizon (Trace::duration_s) past the 4 s of arrivals: most requests complete
+    want, got = run_log(traces, [0.3, 0.7, 0.9], duration=[30.0] * 3, **kw)
+    check_log(want, got)
+    assert all((w["kind"] == 5).sum() > 25 for w in want), [(w["kind"] == 5).sum() for w in want]
+
+
+def test_duration_horizon_and_prediction_overhead():
+    """Trace::duration_s beyond the last arrival (generated scenarios, workload.cpp:213) keeps
+    the run going until then (engine.cpp:120-121); prediction_overhead_ms delays eligibility
+    (engine.cpp:165-168)."""
+    traces = [poisson_trace(800 + s, n_clients=4, rate=200.0, duration=3.0) for s in range(2)]
+    for overhead in (0.0, 7.5):
+        want, got = run_log(traces, [0.5, 0.8], duration=[6.0, 4.5], overhead_ms=overhead, pred_kind=0)
+        check_log(want, got)
+        assert all(w["sim_end"] > 3.0 for w in want)
+
+
+@pytest.mark.parametrize("n_clients", [17, 40, 300])
+def test_large_roster_replays_match_reference(n_clients):
+    """Rosters beyond 16 clients (ledger in global scratch, per-client skipped stamps) --
+    run_simulation accepts any roster (engine.cpp:154-164)."""
+    traces = [poisson_trace(900 + n_clients + s, n_clients=n_clients, rate=400.0, duration=3.0) for s in range(2)]
+    for over in ({}, {"backfill": True, "max_batch": 8}, {"kind": 1}):
+        kw = dict(pred_kind=1)
+        kw.update(over)
+        want, got = run_log(traces, [0.6, 0.75], **kw)
+        check_log(want, got)
+
+
+def test_caller_predictions_column():
+    """Predictions made by a caller's Predictor (here the reference's NoisyOraclePredictor),
+    handed over per row: the device applies max(1, .) and maps them against the evolving
+    profile, exactly as drain_arrivals does with predictor.predict (engine.cpp:177-180)."""
+    traces = [poisson_trace(1000 + s, n_clients=5, rate=250.0, duration=4.0) for s in range(2)]
+    preds = [H.ref_noisy_predict(33.0, 1, np.arange(len(q["client"]), dtype=np.int64), q["true_out"]) for q in traces]
+    want, got = run_log(traces, [0.5, 0.7], predicted=preds, pred_kind=2, noisy_l1=33.0, noisy_seed=1)
+    check_log(want, got)
