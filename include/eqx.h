@@ -269,6 +269,7 @@ typedef struct {
   double mean_service_rate;
   double ttft_p50, ttft_p90;
   int64_t ttft_count;
+  int64_t backlogged;                  /* ClientState::backlogged at the end of the run (ABI 3) */
 } eqx_replay_client;
 
 typedef struct {                     /* host arrays; any may be NULL */

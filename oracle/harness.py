@@ -527,7 +527,7 @@ def ref_replay_log(case: "StepCase", max_sim_time_s=0.0, ema_alpha=0.2, window_s
     cap = 4 * n + 4
     o = {"id": np.zeros(cap, np.int64), "kind": np.zeros(cap, np.int32), "time": np.zeros(cap),
          "i0": np.zeros(cap, np.int32), "d0": np.zeros(cap), "d1": np.zeros(cap), "d2": np.zeros(cap),
-         "profile": np.zeros((3, npf)), "clients": np.zeros((nc, 4)), "totals": np.zeros(8)}
+         "profile": np.zeros((3, npf)), "clients": np.zeros((nc, 5)), "totals": np.zeros(8)}
     err = C.create_string_buffer(512)
     f = lib.ref_replay_log
     f.argtypes = [C.POINTER(StepIn), C.c_double, C.c_double, C.c_double, C.c_int64] + [C.c_void_p] * 10 + \

@@ -989,8 +989,8 @@ extern "C" int ref_scenario_csv(const char* preset, uint64_t seed, double durati
 // kind as EQX_EV_* (admitted 1, rejected 2, arrived 3, first_token 4, completed 5), request
 // id, time and the payload fields as include/eqx.h lays them out (i0: input / predicted /
 // output tokens; d0..d2: predicted_latency_ms, or latency_s / tps / gpu_util), the profile
-// after update_map (prof[3][P]: latency_ms, gpu_util, tps), final clients (cl[C][4]: ufc,
-// rfc, counter, accumulated_service) and totals (sim_end, busy, overhead, max resident KV
+// after update_map (prof[3][P]: latency_ms, gpu_util, tps), final clients (cl[C][5]: ufc,
+// rfc, counter, accumulated_service, backlogged) and totals (sim_end, busy, overhead, max resident KV
 // tokens, completed, rejected, clamps).  Returns the number of log entries or -1.
 extern "C" int64_t ref_replay_log(const eqxo_step_in* in, double max_sim_time_s, double ema_alpha, double window_s,
                                   int64_t cap, int64_t* id, int32_t* kind, double* t, int32_t* i0, double* d0,
@@ -1077,10 +1077,11 @@ extern "C" int64_t ref_replay_log(const eqxo_step_in* in, double max_sim_time_s,
       prof[2 * P + e] = res.profile.entries[e].tps;
     }
     for (std::size_t c = 0; c < res.final_clients.size(); ++c) {
-      cl[4 * c] = res.final_clients[c].ufc;
-      cl[4 * c + 1] = res.final_clients[c].rfc;
-      cl[4 * c + 2] = res.final_clients[c].counter;
-      cl[4 * c + 3] = res.final_clients[c].accumulated_service;
+      cl[5 * c] = res.final_clients[c].ufc;
+      cl[5 * c + 1] = res.final_clients[c].rfc;
+      cl[5 * c + 2] = res.final_clients[c].counter;
+      cl[5 * c + 3] = res.final_clients[c].accumulated_service;
+      cl[5 * c + 4] = res.final_clients[c].backlogged ? 1.0 : 0.0;
     }
     tot[0] = res.sim_end_s;
     tot[1] = res.busy_ms_total;

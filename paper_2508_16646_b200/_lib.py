@@ -87,8 +87,9 @@ REPORT_FIELDS = ("max_diff", "avg_diff", "var_diff", "jain_hf", "jain_ttft_p90",
 REPORT_INT = {"ttft_count", "latency_count", "completed", "rejected", "total_completed_tokens", "n_windows", "n_diff",
               "n_rate", "max_resident_kv_tokens", "drained"}
 REPORT_DTYPE = np.dtype([(f, np.int64 if f in REPORT_INT else np.float64) for f in REPORT_FIELDS])
-CLIENT_FIELDS = ("final_hf", "accumulated_service", "mean_service_rate", "ttft_p50", "ttft_p90", "ttft_count")
-CLIENT_DTYPE = np.dtype([(f, np.int64 if f == "ttft_count" else np.float64) for f in CLIENT_FIELDS])
+CLIENT_FIELDS = ("final_hf", "accumulated_service", "mean_service_rate", "ttft_p50", "ttft_p90", "ttft_count",
+                 "backlogged")
+CLIENT_DTYPE = np.dtype([(f, np.int64 if f in ("ttft_count", "backlogged") else np.float64) for f in CLIENT_FIELDS])
 
 
 class ReplayOut(C.Structure):

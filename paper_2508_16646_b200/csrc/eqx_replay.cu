@@ -749,6 +749,7 @@ __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
         o.ttft_p50 = p50;
         o.ttft_p90 = p90;
         o.ttft_count = cnt;
+        o.backlogged = cl[c].backlogged;
       }
       if (cnt == 0) continue;
       sum = __dadd_rn(sum, p90);

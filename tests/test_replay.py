@@ -239,6 +239,7 @@ def check_log(want, got):
         np.testing.assert_array_equal(got["rfc"][i], w["clients"][:, 1])
         np.testing.assert_array_equal(got["counter"][i], w["clients"][:, 2])
         np.testing.assert_array_equal(got["clients"]["accumulated_service"][i], w["clients"][:, 3])
+        np.testing.assert_array_equal(got["clients"]["backlogged"][i], w["clients"][:, 4])
         rep = got["report"][i]
         assert rep["sim_end_s"] == w["sim_end"] and rep["busy_ms_total"] == w["busy_ms_total"]
         assert rep["overhead_ms_total"] == w["overhead_ms_total"]
