@@ -308,6 +308,106 @@ def run_sharded(args, rank, world):
         dist.destroy_process_group()
 
 
+def run_cfg4_sim(args):
+    """configs[3] at its global shape on ONE GPU: 16M queued requests over 10,000 clients as
+    `--simulate-world` ranks (2M / 1,250 each, the layout an 8-GPU box runs).  Every rank's
+    drain + scoring + exchange-record export runs on its own context, writing its slice of one
+    gathered buffer (what the NCCL all-gather delivers); the selection context then runs the
+    replicated exact selection over all 10k clients' heads.  Reported: the per-rank part (the
+    max over the simulated ranks of drain + export, device time -- on the box the ranks run in
+    parallel), the selection at 10k clients, and their sum as the simulated step (the
+    all-gather itself is not on one GPU: exchange bytes per rank are reported beside it)."""
+    import torch
+    from paper_2508_16646_b200 import scheduler as S
+    from paper_2508_16646_b200.sharded import record_bytes, _a16
+    world = args.simulate_world
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    ranks = []
+    for r in range(world):
+        q, led, names, c_r, perf, model, prof, desc = shard_inputs("cfg4", r, world)
+        ranks.append((q, names))
+    clients = [S.ClientState(nm, ufc=float(u), rfc=float(v), counter=float(c))
+               for nm, u, v, c in zip(names, led["ufc"], led["rfc"], led["counter"])]
+    kw = dict(policy=S.PolicySpec(), perf=perf, profile=prof, predictor="mope", model=model, tag_names=q["tag_names"])
+    sel = S.GpuScheduler(clients, device=0, **kw)
+    stream = torch.cuda.Stream(dev)
+    sel.set_stream(stream.cuda_stream)
+    locs, cols = [], []
+    for r, (q, _) in enumerate(ranks):
+        loc = S.GpuScheduler(clients[r * c_r:(r + 1) * c_r], device=0, **kw)
+        loc.set_stream(stream.cuda_stream)
+        with torch.cuda.stream(stream):
+            cols.append(dict(client=torch.from_numpy(q["client"]).to(dev),
+                             arrival_s=torch.from_numpy(q["arrival"]).to(dev),
+                             input_tokens=torch.from_numpy(q["in_tokens"]).to(dev),
+                             tag=torch.from_numpy(tag_ids(q)).to(dev), ids=torch.from_numpy(q["id"]).to(dev)))
+        locs.append(loc)
+    off = np.arange(world + 1, dtype=np.int32) * c_r
+    with torch.cuda.stream(stream):
+        flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    torch.cuda.synchronize()
+    sel.set_batch(0, 0)
+    sel.checkpoint()
+    W = 8  # ShardedScheduler's default head-window depth (grown 4x on an underflow)
+
+    def step(W):
+        stride = _a16(record_bytes(c_r, W))
+        with torch.cuda.stream(stream):
+            recv = torch.empty(world * stride, dtype=torch.uint8, device=dev)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * world + 2)]
+        with torch.cuda.stream(stream):
+            sel.restore_async()
+            flush.zero_()
+            for r, loc in enumerate(locs):
+                ev[2 * r].record(stream)
+                loc.drain(**cols[r])
+                loc.shard_export_async(1.0, c_r, W, recv[r * stride:(r + 1) * stride])
+                ev[2 * r + 1].record(stream)
+            ev[2 * world].record(stream)
+            sel.shard_select_async(recv, world, stride, off, c_r, W, 1.0)
+            ev[2 * world + 1].record(stream)
+        return ev, recv
+
+    while True:
+        step(W)
+        res = sel.collect(with_events=False)
+        if not res.window_underflow:
+            break
+        W *= 4
+    for _ in range(args.warmup):
+        step(W)
+    torch.cuda.synchronize()
+    recs = [step(W) for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    res = sel.collect(with_events=False)
+    assert not res.window_underflow
+    rank_ms = np.array([[e[2 * r].elapsed_time(e[2 * r + 1]) for r in range(world)] for e, _ in recs])
+    sel_ms = np.array([e[2 * world].elapsed_time(e[2 * world + 1]) for e, _ in recs])
+    per_rank = rank_ms.max(axis=1)
+    step_ms = per_rank + sel_ms
+    n = sum(len(q["client"]) for q, _ in ranks)
+    rec = record_bytes(c_r, W)
+    line = {
+        "metric": "requests scored+scheduled/sec", "value": n / (float(np.median(step_ms)) * 1e-3), "unit": "requests/s",
+        "n_gpus": 1, "simulated_world": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": float(np.mean(step_ms)), "p50_ms": float(np.median(step_ms)),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"cfg4 global shape simulated on one GPU: {n} queued requests, {c_r * world} clients, "
+                               f"{world} ranks x ({n // world} requests / {c_r} clients), warm ledger, max_batch 64",
+                   "policy": "equinox (alpha 0.7, delta 0.1, max_over_clients)",
+                   "l2": "flushed between steps (256 MiB memset outside the events)"},
+        "breakdown_ms": {"rank_drain_export_max_p50": float(np.median(per_rank)),
+                         "rank_drain_export_mean_p50": float(np.median(rank_ms.mean(axis=1))),
+                         "select_10k_p50": float(np.median(sel_ms))},
+        "admitted": res.n_admitted, "window": W, "exchange_bytes_per_rank": rec,
+        "allgather_bytes_total": rec * world,
+        "note": "step = max over simulated ranks of (drain + score + export) + replicated selection; the NCCL "
+                "all-gather of exchange_bytes_per_rank per rank is not part of a one-GPU simulation",
+    }
+    print(json.dumps(line), flush=True)
+
+
 def preset_traces(n_replays: int, duration: float, seed0: int = 1):
     """The reference's poisson preset (workload.cpp:254-260: client1 Poisson 16/s, 512 in / 32
     out; client2 Poisson 3/s, 32 in / 512 out), one seeded trace per replay, concatenated."""
@@ -449,6 +549,8 @@ def run_cfg5(args, rank, world):
 def run_ours(args, rank, world):
     if args.config == "cfg5":
         return run_cfg5(args, rank, world)
+    if args.config == "cfg4" and args.simulate_world > 1 and world == 1:
+        return run_cfg4_sim(args)
     if world > 1 or args.sharded or args.config == "cfg4":
         return run_sharded(args, rank, world)
     import torch
@@ -649,6 +751,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--sharded", action="store_true", help="client-sharded pipeline even at N=1")
+    ap.add_argument("--simulate-world", type=int, default=0,
+                    help="cfg4 on one GPU: simulate this many ranks of the global 16M / 10k-client step")
     ap.add_argument("--cpu-reps", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no e2e / cpu legs")

@@ -2216,6 +2216,7 @@ eqx_status eqx_phase_times(eqx_ctx* ctx, double* out_us, int32_t n) {
     out_us[25] = (static_cast<double>(t[12]) - static_cast<double>(dt[0])) * 1e-3;
     out_us[26] = (static_cast<double>(dt[7]) - static_cast<double>(dt[0])) * 1e-3;
   }
+  for (int i = 27; i < n && i < 35; ++i) out_us[i] = static_cast<double>(ctx->h_state->tk[i - 27]);  // raw counters
   return EQX_OK;
 }
 

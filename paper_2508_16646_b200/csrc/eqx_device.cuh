@@ -69,6 +69,7 @@ struct DevState {
   // epilogue end, rank start (min) / walk end (max) / epilogue end
   unsigned long long dt[8];
   int64_t clamps;          // SchedulerPolicy::counter_clamps() (on_complete clamps at 0)
+  unsigned long long tk[8];  // EQX_PROF builds: top-K selection sub-phase cycles / pass counts
 };
 
 // Order-preserving map double -> uint64 (IEEE total order on non-NaN values, with -0.0 and

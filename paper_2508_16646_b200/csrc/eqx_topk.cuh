@@ -66,6 +66,7 @@ enum : uint32_t { kTkValid = 16 };
 struct TopkShared {
   unsigned long long orv[3], andv[3];
   int32_t nvalid, nsel, nslot, bin, below, inbin, stop, fn, fs;
+  int32_t passes;  // EQX_PROF: radix passes
   int32_t wm[32];
   long long wr[32], wp[32];
 };
@@ -177,6 +178,9 @@ __device__ void topk_radix_select(const V& v, int32_t need, uint32_t* hist, Topk
     }
     const int lo = hi >= 7 ? hi - 7 : 0;
     const uint32_t mask = (1u << (hi - lo + 1)) - 1u;
+#ifdef EQX_PROF
+    if (tid == 0) ++X.passes;
+#endif
     for (int i = tid; i < 256; i += NT) hist[i] = 0;
     if (tid == 0) {
       X.orv[par] = 0;
@@ -306,8 +310,9 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
   const int32_t want = P.backfill ? T.Kcap : max(32, min(T.Kcap, P.max_batch - S.members + 8));
   int32_t K = min(want, 128);
 #ifdef EQX_PROF
-  unsigned long long rounds = 0, cy[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  long long t0 = clock64(), t1;
+  unsigned long long n_total_items = 0;
+  unsigned long long rounds = 0, cy[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tk[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long t0 = clock64(), t1, tk_t1;
 #define TK_STAMP(i) \
   t1 = clock64();   \
   cy[i] += t1 - t0; \
@@ -345,7 +350,16 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
       __syncthreads();
       const int32_t ncand = X.nvalid;
       if (ncand == 0) break;  // no candidates (engine.cpp:217)
+#ifdef EQX_PROF
+      if (tid == 0) X.passes = 0;
+      tk_t1 = clock64();
+      tk[0] += tk_t1 - t0;
+#endif
       if (ncand > K) topk_radix_select(HeadView{T, cw, C}, K, T.hist, X);
+#ifdef EQX_PROF
+      tk[1] += clock64() - tk_t1;
+      tk[2] += X.passes;
+#endif
       for (int32_t c = tid; c < C; c += NT)
         if (T.hst[c] == (ncand > K ? 2 : 1)) T.sc[atomicAdd(&X.nslot, 1)] = c;
       __syncthreads();
@@ -418,6 +432,9 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
       n = X.nvalid;
       __syncthreads();
       if (tid == 0) X.nvalid = 0;
+#ifdef EQX_PROF
+      n_total_items += n;
+#endif
     }
     {  // 1c. head entries: a warp moves 32 consecutive items (mostly one client's contiguous
        //     window run) as 160 coalesced 64-bit words through shared memory
@@ -569,7 +586,14 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
     const int32_t ks = min(nvalid, K);
     const ItemView iv{T, cw, n};
     if (ks < nvalid) {
+#ifdef EQX_PROF
+      if (tid == 0) X.passes = 0;
+#endif
       topk_radix_select(iv, ks, T.hist, X);
+#ifdef EQX_PROF
+      tk[3] += X.passes;
+      tk[4] += 1;
+#endif
     } else {
       for (int64_t x = tid; x < n; x += NT)
         if (T.st[x] == 1) T.st[x] = 2;
@@ -790,6 +814,8 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
   if (tid == 0) {
     a.st->t[7] = rounds;
     for (int i = 0; i < 8; ++i) a.st->t[8 + i] = cy[i];
+    tk[5] = n_total_items;
+    for (int i = 0; i < 8; ++i) a.st->tk[i] = tk[i];
   }
 #endif
 #undef TK_STAMP

@@ -14,7 +14,7 @@ sch.set_batch(0, 0); sch.checkpoint()
 for i in range(3):
     sch.restore_async(); torch.cuda.synchronize()
     sch.drain(**cols); sch.step_async(1.0); r = sch.collect(with_events=False)
-    out = (C.c_double * 22)()
-    L.load().eqx_phase_times(sch._ctx, out, 22)
+    out = (C.c_double * 35)()
+    L.load().eqx_phase_times(sch._ctx, out, 35)
     print(cfg, "admitted", r.n_admitted, "loop us", round(out[3] - out[2], 1) if out[3] else None,
-          "rounds", out[7], "cycles heads/gather/chain/keys/select/rank/scan/seq", [int(x) for x in out[8:16]])
+          "rounds", out[7], "cycles heads/gather/chain/keys/select/rank/scan/seq", [int(x) for x in out[8:16]], "head loads, head radix, head passes, item passes, item selects, items", [int(x) for x in out[27:33]])
