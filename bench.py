@@ -382,6 +382,14 @@ def run_cfg4_sim(args):
     torch.cuda.synchronize()
     res = sel.collect(with_events=False)
     assert not res.window_underflow
+    if os.environ.get("EQX_TOPK_PROF"):  # instrumented library: the selection's round counters
+        import ctypes as C
+        from paper_2508_16646_b200 import _lib as L
+        out = (C.c_double * 35)()
+        L.load().eqx_phase_times(sel._ctx, out, 35)
+        print("phase us (windows filled, loop start, loop end)", [round(x, 1) for x in out[1:4]], "rounds", out[7], "cycles heads/gather/chain/keys/select/rank/scan/seq", [int(x) for x in out[8:16]],
+              "head loads, head radix, head passes, item passes, item selects, items", [int(x) for x in out[27:33]],
+              flush=True)
     rank_ms = np.array([[e[2 * r].elapsed_time(e[2 * r + 1]) for r in range(world)] for e, _ in recs])
     sel_ms = np.array([e[2 * world].elapsed_time(e[2 * world + 1]) for e, _ in recs])
     per_rank = rank_ms.max(axis=1)
@@ -632,8 +640,12 @@ def run_ours(args, rank, world):
     # max(H2D, compute) -- what a serving loop pays.  Three rotating pinned host batches (same
     # content, in the library's huge-page arena) keep the copies distinct.
     from paper_2508_16646_b200 import scheduler as S
+    # client and input_tokens travel as uint16 when they fit (eqx_requests::narrow, checked here:
+    # 64 / 1000 clients, inputs <= 1024 tokens): 13 B per request over PCIe instead of 17
+    narrow = len(q["client_names"]) <= 65536 and int(q["in_tokens"].max()) < 65536 and int(q["in_tokens"].min()) >= 0
+    cdt = np.uint16 if narrow else np.int32
     hosts = [{k: S.pinned_copy(v) for k, v in
-              dict(client=q["client"], arrival_s=q["arrival"], input_tokens=q["in_tokens"],
+              dict(client=q["client"].astype(cdt), arrival_s=q["arrival"], input_tokens=q["in_tokens"].astype(cdt),
                    tag=tag_ids(q)).items()} for _ in range(3)]
     e2e_steps = 0 if args.profile else max(8, args.steps)
     d2h = 0
@@ -722,7 +734,8 @@ def run_ours(args, rank, world):
                 "passes": 3,
                 "single_step_latency_ms": single_ms,
                 "h2d_gbs": (h2d / (e2e_step_ms * 1e-3) / 1e9) if e2e_step_ms else None,
-                "bound": "pcie h2d (17 B/request; ~54.5 GB/s measured pinned H2D on the box, tools/pin_probe.py)",
+                "bound": f"pcie h2d ({h2d / n:.0f} B/request{': uint16 client + input_tokens columns' if narrow else ''}; "
+                         "~54.5 GB/s measured pinned H2D on the box, tools/pin_probe.py)",
                 "note": "wall clock over consecutive steps; the H2D of steps i+1, i+2 (copy stream) "
                         "overlaps step i"},
         # per step: drain_hist, drain_rank, window, score, select, event_fill, pack_cols (state copy)

@@ -119,6 +119,11 @@ typedef struct {
   const int32_t* true_output_tokens; /* ORACLE / NOISY_ORACLE only; may be NULL otherwise */
   const uint8_t* tag;             /* category_tag as a tag id (see eqx_mope.tag_row) */
   int32_t location;               /* EQX_HOST / EQX_DEVICE */
+  int32_t narrow;                 /* ABI 3, EQX_HOST batches of eqx_stage_async / eqx_drain only: 1 =
+                                     client and input_tokens point to uint16_t arrays (rosters up
+                                     to 65536 clients, inputs below 65536 tokens -- the caller's
+                                     lossless choice): 13 instead of 17 bytes per request cross
+                                     PCIe; the copy stream widens them on the device */
 } eqx_requests;
 
 typedef struct {

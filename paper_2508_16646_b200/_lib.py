@@ -53,7 +53,8 @@ class Predictor(C.Structure):
 class Requests(C.Structure):
     _fields_ = [("n", C.c_int64), ("id", C.c_void_p), ("id_base", C.c_int64),
                 ("client", C.c_void_p), ("arrival_s", C.c_void_p), ("input_tokens", C.c_void_p),
-                ("true_output_tokens", C.c_void_p), ("tag", C.c_void_p), ("location", C.c_int32)]
+                ("true_output_tokens", C.c_void_p), ("tag", C.c_void_p), ("location", C.c_int32),
+                ("narrow", C.c_int32)]
 
 
 class StepSummary(C.Structure):

@@ -91,8 +91,9 @@ struct eqx_ctx {
   // step.  `free_` is recorded on the main stream after the last launch that reads a set.
   static constexpr int kStages = 3;
   struct Stage {
-    DevBuf client, arrival, in, tru, tag, id;
+    DevBuf client, arrival, in, tru, tag, id, c16, i16;
     const void* key[6] = {};
+    int32_t narrow = 0;
     int64_t n = -1;
     uint64_t seq = 0;  // staging order: a drain consumes the oldest matching staged batch
     bool valid = false;
@@ -791,14 +792,28 @@ static eqx_status stage_fill(eqx_ctx* ctx, const eqx_requests* r, int b) {
   CUDA_TRY(ctx, st.tag.ensure(nn + 16));
   if (r->true_output_tokens) CUDA_TRY(ctx, st.tru.ensure(4 * nn));
   if (r->id) CUDA_TRY(ctx, st.id.ensure(8 * nn));
+  if (r->narrow) {
+    CUDA_TRY(ctx, st.c16.ensure(2 * nn + 16));
+    CUDA_TRY(ctx, st.i16.ensure(2 * nn + 16));
+  }
   CUDA_TRY(ctx, cudaStreamWaitEvent(cs, st.free_, 0));
   auto h2d = [&](void* dst, const void* src, size_t bytes) {
     return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, cs);
   };
-  if (n > 0) {
+  if (n > 0 && r->narrow) {  // 2-byte client / input columns over PCIe, widened on the device
+    CUDA_TRY(ctx, h2d(st.c16.p, r->client, 2 * n));
+    CUDA_TRY(ctx, h2d(st.arrival.p, r->arrival_s, 8 * n));
+    CUDA_TRY(ctx, h2d(st.i16.p, r->input_tokens, 2 * n));
+    const int blocks = static_cast<int>(std::min<int64_t>((n / 8 + 255) / 256 + 1, 4ll * ctx->sm_count));
+    widen_cols_kernel<<<blocks, 256, 0, cs>>>(st.c16.as<uint16_t>(), st.i16.as<uint16_t>(), n, st.client.as<int32_t>(),
+                                              st.in.as<int32_t>());
+    CUDA_TRY(ctx, cudaGetLastError());
+  } else if (n > 0) {
     CUDA_TRY(ctx, h2d(st.client.p, r->client, 4 * n));
     CUDA_TRY(ctx, h2d(st.arrival.p, r->arrival_s, 8 * n));
     CUDA_TRY(ctx, h2d(st.in.p, r->input_tokens, 4 * n));
+  }
+  if (n > 0) {
     if (r->tag) CUDA_TRY(ctx, h2d(st.tag.p, r->tag, n));
     else CUDA_TRY(ctx, cudaMemsetAsync(st.tag.p, 0, n, cs));
     if (r->true_output_tokens) CUDA_TRY(ctx, h2d(st.tru.p, r->true_output_tokens, 4 * n));
@@ -807,6 +822,7 @@ static eqx_status stage_fill(eqx_ctx* ctx, const eqx_requests* r, int b) {
   CUDA_TRY(ctx, cudaEventRecord(st.ready, cs));
   const void* key[6] = {r->client, r->arrival_s, r->input_tokens, r->tag, r->true_output_tokens, r->id};
   std::memcpy(st.key, key, sizeof(key));
+  st.narrow = r->narrow;
   st.n = n;
   st.seq = ++ctx->stage_seq;
   st.valid = true;
@@ -831,7 +847,7 @@ static int stage_target(const eqx_ctx* ctx) {
 
 static bool stage_matches(const eqx_ctx::Stage& st, const eqx_requests* r) {
   const void* key[6] = {r->client, r->arrival_s, r->input_tokens, r->tag, r->true_output_tokens, r->id};
-  return st.valid && st.n == r->n && std::memcmp(st.key, key, sizeof(key)) == 0;
+  return st.valid && st.n == r->n && st.narrow == r->narrow && std::memcmp(st.key, key, sizeof(key)) == 0;
 }
 
 // The main stream is done with the bound staging set once everything enqueued so far ran.
@@ -843,6 +859,8 @@ static eqx_status release_stage(eqx_ctx* ctx) {
 eqx_status eqx_stage_async(eqx_ctx* ctx, const eqx_requests* r) {
   if (!ctx || !r) return fail(ctx, EQX_ERR_ARG, "eqx_stage_async: NULL argument");
   if (r->location != EQX_HOST) return fail(ctx, EQX_ERR_ARG, "eqx_stage_async: only host batches are staged");
+  if (r->narrow && (reinterpret_cast<uintptr_t>(r->client) & 1 || reinterpret_cast<uintptr_t>(r->input_tokens) & 1))
+    return fail(ctx, EQX_ERR_ARG, "eqx_stage_async: narrow columns must be 2-byte aligned");
   if (r->n < 0 || r->n >= (int64_t(1) << 31) - 1) return fail(ctx, EQX_ERR_ARG, "eqx_stage_async: n out of range");
   if (r->n > 0 && (!r->client || !r->arrival_s || !r->input_tokens))
     return fail(ctx, EQX_ERR_ARG, "eqx_stage_async: missing request column");
@@ -861,6 +879,8 @@ static eqx_status drain_prepare(eqx_ctx* ctx, const eqx_requests* r) {
   const bool needs_true = ctx->model.pred_kind == kPredOracle || ctx->model.pred_kind == kPredNoisy;
   if (n > 0 && (!r->client || !r->arrival_s || !r->input_tokens || (needs_true && !r->true_output_tokens)))
     return fail(ctx, EQX_ERR_ARG, "eqx_drain: missing request column");
+  if (r->narrow && r->location == EQX_DEVICE)
+    return fail(ctx, EQX_ERR_ARG, "eqx_drain: narrow (uint16) columns are for host batches only");
   cudaSetDevice(ctx->device);
   cudaStream_t s = ctx->stream;
   const size_t nn = static_cast<size_t>(std::max<int64_t>(n, 1));
@@ -1775,6 +1795,7 @@ eqx_status eqx_append(eqx_ctx* ctx, const eqx_requests* r) {
     return fail(ctx, EQX_ERR_CONFIG, "eqx_append: the context holds a queue from eqx_drain (which replaces queues)");
   const int64_t m = r->n;
   if (m < 0) return fail(ctx, EQX_ERR_ARG, "eqx_append: negative batch size");
+  if (r->narrow) return fail(ctx, EQX_ERR_ARG, "eqx_append: narrow (uint16) columns are for eqx_stage_async / eqx_drain");
   const int32_t C = ctx->C;
   if (m > 0 && C == 0) return fail(ctx, EQX_ERR_CONFIG, "eqx_append: requests but no clients");
   const bool needs_true = ctx->model.pred_kind == kPredOracle || ctx->model.pred_kind == kPredNoisy;

@@ -3018,6 +3018,32 @@ __global__ void gather_ids_kernel(const int32_t* __restrict__ rows, int64_t n, c
 }
 
 // Columns -> mapped host memory by SM stores over PCIe (16-byte words when aligned).
+// Staged narrow host columns widened in place of the H2D's second half: 8 rows per thread,
+// 16-byte loads of each u16 column, 2 x 16-byte stores per i32 column.
+__global__ void widen_cols_kernel(const uint16_t* c16, const uint16_t* i16, int64_t n, int32_t* c32, int32_t* i32) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t groups = n / 8;
+  for (int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < groups; g += stride) {
+    const uint4 a = reinterpret_cast<const uint4*>(c16)[g];
+    const uint4 b = reinterpret_cast<const uint4*>(i16)[g];
+    const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, bw[4] = {b.x, b.y, b.z, b.w};
+    int4 o[4];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      o[k] = make_int4(aw[2 * k] & 0xffff, aw[2 * k] >> 16, aw[2 * k + 1] & 0xffff, aw[2 * k + 1] >> 16);
+      o[2 + k] = make_int4(bw[2 * k] & 0xffff, bw[2 * k] >> 16, bw[2 * k + 1] & 0xffff, bw[2 * k + 1] >> 16);
+    }
+    reinterpret_cast<int4*>(c32)[2 * g] = o[0];
+    reinterpret_cast<int4*>(c32)[2 * g + 1] = o[1];
+    reinterpret_cast<int4*>(i32)[2 * g] = o[2];
+    reinterpret_cast<int4*>(i32)[2 * g + 1] = o[3];
+  }
+  for (int64_t r = 8 * groups + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < n; r += stride) {
+    c32[r] = c16[r];
+    i32[r] = i16[r];
+  }
+}
+
 __global__ void pack_cols_kernel(const PackCols p) {
   pdl_wait();  // no-op unless launched programmatically after the kernel producing the columns
   pdl_trigger();

@@ -65,8 +65,10 @@ enum : uint32_t { kTkValid = 16 };
 
 struct TopkShared {
   unsigned long long orv[3], andv[3];
-  int32_t nvalid, nsel, nslot, bin, below, inbin, stop, fn, fs;
+  int32_t nvalid, nsel, nslot, bin, below, inbin, stop, fn, fs, fb;
   int32_t passes;  // EQX_PROF: radix passes
+  unsigned long long bk, ba, bo;                 // the boundary tuple (continuation rounds)
+  unsigned long long wbk[32], wba[32], wbo[32];  // its per-warp minima
   int32_t wm[32];
   long long wr[32], wp[32];
 };
@@ -298,7 +300,7 @@ __device__ __forceinline__ void topk_scan(int32_t m, long long rv, long long pv,
 __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTables& M, const ClientWork& cw, SelShared& S,
                             const TopkScratch& T) {
   __shared__ TopkShared X;
-  const int tid = threadIdx.x, NT = blockDim.x;
+  const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31;
   const int32_t C = a.C;
   const Policy P = a.pol;
   const bool maxmode = P.kind == kEquinox && P.norm_mode == 0;
@@ -321,6 +323,15 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
 #define TK_STAMP(i)
 #endif
   __syncthreads();
+  // A round either regenerates the key streams (regen) or continues over the items generated
+  // earlier: those stay valid -- a client's ledger chain depends only on its own admissions --
+  // and only their keys, which move with the maxima, are recomputed.  A continuation stops at
+  // the smallest head of a client outside the slot set (the boundary B), at a stream that ran
+  // out, or when no item is left; the next round then regenerates.
+  bool regen = true;      // block-uniform
+  bool all_slots = true;  // the slots hold every candidate client (no boundary)
+  int64_t n = 0;          // items of the current streams
+  int32_t nslot = 0;
   for (;;) {
     const double mu = S.max_u, mr = S.max_r;
     if (tid == 0) {
@@ -330,10 +341,13 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
       X.stop = 0;
       X.fn = 0x7fffffff;
       X.fs = 0x7fffffff;
+      X.fb = 0x7fffffff;
     }
     __syncthreads();
+    if (regen) {
     // ---- 0. slots: every client, or the K clients with the smallest heads ----
-    int32_t nslot = C;
+    nslot = C;
+    all_slots = true;
     if (big) {
       int32_t nc = 0;
       for (int32_t c = tid; c < C; c += NT) {
@@ -356,6 +370,7 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
       tk[0] += tk_t1 - t0;
 #endif
       if (ncand > K) topk_radix_select(HeadView{T, cw, C}, K, T.hist, X);
+      all_slots = ncand <= K;
 #ifdef EQX_PROF
       tk[1] += clock64() - tk_t1;
       tk[2] += X.passes;
@@ -407,7 +422,6 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
       }
       __syncthreads();
     }
-    int64_t n;
     {
       const int32_t room = T.cap - nslot;  // one item per slot, the rest shared out
       int32_t extra = 0;
@@ -482,6 +496,7 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
             f = kTkValid | (e.alone ? kFlAlone : 0);
           }
           T.fl[li] = f;
+          T.st[li] = 0;
         }
         __syncwarp();
       }
@@ -551,11 +566,6 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
             T.u[x] = ub;
             T.r[x] = rb;
             T.cn[x] = cb;
-            if (pos + d + 1 == end) {
-              if (maxmode && (ub == mu || rb == mr)) f |= kFlHolder;  // a max holder leaves the backlog
-            } else if ((f & kFlAlone) && maxmode && (mu < __dadd_rn(ub, iu) || mr < __dadd_rn(rb, ir))) {
-              f |= kFlMaxChg;  // this admission raises a maximum
-            }
             if (d + 1 == nd && pos + nd < end) f |= kFlExh;  // later items were not generated
             T.fl[x] = f;
           }
@@ -567,21 +577,74 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
     }
     __syncthreads();
     TK_STAMP(2)
+    }  // regen
+    // ---- keys of the items still in play (unconsumed, client not skipped) under the maxima ----
     {
       int32_t nv = 0;
       for (int64_t x = tid; x < n; x += NT) {
-        const bool v = T.fl[x] & kTkValid;
+        const uint8_t st = T.st[x];
+        bool v = (T.fl[x] & kTkValid) && st != 3;
+        if (v && P.backfill) v = !(cw.flags[T.sc[T.sd[x] >> 8]] & kSkipped);
         if (v) T.k[x] = ordered_bits(hf_key(P, T.u[x], T.r[x], mu, mr, T.cn[x]));
-        T.st[x] = v ? 1 : 0;
+        T.st[x] = v ? 1 : (st == 3 ? 3 : 0);
         nv += v;
       }
       nv = __reduce_add_sync(0xffffffffu, nv);
       if ((tid & 31) == 0 && nv) atomicAdd(&X.nvalid, nv);
     }
+    // ---- continuation with clients outside the slots: their smallest head is the boundary ----
+    const bool bounded = !regen && !all_slots;
+    if (bounded) {
+      uint64_t bk = ~0ull, ba = ~0ull, bo = ~0ull;
+      for (int32_t c = tid; c < C; c += NT) {
+        if (T.hst[c] == 2 || cw.pos[c] >= cw.end[c] || (cw.flags[c] & kSkipped)) continue;
+        const uint64_t k = ordered_bits(hf_key(P, cw.ufc[c], cw.rfc[c], mu, mr, cw.cnt[c]));
+        const uint64_t av = T.ha[c], o = static_cast<uint64_t>(cw.order[c]) << 32;
+        if (k < bk || (k == bk && (av < ba || (av == ba && o < bo)))) {
+          bk = k;
+          ba = av;
+          bo = o;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const uint64_t k2 = __shfl_xor_sync(0xffffffffu, bk, o), a2 = __shfl_xor_sync(0xffffffffu, ba, o),
+                       o2 = __shfl_xor_sync(0xffffffffu, bo, o);
+        if (k2 < bk || (k2 == bk && (a2 < ba || (a2 == ba && o2 < bo)))) {
+          bk = k2;
+          ba = a2;
+          bo = o2;
+        }
+      }
+      if (lane == 0) {
+        X.wbk[tid >> 5] = bk;
+        X.wba[tid >> 5] = ba;
+        X.wbo[tid >> 5] = bo;
+      }
+    }
     __syncthreads();
+    if (bounded && tid == 0) {
+      uint64_t bk = X.wbk[0], ba = X.wba[0], bo = X.wbo[0];
+      for (int w = 1; w < (NT >> 5); ++w) {
+        const uint64_t k2 = X.wbk[w], a2 = X.wba[w], o2 = X.wbo[w];
+        if (k2 < bk || (k2 == bk && (a2 < ba || (a2 == ba && o2 < bo)))) {
+          bk = k2;
+          ba = a2;
+          bo = o2;
+        }
+      }
+      X.bk = bk;
+      X.ba = ba;
+      X.bo = bo;
+    }
     const int32_t nvalid = X.nvalid;
     TK_STAMP(3)
-    if (nvalid == 0) break;  // no candidates (engine.cpp:217)
+    if (nvalid == 0) {  // no candidates (engine.cpp:217) -- or none left in the generated streams
+      if (regen) break;
+      regen = true;
+      __syncthreads();
+      continue;
+    }
     // ---- 2. the K smallest tuples ----
     const int32_t ks = min(nvalid, K);
     const ItemView iv{T, cw, n};
@@ -625,12 +688,17 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
         if (rk) atomicAdd(&T.rank[i], rk);
       }
       __syncthreads();
+      const uint64_t bk = X.bk, ba = X.ba, bo = X.bo;
       for (int32_t i = tid; i < ns; i += NT) {
         const int32_t x = T.gx[i], rk = T.rank[i];
         T.srt[rk] = x;
         const uint32_t sdv = T.sd[x];
-        const int32_t c = T.sc[sdv >> 8];
-        T.ent[rk] = topk_entry(a, M, cw, c, cw.pos[c] + static_cast<int32_t>(sdv & 255u));
+        const int32_t s = static_cast<int32_t>(sdv >> 8);
+        T.ent[rk] = topk_entry(a, M, cw, T.sc[s], T.spos[s] + static_cast<int32_t>(sdv & 255u));
+        if (bounded) {  // items past the boundary wait for a regenerating round
+          const uint64_t k = T.gk[i], av = T.ga[i], o = T.go[i];
+          if (!(k < bk || (k == bk && (av < ba || (av == ba && o < bo))))) atomicMin(&X.fb, rk);
+        }
       }
       __syncthreads();
     }
@@ -640,17 +708,29 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
     //     or ends the round
     const int32_t members0 = S.members;
     const int64_t reserved0 = S.reserved;
+    const int32_t nse = min(ns, X.fb);  // the ranked items below the boundary
     {
       int32_t m = 0;
       long long rv = 0, pv = 0;
       bool alone = false, flag = false;
-      if (tid < ns) {
+      if (tid < nse) {
         const int32_t x = T.srt[tid];
-        const int32_t c = T.sc[T.sd[x] >> 8], d = static_cast<int32_t>(T.sd[x] & 255u);
+        const int32_t s = static_cast<int32_t>(T.sd[x] >> 8), c = T.sc[s], d = static_cast<int32_t>(T.sd[x] & 255u);
         const WinEntry& e = T.ent[tid];
-        const uint8_t f = T.fl[x];
-        const bool last = cw.pos[c] + d + 1 == cw.end[c];
+        uint8_t f = T.fl[x] & ~(kFlMaxChg | kFlHolder);
+        const bool last = T.spos[s] + d + 1 == cw.end[c];
         alone = e.alone;
+        // the maxima-dependent outcomes under the current maxima: a max holder leaving the
+        // backlog with its last request, an admission raising a maximum
+        if (maxmode) {
+          const double ub = T.u[x], rb = T.r[x];
+          if (last) {
+            if (ub == mu || rb == mr) f |= kFlHolder;
+          } else if (alone && (mu < __dadd_rn(ub, e.ufc_inc) || mr < __dadd_rn(rb, e.rfc_inc))) {
+            f |= kFlMaxChg;
+          }
+        }
+        T.fl[x] = f;
         m = alone ? 1 : 0;
         rv = alone ? static_cast<long long>(e.in) + e.pred : 0;
         pv = alone ? e.in : 0;
@@ -659,14 +739,14 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
       int32_t mx;
       long long rx, px;
       topk_scan(m, rv, pv, mx, rx, px, X);
-      if (tid < ns) {
+      if (tid < nse) {
         const bool nofit = alone && !((members0 + mx + 1 <= P.max_batch) && (reserved0 + rx + rv <= tmax));
         if (nofit) atomicMin(&X.fn, tid);
         if (flag) atomicMin(&X.fs, tid);
       }
       __syncthreads();
       const int32_t fn = X.fn, fs = X.fs;
-      const int32_t cend = fn <= fs ? min(fn, ns) : fs + 1;  // items [0, cend) are consumed
+      const int32_t cend = fn <= fs ? min(fn, nse) : fs + 1;  // items [0, cend) are consumed
       // 4b. commit: events, admissions, per-client ledgers after the client's last consumed item
       if (tid < cend) {
         const int32_t x = T.srt[tid];
@@ -704,21 +784,24 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
           cw.ufc[c] = nu;
           cw.rfc[c] = nr;
           cw.cnt[c] = ncn;
-          const int32_t np = cw.pos[c] + d + 1;
+          const int32_t np = T.spos[s] + d + 1;
           if (np == cw.end[c]) cw.flags[c] &= ~kBacklogged;  // pop_head emptied the queue
           cw.pos[c] = np;
           if (tid == fs && fs < fn) {  // the item that ends the round
             const uint8_t f = T.fl[x];
             if (np == cw.end[c]) {
               if (f & kFlHolder) X.stop = 4;  // maxima need a rescan
-            } else if (alone && (f & kFlMaxChg)) {
-              if (S.max_u < nu) S.max_u = nu;
-              if (S.max_r < nr) S.max_r = nr;
+            } else {
+              if (alone && (f & kFlMaxChg)) {
+                if (S.max_u < nu) S.max_u = nu;
+                if (S.max_r < nr) S.max_r = nr;
+              }
+              if (f & kFlExh) X.stop = 16;  // the client's stream ran out: regenerate
             }
           }
         }
       }
-      if (tid == 0 && fn < ns && fn <= fs) {
+      if (tid == 0 && fn < nse && fn <= fs) {
         if (!P.backfill) X.stop = 2;  // engine.cpp:239: the head does not fit, the step is over
         else X.stop = 8;              // backfill: skip its client, continue item by item
       }
@@ -731,7 +814,7 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
       int32_t members = S.members;
       int64_t reserved = S.reserved, n_ev = S.n_ev, n_adm = S.n_adm, n_rej = S.n_rej, prefill = S.prefill;
       double max_u = S.max_u, max_r = S.max_r;
-      for (int32_t i = X.fn; i < ns && !stop; ++i) {
+      for (int32_t i = X.fn; i < nse && !stop; ++i) {
         const int32_t x = T.srt[i];
         const int32_t c = T.sc[T.sd[x] >> 8];
         const int32_t fc = cw.flags[c];
@@ -748,12 +831,13 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
           }
           ++n_ev;
           ++n_rej;
+          T.st[x] = 3;
           cw.pos[c] = j + 1;
           if (last) {
             cw.flags[c] = fc & ~kBacklogged;
             if (fl & kFlHolder) stop = 4;
           } else if (fl & kFlExh) {
-            stop = 1;
+            stop = 16;
           }
           continue;
         }
@@ -776,16 +860,18 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
         }
         ++n_ev;
         ++n_adm;
+        T.st[x] = 3;
         cw.pos[c] = j + 1;
         if (last) {
           cw.flags[c] = fc & ~kBacklogged;
           if (fl & kFlHolder) stop = 4;
-        } else if (fl & kFlMaxChg) {
-          if (max_u < nu) max_u = nu;
-          if (max_r < nr) max_r = nr;
-          stop = 1;
-        } else if (fl & kFlExh) {
-          stop = 1;
+        } else {
+          if (fl & kFlMaxChg) {
+            if (max_u < nu) max_u = nu;
+            if (max_r < nr) max_r = nr;
+            stop = 1;
+          }
+          if (fl & kFlExh) stop = 16;
         }
       }
       S.members = members;
@@ -796,18 +882,21 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
       S.prefill = prefill;
       S.max_u = max_u;
       S.max_r = max_r;
-      X.stop = stop;
+      X.stop = stop | (stop ? 0 : 32);  // 32: the walk reached the end of the list
     }
     __syncthreads();
     TK_STAMP(7)
 #ifdef EQX_PROF
     ++rounds;
 #endif
-    const int32_t stop = X.stop, consumed = X.fn <= X.fs ? min(X.fn, ns) : X.fs + 1;
+    const int32_t stop = X.stop, consumed = X.fn <= X.fs ? min(X.fn, nse) : X.fs + 1;
     if (stop == 2) break;
     if (stop & 4) cta_maxima(cw, C, S);  // max over the backlogged clients (scheduler.cpp:40-48)
+    const bool ran_out = (stop & 32) || (X.fn >= nse && X.fs >= nse);
+    // regenerate when a stream ran out, or when the walk reached the boundary
+    regen = (stop & 16) || (ran_out && nse < ns);
     // next K: double it when the list ran out, else about twice what this round consumed
-    K = (X.fn >= ns && X.fs >= ns) ? min(want, 2 * K) : min(want, max(32, 2 * consumed));
+    K = (ran_out && nse == ns) ? min(want, 2 * K) : min(want, max(32, 2 * consumed));
     __syncthreads();
   }
 #ifdef EQX_PROF

@@ -462,8 +462,13 @@ class GpuScheduler:
         keep = [] if keep is None else keep
         cols = {}
         loc = set()
-        for name, x, dt in (("client", client, np.int32), ("arrival_s", arrival_s, np.float64),
-                            ("input_tokens", input_tokens, np.int32), ("tag", tag, np.uint8),
+        # uint16 host client + input_tokens columns travel narrow (13 instead of 17 bytes per
+        # request over PCIe; eqx_requests::narrow) -- the caller chose them, so they are lossless
+        narrow = (isinstance(client, np.ndarray) and client.dtype == np.uint16 and
+                  isinstance(input_tokens, np.ndarray) and input_tokens.dtype == np.uint16)
+        wide = np.uint16 if narrow else np.int32
+        for name, x, dt in (("client", client, wide), ("arrival_s", arrival_s, np.float64),
+                            ("input_tokens", input_tokens, wide), ("tag", tag, np.uint8),
                             ("true_output_tokens", true_output_tokens, np.int32), ("id", ids, np.int64)):
             ptr, where = _as_col(x, dt, keep)
             cols[name] = ptr
@@ -473,7 +478,7 @@ class GpuScheduler:
             raise ValueError("drain: mix of host and device columns")
         n = len(client)
         rq = L.Requests(n, cols["id"], id_base, cols["client"], cols["arrival_s"], cols["input_tokens"],
-                        cols["true_output_tokens"], cols["tag"], loc.pop() if loc else L.EQX_HOST)
+                        cols["true_output_tokens"], cols["tag"], loc.pop() if loc else L.EQX_HOST, 1 if narrow else 0)
         if not staging:
             self._keep = keep  # device columns are used in place: keep them alive with the queue
             self.n_queued = n

@@ -5,8 +5,8 @@ import numpy as np
 import pytest
 
 import harness as H
-from helpers import (case_from_golden, compare_step, default_model, default_profile, golden_names, gpu_run,
-                     load_golden)
+from helpers import (case_columns, case_from_golden, compare_step, default_model, default_profile, golden_names,
+                     gpu_run, load_golden)
 from paper_2508_16646_b200 import workload as W
 
 pytestmark = pytest.mark.gpu
@@ -141,6 +141,38 @@ def test_staged_host_batches_in_order():
             sch.set_batch(*case_batch(case))
             sch.drain(**c)
             res = sch.step(case.now)
+            compare_step(res, sch, want)
+
+
+def test_narrow_host_columns_staged_and_unstaged():
+    """uint16 client / input_tokens host columns (eqx_requests::narrow: 13 B per request over
+    PCIe, widened on the copy stream) give the same step as the i32 columns, staged ahead, staged
+    by the drain itself, and through the graph path."""
+    from helpers import case_batch, case_clients, case_kwargs
+    from paper_2508_16646_b200 import scheduler as S
+    for seed, C in ((51, 64), (52, 1000), (53, 5)):
+        case = _random_case(seed, 30011, C)
+        want = H.run_step(case, "oracle")
+        cols = case_columns(case)
+        cols["client"] = cols["client"].astype(np.uint16)
+        cols["input_tokens"] = cols["input_tokens"].astype(np.uint16)
+        pinned = {k: S.pinned_copy(v) for k, v in cols.items()}
+        for mode in ("plain", "staged", "graph"):
+            sch = S.GpuScheduler(case_clients(case), running=case.running, **case_kwargs(case))
+            sch.set_batch(*case_batch(case))
+            src = cols if mode == "plain" else pinned
+            if mode == "staged":
+                sch.stage_async(**src)
+            if mode == "graph":
+                sch.checkpoint()
+                for _ in range(2):
+                    sch.restore_async()
+                    sch.stage_async(**src)
+                    sch.drain_step_async(case.now, **src)
+                    res = sch.collect(with_events=True)
+            else:
+                sch.drain(**src)
+                res = sch.step(case.now)
             compare_step(res, sch, want)
 
 
