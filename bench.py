@@ -54,6 +54,24 @@ def load_inputs(cfg: str, rank: int):
     return q, led, perf, model, prof, desc
 
 
+def trace_hash(q) -> str:
+    """trace_hash (workload.cpp:422-428) of the bench queue: FNV-1a of its canonical CSV
+    (eqx_trace, host C++), recorded in `config` as the input's provenance."""
+    from paper_2508_16646_b200.trace import Trace
+    return Trace.from_columns(q["client"], q["arrival"], q["in_tokens"], q["true_out"], q["client_names"],
+                              tag=q["tag"], tag_names=q["tag_names"]).hash()
+
+
+def bench_config(desc: str, q, world: int = 1) -> dict:
+    """`config` of the JSON line -- identical in both arms (--impl ours / reference)."""
+    return {"workload": desc, "policy": "equinox (alpha 0.7, delta 0.1, max_over_clients)",
+            "predictor": "mope(3) trained by the reference on its builtin corpus (seed 7)",
+            "queue_per_gpu": int(len(q["client"])), "trace_hash": trace_hash(q),
+            "inputs": "numpy PCG64 draws of the corpus mixture (paper_2508_16646_b200/workload.py)",
+            "l2": "flushed between steps (256 MiB memset outside the events)",
+            "parallelism": f"client-sharded x{world}" if world > 1 else "single GPU"}
+
+
 def make_scheduler(q, led, perf, model, prof, device):
     from paper_2508_16646_b200 import scheduler as S
     clients = [S.ClientState(n, ufc=float(u), rfc=float(r), counter=float(c))
@@ -150,7 +168,7 @@ def run_reference(args, rank, world):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.mean(t) * 1e3),
         "p50_ms": float(np.median(t) * 1e3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": desc, "policy": "equinox max_over_clients", "predictor": "mope(3)"},
+        "config": bench_config(desc, q),
         "cpu_baseline": {"value": val, "unit": "requests/s", "cores": 1, "kind": kind,
                          "sample": f"full {n}-request step x {args.steps} (drain_arrivals + admit_requests "
                                    "via the reference objects, oracle/_ref)"},
@@ -716,10 +734,7 @@ def run_ours(args, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
         "p50_ms": float(np.median(step_ms)), "p99_ms": float(np.percentile(step_ms, 99)),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": desc, "policy": "equinox (alpha 0.7, delta 0.1, max_over_clients)",
-                   "predictor": "mope(3) trained by the reference on its builtin corpus (seed 7)",
-                   "queue_per_gpu": n, "l2": "flushed between steps (256 MiB memset outside the events)",
-                   "parallelism": f"client-sharded replicas x{world}" if world > 1 else "single GPU"},
+        "config": bench_config(desc, q, world),
         "breakdown_ms": {"drain_p50": float(np.median(drain_ms)), "step_p50": float(np.median(kern_ms)),
                          "score_kernel_p50": float(np.median(score_ms)),
                          "select_kernel_p50": float(np.median(select_ms)),

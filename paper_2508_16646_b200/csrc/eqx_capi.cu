@@ -195,7 +195,7 @@ struct Col {
 };
 
 // warp_sel: 0 multi-mode select_kernel; 1 single-warp (shared-memory slots); 2/3/4 single-warp
-// with 1/2/4 register slots per lane; 5 speculative batches; 6 / 7 two / four selection warps
+// with 1/2/4 register slots per lane; 6 / 7 two / four selection warps
 // with one client per lane (33..64 / 65..128 clients)
 const void* select_fn(int warp_sel) {
   switch (warp_sel) {
@@ -203,7 +203,6 @@ const void* select_fn(int warp_sel) {
     case 2: return reinterpret_cast<const void*>(select_warp_kernel<1>);
     case 3: return reinterpret_cast<const void*>(select_warp_kernel<2>);
     case 4: return reinterpret_cast<const void*>(select_warp_kernel<4>);
-    case 5: return reinterpret_cast<const void*>(select_warp_kernel<8>);
     case 6: return reinterpret_cast<const void*>(select_warp_kernel<16>);
     case 7: return reinterpret_cast<const void*>(select_warp_kernel<32>);
     case 8: return reinterpret_cast<const void*>(select_topk_kernel);
@@ -1211,9 +1210,11 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl, int32_t g
   // Default: rounds of block-radix top-K over per-client key streams (select_topk_kernel,
   // eqx_topk.cuh).  EQX_SELECT_MODE=seq keeps the sequential pick loops below (the reference
   // loop one pick at a time; the -m gpu suite runs both).
+  // Sequential variants (each under -m gpu parity, tests/test_select_modes.py): seq (the pick
+  // loops below) and warp / slots / reg (their single-warp / register-slot forms).
   const char* sel_mode = std::getenv("EQX_SELECT_MODE");
-  const bool topk = !(sel_mode && std::string(sel_mode) == "seq");
-  bool batch_kernel = false;
+  const std::string sm = sel_mode ? sel_mode : "";
+  const bool topk = !(sm == "seq" || sm == "warp" || sm == "slots" || sm == "reg");
   if (topk) {
     const size_t static_smem = 12288;
     const int32_t kcap = kTopkThreads;
@@ -1260,7 +1261,6 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl, int32_t g
     a.tk_dsh = 6;
     a.tk_kcap = kcap;
     a.K = 0;
-    a.D = 0;
     a.Ds = 0;
     a.sel_threads = kTopkThreads;
     a.warp_sel = 8;
@@ -1304,31 +1304,9 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl, int32_t g
     a.cw_in_smem = 0;
     a.cw_global = ctx->d_cw.p;
   }
-  const size_t left0 = ctx->smem_optin - static_smem - smem;
-  // Batch lookahead D: about twice the picks a client can get (slots spread over clients),
-  // 2..8, with the C*D-item sort (24 B + 1 B per item) and W >= D windows fitting in smem.
-  auto pow2 = [](int64_t x) { int64_t t = 1; while (t < x) t <<= 1; return t; };
-  auto batch_bytes = [&](int64_t D) {
-    const int64_t tn = pow2(std::max<int64_t>(C * D, 2));
-    return static_cast<size_t>(tn * (sizeof(BatchItem) + 1) + 16 * 3 + 4ll * C);
-  };
-  int64_t D = std::min<int64_t>(8, std::max<int64_t>(2, 2 * static_cast<int64_t>(ctx->perf.max_batch) / std::max(C, 1) + 2));
-  if (const char* bd = std::getenv("EQX_BATCH_D")) D = std::max<int64_t>(2, std::atoi(bd));  // experiments
-  while (D >= 2 && (static_cast<int64_t>(C) * D > 8192 ||
-                    batch_bytes(D) + static_cast<size_t>(D) * C * sizeof(WinEntry) > left0))
-    --D;
-  if (D < 2 || C == 0) D = 0;
-  // Default: register-resident sequential picks (measured faster than speculative batches on
-  // cfg2/cfg3, profiles/); EQX_SELECT_MODE=batch enables the batch path for experiments.
-  {
-    const char* m = std::getenv("EQX_SELECT_MODE");
-    if (!(m && std::string(m) == "batch") && K > 0) D = 0;
-    a.warp_sel = !(m && (std::string(m) == "batch" || std::string(m) == "reg"));
-    batch_kernel = m && std::string(m) == "batch";
-  }
-  a.D = static_cast<int32_t>(D);
-  a.Tn = D ? static_cast<int32_t>(pow2(std::max<int64_t>(C * D, 2))) : 0;
-  if (D) smem += batch_bytes(D);
+  // Register loop (default sequential form); EQX_SELECT_MODE=reg keeps the multi-warp register
+  // loop at any roster, warp / slots the single-warp forms (below).
+  a.warp_sel = !(sm == "reg");
   // key streams of the register loop: up to 16 lookahead items (33 B each) per client, using
   // at most a third of what is left (the head windows get the rest)
   int64_t Ds = 0;
@@ -1398,16 +1376,13 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl, int32_t g
     CUDA_TRY(ctx, set_smem_attr(ctx, 10, select_fn(a.warp_sel), pl.select_smem));
     return EQX_OK;
   }
-  a.warp_sel = a.warp_sel && a.D == 0 && a.K > 0 && a.Ds > 0;
-  if (batch_kernel && a.D > 0) a.warp_sel = 5;  // batch kernel variant (select_fn)
+  a.warp_sel = a.warp_sel && a.K > 0 && a.Ds > 0;
   // kernel variant (select_fn): register slots up to 128 clients; larger rosters keep the
   // multi-warp register loop (measured faster than the shared-memory single-warp variant,
   // which stays selectable with EQX_SELECT_MODE=warp)
-  if (a.warp_sel && a.warp_sel != 5) {
-    const char* m = std::getenv("EQX_SELECT_MODE");
-    const bool slots = m && std::string(m) == "slots";  // one warp, 2 / 4 register slots per lane
-    a.warp_sel = C <= 32 ? 2 : C <= 64 ? (slots ? 3 : 6) : C <= 128 ? (slots ? 4 : 7)
-                                                                  : (m && std::string(m) == "warp") ? 1 : 0;
+  if (a.warp_sel) {
+    const bool slots = sm == "slots";  // one warp, 2 / 4 register slots per lane
+    a.warp_sel = C <= 32 ? 2 : C <= 64 ? (slots ? 3 : 6) : C <= 128 ? (slots ? 4 : 7) : sm == "warp" ? 1 : 0;
   }
   CUDA_TRY(ctx, set_smem_attr(ctx, a.warp_sel + 2, select_fn(a.warp_sel), pl.select_smem));
   return EQX_OK;
@@ -1492,6 +1467,9 @@ static eqx_status step_enqueue(eqx_ctx* ctx, const StepPlan& pl, bool with_drain
   ef.weight = ctx->d_weight.as<double>();
   ef.pol = ctx->pol;
   ef.now = pl.se.now;
+  ef.q_id = ctx->q_id;
+  ef.id_base = ctx->id_base;
+  ef.ev_id = ctx->d_ev_id.as<int64_t>();
   if (ctx->n > 0) {
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ctx->sm_count, (ctx->ev_cap + 255) / 256)));
     CUDA_TRY(ctx, launch_pdl(event_fill_kernel, dim3(grid), dim3(256), 0, s, ef));
@@ -1542,10 +1520,11 @@ eqx_status eqx_drain_step_async(eqx_ctx* ctx, const eqx_requests* r, double now)
   // parameter (pointers, sizes, policy, `now`, smem/tiling plan); two graphs are cached, for a
   // resident queue or the staging buffer sets of host batches (whose H2D and release events
   // stay outside the graph).
-  std::vector<unsigned char> key(sizeof(StepPlan) + 6 * sizeof(int64_t));
+  std::vector<unsigned char> key(sizeof(StepPlan) + 8 * sizeof(int64_t));
   std::memcpy(key.data(), &pl, sizeof(StepPlan));
-  const int64_t extra[6] = {ctx->tile_rows, ctx->n_tiles, ctx->counter_lift, static_cast<int64_t>(ctx->hist_smem),
-                            static_cast<int64_t>(ctx->rank_smem), ctx->staged};
+  const int64_t extra[8] = {ctx->tile_rows, ctx->n_tiles, ctx->counter_lift, static_cast<int64_t>(ctx->hist_smem),
+                            static_cast<int64_t>(ctx->rank_smem), ctx->staged,
+                            static_cast<int64_t>(reinterpret_cast<uintptr_t>(ctx->q_id)), ctx->id_base};
   std::memcpy(key.data() + sizeof(StepPlan), extra, sizeof(extra));
   int slot = -1;
   for (int i = 0; i < eqx_ctx::kGraphs; ++i)
@@ -2170,6 +2149,9 @@ eqx_status eqx_shard_select_async(eqx_ctx* ctx, const void* recs, int32_t world,
   ef.weight = ctx->d_weight.as<double>();
   ef.pol = ctx->pol;
   ef.now = now;
+  ef.q_id = ctx->d_gid.as<int64_t>();
+  ef.id_base = 0;
+  ef.ev_id = ctx->d_ev_id.as<int64_t>();
   shard_event_fill_kernel<<<std::max(1, ctx->sm_count / 4), 256, 0, s>>>(ef, ctx->d_win.as<WinEntry>());
   CUDA_TRY(ctx, cudaGetLastError());
   CUDA_TRY(ctx, state_to_host(ctx, s));
@@ -2267,11 +2249,8 @@ eqx_status eqx_copy_events(eqx_ctx* ctx, int64_t cap, int64_t* id, int32_t* kind
   CUDA_TRY(ctx, cudaStreamSynchronize(s));
   const int64_t n = std::min<int64_t>(std::min<int64_t>(cap, ctx->h_state->n_events), ctx->ev_cap);
   if (n <= 0) return EQX_OK;
-  if (id) {
-    gather_ids_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
-        ctx->d_ev_row.as<int32_t>(), n, ctx->q_id, ctx->id_base, ctx->d_ev_id.as<int64_t>());
-    CUDA_TRY(ctx, cudaGetLastError());
-  }
+  // request ids were gathered inside the step (event_fill_kernel): the id column may live in a
+  // staging set the copy stream refills once the step released it
   const size_t n8 = 8ull * n, n4 = 4ull * n;
   const Col cols[] = {{id, ctx->d_ev_id.p, n8},        {kind, ctx->d_ev_kind.p, n4},
                       {client, ctx->d_ev_client.p, n4}, {pred, ctx->d_ev_pred.p, n4},

@@ -1,18 +1,23 @@
 // eqx_kernels.cu -- sm_100a kernels of the Equinox per-step scheduling path.
 //
 //   drain_arrivals (engine.cpp:171-197), two launches:
-//     drain_hist_kernel  per-tile client histogram; the last CTA to finish scans the
-//                        [client][tile] table into FIFO segment offsets
-//     drain_rank_kernel  stable per-client rank inside each tile (warp ballot peer walk),
-//                        staged in shared memory and written out as contiguous per-client runs
-//                        -> perm (row indices grouped by client, arrival order kept); the last
-//                        CTA applies the on_activated counter lift (scheduler.cpp:235-253)
-//   admit_requests (engine.cpp:207-271), two concurrent launches:
-//     select_kernel      one CTA: the exact sequential admission loop over client heads
-//                        (select_next / holistic_score / fits_alone / can_fit / on_admit)
-//     score_kernel       whole-queue MoPE predict -> map_metrics -> ufc/rfc increments,
-//                        16-byte coalesced loads, streaming stores (HBM-bound stream)
-//   gather_ids_kernel    event rows -> request ids for the caller.
+//     drain_hist_kernel  per-(tile, warp, client) counts and each client's first row
+//     drain_rank_kernel  every CTA derives its segment offsets from the histogram, ranks its rows
+//                        per client (stable), stages the tile client-sorted in shared memory and
+//                        writes contiguous per-client runs -> perm (rows grouped by client, FIFO)
+//   the counter lift (on_activated, scheduler.cpp:235-253): lift_core, in an extra CTA of the
+//     window kernel (fused step) or lift_kernel (standalone drain)
+//   admit_requests (engine.cpp:207-271):
+//     window_kernel      the first W queued requests of every client scored into [C][W] heads
+//     select_topk_kernel one CTA: rounds of block-radix top-K over per-client key streams
+//                        (eqx_topk.cuh); select_warp_kernel / select_kernel keep the
+//                        sequential pick loops (EQX_SELECT_MODE=seq)
+//     score_kernel       whole-queue MoPE predict -> map_metrics -> ufc/rfc increments on a side
+//                        stream (16-byte streaming loads / stores: the HBM-bound stream)
+//     event_fill_kernel  event payloads and request ids from the per-request scores
+//   client-sharded step: shard_export / shard_ingest / shard_unpack kernels
+//   live queues: live_offsets / gather_live / predict_rows kernels
+//   feedback: feedback_kernel
 #include <cstdint>
 #include <type_traits>
 #include <cuda_runtime.h>
@@ -1146,24 +1151,10 @@ __device__ __forceinline__ void group_maxima(const ClientWork& cw, int32_t C, in
   named_sync(1, nthr);
 }
 
-// ---- speculative batch selection ---------------------------------------------------------
-// With the maxima fixed, every client's key only grows along its FIFO (increments >= 0, IEEE
-// rounding monotone), so the greedy argmin over heads is a merge of sorted per-client streams,
-// i.e. a sort.  A batch generates each client's next D keys under the current
-// maxima, sorts the C*D tuples, and accepts the longest prefix whose sequential semantics are
-// unaffected: it stops at the first admission that would move a maximum (kept), a max holder
-// leaving the backlog (kept), a client whose lookahead ran out (kept), or the first request
-// that does not fit (the step ends, or under backfill its client is skipped).
+// Outcome flags of a generated key-stream item (the top-K rounds, eqx_topk.cuh, and the
+// register pick loops): fits alone, its admission raises a maximum, a max holder leaves the
+// backlog with it, the client's generated stream ends with it.
 enum : uint32_t { kFlAlone = 1, kFlMaxChg = 2, kFlHolder = 4, kFlExh = 8 };
-
-// (key, arrival, client rank, lookahead index): the index makes equal tuples of one client
-// keep their FIFO order, so the (non-stable) sort reproduces repeated picks of one head.
-__device__ __forceinline__ bool item_better(const BatchItem& x, const BatchItem& y) {
-  const uint32_t xi = x.meta & 0xffffffu, yi = y.meta & 0xffffffu;
-  const bool lt =
-      (x.k < y.k) | ((x.k == y.k) & ((x.a < y.a) | ((x.a == y.a) & ((x.o < y.o) | ((x.o == y.o) & (xi < yi))))));
-  return (x.o != 0xffffffffu) & ((y.o == 0xffffffffu) | lt);
-}
 
 __device__ __forceinline__ double vtc_inc(const Policy& P, const WinEntry& e, double w) {
   if (P.kind != kVtc) return 0.0;  // scheduler.cpp:169-181
@@ -1204,331 +1195,7 @@ __device__ void cta_maxima(const ClientWork& cw, int32_t C, SelShared& S) {
   __syncthreads();
 }
 
-enum : int32_t { kBatchDone = 1, kBatchNeedMax = 2 };
 
-struct BatchScratch {
-  BatchItem* items;  // [Tn]
-  uint8_t* acc;      // [Tn] 0 = not accepted, 1 = admitted, 2 = rejected
-  int32_t* cnsm;     // [C] entries consumed this batch
-  int32_t* evx;      // [Tn] event index of accepted items
-};
-
-// Bitonic sort of NT*P tuples held P per thread in registers (blocked: thread t owns items
-// t*P .. t*P+P-1): partners inside a thread are compare-exchanged in registers, partners in
-// another lane of the warp through shuffles, and only strides of 32*P and more go through
-// shared memory.  Same network (and result) as the plain shared-memory loop.
-__device__ __forceinline__ BatchItem shfl_item(const BatchItem& x, int m) {
-  BatchItem y;
-  y.k = __shfl_xor_sync(0xffffffffu, x.k, m);
-  y.a = __shfl_xor_sync(0xffffffffu, x.a, m);
-  y.o = __shfl_xor_sync(0xffffffffu, x.o, m);
-  y.meta = __shfl_xor_sync(0xffffffffu, x.meta, m);
-  return y;
-}
-
-template <int P>
-__device__ __noinline__ void bitonic_sort_reg(BatchItem* items, int32_t Tn) {
-  const int tid = threadIdx.x;
-  BatchItem x[P];
-#pragma unroll
-  for (int p = 0; p < P; ++p) x[p] = items[tid * P + p];
-  for (int32_t k = 2; k <= Tn; k <<= 1) {
-    for (int32_t j = k >> 1; j > 0; j >>= 1) {
-      if (j < P) {  // compile-time partner indices keep x[] in registers
-        auto cx = [&](auto J) {
-          constexpr int jj = decltype(J)::value;
-#pragma unroll
-          for (int p = 0; p < P; ++p) {
-            const int q = p ^ jj;
-            if (q > p) {
-              const int32_t i = tid * P + p;
-              const bool up = (i & k) == 0;
-              if (up ? item_better(x[q], x[p]) : item_better(x[p], x[q])) {
-                const BatchItem t = x[p];
-                x[p] = x[q];
-                x[q] = t;
-              }
-            }
-          }
-        };
-        if (j == 1) cx(std::integral_constant<int, 1>{});
-        if constexpr (P > 2) if (j == 2) cx(std::integral_constant<int, 2>{});
-        if constexpr (P > 4) if (j == 4) cx(std::integral_constant<int, 4>{});
-      } else if (j < 32 * P) {
-        const int m = j / P;  // partner lane distance
-        const bool lower = ((tid & 31) & m) == 0;
-#pragma unroll
-        for (int p = 0; p < P; ++p) {
-          const BatchItem y = shfl_item(x[p], m);
-          const int32_t i = tid * P + p;
-          const bool up = (i & k) == 0;
-          const bool want_min = lower == up;
-          const bool take = want_min ? item_better(y, x[p]) : item_better(x[p], y);
-          if (take) x[p] = y;
-        }
-      } else {
-        __syncthreads();
-#pragma unroll
-        for (int p = 0; p < P; ++p) items[tid * P + p] = x[p];
-        __syncthreads();
-#pragma unroll
-        for (int p = 0; p < P; ++p) {
-          const int32_t i = tid * P + p, ixj = i ^ j;
-          const BatchItem y = items[ixj];
-          const bool up = (i & k) == 0;
-          const bool want_min = (i < ixj) == up;
-          const bool take = want_min ? item_better(y, x[p]) : item_better(x[p], y);
-          if (take) x[p] = y;
-        }
-      }
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int p = 0; p < P; ++p) items[tid * P + p] = x[p];
-  __syncthreads();
-}
-
-// One batch by the whole CTA.  Returns kBatchDone / kBatchNeedMax; *accepted = events emitted.
-__device__ int32_t batch_phase(const SelectArgs& a, const WinEntry* win, const ClientWork& cw, SelShared& S,
-                               const BatchScratch& B, int32_t* accepted) {
-  const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5;
-  const int32_t C = a.C, D = a.D, Tn = a.Tn, W = a.W;
-  const Policy& P = a.pol;
-  const bool maxmode = P.kind == kEquinox && P.norm_mode == 0;
-  const double mu = S.max_u, mr = S.max_r;
-  long long c0 = clock64();
-  // 1. per-client key streams under the current maxima
-  for (int32_t c = tid; c < C; c += NT) {
-    B.cnsm[c] = 0;
-    int32_t d = 0;
-    if (cw.pos[c] < cw.end[c] && !(cw.flags[c] & kSkipped)) {
-      double u = cw.ufc[c], r = cw.rfc[c], k = cw.cnt[c];
-      const int32_t pos = cw.pos[c], k0 = pos - cw.pos0[c], end = cw.end[c];
-      const uint32_t o = cw.order[c];
-      for (; d < D; ++d) {
-        const int32_t j = pos + d, kk = k0 + d;
-        if (j >= end || kk >= W) break;
-        const WinEntry e = win[static_cast<int64_t>(c) * W + kk];
-        const uint64_t key = ordered_bits(hf_key(P, u, r, mu, mr, k));
-        uint32_t fl = 0;
-        double nu = u, nr = r, nk = k;
-        if (e.alone) {
-          fl |= kFlAlone;
-          nu = __dadd_rn(u, e.ufc_inc);
-          nr = __dadd_rn(r, e.rfc_inc);
-          nk = (P.kind == kVtc) ? __dadd_rn(k, vtc_inc(P, e, cw.w[c])) : k;
-          if (maxmode && (mu < nu || mr < nr)) fl |= kFlMaxChg;
-        }
-        if (j + 1 == end) {
-          if (maxmode && (u == mu || r == mr)) fl |= kFlHolder;  // holder leaves the backlog
-        } else if (d + 1 == D || kk + 1 >= W) {
-          fl |= kFlExh;  // next entry of this client not generated: later items unordered
-        }
-        B.items[c * D + d] = BatchItem{key, e.abits, o, static_cast<uint32_t>(c * D + d) | (fl << 24)};
-        u = nu;
-        r = nr;
-        k = nk;
-      }
-    }
-    for (; d < D; ++d) B.items[c * D + d] = BatchItem{~0ull, ~0ull, 0xffffffffu, 0u};
-  }
-  for (int32_t i = C * D + tid; i < Tn; i += NT) B.items[i] = BatchItem{~0ull, ~0ull, 0xffffffffu, 0u};
-  for (int32_t i = tid; i < Tn; i += NT) B.acc[i] = 0;
-  __syncthreads();
-  long long c1 = clock64();
-  // 2. bitonic sort of the Tn tuples
-  if (NT == 256 && Tn == 512) {
-    bitonic_sort_reg<2>(B.items, Tn);
-  } else if (NT == 256 && Tn == 1024) {
-    bitonic_sort_reg<4>(B.items, Tn);
-  } else if (NT == 256 && Tn == 2048) {
-    bitonic_sort_reg<8>(B.items, Tn);
-  } else
-  for (int32_t kk = 2; kk <= Tn; kk <<= 1) {
-    for (int32_t j = kk >> 1; j > 0; j >>= 1) {
-      for (int32_t i = tid; i < Tn; i += NT) {
-        const int32_t ixj = i ^ j;
-        if (ixj > i) {
-          const BatchItem x = B.items[i], y = B.items[ixj];
-          const bool up = (i & kk) == 0;
-          if (up ? item_better(y, x) : item_better(x, y)) {
-            B.items[i] = y;
-            B.items[ixj] = x;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
-  long long c2 = clock64();
-  // 3. verify the sequential semantics (warp 0, 32 items per step)
-  __shared__ int32_t s_end, s_flags;
-  if (warp == 0) {
-    int32_t carry_a = 0, flags = 0, base = 0;
-    int64_t carry_r = 0;
-    const int32_t members0 = S.members;
-    const int64_t reserved0 = S.reserved;
-    for (;;) {
-      const int32_t p = base + lane;
-      const BatchItem it = p < Tn ? B.items[p] : BatchItem{~0ull, ~0ull, 0xffffffffu, 0u};
-      const bool valid = it.o != 0xffffffffu;
-      if (!__any_sync(0xffffffffu, valid)) {  // every generated item consumed without a cut
-        if (lane == 0) {
-          s_end = min(base, Tn);
-          s_flags = flags | kBatchDone;
-        }
-        break;
-      }
-      const uint32_t idx = it.meta & 0xffffffu, fl = it.meta >> 24;
-      const int32_t c = valid ? static_cast<int32_t>(idx / D) : 0, d = valid ? static_cast<int32_t>(idx % D) : 0;
-      const bool live = valid && !(cw.flags[c] & kSkipped);
-      const bool alone = live && (fl & kFlAlone);
-      int64_t res = 0;
-      if (alone) {
-        const WinEntry& e = win[static_cast<int64_t>(c) * W + (cw.pos[c] - cw.pos0[c]) + d];
-        res = static_cast<int64_t>(e.in) + e.pred;
-      }
-      int32_t ax = alone ? 1 : 0;
-      int64_t rx = res;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {  // inclusive scans
-        const int32_t t1 = __shfl_up_sync(0xffffffffu, ax, o);
-        const int64_t t2 = __shfl_up_sync(0xffffffffu, rx, o);
-        if (lane >= o) {
-          ax += t1;
-          rx += t2;
-        }
-      }
-      const int32_t a_ex = ax - (alone ? 1 : 0);
-      const int64_t r_ex = rx - res;
-      const bool fits = (members0 + carry_a + a_ex + 1 <= P.max_batch) && (reserved0 + carry_r + r_ex + res <= a.tmax);
-      const bool fail = alone && !fits;
-      const bool cut = live && ((fl & (kFlHolder | kFlExh)) || (alone && fits && (fl & kFlMaxChg)));
-      const unsigned fm = __ballot_sync(0xffffffffu, fail), cm = __ballot_sync(0xffffffffu, cut);
-      const int ff = fm ? __ffs(fm) - 1 : 32, fc = cm ? __ffs(cm) - 1 : 32;
-      const int stop = ff <= fc ? ff : fc + 1;  // lanes [0, stop) are accepted if live
-      if (lane < stop && live) B.acc[p] = alone ? 1 : 2;
-      const int32_t a_tot = __shfl_sync(0xffffffffu, ax, stop > 0 ? stop - 1 : 0);
-      const int64_t r_tot = __shfl_sync(0xffffffffu, rx, stop > 0 ? stop - 1 : 0);
-      if (ff < 32 && ff <= fc) {
-        if (!P.backfill) {  // engine.cpp:239: the step ends at the first head that does not fit
-          if (lane == 0) {
-            s_end = base + ff;
-            s_flags = flags | kBatchDone;
-          }
-          break;
-        }
-        if (lane == ff) cw.flags[c] |= kSkipped;  // engine.cpp:236-238
-        __syncwarp();
-        if (stop > 0) {
-          carry_a += a_tot;
-          carry_r += r_tot;
-        }
-        base += ff + 1;
-        continue;
-      }
-      if (fc < 32) {
-        const uint32_t cfl = __shfl_sync(0xffffffffu, fl, fc);
-        const bool cadm = __shfl_sync(0xffffffffu, alone ? 1 : 0, fc);
-        if ((cfl & kFlHolder) || (cadm && (cfl & kFlMaxChg))) flags |= kBatchNeedMax;
-        if (lane == 0) {
-          s_end = base + fc + 1;
-          s_flags = flags;
-        }
-        break;
-      }
-      carry_a += a_tot;
-      carry_r += r_tot;
-      base += 32;
-    }
-  }
-  __syncthreads();
-  long long c3 = clock64();
-  const int32_t end_pos = s_end, bflags = s_flags;
-  // 4. commit: event slots (exclusive scan of accepted), ledger per client, batch counters
-  __shared__ uint32_t warp_buf[32];
-  const int32_t per = (end_pos + NT - 1) / NT;
-  const int32_t p0 = min(end_pos, per * tid), p1 = min(end_pos, p0 + per);
-  uint32_t cnt = 0;
-  for (int32_t q = p0; q < p1; ++q) cnt += B.acc[q] ? 1u : 0u;
-  uint32_t run;
-  const uint32_t total = block_exclusive_scan(cnt, &run, warp_buf);
-  const int64_t ev0 = S.n_ev;
-  for (int32_t q = p0; q < p1; ++q) {
-    const uint8_t kind = B.acc[q];
-    if (!kind) continue;
-    const uint32_t idx = B.items[q].meta & 0xffffffu;
-    const int32_t c = static_cast<int32_t>(idx / D), d = static_cast<int32_t>(idx % D);
-#ifdef EQX_DEBUG
-    if (c >= C || (cw.pos[c] - cw.pos0[c]) + d >= W)
-      printf("EQX_DEBUG commit q=%d end=%d idx=%u c=%d d=%d pos=%d pos0=%d W=%d meta=%x o=%u\n", q, end_pos, idx, c, d,
-             cw.pos[c], cw.pos0[c], W, B.items[q].meta, B.items[q].o);
-#endif
-    const WinEntry& e = win[static_cast<int64_t>(c) * W + (cw.pos[c] - cw.pos0[c]) + d];
-    const int64_t k = ev0 + run++;
-    if (k < a.ev_cap) {
-      a.ev_row[k] = e.row;
-      a.ev_kind[k] = kind;
-      a.ev_client[k] = c;
-    }
-    atomicMax(&B.cnsm[c], d + 1);
-  }
-  __syncthreads();
-  int32_t nadm = 0, nrej = 0;
-  int64_t res_sum = 0, pre_sum = 0;
-  for (int32_t c = tid; c < C; c += NT) {
-    const int32_t n = B.cnsm[c];
-    if (!n) continue;
-    double u = cw.ufc[c], r = cw.rfc[c], k = cw.cnt[c];
-    const int32_t kb = cw.pos[c] - cw.pos0[c];
-    for (int32_t d = 0; d < n; ++d) {  // the same sequential adds as the stream generation
-      const WinEntry& e = win[static_cast<int64_t>(c) * W + kb + d];
-      if (e.alone) {
-        u = __dadd_rn(u, e.ufc_inc);
-        r = __dadd_rn(r, e.rfc_inc);
-        if (P.kind == kVtc) k = __dadd_rn(k, vtc_inc(P, e, cw.w[c]));
-        ++nadm;
-        res_sum += static_cast<int64_t>(e.in) + e.pred;
-        pre_sum += e.in;
-        cw.adm[c] += 1;
-      } else {
-        ++nrej;
-      }
-    }
-    cw.ufc[c] = u;
-    cw.rfc[c] = r;
-    cw.cnt[c] = k;
-    cw.pos[c] += n;
-    if (cw.pos[c] == cw.end[c]) cw.flags[c] &= ~kBacklogged;
-  }
-  nadm = __reduce_add_sync(0xffffffffu, nadm);
-  nrej = __reduce_add_sync(0xffffffffu, nrej);
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    res_sum += __shfl_xor_sync(0xffffffffu, res_sum, o);
-    pre_sum += __shfl_xor_sync(0xffffffffu, pre_sum, o);
-  }
-  __syncthreads();  // everyone has read S.n_ev before it moves
-  if (lane == 0 && (nadm | nrej)) {
-    atomicAdd(reinterpret_cast<unsigned long long*>(&S.n_adm), static_cast<unsigned long long>(nadm));
-    atomicAdd(reinterpret_cast<unsigned long long*>(&S.n_rej), static_cast<unsigned long long>(nrej));
-    atomicAdd(&S.members, nadm);
-    atomicAdd(reinterpret_cast<unsigned long long*>(&S.reserved), static_cast<unsigned long long>(res_sum));
-    atomicAdd(reinterpret_cast<unsigned long long*>(&S.prefill), static_cast<unsigned long long>(pre_sum));
-  }
-  if (tid == 0) S.n_ev += total;
-  __syncthreads();
-  if (tid == 0) {
-    const long long c4 = clock64();
-    a.st->t[8] += c1 - c0;
-    a.st->t[9] += c2 - c1;
-    a.st->t[10] += c3 - c2;
-    a.st->t[11] += c4 - c3;
-  }
-  *accepted = static_cast<int32_t>(total);
-  return bflags;
-}
 
 // Sequential picks (the exact admit_requests loop) for up to max_picks picks by the first
 // a.sel_threads threads; the others wait at the CTA barrier that follows.
@@ -2706,7 +2373,7 @@ __device__ __forceinline__ void warpn_select(const SelectArgs& a, const ModelTab
 // 64: rounds of block-radix top-K (topk_select)
 template <int kMode>
 __device__ __forceinline__ void select_body(const SelectArgs& a) {
-  constexpr bool kWarp = kMode >= 0 && kMode != 8;  // 8: speculative batches + shared-memory picks
+  constexpr bool kWarp = kMode >= 0;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ SelShared S;
   const int32_t C = a.C;
@@ -2744,13 +2411,6 @@ __device__ __forceinline__ void select_body(const SelectArgs& a) {
   cw.flags = reinterpret_cast<int32_t*>(take(4ull * C));
   cw.adm = reinterpret_cast<int32_t*>(take(4ull * C));
   cw.by_order = reinterpret_cast<int32_t*>(take(4ull * C));
-  BatchScratch B;
-  if (a.D > 0) {
-    B.items = reinterpret_cast<BatchItem*>(carve(sizeof(BatchItem) * static_cast<size_t>(a.Tn)));
-    B.acc = reinterpret_cast<uint8_t*>(carve(static_cast<size_t>(a.Tn)));
-    B.cnsm = reinterpret_cast<int32_t*>(carve(4ull * C));
-    B.evx = nullptr;
-  }
   StreamScratch T;
   T.Ds = a.Ds;
   if (a.Ds > 0) {
@@ -2909,25 +2569,13 @@ __device__ __forceinline__ void select_body(const SelectArgs& a) {
     ns = 1;
   }
   for (; !kWarp && kMode != 64 && !(S.flags & kDone);) {
-    if (a.D > 0) {
-      int32_t acc = 0;
-      const int32_t bf = batch_phase(a, win, cw, S, B, &acc);
-      ++nb;
-      if (bf & kBatchDone) break;
-      if (bf & kBatchNeedMax) cta_maxima(cw, C, S);
-      if (acc >= 4) continue;
-    }
-    const int32_t picks = a.D > 0 ? 8 : 0x7fffffff;
-    if constexpr (kMode == 8) {
-      seq_phase(a, M, win, cw, S, picks);
-    } else {
-      switch (a.K) {  // register-resident slots per thread (selection threads = a.sel_threads)
-        case 1: seq_reg_phase<1>(a, M, win, cw, S, picks, T); break;
-        case 2: seq_reg_phase<2>(a, M, win, cw, S, picks, T); break;
-        case 4: seq_reg_phase<4>(a, M, win, cw, S, picks, T); break;
-        case 8: seq_reg_phase<8>(a, M, win, cw, S, picks, T); break;
-        default: seq_phase(a, M, win, cw, S, picks); break;
-      }
+    const int32_t picks = 0x7fffffff;
+    switch (a.K) {  // register-resident slots per thread (selection threads = a.sel_threads)
+      case 1: seq_reg_phase<1>(a, M, win, cw, S, picks, T); break;
+      case 2: seq_reg_phase<2>(a, M, win, cw, S, picks, T); break;
+      case 4: seq_reg_phase<4>(a, M, win, cw, S, picks, T); break;
+      case 8: seq_reg_phase<8>(a, M, win, cw, S, picks, T); break;
+      default: seq_phase(a, M, win, cw, S, picks); break;
     }
     ++ns;
     __syncthreads();
@@ -2964,8 +2612,9 @@ __device__ __forceinline__ void select_body(const SelectArgs& a) {
   }
 }
 
-// Multi-mode selection (register slots / shared-memory loop / speculative batches) and the
-// default single-warp selection, as separate kernels so each gets its own register budget.
+// The sequential pick loops (EQX_SELECT_MODE=seq/warp/slots/reg: multi-warp register slots or
+// the shared-memory loop, single-warp forms) and the default top-K rounds, as separate kernels
+// so each gets its own register budget.
 __global__ void __launch_bounds__(kSelectMaxThreads, 1) select_kernel(const SelectArgs a) { select_body<-1>(a); }
 template <int kMode>
 __global__ void __launch_bounds__(kSelectMaxThreads, 1) select_warp_kernel(const SelectArgs a) { select_body<kMode>(a); }
@@ -2974,7 +2623,6 @@ template __global__ void select_warp_kernel<0>(SelectArgs);
 template __global__ void select_warp_kernel<1>(SelectArgs);
 template __global__ void select_warp_kernel<2>(SelectArgs);
 template __global__ void select_warp_kernel<4>(SelectArgs);
-template __global__ void select_warp_kernel<8>(SelectArgs);
 template __global__ void select_warp_kernel<16>(SelectArgs);
 template __global__ void select_warp_kernel<32>(SelectArgs);
 
@@ -2988,6 +2636,7 @@ __global__ void event_fill_kernel(const EventFillArgs a) {
     const int32_t row = a.ev_row[i];
     const bool adm = a.ev_kind[i] == 1;
     const int32_t pred = a.pred[row];
+    a.ev_id[i] = a.q_id ? a.q_id[row] : a.id_base + row;  // read in-step: the id column may be a staging set
     a.ev_pred[i] = pred;
     a.ev_ufc[i] = adm ? a.ufc_inc[row] : 0.0;
     a.ev_rfc[i] = adm ? a.rfc_inc[row] : 0.0;
@@ -3008,16 +2657,6 @@ __global__ void event_fill_kernel(const EventFillArgs a) {
 #endif
 }
 
-__global__ void gather_ids_kernel(const int32_t* __restrict__ rows, int64_t n, const int64_t* __restrict__ id,
-                                  int64_t id_base, int64_t* __restrict__ out) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n) {
-    const int32_t r = rows[i];
-    out[i] = r < 0 ? -1 : (id ? id[r] : id_base + r);
-  }
-}
-
-// Columns -> mapped host memory by SM stores over PCIe (16-byte words when aligned).
 // Staged narrow host columns widened in place of the H2D's second half: 8 rows per thread,
 // 16-byte loads of each u16 column, 2 x 16-byte stores per i32 column.
 __global__ void widen_cols_kernel(const uint16_t* c16, const uint16_t* i16, int64_t n, int32_t* c32, int32_t* i32) {
@@ -3044,6 +2683,7 @@ __global__ void widen_cols_kernel(const uint16_t* c16, const uint16_t* i16, int6
   }
 }
 
+// Columns -> mapped host memory by SM stores over PCIe (16-byte words when aligned).
 __global__ void pack_cols_kernel(const PackCols p) {
   pdl_wait();  // no-op unless launched programmatically after the kernel producing the columns
   pdl_trigger();
@@ -3331,6 +2971,7 @@ __global__ void shard_event_fill_kernel(const EventFillArgs a, const WinEntry* _
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int32_t row = a.ev_row[i];
     const bool adm = a.ev_kind[i] == 1 && row >= 0;
+    a.ev_id[i] = row < 0 ? -1 : (a.q_id ? a.q_id[row] : a.id_base + row);
     WinEntry e;
     if (row >= 0) {
       e = win[row];

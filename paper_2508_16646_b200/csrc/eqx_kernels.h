@@ -41,13 +41,6 @@ struct WinEntry {
   int32_t alone;    // fits_alone(in, pred) (gpu_model.cpp:69-72)
 };
 
-// One (client, lookahead) tuple of a speculative selection batch (24 B, shared memory).
-struct BatchItem {
-  uint64_t k;     // ordered bits of the key
-  uint64_t a;     // ordered bits of the head arrival
-  uint32_t o;     // client_id rank; 0xffffffff = sentinel
-  uint32_t meta;  // (c * D + d) | flags << 24
-};
 
 struct DrainArgs {
   const int32_t* client;
@@ -160,8 +153,6 @@ struct SelectArgs {
   const WinEntry* win_g; // [C][W] windows produced by window_kernel ([C][gW] when gathered)
   int32_t gW;            // > 0: client-sharded step; win_g holds the gathered [C][gW] windows and
                          // a head beyond them raises DevState::underflow instead of reading HBM
-  int32_t D;             // batch lookahead per client (0 = sequential picks only)
-  int32_t Tn;            // batch sort size (power of two >= C * D)
   int32_t sel_threads;   // threads in the selection loop (multiple of 32)
   int32_t K;             // register client slots per selection thread (1/2/4/8; 0 = smem loop)
   int32_t warp_sel;      // selection kernel variant (eqx_capi.cu select_fn)
@@ -226,6 +217,9 @@ struct EventFillArgs {
   const double* weight;
   Policy pol;
   double now;
+  const int64_t* q_id;      // the queue's id column (nullptr: id_base + row)
+  int64_t id_base;
+  int64_t* ev_id;           // [ev_cap] request id of each event
 };
 
 // ---- client-sharded step ------------------------------------------------
@@ -443,7 +437,5 @@ __global__ void select_topk_kernel(SelectArgs a);  // rounds of block-radix top-
 template <int kMode>
 __global__ void select_warp_kernel(SelectArgs a);  // kMode 0: smem slots; 1/2/4: register slots;
                                                    // 16: two selection warps, one client per lane
-__global__ void gather_ids_kernel(const int32_t* rows, int64_t n, const int64_t* id, int64_t id_base,
-                                  int64_t* out);
 
 }  // namespace eqx

@@ -12,7 +12,8 @@ import harness as H
 from helpers import case_clients, case_kwargs, default_model, default_profile
 from paper_2508_16646_b200 import workload as W
 
-pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not H.available("ref"), reason="reference build not present")]
+pytestmark = pytest.mark.gpu
+needs_ref = pytest.mark.skipif(not H.available("ref"), reason="reference build not present")
 
 
 def poisson_trace(seed, n_clients=8, rate=400.0, duration=6.0):
@@ -78,6 +79,7 @@ def check(ref, got):
         np.testing.assert_array_equal(got["counter"][i], c, err_msg=f"replay {i} counter")
 
 
+@needs_ref
 @pytest.mark.parametrize("pred_kind", [0, 1])
 def test_cfg1_shaped_replays_match_reference(pred_kind):
     traces = [poisson_trace(s) for s in range(4)]
@@ -86,6 +88,7 @@ def test_cfg1_shaped_replays_match_reference(pred_kind):
     assert all(len(r[0]) > 30 for r in ref), [len(r[0]) for r in ref]
 
 
+@needs_ref
 @pytest.mark.parametrize("over", [{"kind": 1}, {"kind": 1, "vtc_use_prediction": True}, {"kind": 0},
                                   {"backfill": True, "max_batch": 8}, {"norm_mode": 1},
                                   {"mem_per_token_bytes": 1.0, "mem_capacity_bytes": 40000.0}])
@@ -95,6 +98,7 @@ def test_replay_policies_match_reference(over):
     check(ref, got)
 
 
+@needs_ref
 def test_alpha_sweep_preset_replays_match_reference():
     """configs[4]'s shape: the poisson preset under an alpha grid, many replays in one launch."""
     alphas = np.repeat(np.arange(0.5, 0.86, 0.05), 4)
@@ -103,6 +107,7 @@ def test_alpha_sweep_preset_replays_match_reference():
     check(ref, got)
 
 
+@needs_ref
 def test_sweep_metrics_match_reference_build_report():
     """build_report's jain_ttft_p90 and throughput_tps per replay (what run_sweep_alpha averages)."""
     alphas = [0.5, 0.7, 0.85]
@@ -163,6 +168,7 @@ def check_full(want, got, win_cap):
         np.testing.assert_array_equal(got["rate"][i, :, :nr], w["rate"][:, :nr], err_msg=f"replay {i} service rates")
 
 
+@needs_ref
 @pytest.mark.parametrize("window_s", [1.0, 0.25, 0.7])
 def test_full_report_preset_sweep(window_s):
     """build_report (metrics.cpp:151-229) and the engine's window samples (engine.cpp:379-430),
@@ -174,6 +180,7 @@ def test_full_report_preset_sweep(window_s):
     assert all(w["report"]["n_diff"] >= 10 for w in want)
 
 
+@needs_ref
 @pytest.mark.parametrize("over", [{}, {"kind": 1}, {"kind": 0, "max_batch": 8}, {"norm_mode": 1},
                                   {"pred_kind": 1}, {"backfill": True, "max_batch": 6}])
 def test_full_report_policies(over):
@@ -184,6 +191,7 @@ def test_full_report_policies(over):
     check_full(want, got, 64)
 
 
+@needs_ref
 def test_full_report_cutoff_caps_and_single_client():
     # max_sim_time_s cuts the run mid-window; a small win_cap truncates the series only
     traces = [poisson_trace(600, n_clients=4, rate=300.0, duration=5.0)]
@@ -248,6 +256,7 @@ def check_log(want, got):
         assert got["counter_clamps"][i] == w["counter_clamps"]
 
 
+@needs_ref
 @pytest.mark.parametrize("over", [{}, {"kind": 1}, {"kind": 1, "vtc_use_prediction": True}, {"kind": 0},
                                   {"backfill": True, "max_batch": 6}, {"norm_mode": 1}, {"pred_kind": 1},
                                   {"mem_per_token_bytes": 1.0, "mem_capacity_bytes": 40000.0}])
@@ -263,6 +272,7 @@ def test_full_event_log_matches_reference(over):
     assert all((w["kind"] == 5).sum() > 25 for w in want), [(w["kind"] == 5).sum() for w in want]
 
 
+@needs_ref
 def test_duration_horizon_and_prediction_overhead():
     """Trace::duration_s beyond the last arrival (generated scenarios, workload.cpp:213) keeps
     the run going until then (engine.cpp:120-121); prediction_overhead_ms delays eligibility
@@ -274,6 +284,7 @@ def test_duration_horizon_and_prediction_overhead():
         assert all(w["sim_end"] > 3.0 for w in want)
 
 
+@needs_ref
 @pytest.mark.parametrize("n_clients", [17, 40, 300])
 def test_large_roster_replays_match_reference(n_clients):
     """Rosters beyond 16 clients (ledger in global scratch, per-client skipped stamps) --
@@ -286,6 +297,7 @@ def test_large_roster_replays_match_reference(n_clients):
         check_log(want, got)
 
 
+@needs_ref
 def test_caller_predictions_column():
     """Predictions made by a caller's Predictor (here the reference's NoisyOraclePredictor),
     handed over per row: the device applies max(1, .) and maps them against the evolving
@@ -294,3 +306,28 @@ def test_caller_predictions_column():
     preds = [H.ref_noisy_predict(33.0, 1, np.arange(len(q["client"]), dtype=np.int64), q["true_out"]) for q in traces]
     want, got = run_log(traces, [0.5, 0.7], predicted=preds, pred_kind=2, noisy_l1=33.0, noisy_seed=1)
     check_log(want, got)
+
+
+def test_committed_cfg1_replay_golden():
+    """tests/golden/replay_cfg1.npz: a cfg1-shaped run_simulation replay (8 clients, 3000
+    Poisson-ish arrivals over 25 s, MoPE, max_sim_time_s 25) recorded from the reference build
+    by oracle/gen_golden.py -- checked without the reference present: admitted / rejected
+    sequence with its times and the final ledgers, bit-exact."""
+    import os
+    from paper_2508_16646_b200 import scheduler as S
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "replay_cfg1.npz"))
+    n = len(z["client"])
+    case = H.StepCase(client=z["client"], arrival=z["arrival"], in_tokens=z["in_tokens"], true_out=z["true_out"],
+                      tag=z["tag"], client_names=[f"client{i}" for i in range(8)], model=default_model(),
+                      profile=default_profile())
+    sch = S.GpuScheduler(case_clients(case), running=np.zeros(8, np.int32), **case_kwargs(case))
+    tag = np.where(z["tag"] < 0, 0, z["tag"] + 1).astype(np.uint8)
+    got = sch.replay(np.array([0, n]), z["client"], z["arrival"], z["in_tokens"], z["true_out"], [case.alpha],
+                     tag=tag, ema_alpha=0.2, ev_cap=len(z["ev_id"]) + 1, max_sim_time_s=25.0)
+    ne = int(got["n_events"][0])
+    assert ne == len(z["ev_id"]) > 100
+    np.testing.assert_array_equal(got["ev_id"][0, :ne], z["ev_id"])
+    np.testing.assert_array_equal(got["ev_kind"][0, :ne], z["ev_kind"])
+    np.testing.assert_array_equal(got["ev_time"][0, :ne], z["ev_time"])
+    for k in ("ufc", "rfc", "counter"):
+        np.testing.assert_array_equal(got[k][0], z[k], err_msg=k)

@@ -1,0 +1,54 @@
+"""Every selection variant the library can run, under the same parity bar as the default.
+
+The default selection is rounds of block-radix top-K (select_topk_kernel).  The sequential
+variants stay selectable through EQX_SELECT_MODE (read at each step's plan): ``seq`` -- the
+reference loop one pick at a time (select_warp_kernel with one client per lane up to 128 clients,
+the multi-warp register-slot / shared-memory loops beyond), ``warp`` and ``slots`` -- its
+single-warp shared-memory and register-slot forms, ``reg`` -- the multi-warp register loop at any
+roster.  The scoring
+variants: EQX_SCORE=tma (bulk-copy ring) and EQX_NO_DIRECT (the interval / bucket searches instead
+of the direct predict table).  Each is checked bit-exact against the reference goldens and the
+C restatement on random rosters (C up to 3000) through the C ABI."""
+import os
+
+import numpy as np
+import pytest
+
+import harness as H
+from helpers import case_from_golden, compare_step, golden_names, gpu_run, load_golden
+
+pytestmark = pytest.mark.gpu
+
+VARIANTS = [("EQX_SELECT_MODE", "seq"), ("EQX_SELECT_MODE", "warp"), ("EQX_SELECT_MODE", "slots"),
+            ("EQX_SELECT_MODE", "reg"), ("EQX_SCORE", "tma"), ("EQX_NO_DIRECT", "1")]
+
+
+@pytest.fixture(params=VARIANTS, ids=[f"{k}={v}" for k, v in VARIANTS])
+def variant(request):
+    k, v = request.param
+    old = os.environ.get(k)
+    os.environ[k] = v
+    yield request.param
+    if old is None:
+        del os.environ[k]
+    else:
+        os.environ[k] = old
+
+
+def test_goldens(variant):
+    for name in golden_names():
+        meta, ins, outs = load_golden(name)
+        case = case_from_golden(meta, ins)
+        sch, res = gpu_run(case)
+        compare_step(res, sch, outs, flagged_near_ties=res.noisy_near_ties, row_ids=case.id)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_rosters(variant, seed):
+    from test_gpu_parity import _random_case
+    rng = np.random.default_rng(4000 + seed)
+    C = int([1, 31, 64, 100, 777, 3000][seed])
+    case = _random_case(4100 + seed, int(rng.integers(1000, 40000)), C)
+    want = H.run_step(case, "oracle")
+    sch, res = gpu_run(case, device_columns=bool(seed % 2))
+    compare_step(res, sch, want)
