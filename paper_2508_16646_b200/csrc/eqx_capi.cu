@@ -102,7 +102,9 @@ struct eqx_ctx {
   int bound_stage = -1;
   uint64_t stage_seq = 0;
   cudaStream_t copy_stream = nullptr;
-  DevBuf d_perm, d_hist;
+  DevBuf d_perm, d_hist, d_tbase, d_ctot, d_tsorted;
+  bool sort_drain = false;         // small rosters: drain_sort + drain_scan + drain_scatter
+  size_t sort_smem = 0;
   bool queue_ready = false;
 
   DevBuf d_pred, d_bucket, d_ufc_out, d_rfc_out;
@@ -468,7 +470,7 @@ void eqx_ctx_destroy(eqx_ctx* ctx) {
   DevBuf* bufs[] = {&ctx->d_model, &ctx->d_ufc, &ctx->d_rfc, &ctx->d_counter, &ctx->d_weight,
                     &ctx->d_order, &ctx->d_running, &ctx->d_backlogged, &ctx->d_head,
                     &ctx->d_count, &ctx->d_first, &ctx->d_qlen_before, &ctx->d_seg_off,
-                    &ctx->own_tag, &ctx->d_perm, &ctx->d_hist, &ctx->d_pred,
+                    &ctx->own_tag, &ctx->d_perm, &ctx->d_hist, &ctx->d_tbase, &ctx->d_ctot, &ctx->d_tsorted, &ctx->d_pred,
                     &ctx->d_bucket, &ctx->d_ufc_out, &ctx->d_rfc_out, &ctx->d_ev_row,
                     &ctx->d_ev_kind, &ctx->d_ev_client, &ctx->d_ev_pred, &ctx->d_ev_ufc,
                     &ctx->d_ev_rfc, &ctx->d_ev_vtc, &ctx->d_ev_wait, &ctx->d_ev_id,
@@ -944,10 +946,21 @@ static eqx_status drain_prepare(eqx_ctx* ctx, const eqx_requests* r) {
   // staged in shared memory (coalesced per-client runs) when it fits.
   int64_t tile_rows = (n + ctx->sm_count - 1) / std::max(ctx->sm_count, 1);
   tile_rows = std::max<int64_t>(1024, (tile_rows + 1023) / 1024 * 1024);
+  // small rosters: per-tile counting sort (one read of the client column, no peer masks)
+  ctx->sort_drain = C <= kSortMaxClients;
+  if (ctx->sort_drain) {
+    tile_rows = kSortTile;
+    CUDA_TRY(ctx, ctx->d_tsorted.ensure(4 * nn));
+    const size_t cbytes = (2ull * sort_pad((C + (C & 1)) * kSortThreads) + 2 + 15) & ~size_t(15);
+    ctx->sort_smem = cbytes + 4ull * kSortTile;
+    CUDA_TRY(ctx, set_smem_attr(ctx, 11, reinterpret_cast<const void*>(drain_sort_kernel), ctx->sort_smem));
+  }
   if (tile_rows / kDrainWarps > 65535) return fail(ctx, EQX_ERR_CONFIG, "queue too long for the drain tiling");
   const int32_t n_tiles = static_cast<int32_t>(std::max<int64_t>(1, (n + tile_rows - 1) / tile_rows));
   const int64_t L = static_cast<int64_t>(C) * n_tiles;
   CUDA_TRY(ctx, ctx->d_hist.ensure(4 * std::max<int64_t>(L, 1)));
+  CUDA_TRY(ctx, ctx->d_tbase.ensure(4 * std::max<int64_t>(L, 1)));
+  CUDA_TRY(ctx, ctx->d_ctot.ensure(4 * std::max<int64_t>(C, 1)));
   ctx->tile_rows = tile_rows;
   ctx->n_tiles = n_tiles;
   ctx->hist_L = L;
@@ -976,6 +989,9 @@ static DrainArgs drain_args(eqx_ctx* ctx) {
   d.n_tiles = ctx->n_tiles;
   d.staged = ctx->staged ? 1 : 0;
   d.hist = ctx->d_hist.as<uint32_t>();
+  d.tbase = ctx->d_tbase.as<uint32_t>();
+  d.ctot = ctx->d_ctot.as<uint32_t>();
+  d.tsorted = ctx->d_tsorted.as<uint32_t>();
   d.hist_L = ctx->hist_L;
   d.seg_off = ctx->d_seg_off.as<int32_t>();
   d.perm = ctx->d_perm.as<uint32_t>();
@@ -1014,8 +1030,15 @@ static eqx_status drain_enqueue(eqx_ctx* ctx, bool lift, bool keep_qlen = false)
   }
 #endif
   const DrainArgs d = drain_args(ctx);
-  drain_hist_kernel<<<ctx->n_tiles, kDrainThreads, ctx->hist_smem, s>>>(d);
-  CUDA_TRY(ctx, launch_pdl(drain_rank_kernel, dim3(ctx->n_tiles), dim3(kDrainThreads), ctx->rank_smem, s, d));
+  if (ctx->sort_drain) {
+    drain_sort_kernel<<<ctx->n_tiles, kSortThreads, ctx->sort_smem, s>>>(d);
+    CUDA_TRY(ctx, launch_pdl(drain_scan_kernel, dim3((C + 31) / 32), dim3(1024), 0, s, d));
+    CUDA_TRY(ctx, launch_pdl(drain_scatter_kernel, dim3(ctx->n_tiles), dim3(kSortThreads), 0, s, d));
+  } else {
+    drain_hist_kernel<<<ctx->n_tiles, kDrainThreads, ctx->hist_smem, s>>>(d);
+    CUDA_TRY(ctx, launch_pdl(drain_scan_kernel, dim3((C + 31) / 32), dim3(1024), 0, s, d));
+    CUDA_TRY(ctx, launch_pdl(drain_rank_kernel, dim3(ctx->n_tiles), dim3(kDrainThreads), ctx->rank_smem, s, d));
+  }
   if (lift) lift_kernel<<<1, 1024, 0, s>>>(d);
   CUDA_TRY(ctx, cudaGetLastError());
   return EQX_OK;

@@ -344,9 +344,7 @@ __device__ __forceinline__ void drain_hist_body(const DrainArgs& a) {
     uint32_t t = 0;
 #pragma unroll 8
     for (int w = 0; w < kDrainWarps; ++w) t += wc[w * C + c];
-    // small rosters: [client][tile] (the rank prologue's thread groups read tile runs);
-    // large rosters (one thread per client): [tile][client] (a warp reads adjacent clients)
-    a.hist[C <= kHistClientMajor ? static_cast<int64_t>(c) * a.n_tiles + tile : static_cast<int64_t>(tile) * C + c] = t;
+    a.hist[static_cast<int64_t>(tile) * C + c] = t;  // [tile][client]: drain_scan_kernel's lanes read adjacent clients
   }
   EQX_DT_MAX(1);
 }
@@ -367,6 +365,206 @@ __device__ __forceinline__ void drain_hist_body(const DrainArgs& a) {
   }
 
 __global__ void __launch_bounds__(kDrainThreads) drain_hist_kernel(const DrainArgs a) { EQX_NB_DISPATCH(drain_hist_body) }
+
+// ---- small rosters (C <= kSortMaxClients): per-tile stable counting sort ----------------------
+// Thread t owns rows t*8 .. t*8+7 of the tile (in registers).  Counters cnt[c][t] (u16, one
+// word of padding per 64 so the raking scan below is conflict-free) count its rows per client;
+// the exclusive scan of the counters in (client, thread) order gives every row its slot in the
+// client-sorted tile, stable because threads own ascending row ranges.  The tile leaves as
+// (client << 16 | tile row) words plus the per-client tile counts; drain_scan_kernel and
+// drain_scatter_kernel turn them into perm.  One read of the client column per row.
+__global__ void __launch_bounds__(kSortThreads) drain_sort_kernel(const DrainArgs a) {
+  extern __shared__ __align__(16) uint32_t sh[];
+  EQX_DT_MIN(0);
+  pdl_trigger();
+  const int32_t C = a.C, Cp = C + (C & 1);  // counter rows padded to even: raking reads word pairs
+  const int tid = threadIdx.x;
+  const int32_t t0 = blockIdx.x * kSortTile;
+  const int32_t rows = min(kSortTile, a.n - t0);
+  const int L = Cp * kSortThreads;
+  uint16_t* cnt = reinterpret_cast<uint16_t*>(sh);
+  const int cwords = (sort_pad(L) + 1) / 2;
+  uint32_t* srow = sh + ((cwords + 3) & ~3);
+  __shared__ uint32_t warp_buf[32];
+  __shared__ uint32_t cstart[kSortMaxClients + 1];
+  for (int i = tid; i < cwords; i += kSortThreads) sh[i] = 0u;
+  int32_t cv[kSortRows];
+  const int32_t r0 = tid * kSortRows;
+  if (r0 + kSortRows <= rows) {  // 4 x 16-byte loads
+#pragma unroll
+    for (int q = 0; q < kSortRows / 4; ++q) {
+      const int4 v = ldg_stream(reinterpret_cast<const int4*>(a.client + t0 + r0) + q);
+      cv[4 * q] = v.x;
+      cv[4 * q + 1] = v.y;
+      cv[4 * q + 2] = v.z;
+      cv[4 * q + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < kSortRows; ++j) cv[j] = r0 + j < rows ? a.client[t0 + r0 + j] : -1;
+  }
+  __syncthreads();
+  bool bad = false;
+#pragma unroll
+  for (int j = 0; j < kSortRows; ++j) {
+    const int32_t c = cv[j];
+    if (static_cast<uint32_t>(c) < static_cast<uint32_t>(C)) {
+      cnt[sort_pad(c * kSortThreads + tid)] += 1;
+    } else {
+      bad |= r0 + j < rows;
+      cv[j] = -1;
+    }
+  }
+  if (bad) a.st->bad_client = 1;
+  __syncthreads();
+  {  // exclusive scan of the counters in (client, thread) order: thread t rakes entries
+     // [t Cp, t Cp + Cp) as Cp / 2 words (an even entry and its successor share a word),
+     // 8 independent loads at a time
+    const int w0 = tid * (Cp / 2), nw = Cp / 2;
+    auto waddr = [&](int w) { return (w + ((2 * w) >> 6)); };  // word index of entries 2w, 2w + 1
+    uint32_t s = 0;
+    for (int k = 0; k < nw; k += 8) {
+      uint32_t v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = k + u < nw ? sh[waddr(w0 + k + u)] : 0u;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s += (v[u] & 0xffffu) + (v[u] >> 16);
+    }
+    uint32_t run;
+    block_exclusive_scan(s, &run, warp_buf);
+    for (int k = 0; k < nw; k += 8) {
+      uint32_t v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = k + u < nw ? sh[waddr(w0 + k + u)] : 0u;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t lo = run;
+        run += v[u] & 0xffffu;
+        const uint32_t hi = run;
+        run += v[u] >> 16;
+        if (k + u < nw) sh[waddr(w0 + k + u)] = lo | (hi << 16);
+      }
+    }
+  }
+  __syncthreads();
+  if (tid <= C) cstart[tid] = tid < C ? cnt[sort_pad(tid * kSortThreads)] : 0xffffffffu;
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kSortRows; ++j) {  // walk 2: rows into their slots
+    const int32_t c = cv[j];
+    if (c >= 0) {
+      const int p = sort_pad(c * kSortThreads + tid);
+      const uint32_t slot = cnt[p];
+      cnt[p] = static_cast<uint16_t>(slot + 1);
+      srow[slot] = (static_cast<uint32_t>(c) << 16) | static_cast<uint32_t>(r0 + j);
+    }
+  }
+  __syncthreads();
+  // per-client tile counts (the start of the next client, or the number of valid rows) and first rows
+  const uint32_t nvalid = cnt[sort_pad((Cp - 1) * kSortThreads + kSortThreads - 1)];
+  if (tid < C) {
+    const uint32_t st = cstart[tid];
+    const uint32_t en = tid + 1 < C ? cstart[tid + 1] : nvalid;
+    a.hist[static_cast<int64_t>(blockIdx.x) * C + tid] = en - st;
+    if (en > st) atomicMin(reinterpret_cast<unsigned int*>(a.first_row) + tid, static_cast<uint32_t>(t0) + (srow[st] & 0xffffu));
+  }
+  for (int i = tid; i < static_cast<int>(nvalid); i += kSortThreads) a.tsorted[t0 + i] = srow[i];
+  EQX_DT_MAX(1);
+}
+
+// Sorted tiles -> perm: each tile's client runs go to segment start + rows of the client in
+// earlier tiles (drain_scan_kernel) + offset in the run.  Tile 0 writes seg_off / count.
+__global__ void __launch_bounds__(kSortThreads) drain_scatter_kernel(const DrainArgs a) {
+  __shared__ uint32_t base[kSortMaxClients], toff[kSortMaxClients];
+  __shared__ uint32_t warp_buf[32];
+  EQX_DT_MIN(3);
+  pdl_wait();     // drain_scan_kernel (and through it drain_sort_kernel) is complete
+  pdl_trigger();  // the window kernel may get scheduled
+  const int32_t C = a.C, tile = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int32_t t0 = tile * kSortTile;
+  uint32_t tot = 0, h = 0, tb = 0;
+  if (tid < C) {
+    tot = __ldcg(a.ctot + tid);
+    h = __ldcg(a.hist + static_cast<int64_t>(tile) * C + tid);
+    tb = __ldcg(a.tbase + static_cast<int64_t>(tile) * C + tid);
+  }
+  uint32_t seg, loc;
+  const uint32_t total = block_exclusive_scan(tot, &seg, warp_buf);
+  const uint32_t nvalid = block_exclusive_scan(h, &loc, warp_buf);
+  if (tid < C) {
+    base[tid] = seg + tb;
+    toff[tid] = loc;
+    if (tile == 0) {
+      a.seg_off[tid] = static_cast<int32_t>(seg);
+      a.count[tid] = static_cast<int32_t>(tot);
+    }
+  }
+  if (tile == 0 && tid == 0) a.seg_off[C] = static_cast<int32_t>(total);
+  __syncthreads();
+  uint32_t v[kSortRows];  // every load in flight before the stores
+#pragma unroll
+  for (int j = 0; j < kSortRows; ++j) {
+    const int i = tid + j * kSortThreads;
+    v[j] = i < static_cast<int>(nvalid) ? __ldcg(a.tsorted + t0 + i) : 0u;
+  }
+#pragma unroll
+  for (int j = 0; j < kSortRows; ++j) {
+    const int i = tid + j * kSortThreads;
+    if (i < static_cast<int>(nvalid)) {
+      const uint32_t c = v[j] >> 16;
+      a.perm[base[c] + (static_cast<uint32_t>(i) - toff[c])] = static_cast<uint32_t>(t0) + (v[j] & 0xffffu);
+    }
+  }
+  EQX_DT_MAX(4);
+}
+
+// Per-client prefix over tiles of the drain histogram, once for the whole batch: CTA b owns
+// clients 32b..32b+31 (one per lane); its 32 warps split the tiles into contiguous chunks,
+// sum them, exchange the chunk sums through shared memory and write every tile's exclusive
+// prefix.  tbase[t][c] = rows of client c in tiles < t, ctot[c] = rows of client c.
+__global__ void __launch_bounds__(1024) drain_scan_kernel(const DrainArgs a) {
+  __shared__ uint32_t part[32][33];
+  pdl_wait();     // drain_hist_kernel's histogram is complete
+  pdl_trigger();  // drain_rank_kernel may get scheduled
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int32_t C = a.C, nt = a.n_tiles;
+  const int32_t c = blockIdx.x * 32 + lane;
+  const int32_t per = (nt + 31) / 32;
+  const int32_t t0 = min(nt, warp * per), t1 = min(nt, t0 + per);
+  uint32_t h[8];  // up to 8 tiles per warp in registers (per <= 8 for <= 256 tiles), else re-read
+  uint32_t sum = 0;
+  if (c < C) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      h[u] = t0 + u < t1 ? __ldcg(a.hist + static_cast<int64_t>(t0 + u) * C + c) : 0u;
+      sum += h[u];
+    }
+    for (int32_t t = t0 + 8; t < t1; ++t) sum += __ldcg(a.hist + static_cast<int64_t>(t) * C + c);
+  }
+  part[warp][lane] = sum;
+  __syncthreads();
+  uint32_t run = 0, tot = 0;
+  for (int w = 0; w < 32; ++w) {
+    const uint32_t v = part[w][lane];
+    run += w < warp ? v : 0u;
+    tot += v;
+  }
+  if (c < C) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (t0 + u < t1) {
+        a.tbase[static_cast<int64_t>(t0 + u) * C + c] = run;
+        run += h[u];
+      }
+    }
+    for (int32_t t = t0 + 8; t < t1; ++t) {
+      a.tbase[static_cast<int64_t>(t) * C + c] = run;
+      run += __ldcg(a.hist + static_cast<int64_t>(t) * C + c);
+    }
+    if (warp == 0) a.ctot[c] = tot;
+  }
+}
 
 
 
@@ -391,7 +589,7 @@ __device__ __forceinline__ void drain_rank_body(const DrainArgs& a) {
   uint32_t* base = sh;                                     // [C] global start of this tile's run
   uint32_t* toff = sh + C;                                 // [C] tile-local start / totals
   uint16_t* wc = reinterpret_cast<uint16_t*>(sh + 2 * C);  // [kDrainWarps][C]
-  pdl_wait();     // drain_hist_kernel's counts, histogram and first rows are complete
+  pdl_wait();     // drain_scan_kernel (and through it drain_hist_kernel) is complete
   pdl_trigger();  // the window kernel may get scheduled
   {  // per-warp client counts from drain_hist_kernel's walk (4 independent L2 loads in flight)
     const uint16_t* g = a.wcnt + static_cast<int64_t>(tile) * kDrainWarps * C;
@@ -405,67 +603,28 @@ __device__ __forceinline__ void drain_rank_body(const DrainArgs& a) {
         if (i0 + u * NT < nwc) wc[i0 + u * NT] = v[u];
     }
   }
-  // Every CTA derives its own global offsets from the histogram (no serial scan):
-  // base[c] = sum_{c' < c} total[c'] + sum_{t < tile} hist(c, t).  G threads per client split
-  // the tiles; the layout (kHistClientMajor) keeps either layout's reads coalesced.
-  for (int c = tid; c < C; c += blockDim.x) base[c] = toff[c] = 0;
-  __syncthreads();
+  // global offsets: segment start of the client (exclusive scan of the per-client totals) +
+  // its rows in earlier tiles (drain_scan_kernel)
   {
-    const int NT = blockDim.x;
-    int G = 1;  // threads per client: a power of two, so client groups never straddle warps
-    while (G * 2 * C <= NT) G *= 2;  // every thread takes part (G * C <= NT)
-    const int32_t nt = a.n_tiles;
-    for (int c0 = 0; c0 < C; c0 += NT / G) {
-      const int c = c0 + tid / G, g = tid % G;
-      uint32_t pre = 0, tot = 0;
-      if (tid / G < NT / G && c < C) {
-        for (int32_t t0 = g; t0 < nt; t0 += 16 * G) {  // 16 independent L2 loads in flight
-          uint32_t h[16];
-#pragma unroll
-          for (int u = 0; u < 16; ++u) {
-            const int32_t t = t0 + u * G;
-            h[u] = t < nt ? __ldcg(a.hist + (C <= kHistClientMajor ? static_cast<int64_t>(c) * nt + t
-                                                                   : static_cast<int64_t>(t) * C + c))
-                          : 0u;
-          }
-#pragma unroll
-          for (int u = 0; u < 16; ++u) {
-            tot += h[u];
-            pre += t0 + u * G < tile ? h[u] : 0u;
-          }
-        }
-      }
-      for (int o = 1; o < G && o < 32; o <<= 1) {  // segment sums (lane g == 0 of each group)
-        pre += __shfl_down_sync(0xffffffffu, pre, o);
-        tot += __shfl_down_sync(0xffffffffu, tot, o);
-      }
-      if (G > 32) {  // combine the warps of one client through shared memory
-        if (lane == 0 && c < C) {
-          atomicAdd(&base[c], pre);
-          atomicAdd(&toff[c], tot);
-        }
-      } else if (g == 0 && c < C) {
-        base[c] = pre;
-        toff[c] = tot;
-      }
-    }
-  }
-  __syncthreads();
-  {  // segment starts: exclusive scan of the per-client totals
     __shared__ uint32_t warp_buf[32];
     const int per = (C + blockDim.x - 1) / blockDim.x;
     const int c0 = min(C, per * tid), c1 = min(C, c0 + per);
     uint32_t s = 0;
-    for (int c = c0; c < c1; ++c) s += toff[c];
+    for (int c = c0; c < c1; ++c) {
+      const uint32_t t = __ldcg(a.ctot + c);
+      toff[c] = t;
+      s += t;
+    }
     uint32_t run;
     const uint32_t total = block_exclusive_scan(s, &run, warp_buf);
+    const uint32_t* tb = a.tbase + static_cast<int64_t>(tile) * C;
     for (int c = c0; c < c1; ++c) {
       const uint32_t t = toff[c];
       if (tile == 0) {
         a.seg_off[c] = static_cast<int32_t>(run);
         a.count[c] = static_cast<int32_t>(t);
       }
-      base[c] += run;
+      base[c] = run + __ldcg(tb + c);
       run += t;
     }
     if (tile == 0 && tid == 0) a.seg_off[C] = static_cast<int32_t>(total);

@@ -10,8 +10,13 @@
 namespace eqx {
 
 constexpr int kDrainThreads = 1024;  // 32 warps per tile
+// small rosters: tile-local counting sort, one thread per 16 consecutive rows
+constexpr int kSortThreads = 512;
+constexpr int kSortRows = 16;
+constexpr int kSortTile = kSortThreads * kSortRows;  // 8192 rows
+constexpr int kSortMaxClients = 128;
+__host__ __device__ constexpr int sort_pad(int L) { return L + 2 * (L >> 6); }  // one word per 64 counters
 constexpr int kDrainWarps = kDrainThreads / 32;
-constexpr int kHistClientMajor = 128;  // rosters up to this size store the drain histogram [client][tile]
 constexpr int kScoreThreads = 256;
 constexpr int kScoreTmaThreads = 256;                        // score_tma_kernel block
 constexpr int kScoreTile = 1024;                             // requests per bulk-copied tile
@@ -50,7 +55,10 @@ struct DrainArgs {
   int32_t tile_rows;
   int32_t n_tiles;
   int32_t staged;       // 1: smem-staged coalesced scatter (when the tile fits in smem)
-  uint32_t* hist;       // per-tile client counts: [C][n_tiles] (C <= kHistClientMajor) or [n_tiles][C]
+  uint32_t* hist;       // per-tile client counts [n_tiles][C]
+  uint32_t* tbase;      // [n_tiles][C] rows of the client in earlier tiles (drain_scan_kernel)
+  uint32_t* ctot;       // [C] rows of the client in the batch (drain_scan_kernel)
+  uint32_t* tsorted;    // [n] small rosters: each tile's rows sorted by client, (client << 16) | row - t0
   int64_t hist_L;
   int32_t* seg_off;     // [C+1]
   uint32_t* perm;       // [n] row indices grouped by client, FIFO order
@@ -428,6 +436,9 @@ __global__ void replay_kernel(ReplayArgs a);  // KIND: kFcfs / kVtc / kEquinox; 
 __global__ void drain_hist_kernel(DrainArgs a);
 __global__ void lift_kernel(DrainArgs a);
 __global__ void event_fill_kernel(EventFillArgs a);
+__global__ void drain_scan_kernel(DrainArgs a);
+__global__ void drain_sort_kernel(DrainArgs a);     // small rosters: per-tile stable counting sort
+__global__ void drain_scatter_kernel(DrainArgs a);  // small rosters: sorted tiles -> perm
 __global__ void drain_rank_kernel(DrainArgs a);
 __global__ void score_kernel(ScoreArgs a);
 __global__ void score_tma_kernel(ScoreArgs a);
