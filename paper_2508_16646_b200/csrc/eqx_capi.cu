@@ -51,6 +51,11 @@ struct DevBuf {
     p = nullptr;
     bytes = 0;
   }
+  // every buffer of a context is freed with it (eqx_ctx_destroy deletes the context)
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
 };
 
 }  // namespace
@@ -196,21 +201,8 @@ struct Col {
   size_t bytes;
 };
 
-// warp_sel: 0 multi-mode select_kernel; 1 single-warp (shared-memory slots); 2/3/4 single-warp
-// with 1/2/4 register slots per lane; 6 / 7 two / four selection warps
-// with one client per lane (33..64 / 65..128 clients)
-const void* select_fn(int warp_sel) {
-  switch (warp_sel) {
-    case 1: return reinterpret_cast<const void*>(select_warp_kernel<0>);
-    case 2: return reinterpret_cast<const void*>(select_warp_kernel<1>);
-    case 3: return reinterpret_cast<const void*>(select_warp_kernel<2>);
-    case 4: return reinterpret_cast<const void*>(select_warp_kernel<4>);
-    case 6: return reinterpret_cast<const void*>(select_warp_kernel<16>);
-    case 7: return reinterpret_cast<const void*>(select_warp_kernel<32>);
-    case 8: return reinterpret_cast<const void*>(select_topk_kernel);
-    default: return reinterpret_cast<const void*>(select_kernel);
-  }
-}
+// The selection kernel (one variant: rounds of block-radix top-K, eqx_topk.cuh).
+const void* select_fn(int) { return reinterpret_cast<const void*>(select_topk_kernel); }
 
 // Programmatic dependent launch: the kernel may be scheduled while its predecessor on the
 // stream is still finishing; it executes griddepcontrol.wait before touching the predecessor's
@@ -1229,19 +1221,11 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl, int32_t g
   a.pol = ctx->pol;
   a.frozen = ctx->live_mode ? ctx->frozen : Frozen{};
   a.now = now;
-  pl.select_threads = kSelectMaxThreads;
-  // Default: rounds of block-radix top-K over per-client key streams (select_topk_kernel,
-  // eqx_topk.cuh).  EQX_SELECT_MODE=seq keeps the sequential pick loops below (the reference
-  // loop one pick at a time; the -m gpu suite runs both).
-  // Sequential variants (each under -m gpu parity, tests/test_select_modes.py): seq (the pick
-  // loops below) and warp / slots / reg (their single-warp / register-slot forms).
-  const char* sel_mode = std::getenv("EQX_SELECT_MODE");
-  const std::string sm = sel_mode ? sel_mode : "";
-  const bool topk = !(sm == "seq" || sm == "warp" || sm == "slots" || sm == "reg");
-  if (topk) {
+  // Rounds of block-radix top-K over per-client key streams (select_topk_kernel, eqx_topk.cuh)
+  {
     const size_t static_smem = 12288;
     const int32_t kcap = kTopkThreads;
-    const size_t cw_bytes = 13ull * 16 + static_cast<size_t>(C) * (6 * 8 + 7 * 4);
+    const size_t cw_bytes = 11ull * 16 + static_cast<size_t>(C) * (4 * 8 + 7 * 4);
     const size_t k_bytes = static_cast<size_t>(kcap) * (6 * 4 + 3 * 8 + 3 * 4 + sizeof(WinEntry)) + 15 * 16 + 4 * 256 +
                            8 * 160 * (kTopkThreads / 32);
     const size_t heads_bytes = C > kcap ? 17 * static_cast<size_t>((C + 1) & ~1) + 16 : 0;
@@ -1283,84 +1267,11 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl, int32_t g
     a.tk_cap = static_cast<int32_t>(cap);
     a.tk_dsh = 6;
     a.tk_kcap = kcap;
-    a.K = 0;
-    a.Ds = 0;
-    a.sel_threads = kTopkThreads;
-    a.warp_sel = 8;
     pl.select_threads = kTopkThreads;
     pl.select_smem = smem;
     CUDA_TRY(ctx, ctx->d_win.ensure(std::max<size_t>(static_cast<size_t>(gW > 0 ? gW : a.W) * C * sizeof(WinEntry), 64)));
     a.win_g = ctx->d_win.as<WinEntry>();
-  } else {
-  // selection threads: one warp holding up to 8 clients per lane when C <= 256 (no barriers),
-  // otherwise up to 8 warps with 1/2/4/8 register slots per thread; beyond 2048 clients the
-  // shared-memory loop (seq_phase) takes over.
-  const int max_warps = kSelectMaxThreads / 32;
-  int K = 0, G = 1;
-  if (C <= 32) K = 1;
-  else if (C <= 64) K = 2;
-  else if (C <= 128) K = 4;
-  else if (C <= 256) K = 8;
-  else {
-    for (int k : {1, 2, 4, 8}) {
-      if (C <= 32 * max_warps * k) {
-        K = k;
-        G = (C + 32 * k - 1) / (32 * k);
-        break;
-      }
-    }
-    if (K == 0) G = max_warps;
   }
-  a.K = K;
-  a.sel_threads = 32 * G;
-  // shared memory: model | per-client work (if it fits) | batch scratch | head windows
-  const size_t static_smem = 12288;
-  const size_t cw_bytes = 13ull * 16 + static_cast<size_t>(C) * (6 * 8 + 7 * 4);
-  size_t smem = model_smem;
-  const size_t budget = ctx->smem_optin - static_smem - model_smem;
-  if (cw_bytes <= budget / 2) {
-    a.cw_in_smem = 1;
-    a.cw_global = nullptr;
-    smem += cw_bytes;
-  } else {
-    CUDA_TRY(ctx, ctx->d_cw.ensure(cw_bytes));
-    a.cw_in_smem = 0;
-    a.cw_global = ctx->d_cw.p;
-  }
-  // Register loop (default sequential form); EQX_SELECT_MODE=reg keeps the multi-warp register
-  // loop at any roster, warp / slots the single-warp forms (below).
-  a.warp_sel = !(sm == "reg");
-  // key streams of the register loop: up to 16 lookahead items (33 B each) per client, using
-  // at most a third of what is left (the head windows get the rest)
-  int64_t Ds = 0;
-  auto stream_bytes = [&](int64_t d) {
-    return 4 * ((8ull * C * d + 15) & ~15ull) + ((1ull * C * d + 15) & ~15ull) + 2 * ((4ull * C + 15) & ~15ull);
-  };
-  if (K > 0 && C > 0) {
-    const size_t left_s = ctx->smem_optin - static_smem - smem;
-    Ds = 16;
-    while (Ds >= 1 && stream_bytes(Ds) > left_s / 3) --Ds;
-    if (Ds < 1) {
-      Ds = 0;
-      K = 0;  // no room: shared-memory loop
-    }
-    a.K = K;
-  }
-  a.Ds = static_cast<int32_t>(Ds);
-  if (Ds) smem += stream_bytes(Ds);
-  const size_t left = ctx->smem_optin - static_smem - smem;
-  // A client is picked at most max_batch times before the slots run out (+1 for the next
-  // head's arrival); deeper heads (rejection streams) are scored on demand from HBM.
-  int64_t W = std::min<int64_t>(static_cast<int64_t>(ctx->perf.max_batch) + 2,
-                                C > 0 ? static_cast<int64_t>(left / (sizeof(WinEntry) * C)) : 0);
-  if (gW > 0) W = std::min<int64_t>(W, gW);
-  a.W = static_cast<int32_t>(std::max<int64_t>(W, 0));
-  a.gW = gW;
-  smem += static_cast<size_t>(a.W) * C * sizeof(WinEntry);
-  pl.select_smem = smem;
-  CUDA_TRY(ctx, ctx->d_win.ensure(std::max<size_t>(static_cast<size_t>(gW > 0 ? gW : a.W) * C * sizeof(WinEntry), 64)));
-  a.win_g = ctx->d_win.as<WinEntry>();
-  }  // sequential pick loops
   WindowArgs& wi = pl.wi;
   wi.arrival = ctx->q_arrival;
   wi.in_tok = ctx->q_in;
@@ -1395,19 +1306,7 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl, int32_t g
   pl.window_smem = model_smem;
   const int64_t witems = static_cast<int64_t>(C) * a.W;
   pl.window_grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((witems + 255) / 256, 8ll * ctx->sm_count)));
-  if (topk) {
-    CUDA_TRY(ctx, set_smem_attr(ctx, 10, select_fn(a.warp_sel), pl.select_smem));
-    return EQX_OK;
-  }
-  a.warp_sel = a.warp_sel && a.K > 0 && a.Ds > 0;
-  // kernel variant (select_fn): register slots up to 128 clients; larger rosters keep the
-  // multi-warp register loop (measured faster than the shared-memory single-warp variant,
-  // which stays selectable with EQX_SELECT_MODE=warp)
-  if (a.warp_sel) {
-    const bool slots = sm == "slots";  // one warp, 2 / 4 register slots per lane
-    a.warp_sel = C <= 32 ? 2 : C <= 64 ? (slots ? 3 : 6) : C <= 128 ? (slots ? 4 : 7) : sm == "warp" ? 1 : 0;
-  }
-  CUDA_TRY(ctx, set_smem_attr(ctx, a.warp_sel + 2, select_fn(a.warp_sel), pl.select_smem));
+  CUDA_TRY(ctx, set_smem_attr(ctx, 10, select_fn(0), pl.select_smem));
   return EQX_OK;
 }
 
@@ -1464,7 +1363,7 @@ static eqx_status step_enqueue(eqx_ctx* ctx, const StepPlan& pl, bool with_drain
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    CUDA_TRY(ctx, cudaLaunchKernelExC(&cfg, select_fn(pl.se.warp_sel), args));
+    CUDA_TRY(ctx, cudaLaunchKernelExC(&cfg, select_fn(0), args));
   }
   if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[3], s));
   CUDA_TRY(ctx, cudaGetLastError());
@@ -1678,6 +1577,25 @@ eqx_status eqx_replay(eqx_ctx* ctx, const eqx_replays* R, eqx_replay_out* O) {
   }
   CUDA_TRY(ctx, up(o_id, R->id ? static_cast<const void*>(R->id) : ids.data(), 8 * rows));
   if (O->rate && wcap > 0) CUDA_TRY(ctx, cudaMemsetAsync(b + o_rate, 0, 8 * n8 * c8 * w8, s));
+  // slots past a replay's own count (events, window samples) read back as zeros, not as stale
+  // scratch: the outputs a caller asked for start cleared
+  auto clear = [&](const void* want, size_t o, size_t bytes) {
+    return want && bytes ? cudaMemsetAsync(b + o, 0, bytes, s) : cudaSuccess;
+  };
+  CUDA_TRY(ctx, clear(O->ev_id, o_evid, 8 * n8 * cap));
+  CUDA_TRY(ctx, clear(O->ev_kind, o_evk, 4 * n8 * cap));
+  CUDA_TRY(ctx, clear(O->ev_time, o_evt, 8 * n8 * cap));
+  if (full) {
+    CUDA_TRY(ctx, clear(O->ev_i0, o_i0, 4 * n8 * cap));
+    CUDA_TRY(ctx, clear(O->ev_d0, o_d0, 8 * n8 * cap));
+    CUDA_TRY(ctx, clear(O->ev_d1, o_d1, 8 * n8 * cap));
+    CUDA_TRY(ctx, clear(O->ev_d2, o_d2, 8 * n8 * cap));
+  }
+  if (wcap > 0) {
+    CUDA_TRY(ctx, clear(O->win, o_win, 8 * 4 * n8 * w8));
+    CUDA_TRY(ctx, clear(O->win_clients, o_winc, 8 * 4 * n8 * w8 * c8));
+    CUDA_TRY(ctx, clear(O->diff, o_diff, 8 * 2 * n8 * w8));
+  }
   ReplayArgs A;
   std::memset(&A, 0, sizeof(A));
   A.n_replays = nr;
@@ -2152,7 +2070,7 @@ eqx_status eqx_shard_select_async(eqx_ctx* ctx, const void* recs, int32_t world,
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[2], s));
   {
     void* args[] = {const_cast<SelectArgs*>(&pl.se)};
-    CUDA_TRY(ctx, cudaLaunchKernel(select_fn(pl.se.warp_sel), dim3(1), dim3(pl.select_threads), args, pl.select_smem, s));
+    CUDA_TRY(ctx, cudaLaunchKernel(select_fn(0), dim3(1), dim3(pl.select_threads), args, pl.select_smem, s));
   }
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[3], s));
   CUDA_TRY(ctx, cudaGetLastError());

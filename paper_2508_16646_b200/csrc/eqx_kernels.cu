@@ -10,8 +10,7 @@
 //   admit_requests (engine.cpp:207-271):
 //     window_kernel      the first W queued requests of every client scored into [C][W] heads
 //     select_topk_kernel one CTA: rounds of block-radix top-K over per-client key streams
-//                        (eqx_topk.cuh); select_warp_kernel / select_kernel keep the
-//                        sequential pick loops (EQX_SELECT_MODE=seq)
+//                        (eqx_topk.cuh)
 //     score_kernel       whole-queue MoPE predict -> map_metrics -> ufc/rfc increments on a side
 //                        stream (16-byte streaming loads / stores: the HBM-bound stream)
 //     event_fill_kernel  event payloads and request ids from the per-request scores
@@ -985,70 +984,8 @@ __global__ void __launch_bounds__(kScoreTmaThreads, 2) score_tma_kernel(const Sc
 
 // ===================================== selection =========================================
 
-// Candidate tuple of select_next (scheduler.cpp:139-153): (key, head arrival, client_id rank),
-// all as integers.  o = 0xffffffff marks "no candidate".
-struct Cand {
-  uint64_t k;
-  uint64_t a;
-  uint32_t o;
-};
-
-__device__ __forceinline__ bool better(const Cand& x, const Cand& y) {
-  const bool lt = (x.k < y.k) | ((x.k == y.k) & ((x.a < y.a) | ((x.a == y.a) & (x.o < y.o))));
-  return (x.o != 0xffffffffu) & ((y.o == 0xffffffffu) | lt);
-}
-
-__device__ __forceinline__ Cand no_cand() { return Cand{~0ull, ~0ull, 0xffffffffu}; }
-
-// Warp argmin of the (key, arrival, rank) tuples: two redux.sync mins on the key halves and a
-// ballot settle it unless several lanes share the minimal key (then arrival and rank decide
-// through the same redux pattern).  Sentinels carry k = a = ~0 and o = ~0.
-__device__ __forceinline__ Cand warp_argmin(Cand v) {
-  const uint32_t hi = static_cast<uint32_t>(v.k >> 32), lo = static_cast<uint32_t>(v.k);
-  const uint32_t mhi = __reduce_min_sync(0xffffffffu, hi);
-  const uint32_t mlo = __reduce_min_sync(0xffffffffu, hi == mhi ? lo : 0xffffffffu);
-  unsigned m = __ballot_sync(0xffffffffu, hi == mhi && lo == mlo);
-  if (__popc(m) > 1) {  // equal keys: arrival, then client rank
-    const bool in = (m >> (threadIdx.x & 31)) & 1u;
-    const uint32_t ahi = static_cast<uint32_t>(v.a >> 32), alo = static_cast<uint32_t>(v.a);
-    const uint32_t mahi = __reduce_min_sync(0xffffffffu, in ? ahi : 0xffffffffu);
-    const bool in2 = in && ahi == mahi;
-    const uint32_t malo = __reduce_min_sync(0xffffffffu, in2 ? alo : 0xffffffffu);
-    const bool in3 = in2 && alo == malo;
-    const uint32_t mo = __reduce_min_sync(0xffffffffu, in3 ? v.o : 0xffffffffu);
-    m = __ballot_sync(0xffffffffu, in3 && v.o == mo);
-  }
-  const int src = __ffs(m) - 1;
-  Cand w;
-  w.k = __shfl_sync(0xffffffffu, v.k, src);
-  w.a = __shfl_sync(0xffffffffu, v.a, src);
-  w.o = __shfl_sync(0xffffffffu, v.o, src);
-  return w;
-}
-
-// Lane holding the warp minimum (same tie-break as warp_argmin).
-__device__ __forceinline__ int warp_argmin_lane(const Cand& v) {
-  const uint32_t hi = static_cast<uint32_t>(v.k >> 32), lo = static_cast<uint32_t>(v.k);
-  const uint32_t mhi = __reduce_min_sync(0xffffffffu, hi);
-  const uint32_t mlo = __reduce_min_sync(0xffffffffu, hi == mhi ? lo : 0xffffffffu);
-  unsigned m = __ballot_sync(0xffffffffu, hi == mhi && lo == mlo);
-  if (__popc(m) > 1) {
-    const bool in = (m >> (threadIdx.x & 31)) & 1u;
-    const uint32_t ahi = static_cast<uint32_t>(v.a >> 32), alo = static_cast<uint32_t>(v.a);
-    const uint32_t mahi = __reduce_min_sync(0xffffffffu, in ? ahi : 0xffffffffu);
-    const bool in2 = in && ahi == mahi;
-    const uint32_t malo = __reduce_min_sync(0xffffffffu, in2 ? alo : 0xffffffffu);
-    const bool in3 = in2 && alo == malo;
-    const uint32_t mo = __reduce_min_sync(0xffffffffu, in3 ? v.o : 0xffffffffu);
-    m = __ballot_sync(0xffffffffu, in3 && v.o == mo);
-  }
-  return __ffs(m) - 1;
-}
-
 // Per-client working state of the loop (shared memory, or global scratch for huge rosters).
 struct ClientWork {
-  uint64_t* kb;     // ordered bits of the selection key of the current head
-  uint64_t* ab;     // ordered bits of the head arrival
   double* ufc;
   double* rfc;
   double* cnt;
@@ -1063,10 +1000,9 @@ struct ClientWork {
 };
 
 enum : int32_t { kBacklogged = 1, kSkipped = 2 };
-enum : int32_t { kDone = 1, kDirty = 2, kNeedMax = 4 };
+enum : int32_t { kDone = 1 };
 
 struct SelShared {
-  Cand wbest[32];
   double red_u[32], red_r[32];
   double max_u, max_r;
   int32_t flags;
@@ -1126,13 +1062,6 @@ __device__ __noinline__ WinEntry deep_entry(const SelectArgs& a, const ModelTabl
   return make_entry(a, M, static_cast<int32_t>(a.perm[a.seg_off[c] + j]), w);
 }
 
-__device__ __forceinline__ WinEntry get_entry(const SelectArgs& a, const ModelTables& M, const WinEntry* win,
-                                              const ClientWork& cw, int32_t c, int32_t j) {
-  const int32_t k = j - cw.pos0[c];
-  if (k < a.W) return win[static_cast<int64_t>(c) * a.W + k];
-  return deep_entry(a, M, c, j, k, cw.w[c]);
-}
-
 // First W queued entries of every client (C*W items, one per thread across many CTAs).
 __global__ void __launch_bounds__(256) window_kernel(const WindowArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -1161,153 +1090,6 @@ __global__ void __launch_bounds__(256) window_kernel(const WindowArgs a) {
   __syncthreads();
   if (threadIdx.x == 0) atomicMax(&a.st->dt[6], global_ns());
 #endif
-}
-
-__device__ __forceinline__ Cand cand_of(const ClientWork& cw, int32_t c) {
-  if (cw.pos[c] < cw.end[c] && !(cw.flags[c] & kSkipped)) return Cand{cw.kb[c], cw.ab[c], cw.order[c]};
-  return no_cand();
-}
-
-// One iteration of admit_requests' loop body for the chosen client (engine.cpp:216-268),
-// run by the thread that owns the client.  Returns kDone / kDirty / kNeedMax.
-__device__ __forceinline__ int32_t process_pick(const SelectArgs& a, const ModelTables& M, const WinEntry* win,
-                                                const ClientWork& cw, SelShared& S, int32_t c) {
-  const Policy& P = a.pol;
-  const bool maxmode = P.kind == kEquinox && P.norm_mode == 0;
-  const int32_t j = cw.pos[c];
-  const WinEntry e = get_entry(a, M, win, cw, c, j);
-  if (!e.alone) {  // engine.cpp:223-234: Rejected, pop_head, no counter change
-    const int64_t k = S.n_ev++;
-    if (k < a.ev_cap) {
-      a.ev_row[k] = e.row;
-      a.ev_kind[k] = 2;
-      a.ev_client[k] = c;
-    }
-    S.n_rej++;
-    cw.pos[c] = j + 1;
-    if (j + 1 == cw.end[c]) {
-      cw.flags[c] &= ~kBacklogged;
-      if (maxmode && (cw.ufc[c] == S.max_u || cw.rfc[c] == S.max_r)) return kDirty | kNeedMax;
-    } else {
-      cw.ab[c] = get_entry(a, M, win, cw, c, j + 1).abits;
-    }
-    return 0;
-  }
-  // can_fit (gpu_model.cpp:58-67) with the KV test as the exact integer threshold
-  if (!((S.members + 1 <= P.max_batch) && (S.reserved + e.in + e.pred <= a.tmax))) {
-    if (P.backfill) {  // engine.cpp:236-238
-      cw.flags[c] |= kSkipped;
-      return 0;
-    }
-    return kDone;  // engine.cpp:239
-  }
-  // admit (engine.cpp:242-268) + on_admit (scheduler.cpp:158-183)
-  S.members += 1;
-  S.reserved += static_cast<int64_t>(e.in) + e.pred;  // reserved_output = pred, generated = 0
-  S.prefill += e.in;
-  const double old_u = cw.ufc[c], old_r = cw.rfc[c];
-  const double nu = __dadd_rn(old_u, e.ufc_inc), nr = __dadd_rn(old_r, e.rfc_inc);
-  cw.ufc[c] = nu;
-  cw.rfc[c] = nr;
-  double vtc = 0.0;
-  if (P.kind == kVtc) {
-    const double w = cw.w[c];
-    vtc = P.vtc_use_prediction
-              ? __dmul_rn(w, __dadd_rn(static_cast<double>(e.in), __dmul_rn(P.ow, static_cast<double>(e.pred))))
-              : __dmul_rn(w, static_cast<double>(e.in));
-    cw.cnt[c] = __dadd_rn(cw.cnt[c], vtc);
-  }
-  cw.adm[c] += 1;
-  const int64_t k = S.n_ev++;
-  if (k < a.ev_cap) {
-    a.ev_row[k] = e.row;
-    a.ev_kind[k] = 1;
-    a.ev_client[k] = c;
-  }
-  S.n_adm++;
-  cw.pos[c] = j + 1;
-  if (j + 1 == cw.end[c]) {  // pop_head emptied the queue: set_backlogged(false)
-    cw.flags[c] &= ~kBacklogged;
-    if (maxmode && (old_u == S.max_u || old_r == S.max_r)) return kDirty | kNeedMax;
-    return 0;
-  }
-  cw.ab[c] = get_entry(a, M, win, cw, c, j + 1).abits;
-  if (maxmode) {
-    bool d = false;
-    if (S.max_u < nu) {
-      S.max_u = nu;
-      d = true;
-    }
-    if (S.max_r < nr) {
-      S.max_r = nr;
-      d = true;
-    }
-    if (d) return kDirty;
-  }
-  cw.kb[c] = ordered_bits(hf_key(P, nu, nr, S.max_u, S.max_r, cw.cnt[c]));
-  return 0;
-}
-
-__device__ __forceinline__ Cand rescan_owned(const ClientWork& cw, int32_t C, int tid, int nthr) {
-  Cand best = no_cand();
-  for (int32_t c = tid; c < C; c += nthr) {
-    const Cand v = cand_of(cw, c);
-    if (better(v, best)) best = v;
-  }
-  return best;
-}
-
-__device__ __forceinline__ Cand recompute_owned(const Policy& P, const ClientWork& cw, int32_t C, int tid, int nthr,
-                                                double mu, double mr) {
-  Cand best = no_cand();
-  for (int32_t c = tid; c < C; c += nthr) {
-    cw.kb[c] = ordered_bits(hf_key(P, cw.ufc[c], cw.rfc[c], mu, mr, cw.cnt[c]));
-    const Cand v = cand_of(cw, c);
-    if (better(v, best)) best = v;
-  }
-  return best;
-}
-
-// Max over backlogged clients (scheduler.cpp:40-48), starting from 0.0 like the reference.
-__device__ __forceinline__ void group_maxima(const ClientWork& cw, int32_t C, int tid, int nthr, SelShared& S) {
-  double mu = 0.0, mr = 0.0;
-  for (int32_t c = tid; c < C; c += nthr) {
-    if (!(cw.flags[c] & kBacklogged)) continue;
-    if (mu < cw.ufc[c]) mu = cw.ufc[c];
-    if (mr < cw.rfc[c]) mr = cw.rfc[c];
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    const double ou = __shfl_xor_sync(0xffffffffu, mu, o);
-    const double orr = __shfl_xor_sync(0xffffffffu, mr, o);
-    if (mu < ou) mu = ou;
-    if (mr < orr) mr = orr;
-  }
-  const int nw = nthr >> 5;
-  if (nw == 1) {
-    if (tid == 0) {
-      S.max_u = mu;
-      S.max_r = mr;
-    }
-    __syncwarp();
-    return;
-  }
-  const int lane = tid & 31, warp = tid >> 5;
-  if (lane == 0) {
-    S.red_u[warp] = mu;
-    S.red_r[warp] = mr;
-  }
-  named_sync(1, nthr);
-  if (tid == 0) {
-    double u = 0.0, r = 0.0;
-    for (int w = 0; w < nw; ++w) {
-      if (u < S.red_u[w]) u = S.red_u[w];
-      if (r < S.red_r[w]) r = S.red_r[w];
-    }
-    S.max_u = u;
-    S.max_r = r;
-  }
-  named_sync(1, nthr);
 }
 
 // Outcome flags of a generated key-stream item (the top-K rounds, eqx_topk.cuh, and the
@@ -1356,1183 +1138,14 @@ __device__ void cta_maxima(const ClientWork& cw, int32_t C, SelShared& S) {
 
 
 
-// Sequential picks (the exact admit_requests loop) for up to max_picks picks by the first
-// a.sel_threads threads; the others wait at the CTA barrier that follows.
-__device__ void seq_phase(const SelectArgs& a, const ModelTables& M, const WinEntry* win, const ClientWork& cw,
-                          SelShared& S, int32_t max_picks) {
-  const int32_t C = a.C;
-  const int tid = threadIdx.x, nthr = a.sel_threads;
-  if (tid >= nthr) return;
-  const Policy& P = a.pol;
-  const int lane = tid & 31, warp = tid >> 5, nw = nthr >> 5;
-  for (int32_t c = tid; c < C; c += nthr)
-    cw.ab[c] = cw.pos[c] < cw.end[c] ? get_entry(a, M, win, cw, c, cw.pos[c]).abits : 0ull;
-  Cand local = recompute_owned(P, cw, C, tid, nthr, S.max_u, S.max_r);
-  named_sync(1, nthr);
-  int32_t picks = 0;
-  long long cy_arg = 0, cy_proc = 0, cy_tail = 0, t_a = clock64();
-  for (;;) {
-    if (picks++ >= max_picks) break;
-    Cand v = warp_argmin(local);
-    if (nw > 1) {  // every warp reduces the warp winners redundantly: one barrier per pick
-      if (lane == 0) S.wbest[warp] = v;
-      named_sync(1, nthr);
-      v = warp_argmin(lane < nw ? S.wbest[lane] : no_cand());
-    }
-    if (v.o == 0xffffffffu) {  // no candidates (engine.cpp:217)
-      if (tid == 0) S.flags = kDone;
-      break;
-    }
-    const int32_t c = cw.by_order[v.o];
-    const int owner = c % nthr;
-    int32_t f = 0;
-    const long long t_b = clock64();
-    if (tid == owner) f = process_pick(a, M, win, cw, S, c);
-    if (nw == 1) {
-      f = __shfl_sync(0xffffffffu, f, owner);
-      __syncwarp();
-      const long long t_c = clock64();
-      cy_arg += t_b - t_a;
-      cy_proc += t_c - t_b;
-      t_a = t_c;
-    } else {
-      if (tid == owner) S.flags = f;
-      named_sync(1, nthr);
-      f = S.flags;
-    }
-    if (f & kDone) {
-      if (tid == 0) S.flags = kDone;
-      break;
-    }
-    if (f & kDirty) {
-      if (f & kNeedMax) group_maxima(cw, C, tid, nthr, S);
-      local = recompute_owned(P, cw, C, tid, nthr, S.max_u, S.max_r);
-    } else if (tid == owner) {
-      local = rescan_owned(cw, C, tid, nthr);
-    }
-    if (nw > 1) named_sync(1, nthr);
-    if (nw == 1) {
-      const long long t_d = clock64();
-      cy_tail += t_d - t_a;
-      t_a = t_d;
-    }
-  }
-  if (tid == 0) {
-    a.st->t[12] += cy_arg;
-    a.st->t[13] += cy_proc;
-    a.st->t[14] += cy_tail;
-    a.st->t[15] += picks;
-  }
-}
-
-// ---- register-resident sequential picks over precomputed key streams ----------------------
-// Every selection thread owns K client slots in registers.  For each slot the next Ds keys
-// (and the ledger after each of those requests) are generated ahead under the current maxima
-// (the same sequential FP64 adds and divisions as on_admit + holistic_score), so a pick is a
-// warp argmin (redux) plus shared-memory lookups evaluated *uniformly* by every thread
-// (replicated batch counters and maxima, no divergence); only the owner writes its slot.
-// Streams are regenerated when a maximum moves (an admission above it, or a max holder
-// leaving the backlog) and per client when its stream runs out.
-struct WarpWin {
-  uint64_t k, a;
-  uint32_t o;
-  int32_t c, pos, pos0, end, d;
-};
-
-struct StreamScratch {
-  uint64_t* k;  // [C][Ds] key of lookahead item d
-  double* u;    // [C][Ds] ufc after item d (unchanged when rejected)
-  double* r;
-  double* cn;   // VTC counter after item d
-  uint8_t* fl;  // [C][Ds] kFlAlone | kFlMaxChg | kFlHolder
-  int32_t* sd;  // [C] stream cursor (item of the current head)
-  int32_t* sdl; // [C] items generated
-  int32_t Ds;
-};
-
-template <int K>
-__device__ void seq_reg_phase(const SelectArgs& a, const ModelTables& M, const WinEntry* win, const ClientWork& cw,
-                              SelShared& S, int32_t max_picks, const StreamScratch& T) {
-  const int nthr = a.sel_threads, tid = threadIdx.x;
-  if (tid >= nthr) return;
-  __shared__ WarpWin s_ww[2][kSelectMaxThreads / 32];
-  __shared__ double s_mx[2][kSelectMaxThreads / 32][2];
-  const int lane = tid & 31, warp = tid >> 5, G = nthr >> 5;
-  const int32_t C = a.C, W = a.W, Ds = T.Ds;
-  const Policy P = a.pol;
-  const bool maxmode = P.kind == kEquinox && P.norm_mode == 0;
-  const int64_t tmax = a.tmax;
-  double su[K], sr[K], sk[K];
-  uint64_t skb[K], sab[K];
-  int32_t spos[K], send[K], spos0[K], sfl[K], sadm[K], sd[K], sdl[K];
-  uint32_t so[K];
-#pragma unroll
-  for (int s = 0; s < K; ++s) {
-    const int32_t c = tid + s * nthr;
-    sd[s] = sdl[s] = 0;
-    skb[s] = sab[s] = ~0ull;
-    if (c < C) {
-      su[s] = cw.ufc[c];
-      sr[s] = cw.rfc[c];
-      sk[s] = cw.cnt[c];
-      spos[s] = cw.pos[c];
-      send[s] = cw.end[c];
-      spos0[s] = cw.pos0[c];
-      sfl[s] = cw.flags[c];
-      sadm[s] = cw.adm[c];
-      so[s] = cw.order[c];
-    } else {
-      su[s] = sr[s] = sk[s] = 0.0;
-      spos[s] = send[s] = spos0[s] = 0;
-      sfl[s] = kSkipped;
-      sadm[s] = 0;
-      so[s] = 0xffffffffu;
-    }
-  }
-  int32_t members = S.members;
-  int64_t reserved = S.reserved, n_ev = S.n_ev, n_adm = S.n_adm, n_rej = S.n_rej, prefill = S.prefill;
-  double mu = S.max_u, mr = S.max_r;
-  auto entry = [&](int32_t c, int32_t j, int32_t pos0) -> WinEntry {
-    const int32_t k = j - pos0;
-    return k < W ? win[static_cast<int64_t>(c) * W + k] : deep_entry(a, M, c, j, k, cw.w[c]);
-  };
-  // (re)generate the lookahead stream of slot s under the current maxima
-  auto gen = [&](int s, int depth) {
-    const int32_t c = tid + s * nthr;
-    sd[s] = 0;
-    sdl[s] = 0;
-    if (!(spos[s] < send[s]) || (sfl[s] & kSkipped)) return;
-    double u = su[s], r = sr[s], k = sk[s];
-    const int32_t pos = spos[s], end = send[s], pos0 = spos0[s];
-    int d = 0;
-    for (; d < depth; ++d) {
-      const int32_t j = pos + d;
-      if (j >= end) break;
-      const WinEntry e = entry(c, j, pos0);
-      const uint64_t key = ordered_bits(hf_key(P, u, r, mu, mr, k));
-      uint8_t f = 0;
-      double nu = u, nr = r, nk = k;
-      if (e.alone) {
-        f |= kFlAlone;
-        nu = __dadd_rn(u, e.ufc_inc);
-        nr = __dadd_rn(r, e.rfc_inc);
-        if (P.kind == kVtc) nk = __dadd_rn(k, vtc_inc(P, e, cw.w[c]));
-      }
-      if (j + 1 == end) {
-        if (maxmode && (u == mu || r == mr)) f |= kFlHolder;  // a max holder leaves the backlog
-      } else if (e.alone && maxmode && (mu < nu || mr < nr)) {
-        f |= kFlMaxChg;  // this admission raises a maximum
-      }
-      const int64_t x = static_cast<int64_t>(c) * Ds + d;
-      T.k[x] = key;
-      T.u[x] = nu;
-      T.r[x] = nr;
-      T.cn[x] = nk;
-      T.fl[x] = f;
-      u = nu;
-      r = nr;
-      k = nk;
-    }
-    sdl[s] = d;
-    if (d > 0) {
-      skb[s] = T.k[static_cast<int64_t>(c) * Ds];
-      sab[s] = entry(c, pos, pos0).abits;
-    }
-  };
-  int depth = Ds, since_regen = 1 << 30;
-#pragma unroll
-  for (int s = 0; s < K; ++s) gen(s, depth);
-  __syncwarp();
-  if (G > 1) named_sync(1, nthr);
-  int parity = 0;
-  bool done = false;
-#ifdef EQX_PROF
-  long long cy0 = 0, cy1 = 0, cy2 = 0, cyp = 0;
-#endif
-  for (int32_t pick = 0; pick < max_picks; ++pick) {
-#ifdef EQX_PROF
-    const long long ta = clock64();
-#endif
-    Cand best = no_cand();
-    int bs = 0;
-#pragma unroll
-    for (int s = 0; s < K; ++s) {
-      if (spos[s] < send[s] && !(sfl[s] & kSkipped)) {
-        const Cand v{skb[s], sab[s], so[s]};
-        if (better(v, best)) {
-          best = v;
-          bs = s;
-        }
-      }
-    }
-    const int src = warp_argmin_lane(best);
-    WarpWin w;
-    {
-      int32_t pos = 0, pos0 = 0, end = 0, dd = 0;
-#pragma unroll
-      for (int s = 0; s < K; ++s)
-        if (s == bs) {
-          pos = spos[s];
-          pos0 = spos0[s];
-          end = send[s];
-          dd = sd[s];
-        }
-      const int32_t cc = tid + bs * nthr;
-      if (G == 1) {
-        w.o = __shfl_sync(0xffffffffu, best.o, src);
-        w.c = __shfl_sync(0xffffffffu, cc, src);
-        w.pos = __shfl_sync(0xffffffffu, pos, src);
-        w.pos0 = __shfl_sync(0xffffffffu, pos0, src);
-        w.end = __shfl_sync(0xffffffffu, end, src);
-        w.d = __shfl_sync(0xffffffffu, dd, src);
-      } else {
-        if (lane == src) s_ww[parity][warp] = WarpWin{best.k, best.a, best.o, cc, pos, pos0, end, dd};
-        named_sync(1, nthr);
-        const WarpWin x = lane < G ? s_ww[parity][lane] : WarpWin{~0ull, ~0ull, 0xffffffffu, 0, 0, 0, 0, 0};
-        const int wl = warp_argmin_lane(Cand{x.k, x.a, x.o});
-        w = s_ww[parity][wl < G ? wl : 0];
-        if (wl >= G) w.o = 0xffffffffu;
-        parity ^= 1;
-      }
-    }
-    if (w.o == 0xffffffffu) {  // no candidates (engine.cpp:217)
-      done = true;
-      break;
-    }
-#ifdef EQX_PROF
-    const long long tb = clock64();
-#endif
-    // ---- uniform evaluation of the pick (engine.cpp:216-268) ----
-    const int32_t c = w.c, j = w.pos;
-    const int64_t x = static_cast<int64_t>(c) * Ds + w.d;
-    const WinEntry e = entry(c, j, w.pos0);
-    const uint8_t fl = T.fl[x];
-    const bool owner = (c % nthr) == tid;
-    const int os = c / nthr;
-    int32_t kind;
-    if (!e.alone) {
-      kind = 2;  // Rejected, pop_head, no counter change
-      ++n_rej;
-    } else if (!((members + 1 <= P.max_batch) && (reserved + e.in + e.pred <= tmax))) {
-      if (!P.backfill) {
-        done = true;
-        break;
-      }
-      kind = 0;  // skipped for the rest of the step
-    } else {
-      kind = 1;
-      members += 1;
-      reserved += static_cast<int64_t>(e.in) + e.pred;
-      prefill += e.in;
-      ++n_adm;
-    }
-    const bool leaving = kind != 0 && j + 1 == w.end;
-    const bool maxchg = kind == 1 && (fl & kFlMaxChg);
-    const bool holder = kind != 0 && (fl & kFlHolder);
-    double nu = 0.0, nr = 0.0;
-    if (kind != 0) {
-      if (lane == 0 && warp == 0 && n_ev < a.ev_cap) {
-        a.ev_row[n_ev] = e.row;
-        a.ev_kind[n_ev] = kind;
-        a.ev_client[n_ev] = c;
-      }
-      ++n_ev;
-      nu = T.u[x];
-      nr = T.r[x];
-    }
-    bool own_regen = false;
-#ifdef EQX_PROF
-    const long long tc = clock64();
-#endif
-    if (owner) {
-#pragma unroll
-      for (int s = 0; s < K; ++s)
-        if (s == os) {
-          if (kind == 0) {
-            sfl[s] |= kSkipped;
-          } else {
-            spos[s] = j + 1;
-            su[s] = nu;
-            sr[s] = nr;
-            sk[s] = T.cn[x];
-            if (kind == 1) sadm[s] += 1;
-            if (leaving) {
-              sfl[s] &= ~kBacklogged;
-            } else {
-              sd[s] += 1;
-              if (sd[s] < sdl[s]) {
-                skb[s] = T.k[x + 1];
-                sab[s] = entry(c, j + 1, spos0[s]).abits;
-              } else {
-                own_regen = true;
-              }
-            }
-          }
-        }
-    }
-    ++since_regen;
-    if (maxchg || holder) {
-      if (maxchg) {  // the new maximum is the admitted client's counter
-        if (mu < nu) mu = nu;
-        if (mr < nr) mr = nr;
-      } else {  // max over backlogged clients (scheduler.cpp:40-48)
-        double xu = 0.0, xr = 0.0;
-#pragma unroll
-        for (int s = 0; s < K; ++s)
-          if (sfl[s] & kBacklogged) {
-            if (xu < su[s]) xu = su[s];
-            if (xr < sr[s]) xr = sr[s];
-          }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-          const double ou = __shfl_xor_sync(0xffffffffu, xu, o), orr = __shfl_xor_sync(0xffffffffu, xr, o);
-          if (xu < ou) xu = ou;
-          if (xr < orr) xr = orr;
-        }
-        if (G > 1) {
-          if (lane == 0) {
-            s_mx[parity][warp][0] = xu;
-            s_mx[parity][warp][1] = xr;
-          }
-          named_sync(1, nthr);
-          xu = 0.0;
-          xr = 0.0;
-          for (int g = 0; g < G; ++g) {
-            if (xu < s_mx[parity][g][0]) xu = s_mx[parity][g][0];
-            if (xr < s_mx[parity][g][1]) xr = s_mx[parity][g][1];
-          }
-          parity ^= 1;
-        }
-        mu = xu;
-        mr = xr;
-      }
-      // maxima moving every few picks (cold ledgers): short lookahead; otherwise the full one
-      depth = since_regen < 4 ? 1 : Ds;
-      since_regen = 0;
-#pragma unroll
-      for (int s = 0; s < K; ++s) gen(s, depth);
-    } else if (own_regen) {
-#pragma unroll
-      for (int s = 0; s < K; ++s)
-        if (s == os) gen(s, Ds);
-    }
-    __syncwarp();
-    if (G > 1) named_sync(1, nthr);
-#ifdef EQX_PROF
-    const long long td = clock64();
-    cy0 += tb - ta;
-    cy1 += tc - tb;
-    cy2 += td - tc;
-    ++cyp;
-#endif
-  }
-#ifdef EQX_PROF
-  if (tid == 0) {
-    a.st->t[12] += cy0;
-    a.st->t[13] += cy1;
-    a.st->t[14] += cy2;
-    a.st->t[15] += cyp;
-  }
-#endif
-#pragma unroll
-  for (int s = 0; s < K; ++s) {
-    const int32_t c = tid + s * nthr;
-    if (c < C) {
-      cw.ufc[c] = su[s];
-      cw.rfc[c] = sr[s];
-      cw.cnt[c] = sk[s];
-      cw.pos[c] = spos[s];
-      cw.flags[c] = sfl[s];
-      cw.adm[c] = sadm[s];
-    }
-  }
-  if (tid == 0) {
-    S.members = members;
-    S.reserved = reserved;
-    S.n_ev = n_ev;
-    S.n_adm = n_adm;
-    S.n_rej = n_rej;
-    S.prefill = prefill;
-    S.max_u = mu;
-    S.max_r = mr;
-    S.flags = done ? kDone : 0;
-  }
-}
-
-// ---- single-warp selection with winner-lane updates -------------------------------------
-// Warp 0 runs the exact admit_requests loop; lane L owns clients L, L+32, ...  Every client's
-// next Ds keys (and the ledger after each of those requests) are generated ahead under the
-// current maxima (same sequential FP64 adds/divisions as on_admit + holistic_score), so
-// cw.kb/cw.ab hold each client's current head tuple (~0 = not a candidate).  Each lane keeps
-// its best candidate and that candidate's pick outcome (reject / admit / skip / stop, from the
-// replicated batch counters) in registers; a pick is a warp argmin (redux) plus one broadcast
-// of the winner's outcome, after which only the winning lane touches shared memory (advance
-// the client's stream, rescan its own clients).  A maximum moving (an admission above it, or a
-// max holder leaving the backlog) regenerates every stream with the whole CTA: the other
-// warps wait at a barrier for such commands.
-enum : int32_t { kCmdRegen = 1, kCmdMaxRegen = 2, kCmdExit = 3 };
-enum : int32_t { kOutNone = 0, kOutRej = 1, kOutAdm = 2, kOutSkip = 3, kOutStop = 4 };
-
-struct WarpSelShared {
-  int32_t cmd, depth;
-};
-
-// (Re)generate client c's stream from its current head under the maxima (mu, mr).
-__device__ __forceinline__ void gen_stream(const SelectArgs& a, const ModelTables& M, const WinEntry* win,
-                                           const ClientWork& cw, const StreamScratch& T, int32_t c, int depth,
-                                           double mu, double mr) {
-  const Policy& P = a.pol;
-  const bool maxmode = P.kind == kEquinox && P.norm_mode == 0;
-  const int32_t pos = cw.pos[c], end = cw.end[c], pos0 = cw.pos0[c];
-  T.sd[c] = 0;
-  if (!(pos < end) || (cw.flags[c] & kSkipped)) {
-    T.sdl[c] = 0;
-    cw.kb[c] = ~0ull;
-    return;
-  }
-  double u = cw.ufc[c], r = cw.rfc[c], k = cw.cnt[c];
-  const double w = cw.w[c];
-  const int64_t base = static_cast<int64_t>(c) * T.Ds;
-  int d = 0;
-  for (; d < depth && pos + d < end; ++d) {
-    const int32_t j = pos + d, kk = j - pos0;
-    const WinEntry e = kk < a.W ? win[static_cast<int64_t>(c) * a.W + kk] : deep_entry(a, M, c, j, kk, w);
-    if (d == 0) cw.ab[c] = e.abits;
-    uint8_t f = 0;
-    double nu = u, nr = r, nk = k;
-    if (e.alone) {
-      f |= kFlAlone;
-      nu = __dadd_rn(u, e.ufc_inc);
-      nr = __dadd_rn(r, e.rfc_inc);
-      if (P.kind == kVtc) nk = __dadd_rn(k, vtc_inc(P, e, w));
-    }
-    if (j + 1 == end) {
-      if (maxmode && (u == mu || r == mr)) f |= kFlHolder;  // a max holder leaves the backlog
-    } else if (e.alone && maxmode && (mu < nu || mr < nr)) {
-      f |= kFlMaxChg;  // this admission raises a maximum
-    }
-    T.k[base + d] = ordered_bits(hf_key(P, u, r, mu, mr, k));
-    T.u[base + d] = nu;
-    T.r[base + d] = nr;
-    T.cn[base + d] = nk;
-    T.fl[base + d] = f;
-    u = nu;
-    r = nr;
-    k = nk;
-  }
-  T.sdl[c] = d;
-  cw.kb[c] = T.k[base];
-}
-
-__device__ __forceinline__ void warp_select_phase(const SelectArgs& a, const ModelTables& M, const WinEntry* win,
-                                                  const ClientWork& cw, SelShared& S, const StreamScratch& T) {
-  __shared__ WarpSelShared X;
-  const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31;
-  const int32_t C = a.C, Ds = T.Ds, W = a.W;
-  const Policy P = a.pol;
-  auto regen_all = [&](int depth) {
-    for (int32_t c = tid; c < C; c += NT) gen_stream(a, M, win, cw, T, c, depth, S.max_u, S.max_r);
-  };
-  // initial streams (maxima from cta_maxima)
-  regen_all(Ds);
-  __syncthreads();
-  if (tid >= 32) {  // helper warps: CTA-wide stream regeneration on command
-    for (;;) {
-      __syncthreads();
-      const int32_t cmd = X.cmd;
-      if (cmd == kCmdExit) break;
-      if (cmd == kCmdMaxRegen) cta_maxima(cw, C, S);
-      regen_all(X.depth);
-      __syncthreads();
-    }
-    return;
-  }
-  // ---------------- selection warp ----------------
-  uint64_t* const kb = cw.kb;
-  uint64_t* const ab = cw.ab;
-  const uint32_t* const order = cw.order;
-  int32_t* const posv = cw.pos;
-  const int32_t* const pos0v = cw.pos0;
-  const int32_t* const endv = cw.end;
-  const int32_t K = (C + 31) >> 5;  // clients per lane
-  const int64_t tmax = a.tmax;
-  int32_t members = S.members;
-  int64_t reserved = S.reserved, n_ev = S.n_ev, n_adm = S.n_adm, n_rej = S.n_rej, prefill = S.prefill;
-  // The lane's best candidate and everything a pick of it needs, prefetched so that the
-  // winning lane's update is stores only.
-  uint64_t bk = ~0ull, ba = ~0ull, bnk = ~0ull, bna = ~0ull;
-  uint32_t bo = 0xffffffffu;
-  int32_t bc = -1, bin = 0, brow = 0, bflags = 0, bpos = 0, bd = 0;
-  int64_t bneed = 0;
-  double bnu = 0.0, bnr = 0.0, bncn = 0.0;
-  auto head_entry = [&](int32_t c, int32_t j) -> WinEntry {
-    const int32_t kk = j - pos0v[c];
-    return kk < W ? win[static_cast<int64_t>(c) * W + kk] : deep_entry(a, M, c, j, kk, cw.w[c]);
-  };
-  auto lane_best = [&]() {
-    bk = ~0ull;
-    ba = ~0ull;
-    bo = 0xffffffffu;
-    bc = -1;
-    for (int32_t i = 0; i < K; ++i) {
-      const int32_t c = lane + 32 * i;
-      if (c >= C) break;
-      const uint64_t k = kb[c];
-      if (k == ~0ull) continue;
-      const uint64_t av = ab[c];
-      const uint32_t o = order[c];
-      const bool lt = (k < bk) | ((k == bk) & ((av < ba) | ((av == ba) & (o < bo))));
-      if (bc < 0 || lt) {
-        bk = k;
-        ba = av;
-        bo = o;
-        bc = c;
-      }
-    }
-    if (bc >= 0) {
-      const int32_t c = bc, j = posv[c], d = T.sd[c], dl = T.sdl[c], end = endv[c];
-      const int64_t x = static_cast<int64_t>(c) * Ds + d;
-      const WinEntry e = head_entry(c, j);
-      const uint8_t f = T.fl[x];
-      bpos = j;
-      bd = d;
-      bin = e.in;
-      brow = e.row;
-      bneed = static_cast<int64_t>(e.in) + e.pred;
-      bnu = T.u[x];
-      bnr = T.r[x];
-      bncn = T.cn[x];
-      const bool leaving = j + 1 == end, more = d + 1 < dl;
-      bflags = (e.alone ? 1 : 0) | ((f & kFlMaxChg) ? 2 : 0) | ((f & kFlHolder) ? 4 : 0) | (leaving ? 8 : 0) |
-               (more ? 16 : 0);
-      if (!leaving && more) {
-        bnk = T.k[x + 1];
-        bna = head_entry(c, j + 1).abits;
-      }
-    }
-  };
-  auto command = [&](int32_t cmd, int depth) {  // CTA-wide regeneration (all warps)
-    if (lane == 0) {
-      X.cmd = cmd;
-      X.depth = depth;
-    }
-    __syncthreads();
-    if (cmd == kCmdMaxRegen) cta_maxima(cw, C, S);
-    regen_all(depth);
-    __syncthreads();
-  };
-  lane_best();
-  int since_regen = 1 << 30;
-#ifdef EQX_PROF
-  long long cy0 = 0, cy1 = 0, cy2 = 0, cyp = 0;
-#endif
-  for (;;) {
-#ifdef EQX_PROF
-    const long long ta = clock64();
-#endif
-    // outcome of picking this lane's best (engine.cpp:216-268 with can_fit/fits_alone)
-    int32_t out = kOutNone;
-    if (bc >= 0) {
-      if (!(bflags & 1)) out = kOutRej;
-      else if ((members + 1 <= P.max_batch) && (reserved + bneed <= tmax)) out = kOutAdm;
-      else out = P.backfill ? kOutSkip : kOutStop;
-    }
-    const int src = warp_argmin_lane(Cand{bk, ba, bo});
-    const uint64_t pk = __shfl_sync(0xffffffffu, static_cast<uint64_t>(static_cast<uint32_t>(out | (bflags << 4))) |
-                                                      (static_cast<uint64_t>(static_cast<uint32_t>(bin)) << 32), src);
-    const int64_t need = __shfl_sync(0xffffffffu, bneed, src);
-    const int32_t o = static_cast<int32_t>(pk & 15), fl = static_cast<int32_t>((pk >> 4) & 31);
-    if (o == kOutNone || o == kOutStop) break;  // no candidates (engine.cpp:217) / batch full (:239)
-    const int64_t ev = n_ev;
-    if (o == kOutRej) {
-      ++n_rej;
-      ++n_ev;
-    } else if (o == kOutAdm) {
-      members += 1;
-      reserved += need;
-      prefill += static_cast<int32_t>(pk >> 32);
-      ++n_adm;
-      ++n_ev;
-    }
-    const bool maxchg = o == kOutAdm && (fl & 2);
-    const bool holder = o != kOutSkip && (fl & 4) && (fl & 8);
-    ++since_regen;
-#ifdef EQX_PROF
-    const long long tb = clock64();
-#endif
-    bool rescan = false;
-    if (lane == src) {  // the winning lane applies the pick to its client (stores only)
-      const int32_t c = bc;
-      rescan = true;
-      if (o == kOutSkip) {
-        cw.flags[c] = kBacklogged | kSkipped;  // engine.cpp:236-238 (a candidate is backlogged)
-        kb[c] = ~0ull;
-      } else {
-        if (ev < a.ev_cap) {
-          a.ev_row[ev] = brow;
-          a.ev_kind[ev] = o == kOutAdm ? 1 : 2;
-          a.ev_client[ev] = c;
-        }
-        posv[c] = bpos + 1;
-        cw.ufc[c] = bnu;
-        cw.rfc[c] = bnr;
-        cw.cnt[c] = bncn;
-        if (o == kOutAdm) cw.adm[c] += 1;
-        if (fl & 8) {  // pop_head emptied the queue: set_backlogged(false)
-          cw.flags[c] = 0;
-          kb[c] = ~0ull;
-        } else if (maxchg) {
-          if (S.max_u < bnu) S.max_u = bnu;
-          if (S.max_r < bnr) S.max_r = bnr;
-        } else if (fl & 16) {
-          T.sd[c] = bd + 1;
-          kb[c] = bnk;
-          ab[c] = bna;
-        } else {
-          gen_stream(a, M, win, cw, T, c, Ds, S.max_u, S.max_r);  // its lookahead ran out
-        }
-      }
-    }
-#ifdef EQX_PROF
-    const long long tc = clock64();
-#endif
-    if (maxchg || holder) {
-      __syncwarp();
-      // maxima moving every few picks (cold ledgers): short lookahead; otherwise the full one
-      const int depth = since_regen < 4 ? min(2, Ds) : Ds;
-      since_regen = 0;
-      command(holder ? kCmdMaxRegen : kCmdRegen, depth);
-      lane_best();
-    } else if (rescan) {
-      lane_best();
-    }
-#ifdef EQX_PROF
-    __syncwarp();
-    const long long td = clock64();
-    cy0 += tb - ta;
-    cy1 += tc - tb;
-    cy2 += td - tc;
-    ++cyp;
-#endif
-  }
-#ifdef EQX_PROF
-  if (lane == 0) {
-    a.st->t[12] += cy0;
-    a.st->t[13] += cy1;
-    a.st->t[14] += cy2;
-    a.st->t[15] += cyp;
-  }
-#endif
-  if (lane == 0) {
-    S.members = members;
-    S.reserved = reserved;
-    S.n_ev = n_ev;
-    S.n_adm = n_adm;
-    S.n_rej = n_rej;
-    S.prefill = prefill;
-    S.flags |= kDone;
-    X.cmd = kCmdExit;
-  }
-  __syncthreads();  // releases the helper warps
-}
-
-// Register-slot variant of warp_select_phase for rosters of up to 32*K clients (K <= 4): each
-// lane keeps its clients' current head item *and* the next stream item in registers, so a pick
-// is a slot compare, a warp argmin and a broadcast; the winning lane promotes its prefetched
-// next item and issues the loads of the one after, whose latency hides behind later picks.
-struct RegItem {  // raw loads only: nothing is computed from them until the item is promoted
-  uint64_t k, a;
-  double nu, nr, ncn;
-  int32_t in, pred, row, alone;
-  uint32_t fl;      // T.fl byte (kFlMaxChg / kFlHolder)
-};
-
-template <int K>
-__device__ __forceinline__ void warp_select_reg(const SelectArgs& a, const ModelTables& M, const WinEntry* win,
-                                                const ClientWork& cw, SelShared& S, const StreamScratch& T) {
-  __shared__ WarpSelShared X;
-  const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31;
-  const int32_t C = a.C, Ds = T.Ds, W = a.W;
-  const Policy P = a.pol;
-  auto regen_all = [&](int depth) {
-    for (int32_t c = tid; c < C; c += NT) gen_stream(a, M, win, cw, T, c, depth, S.max_u, S.max_r);
-  };
-  regen_all(Ds);
-  __syncthreads();
-  if (tid >= 32) {  // helper warps: CTA-wide stream regeneration on command
-    for (;;) {
-      __syncthreads();
-      const int32_t cmd = X.cmd;
-      if (cmd == kCmdExit) break;
-      if (cmd == kCmdMaxRegen) cta_maxima(cw, C, S);
-      regen_all(X.depth);
-      __syncthreads();
-    }
-    return;
-  }
-  const int64_t tmax = a.tmax;
-  // per-slot registers
-  RegItem cur[K], nxt[K];
-  int32_t spos[K], spos0[K], send[K], sd[K], sdl[K], sadm[K], sfl[K];
-  uint32_t so[K];
-  double su[K], sr[K], scn[K];
-  auto load_item = [&](int s, int32_t c, int32_t d, int32_t j) -> RegItem {
-    RegItem it;
-    const int64_t x = static_cast<int64_t>(c) * Ds + d;
-    const int32_t kk = j - spos0[s];
-    const WinEntry e = kk < W ? win[static_cast<int64_t>(c) * W + kk] : deep_entry(a, M, c, j, kk, cw.w[c]);
-    it.k = T.k[x];
-    it.a = e.abits;
-    it.nu = T.u[x];
-    it.nr = T.r[x];
-    it.ncn = T.cn[x];
-    it.in = e.in;
-    it.pred = e.pred;
-    it.row = e.row;
-    it.alone = e.alone;
-    it.fl = T.fl[x];
-    return it;
-  };
-  auto load_slot = [&](int s) {  // after (re)generation: current head and the item after it
-    const int32_t c = lane + 32 * s;
-    cur[s].k = ~0ull;
-    if (c >= C) return;
-    spos[s] = cw.pos[c];
-    spos0[s] = cw.pos0[c];
-    send[s] = cw.end[c];
-    sfl[s] = cw.flags[c];
-    su[s] = cw.ufc[c];
-    sr[s] = cw.rfc[c];
-    scn[s] = cw.cnt[c];
-    sd[s] = 0;
-    sdl[s] = T.sdl[c];
-    if (sdl[s] == 0) return;  // not a candidate
-    cur[s] = load_item(s, c, 0, spos[s]);
-    if (1 < sdl[s]) nxt[s] = load_item(s, c, 1, spos[s] + 1);
-  };
-#pragma unroll
-  for (int s = 0; s < K; ++s) {
-    so[s] = lane + 32 * s < C ? cw.order[lane + 32 * s] : 0xffffffffu;
-    sadm[s] = lane + 32 * s < C ? cw.adm[lane + 32 * s] : 0;
-    load_slot(s);
-  }
-  int32_t members = S.members;
-  int64_t reserved = S.reserved, n_ev = S.n_ev, n_adm = S.n_adm, n_rej = S.n_rej, prefill = S.prefill;
-  int since_regen = 1 << 30;
-  auto command = [&](int32_t cmd, int depth) {
-#pragma unroll
-    for (int s = 0; s < K; ++s) {  // publish the slots' state for the regeneration
-      const int32_t c = lane + 32 * s;
-      if (c < C) {
-        cw.pos[c] = spos[s];
-        cw.flags[c] = sfl[s];
-        cw.ufc[c] = su[s];
-        cw.rfc[c] = sr[s];
-        cw.cnt[c] = scn[s];
-      }
-    }
-    if (lane == 0) {
-      X.cmd = cmd;
-      X.depth = depth;
-    }
-    __syncthreads();
-    if (cmd == kCmdMaxRegen) cta_maxima(cw, C, S);
-    regen_all(depth);
-    __syncthreads();
-#pragma unroll
-    for (int s = 0; s < K; ++s) load_slot(s);
-  };
-#ifdef EQX_PROF
-  long long cy0 = 0, cy1 = 0, cy2 = 0, cyp = 0;
-#endif
-  for (;;) {
-#ifdef EQX_PROF
-    const long long ta = clock64();
-#endif
-    // the lane's best slot (select_next order: key, head arrival, client_id rank)
-    int bs = -1;
-    uint64_t bk = ~0ull, ba = ~0ull;
-    uint32_t bo = 0xffffffffu;
-#pragma unroll
-    for (int s = 0; s < K; ++s) {
-      if (cur[s].k == ~0ull) continue;
-      const bool lt = (cur[s].k < bk) | ((cur[s].k == bk) & ((cur[s].a < ba) | ((cur[s].a == ba) & (so[s] < bo))));
-      if (bs < 0 || lt) {
-        bs = s;
-        bk = cur[s].k;
-        ba = cur[s].a;
-        bo = so[s];
-      }
-    }
-    int32_t out = kOutNone, bflags = 0, bin = 0;
-    int64_t bneed = 0;
-#pragma unroll
-    for (int s = 0; s < K; ++s)
-      if (s == bs) {
-        bflags = (cur[s].alone ? 1 : 0) | ((cur[s].fl & kFlMaxChg) ? 2 : 0) | ((cur[s].fl & kFlHolder) ? 4 : 0) |
-                 ((spos[s] + 1 == send[s]) ? 8 : 0) | ((sd[s] + 1 < sdl[s]) ? 16 : 0);
-        bin = cur[s].in;
-        bneed = static_cast<int64_t>(cur[s].in) + cur[s].pred;
-      }
-    if (bs >= 0) {
-      if (!(bflags & 1)) out = kOutRej;
-      else if ((members + 1 <= P.max_batch) && (reserved + bneed <= tmax)) out = kOutAdm;
-      else out = P.backfill ? kOutSkip : kOutStop;
-    }
-    const int src = warp_argmin_lane(Cand{bk, ba, bo});
-    const uint64_t pk = __shfl_sync(0xffffffffu, static_cast<uint64_t>(static_cast<uint32_t>(out | (bflags << 4))) |
-                                                      (static_cast<uint64_t>(static_cast<uint32_t>(bin)) << 32), src);
-    const int64_t need = __shfl_sync(0xffffffffu, bneed, src);
-    const int32_t o = static_cast<int32_t>(pk & 15), fl = static_cast<int32_t>((pk >> 4) & 31);
-    if (o == kOutNone || o == kOutStop) break;  // no candidates (engine.cpp:217) / batch full (:239)
-    const int64_t ev = n_ev;
-    if (o == kOutRej) {
-      ++n_rej;
-      ++n_ev;
-    } else if (o == kOutAdm) {
-      members += 1;
-      reserved += need;
-      prefill += static_cast<int32_t>(pk >> 32);
-      ++n_adm;
-      ++n_ev;
-    }
-    const bool maxchg = o == kOutAdm && (fl & 2);
-    const bool holder = o != kOutSkip && (fl & 4) && (fl & 8);
-    ++since_regen;
-#ifdef EQX_PROF
-    const long long tb = clock64();
-#endif
-    bool own_regen = false;
-    if (lane == src) {
-#pragma unroll
-      for (int s = 0; s < K; ++s) {
-        if (s != bs) continue;
-        const int32_t c = lane + 32 * s;
-        if (o == kOutSkip) {
-          sfl[s] |= kSkipped;  // engine.cpp:236-238
-          cur[s].k = ~0ull;
-          continue;
-        }
-        if (ev < a.ev_cap) {
-          a.ev_row[ev] = cur[s].row;
-          a.ev_kind[ev] = o == kOutAdm ? 1 : 2;
-          a.ev_client[ev] = c;
-        }
-        spos[s] += 1;
-        su[s] = cur[s].nu;
-        sr[s] = cur[s].nr;
-        scn[s] = cur[s].ncn;
-        if (o == kOutAdm) sadm[s] += 1;
-        if (fl & 8) {  // pop_head emptied the queue: set_backlogged(false)
-          sfl[s] &= ~kBacklogged;
-          cur[s].k = ~0ull;
-        } else if (maxchg) {
-          if (S.max_u < su[s]) S.max_u = su[s];
-          if (S.max_r < sr[s]) S.max_r = sr[s];
-        } else if (fl & 16) {  // promote the prefetched item, prefetch the one after
-          cur[s] = nxt[s];
-          sd[s] += 1;
-          if (sd[s] + 1 < sdl[s]) nxt[s] = load_item(s, c, sd[s] + 1, spos[s] + 1);
-        } else {
-          own_regen = true;
-        }
-      }
-    }
-    if (own_regen) {  // the winner's lookahead ran out: regenerate its stream alone
-#pragma unroll
-      for (int s = 0; s < K; ++s) {
-        if (s != bs) continue;
-        const int32_t c = lane + 32 * s;
-        cw.pos[c] = spos[s];
-        cw.ufc[c] = su[s];
-        cw.rfc[c] = sr[s];
-        cw.cnt[c] = scn[s];
-        gen_stream(a, M, win, cw, T, c, Ds, S.max_u, S.max_r);
-        load_slot(s);
-      }
-    }
-#ifdef EQX_PROF
-    const long long tc = clock64();
-#endif
-    if (maxchg || holder) {
-      __syncwarp();
-      const int depth = since_regen < 4 ? min(2, Ds) : Ds;
-      since_regen = 0;
-      command(holder ? kCmdMaxRegen : kCmdRegen, depth);
-    }
-#ifdef EQX_PROF
-    __syncwarp();
-    const long long td = clock64();
-    cy0 += tb - ta;
-    cy1 += tc - tb;
-    cy2 += td - tc;
-    ++cyp;
-#endif
-  }
-#ifdef EQX_PROF
-  if (lane == 0) {
-    a.st->t[12] += cy0;
-    a.st->t[13] += cy1;
-    a.st->t[14] += cy2;
-    a.st->t[15] += cyp;
-  }
-#endif
-#pragma unroll
-  for (int s = 0; s < K; ++s) {
-    const int32_t c = lane + 32 * s;
-    if (c < C) {
-      cw.pos[c] = spos[s];
-      cw.flags[c] = sfl[s];
-      cw.ufc[c] = su[s];
-      cw.rfc[c] = sr[s];
-      cw.cnt[c] = scn[s];
-      cw.adm[c] = sadm[s];
-    }
-  }
-  if (lane == 0) {
-    S.members = members;
-    S.reserved = reserved;
-    S.n_ev = n_ev;
-    S.n_adm = n_adm;
-    S.n_rej = n_rej;
-    S.prefill = prefill;
-    S.flags |= kDone;
-    X.cmd = kCmdExit;
-  }
-  __syncthreads();  // releases the helper warps
-}
-
-// Multi-warp variant of warp_select_reg<1> for rosters of 33..32*NW clients: lane L of selection
-// warp w owns client 32 w + L alone, so no lane compares or predicates over slots.  A pick is a
-// warp argmin in each selection warp, the NW warp winners exchanged through double-buffered
-// shared memory behind one named barrier of the selection warps, and the same select_next
-// comparison over them; the winning lane alone updates its client.  All selection warps keep
-// identical copies of the batch counters and issue the same regeneration commands.
-struct Warp2Cand {
-  uint64_t k, a, pk;
-  int64_t need;
-  uint32_t o;
-  int32_t lane;
-};
-
-template <int NW>
-__device__ __forceinline__ void warpn_select(const SelectArgs& a, const ModelTables& M, const WinEntry* win,
-                                             const ClientWork& cw, SelShared& S, const StreamScratch& T) {
-  __shared__ WarpSelShared X;
-  __shared__ Warp2Cand xw[2][NW];  // [pick parity][selection warp]
-  const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5;
-  const int32_t C = a.C, Ds = T.Ds, W = a.W;
-  const Policy P = a.pol;
-  auto regen_all = [&](int depth) {
-    for (int32_t c = tid; c < C; c += NT) gen_stream(a, M, win, cw, T, c, depth, S.max_u, S.max_r);
-  };
-  regen_all(Ds);
-  __syncthreads();
-  if (tid >= 32 * NW) {  // helper warps: CTA-wide stream regeneration on command
-    for (;;) {
-      __syncthreads();
-      const int32_t cmd = X.cmd;
-      if (cmd == kCmdExit) break;
-      if (cmd == kCmdMaxRegen) cta_maxima(cw, C, S);
-      regen_all(X.depth);
-      __syncthreads();
-    }
-    return;
-  }
-  const int64_t tmax = a.tmax;
-  const int32_t c = warp * 32 + lane;  // this lane's client
-  RegItem cur, nxt;
-  int32_t spos = 0, spos0 = 0, send = 0, sd = 0, sdl = 0, sadm = 0, sfl = 0;
-  double su = 0.0, sr = 0.0, scn = 0.0;
-  const uint32_t so = c < C ? cw.order[c] : 0xffffffffu;
-  auto load_item = [&](int32_t d, int32_t j) -> RegItem {
-    RegItem it;
-    const int64_t x = static_cast<int64_t>(c) * Ds + d;
-    const int32_t kk = j - spos0;
-    const WinEntry e = kk < W ? win[static_cast<int64_t>(c) * W + kk] : deep_entry(a, M, c, j, kk, cw.w[c]);
-    it.k = T.k[x];
-    it.a = e.abits;
-    it.nu = T.u[x];
-    it.nr = T.r[x];
-    it.ncn = T.cn[x];
-    it.in = e.in;
-    it.pred = e.pred;
-    it.row = e.row;
-    it.alone = e.alone;
-    it.fl = T.fl[x];
-    return it;
-  };
-  auto load_slot = [&]() {  // after (re)generation: current head and the item after it
-    cur.k = ~0ull;
-    if (c >= C) return;
-    spos = cw.pos[c];
-    spos0 = cw.pos0[c];
-    send = cw.end[c];
-    sfl = cw.flags[c];
-    su = cw.ufc[c];
-    sr = cw.rfc[c];
-    scn = cw.cnt[c];
-    sd = 0;
-    sdl = T.sdl[c];
-    if (sdl == 0) return;  // not a candidate
-    cur = load_item(0, spos);
-    if (1 < sdl) nxt = load_item(1, spos + 1);
-  };
-  sadm = c < C ? cw.adm[c] : 0;
-  load_slot();
-  int32_t members = S.members;
-  int64_t reserved = S.reserved, n_ev = S.n_ev, n_adm = S.n_adm, n_rej = S.n_rej, prefill = S.prefill;
-  int since_regen = 1 << 30;
-  int par = 0;
-  auto publish = [&]() {
-    if (c < C) {
-      cw.pos[c] = spos;
-      cw.flags[c] = sfl;
-      cw.ufc[c] = su;
-      cw.rfc[c] = sr;
-      cw.cnt[c] = scn;
-    }
-  };
-  auto command = [&](int32_t cmd, int depth) {
-    publish();
-    if (tid == 0) {
-      X.cmd = cmd;
-      X.depth = depth;
-    }
-    __syncthreads();
-    if (cmd == kCmdMaxRegen) cta_maxima(cw, C, S);
-    regen_all(depth);
-    __syncthreads();
-    load_slot();
-  };
-  for (;;) {
-    const bool has = cur.k != ~0ull;
-    int32_t out = kOutNone, bflags = 0;
-    int64_t bneed = 0;
-    if (has) {
-      bflags = (cur.alone ? 1 : 0) | ((cur.fl & kFlMaxChg) ? 2 : 0) | ((cur.fl & kFlHolder) ? 4 : 0) |
-               ((spos + 1 == send) ? 8 : 0) | ((sd + 1 < sdl) ? 16 : 0);
-      bneed = static_cast<int64_t>(cur.in) + cur.pred;
-      if (!(bflags & 1)) out = kOutRej;
-      else if ((members + 1 <= P.max_batch) && (reserved + bneed <= tmax)) out = kOutAdm;
-      else out = P.backfill ? kOutSkip : kOutStop;
-    }
-    const Cand mine = has ? Cand{cur.k, cur.a, so} : no_cand();
-    const int wsrc = warp_argmin_lane(mine);
-    if (lane == wsrc) {
-      Warp2Cand& x = xw[par][warp];
-      x.k = mine.k;
-      x.a = mine.a;
-      x.o = mine.o;
-      x.lane = lane;
-      x.pk = static_cast<uint64_t>(static_cast<uint32_t>(out | (bflags << 4))) |
-             (static_cast<uint64_t>(static_cast<uint32_t>(has ? cur.in : 0)) << 32);
-      x.need = bneed;
-    }
-    asm volatile("bar.sync 1, %0;" ::"n"(32 * NW) : "memory");
-    Warp2Cand xb = xw[par][0];
-    int win_warp = 0;
-#pragma unroll
-    for (int w = 1; w < NW; ++w) {
-      const Warp2Cand xo = xw[par][w];
-      if (better(Cand{xo.k, xo.a, xo.o}, Cand{xb.k, xb.a, xb.o})) {
-        xb = xo;
-        win_warp = w;
-      }
-    }
-    par ^= 1;
-    const uint64_t pk = xb.pk;
-    const int64_t need = xb.need;
-    const int32_t o = static_cast<int32_t>(pk & 15), fl = static_cast<int32_t>((pk >> 4) & 31);
-    if (o == kOutNone || o == kOutStop) break;  // no candidates (engine.cpp:217) / batch full (:239)
-    const int64_t ev = n_ev;
-    if (o == kOutRej) {
-      ++n_rej;
-      ++n_ev;
-    } else if (o == kOutAdm) {
-      members += 1;
-      reserved += need;
-      prefill += static_cast<int32_t>(pk >> 32);
-      ++n_adm;
-      ++n_ev;
-    }
-    const bool maxchg = o == kOutAdm && (fl & 2);
-    const bool holder = o != kOutSkip && (fl & 4) && (fl & 8);
-    ++since_regen;
-    if (warp == win_warp && lane == xb.lane) {
-      bool own_regen = false;
-      if (o == kOutSkip) {
-        sfl |= kSkipped;  // engine.cpp:236-238
-        cur.k = ~0ull;
-      } else {
-        if (ev < a.ev_cap) {
-          a.ev_row[ev] = cur.row;
-          a.ev_kind[ev] = o == kOutAdm ? 1 : 2;
-          a.ev_client[ev] = c;
-        }
-        spos += 1;
-        su = cur.nu;
-        sr = cur.nr;
-        scn = cur.ncn;
-        if (o == kOutAdm) sadm += 1;
-        if (fl & 8) {  // pop_head emptied the queue: set_backlogged(false)
-          sfl &= ~kBacklogged;
-          cur.k = ~0ull;
-        } else if (maxchg) {
-          if (S.max_u < su) S.max_u = su;
-          if (S.max_r < sr) S.max_r = sr;
-        } else if (fl & 16) {  // promote the prefetched item, prefetch the one after
-          cur = nxt;
-          sd += 1;
-          if (sd + 1 < sdl) nxt = load_item(sd + 1, spos + 1);
-        } else {
-          own_regen = true;
-        }
-      }
-      if (own_regen) {  // the winner's lookahead ran out: regenerate its stream alone
-        cw.pos[c] = spos;
-        cw.ufc[c] = su;
-        cw.rfc[c] = sr;
-        cw.cnt[c] = scn;
-        gen_stream(a, M, win, cw, T, c, Ds, S.max_u, S.max_r);
-        load_slot();
-      }
-    }
-    if (maxchg || holder) {
-      __syncwarp();
-      const int depth = since_regen < 4 ? min(2, Ds) : Ds;
-      since_regen = 0;
-      command(holder ? kCmdMaxRegen : kCmdRegen, depth);
-    }
-  }
-  if (c < C) {
-    cw.pos[c] = spos;
-    cw.flags[c] = sfl;
-    cw.ufc[c] = su;
-    cw.rfc[c] = sr;
-    cw.cnt[c] = scn;
-    cw.adm[c] = sadm;
-  }
-  if (tid == 0) {
-    S.members = members;
-    S.reserved = reserved;
-    S.n_ev = n_ev;
-    S.n_adm = n_adm;
-    S.n_rej = n_rej;
-    S.prefill = prefill;
-    S.flags |= kDone;
-    X.cmd = kCmdExit;
-  }
-  __syncthreads();  // releases the helper warps
-}
-
 #include "eqx_topk.cuh"
 
-// kMode: -1 multi-mode loops (select_kernel); 0 warp_select_phase; 1/2/4 warp_select_reg<kMode>;
-// 64: rounds of block-radix top-K (topk_select)
-template <int kMode>
-__device__ __forceinline__ void select_body(const SelectArgs& a) {
-  constexpr bool kWarp = kMode >= 0;
+// The selection kernel: one CTA runs the exact admit_requests loop as rounds of block-radix
+// top-K over per-client key streams (eqx_topk.cuh).  The prologue stages the model, carves the
+// per-client work arrays (shared memory, or global scratch on huge rosters) and loads the
+// ledger -- after the window kernel's programmatic completion when that kernel applied the
+// drain's counter lift -- and the epilogue writes back ledger, heads, batch and summary.
+__global__ void __launch_bounds__(kTopkThreads, 1) select_topk_kernel(const SelectArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ SelShared S;
   const int32_t C = a.C;
@@ -2542,7 +1155,7 @@ __device__ __forceinline__ void select_body(const SelectArgs& a) {
     a.st->t[0] = global_ns();
     for (int i = 8; i < 16; ++i) a.st->t[i] = 0;
   }
-  // ---- carve per-client work arrays, batch scratch, windows ----
+  // ---- carve per-client work arrays and the top-K scratch ----
   unsigned char* p = smem + ((a.model_words * 4 + 15) & ~15);
   unsigned char* g = reinterpret_cast<unsigned char*>(a.cw_global);
   auto carve = [&](size_t bytes) {
@@ -2557,8 +1170,6 @@ __device__ __forceinline__ void select_body(const SelectArgs& a) {
     return r;
   };
   ClientWork cw;
-  cw.kb = reinterpret_cast<uint64_t*>(take(8ull * C));
-  cw.ab = reinterpret_cast<uint64_t*>(take(8ull * C));
   cw.ufc = reinterpret_cast<double*>(take(8ull * C));
   cw.rfc = reinterpret_cast<double*>(take(8ull * C));
   cw.cnt = reinterpret_cast<double*>(take(8ull * C));
@@ -2570,20 +1181,8 @@ __device__ __forceinline__ void select_body(const SelectArgs& a) {
   cw.flags = reinterpret_cast<int32_t*>(take(4ull * C));
   cw.adm = reinterpret_cast<int32_t*>(take(4ull * C));
   cw.by_order = reinterpret_cast<int32_t*>(take(4ull * C));
-  StreamScratch T;
-  T.Ds = a.Ds;
-  if (a.Ds > 0) {
-    const size_t items = static_cast<size_t>(C) * a.Ds;
-    T.k = reinterpret_cast<uint64_t*>(carve(8 * items));
-    T.u = reinterpret_cast<double*>(carve(8 * items));
-    T.r = reinterpret_cast<double*>(carve(8 * items));
-    T.cn = reinterpret_cast<double*>(carve(8 * items));
-    T.fl = reinterpret_cast<uint8_t*>(carve(items));
-    T.sd = reinterpret_cast<int32_t*>(carve(4ull * C));
-    T.sdl = reinterpret_cast<int32_t*>(carve(4ull * C));
-  }
   TopkScratch TK;
-  if constexpr (kMode == 64) {
+  {
     const size_t items = static_cast<size_t>(a.tk_cap);
     const size_t kc = static_cast<size_t>(a.tk_kcap);
     TK.dsh_max = a.tk_dsh;
@@ -2620,7 +1219,6 @@ __device__ __forceinline__ void select_body(const SelectArgs& a) {
     TK.ha = hp ? reinterpret_cast<uint64_t*>(hp + 8 * cc) : nullptr;
     TK.hst = hp ? hp + 16 * cc : nullptr;
   }
-  WinEntry* win = reinterpret_cast<WinEntry*>(p);
   __syncthreads();
   const ModelTables& M = *reinterpret_cast<const ModelTables*>(smem);
 
@@ -2629,79 +1227,23 @@ __device__ __forceinline__ void select_body(const SelectArgs& a) {
     lift_core<int32_t>(l, a.first_row);
     __syncthreads();
   }
-#ifdef EQX_PROF
-  if (tid == 0) a.st->t[8] = global_ns() - a.st->t[0];  // ns after the selection start
-#endif
-  // ---- ledger in, head windows (bulk copy of window_kernel's [C][W] entries) ----
-  auto ledger_in = [&]() {
-    for (int32_t c = tid; c < C; c += NT) {
-      cw.ufc[c] = a.ufc[c];
-      cw.rfc[c] = a.rfc[c];
-      cw.cnt[c] = a.counter[c];
-      cw.w[c] = a.weight[c];
-      cw.pos[c] = a.head[c];
-      cw.pos0[c] = a.head[c];
-      cw.end[c] = a.count[c];
-      const uint32_t o = a.order[c];
-      cw.order[c] = o;
-      cw.by_order[o] = c;
-      cw.flags[c] = a.backlogged[c] ? kBacklogged : 0;
-      cw.adm[c] = 0;
-    }
-  };
-  if (!a.ledger_after_wait) ledger_in();
-#ifdef EQX_PROF
-  if (tid == 0) a.st->t[9] = global_ns() - a.st->t[0];
-#endif
-  pdl_wait();  // window_kernel's [C][W] entries (programmatic launch: the prologue above overlapped it)
-  if (a.ledger_after_wait) ledger_in();  // lifted by the window kernel's extra CTA
-#ifdef EQX_PROF
-  if (tid == 0) a.st->t[10] = global_ns() - a.st->t[0];
-#endif
-  if (kMode == 64) {
-    // top-K rounds read the head windows from L2 (topk_entry)
-  } else if (a.gW > 0 && a.gW != a.W) {  // gathered [C][gW] windows: the first W of every client
-    constexpr int kWords = sizeof(WinEntry) / 8;
-    const int64_t per = static_cast<int64_t>(a.W) * kWords;
-    const int64_t words = static_cast<int64_t>(C) * per;
-    const uint2* src = reinterpret_cast<const uint2*>(a.win_g);
-    uint2* dst = reinterpret_cast<uint2*>(win);
-    for (int64_t i = tid; i < words; i += NT) {
-      const int64_t c = i / per;
-      dst[i] = __ldcg(src + c * a.gW * kWords + (i - c * per));
-    }
-  } else if (const uint64_t wbytes = static_cast<uint64_t>(C) * a.W * sizeof(WinEntry);
-             wbytes > 0 && wbytes < (1u << 20) && wbytes % 16 == 0 && (reinterpret_cast<uintptr_t>(a.win_g) & 15) == 0) {
-    // one elected thread moves the whole [C][W] block with 1-D bulk copies (TMA engine)
-    __shared__ uint64_t wbar;
-    if (tid == 0) {
-      mbar_init(&wbar, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (tid == 0) {
-      mbar_expect_tx(&wbar, static_cast<uint32_t>(wbytes));
-      const unsigned char* src = reinterpret_cast<const unsigned char*>(a.win_g);
-      unsigned char* dst = reinterpret_cast<unsigned char*>(win);
-      for (uint32_t off = 0; off < wbytes; off += 32768u)
-        bulk_g2s(dst + off, src + off, min(32768u, static_cast<uint32_t>(wbytes) - off), &wbar);
-    }
-    mbar_wait(&wbar, 0);
-  } else {
-    const int64_t words = static_cast<int64_t>(C) * a.W * (sizeof(WinEntry) / 8);
-    const uint2* src = reinterpret_cast<const uint2*>(a.win_g);
-    uint2* dst = reinterpret_cast<uint2*>(win);
-    int64_t i = tid;
-    for (; i + 3 * NT < words; i += 4 * NT) {  // 4 independent loads in flight per thread
-      const uint2 v0 = __ldcg(src + i), v1 = __ldcg(src + i + NT), v2 = __ldcg(src + i + 2 * NT),
-                  v3 = __ldcg(src + i + 3 * NT);
-      dst[i] = v0;
-      dst[i + NT] = v1;
-      dst[i + 2 * NT] = v2;
-      dst[i + 3 * NT] = v3;
-    }
-    for (; i < words; i += NT) dst[i] = __ldcg(src + i);
+  // ---- ledger in ----
+  if (a.ledger_after_wait) pdl_wait();  // lifted by the window kernel's extra CTA
+  for (int32_t c = tid; c < C; c += NT) {
+    cw.ufc[c] = a.ufc[c];
+    cw.rfc[c] = a.rfc[c];
+    cw.cnt[c] = a.counter[c];
+    cw.w[c] = a.weight[c];
+    cw.pos[c] = a.head[c];
+    cw.pos0[c] = a.head[c];
+    cw.end[c] = a.count[c];
+    const uint32_t o = a.order[c];
+    cw.order[c] = o;
+    cw.by_order[o] = c;
+    cw.flags[c] = a.backlogged[c] ? kBacklogged : 0;
+    cw.adm[c] = 0;
   }
+  if (!a.ledger_after_wait) pdl_wait();  // window_kernel's [C][W] head entries (read from L2 by the rounds)
   if (tid == 0) {
     S.n_ev = S.n_adm = S.n_rej = S.prefill = 0;
     S.members = a.st->members;
@@ -2712,42 +1254,8 @@ __device__ __forceinline__ void select_body(const SelectArgs& a) {
   if (tid == 0) a.st->t[1] = global_ns();
   cta_maxima(cw, C, S);
   if (tid == 0) a.st->t[2] = global_ns();
-
-  // ---- batches; short batches (maxima moving every pick) fall back to sequential picks ----
-  unsigned long long nb = 0, ns = 0;
-  if constexpr (kMode == 64) {
-    topk_select(a, M, cw, S, TK);
-  } else if constexpr (kMode == 0) {  // single-warp selection
-    warp_select_phase(a, M, win, cw, S, T);
-    ns = 1;
-  } else if constexpr (kMode == 16 || kMode == 32) {  // 2 / 4 selection warps, one client per lane
-    warpn_select<kMode / 8>(a, M, win, cw, S, T);
-    ns = 1;
-  } else if constexpr (kWarp && kMode > 0) {
-    warp_select_reg<kMode>(a, M, win, cw, S, T);
-    ns = 1;
-  }
-  for (; !kWarp && kMode != 64 && !(S.flags & kDone);) {
-    const int32_t picks = 0x7fffffff;
-    switch (a.K) {  // register-resident slots per thread (selection threads = a.sel_threads)
-      case 1: seq_reg_phase<1>(a, M, win, cw, S, picks, T); break;
-      case 2: seq_reg_phase<2>(a, M, win, cw, S, picks, T); break;
-      case 4: seq_reg_phase<4>(a, M, win, cw, S, picks, T); break;
-      case 8: seq_reg_phase<8>(a, M, win, cw, S, picks, T); break;
-      default: seq_phase(a, M, win, cw, S, picks); break;
-    }
-    ++ns;
-    __syncthreads();
-    if (S.flags & kDone) break;
-    cta_maxima(cw, C, S);
-  }
-  if (tid == 0) {
-    a.st->t[3] = global_ns();
-    if (kMode != 64) {  // topk_select stamps its own round count / phase cycles
-      a.st->t[6] = nb;
-      a.st->t[7] = ns;
-    }
-  }
+  topk_select(a, M, cw, S, TK);
+  if (tid == 0) a.st->t[3] = global_ns();
   pdl_trigger();  // the event fill may get scheduled while the ledger is written back
   // ---- write back ledger, heads, batch, summary ----
   for (int32_t c = tid; c < C; c += NT) {
@@ -2765,25 +1273,8 @@ __device__ __forceinline__ void select_body(const SelectArgs& a) {
     a.st->n_admitted = S.n_adm;
     a.st->n_rejected = S.n_rej;
     a.st->new_prefill = S.prefill;
-#ifdef EQX_PROF
-    if (kMode == 16 || kMode == 32) a.st->t[12] = global_ns();  // selection epilogue done
-#endif
   }
 }
-
-// The sequential pick loops (EQX_SELECT_MODE=seq/warp/slots/reg: multi-warp register slots or
-// the shared-memory loop, single-warp forms) and the default top-K rounds, as separate kernels
-// so each gets its own register budget.
-__global__ void __launch_bounds__(kSelectMaxThreads, 1) select_kernel(const SelectArgs a) { select_body<-1>(a); }
-template <int kMode>
-__global__ void __launch_bounds__(kSelectMaxThreads, 1) select_warp_kernel(const SelectArgs a) { select_body<kMode>(a); }
-__global__ void __launch_bounds__(kTopkThreads, 1) select_topk_kernel(const SelectArgs a) { select_body<64>(a); }
-template __global__ void select_warp_kernel<0>(SelectArgs);
-template __global__ void select_warp_kernel<1>(SelectArgs);
-template __global__ void select_warp_kernel<2>(SelectArgs);
-template __global__ void select_warp_kernel<4>(SelectArgs);
-template __global__ void select_warp_kernel<16>(SelectArgs);
-template __global__ void select_warp_kernel<32>(SelectArgs);
 
 // Event payloads (scheduler.hpp:131-138 PendingContribution) from the per-request scores the
 // scoring kernel wrote: predicted tokens, ufc/rfc increments, the VTC charge and wait_s.

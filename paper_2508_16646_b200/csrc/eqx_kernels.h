@@ -22,7 +22,6 @@ constexpr int kScoreTmaThreads = 256;                        // score_tma_kernel
 constexpr int kScoreTile = 1024;                             // requests per bulk-copied tile
 constexpr int kScoreStages = 3;                              // tiles in flight per CTA
 constexpr int kScoreStageBytes = kScoreTile * (4 + 8 + 4 + 1 + 4);  // columns (+ true_out)
-constexpr int kSelectMaxThreads = 256;
 constexpr int kTopkThreads = 512;                           // select_topk_kernel block
 
 // Prediction records frozen when a request joined a live queue (drain_arrivals stores
@@ -157,20 +156,16 @@ struct SelectArgs {
   const int32_t* count;
   int32_t* head;
   int32_t C;
-  int32_t W;             // head-window depth cached in shared memory per client
+  int32_t W;             // head-window depth per client (window_kernel's [C][W] entries)
   const WinEntry* win_g; // [C][W] windows produced by window_kernel ([C][gW] when gathered)
   int32_t gW;            // > 0: client-sharded step; win_g holds the gathered [C][gW] windows and
                          // a head beyond them raises DevState::underflow instead of reading HBM
-  int32_t sel_threads;   // threads in the selection loop (multiple of 32)
-  int32_t K;             // register client slots per selection thread (1/2/4/8; 0 = smem loop)
-  int32_t warp_sel;      // selection kernel variant (eqx_capi.cu select_fn)
   int32_t do_lift;       // run the drain's counter lift / backlog flags first (drain + step)
   int32_t ledger_after_wait;  // the preceding window kernel lifted the ledger: load it after the
                               // programmatic wait
   const int32_t* first_row;
   const int32_t* qlen_before;
   int32_t counter_lift;
-  int32_t Ds;            // key-stream lookahead per client for the register loop
   int32_t cw_in_smem;
   void* cw_global;       // per-client work arrays when they do not fit in smem
   // top-K rounds (select_topk_kernel, eqx_topk.cuh)
@@ -443,10 +438,6 @@ __global__ void drain_rank_kernel(DrainArgs a);
 __global__ void score_kernel(ScoreArgs a);
 __global__ void score_tma_kernel(ScoreArgs a);
 __global__ void window_kernel(WindowArgs a);
-__global__ void select_kernel(SelectArgs a);
-__global__ void select_topk_kernel(SelectArgs a);  // rounds of block-radix top-K (eqx_topk.cuh)
-template <int kMode>
-__global__ void select_warp_kernel(SelectArgs a);  // kMode 0: smem slots; 1/2/4: register slots;
-                                                   // 16: two selection warps, one client per lane
+__global__ void select_topk_kernel(SelectArgs a);  // the admission loop as rounds of block-radix top-K (eqx_topk.cuh)
 
 }  // namespace eqx

@@ -498,6 +498,7 @@ __global__ void __launch_bounds__(128) replay_kernel(const ReplayArgs A) {
       }
       pop_head(c);
       ReplayMember& m = mb[members++];
+      m.pad = 0;
       m.row = row;
       m.client = c;
       m.in = in;

@@ -809,7 +809,8 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
     }
     TK_STAMP(6)
     // 4c. backfill after a head that did not fit: the exact loop body, one item at a time
-    if (X.stop == 8 && tid == 0) {
+    // (a volatile read inside the thread-0 branch: the flag is rewritten by that thread below)
+    if (tid == 0 && *reinterpret_cast<volatile int32_t*>(&X.stop) == 8) {
       int32_t stop = 0;
       int32_t members = S.members;
       int64_t reserved = S.reserved, n_ev = S.n_ev, n_adm = S.n_adm, n_rej = S.n_rej, prefill = S.prefill;

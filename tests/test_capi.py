@@ -64,3 +64,37 @@ def test_pinned_host_arena():
     lib = S.L.load()
     assert lib.eqx_host_free(None) == 0
     assert lib.eqx_host_alloc(0) is None
+
+
+@pytest.mark.gpu
+def test_context_teardown_frees_device_memory():
+    """eqx_ctx_destroy frees every device buffer a context grew (drain, step, live queue, replay
+    and staging buffers): 30 create / use / destroy cycles leave the free device memory where it
+    was (compute-sanitizer's leak report at exit lists only objects still alive then)."""
+    import gc
+
+    import torch
+    from helpers import case_batch, case_clients, case_columns, case_kwargs
+    from test_gpu_parity import _random_case
+    from paper_2508_16646_b200 import scheduler as S
+    case = _random_case(77, 20000, 300)
+    cols = case_columns(case)
+
+    def cycle():
+        sch = S.GpuScheduler(case_clients(case), running=case.running, **case_kwargs(case))
+        sch.set_batch(*case_batch(case))
+        sch.stage_async(**{k: S.pinned_copy(v) for k, v in cols.items()})
+        sch.drain(**cols)
+        sch.step(case.now)
+        sch.close()
+
+    cycle()
+    torch.cuda.synchronize()
+    gc.collect()
+    free0 = torch.cuda.mem_get_info()[0]
+    for _ in range(30):
+        cycle()
+    torch.cuda.synchronize()
+    gc.collect()
+    free1 = torch.cuda.mem_get_info()[0]
+    assert free0 - free1 < 8 << 20, f"{(free0 - free1) >> 20} MiB not returned"
