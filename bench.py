@@ -237,8 +237,13 @@ def run_sharded(args, rank, world):
         flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     torch.cuda.synchronize()
     sch.set_batch(0, 0)
-    window = perf.max_batch + 1  # free slots + 1: exact without rejections (underflow is checked)
     sch.sel.checkpoint()
+    # head-window depth: ShardedScheduler's adaptive default (8, grown 4x after an underflow and
+    # kept), settled by one public step before the timed loop
+    sch.drain(local=True, **cols)
+    sch.step(1.0, with_events=False)
+    window = sch.default_window()
+    sch.sel.restore_async()
 
     def enqueue_step():
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -316,8 +321,8 @@ def run_sharded(args, rank, world):
             "exchange_bytes_per_rank": rec,
             "e2e": {"value": world * n / e2e_med, "unit": "requests/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "p50_ms": e2e_med * 1e3},
-            # drain_hist, drain_rank, score, shard_export, shard_ingest, shard_unpack, select, event_fill
-            "gpu_launches": 8 * args.steps,
+            # drain (3), score, shard_export, shard_ingest, shard_unpack, select, event_fill
+            "gpu_launches": 9 * args.steps,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -753,8 +758,9 @@ def run_ours(args, rank, world):
                          "~54.5 GB/s measured pinned H2D on the box, tools/pin_probe.py)",
                 "note": "wall clock over consecutive steps; the H2D of steps i+1, i+2 (copy stream) "
                         "overlaps step i"},
-        # per step: drain_hist, drain_rank, window, score, select, event_fill, pack_cols (state copy)
-        "gpu_launches": 7 * args.steps,
+        # per step: drain (sort / hist, scan, scatter / rank), window, score, select, event_fill,
+        # pack_cols (state copy)
+        "gpu_launches": 8 * args.steps,
         "clocks": clk.summary(),
     }
     if not (args.no_cpu_baseline or args.profile):
