@@ -299,3 +299,68 @@ def test_sharded_cfg4_global_shape_vs_reference():
     res, led, sc, retries = sharded_sim(case, 8, device_columns=True)
     compare_sharded(res, led, sc, H.run_step(case, "ref"))
     assert res.n_admitted == 64
+
+
+def _gpu_gloo_worker(rank, world, port, q, seed):
+    """One rank of a real two-process sharded step on cuda:0 (gloo: the exchange is staged
+    through the host): ShardedScheduler drains this rank's clients, exports its record with
+    shard_export_kernel, all-gathers it with the other process and runs the replicated selection."""
+    import sys
+    sys.path[:0] = [os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), d) for d in ("", "oracle", "tests")]
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2508_16646_b200.sharded import ShardedScheduler
+        from test_gpu_parity import _random_case
+        case = _random_case(seed, 20000, 50 + seed)
+        case.finalize()
+        kw = case_kwargs(case)
+        sch = ShardedScheduler(case_clients(case), rank, world, running=case.running, device=0, **kw)
+        sch.set_batch(*case_batch(case))
+        cols = case_columns(case)
+        owner = sch.layout.owner[cols["client"]]
+        rows = np.nonzero(owner == rank)[0]
+        sch.drain(**{k: v[rows] for k, v in cols.items()})
+        res = sch.step(case.now)
+        led = sch.ledger()
+        q.put((rank, res.ids.tolist(), res.kinds.tolist(), res.clients.tolist(), res.ufc_inc.tolist(),
+               {k: led[k].tolist() for k in ("ufc", "rfc", "counter", "backlogged")}, sch.retries))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", [1, 2])
+def test_two_process_sharded_step_on_one_gpu(seed):
+    """The multi-process path of bench.py --gpus N with real kernels: two processes on cuda:0,
+    each exporting its shard with shard_export_kernel, exchanged through torch.distributed
+    (gloo; NCCL needs distinct GPUs), identical schedules on both ranks, bit-exact against the
+    oracle of the unsharded queue, with the adaptive head-window depth (8, grown on underflow)."""
+    import torch.multiprocessing as mp
+    from test_gpu_parity import _random_case
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gpu_gloo_worker, args=(r, world, port, q, seed)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict((r[0], r[1:]) for r in (q.get(timeout=300) for _ in range(world)))
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    assert got[0][:5] == got[1][:5]  # identical schedule and ledger on both ranks
+    case = _random_case(seed, 20000, 50 + seed)
+    want = H.run_step(case, "oracle")
+    ids, kinds, clients, ufc_inc, led, _ = got[0]
+    np.testing.assert_array_equal(ids, want["ev_id"])
+    np.testing.assert_array_equal(kinds, want["ev_kind"])
+    np.testing.assert_array_equal(clients, want["ev_client"])
+    adm = want["ev_kind"] == H.EV_ADMIT
+    np.testing.assert_array_equal(np.asarray(ufc_inc)[adm], want["ev_ufc_inc"][adm])
+    for k in ("ufc", "rfc", "counter", "backlogged"):
+        np.testing.assert_array_equal(led[k], want[k], err_msg=k)
