@@ -107,7 +107,7 @@ struct eqx_ctx {
   int bound_stage = -1;
   uint64_t stage_seq = 0;
   cudaStream_t copy_stream = nullptr;
-  DevBuf d_perm, d_hist, d_tbase, d_ctot, d_tsorted;
+  DevBuf d_perm, d_hist, d_tbase, d_ctot, d_tsorted, d_tfirst;
   bool sort_drain = false;         // small rosters: drain_sort + drain_scan + drain_scatter
   size_t sort_smem = 0;
   bool queue_ready = false;
@@ -952,6 +952,7 @@ static eqx_status drain_prepare(eqx_ctx* ctx, const eqx_requests* r) {
   const int64_t L = static_cast<int64_t>(C) * n_tiles;
   CUDA_TRY(ctx, ctx->d_hist.ensure(4 * std::max<int64_t>(L, 1)));
   CUDA_TRY(ctx, ctx->d_tbase.ensure(4 * std::max<int64_t>(L, 1)));
+  CUDA_TRY(ctx, ctx->d_tfirst.ensure(4 * std::max<int64_t>(L, 1)));
   CUDA_TRY(ctx, ctx->d_ctot.ensure(4 * std::max<int64_t>(C, 1)));
   ctx->tile_rows = tile_rows;
   ctx->n_tiles = n_tiles;
@@ -984,6 +985,9 @@ static DrainArgs drain_args(eqx_ctx* ctx) {
   d.tbase = ctx->d_tbase.as<uint32_t>();
   d.ctot = ctx->d_ctot.as<uint32_t>();
   d.tsorted = ctx->d_tsorted.as<uint32_t>();
+  d.tfirst = ctx->d_tfirst.as<uint32_t>();
+  d.head = ctx->d_head.as<int32_t>();
+  d.zero_qlen = 1;
   d.hist_L = ctx->hist_L;
   d.seg_off = ctx->d_seg_off.as<int32_t>();
   d.perm = ctx->d_perm.as<uint32_t>();
@@ -1002,16 +1006,15 @@ static DrainArgs drain_args(eqx_ctx* ctx) {
   return d;
 }
 
-// Pure stream work of a drain (2 memsets + 2 kernels); capturable into a CUDA graph.
+// Pure stream work of a drain (3 kernels, no memsets); capturable into a CUDA graph.
 // lift: also apply on_activated / set_backlogged now (a standalone drain); a drain fused into a
 // step leaves that to the selection kernel's prologue (SelectArgs::do_lift).
 static eqx_status drain_enqueue(eqx_ctx* ctx, bool lift, bool keep_qlen = false) {
   cudaStream_t s = ctx->stream;
   const int32_t C = ctx->C;
   if (C == 0) return EQX_OK;
-  CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_head.p, 0, 4ull * C, s));
-  if (!keep_qlen) CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_qlen_before.p, 0, 4ull * C, s));
-  CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_first.p, 0xff, 4ull * C, s));  // atomicMin target
+  // heads, qlen_before (unless the queue is kept) and first rows are written by
+  // drain_scan_kernel: no memset nodes in front of the drain
 #ifdef EQX_PROF
   {
     char* dt = reinterpret_cast<char*>(ctx->d_state.p) + offsetof(DevState, dt);
@@ -1021,7 +1024,8 @@ static eqx_status drain_enqueue(eqx_ctx* ctx, bool lift, bool keep_qlen = false)
     CUDA_TRY(ctx, cudaMemsetAsync(dt + 40, 0xff, 8, s));
   }
 #endif
-  const DrainArgs d = drain_args(ctx);
+  DrainArgs d = drain_args(ctx);
+  d.zero_qlen = keep_qlen ? 0 : 1;
   if (ctx->sort_drain) {
     drain_sort_kernel<<<ctx->n_tiles, kSortThreads, ctx->sort_smem, s>>>(d);
     CUDA_TRY(ctx, launch_pdl(drain_scan_kernel, dim3((C + 31) / 32), dim3(1024), 0, s, d));

@@ -335,8 +335,7 @@ __device__ __forceinline__ void drain_hist_body(const DrainArgs& a) {
   }
   if (bad) a.st->bad_client = 1;
   __syncthreads();
-  for (int c = tid; c < C; c += blockDim.x)
-    if (fr[c] != 0xffffffffu) atomicMin(reinterpret_cast<unsigned int*>(a.first_row) + c, fr[c]);
+  for (int c = tid; c < C; c += blockDim.x) a.tfirst[static_cast<int64_t>(tile) * C + c] = fr[c];
   uint16_t* g = a.wcnt + static_cast<int64_t>(tile) * kDrainWarps * C;
   for (int i = tid; i < kDrainWarps * C; i += blockDim.x) g[i] = wc[i];
   for (int c = tid; c < C; c += blockDim.x) {
@@ -465,7 +464,8 @@ __global__ void __launch_bounds__(kSortThreads) drain_sort_kernel(const DrainArg
     const uint32_t st = cstart[tid];
     const uint32_t en = tid + 1 < C ? cstart[tid + 1] : nvalid;
     a.hist[static_cast<int64_t>(blockIdx.x) * C + tid] = en - st;
-    if (en > st) atomicMin(reinterpret_cast<unsigned int*>(a.first_row) + tid, static_cast<uint32_t>(t0) + (srow[st] & 0xffffu));
+    a.tfirst[static_cast<int64_t>(blockIdx.x) * C + tid] =
+        en > st ? static_cast<uint32_t>(t0) + (srow[st] & 0xffffu) : 0xffffffffu;
   }
   for (int i = tid; i < static_cast<int>(nvalid); i += kSortThreads) a.tsorted[t0 + i] = srow[i];
   EQX_DT_MAX(1);
@@ -521,9 +521,11 @@ __global__ void __launch_bounds__(kSortThreads) drain_scatter_kernel(const Drain
 // Per-client prefix over tiles of the drain histogram, once for the whole batch: CTA b owns
 // clients 32b..32b+31 (one per lane); its 32 warps split the tiles into contiguous chunks,
 // sum them, exchange the chunk sums through shared memory and write every tile's exclusive
-// prefix.  tbase[t][c] = rows of client c in tiles < t, ctot[c] = rows of client c.
+// prefix.  tbase[t][c] = rows of client c in tiles < t, ctot[c] = rows of client c; also the
+// client's first row (min over the tiles' first rows) and the reset queue heads, so the drain
+// needs no memset in front of it.
 __global__ void __launch_bounds__(1024) drain_scan_kernel(const DrainArgs a) {
-  __shared__ uint32_t part[32][33];
+  __shared__ uint32_t part[32][33], pfirst[32][33];
   pdl_wait();     // drain_hist_kernel's histogram is complete
   pdl_trigger();  // drain_rank_kernel may get scheduled
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -532,22 +534,29 @@ __global__ void __launch_bounds__(1024) drain_scan_kernel(const DrainArgs a) {
   const int32_t per = (nt + 31) / 32;
   const int32_t t0 = min(nt, warp * per), t1 = min(nt, t0 + per);
   uint32_t h[8];  // up to 8 tiles per warp in registers (per <= 8 for <= 256 tiles), else re-read
-  uint32_t sum = 0;
+  uint32_t sum = 0, fmin = 0xffffffffu;
   if (c < C) {
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       h[u] = t0 + u < t1 ? __ldcg(a.hist + static_cast<int64_t>(t0 + u) * C + c) : 0u;
+      const uint32_t f = t0 + u < t1 ? __ldcg(a.tfirst + static_cast<int64_t>(t0 + u) * C + c) : 0xffffffffu;
       sum += h[u];
+      fmin = min(fmin, f);
     }
-    for (int32_t t = t0 + 8; t < t1; ++t) sum += __ldcg(a.hist + static_cast<int64_t>(t) * C + c);
+    for (int32_t t = t0 + 8; t < t1; ++t) {
+      sum += __ldcg(a.hist + static_cast<int64_t>(t) * C + c);
+      fmin = min(fmin, __ldcg(a.tfirst + static_cast<int64_t>(t) * C + c));
+    }
   }
   part[warp][lane] = sum;
+  pfirst[warp][lane] = fmin;
   __syncthreads();
-  uint32_t run = 0, tot = 0;
+  uint32_t run = 0, tot = 0, first = 0xffffffffu;
   for (int w = 0; w < 32; ++w) {
     const uint32_t v = part[w][lane];
     run += w < warp ? v : 0u;
     tot += v;
+    first = min(first, pfirst[w][lane]);
   }
   if (c < C) {
 #pragma unroll
@@ -561,7 +570,12 @@ __global__ void __launch_bounds__(1024) drain_scan_kernel(const DrainArgs a) {
       a.tbase[static_cast<int64_t>(t) * C + c] = run;
       run += __ldcg(a.hist + static_cast<int64_t>(t) * C + c);
     }
-    if (warp == 0) a.ctot[c] = tot;
+    if (warp == 0) {
+      a.ctot[c] = tot;
+      a.first_row[c] = static_cast<int32_t>(first);
+      a.head[c] = 0;
+      if (a.zero_qlen) a.qlen_before[c] = 0;
+    }
   }
 }
 

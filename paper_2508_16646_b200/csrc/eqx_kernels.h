@@ -58,12 +58,15 @@ struct DrainArgs {
   uint32_t* tbase;      // [n_tiles][C] rows of the client in earlier tiles (drain_scan_kernel)
   uint32_t* ctot;       // [C] rows of the client in the batch (drain_scan_kernel)
   uint32_t* tsorted;    // [n] small rosters: each tile's rows sorted by client, (client << 16) | row - t0
+  uint32_t* tfirst;     // [n_tiles][C] first row of the client in the tile (0xffffffff: none)
+  int32_t* head;        // [C] queue heads, reset by drain_scan_kernel
+  int32_t zero_qlen;    // drain_scan_kernel also resets qlen_before (a drain that replaces the queue)
   int64_t hist_L;
   int32_t* seg_off;     // [C+1]
   uint32_t* perm;       // [n] row indices grouped by client, FIFO order
   int32_t* count;       // [C] queued requests per client
   int32_t* first_row;   // [C] first arrival row of the client in this drain
-  const int32_t* qlen_before;
+  int32_t* qlen_before;
   const int32_t* running;
   double* ufc;
   double* rfc;

@@ -78,6 +78,7 @@ def test_context_teardown_frees_device_memory():
     from test_gpu_parity import _random_case
     from paper_2508_16646_b200 import scheduler as S
     case = _random_case(77, 20000, 300)
+    case.finalize()
     cols = case_columns(case)
 
     def cycle():
