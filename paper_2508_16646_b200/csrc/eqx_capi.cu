@@ -129,6 +129,11 @@ struct eqx_ctx {
   size_t hist_smem = 0, rank_smem = 0;
   bool staged = true;
   cudaStream_t stream2 = nullptr;  // side stream for whole-queue scoring
+  cudaStream_t stream3 = nullptr;  // the selection's code warm-up (graph step)
+  cudaEvent_t ev_warm = nullptr, ev_warm_done = nullptr;
+  DevBuf d_warm;                   // the warm-up selection's own small problem (scratch)
+  int32_t warm_C = -1;             // clients of the problem d_warm holds
+  SelectArgs warm_se{};            // its launch arguments (prepared before a graph capture)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_k[6] = {};        // timing: score start/end, select start/end, drain start/end
   DevBuf d_done;                   // last-CTA counters of the drain kernels
@@ -481,6 +486,12 @@ void eqx_ctx_destroy(eqx_ctx* ctx) {
     if (ev) cudaEventDestroy(ev);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->stream2) cudaStreamDestroy(ctx->stream2);
+  if (ctx->stream3) {
+    cudaStreamSynchronize(ctx->stream3);
+    cudaStreamDestroy(ctx->stream3);
+  }
+  if (ctx->ev_warm) cudaEventDestroy(ctx->ev_warm);
+  if (ctx->ev_warm_done) cudaEventDestroy(ctx->ev_warm_done);
   if (ctx->copy_stream) {
     cudaStreamSynchronize(ctx->copy_stream);
     cudaStreamDestroy(ctx->copy_stream);
@@ -1314,6 +1325,87 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl, int32_t g
   return EQX_OK;
 }
 
+// The selection kernel's instructions are fetched cold once per step when the L2 was flushed
+// (bench.py's timed steps; ~12 us of cfg2's selection loop).  The graph step therefore starts
+// with a warm-up launch of the same kernel on a small problem of its own (up to 64 clients x 8
+// queued heads in scratch memory: every phase of a regenerating round runs once) on a third
+// stream, concurrently with the drain; the real selection then fetches its code from L2.  The
+// warm-up reads and writes only its scratch.
+static eqx_status warm_args(eqx_ctx* ctx, const StepPlan& pl, SelectArgs& w) {
+  const int32_t C = std::max(1, std::min<int32_t>(64, ctx->C));
+  constexpr int32_t W = 8;
+  // layout: windows | ufc rfc counter weight (f64) | order count head running backlogged (i32)
+  //         | 128 events x 8 columns | DevState | per-client work (cw_global plans)
+  const size_t wb = sizeof(WinEntry) * C * W, ld = 8ull * C, li = 4ull * C, ev = 128;
+  const size_t o_win = 0, o_u = o_win + ((wb + 15) & ~15), o_r = o_u + ld, o_k = o_r + ld, o_w = o_k + ld,
+               o_ord = o_w + ld, o_cnt = o_ord + li, o_head = o_cnt + li, o_run = o_head + li, o_bl = o_run + li,
+               o_ev = (o_bl + li + 15) & ~size_t(15), o_st = o_ev + 8 * 8 * ev,
+               o_cw = (o_st + sizeof(DevState) + 255) & ~size_t(255);
+  const size_t total = o_cw + 64 * 1024;
+  if (ctx->warm_C != C) {
+    CUDA_TRY(ctx, ctx->d_warm.ensure(total));
+    std::vector<unsigned char> h(o_cw, 0);
+    WinEntry* win = reinterpret_cast<WinEntry*>(h.data() + o_win);
+    for (int32_t c = 0; c < C; ++c)
+      for (int32_t k = 0; k < W; ++k) {
+        WinEntry& e = win[c * W + k];
+        e.ufc_inc = 100.0 + 7.0 * ((c * 13 + k * 5) % 17);
+        e.rfc_inc = 50.0 + 3.0 * ((c * 7 + k * 11) % 13);
+        const double arr = 1e-3 * (k * C + c);
+        uint64_t b;
+        std::memcpy(&b, &arr, 8);
+        e.abits = b | 0x8000000000000000ull;  // ordered bits of a non-negative double
+        e.in = 16 + (c + k) % 32;
+        e.pred = 8 + (c * 3 + k) % 24;
+        e.row = c * W + k;
+        e.alone = 1;
+      }
+    for (int32_t c = 0; c < C; ++c) {
+      reinterpret_cast<double*>(h.data() + o_u)[c] = 1000.0 * ((c * 37) % C);
+      reinterpret_cast<double*>(h.data() + o_r)[c] = 100.0 * ((c * 11) % C);
+      reinterpret_cast<double*>(h.data() + o_w)[c] = 1.0;
+      reinterpret_cast<uint32_t*>(h.data() + o_ord)[c] = static_cast<uint32_t>(c);
+      reinterpret_cast<int32_t*>(h.data() + o_cnt)[c] = W;
+      reinterpret_cast<int32_t*>(h.data() + o_bl)[c] = 1;
+    }
+    CUDA_TRY(ctx, cudaMemcpy(ctx->d_warm.p, h.data(), o_cw, cudaMemcpyHostToDevice));
+    ctx->warm_C = C;
+  }
+  char* b = static_cast<char*>(ctx->d_warm.p);
+  w = pl.se;
+  w.C = C;
+  w.W = W;
+  w.gW = 0;
+  w.win_g = reinterpret_cast<const WinEntry*>(b + o_win);
+  w.do_lift = 0;
+  w.ledger_after_wait = 0;
+  w.frozen = Frozen{};
+  w.count = reinterpret_cast<const int32_t*>(b + o_cnt);
+  w.head = reinterpret_cast<int32_t*>(b + o_head);
+  w.ufc = reinterpret_cast<double*>(b + o_u);
+  w.rfc = reinterpret_cast<double*>(b + o_r);
+  w.counter = reinterpret_cast<double*>(b + o_k);
+  w.weight = reinterpret_cast<const double*>(b + o_w);
+  w.order = reinterpret_cast<const uint32_t*>(b + o_ord);
+  w.running = reinterpret_cast<int32_t*>(b + o_run);
+  w.backlogged = reinterpret_cast<int32_t*>(b + o_bl);
+  int32_t* evi = reinterpret_cast<int32_t*>(b + o_ev);
+  w.ev_row = evi;
+  w.ev_kind = evi + ev;
+  w.ev_client = evi + 2 * ev;
+  w.ev_pred = evi + 3 * ev;
+  double* evd = reinterpret_cast<double*>(b + o_ev + 4 * 4 * ev);
+  w.ev_ufc = evd;
+  w.ev_rfc = evd + ev;
+  w.ev_vtc = evd + 2 * ev;
+  w.ev_wait = evd + 3 * ev;
+  w.ev_cap = ev;
+  w.st = reinterpret_cast<DevState*>(b + o_st);
+  w.tk_heads = nullptr;
+  w.cw_global = w.cw_in_smem ? nullptr : static_cast<void*>(b + o_cw);
+  return EQX_OK;
+}
+
 // Stream work of a step.  Scoring (HBM-bound, whole queue) runs on the side stream
 // concurrently with [optional drain ->] selection on the main stream; both join before the
 // summary D2H.  Capturable into a CUDA graph (fork/join through events).
@@ -1333,6 +1425,15 @@ static eqx_status step_enqueue(eqx_ctx* ctx, const StepPlan& pl, bool with_drain
     CUDA_TRY(ctx, cudaMemsetAsync(st + offsetof(DevState, t) + 5 * 8, 0, 8, s));
   }
   if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[4], s));
+  const bool warm = with_drain && ctx->C > 0 && ctx->stream3;
+  if (warm) {  // the selection's code warm-up, concurrent with the drain (see warm_args)
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_warm, s));
+    CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream3, ctx->ev_warm, 0));
+    SelectArgs w = ctx->warm_se;
+    void* args[] = {&w};
+    CUDA_TRY(ctx, cudaLaunchKernel(select_fn(0), dim3(1), dim3(pl.select_threads), args, pl.select_smem, ctx->stream3));
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_warm_done, ctx->stream3));
+  }
   if (with_drain) {
     eqx_status e = drain_enqueue(ctx, false);
     if (e != EQX_OK) return e;
@@ -1372,6 +1473,7 @@ static eqx_status step_enqueue(eqx_ctx* ctx, const StepPlan& pl, bool with_drain
   if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[3], s));
   CUDA_TRY(ctx, cudaGetLastError());
   CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_join, 0));
+  if (warm) CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_warm_done, 0));
   EventFillArgs ef;
   std::memset(&ef, 0, sizeof(ef));
   ef.st = ctx->d_state.as<DevState>();
@@ -1446,6 +1548,15 @@ eqx_status eqx_drain_step_async(eqx_ctx* ctx, const eqx_requests* r, double now)
   // parameter (pointers, sizes, policy, `now`, smem/tiling plan); two graphs are cached, for a
   // resident queue or the staging buffer sets of host batches (whose H2D and release events
   // stay outside the graph).
+  if (ctx->C > 0) {  // the selection code warm-up's problem and stream (outside any capture)
+    eqx_status we = warm_args(ctx, pl, ctx->warm_se);
+    if (we != EQX_OK) return we;
+    if (!ctx->stream3) {
+      CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->stream3, cudaStreamNonBlocking));
+      CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->ev_warm, cudaEventDisableTiming));
+      CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->ev_warm_done, cudaEventDisableTiming));
+    }
+  }
   std::vector<unsigned char> key(sizeof(StepPlan) + 8 * sizeof(int64_t));
   std::memcpy(key.data(), &pl, sizeof(StepPlan));
   const int64_t extra[8] = {ctx->tile_rows, ctx->n_tiles, ctx->counter_lift, static_cast<int64_t>(ctx->hist_smem),
