@@ -1224,6 +1224,7 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl, int32_t g
   a.ev_rfc = ctx->d_ev_rfc.as<double>();
   a.ev_vtc = ctx->d_ev_vtc.as<double>();
   a.ev_wait = ctx->d_ev_wait.as<double>();
+  a.ev_id = ctx->d_ev_id.as<int64_t>();
   a.ev_cap = ctx->ev_cap;
   a.st = ctx->d_state.as<DevState>();
   a.model = ctx->d_model.as<ModelTables>();
@@ -1444,7 +1445,7 @@ static eqx_status step_enqueue(eqx_ctx* ctx, const StepPlan& pl, bool with_drain
   CUDA_TRY(ctx, launch_pdl(window_kernel, dim3(pl.window_grid), dim3(256), pl.window_smem, s, pl.wi));
   // Whole-queue scoring forks off after the windows: the selection CTA (PDL) is resident by
   // then, so the scoring grid fills the other SMs while the one-warp selection loop runs
-  // (nothing in the selection reads the per-request scores; event_fill joins them).
+  // (nothing in the selection reads the per-request scores; the state copy joins them).
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fork, s));
   CUDA_TRY(ctx, cudaStreamWaitEvent(s2, ctx->ev_fork, 0));
   if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[0], s2));
@@ -1472,37 +1473,10 @@ static eqx_status step_enqueue(eqx_ctx* ctx, const StepPlan& pl, bool with_drain
   }
   if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[3], s));
   CUDA_TRY(ctx, cudaGetLastError());
+  // the selection wrote every event with its payload and request id (topk_event); the state
+  // copy follows the scoring (DevState::fallbacks / near_ties) and the warm-up
   CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_join, 0));
   if (warm) CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_warm_done, 0));
-  EventFillArgs ef;
-  std::memset(&ef, 0, sizeof(ef));
-  ef.st = ctx->d_state.as<DevState>();
-  ef.n_events = &ctx->d_state.as<DevState>()->n_events;
-  ef.ev_cap = ctx->ev_cap;
-  ef.ev_row = ctx->d_ev_row.as<int32_t>();
-  ef.ev_kind = ctx->d_ev_kind.as<int32_t>();
-  ef.ev_client = ctx->d_ev_client.as<int32_t>();
-  ef.ev_pred = ctx->d_ev_pred.as<int32_t>();
-  ef.ev_ufc = ctx->d_ev_ufc.as<double>();
-  ef.ev_rfc = ctx->d_ev_rfc.as<double>();
-  ef.ev_vtc = ctx->d_ev_vtc.as<double>();
-  ef.ev_wait = ctx->d_ev_wait.as<double>();
-  ef.pred = ctx->d_pred.as<int32_t>();
-  ef.ufc_inc = ctx->d_ufc_out.as<double>();
-  ef.rfc_inc = ctx->d_rfc_out.as<double>();
-  ef.arrival = ctx->q_arrival;
-  ef.in_tok = ctx->q_in;
-  ef.weight = ctx->d_weight.as<double>();
-  ef.pol = ctx->pol;
-  ef.now = pl.se.now;
-  ef.q_id = ctx->q_id;
-  ef.id_base = ctx->id_base;
-  ef.ev_id = ctx->d_ev_id.as<int64_t>();
-  if (ctx->n > 0) {
-    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ctx->sm_count, (ctx->ev_cap + 255) / 256)));
-    CUDA_TRY(ctx, launch_pdl(event_fill_kernel, dim3(grid), dim3(256), 0, s, ef));
-  }
-  CUDA_TRY(ctx, cudaGetLastError());
   CUDA_TRY(ctx, state_to_host(ctx, s, true));
   return EQX_OK;
 }
@@ -2161,6 +2135,8 @@ eqx_status eqx_shard_select_async(eqx_ctx* ctx, const void* recs, int32_t world,
   StepPlan pl;
   eqx_status st = step_prepare(ctx, now, pl, W);
   if (st != EQX_OK) return st;
+  pl.se.id = ctx->d_gid.as<int64_t>();  // event ids: the gathered heads' global trace positions
+  pl.se.id_base = 0;
   cudaStream_t s = ctx->stream;
   ShardSelectBufs b;
   b.count = ctx->d_count.as<int32_t>();
@@ -2188,27 +2164,6 @@ eqx_status eqx_shard_select_async(eqx_ctx* ctx, const void* recs, int32_t world,
     CUDA_TRY(ctx, cudaLaunchKernel(select_fn(0), dim3(1), dim3(pl.select_threads), args, pl.select_smem, s));
   }
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[3], s));
-  CUDA_TRY(ctx, cudaGetLastError());
-  EventFillArgs ef;
-  std::memset(&ef, 0, sizeof(ef));
-  ef.st = ctx->d_state.as<DevState>();
-  ef.n_events = &ctx->d_state.as<DevState>()->n_events;
-  ef.ev_cap = ctx->ev_cap;
-  ef.ev_row = ctx->d_ev_row.as<int32_t>();
-  ef.ev_kind = ctx->d_ev_kind.as<int32_t>();
-  ef.ev_client = ctx->d_ev_client.as<int32_t>();
-  ef.ev_pred = ctx->d_ev_pred.as<int32_t>();
-  ef.ev_ufc = ctx->d_ev_ufc.as<double>();
-  ef.ev_rfc = ctx->d_ev_rfc.as<double>();
-  ef.ev_vtc = ctx->d_ev_vtc.as<double>();
-  ef.ev_wait = ctx->d_ev_wait.as<double>();
-  ef.weight = ctx->d_weight.as<double>();
-  ef.pol = ctx->pol;
-  ef.now = now;
-  ef.q_id = ctx->d_gid.as<int64_t>();
-  ef.id_base = 0;
-  ef.ev_id = ctx->d_ev_id.as<int64_t>();
-  shard_event_fill_kernel<<<std::max(1, ctx->sm_count / 4), 256, 0, s>>>(ef, ctx->d_win.as<WinEntry>());
   CUDA_TRY(ctx, cudaGetLastError());
   CUDA_TRY(ctx, state_to_host(ctx, s));
   ctx->q_id = ctx->d_gid.as<int64_t>();
@@ -2305,7 +2260,7 @@ eqx_status eqx_copy_events(eqx_ctx* ctx, int64_t cap, int64_t* id, int32_t* kind
   CUDA_TRY(ctx, cudaStreamSynchronize(s));
   const int64_t n = std::min<int64_t>(std::min<int64_t>(cap, ctx->h_state->n_events), ctx->ev_cap);
   if (n <= 0) return EQX_OK;
-  // request ids were gathered inside the step (event_fill_kernel): the id column may live in a
+  // request ids were gathered inside the step (the selection): the id column may live in a
   // staging set the copy stream refills once the step released it
   const size_t n8 = 8ull * n, n4 = 4ull * n;
   const Col cols[] = {{id, ctx->d_ev_id.p, n8},        {kind, ctx->d_ev_kind.p, n4},

@@ -10,10 +10,9 @@
 //   admit_requests (engine.cpp:207-271):
 //     window_kernel      the first W queued requests of every client scored into [C][W] heads
 //     select_topk_kernel one CTA: rounds of block-radix top-K over per-client key streams
-//                        (eqx_topk.cuh)
+//                        (eqx_topk.cuh); writes every event with its payload and request id
 //     score_kernel       whole-queue MoPE predict -> map_metrics -> ufc/rfc increments on a side
 //                        stream (16-byte streaming loads / stores: the HBM-bound stream)
-//     event_fill_kernel  event payloads and request ids from the per-request scores
 //   client-sharded step: shard_export / shard_ingest / shard_unpack kernels
 //   live queues: live_offsets / gather_live / predict_rows kernels
 //   feedback: feedback_kernel
@@ -1290,37 +1289,6 @@ __global__ void __launch_bounds__(kTopkThreads, 1) select_topk_kernel(const Sele
   }
 }
 
-// Event payloads (scheduler.hpp:131-138 PendingContribution) from the per-request scores the
-// scoring kernel wrote: predicted tokens, ufc/rfc increments, the VTC charge and wait_s.
-__global__ void event_fill_kernel(const EventFillArgs a) {
-  pdl_wait();  // programmatic launch: the selection's events are complete
-  const int64_t n = *a.n_events;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n && i < a.ev_cap;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int32_t row = a.ev_row[i];
-    const bool adm = a.ev_kind[i] == 1;
-    const int32_t pred = a.pred[row];
-    a.ev_id[i] = a.q_id ? a.q_id[row] : a.id_base + row;  // read in-step: the id column may be a staging set
-    a.ev_pred[i] = pred;
-    a.ev_ufc[i] = adm ? a.ufc_inc[row] : 0.0;
-    a.ev_rfc[i] = adm ? a.rfc_inc[row] : 0.0;
-    double v = 0.0;
-    if (adm && a.pol.kind == kVtc) {  // scheduler.cpp:169-181
-      const double w = a.weight[a.ev_client[i]];
-      const int32_t in = a.in_tok[row];
-      v = a.pol.vtc_use_prediction
-              ? __dmul_rn(w, __dadd_rn(static_cast<double>(in), __dmul_rn(a.pol.ow, static_cast<double>(pred))))
-              : __dmul_rn(w, static_cast<double>(in));
-    }
-    a.ev_vtc[i] = v;
-    a.ev_wait[i] = adm ? __dsub_rn(a.now, a.arrival[row]) : 0.0;  // engine.cpp:257
-  }
-#ifdef EQX_PROF
-  __syncthreads();
-  if (threadIdx.x == 0) atomicMax(&a.st->dt[7], global_ns());
-#endif
-}
-
 // Staged narrow host columns widened in place of the H2D's second half: 8 rows per thread,
 // 16-byte loads of each u16 column, 2 x 16-byte stores per i32 column.
 __global__ void widen_cols_kernel(const uint16_t* c16, const uint16_t* i16, int64_t n, int32_t* c32, int32_t* i32) {
@@ -1625,37 +1593,6 @@ __global__ void __launch_bounds__(256) shard_unpack_kernel(const ShardMap m, con
     e.row = static_cast<int32_t>(it);
     b.win[it] = e;
     b.gid[it] = reinterpret_cast<const int64_t*>(base + L.id)[src];
-  }
-}
-
-// event_fill_kernel over the gathered windows (row = c * W + k indexes b.win).
-__global__ void shard_event_fill_kernel(const EventFillArgs a, const WinEntry* __restrict__ win) {
-  const int64_t n = *a.n_events;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n && i < a.ev_cap;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int32_t row = a.ev_row[i];
-    const bool adm = a.ev_kind[i] == 1 && row >= 0;
-    a.ev_id[i] = row < 0 ? -1 : (a.q_id ? a.q_id[row] : a.id_base + row);
-    WinEntry e;
-    if (row >= 0) {
-      e = win[row];
-    } else {
-      e.ufc_inc = e.rfc_inc = 0.0;
-      e.abits = 0;
-      e.in = e.pred = 0;
-    }
-    a.ev_pred[i] = e.pred;
-    a.ev_ufc[i] = adm ? e.ufc_inc : 0.0;
-    a.ev_rfc[i] = adm ? e.rfc_inc : 0.0;
-    double v = 0.0;
-    if (adm && a.pol.kind == kVtc) {  // scheduler.cpp:169-181
-      const double w = a.weight[a.ev_client[i]];
-      v = a.pol.vtc_use_prediction
-              ? __dmul_rn(w, __dadd_rn(static_cast<double>(e.in), __dmul_rn(a.pol.ow, static_cast<double>(e.pred))))
-              : __dmul_rn(w, static_cast<double>(e.in));
-    }
-    a.ev_vtc[i] = v;
-    a.ev_wait[i] = adm ? __dsub_rn(a.now, from_ordered_bits(e.abits)) : 0.0;  // engine.cpp:257
   }
 }
 

@@ -194,6 +194,7 @@ struct SelectArgs {
   double* ev_rfc;
   double* ev_vtc;
   double* ev_wait;
+  int64_t* ev_id;
   int64_t ev_cap;
   DevState* st;
   const ModelTables* model;
@@ -201,31 +202,6 @@ struct SelectArgs {
   int64_t tmax;          // largest T with double(T) * m <= M (exact, host binary search)
   Policy pol;
   double now;
-};
-
-struct EventFillArgs {
-  DevState* st;             // EQX_PROF stamp (dt[7]: last event-fill CTA done)
-  const int64_t* n_events;  // &DevState::n_events
-  int64_t ev_cap;
-  const int32_t* ev_row;
-  const int32_t* ev_kind;
-  const int32_t* ev_client;
-  int32_t* ev_pred;
-  double* ev_ufc;
-  double* ev_rfc;
-  double* ev_vtc;
-  double* ev_wait;
-  const int32_t* pred;
-  const double* ufc_inc;
-  const double* rfc_inc;
-  const double* arrival;
-  const int32_t* in_tok;
-  const double* weight;
-  Policy pol;
-  double now;
-  const int64_t* q_id;      // the queue's id column (nullptr: id_base + row)
-  int64_t id_base;
-  int64_t* ev_id;           // [ev_cap] request id of each event
 };
 
 // ---- client-sharded step ------------------------------------------------
@@ -280,7 +256,6 @@ struct ShardSelectBufs {
 __global__ void shard_export_kernel(WindowArgs a, int32_t cmax, unsigned char* rec);
 __global__ void shard_ingest_kernel(ShardMap m, ShardSelectBufs b);
 __global__ void shard_unpack_kernel(ShardMap m, ShardSelectBufs b);
-__global__ void shard_event_fill_kernel(EventFillArgs a, const WinEntry* win);
 
 // ---- completion / feedback ------------------------------------------
 struct FeedbackArgs {
@@ -433,7 +408,6 @@ __global__ void replay_kernel(ReplayArgs a);  // KIND: kFcfs / kVtc / kEquinox; 
 
 __global__ void drain_hist_kernel(DrainArgs a);
 __global__ void lift_kernel(DrainArgs a);
-__global__ void event_fill_kernel(EventFillArgs a);
 __global__ void drain_scan_kernel(DrainArgs a);
 __global__ void drain_sort_kernel(DrainArgs a);     // small rosters: per-tile stable counting sort
 __global__ void drain_scatter_kernel(DrainArgs a);  // small rosters: sorted tiles -> perm

@@ -63,6 +63,26 @@ struct TopkScratch {
 
 enum : uint32_t { kTkValid = 16 };
 
+// One event of the step's log with its payload, written by the selection itself from the item's
+// head entry (the window kernel scored it with the same function the whole-queue scoring uses):
+// the request id, and for an admission the PendingContribution (scheduler.hpp:131-138) --
+// ufc / rfc increments, the VTC charge (scheduler.cpp:169-181) and wait_s = now - arrival
+// (engine.cpp:257).
+__device__ __forceinline__ void topk_event(const SelectArgs& a, int64_t ev, const WinEntry& e, int32_t kind, int32_t c,
+                                           double w) {
+  if (ev >= a.ev_cap) return;
+  const bool adm = kind == 1;
+  a.ev_row[ev] = e.row;
+  a.ev_kind[ev] = kind;
+  a.ev_client[ev] = c;
+  a.ev_pred[ev] = e.pred;
+  a.ev_ufc[ev] = adm ? e.ufc_inc : 0.0;
+  a.ev_rfc[ev] = adm ? e.rfc_inc : 0.0;
+  a.ev_vtc[ev] = adm ? vtc_inc(a.pol, e, w) : 0.0;
+  a.ev_wait[ev] = adm ? __dsub_rn(a.now, from_ordered_bits(e.abits)) : 0.0;
+  a.ev_id[ev] = e.row < 0 ? -1 : (a.id ? a.id[e.row] : a.id_base + e.row);
+}
+
 struct TopkShared {
   unsigned long long orv[3], andv[3];
   int32_t nvalid, nsel, nslot, bin, below, inbin, stop, fn, fs, fb;
@@ -751,13 +771,7 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
       if (tid < cend) {
         const int32_t x = T.srt[tid];
         const int32_t c = T.sc[T.sd[x] >> 8];
-        const WinEntry& e = T.ent[tid];
-        const int64_t ev = S.n_ev + tid;
-        if (ev < a.ev_cap) {
-          a.ev_row[ev] = e.row;
-          a.ev_kind[ev] = alone ? 1 : 2;
-          a.ev_client[ev] = c;
-        }
+        topk_event(a, S.n_ev + tid, T.ent[tid], alone ? 1 : 2, c, cw.w[c]);
         if (alone) atomicAdd(&cw.adm[c], 1);
         T.st[x] = 3;
       }
@@ -825,11 +839,7 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
         const int32_t j = cw.pos[c];
         const bool last = j + 1 == cw.end[c];
         if (!e.alone) {  // engine.cpp:223-234: Rejected, pop_head, no counter change
-          if (n_ev < a.ev_cap) {
-            a.ev_row[n_ev] = e.row;
-            a.ev_kind[n_ev] = 2;
-            a.ev_client[n_ev] = c;
-          }
+          topk_event(a, n_ev, e, 2, c, cw.w[c]);
           ++n_ev;
           ++n_rej;
           T.st[x] = 3;
@@ -854,11 +864,7 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
         cw.rfc[c] = nr;
         if (P.kind == kVtc) cw.cnt[c] = __dadd_rn(cw.cnt[c], vtc_inc(P, e, cw.w[c]));
         cw.adm[c] += 1;
-        if (n_ev < a.ev_cap) {
-          a.ev_row[n_ev] = e.row;
-          a.ev_kind[n_ev] = 1;
-          a.ev_client[n_ev] = c;
-        }
+        topk_event(a, n_ev, e, 1, c, cw.w[c]);
         ++n_ev;
         ++n_adm;
         T.st[x] = 3;
