@@ -62,6 +62,7 @@ struct TopkScratch {
 };
 
 enum : uint32_t { kTkValid = 16 };
+constexpr uint64_t kZeroKey = 0x8000000000000000ull;  // ordered_bits(0.0)
 
 // One event of the step's log with its payload, written by the selection itself from the item's
 // head entry (the window kernel scored it with the same function the whole-queue scoring uses):
@@ -85,7 +86,7 @@ __device__ __forceinline__ void topk_event(const SelectArgs& a, int64_t ev, cons
 
 struct TopkShared {
   unsigned long long orv[3], andv[3];
-  int32_t nvalid, nsel, nslot, bin, below, inbin, stop, fn, fs, fb;
+  int32_t nvalid, nsel, nslot, bin, below, inbin, stop, fn, fs, fb, bad;
   int32_t passes;  // EQX_PROF: radix passes
   unsigned long long bk, ba, bo;                 // the boundary tuple (continuation rounds)
   unsigned long long wbk[32], wba[32], wbo[32];  // its per-warp minima
@@ -316,6 +317,59 @@ __device__ __forceinline__ void topk_scan(int32_t m, long long rv, long long pv,
   px = pb + pi - pv;
 }
 
+// tuple order of select_next: key, head arrival, client_id rank (and stream index for items)
+__device__ __forceinline__ bool tuple_lt(uint64_t k1, uint64_t a1, uint64_t o1, uint64_t k2, uint64_t a2, uint64_t o2) {
+  return k1 < k2 || (k1 == k2 && (a1 < a2 || (a1 == a2 && o1 < o2)));
+}
+
+// The boundary of a continuation: the smallest head tuple (key under maxima mu / mr, head
+// arrival, client rank) among the candidate clients outside the slots, into X.bk / ba / bo.
+// Whole CTA; the caller synchronises before reading X.b*.
+__device__ __noinline__ void topk_boundary(const Policy& P, const ClientWork& cw, const TopkScratch& T, TopkShared& X,
+                                           int32_t C, double mu, double mr) {
+  const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31;
+  uint64_t bk = ~0ull, ba = ~0ull, bo = ~0ull;
+  for (int32_t c = tid; c < C; c += NT) {
+    if (T.hst[c] == 2 || cw.pos[c] >= cw.end[c] || (cw.flags[c] & kSkipped)) continue;
+    const uint64_t k = ordered_bits(hf_key(P, cw.ufc[c], cw.rfc[c], mu, mr, cw.cnt[c]));
+    const uint64_t av = T.ha[c], o = static_cast<uint64_t>(cw.order[c]) << 32;
+    if (tuple_lt(k, av, o, bk, ba, bo)) {
+      bk = k;
+      ba = av;
+      bo = o;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const uint64_t k2 = __shfl_xor_sync(0xffffffffu, bk, o), a2 = __shfl_xor_sync(0xffffffffu, ba, o),
+                   o2 = __shfl_xor_sync(0xffffffffu, bo, o);
+    if (tuple_lt(k2, a2, o2, bk, ba, bo)) {
+      bk = k2;
+      ba = a2;
+      bo = o2;
+    }
+  }
+  if (lane == 0) {
+    X.wbk[tid >> 5] = bk;
+    X.wba[tid >> 5] = ba;
+    X.wbo[tid >> 5] = bo;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 1; w < (NT >> 5); ++w) {
+      const uint64_t k2 = X.wbk[w], a2 = X.wba[w], o2 = X.wbo[w];
+      if (tuple_lt(k2, a2, o2, bk, ba, bo)) {
+        bk = k2;
+        ba = a2;
+        bo = o2;
+      }
+    }
+    X.bk = bk;
+    X.ba = ba;
+    X.bo = bo;
+  }
+}
+
 // The rounds (see the file comment).  Runs on the whole CTA after select_body's prologue.
 __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTables& M, const ClientWork& cw, SelShared& S,
                             const TopkScratch& T) {
@@ -348,6 +402,11 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
   // and only their keys, which move with the maxima, are recomputed.  A continuation stops at
   // the smallest head of a client outside the slot set (the boundary B), at a stream that ran
   // out, or when no item is left; the next round then regenerates.
+  // every ledger non-negative (then so is every generated item's: streams end at a negative
+  // increment) -- a condition of the zero-key fast path below
+  bool nonneg = true;
+  for (int32_t c = tid; c < C; c += NT) nonneg &= cw.ufc[c] >= 0.0 && cw.rfc[c] >= 0.0;
+  nonneg = __syncthreads_and(nonneg) != 0;
   bool regen = true;      // block-uniform
   bool all_slots = true;  // the slots hold every candidate client (no boundary)
   int64_t n = 0;          // items of the current streams
@@ -614,49 +673,8 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
     }
     // ---- continuation with clients outside the slots: their smallest head is the boundary ----
     const bool bounded = !regen && !all_slots;
-    if (bounded) {
-      uint64_t bk = ~0ull, ba = ~0ull, bo = ~0ull;
-      for (int32_t c = tid; c < C; c += NT) {
-        if (T.hst[c] == 2 || cw.pos[c] >= cw.end[c] || (cw.flags[c] & kSkipped)) continue;
-        const uint64_t k = ordered_bits(hf_key(P, cw.ufc[c], cw.rfc[c], mu, mr, cw.cnt[c]));
-        const uint64_t av = T.ha[c], o = static_cast<uint64_t>(cw.order[c]) << 32;
-        if (k < bk || (k == bk && (av < ba || (av == ba && o < bo)))) {
-          bk = k;
-          ba = av;
-          bo = o;
-        }
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        const uint64_t k2 = __shfl_xor_sync(0xffffffffu, bk, o), a2 = __shfl_xor_sync(0xffffffffu, ba, o),
-                       o2 = __shfl_xor_sync(0xffffffffu, bo, o);
-        if (k2 < bk || (k2 == bk && (a2 < ba || (a2 == ba && o2 < bo)))) {
-          bk = k2;
-          ba = a2;
-          bo = o2;
-        }
-      }
-      if (lane == 0) {
-        X.wbk[tid >> 5] = bk;
-        X.wba[tid >> 5] = ba;
-        X.wbo[tid >> 5] = bo;
-      }
-    }
+    if (bounded) topk_boundary(P, cw, T, X, C, mu, mr);
     __syncthreads();
-    if (bounded && tid == 0) {
-      uint64_t bk = X.wbk[0], ba = X.wba[0], bo = X.wbo[0];
-      for (int w = 1; w < (NT >> 5); ++w) {
-        const uint64_t k2 = X.wbk[w], a2 = X.wba[w], o2 = X.wbo[w];
-        if (k2 < bk || (k2 == bk && (a2 < ba || (a2 == ba && o2 < bo)))) {
-          bk = k2;
-          ba = a2;
-          bo = o2;
-        }
-      }
-      X.bk = bk;
-      X.ba = ba;
-      X.bo = bo;
-    }
     const int32_t nvalid = X.nvalid;
     TK_STAMP(3)
     if (nvalid == 0) {  // no candidates (engine.cpp:217) -- or none left in the generated streams
@@ -724,19 +742,28 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
     }
     TK_STAMP(5)
     // ---- 4. the loop body over the ranked items (engine.cpp:216-268) ----
-    // 4a. block scan: slot / KV budgets as prefix sums, up to the first item that does not fit
-    //     or ends the round
-    const int32_t members0 = S.members;
-    const int64_t reserved0 = S.reserved;
+    // The ranked list is walked in segments: a segment ends at the first item that does not
+    // fit or that ends the sorted order's validity (an admission raising a maximum, a max
+    // holder leaving the backlog, the last generated item of a stream).  After a moved maximum
+    // the rest of the list stays usable when, under the new maxima, it is still sorted and its
+    // last item is still below every other unconsumed item and the boundary: the keys are
+    // recomputed and checked in place, and the next segment continues the walk.
     const int32_t nse = min(ns, X.fb);  // the ranked items below the boundary
-    {
+    int32_t base = 0;                   // first ranked position of the segment
+    for (;;) {
+      // 4a. block scan: slot / KV budgets as prefix sums, up to the first item that does not
+      //     fit or ends the segment
+      const int32_t members0 = S.members;
+      const int64_t reserved0 = S.reserved;
+      const double smu = S.max_u, smr = S.max_r;
+      const int32_t q = base + tid;  // this thread's ranked position
       int32_t m = 0;
       long long rv = 0, pv = 0;
       bool alone = false, flag = false;
-      if (tid < nse) {
-        const int32_t x = T.srt[tid];
+      if (q < nse) {
+        const int32_t x = T.srt[q];
         const int32_t s = static_cast<int32_t>(T.sd[x] >> 8), c = T.sc[s], d = static_cast<int32_t>(T.sd[x] & 255u);
-        const WinEntry& e = T.ent[tid];
+        const WinEntry& e = T.ent[q];
         uint8_t f = T.fl[x] & ~(kFlMaxChg | kFlHolder);
         const bool last = T.spos[s] + d + 1 == cw.end[c];
         alone = e.alone;
@@ -745,8 +772,8 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
         if (maxmode) {
           const double ub = T.u[x], rb = T.r[x];
           if (last) {
-            if (ub == mu || rb == mr) f |= kFlHolder;
-          } else if (alone && (mu < __dadd_rn(ub, e.ufc_inc) || mr < __dadd_rn(rb, e.rfc_inc))) {
+            if (ub == smu || rb == smr) f |= kFlHolder;
+          } else if (alone && (smu < __dadd_rn(ub, e.ufc_inc) || smr < __dadd_rn(rb, e.rfc_inc))) {
             f |= kFlMaxChg;
           }
         }
@@ -759,36 +786,36 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
       int32_t mx;
       long long rx, px;
       topk_scan(m, rv, pv, mx, rx, px, X);
-      if (tid < nse) {
+      if (q < nse) {
         const bool nofit = alone && !((members0 + mx + 1 <= P.max_batch) && (reserved0 + rx + rv <= tmax));
-        if (nofit) atomicMin(&X.fn, tid);
-        if (flag) atomicMin(&X.fs, tid);
+        if (nofit) atomicMin(&X.fn, q);
+        if (flag) atomicMin(&X.fs, q);
       }
       __syncthreads();
       const int32_t fn = X.fn, fs = X.fs;
-      const int32_t cend = fn <= fs ? min(fn, nse) : fs + 1;  // items [0, cend) are consumed
+      const int32_t cend = fn <= fs ? min(fn, nse) : fs + 1;  // positions [base, cend) are consumed
       // 4b. commit: events, admissions, per-client ledgers after the client's last consumed item
-      if (tid < cend) {
-        const int32_t x = T.srt[tid];
+      if (q < cend) {
+        const int32_t x = T.srt[q];
         const int32_t c = T.sc[T.sd[x] >> 8];
-        topk_event(a, S.n_ev + tid, T.ent[tid], alone ? 1 : 2, c, cw.w[c]);
+        topk_event(a, S.n_ev + tid, T.ent[q], alone ? 1 : 2, c, cw.w[c]);
         if (alone) atomicAdd(&cw.adm[c], 1);
         T.st[x] = 3;
       }
       __syncthreads();
-      if (tid == cend - 1) {  // round totals
+      if (q == cend - 1) {  // segment totals
         S.members = members0 + mx + m;
         S.reserved = reserved0 + rx + rv;
         S.prefill += px + pv;
         S.n_adm += mx + m;
-        S.n_rej += cend - (mx + m);
-        S.n_ev += cend;
+        S.n_rej += (cend - base) - (mx + m);
+        S.n_ev += cend - base;
       }
-      if (tid < cend) {
-        const int32_t x = T.srt[tid];
+      if (q < cend) {
+        const int32_t x = T.srt[q];
         const int32_t s = static_cast<int32_t>(T.sd[x] >> 8), c = T.sc[s], d = static_cast<int32_t>(T.sd[x] & 255u);
         if (d + 1 >= T.snd[s] || T.st[x + 1] != 3) {  // the client's last consumed item
-          const WinEntry& e = T.ent[tid];
+          const WinEntry& e = T.ent[q];
           double nu = T.u[x], nr = T.r[x], ncn = T.cn[x];
           if (alone) {
             nu = __dadd_rn(nu, e.ufc_inc);
@@ -801,7 +828,7 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
           const int32_t np = T.spos[s] + d + 1;
           if (np == cw.end[c]) cw.flags[c] &= ~kBacklogged;  // pop_head emptied the queue
           cw.pos[c] = np;
-          if (tid == fs && fs < fn) {  // the item that ends the round
+          if (q == fs && fs < fn) {  // the item that ends the segment
             const uint8_t f = T.fl[x];
             if (np == cw.end[c]) {
               if (f & kFlHolder) X.stop = 4;  // maxima need a rescan
@@ -819,6 +846,80 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
         if (!P.backfill) X.stop = 2;  // engine.cpp:239: the head does not fit, the step is over
         else X.stop = 8;              // backfill: skip its client, continue item by item
       }
+      __syncthreads();
+      // 4c'. continue the walk after a moved maximum when the rest of the list is still valid
+      const int32_t sstop = X.stop;
+      if (!(fs < fn && fs < nse) || (sstop & 16) || cend >= nse) break;
+      // Fast path: a maximum rose (no holder left) and the rest of the list has key 0 from its
+      // first to its last item.  With non-negative ledgers and both maxima positive before the
+      // rise, a key is 0 exactly when its weighted numerators are, which a rising maximum keeps
+      // (a positive key stays positive, a zero key stays zero), so those items keep their order
+      // and stay below every other item -- nothing to recompute.
+      if (sstop == 0 && nonneg && smu > 0.0 && smr > 0.0 && T.k[T.srt[cend]] == kZeroKey &&
+          T.k[T.srt[nse - 1]] == kZeroKey) {
+        if (tid == 0) {
+          X.fn = 0x7fffffff;
+          X.fs = 0x7fffffff;
+        }
+        base = cend;
+        __syncthreads();
+        continue;
+      }
+#ifdef EQX_PROF
+      const long long tv0 = clock64();
+#endif
+      if (sstop & 4) cta_maxima(cw, C, S);  // a holder left: the maxima over the backlog
+      const double nmu = S.max_u, nmr = S.max_r;
+      if (tid == 0) X.bad = 0;
+      for (int64_t x = tid; x < n; x += NT) {  // the unconsumed items' keys under the new maxima
+        if (T.st[x] == 3 || !(T.fl[x] & kTkValid)) continue;
+        T.k[x] = ordered_bits(hf_key(P, T.u[x], T.r[x], nmu, nmr, T.cn[x]));
+      }
+      if (bounded) topk_boundary(P, cw, T, X, C, nmu, nmr);
+      __syncthreads();
+      auto item_tuple = [&](int64_t x, uint64_t& k, uint64_t& av, uint64_t& o) {
+        const uint32_t sdv = T.sd[x];
+        k = T.k[x];
+        av = T.a[x];
+        o = (static_cast<uint64_t>(cw.order[T.sc[sdv >> 8]]) << 32) | (sdv & 255u);
+      };
+      uint64_t lk, la, lo;
+      item_tuple(T.srt[nse - 1], lk, la, lo);
+      bool bad = bounded && !tuple_lt(lk, la, lo, X.bk, X.ba, X.bo);
+      for (int32_t r = cend + tid; r + 1 < nse && !bad; r += NT) {  // still sorted
+        uint64_t k1, a1, o1, k2, a2, o2;
+        item_tuple(T.srt[r], k1, a1, o1);
+        item_tuple(T.srt[r + 1], k2, a2, o2);
+        bad = !tuple_lt(k1, a1, o1, k2, a2, o2);
+      }
+      for (int64_t x = tid; x < n && !bad; x += NT) {  // below every other unconsumed item:
+        if (T.st[x] != 0 || !(T.fl[x] & kTkValid)) continue;  // the ones not selected
+        uint64_t k2, a2, o2;
+        item_tuple(x, k2, a2, o2);
+        bad = !tuple_lt(lk, la, lo, k2, a2, o2);
+      }
+      for (int32_t r = nse + tid; r < ns && !bad; r += NT) {  // and the selected ones past the boundary
+        uint64_t k2, a2, o2;
+        item_tuple(T.srt[r], k2, a2, o2);
+        bad = !tuple_lt(lk, la, lo, k2, a2, o2);
+      }
+      if (bad) X.bad = 1;
+      __syncthreads();
+#ifdef EQX_PROF
+      tk[6] += clock64() - tv0;
+      tk[7] += 1;
+#endif
+      if (X.bad) {  // end the round; the next one re-selects under the new maxima
+        if (tid == 0) X.stop = sstop & ~4;  // the maxima were rescanned here already
+        __syncthreads();
+        break;
+      }
+      if (tid == 0) {
+        X.stop = 0;
+        X.fn = 0x7fffffff;
+        X.fs = 0x7fffffff;
+      }
+      base = cend;
       __syncthreads();
     }
     TK_STAMP(6)
@@ -910,7 +1011,7 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
   if (tid == 0) {
     a.st->t[7] = rounds;
     for (int i = 0; i < 8; ++i) a.st->t[8 + i] = cy[i];
-    tk[5] = n_total_items;
+    tk[5] = n_total_items;  // tk[6] / tk[7]: in-round verification cycles / segments
     for (int i = 0; i < 8; ++i) a.st->tk[i] = tk[i];
   }
 #endif

@@ -17,4 +17,4 @@ for i in range(3):
     out = (C.c_double * 35)()
     L.load().eqx_phase_times(sch._ctx, out, 35)
     print(cfg, "admitted", r.n_admitted, "loop us", round(out[3] - out[2], 1) if out[3] else None,
-          "rounds", out[7], "cycles heads/gather/chain/keys/select/rank/scan/seq", [int(x) for x in out[8:16]], "head loads, head radix, head passes, item passes, item selects, items", [int(x) for x in out[27:33]])
+          "rounds", out[7], "cycles heads/gather/chain/keys/select/rank/scan/seq", [int(x) for x in out[8:16]], "head loads, head radix, head passes, item passes, item selects, items, verify cycles, segments", [int(x) for x in out[27:35]])
