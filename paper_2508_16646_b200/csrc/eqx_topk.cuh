@@ -33,7 +33,7 @@ struct TopkScratch {
   double* u;      // gathered: ufc increment -> ufc before the item
   double* r;      // gathered: rfc increment -> rfc before the item
   double* cn;     // gathered: VTC charge -> counter before the item
-  uint8_t* fl;    // kTkValid | kFlAlone | kFlMaxChg | kFlHolder | kFlExh
+  uint8_t* fl;    // kTkValid | kFlAlone | kFlExh
   uint8_t* st;    // radix state: 0 out, 1 in play, 2 selected, 3 consumed
   uint32_t* sd;   // slot << 8 | d
   int32_t cap;
@@ -92,6 +92,7 @@ struct TopkShared {
   unsigned long long wbk[32], wba[32], wbo[32];  // its per-warp minima
   int32_t wm[32];
   long long wr[32], wp[32];
+  double wu[32], wv[32];
 };
 
 // Head entry j of client c: the head windows of window_kernel (L2), or scored on demand beyond
@@ -315,6 +316,58 @@ __device__ __forceinline__ void topk_scan(int32_t m, long long rv, long long pv,
   mx = mb + mi - m;
   rx = rb + ri - rv;
   px = pb + pi - pv;
+}
+
+// topk_scan plus the running maxima of two doubles: exclusive (before this position) and
+// inclusive maxima of (cu, cr) over list positions (-inf where an item contributes nothing).
+__device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }
+__device__ __forceinline__ void topk_scan_mx(int32_t m, long long rv, long long pv, double cu, double cr, int32_t& mx,
+                                             long long& rx, long long& px, double& xu, double& xr, double& iu_out,
+                                             double& ir_out, TopkShared& X) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int32_t mi = m;
+  long long ri = rv, pi = pv;
+  double iu = cu, ir = cr;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t a = __shfl_up_sync(0xffffffffu, mi, o);
+    const long long b = __shfl_up_sync(0xffffffffu, ri, o), c = __shfl_up_sync(0xffffffffu, pi, o);
+    const double du = __shfl_up_sync(0xffffffffu, iu, o), dr = __shfl_up_sync(0xffffffffu, ir, o);
+    if (lane >= o) {
+      mi += a;
+      ri += b;
+      pi += c;
+      iu = dmax(iu, du);
+      ir = dmax(ir, dr);
+    }
+  }
+  double pu = __shfl_up_sync(0xffffffffu, iu, 1), pr = __shfl_up_sync(0xffffffffu, ir, 1);
+  if (lane == 0) pu = pr = -INFINITY;
+  if (lane == 31) {
+    X.wm[warp] = mi;
+    X.wr[warp] = ri;
+    X.wp[warp] = pi;
+    X.wu[warp] = iu;
+    X.wv[warp] = ir;
+  }
+  __syncthreads();
+  int32_t mb = 0;
+  long long rb = 0, pb = 0;
+  double bu = -INFINITY, br = -INFINITY;
+  for (int w = 0; w < warp; ++w) {
+    mb += X.wm[w];
+    rb += X.wr[w];
+    pb += X.wp[w];
+    bu = dmax(bu, X.wu[w]);
+    br = dmax(br, X.wv[w]);
+  }
+  mx = mb + mi - m;
+  rx = rb + ri - rv;
+  px = pb + pi - pv;
+  xu = dmax(bu, pu);
+  xr = dmax(br, pr);
+  iu_out = dmax(bu, iu);
+  ir_out = dmax(br, ir);
 }
 
 // tuple order of select_next: key, head arrival, client_id rank (and stream index for items)
@@ -757,35 +810,49 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
       const int64_t reserved0 = S.reserved;
       const double smu = S.max_u, smr = S.max_r;
       const int32_t q = base + tid;  // this thread's ranked position
+      // zero-key regime: the rest of the list keys 0 under positive maxima and non-negative
+      // ledgers -- rising maxima leave its order and its place below every other item as they
+      // are, so the walk goes on through them (their running maxima are a prefix max)
+      const bool zfast = maxmode && nonneg && smu > 0.0 && smr > 0.0 && T.k[T.srt[base]] == kZeroKey &&
+                         T.k[T.srt[nse - 1]] == kZeroKey;
       int32_t m = 0;
       long long rv = 0, pv = 0;
-      bool alone = false, flag = false;
+      bool alone = false, last = false;
+      double ub = 0.0, rb = 0.0, cu = -INFINITY, cr = -INFINITY;
+      uint8_t f = 0;
       if (q < nse) {
         const int32_t x = T.srt[q];
         const int32_t s = static_cast<int32_t>(T.sd[x] >> 8), c = T.sc[s], d = static_cast<int32_t>(T.sd[x] & 255u);
         const WinEntry& e = T.ent[q];
-        uint8_t f = T.fl[x] & ~(kFlMaxChg | kFlHolder);
-        const bool last = T.spos[s] + d + 1 == cw.end[c];
+        f = T.fl[x];
+        last = T.spos[s] + d + 1 == cw.end[c];
         alone = e.alone;
-        // the maxima-dependent outcomes under the current maxima: a max holder leaving the
-        // backlog with its last request, an admission raising a maximum
-        if (maxmode) {
-          const double ub = T.u[x], rb = T.r[x];
-          if (last) {
-            if (ub == smu || rb == smr) f |= kFlHolder;
-          } else if (alone && (smu < __dadd_rn(ub, e.ufc_inc) || smr < __dadd_rn(rb, e.rfc_inc))) {
-            f |= kFlMaxChg;
-          }
+        ub = T.u[x];
+        rb = T.r[x];
+        if (alone && !last) {  // an admission that keeps its client backlogged: a max candidate
+          cu = __dadd_rn(ub, e.ufc_inc);
+          cr = __dadd_rn(rb, e.rfc_inc);
         }
-        T.fl[x] = f;
         m = alone ? 1 : 0;
         rv = alone ? static_cast<long long>(e.in) + e.pred : 0;
         pv = alone ? e.in : 0;
-        flag = last ? (f & kFlHolder) : ((f & kFlExh) || (alone && (f & kFlMaxChg)));
       }
       int32_t mx;
       long long rx, px;
-      topk_scan(m, rv, pv, mx, rx, px, X);
+      double xu = -INFINITY, xr = -INFINITY, iu = cu, ir = cr;
+      // running maxima only in the zero-key regime; otherwise the segment ends at its first
+      // raise, so the segment-start maxima hold up to it (and its own values raise them)
+      if (zfast) topk_scan_mx(m, rv, pv, cu, cr, mx, rx, px, xu, xr, iu, ir, X);
+      else topk_scan(m, rv, pv, mx, rx, px, X);
+      bool flag = false;
+      if (q < nse) {
+        // the maxima-dependent outcomes under the maxima in force at this position: a max
+        // holder leaving the backlog with its last request, an admission raising a maximum
+        const double cmu = dmax(smu, xu), cmr = dmax(smr, xr);
+        const bool holder = maxmode && last && (ub == cmu || rb == cmr);
+        const bool raise = maxmode && alone && !last && (cmu < cu || cmr < cr);
+        flag = last ? holder : ((f & kFlExh) || (raise && !zfast));
+      }
       if (q < nse) {
         const bool nofit = alone && !((members0 + mx + 1 <= P.max_batch) && (reserved0 + rx + rv <= tmax));
         if (nofit) atomicMin(&X.fn, q);
@@ -803,7 +870,9 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
         T.st[x] = 3;
       }
       __syncthreads();
-      if (q == cend - 1) {  // segment totals
+      if (q == cend - 1) {  // segment totals; the maxima after its admissions
+        S.max_u = dmax(smu, iu);
+        S.max_r = dmax(smr, ir);
         S.members = members0 + mx + m;
         S.reserved = reserved0 + rx + rv;
         S.prefill += px + pv;
@@ -829,16 +898,8 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
           if (np == cw.end[c]) cw.flags[c] &= ~kBacklogged;  // pop_head emptied the queue
           cw.pos[c] = np;
           if (q == fs && fs < fn) {  // the item that ends the segment
-            const uint8_t f = T.fl[x];
-            if (np == cw.end[c]) {
-              if (f & kFlHolder) X.stop = 4;  // maxima need a rescan
-            } else {
-              if (alone && (f & kFlMaxChg)) {
-                if (S.max_u < nu) S.max_u = nu;
-                if (S.max_r < nr) S.max_r = nr;
-              }
-              if (f & kFlExh) X.stop = 16;  // the client's stream ran out: regenerate
-            }
+            if (np == cw.end[c]) X.stop = 4;             // a holder left: maxima need a rescan
+            else if (T.fl[x] & kFlExh) X.stop = 16;      // the client's stream ran out: regenerate
           }
         }
       }
@@ -905,11 +966,13 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
       }
       if (bad) X.bad = 1;
       __syncthreads();
+      const bool valid = X.bad == 0;
+
 #ifdef EQX_PROF
       tk[6] += clock64() - tv0;
       tk[7] += 1;
 #endif
-      if (X.bad) {  // end the round; the next one re-selects under the new maxima
+      if (!valid) {  // end the round; the next one re-selects under the new maxima
         if (tid == 0) X.stop = sstop & ~4;  // the maxima were rescanned here already
         __syncthreads();
         break;
@@ -939,6 +1002,8 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
         const uint8_t fl = T.fl[x];
         const int32_t j = cw.pos[c];
         const bool last = j + 1 == cw.end[c];
+        // a max holder leaving the backlog, under the maxima in force now
+        const bool holder = maxmode && last && (cw.ufc[c] == max_u || cw.rfc[c] == max_r);
         if (!e.alone) {  // engine.cpp:223-234: Rejected, pop_head, no counter change
           topk_event(a, n_ev, e, 2, c, cw.w[c]);
           ++n_ev;
@@ -947,7 +1012,7 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
           cw.pos[c] = j + 1;
           if (last) {
             cw.flags[c] = fc & ~kBacklogged;
-            if (fl & kFlHolder) stop = 4;
+            if (holder) stop = 4;
           } else if (fl & kFlExh) {
             stop = 16;
           }
@@ -972,9 +1037,9 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
         cw.pos[c] = j + 1;
         if (last) {
           cw.flags[c] = fc & ~kBacklogged;
-          if (fl & kFlHolder) stop = 4;
+          if (holder) stop = 4;
         } else {
-          if (fl & kFlMaxChg) {
+          if (maxmode && (max_u < nu || max_r < nr)) {  // the admission raises a maximum
             if (max_u < nu) max_u = nu;
             if (max_r < nr) max_r = nr;
             stop = 1;
