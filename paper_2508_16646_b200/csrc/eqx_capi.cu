@@ -1283,6 +1283,10 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl, int32_t g
     a.tk_cap = static_cast<int32_t>(cap);
     a.tk_dsh = 6;
     a.tk_kcap = kcap;
+    // K of the first round (then doubled while lists run out, else about twice what a round
+    // consumed): 256 measured best across cfg2 / cfg3 / cfg4's 10k roster (64: cfg3 -15%, cfg2
+    // and the 10k roster +12% / +30%; 128 / 512: cfg3 +9% / +26%)
+    a.tk_k0 = 256;
     pl.select_threads = kTopkThreads;
     pl.select_smem = smem;
     CUDA_TRY(ctx, ctx->d_win.ensure(std::max<size_t>(static_cast<size_t>(gW > 0 ? gW : a.W) * C * sizeof(WinEntry), 64)));

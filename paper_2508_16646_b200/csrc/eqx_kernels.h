@@ -174,6 +174,7 @@ struct SelectArgs {
   // top-K rounds (select_topk_kernel, eqx_topk.cuh)
   int32_t tk_dsh;        // log2 of the largest key-stream depth per client
   int32_t tk_kcap;       // largest K of one round (<= threads)
+  int32_t tk_k0;         // K of the first round
   int32_t tk_cap;        // stream items per round
   void* tk_heads;        // [C] head tuples in global scratch (rosters beyond tk_kcap clients whose
                          // tuples do not fit in shared memory; nullptr: shared memory)

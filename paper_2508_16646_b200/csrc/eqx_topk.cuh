@@ -437,7 +437,7 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
     for (int32_t s = tid; s < C; s += NT) T.sc[s] = s;
   // K of a round: the free slots (+ a margin for rejections), grown while lists run out
   const int32_t want = P.backfill ? T.Kcap : max(32, min(T.Kcap, P.max_batch - S.members + 8));
-  int32_t K = min(want, 128);
+  int32_t K = min(want, a.tk_k0);
 #ifdef EQX_PROF
   unsigned long long n_total_items = 0;
   unsigned long long rounds = 0, cy[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tk[8] = {0, 0, 0, 0, 0, 0, 0, 0};
