@@ -194,19 +194,37 @@ __device__ void lift_core(const LiftIn& a, const Key* first_row) {
     int any0 = 0, anyR = 0;
     Key fr = kNone;
     int fc = -1;
-    for (int c = tid; c < C; c += blockDim.x) {
-      const int32_t cnt = a.count[c];
-      if (a.qlen_before[c] > 0) {
-        any0 = 1;
-        mu = fmin(mu, a.ufc[c]);
-        mr = fmin(mr, a.rfc[c]);
-        mc = fmin(mc, a.counter[c]);
-      } else if (cnt > 0 && a.running[c] != 0) {
-        anyR = 1;
+    const int NT = blockDim.x;
+    for (int c0 = tid; c0 < C; c0 += 4 * NT) {  // 4 clients' loads in flight
+      int32_t cnt[4], qb[4], run[4];
+      double u[4], r[4], k[4];
+      Key f[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int c = c0 + j * NT;
+        const bool in = c < C;
+        cnt[j] = in ? a.count[c] : 0;
+        qb[j] = in ? a.qlen_before[c] : 0;
+        run[j] = in ? a.running[c] : 0;
+        u[j] = in ? a.ufc[c] : 0.0;
+        r[j] = in ? a.rfc[c] : 0.0;
+        k[j] = in ? a.counter[c] : 0.0;
+        f[j] = in ? first_row[c] : kNone;
       }
-      if (cnt > 0 && first_row[c] < fr) {
-        fr = first_row[c];
-        fc = c;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (qb[j] > 0) {
+          any0 = 1;
+          mu = fmin(mu, u[j]);
+          mr = fmin(mr, r[j]);
+          mc = fmin(mc, k[j]);
+        } else if (cnt[j] > 0 && run[j] != 0) {
+          anyR = 1;
+        }
+        if (cnt[j] > 0 && f[j] < fr) {
+          fr = f[j];
+          fc = c0 + j * NT;
+        }
       }
     }
 #pragma unroll
@@ -252,7 +270,34 @@ __device__ void lift_core(const LiftIn& a, const Key* first_row) {
       bc = a.counter[fc0];
     }
     __syncthreads();  // everyone has read the base before any lift is written
-    if (any_s0 || fc0 >= 0) {
+    if ((any_s0 || fc0 >= 0) && !any_r) {  // the common case: one base for every lifted client
+      const int NT = blockDim.x;
+      for (int c0 = tid; c0 < C; c0 += 4 * NT) {  // 4 clients' loads in flight
+        int32_t cnt[4], qb[4], run[4];
+        double u[4], r[4], k[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int c = c0 + j * NT;
+          const bool in = c < C;
+          cnt[j] = in ? a.count[c] : 0;
+          qb[j] = in ? a.qlen_before[c] : 0;
+          run[j] = in ? a.running[c] : 0;
+          u[j] = in ? a.ufc[c] : 0.0;
+          r[j] = in ? a.rfc[c] : 0.0;
+          k[j] = in ? a.counter[c] : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int c = c0 + j * NT;
+          if (cnt[j] == 0 || qb[j] > 0 || run[j] != 0) continue;
+          if (!any_s0 && c == fc0) continue;
+          // std::max(own, min): own unless own < min
+          if (u[j] < bu) a.ufc[c] = bu;
+          if (r[j] < br) a.rfc[c] = br;
+          if (k[j] < bc) a.counter[c] = bc;
+        }
+      }
+    } else if (any_s0 || fc0 >= 0) {
       for (int c = tid; c < C; c += blockDim.x) {
         if (a.count[c] == 0 || a.qlen_before[c] > 0 || a.running[c] != 0) continue;
         if (!any_s0 && c == fc0) continue;
@@ -275,7 +320,20 @@ __device__ void lift_core(const LiftIn& a, const Key* first_row) {
       }
     }
   }
-  for (int c = tid; c < C; c += blockDim.x) a.backlogged[c] = (a.qlen_before[c] + a.count[c]) > 0 ? 1 : 0;
+  {
+    const int NT = blockDim.x;
+    for (int c0 = tid; c0 < C; c0 += 4 * NT) {
+      int32_t v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int c = c0 + j * NT;
+        v[j] = c < C ? a.qlen_before[c] + a.count[c] : 0;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (c0 + j * NT < C) a.backlogged[c0 + j * NT] = v[j] > 0 ? 1 : 0;
+    }
+  }
 }
 
 // on_activated / set_backlogged for a drained queue (counts from drain_rank_kernel, first
@@ -1121,10 +1179,23 @@ __device__ __forceinline__ double vtc_inc(const Policy& P, const WinEntry& e, do
 __device__ void cta_maxima(const ClientWork& cw, int32_t C, SelShared& S) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   double mu = 0.0, mr = 0.0;
-  for (int32_t c = tid; c < C; c += blockDim.x) {
-    if (!(cw.flags[c] & kBacklogged)) continue;
-    if (mu < cw.ufc[c]) mu = cw.ufc[c];
-    if (mr < cw.rfc[c]) mr = cw.rfc[c];
+  const int NT = blockDim.x;
+  for (int32_t c0 = tid; c0 < C; c0 += 4 * NT) {  // 4 clients' loads in flight (huge rosters: L2)
+    int32_t fl[4];
+    double u[4], r[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int32_t c = c0 + k * NT;
+      fl[k] = c < C ? cw.flags[c] : 0;
+      u[k] = c < C ? cw.ufc[c] : 0.0;
+      r[k] = c < C ? cw.rfc[c] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (!(fl[k] & kBacklogged)) continue;
+      if (mu < u[k]) mu = u[k];
+      if (mr < r[k]) mr = r[k];
+    }
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
@@ -1242,19 +1313,42 @@ __global__ void __launch_bounds__(kTopkThreads, 1) select_topk_kernel(const Sele
   }
   // ---- ledger in ----
   if (a.ledger_after_wait) pdl_wait();  // lifted by the window kernel's extra CTA
-  for (int32_t c = tid; c < C; c += NT) {
-    cw.ufc[c] = a.ufc[c];
-    cw.rfc[c] = a.rfc[c];
-    cw.cnt[c] = a.counter[c];
-    cw.w[c] = a.weight[c];
-    cw.pos[c] = a.head[c];
-    cw.pos0[c] = a.head[c];
-    cw.end[c] = a.count[c];
-    const uint32_t o = a.order[c];
-    cw.order[c] = o;
-    cw.by_order[o] = c;
-    cw.flags[c] = a.backlogged[c] ? kBacklogged : 0;
-    cw.adm[c] = 0;
+  // Loads of 2 clients are issued before any store: the work arrays may alias nothing, but the
+  // compiler cannot know it, and a load-store-load chain costs one memory round trip per field.
+  for (int32_t c0 = tid; c0 < C; c0 += 2 * NT) {
+    double u[2], r[2], k[2], w[2];
+    int32_t h[2], n[2], bl[2];
+    uint32_t o[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int32_t c = c0 + j * NT;
+      if (c < C) {
+        u[j] = a.ufc[c];
+        r[j] = a.rfc[c];
+        k[j] = a.counter[c];
+        w[j] = a.weight[c];
+        h[j] = a.head[c];
+        n[j] = a.count[c];
+        o[j] = a.order[c];
+        bl[j] = a.backlogged[c];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int32_t c = c0 + j * NT;
+      if (c >= C) continue;
+      cw.ufc[c] = u[j];
+      cw.rfc[c] = r[j];
+      cw.cnt[c] = k[j];
+      cw.w[c] = w[j];
+      cw.pos[c] = h[j];
+      cw.pos0[c] = h[j];
+      cw.end[c] = n[j];
+      cw.order[c] = o[j];
+      cw.by_order[o[j]] = c;
+      cw.flags[c] = bl[j] ? kBacklogged : 0;
+      cw.adm[c] = 0;
+    }
   }
   if (!a.ledger_after_wait) pdl_wait();  // window_kernel's [C][W] head entries (read from L2 by the rounds)
   if (tid == 0) {
@@ -1271,13 +1365,33 @@ __global__ void __launch_bounds__(kTopkThreads, 1) select_topk_kernel(const Sele
   if (tid == 0) a.st->t[3] = global_ns();
   pdl_trigger();  // the event fill may get scheduled while the ledger is written back
   // ---- write back ledger, heads, batch, summary ----
-  for (int32_t c = tid; c < C; c += NT) {
-    a.ufc[c] = cw.ufc[c];
-    a.rfc[c] = cw.rfc[c];
-    a.counter[c] = cw.cnt[c];
-    a.head[c] = cw.pos[c];
-    a.backlogged[c] = (cw.flags[c] & kBacklogged) ? 1 : 0;
-    a.running[c] += cw.adm[c];
+  for (int32_t c0 = tid; c0 < C; c0 += 2 * NT) {  // loads first, as for the ledger in
+    double u[2], r[2], k[2];
+    int32_t h[2], f[2], ad[2], run[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int32_t c = c0 + j * NT;
+      if (c < C) {
+        u[j] = cw.ufc[c];
+        r[j] = cw.rfc[c];
+        k[j] = cw.cnt[c];
+        h[j] = cw.pos[c];
+        f[j] = cw.flags[c];
+        ad[j] = cw.adm[c];
+        run[j] = a.running[c];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int32_t c = c0 + j * NT;
+      if (c >= C) continue;
+      a.ufc[c] = u[j];
+      a.rfc[c] = r[j];
+      a.counter[c] = k[j];
+      a.head[c] = h[j];
+      a.backlogged[c] = (f[j] & kBacklogged) ? 1 : 0;
+      a.running[c] = run[j] + ad[j];
+    }
   }
   if (tid == 0) {
     a.st->members = S.members;
@@ -1554,13 +1668,33 @@ __global__ void __launch_bounds__(256) shard_export_kernel(const WindowArgs a, i
 
 __global__ void __launch_bounds__(1024) shard_ingest_kernel(const ShardMap m, const ShardSelectBufs b) {
   const RecLayout L = rec_layout(m.cmax, m.W);
-  for (int32_t c = threadIdx.x; c < m.C; c += blockDim.x) {
-    const int32_t r = rank_of(m, c), l = c - m.off[r];
-    const unsigned char* base = m.recs + static_cast<int64_t>(r) * m.stride;
-    b.count[c] = reinterpret_cast<const int32_t*>(base + L.count)[l];
-    b.first[c] = reinterpret_cast<const int64_t*>(base + L.first)[l];
-    b.head[c] = 0;
-    b.qlen_before[c] = 0;
+  const int NT = blockDim.x;
+  unsigned long long mine = 0;
+  for (int32_t c0 = threadIdx.x; c0 < m.C; c0 += 4 * NT) {  // 4 clients' record loads in flight
+    int32_t cnt[4];
+    int64_t f[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int32_t c = c0 + j * NT;
+      cnt[j] = 0;
+      f[j] = 0;
+      if (c < m.C) {
+        const int32_t r = rank_of(m, c), l = c - m.off[r];
+        const unsigned char* base = m.recs + static_cast<int64_t>(r) * m.stride;
+        cnt[j] = reinterpret_cast<const int32_t*>(base + L.count)[l];
+        f[j] = reinterpret_cast<const int64_t*>(base + L.first)[l];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int32_t c = c0 + j * NT;
+      if (c >= m.C) continue;
+      b.count[c] = cnt[j];
+      b.first[c] = f[j];
+      b.head[c] = 0;
+      b.qlen_before[c] = 0;
+      mine += static_cast<unsigned long long>(cnt[j]);
+    }
   }
   __shared__ unsigned long long total;
   if (threadIdx.x == 0) {
@@ -1568,8 +1702,6 @@ __global__ void __launch_bounds__(1024) shard_ingest_kernel(const ShardMap m, co
     total = 0;
   }
   __syncthreads();
-  unsigned long long mine = 0;
-  for (int32_t c = threadIdx.x; c < m.C; c += blockDim.x) mine += static_cast<unsigned long long>(b.count[c]);
 #pragma unroll
   for (int o = 16; o; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
   if ((threadIdx.x & 31) == 0) atomicAdd(&total, mine);  // one shared atomic per warp
