@@ -155,7 +155,7 @@ struct eqx_ctx {
   size_t h_scratch_bytes = 0;
   DevState* h_state_dev = nullptr; // device alias of the mapped h_state
   // launch-attribute caches (cudaFuncSetAttribute / occupancy queries cost host time per step)
-  int smem_attr[12] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};  // drain_hist, drain_rank, select kernels (select_fn)
+  int smem_attr[13] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};  // drain_hist, drain_rank, select kernels (select_fn)
   size_t occ_smem = SIZE_MAX;
   int occ_per_sm = 1;
   // client-sharded step (selection context): gathered windows and their ids
@@ -207,7 +207,12 @@ struct Col {
 };
 
 // The selection kernel (one variant: rounds of block-radix top-K, eqx_topk.cuh).
-const void* select_fn(int) { return reinterpret_cast<const void*>(select_topk_kernel); }
+// the selection kernel of a plan: the huge-roster instantiation when the head tuples live in
+// global scratch
+const void* select_fn(bool huge) {
+  return huge ? reinterpret_cast<const void*>(select_topk_kernel<true>)
+              : reinterpret_cast<const void*>(select_topk_kernel<false>);
+}
 
 // Programmatic dependent launch: the kernel may be scheduled while its predecessor on the
 // stream is still finishing; it executes griddepcontrol.wait before touching the predecessor's
@@ -1326,7 +1331,7 @@ static eqx_status step_prepare(eqx_ctx* ctx, double now, StepPlan& pl, int32_t g
   pl.window_smem = model_smem;
   const int64_t witems = static_cast<int64_t>(C) * a.W;
   pl.window_grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((witems + 255) / 256, 8ll * ctx->sm_count)));
-  CUDA_TRY(ctx, set_smem_attr(ctx, 10, select_fn(0), pl.select_smem));
+  CUDA_TRY(ctx, set_smem_attr(ctx, a.tk_heads ? 12 : 10, select_fn(a.tk_heads != nullptr), pl.select_smem));
   return EQX_OK;
 }
 
@@ -1436,7 +1441,7 @@ static eqx_status step_enqueue(eqx_ctx* ctx, const StepPlan& pl, bool with_drain
     CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream3, ctx->ev_warm, 0));
     SelectArgs w = ctx->warm_se;
     void* args[] = {&w};
-    CUDA_TRY(ctx, cudaLaunchKernel(select_fn(0), dim3(1), dim3(pl.select_threads), args, pl.select_smem, ctx->stream3));
+    CUDA_TRY(ctx, cudaLaunchKernel(select_fn(pl.se.tk_heads != nullptr), dim3(1), dim3(pl.select_threads), args, pl.select_smem, ctx->stream3));
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev_warm_done, ctx->stream3));
   }
   if (with_drain) {
@@ -1473,7 +1478,7 @@ static eqx_status step_enqueue(eqx_ctx* ctx, const StepPlan& pl, bool with_drain
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    CUDA_TRY(ctx, cudaLaunchKernelExC(&cfg, select_fn(0), args));
+    CUDA_TRY(ctx, cudaLaunchKernelExC(&cfg, select_fn(pl.se.tk_heads != nullptr), args));
   }
   if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[3], s));
   CUDA_TRY(ctx, cudaGetLastError());
@@ -2165,7 +2170,7 @@ eqx_status eqx_shard_select_async(eqx_ctx* ctx, const void* recs, int32_t world,
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[2], s));
   {
     void* args[] = {const_cast<SelectArgs*>(&pl.se)};
-    CUDA_TRY(ctx, cudaLaunchKernel(select_fn(0), dim3(1), dim3(pl.select_threads), args, pl.select_smem, s));
+    CUDA_TRY(ctx, cudaLaunchKernel(select_fn(pl.se.tk_heads != nullptr), dim3(1), dim3(pl.select_threads), args, pl.select_smem, s));
   }
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[3], s));
   CUDA_TRY(ctx, cudaGetLastError());

@@ -1229,6 +1229,7 @@ __device__ void cta_maxima(const ClientWork& cw, int32_t C, SelShared& S) {
 // per-client work arrays (shared memory, or global scratch on huge rosters) and loads the
 // ledger -- after the window kernel's programmatic completion when that kernel applied the
 // drain's counter lift -- and the epilogue writes back ledger, heads, batch and summary.
+template <bool kHugeRoster>
 __global__ void __launch_bounds__(kTopkThreads, 1) select_topk_kernel(const SelectArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ SelShared S;
@@ -1361,7 +1362,7 @@ __global__ void __launch_bounds__(kTopkThreads, 1) select_topk_kernel(const Sele
   if (tid == 0) a.st->t[1] = global_ns();
   cta_maxima(cw, C, S);
   if (tid == 0) a.st->t[2] = global_ns();
-  topk_select(a, M, cw, S, TK);
+  topk_select<kHugeRoster>(a, M, cw, S, TK);
   if (tid == 0) a.st->t[3] = global_ns();
   pdl_trigger();  // the event fill may get scheduled while the ledger is written back
   // ---- write back ledger, heads, batch, summary ----
@@ -1402,6 +1403,8 @@ __global__ void __launch_bounds__(kTopkThreads, 1) select_topk_kernel(const Sele
     a.st->new_prefill = S.prefill;
   }
 }
+template __global__ void select_topk_kernel<false>(SelectArgs);
+template __global__ void select_topk_kernel<true>(SelectArgs);
 
 // Staged narrow host columns widened in place of the H2D's second half: 8 rows per thread,
 // 16-byte loads of each u16 column, 2 x 16-byte stores per i32 column.

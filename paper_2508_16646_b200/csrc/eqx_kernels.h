@@ -416,6 +416,7 @@ __global__ void drain_rank_kernel(DrainArgs a);
 __global__ void score_kernel(ScoreArgs a);
 __global__ void score_tma_kernel(ScoreArgs a);
 __global__ void window_kernel(WindowArgs a);
+template <bool kHugeRoster>  // true: head tuples in global scratch (tk_heads != nullptr)
 __global__ void select_topk_kernel(SelectArgs a);  // the admission loop as rounds of block-radix top-K (eqx_topk.cuh)
 
 }  // namespace eqx

@@ -86,7 +86,7 @@ __device__ __forceinline__ void topk_event(const SelectArgs& a, int64_t ev, cons
 
 struct TopkShared {
   unsigned long long orv[3], andv[3];
-  int32_t nvalid, nsel, nslot, bin, below, inbin, stop, fn, fs, fb, bad;
+  int32_t nvalid, nsel, nslot, bin, below, inbin, stop, fn, fs, fb, bad, nlist;
   int32_t passes;  // EQX_PROF: radix passes
   unsigned long long bk, ba, bo;                 // the boundary tuple (continuation rounds)
   unsigned long long wbk[32], wba[32], wbo[32];  // its per-warp minima
@@ -144,6 +144,23 @@ struct HeadView {
   }
 };
 
+// The in-play heads after a first pass over a large roster, compacted into shared memory: list
+// entry i is client idx[i], with its own radix state lst[i].
+struct HeadListView {
+  const TopkScratch& T;
+  const ClientWork& cw;
+  const uint32_t* idx;
+  uint8_t* lst;
+  int64_t n;
+  __device__ __forceinline__ uint8_t* st() const { return lst; }
+  __device__ __forceinline__ uint64_t field(int64_t x, int f) const {
+    const uint32_t c = idx[x];
+    if (f == 0) return T.hk[c];
+    if (f == 1) return T.ha[c];
+    return static_cast<uint64_t>(cw.order[c]) << 32;
+  }
+};
+
 __device__ __forceinline__ void topk_or_and_commit(uint64_t o, uint64_t an, TopkShared& X, int b) {
   const uint32_t ohi = __reduce_or_sync(0xffffffffu, static_cast<uint32_t>(o >> 32));
   const uint32_t olo = __reduce_or_sync(0xffffffffu, static_cast<uint32_t>(o));
@@ -176,6 +193,43 @@ __device__ __forceinline__ uint64_t topk_diff(const V& v, int f, TopkShared& X) 
   const uint64_t d = X.orv[2] ^ X.andv[2];
   __syncthreads();  // X.orv[2] / X.andv[2] are reset by the next call
   return d;
+}
+
+// Warp 0: the histogram bin where the running count reaches need, into X.bin / below / inbin.
+__device__ __forceinline__ void topk_find_bin(const uint32_t* hist, int32_t need, TopkShared& X) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid < 32) {  // the bin where the running count reaches need
+    uint32_t h[8], sum = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      h[i] = hist[lane * 8 + i];
+      sum += h[i];
+    }
+    uint32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const uint32_t excl = incl - sum;
+    const unsigned hit =
+        __ballot_sync(0xffffffffu, excl < static_cast<uint32_t>(need) && static_cast<uint32_t>(need) <= incl);
+    if (lane == __ffs(hit) - 1) {
+      uint32_t cum = excl;
+      int b = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (cum + h[i] >= static_cast<uint32_t>(need)) {
+          b = i;
+          break;
+        }
+        cum += h[i];
+      }
+      X.bin = lane * 8 + b;
+      X.below = static_cast<int32_t>(cum);
+      X.inbin = static_cast<int32_t>(h[b]);
+    }
+  }
 }
 
 // MSB-first radix select of the `need` smallest composites among the in-play entries (st == 1):
@@ -221,38 +275,7 @@ __device__ void topk_radix_select(const V& v, int32_t need, uint32_t* hist, Topk
       if (dg != 256 && lane == __ffs(m) - 1) atomicAdd(&hist[dg], static_cast<uint32_t>(__popc(m)));
     }
     __syncthreads();
-    if (tid < 32) {  // the bin where the running count reaches need
-      uint32_t h[8], sum = 0;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        h[i] = hist[lane * 8 + i];
-        sum += h[i];
-      }
-      uint32_t incl = sum;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
-      }
-      const uint32_t excl = incl - sum;
-      const unsigned hit =
-          __ballot_sync(0xffffffffu, excl < static_cast<uint32_t>(need) && static_cast<uint32_t>(need) <= incl);
-      if (lane == __ffs(hit) - 1) {
-        uint32_t cum = excl;
-        int b = 0;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          if (cum + h[i] >= static_cast<uint32_t>(need)) {
-            b = i;
-            break;
-          }
-          cum += h[i];
-        }
-        X.bin = lane * 8 + b;
-        X.below = static_cast<int32_t>(cum);
-        X.inbin = static_cast<int32_t>(h[b]);
-      }
-    }
+    topk_find_bin(hist, need, X);
     __syncthreads();
     const uint32_t bin = static_cast<uint32_t>(X.bin);
     need -= X.below;
@@ -423,7 +446,100 @@ __device__ __noinline__ void topk_boundary(const Policy& P, const ClientWork& cw
   }
 }
 
+// The K smallest head tuples of a large roster (entries with T.hst == 1; X.orv / andv hold each
+// field's OR / AND over them): they end with hst == 2, the others with 0.  The first radix pass
+// runs over the whole roster in global scratch and compacts the entries left in play (the bin
+// that holds the K-th tuple) into shared memory; the remaining passes run over that list.
+__device__ __forceinline__ void topk_head_select(const TopkScratch& T, const ClientWork& cw, int32_t C, int32_t K,
+                                                 TopkShared& X) {
+  const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31;
+  int f = 0;
+  uint64_t diff = X.orv[0] ^ X.andv[0];
+  if (!diff) {
+    f = 1;
+    diff = X.orv[1] ^ X.andv[1];
+  }
+  if (!diff) {
+    f = 2;
+    diff = X.orv[2] ^ X.andv[2];  // client ranks are distinct: nonzero with two candidates
+  }
+  const int hi = 63 - __clzll(static_cast<long long>(diff));
+  const int lo = hi >= 7 ? hi - 7 : 0;
+  const uint32_t mask = (1u << (hi - lo + 1)) - 1u;
+  const HeadView hv{T, cw, C};
+  uint32_t* hist = T.hist;
+  for (int i = tid; i < 256; i += NT) hist[i] = 0;
+  if (tid == 0) X.nlist = 0;
+  __syncthreads();
+  // the scans load kB entries' state and field together (one L2 round trip per batch; the field
+  // of a non-candidate is a stale but readable word)
+  constexpr int kB = 4;
+  for (int64_t base = tid - lane; base < C; base += kB * NT) {
+    uint32_t dg[kB];
+#pragma unroll
+    for (int j = 0; j < kB; ++j) {
+      const int64_t x = base + lane + j * NT;
+      const bool in = x < C;
+      const uint8_t h = in ? T.hst[x] : 0;
+      const uint64_t w = in ? hv.field(x, f) : 0;
+      dg[j] = h == 1 ? static_cast<uint32_t>(w >> lo) & mask : 256u;
+    }
+#pragma unroll
+    for (int j = 0; j < kB; ++j) {
+      if (!__ballot_sync(0xffffffffu, dg[j] != 256)) continue;
+      const unsigned m = peer_mask(dg[j], 9);
+      if (dg[j] != 256 && lane == __ffs(m) - 1) atomicAdd(&hist[dg[j]], static_cast<uint32_t>(__popc(m)));
+    }
+  }
+  __syncthreads();
+  topk_find_bin(hist, K, X);
+  __syncthreads();
+  const uint32_t bin = static_cast<uint32_t>(X.bin);
+  const int32_t need = K - X.below;
+  const bool all_in = X.inbin == need;
+  uint32_t* idx = T.sd;  // item arrays are free before a round's streams are generated
+  uint8_t* lst = T.st;
+  for (int64_t base = tid - lane; base < C; base += kB * NT) {
+    uint32_t dg[kB];
+#pragma unroll
+    for (int j = 0; j < kB; ++j) {
+      const int64_t x = base + lane + j * NT;
+      const bool in = x < C;
+      const uint8_t h = in ? T.hst[x] : 0;
+      const uint64_t w = in ? hv.field(x, f) : 0;
+      dg[j] = h == 1 ? static_cast<uint32_t>(w >> lo) & mask : 256u;
+    }
+#pragma unroll
+    for (int j = 0; j < kB; ++j) {
+      const int64_t x = base + lane + j * NT;
+      const bool keep = dg[j] == bin && !all_in;
+      if (dg[j] != 256 && !keep) T.hst[x] = dg[j] < bin || dg[j] == bin ? 2 : 0;
+      const unsigned km = __ballot_sync(0xffffffffu, keep);
+      if (!km) continue;
+      int32_t b0 = 0;
+      if (lane == __ffs(km) - 1) b0 = atomicAdd(&X.nlist, __popc(km));
+      b0 = __shfl_sync(0xffffffffu, b0, __ffs(km) - 1);
+      const int32_t i = b0 + __popc(km & ((1u << lane) - 1u));
+      if (keep && i < T.cap) {
+        idx[i] = static_cast<uint32_t>(x);
+        lst[i] = 1;
+      }
+    }
+  }
+  __syncthreads();
+  if (all_in) return;
+  const int32_t nl = X.nlist;
+  if (nl > T.cap) {  // the bin overflows the list: the remaining passes over the whole roster
+    topk_radix_select(hv, need, hist, X);
+    return;
+  }
+  topk_radix_select(HeadListView{T, cw, idx, lst, nl}, need, hist, X);
+  for (int32_t i = tid; i < nl; i += NT) T.hst[idx[i]] = lst[i];
+  __syncthreads();
+}
+
 // The rounds (see the file comment).  Runs on the whole CTA after select_body's prologue.
+template <bool kHugeRoster>
 __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTables& M, const ClientWork& cw, SelShared& S,
                             const TopkScratch& T) {
   __shared__ TopkShared X;
@@ -481,19 +597,86 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
     nslot = C;
     all_slots = true;
     if (big) {
+      // Heads in global scratch (huge rosters): every candidate's head tuple with the OR / AND of
+      // each field, then topk_head_select (first pass over the roster, the rest over a shared-
+      // memory list).  Heads in shared memory: the tuples, then the generic radix select.
+      constexpr bool gheads = kHugeRoster;  // == (a.tk_heads != nullptr)
       int32_t nc = 0;
-      for (int32_t c = tid; c < C; c += NT) {
-        const bool cand = cw.pos[c] < cw.end[c] && !(cw.flags[c] & kSkipped);
-        if (cand) {
-          T.ha[c] = topk_entry(a, M, cw, c, cw.pos[c]).abits;
-          T.hk[c] = ordered_bits(hf_key(P, cw.ufc[c], cw.rfc[c], mu, mr, cw.cnt[c]));
+      uint64_t o0 = 0, a0 = ~0ull, o1 = 0, a1 = ~0ull, o2 = 0, a2 = ~0ull;
+      if (gheads) {
+        if (tid == 0)
+          for (int i = 0; i < 3; ++i) {
+            X.orv[i] = 0;
+            X.andv[i] = ~0ull;
+          }
+        const int32_t depth = a.gW > 0 ? a.gW : a.W;
+        for (int32_t c0 = tid; c0 < C; c0 += 2 * NT) {  // two clients' loads in flight together
+          int32_t pos[2], k0[2];
+          bool cnd[2];
+          double u[2], r[2], n[2];
+          uint32_t ord[2];
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int32_t c = min(c0 + j * NT, C - 1);
+            pos[j] = cw.pos[c];
+            k0[j] = pos[j] - cw.pos0[c];
+            cnd[j] = c0 + j * NT < C && pos[j] < cw.end[c] && !(cw.flags[c] & kSkipped);
+            u[j] = cw.ufc[c];
+            r[j] = cw.rfc[c];
+            n[j] = cw.cnt[c];
+            ord[j] = cw.order[c];
+          }
+          uint64_t hab[2];
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int32_t c = min(c0 + j * NT, C - 1);
+            hab[j] = cnd[j] && k0[j] < depth
+                         ? __ldcg(reinterpret_cast<const unsigned long long*>(
+                                      a.win_g + static_cast<int64_t>(c) * depth + k0[j]) + 2)
+                         : 0;
+          }
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int32_t c = c0 + j * NT;
+            if (c >= C) continue;
+            const bool cand = cnd[j];
+            if (cand) {
+              const uint64_t hav = k0[j] < depth ? hab[j] : topk_entry(a, M, cw, c, pos[j]).abits;
+              const uint64_t hkv = ordered_bits(hf_key(P, u[j], r[j], mu, mr, n[j]));
+              const uint64_t hov = static_cast<uint64_t>(ord[j]) << 32;
+              T.ha[c] = hav;
+              T.hk[c] = hkv;
+              o0 |= hkv;
+              a0 &= hkv;
+              o1 |= hav;
+              a1 &= hav;
+              o2 |= hov;
+              a2 &= hov;
+            }
+            T.hst[c] = cand ? 1 : 0;
+            nc += cand;
+          }
         }
-        T.hst[c] = cand ? 1 : 0;
-        nc += cand;
+      } else {
+        for (int32_t c = tid; c < C; c += NT) {
+          const bool cand = cw.pos[c] < cw.end[c] && !(cw.flags[c] & kSkipped);
+          if (cand) {
+            T.ha[c] = topk_entry(a, M, cw, c, cw.pos[c]).abits;
+            T.hk[c] = ordered_bits(hf_key(P, cw.ufc[c], cw.rfc[c], mu, mr, cw.cnt[c]));
+          }
+          T.hst[c] = cand ? 1 : 0;
+          nc += cand;
+        }
       }
       nc = __reduce_add_sync(0xffffffffu, nc);
       if ((tid & 31) == 0 && nc) atomicAdd(&X.nvalid, nc);
-      __syncthreads();
+      __syncthreads();  // X.orv / andv reset before the commits
+      if constexpr (gheads) {
+        topk_or_and_commit(o0, a0, X, 0);
+        topk_or_and_commit(o1, a1, X, 1);
+        topk_or_and_commit(o2, a2, X, 2);
+        __syncthreads();
+      }
       const int32_t ncand = X.nvalid;
       if (ncand == 0) break;  // no candidates (engine.cpp:217)
 #ifdef EQX_PROF
@@ -501,7 +684,10 @@ __device__ __forceinline__ void topk_select(const SelectArgs& a, const ModelTabl
       tk_t1 = clock64();
       tk[0] += tk_t1 - t0;
 #endif
-      if (ncand > K) topk_radix_select(HeadView{T, cw, C}, K, T.hist, X);
+      if (ncand > K) {
+        if (gheads) topk_head_select(T, cw, C, K, X);
+        else topk_radix_select(HeadView{T, cw, C}, K, T.hist, X);
+      }
       all_slots = ncand <= K;
 #ifdef EQX_PROF
       tk[1] += clock64() - tk_t1;
