@@ -706,6 +706,24 @@ def run_ours(args, rank, world):
         total_ms = float(t.item())
     value = world * n * args.steps / (total_ms * 1e-3)
 
+    # ---- the practical floor of a kernel moving the same bytes: a device copy of 19 MB (19 MB read
+    # + 19 MB written = 38 B/request x 1M) after the same L2 flush, CUDA events around it ----
+    cbytes = n * ALGO_BYTES_K1 // 2
+    csrc = torch.empty(cbytes, dtype=torch.uint8, device=dev).random_(0, 255)
+    cdst = torch.empty_like(csrc)
+    copy_us = []
+    for i in range(0 if args.profile else max(5, args.steps) + 3):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        cdst.copy_(csrc)
+        e1.record()
+        torch.cuda.synchronize()
+        if i >= 3:
+            copy_us.append(e0.elapsed_time(e1) * 1e3)
+    copy_floor_us = float(np.median(copy_us)) if copy_us else float("nan")
+    del csrc, cdst
+
     # ---- e2e through the public API with pinned host buffers ----
     # Every step copies its batch H2D from pinned memory and reads its events + ledger back.
     # The batches of steps i+1 and i+2 are staged (eqx_stage_async, copy stream, three staging
@@ -799,7 +817,12 @@ def run_ours(args, rank, world):
         "admitted": res.n_admitted,
         "roofline": {"bound": "hbm", "kernel": "score_kernel (whole-queue predict/map/increments, HBM stream)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "algo_bytes_per_request": ALGO_BYTES_K1, "peak_source": peak_src},
+                     "traffic": traffic, "algo_bytes_per_request": ALGO_BYTES_K1, "peak_source": peak_src,
+                     "kernel_us_mean": k_ms * 1e3,
+                     "copy_floor": {"what": f"torch device copy of {2 * cbytes / 1e6:.0f} MB (read + write) after "
+                                            "the same L2 flush, CUDA events, median",
+                                    "us": copy_floor_us, "gbs": 2 * cbytes / (copy_floor_us * 1e-6) / 1e9,
+                                    "kernel_over_copy": k_ms * 1e3 / copy_floor_us}},
         "e2e": {"value": e2e_val, "unit": "requests/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_step_ms, "steps": e2e_steps,
                 "passes": 3,

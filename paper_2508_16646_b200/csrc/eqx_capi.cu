@@ -136,7 +136,7 @@ struct eqx_ctx {
   SelectArgs warm_se{};            // its launch arguments (prepared before a graph capture)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_k[6] = {};        // timing: score start/end, select start/end, drain start/end
-  DevBuf d_done;                   // last-CTA counters of the drain kernels
+  DevBuf d_done;                   // last-CTA counters [0..1] of the drain kernels; bytes 32..47: score_counts
   DevBuf d_win;                    // [C][W] head windows
   DevBuf d_wcnt;                   // per-(tile, warp, client) counts of the drain walk
   DevBuf d_direct;                 // direct predict/map table (see ScoreArgs::direct)
@@ -1457,17 +1457,29 @@ static eqx_status step_enqueue(eqx_ctx* ctx, const StepPlan& pl, bool with_drain
   // (nothing in the selection reads the per-request scores; the state copy joins them).
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fork, s));
   CUDA_TRY(ctx, cudaStreamWaitEvent(s2, ctx->ev_fork, 0));
+  // The selection CTA writes the host-visible DevState itself, with the scoring's counts once
+  // every scoring CTA has added them (score_counts): no copy kernel after the join.  An empty
+  // queue launches no scoring: the copy kernel remains.
+  const bool publish = ctx->n > 0;
+  ScoreArgs sc = pl.sc;
+  SelectArgs se = pl.se;
+  if (publish) {
+    sc.done = reinterpret_cast<unsigned long long*>(ctx->d_done.as<unsigned char>() + 32);
+    se.h_st = ctx->h_state_dev;
+    se.score_done = sc.done;
+    se.score_ctas = pl.score_grid;
+  }
   if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[0], s2));
   if (ctx->n > 0) {
-    if (pl.score_tma) score_tma_kernel<<<pl.score_grid, kScoreTmaThreads, pl.score_smem, s2>>>(pl.sc);
-    else score_kernel<<<pl.score_grid, kScoreThreads, pl.score_smem, s2>>>(pl.sc);
+    if (pl.score_tma) score_tma_kernel<<<pl.score_grid, kScoreTmaThreads, pl.score_smem, s2>>>(sc);
+    else score_kernel<<<pl.score_grid, kScoreThreads, pl.score_smem, s2>>>(sc);
   }
   CUDA_TRY(ctx, cudaGetLastError());
   if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[1], s2));
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_join, s2));
   if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[2], s));
   {  // PDL: the selection CTA stages its model, lifts and loads the ledger while the windows fill
-    void* args[] = {const_cast<SelectArgs*>(&pl.se)};
+    void* args[] = {&se};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(1);
     cfg.blockDim = dim3(pl.select_threads);
@@ -1486,7 +1498,7 @@ static eqx_status step_enqueue(eqx_ctx* ctx, const StepPlan& pl, bool with_drain
   // copy follows the scoring (DevState::fallbacks / near_ties) and the warm-up
   CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_join, 0));
   if (warm) CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_warm_done, 0));
-  CUDA_TRY(ctx, state_to_host(ctx, s, true));
+  if (!publish) CUDA_TRY(ctx, state_to_host(ctx, s, true));
   return EQX_OK;
 }
 

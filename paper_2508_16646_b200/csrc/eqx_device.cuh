@@ -6,6 +6,7 @@
 // bit-identical to the reference CPU path compiled without -march.
 #pragma once
 
+#include <cstddef>
 #include <cstdint>
 
 namespace eqx {
@@ -71,6 +72,11 @@ struct DevState {
   int64_t clamps;          // SchedulerPolicy::counter_clamps() (on_complete clamps at 0)
   unsigned long long tk[8];  // EQX_PROF builds: top-K selection sub-phase cycles / pass counts
 };
+
+// The host-visible copy of a step's DevState (mapped host memory) is written by the selection
+// CTA's epilogue, with no copy kernel behind the step, once the concurrently running scoring
+// kernel (fallbacks, near_ties, the t[4] / t[5] stamps) has signalled completion.
+static_assert(sizeof(DevState) % 8 == 0, "DevState is copied in 8-byte words");
 
 // Order-preserving map double -> uint64 (IEEE total order on non-NaN values, with -0.0 and
 // +0.0 made equal as operator< / operator== treat them), so tuple comparisons in the

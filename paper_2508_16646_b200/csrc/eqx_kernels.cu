@@ -787,6 +787,41 @@ __global__ void __launch_bounds__(kDrainThreads) drain_rank_kernel(const DrainAr
 
 // ===================================== scoring ===========================================
 
+// A scoring CTA's length-fallback and near-tie counts (fb, nt: warp totals in lane 0; every
+// thread of the CTA calls this).  Without a publication target they are added to DevState.
+// With one (a.done: the step's selection CTA publishes DevState, see SelectArgs::h_st), thread 0
+// adds the CTA's totals to two 64-bit words that also count the CTAs above bit 40: one relaxed
+// atomic carries the data and the completion count together, so the selection knows the totals
+// are final once both counts reach the grid size -- no fence behind the CTA's output stores.
+__device__ __forceinline__ void score_counts(const ScoreArgs& a, uint32_t fb, uint32_t nt) {
+  if (!a.done) {
+    if ((threadIdx.x & 31) == 0) {
+      if (fb) atomicAdd(&a.st->fallbacks, static_cast<unsigned long long>(fb));
+      if (nt) atomicAdd(&a.st->near_ties, static_cast<unsigned long long>(nt));
+    }
+    return;
+  }
+  __shared__ uint32_t s_fb[32], s_nt[32];
+  if ((threadIdx.x & 31) == 0) {
+    s_fb[threadIdx.x >> 5] = fb;
+    s_nt[threadIdx.x >> 5] = nt;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long f = 0, t = 0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+      f += s_fb[w];
+      t += s_nt[w];
+    }
+#ifdef EQX_PROF
+    atomicMax(&a.st->t[5], global_ns());
+    __threadfence();  // the timeline stamps before the count
+#endif
+    atomicAdd(a.done, f + kScoreCtaOne);
+    atomicAdd(a.done + 1, t + kScoreCtaOne);
+  }
+}
+
 // Whole-queue scoring: 4 requests per thread per iteration through 16-byte loads of every
 // column, predict + map_metrics through the direct table (read-only cache), FP64 increments,
 // streaming stores of pred/bucket/ufc_inc/rfc_inc.
@@ -860,10 +895,7 @@ __device__ __forceinline__ void score_body(const ScoreArgs& a, const ModelTables
   }
   fb = __reduce_add_sync(0xffffffffu, fb);
   nt = __reduce_add_sync(0xffffffffu, nt);
-  if ((threadIdx.x & 31) == 0) {
-    if (fb) atomicAdd(&a.st->fallbacks, static_cast<unsigned long long>(fb));
-    if (nt) atomicAdd(&a.st->near_ties, static_cast<unsigned long long>(nt));
-  }
+  score_counts(a, fb, nt);
 }
 
 // Live queue: increments at `now` from the frozen prediction records.
@@ -882,6 +914,7 @@ __global__ void __launch_bounds__(kScoreThreads, 4) score_kernel(const ScoreArgs
   extern __shared__ __align__(16) unsigned char smem[];
   if (a.frozen.pred) {
     score_frozen_body(a);
+    score_counts(a, 0u, 0u);
     return;
   }
   stage_model(a.model, a.model_words, smem);
@@ -1017,10 +1050,7 @@ __device__ __forceinline__ void score_tma_body(const ScoreArgs& a, const ModelTa
   }
   fb = __reduce_add_sync(0xffffffffu, fb);
   nt = __reduce_add_sync(0xffffffffu, nt);
-  if ((tid & 31) == 0) {
-    if (fb) atomicAdd(&a.st->fallbacks, static_cast<unsigned long long>(fb));
-    if (nt) atomicAdd(&a.st->near_ties, static_cast<unsigned long long>(nt));
-  }
+  score_counts(a, fb, nt);
 }
 
 __global__ void __launch_bounds__(kScoreTmaThreads, 2) score_tma_kernel(const ScoreArgs a) {
@@ -1401,6 +1431,38 @@ __global__ void __launch_bounds__(kTopkThreads, 1) select_topk_kernel(const Sele
     a.st->n_admitted = S.n_adm;
     a.st->n_rejected = S.n_rej;
     a.st->new_prefill = S.prefill;
+  }
+  if (a.h_st) {  // the step's summary straight to the mapped host copy (no copy kernel)
+    __syncthreads();
+    if (tid >= 32) return;
+    if (tid == 0) {  // the scoring runs beside the selection on a side stream and is normally long
+                     // done: its counts are final once every CTA has added (score_counts)
+      volatile unsigned long long* sig = a.score_done;
+      unsigned long long f, t;
+      while (true) {
+        f = sig[0];
+        t = sig[1];
+        if (static_cast<int64_t>(f / kScoreCtaOne) >= a.score_ctas &&
+            static_cast<int64_t>(t / kScoreCtaOne) >= a.score_ctas)
+          break;
+        __nanosleep(128);
+      }
+      sig[0] = 0ull;  // the next step's counts
+      sig[1] = 0ull;
+      a.st->fallbacks += f % kScoreCtaOne;
+      a.st->near_ties += t % kScoreCtaOne;
+    }
+    __syncwarp();
+    constexpr int kWords = static_cast<int>(sizeof(DevState) / 8), kPer = (kWords + 31) / 32;
+    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(a.st);
+    unsigned long long* dst = reinterpret_cast<unsigned long long*>(a.h_st);
+    unsigned long long v[kPer];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k)  // every load in flight before the PCIe stores
+      if (tid + 32 * k < kWords) v[k] = __ldcg(src + tid + 32 * k);
+#pragma unroll
+    for (int k = 0; k < kPer; ++k)
+      if (tid + 32 * k < kWords) dst[tid + 32 * k] = v[k];
   }
 }
 template __global__ void select_topk_kernel<false>(SelectArgs);

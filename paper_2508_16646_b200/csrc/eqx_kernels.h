@@ -18,6 +18,7 @@ constexpr int kSortMaxClients = 128;
 __host__ __device__ constexpr int sort_pad(int L) { return L + 2 * (L >> 6); }  // one word per 64 counters
 constexpr int kDrainWarps = kDrainThreads / 32;
 constexpr int kScoreThreads = 256;
+constexpr unsigned long long kScoreCtaOne = 1ull << 40;  // one CTA in score_counts' packed words
 constexpr int kScoreTmaThreads = 256;                        // score_tma_kernel block
 constexpr int kScoreTile = 1024;                             // requests per bulk-copied tile
 constexpr int kScoreStages = 3;                              // tiles in flight per CTA
@@ -94,6 +95,8 @@ struct ScoreArgs {
   double* ufc_out;
   double* rfc_out;
   DevState* st;
+  unsigned long long* done;  // [2] fallback / near-tie totals + CTA counts for the selection's
+                             // DevState publication (score_counts), or nullptr
   const ModelTables* model;
   int32_t model_words;  // uint32 words of ModelTables to stage in smem (header + used LUT)
   // Direct tables compiled on the host from the same LUT/profile (bit-identical results):
@@ -198,6 +201,9 @@ struct SelectArgs {
   int64_t* ev_id;
   int64_t ev_cap;
   DevState* st;
+  DevState* h_st;        // mapped host copy the epilogue writes the step's DevState to (or nullptr)
+  unsigned long long* score_done;  // ... with the scoring's counts from here (ScoreArgs::done)
+  int32_t score_ctas;
   const ModelTables* model;
   int32_t model_words;
   int64_t tmax;          // largest T with double(T) * m <= M (exact, host binary search)
