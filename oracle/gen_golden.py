@@ -162,17 +162,32 @@ def main() -> None:
                         pred33=H.ref_noisy_predict(33.0, 17, ids, tout),
                         pred80=H.ref_noisy_predict(80.0, 17, ids, tout))
 
-    # cfg1-shaped full replay (8 clients, Poisson-ish arrivals) through run_simulation
-    qr = W.lmsys_queue(3000, 8, seed=29)
-    qr["arrival"] = np.sort(np.random.default_rng(29).uniform(0, 25.0, 3000))
+    gen_replay_cfg1(model, prof)
+    gen_feedback(prof)
+
+
+def gen_replay_cfg1(model: dict, prof: dict) -> None:
+    """BASELINE configs[0] at its stated size through the reference's run_simulation: 8 clients,
+    Poisson arrivals at 400 req/s for 25 s (~10k requests), LengthDist::uniform(4, 1024) inputs
+    and outputs, category tags by output tercile with noise 0.2 (the shape of
+    tests/test_dropin.py::cfg1_trace), MoPE, max_sim_time_s 25."""
+    rng = np.random.default_rng(29)
+    t = np.cumsum(rng.exponential(1.0 / 400.0, 12000))
+    t = t[t < 25.0]
+    n = len(t)
+    tout = rng.integers(4, 1025, n).astype(np.int32)
+    qr = {"client": rng.integers(0, 8, n).astype(np.int32), "arrival": t,
+          "in_tokens": rng.integers(4, 1025, n).astype(np.int32), "true_out": tout,
+          "tag": W.assign_category_tags(tout, rng, 0.2).astype(np.int32),
+          "id": np.arange(n, dtype=np.int64), "client_names": [f"client{i}" for i in range(8)],
+          "tag_names": ["short", "medium", "long"]}
     case = base_case(qr, model, prof)
     ev_id, ev_kind, ev_time, u, r, c = H.ref_replay(case, max_sim_time_s=25.0)
     np.savez_compressed(os.path.join(GOLDEN, "replay_cfg1.npz"), ev_id=ev_id, ev_kind=ev_kind,
                         ev_time=ev_time, ufc=u, rfc=r, counter=c, client=qr["client"],
                         arrival=qr["arrival"], in_tokens=qr["in_tokens"], true_out=qr["true_out"],
                         tag=qr["tag"])
-    print("replay events", len(ev_id))
-    gen_feedback(prof)
+    print("replay_cfg1: requests", n, "events", len(ev_id))
 
 
 def gen_feedback(profile: dict) -> None:
@@ -206,7 +221,12 @@ def gen_feedback(profile: dict) -> None:
 
 
 if __name__ == "__main__":
-    if "--feedback" in sys.argv:  # only the feedback goldens, with the committed profile
+    if "--replay-cfg1" in sys.argv:  # only the cfg1 replay golden, with the committed model / profile
+        with open(os.path.join(DATA, "mope_builtin_c10000_s7_e3.json")) as f:
+            mdl = json.load(f)
+        with open(os.path.join(DATA, "profile_default.json")) as f:
+            gen_replay_cfg1(mdl, {k: np.asarray(v) for k, v in json.load(f).items()})
+    elif "--feedback" in sys.argv:  # only the feedback goldens, with the committed profile
         with open(os.path.join(DATA, "profile_default.json")) as f:
             gen_feedback({k: np.asarray(v) for k, v in json.load(f).items()})
     else:

@@ -309,10 +309,12 @@ def test_caller_predictions_column():
 
 
 def test_committed_cfg1_replay_golden():
-    """tests/golden/replay_cfg1.npz: a cfg1-shaped run_simulation replay (8 clients, 3000
-    Poisson-ish arrivals over 25 s, MoPE, max_sim_time_s 25) recorded from the reference build
-    by oracle/gen_golden.py -- checked without the reference present: admitted / rejected
-    sequence with its times and the final ledgers, bit-exact."""
+    """tests/golden/replay_cfg1.npz: BASELINE configs[0] at its stated size through
+    run_simulation (8 clients, Poisson arrivals at 400 req/s for 25 s = 10,218 requests,
+    uniform(4, 1024) lengths, MoPE, max_sim_time_s 25) recorded from the reference build by
+    `oracle/gen_golden.py --replay-cfg1` -- checked without the reference present: admitted /
+    rejected sequence with its times and the final ledgers, bit-exact.  400 req/s overloads the
+    64-slot batch, so the log is short (81 events) while the ledgers see every arrival."""
     import os
     from paper_2508_16646_b200 import scheduler as S
     z = np.load(os.path.join(os.path.dirname(__file__), "golden", "replay_cfg1.npz"))
@@ -325,7 +327,7 @@ def test_committed_cfg1_replay_golden():
     got = sch.replay(np.array([0, n]), z["client"], z["arrival"], z["in_tokens"], z["true_out"], [case.alpha],
                      tag=tag, ema_alpha=0.2, ev_cap=len(z["ev_id"]) + 1, max_sim_time_s=25.0)
     ne = int(got["n_events"][0])
-    assert ne == len(z["ev_id"]) > 100
+    assert n > 10000 and ne == len(z["ev_id"]) > 50
     np.testing.assert_array_equal(got["ev_id"][0, :ne], z["ev_id"])
     np.testing.assert_array_equal(got["ev_kind"][0, :ne], z["ev_kind"])
     np.testing.assert_array_equal(got["ev_time"][0, :ne], z["ev_time"])
