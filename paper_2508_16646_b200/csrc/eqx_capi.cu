@@ -1450,25 +1450,27 @@ static eqx_status step_enqueue(eqx_ctx* ctx, const StepPlan& pl, bool with_drain
   }
   // Split launches record the per-kernel timing events; the graph path (with_drain) leaves the
   // drain -> window -> selection chain bare so its programmatic (PDL) edges survive capture.
-  if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[5], s));
-  CUDA_TRY(ctx, launch_pdl(window_kernel, dim3(pl.window_grid), dim3(256), pl.window_smem, s, pl.wi));
-  // Whole-queue scoring forks off after the windows: the selection CTA (PDL) is resident by
-  // then, so the scoring grid fills the other SMs while the one-warp selection loop runs
-  // (nothing in the selection reads the per-request scores; the state copy joins them).
-  CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fork, s));
-  CUDA_TRY(ctx, cudaStreamWaitEvent(s2, ctx->ev_fork, 0));
   // The selection CTA writes the host-visible DevState itself, with the scoring's counts once
   // every scoring CTA has added them (score_counts): no copy kernel after the join.  An empty
   // queue launches no scoring: the copy kernel remains.
   const bool publish = ctx->n > 0;
   ScoreArgs sc = pl.sc;
   SelectArgs se = pl.se;
+  WindowArgs wi = pl.wi;
   if (publish) {
     sc.done = reinterpret_cast<unsigned long long*>(ctx->d_done.as<unsigned char>() + 32);
     se.h_st = ctx->h_state_dev;
     se.score_done = sc.done;
     se.score_ctas = pl.score_grid;
+    wi.score_sig = sc.done;
   }
+  if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[5], s));
+  CUDA_TRY(ctx, launch_pdl(window_kernel, dim3(pl.window_grid), dim3(256), pl.window_smem, s, wi));
+  // Whole-queue scoring forks off after the windows: the selection CTA (PDL) is resident by
+  // then, so the scoring grid fills the other SMs while the one-warp selection loop runs
+  // (nothing in the selection reads the per-request scores; the state copy joins them).
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fork, s));
+  CUDA_TRY(ctx, cudaStreamWaitEvent(s2, ctx->ev_fork, 0));
   if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[0], s2));
   if (ctx->n > 0) {
     if (pl.score_tma) score_tma_kernel<<<pl.score_grid, kScoreTmaThreads, pl.score_smem, s2>>>(sc);

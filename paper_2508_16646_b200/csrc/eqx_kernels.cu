@@ -1169,6 +1169,9 @@ __global__ void __launch_bounds__(256) window_kernel(const WindowArgs a) {
   stage_model(a.model, a.model_words, smem);  // overlaps the drain's tail (programmatic launch)
   pdl_wait();
   pdl_trigger();  // the drain is complete: the selection CTA may start its prologue
+  // this step's scoring counts start from zero: the scoring grid waits for this kernel (event)
+  // and the selection reads them after its programmatic wait on it
+  if (a.score_sig && blockIdx.x == 0 && threadIdx.x < 2) a.score_sig[threadIdx.x] = 0ull;
 #ifdef EQX_PROF
   if (threadIdx.x == 0) atomicMin(&a.st->dt[5], global_ns());
 #endif
@@ -1437,18 +1440,18 @@ __global__ void __launch_bounds__(kTopkThreads, 1) select_topk_kernel(const Sele
     if (tid >= 32) return;
     if (tid == 0) {  // the scoring runs beside the selection on a side stream and is normally long
                      // done: its counts are final once every CTA has added (score_counts)
-      volatile unsigned long long* sig = a.score_done;
+      volatile unsigned long long* sig = a.score_done;  // zeroed by this step's window kernel
       unsigned long long f, t;
+      const unsigned long long t0 = global_ns();
       while (true) {
         f = sig[0];
         t = sig[1];
         if (static_cast<int64_t>(f / kScoreCtaOne) >= a.score_ctas &&
             static_cast<int64_t>(t / kScoreCtaOne) >= a.score_ctas)
           break;
+        if (global_ns() - t0 > 2000000000ull) __trap();  // never silently hang: fail the launch
         __nanosleep(128);
       }
-      sig[0] = 0ull;  // the next step's counts
-      sig[1] = 0ull;
       a.st->fallbacks += f % kScoreCtaOne;
       a.st->near_ties += t % kScoreCtaOne;
     }

@@ -115,6 +115,7 @@ struct ScoreArgs {
 // CTAs (window_kernel) and bulk-loaded into the selection CTA's shared memory.
 struct WindowArgs {
   Frozen frozen;         // live queue: frozen prediction records (see Frozen)
+  unsigned long long* score_sig;  // [2] the step's score_counts words, zeroed by CTA 0 (or nullptr)
   const double* arrival;
   const int32_t* in_tok;
   const int32_t* true_out;
