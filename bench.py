@@ -321,8 +321,8 @@ def run_sharded(args, rank, world):
             "exchange_bytes_per_rank": rec,
             "e2e": {"value": world * n / e2e_med, "unit": "requests/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "p50_ms": e2e_med * 1e3},
-            # drain (3), score, shard_export, shard_ingest, shard_unpack, select, pack_cols (state copy)
-            "gpu_launches": 9 * args.steps,
+            # drain (3), score, shard_export, shard_ingest, shard_unpack, select (publishes the summary)
+            "gpu_launches": 8 * args.steps,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -2182,13 +2182,15 @@ eqx_status eqx_shard_select_async(eqx_ctx* ctx, const void* recs, int32_t world,
     CUDA_TRY(ctx, cudaGetLastError());
   }
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[2], s));
-  {
-    void* args[] = {const_cast<SelectArgs*>(&pl.se)};
+  {  // the local scoring joined the stream in eqx_shard_export_async: the selection publishes the
+     // summary to the mapped host copy with no wait and no copy kernel behind it
+    SelectArgs se = pl.se;
+    se.h_st = ctx->h_state_dev;
+    void* args[] = {&se};
     CUDA_TRY(ctx, cudaLaunchKernel(select_fn(pl.se.tk_heads != nullptr), dim3(1), dim3(pl.select_threads), args, pl.select_smem, s));
   }
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[3], s));
   CUDA_TRY(ctx, cudaGetLastError());
-  CUDA_TRY(ctx, state_to_host(ctx, s));
   ctx->q_id = ctx->d_gid.as<int64_t>();
   ctx->id_base = 0;
   ctx->shard_W = W;

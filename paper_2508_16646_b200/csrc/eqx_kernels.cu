@@ -1438,8 +1438,9 @@ __global__ void __launch_bounds__(kTopkThreads, 1) select_topk_kernel(const Sele
   if (a.h_st) {  // the step's summary straight to the mapped host copy (no copy kernel)
     __syncthreads();
     if (tid >= 32) return;
-    if (tid == 0) {  // the scoring runs beside the selection on a side stream and is normally long
-                     // done: its counts are final once every CTA has added (score_counts)
+    if (tid == 0 && a.score_done) {  // the scoring runs beside the selection on a side stream and is
+                                     // normally long done: its counts are final once every CTA has
+                                     // added (score_counts); without score_done it finished earlier
       volatile unsigned long long* sig = a.score_done;  // zeroed by this step's window kernel
       unsigned long long f, t;
       const unsigned long long t0 = global_ns();
