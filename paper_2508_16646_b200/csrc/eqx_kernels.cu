@@ -1450,7 +1450,7 @@ __global__ void __launch_bounds__(kTopkThreads, 1) select_topk_kernel(const Sele
         if (static_cast<int64_t>(f / kScoreCtaOne) >= a.score_ctas &&
             static_cast<int64_t>(t / kScoreCtaOne) >= a.score_ctas)
           break;
-        if (global_ns() - t0 > 2000000000ull) __trap();  // never silently hang: fail the launch
+        if (global_ns() - t0 > 10000000000ull) __trap();  // never silently hang: fail the launch
         __nanosleep(128);
       }
       a.st->fallbacks += f % kScoreCtaOne;
