@@ -119,12 +119,32 @@ typedef struct {
   const int32_t* true_output_tokens; /* ORACLE / NOISY_ORACLE only; may be NULL otherwise */
   const uint8_t* tag;             /* category_tag as a tag id (see eqx_mope.tag_row) */
   int32_t location;               /* EQX_HOST / EQX_DEVICE */
-  int32_t narrow;                 /* ABI 3, EQX_HOST batches of eqx_stage_async / eqx_drain only: 1 =
-                                     client and input_tokens point to uint16_t arrays (rosters up
-                                     to 65536 clients, inputs below 65536 tokens -- the caller's
-                                     lossless choice): 13 instead of 17 bytes per request cross
-                                     PCIe; the copy stream widens them on the device */
+  int32_t narrow;                 /* ABI 3, EQX_HOST batches of eqx_stage_async / eqx_drain only, bit
+                                     flags (0 = every column as typed above):
+                                     EQX_NARROW_U16: client and input_tokens point to uint16_t
+                                     arrays (rosters up to 65536 clients, inputs below 65536
+                                     tokens -- the caller's lossless choice);
+                                     EQX_PACKED_ARRIVALS: arrival_s points to the output of
+                                     eqx_pack_arrivals for these n rows (about 6 instead of 8
+                                     bytes per request, lossless).
+                                     Both: 11 instead of 17 bytes per request cross PCIe; the
+                                     copy stream widens / unpacks them on the device */
 } eqx_requests;
+
+#define EQX_NARROW_U16 1
+#define EQX_PACKED_ARRIVALS 2
+
+/* Lossless packing of an arrival_s column for eqx_requests::narrow & EQX_PACKED_ARRIVALS.
+ * Layout: the packed size in bytes (u64), then per block of 256 rows a base (u64) and the byte
+ * offset of the block's data (u64), then the blocks' data, 16-byte aligned.  A block whose rows
+ * are non-negative and non-decreasing with bit patterns within 2^48 of its first row's (about 2 s
+ * of arrivals at 40 s: non-negative doubles order like their bit patterns) stores that pattern
+ * as the base and each row's offset from it in 6 bytes (little endian).  Any other block (near
+ * zero, or a wide span) stores its doubles (base = all ones).
+ * out == NULL: returns the packed size of this column.  Otherwise writes it and returns the
+ * size, -1 for bad arguments, -2 when cap is smaller than the packed size.  Host-only; no
+ * context needed. */
+int64_t eqx_pack_arrivals(const double* arrival_s, int64_t n, void* out, int64_t cap);
 
 typedef struct {
   int64_t n_events;          /* admitted + rejected, in log order */

@@ -162,7 +162,9 @@ _SIGS = {
     "eqx_copy_scores": ([C.c_void_p, C.c_int64, _i32p, _u8p, _dp, _dp], C.c_int),
     "eqx_ufc_increment": ([C.c_double, C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_double, C.c_double], C.c_double),
     "eqx_rfc_increment": ([C.c_double, C.c_double, C.c_double], C.c_double),
+    "eqx_pack_arrivals": ([C.c_void_p, C.c_int64, C.c_void_p, C.c_int64], C.c_int64),
 }
+EQX_NARROW_U16, EQX_PACKED_ARRIVALS = 1, 2
 
 EXPORTED = sorted(_SIGS)
 

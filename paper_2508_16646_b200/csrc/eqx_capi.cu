@@ -96,7 +96,7 @@ struct eqx_ctx {
   // step.  `free_` is recorded on the main stream after the last launch that reads a set.
   static constexpr int kStages = 3;
   struct Stage {
-    DevBuf client, arrival, in, tru, tag, id, c16, i16;
+    DevBuf client, arrival, in, tru, tag, id, c16, i16, apk;  // apk: packed arrivals
     const void* key[6] = {};
     int32_t narrow = 0;
     int64_t n = -1;
@@ -801,17 +801,32 @@ static eqx_status stage_fill(eqx_ctx* ctx, const eqx_requests* r, int b) {
   CUDA_TRY(ctx, st.tag.ensure(nn + 16));
   if (r->true_output_tokens) CUDA_TRY(ctx, st.tru.ensure(4 * nn));
   if (r->id) CUDA_TRY(ctx, st.id.ensure(8 * nn));
-  if (r->narrow) {
+  const bool n16 = (r->narrow & EQX_NARROW_U16) != 0, packed = (r->narrow & EQX_PACKED_ARRIVALS) != 0;
+  if (n16) {
     CUDA_TRY(ctx, st.c16.ensure(2 * nn + 16));
     CUDA_TRY(ctx, st.i16.ensure(2 * nn + 16));
   }
+  int64_t pk_bytes = 0;  // the packed column's size is its first word
+  if (packed && n > 0) std::memcpy(&pk_bytes, r->arrival_s, 8);
+  if (packed && n > 0 && (pk_bytes < 16 + 16 * ((n + 255) / 256) + 6 * n ||
+                          pk_bytes > 16 + 32 * ((n + 255) / 256) + 8 * n))
+    return fail(ctx, EQX_ERR_ARG, "packed arrivals: not an eqx_pack_arrivals column of n rows");
+  if (packed) CUDA_TRY(ctx, st.apk.ensure(static_cast<size_t>(pk_bytes) + 16));
   CUDA_TRY(ctx, cudaStreamWaitEvent(cs, st.free_, 0));
   auto h2d = [&](void* dst, const void* src, size_t bytes) {
     return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, cs);
   };
-  if (n > 0 && r->narrow) {  // 2-byte client / input columns over PCIe, widened on the device
+  auto arrivals = [&]() -> cudaError_t {  // 8-byte doubles, or the packed form unpacked on the device
+    if (!packed) return h2d(st.arrival.p, r->arrival_s, 8 * n);
+    cudaError_t e = h2d(st.apk.p, r->arrival_s, static_cast<size_t>(pk_bytes));
+    if (e != cudaSuccess) return e;
+    const int blocks = static_cast<int>(std::min<int64_t>((n / 8 + 255) / 256 + 1, 4ll * ctx->sm_count));
+    unpack_arrivals_kernel<<<blocks, 256, 0, cs>>>(st.apk.as<unsigned char>(), n, st.arrival.as<double>());
+    return cudaGetLastError();
+  };
+  if (n > 0 && n16) {  // 2-byte client / input columns over PCIe, widened on the device
     CUDA_TRY(ctx, h2d(st.c16.p, r->client, 2 * n));
-    CUDA_TRY(ctx, h2d(st.arrival.p, r->arrival_s, 8 * n));
+    CUDA_TRY(ctx, arrivals());
     CUDA_TRY(ctx, h2d(st.i16.p, r->input_tokens, 2 * n));
     const int blocks = static_cast<int>(std::min<int64_t>((n / 8 + 255) / 256 + 1, 4ll * ctx->sm_count));
     widen_cols_kernel<<<blocks, 256, 0, cs>>>(st.c16.as<uint16_t>(), st.i16.as<uint16_t>(), n, st.client.as<int32_t>(),
@@ -819,7 +834,7 @@ static eqx_status stage_fill(eqx_ctx* ctx, const eqx_requests* r, int b) {
     CUDA_TRY(ctx, cudaGetLastError());
   } else if (n > 0) {
     CUDA_TRY(ctx, h2d(st.client.p, r->client, 4 * n));
-    CUDA_TRY(ctx, h2d(st.arrival.p, r->arrival_s, 8 * n));
+    CUDA_TRY(ctx, arrivals());
     CUDA_TRY(ctx, h2d(st.in.p, r->input_tokens, 4 * n));
   }
   if (n > 0) {
@@ -859,6 +874,58 @@ static bool stage_matches(const eqx_ctx::Stage& st, const eqx_requests* r) {
   return st.valid && st.n == r->n && st.narrow == r->narrow && std::memcmp(st.key, key, sizeof(key)) == 0;
 }
 
+// Layout (see include/eqx.h): [u64 total bytes][u64 base[nb]][u64 off[nb]] then per block,
+// 16-byte aligned at off[b]: 6-byte offsets (packed) or the raw doubles (base[b] == ~0).
+int64_t eqx_pack_arrivals(const double* a, int64_t n, void* out, int64_t cap) {
+  if (n < 0 || (n > 0 && !a)) return -1;
+  const int64_t nb = (n + 255) / 256;
+  auto packable = [&](int64_t r0, int64_t r1, uint64_t* base) {
+    uint64_t b0, prev;
+    std::memcpy(&b0, a + r0, 8);
+    prev = b0;
+    for (int64_t r = r0; r < r1; ++r) {
+      uint64_t v;
+      std::memcpy(&v, a + r, 8);
+      // non-negative (sign clear), not NaN, non-decreasing bit patterns, 48-bit span
+      if ((v >> 63) || v > 0x7ff0000000000000ull || v < prev || v - b0 >= (uint64_t(1) << 48)) return false;
+      prev = v;
+    }
+    *base = b0;
+    return true;
+  };
+  int64_t cur = (8 + 16 * nb + 15) & ~int64_t(15), total = cur;
+  for (int64_t b = 0; b < nb; ++b) {  // size pass
+    const int64_t r0 = 256 * b, r1 = std::min<int64_t>(n, r0 + 256);
+    uint64_t base;
+    total += ((packable(r0, r1, &base) ? 6 : 8) * (r1 - r0) + 15) & ~int64_t(15);
+  }
+  if (!out) return total;
+  if (cap < total) return -2;
+  unsigned char* o = static_cast<unsigned char*>(out);
+  std::memset(o, 0, static_cast<size_t>(total));
+  std::memcpy(o, &total, 8);
+  for (int64_t b = 0; b < nb; ++b) {
+    const int64_t r0 = 256 * b, r1 = std::min<int64_t>(n, r0 + 256);
+    uint64_t base = ~0ull;
+    const bool pk = packable(r0, r1, &base);
+    if (!pk) base = ~0ull;
+    std::memcpy(o + 8 + 8 * b, &base, 8);
+    std::memcpy(o + 8 + 8 * nb + 8 * b, &cur, 8);
+    for (int64_t r = r0; r < r1; ++r) {
+      uint64_t v;
+      std::memcpy(&v, a + r, 8);
+      if (pk) {
+        const uint64_t d = v - base;
+        std::memcpy(o + cur + 6 * (r - r0), &d, 6);  // little endian: the low 6 bytes
+      } else {
+        std::memcpy(o + cur + 8 * (r - r0), &v, 8);
+      }
+    }
+    cur += ((pk ? 6 : 8) * (r1 - r0) + 15) & ~int64_t(15);
+  }
+  return total;
+}
+
 // The main stream is done with the bound staging set once everything enqueued so far ran.
 static eqx_status release_stage(eqx_ctx* ctx) {
   if (ctx->bound_stage >= 0) CUDA_TRY(ctx, cudaEventRecord(ctx->stg[ctx->bound_stage].free_, ctx->stream));
@@ -868,7 +935,10 @@ static eqx_status release_stage(eqx_ctx* ctx) {
 eqx_status eqx_stage_async(eqx_ctx* ctx, const eqx_requests* r) {
   if (!ctx || !r) return fail(ctx, EQX_ERR_ARG, "eqx_stage_async: NULL argument");
   if (r->location != EQX_HOST) return fail(ctx, EQX_ERR_ARG, "eqx_stage_async: only host batches are staged");
-  if (r->narrow && (reinterpret_cast<uintptr_t>(r->client) & 1 || reinterpret_cast<uintptr_t>(r->input_tokens) & 1))
+  if (r->narrow & ~(EQX_NARROW_U16 | EQX_PACKED_ARRIVALS))
+    return fail(ctx, EQX_ERR_ARG, "eqx_stage_async: unknown narrow flags");
+  if ((r->narrow & EQX_NARROW_U16) &&
+      (reinterpret_cast<uintptr_t>(r->client) & 1 || reinterpret_cast<uintptr_t>(r->input_tokens) & 1))
     return fail(ctx, EQX_ERR_ARG, "eqx_stage_async: narrow columns must be 2-byte aligned");
   if (r->n < 0 || r->n >= (int64_t(1) << 31) - 1) return fail(ctx, EQX_ERR_ARG, "eqx_stage_async: n out of range");
   if (r->n > 0 && (!r->client || !r->arrival_s || !r->input_tokens))
@@ -889,7 +959,11 @@ static eqx_status drain_prepare(eqx_ctx* ctx, const eqx_requests* r) {
   if (n > 0 && (!r->client || !r->arrival_s || !r->input_tokens || (needs_true && !r->true_output_tokens)))
     return fail(ctx, EQX_ERR_ARG, "eqx_drain: missing request column");
   if (r->narrow && r->location == EQX_DEVICE)
-    return fail(ctx, EQX_ERR_ARG, "eqx_drain: narrow (uint16) columns are for host batches only");
+    return fail(ctx, EQX_ERR_ARG, "eqx_drain: narrow (uint16 / packed) columns are for host batches only");
+  if (r->narrow & ~(EQX_NARROW_U16 | EQX_PACKED_ARRIVALS)) return fail(ctx, EQX_ERR_ARG, "eqx_drain: unknown narrow flags");
+  if ((r->narrow & EQX_NARROW_U16) &&
+      (reinterpret_cast<uintptr_t>(r->client) & 1 || reinterpret_cast<uintptr_t>(r->input_tokens) & 1))
+    return fail(ctx, EQX_ERR_ARG, "eqx_drain: narrow columns must be 2-byte aligned");
   cudaSetDevice(ctx->device);
   cudaStream_t s = ctx->stream;
   const size_t nn = static_cast<size_t>(std::max<int64_t>(n, 1));

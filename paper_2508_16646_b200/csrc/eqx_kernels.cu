@@ -1498,6 +1498,54 @@ __global__ void widen_cols_kernel(const uint16_t* c16, const uint16_t* i16, int6
   }
 }
 
+// Packed arrivals (eqx_pack_arrivals) -> doubles.  Per 256-row block: a base bit pattern and
+// the byte offset of the block's data, either 6-byte offsets from the base (packed) or the raw
+// doubles (base == ~0: blocks spanning more than 48 bits of the bit pattern, e.g. near zero).
+// 8 rows per thread (48 or 64 bytes, 16-byte loads).
+__device__ __forceinline__ double unpack_row(const unsigned char* pk, unsigned long long base, int64_t off, int i) {
+  if (base == ~0ull) return reinterpret_cast<const double*>(pk + off)[i];
+  unsigned long long d = 0;
+  for (int j = 5; j >= 0; --j) d = (d << 8) | pk[off + 6 * i + j];
+  return __longlong_as_double(static_cast<long long>(base + d));
+}
+__global__ void unpack_arrivals_kernel(const unsigned char* pk, int64_t n, double* out) {
+  const int64_t nb = (n + 255) / 256;
+  const unsigned long long* base = reinterpret_cast<const unsigned long long*>(pk + 8);
+  const long long* off = reinterpret_cast<const long long*>(pk + 8 + 8 * nb);
+  constexpr unsigned long long kM48 = (1ull << 48) - 1;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t groups = n / 8;
+  for (int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < groups; g += stride) {
+    const int64_t blk = (8 * g) >> 8, i0 = (8 * g) & 255;  // 8 rows never straddle a block
+    const unsigned long long b = base[blk];
+    const long long o0 = off[blk];
+    double2* o = reinterpret_cast<double2*>(out + 8 * g);
+    if (b == ~0ull) {
+      const double2* p = reinterpret_cast<const double2*>(pk + o0 + 8 * i0);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) o[k] = p[k];
+      continue;
+    }
+    const ulonglong2* p = reinterpret_cast<const ulonglong2*>(pk + o0 + 6 * i0);
+    const ulonglong2 x0 = p[0], x1 = p[1], x2 = p[2];
+    const unsigned long long w[6] = {x0.x, x0.y, x1.x, x1.y, x2.x, x2.y};
+    const unsigned long long d[8] = {w[0] & kM48,
+                                     ((w[0] >> 48) | (w[1] << 16)) & kM48,
+                                     ((w[1] >> 32) | (w[2] << 32)) & kM48,
+                                     w[2] >> 16,
+                                     w[3] & kM48,
+                                     ((w[3] >> 48) | (w[4] << 16)) & kM48,
+                                     ((w[4] >> 32) | (w[5] << 32)) & kM48,
+                                     w[5] >> 16};
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      o[k] = make_double2(__longlong_as_double(static_cast<long long>(b + d[2 * k])),
+                          __longlong_as_double(static_cast<long long>(b + d[2 * k + 1])));
+  }
+  for (int64_t r = 8 * groups + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < n; r += stride)
+    out[r] = unpack_row(pk, base[r >> 8], off[r >> 8], static_cast<int>(r & 255));
+}
+
 // Columns -> mapped host memory by SM stores over PCIe (16-byte words when aligned).
 __global__ void pack_cols_kernel(const PackCols p) {
   pdl_wait();  // no-op unless launched programmatically after the kernel producing the columns

@@ -207,7 +207,38 @@ def pinned_empty(shape, dtype) -> np.ndarray:
     return np.frombuffer(buf, dtype=dt, count=count).reshape(shape)
 
 
-def pinned_copy(x) -> np.ndarray:
+class PackedArrivals:
+    """An arrival_s column packed by eqx_pack_arrivals (include/eqx.h): pass it as `arrival_s` of
+    a host batch (drain / stage_async / drain_step_async) and about 6 instead of 8 bytes per
+    request cross PCIe; the copy stream unpacks it on the device, bit-exact."""
+
+    def __init__(self, data: np.ndarray, n: int):
+        self.data = data  # uint8
+        self.n = int(n)
+
+    def __len__(self) -> int:
+        return self.n
+
+
+def pack_arrivals(arrival_s) -> PackedArrivals:
+    """Lossless packing of an arrival column (pageable memory; pinned_copy() pins it): 256-row
+    blocks of non-decreasing non-negative arrivals within 2^48 ulps of their first take 6 bytes
+    per row, other blocks their 8-byte doubles (include/eqx.h: eqx_pack_arrivals)."""
+    a = np.ascontiguousarray(arrival_s, dtype=np.float64)
+    lib = L.load()
+    ptr = a.ctypes.data if len(a) else None
+    nbytes = int(lib.eqx_pack_arrivals(ptr, len(a), None, 0))
+    if nbytes < 0:
+        raise ValueError("eqx_pack_arrivals: bad arguments")
+    out = np.empty(max(nbytes, 16), np.uint8)
+    if int(lib.eqx_pack_arrivals(ptr, len(a), out.ctypes.data, out.nbytes)) != nbytes:
+        raise RuntimeError("eqx_pack_arrivals: packing failed")
+    return PackedArrivals(out, len(a))
+
+
+def pinned_copy(x):
+    if isinstance(x, PackedArrivals):
+        return PackedArrivals(pinned_copy(x.data), x.n)
     a = np.ascontiguousarray(x)
     out = pinned_empty(a.shape, a.dtype)
     out[...] = a
@@ -467,9 +498,18 @@ class GpuScheduler:
         narrow = (isinstance(client, np.ndarray) and client.dtype == np.uint16 and
                   isinstance(input_tokens, np.ndarray) and input_tokens.dtype == np.uint16)
         wide = np.uint16 if narrow else np.int32
-        for name, x, dt in (("client", client, wide), ("arrival_s", arrival_s, np.float64),
+        packed = isinstance(arrival_s, PackedArrivals)
+        if packed:
+            if arrival_s.n != len(client):
+                raise ValueError("packed arrivals: row count differs from the client column")
+            keep.append(arrival_s.data)
+            cols["arrival_s"] = arrival_s.data.ctypes.data
+            loc.add(L.EQX_HOST)
+        for name, x, dt in (("client", client, wide), ("arrival_s", None if packed else arrival_s, np.float64),
                             ("input_tokens", input_tokens, wide), ("tag", tag, np.uint8),
                             ("true_output_tokens", true_output_tokens, np.int32), ("id", ids, np.int64)):
+            if name == "arrival_s" and packed:
+                continue
             ptr, where = _as_col(x, dt, keep)
             cols[name] = ptr
             if where is not None:
@@ -478,7 +518,8 @@ class GpuScheduler:
             raise ValueError("drain: mix of host and device columns")
         n = len(client)
         rq = L.Requests(n, cols["id"], id_base, cols["client"], cols["arrival_s"], cols["input_tokens"],
-                        cols["true_output_tokens"], cols["tag"], loc.pop() if loc else L.EQX_HOST, 1 if narrow else 0)
+                        cols["true_output_tokens"], cols["tag"], loc.pop() if loc else L.EQX_HOST,
+                        (L.EQX_NARROW_U16 if narrow else 0) | (L.EQX_PACKED_ARRIVALS if packed else 0))
         if not staging:
             self._keep = keep  # device columns are used in place: keep them alive with the queue
             self.n_queued = n

@@ -176,6 +176,46 @@ def test_narrow_host_columns_staged_and_unstaged():
             compare_step(res, sch, want)
 
 
+@pytest.mark.parametrize("narrow", [False, True])
+def test_packed_arrival_host_columns(narrow):
+    """Packed arrivals (eqx_pack_arrivals, eqx_requests::narrow & EQX_PACKED_ARRIVALS: ~6 B per
+    request over PCIe, unpacked on the copy stream) give the same step as the doubles, with and
+    without the uint16 columns, unstaged, staged and through the graph path.  The random queues
+    start near zero, so their first blocks are stored raw and the rest packed; one case shifts
+    the arrivals far from zero (every block packed), one draws them sparse (every block raw)."""
+    from helpers import case_batch, case_clients, case_kwargs
+    from paper_2508_16646_b200 import scheduler as S
+    for seed, C, shift, sparse in ((61, 64, 0.0, False), (62, 1000, 1000.0, False), (63, 5, 0.0, True)):
+        case = _random_case(seed, 30011, C)
+        if sparse:
+            case.arrival = np.sort(np.random.default_rng(seed).uniform(0.0, 1e6, len(case.arrival)))
+        case.arrival = case.arrival + shift
+        want = H.run_step(case, "oracle")
+        cols = case_columns(case)
+        if narrow:
+            cols["client"] = cols["client"].astype(np.uint16)
+            cols["input_tokens"] = cols["input_tokens"].astype(np.uint16)
+        cols["arrival_s"] = S.pack_arrivals(cols["arrival_s"])
+        pinned = {k: S.pinned_copy(v) for k, v in cols.items()}
+        for mode in ("plain", "staged", "graph"):
+            sch = S.GpuScheduler(case_clients(case), running=case.running, **case_kwargs(case))
+            sch.set_batch(*case_batch(case))
+            src = cols if mode == "plain" else pinned
+            if mode == "staged":
+                sch.stage_async(**src)
+            if mode == "graph":
+                sch.checkpoint()
+                for _ in range(2):
+                    sch.restore_async()
+                    sch.stage_async(**src)
+                    sch.drain_step_async(case.now, **src)
+                    res = sch.collect(with_events=True)
+            else:
+                sch.drain(**src)
+                res = sch.step(case.now)
+            compare_step(res, sch, want)
+
+
 def _graph_step(case, device_columns: bool, staged: bool = False, reps: int = 2):
     """The path bench.py times: eqx_drain_step_async (one CUDA-graph replay of drain, windows
     with the counter lift, scoring and selection), repeated on the restored ledger so the cached
