@@ -302,8 +302,9 @@ struct PackCols {
   int32_t n;
 };
 __global__ void pack_cols_kernel(PackCols p);
-// u16 host columns (eqx_requests::narrow) -> the i32 client / input_tokens columns, on the copy stream
+// packed arrivals (eqx_pack_arrivals) -> the f64 arrival column, on the copy stream
 __global__ void unpack_arrivals_kernel(const unsigned char* pk, int64_t n, double* out);
+// u16 host columns (eqx_requests::narrow) -> the i32 client / input_tokens columns, on the copy stream
 __global__ void widen_cols_kernel(const uint16_t* c16, const uint16_t* i16, int64_t n, int32_t* c32, int32_t* i32);
 
 // ---- live queues: append arrivals to the remaining queue ------------
