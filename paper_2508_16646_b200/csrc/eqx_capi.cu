@@ -102,11 +102,12 @@ struct eqx_ctx {
     int64_t n = -1;
     uint64_t seq = 0;  // staging order: a drain consumes the oldest matching staged batch
     bool valid = false;
-    cudaEvent_t ready = nullptr, free_ = nullptr;
+    cudaEvent_t ready = nullptr, free_ = nullptr, copied = nullptr;
   } stg[kStages];
   int bound_stage = -1;
   uint64_t stage_seq = 0;
   cudaStream_t copy_stream = nullptr;
+  cudaStream_t unpack_stream = nullptr;  // widen / unpack kernels of staged batches (the copy stream moves on)
   DevBuf d_perm, d_hist, d_tbase, d_ctot, d_tsorted, d_tfirst;
   bool sort_drain = false;         // small rosters: drain_sort + drain_scan + drain_scatter
   size_t sort_smem = 0;
@@ -434,9 +435,11 @@ eqx_status eqx_ctx_create(int32_t device, eqx_ctx** out) {
   e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->unpack_stream, cudaStreamNonBlocking);
   for (int b = 0; b < eqx_ctx::kStages && e == cudaSuccess; ++b) {
     e = cudaEventCreateWithFlags(&ctx->stg[b].ready, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->stg[b].free_, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->stg[b].copied, cudaEventDisableTiming);
   }
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming);
@@ -501,11 +504,16 @@ void eqx_ctx_destroy(eqx_ctx* ctx) {
     cudaStreamSynchronize(ctx->copy_stream);
     cudaStreamDestroy(ctx->copy_stream);
   }
+  if (ctx->unpack_stream) {
+    cudaStreamSynchronize(ctx->unpack_stream);
+    cudaStreamDestroy(ctx->unpack_stream);
+  }
   for (auto& st : ctx->stg) {
     DevBuf* sb[] = {&st.client, &st.arrival, &st.in, &st.tru, &st.tag, &st.id};
     for (DevBuf* b : sb) b->release();
     if (st.ready) cudaEventDestroy(st.ready);
     if (st.free_) cudaEventDestroy(st.free_);
+    if (st.copied) cudaEventDestroy(st.copied);
   }
   for (auto& g : ctx->graphs)
     if (g) cudaGraphExecDestroy(g);
@@ -829,34 +837,32 @@ static eqx_status stage_fill(eqx_ctx* ctx, const eqx_requests* r, int b) {
   auto h2d = [&](void* dst, const void* src, size_t bytes) {
     return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, cs);
   };
-  auto arrivals = [&]() -> cudaError_t {  // 8-byte doubles, or the packed form unpacked on the device
-    if (!packed) return h2d(st.arrival.p, r->arrival_s, 8 * n);
-    cudaError_t e = h2d(st.apk.p, r->arrival_s, static_cast<size_t>(pk_bytes));
-    if (e != cudaSuccess) return e;
-    const int blocks = static_cast<int>(std::min<int64_t>((n / 8 + 255) / 256 + 1, 4ll * ctx->sm_count));
-    unpack_arrivals_kernel<<<blocks, 256, 0, cs>>>(st.apk.as<unsigned char>(), n, st.arrival.as<double>());
-    return cudaGetLastError();
-  };
-  if (n > 0 && n16) {  // 2-byte client / input columns over PCIe, widened on the device
-    CUDA_TRY(ctx, h2d(st.c16.p, r->client, 2 * n));
-    CUDA_TRY(ctx, arrivals());
-    CUDA_TRY(ctx, h2d(st.i16.p, r->input_tokens, 2 * n));
-    const int blocks = static_cast<int>(std::min<int64_t>((n / 8 + 255) / 256 + 1, 4ll * ctx->sm_count));
-    widen_cols_kernel<<<blocks, 256, 0, cs>>>(st.c16.as<uint16_t>(), st.i16.as<uint16_t>(), n, st.client.as<int32_t>(),
-                                              st.in.as<int32_t>());
-    CUDA_TRY(ctx, cudaGetLastError());
-  } else if (n > 0) {
-    CUDA_TRY(ctx, h2d(st.client.p, r->client, 4 * n));
-    CUDA_TRY(ctx, arrivals());
-    CUDA_TRY(ctx, h2d(st.in.p, r->input_tokens, 4 * n));
-  }
+  // every H2D first on the copy stream; the widen / unpack kernels run on their own stream behind
+  // an event, so the copy engine moves straight on to the next batch
   if (n > 0) {
+    CUDA_TRY(ctx, n16 ? h2d(st.c16.p, r->client, 2 * n) : h2d(st.client.p, r->client, 4 * n));
+    CUDA_TRY(ctx, packed ? h2d(st.apk.p, r->arrival_s, static_cast<size_t>(pk_bytes))
+                         : h2d(st.arrival.p, r->arrival_s, 8 * n));
+    CUDA_TRY(ctx, n16 ? h2d(st.i16.p, r->input_tokens, 2 * n) : h2d(st.in.p, r->input_tokens, 4 * n));
     if (r->tag) CUDA_TRY(ctx, h2d(st.tag.p, r->tag, n));
     else CUDA_TRY(ctx, cudaMemsetAsync(st.tag.p, 0, n, cs));
     if (r->true_output_tokens) CUDA_TRY(ctx, h2d(st.tru.p, r->true_output_tokens, 4 * n));
     if (r->id) CUDA_TRY(ctx, h2d(st.id.p, r->id, 8 * n));
   }
-  CUDA_TRY(ctx, cudaEventRecord(st.ready, cs));
+  if (n > 0 && (n16 || packed)) {
+    cudaStream_t us = ctx->unpack_stream;
+    CUDA_TRY(ctx, cudaEventRecord(st.copied, cs));
+    CUDA_TRY(ctx, cudaStreamWaitEvent(us, st.copied, 0));
+    const int blocks = static_cast<int>(std::min<int64_t>((n / 8 + 255) / 256 + 1, 4ll * ctx->sm_count));
+    if (packed) unpack_arrivals_kernel<<<blocks, 256, 0, us>>>(st.apk.as<unsigned char>(), n, st.arrival.as<double>());
+    if (n16)
+      widen_cols_kernel<<<blocks, 256, 0, us>>>(st.c16.as<uint16_t>(), st.i16.as<uint16_t>(), n,
+                                                st.client.as<int32_t>(), st.in.as<int32_t>());
+    CUDA_TRY(ctx, cudaGetLastError());
+    CUDA_TRY(ctx, cudaEventRecord(st.ready, us));
+  } else {
+    CUDA_TRY(ctx, cudaEventRecord(st.ready, cs));
+  }
   const void* key[6] = {r->client, r->arrival_s, r->input_tokens, r->tag, r->true_output_tokens, r->id};
   std::memcpy(st.key, key, sizeof(key));
   st.narrow = r->narrow;
