@@ -755,7 +755,7 @@ def run_ours(args, rank, world):
             sch.restore_async()
             sch.drain_step_async(1.0, **hosts[i % 3])  # staged batch -> one graph launch
             r = sch.collect(with_events=True)
-            led_out = sch.ledger()
+            led_out = sch.step_ledger()  # written over PCIe by the step's selection CTA
             adm.append(r.n_admitted)
             d2h = r.ids.nbytes + r.kinds.nbytes + r.clients.nbytes + r.preds.nbytes + 4 * r.ufc_inc.nbytes + \
                 sum(v.nbytes for v in led_out.values()) + 80

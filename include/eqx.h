@@ -188,6 +188,13 @@ eqx_status eqx_set_clients(eqx_ctx* ctx, int32_t n, const char* names, const dou
                            const int32_t* running);
 eqx_status eqx_get_clients(eqx_ctx* ctx, int32_t n, double* ufc, double* rfc, double* counter,
                            int32_t* backlogged, int32_t* running);
+/* The ledger as the last collected step left it, read from mapped host memory the step's
+ * selection CTA wrote it to (no device copy, no synchronisation): same arrays as
+ * eqx_get_clients.  Valid after eqx_step_collect of a step on a non-empty queue until the next
+ * call that changes the ledger on the device (drain, restore, set_clients, append, feedback,
+ * sharded steps, replays); EQX_ERR_CONFIG otherwise. */
+eqx_status eqx_step_ledger(eqx_ctx* ctx, int32_t n, double* ufc, double* rfc, double* counter,
+                           int32_t* backlogged, int32_t* running);
 /* Existing batch: BatchState::members.size() and reserved_kv_tokens() (gpu_model.cpp:40-46). */
 eqx_status eqx_set_batch(eqx_ctx* ctx, int32_t members, int64_t reserved_kv_tokens);
 

@@ -146,6 +146,7 @@ _SIGS = {
     "eqx_set_predictor": ([C.c_void_p, C.POINTER(Predictor)], C.c_int),
     "eqx_set_clients": ([C.c_void_p, C.c_int32, C.c_char_p, _dp, _dp, _dp, _dp, _i32p], C.c_int),
     "eqx_get_clients": ([C.c_void_p, C.c_int32, _dp, _dp, _dp, _i32p, _i32p], C.c_int),
+    "eqx_step_ledger": ([C.c_void_p, C.c_int32, _dp, _dp, _dp, _i32p, _i32p], C.c_int),
     "eqx_set_batch": ([C.c_void_p, C.c_int32, C.c_int64], C.c_int),
     "eqx_ledger_checkpoint": ([C.c_void_p], C.c_int),
     "eqx_ledger_restore_async": ([C.c_void_p], C.c_int),

@@ -155,6 +155,11 @@ struct eqx_ctx {
   void* h_scratch_dev = nullptr;   // its device alias
   size_t h_scratch_bytes = 0;
   DevState* h_state_dev = nullptr; // device alias of the mapped h_state
+  unsigned char* h_ledger = nullptr;      // mapped host copy of a step's ledger (eqx_step_ledger)
+  unsigned char* h_ledger_dev = nullptr;  // its device alias
+  size_t h_ledger_cap = 0;
+  uint64_t ledger_epoch = 0;              // bumped by every call that changes the device ledger
+  uint64_t ledger_pub_epoch = ~0ull;      // the epoch whose ledger h_ledger holds
   // launch-attribute caches (cudaFuncSetAttribute / occupancy queries cost host time per step)
   int smem_attr[13] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};  // drain_hist, drain_rank, select kernels (select_fn)
   size_t occ_smem = SIZE_MAX;
@@ -483,6 +488,7 @@ void eqx_ctx_destroy(eqx_ctx* ctx) {
                     &ctx->snap_counter, &ctx->snap_running, &ctx->snap_backlogged, &ctx->snap_state};
   for (DevBuf* b : bufs) b->release();
   if (ctx->h_state) cudaFreeHost(ctx->h_state);
+  if (ctx->h_ledger) cudaFreeHost(ctx->h_ledger);
   if (ctx->h_scratch) cudaFreeHost(ctx->h_scratch);
   if (ctx->stream2) cudaStreamSynchronize(ctx->stream2);
   ctx->d_done.release();
@@ -681,6 +687,7 @@ eqx_status eqx_set_predictor(eqx_ctx* ctx, const eqx_predictor* p) {
 eqx_status eqx_set_clients(eqx_ctx* ctx, int32_t n, const char* names, const double* weight,
                            const double* ufc, const double* rfc, const double* counter,
                            const int32_t* running) {
+  if (ctx) ++ctx->ledger_epoch;  // the published step ledger (eqx_step_ledger) is stale
   if (!ctx || n < 0 || (n > 0 && (!names || !weight))) return fail(ctx, EQX_ERR_ARG, "eqx_set_clients: bad arguments");
   cudaSetDevice(ctx->device);
   std::vector<std::string> ids;
@@ -745,6 +752,21 @@ eqx_status eqx_get_clients(eqx_ctx* ctx, int32_t n, double* ufc, double* rfc, do
   return read_cols(ctx, cols, n > 0 ? 5 : 0);
 }
 
+eqx_status eqx_step_ledger(eqx_ctx* ctx, int32_t n, double* ufc, double* rfc, double* counter,
+                           int32_t* backlogged, int32_t* running) {
+  if (!ctx || n != ctx->C) return fail(ctx, EQX_ERR_ARG, "eqx_step_ledger: roster size mismatch");
+  if (ctx->step_pending || !ctx->h_ledger || ctx->ledger_pub_epoch != ctx->ledger_epoch)
+    return fail(ctx, EQX_ERR_CONFIG, "eqx_step_ledger: no collected step ledger (use eqx_get_clients)");
+  const double* hd = reinterpret_cast<const double*>(ctx->h_ledger);
+  const int32_t* hi = reinterpret_cast<const int32_t*>(hd + 3 * static_cast<int64_t>(n));
+  if (ufc) std::memcpy(ufc, hd, 8ull * n);
+  if (rfc) std::memcpy(rfc, hd + n, 8ull * n);
+  if (counter) std::memcpy(counter, hd + 2 * static_cast<int64_t>(n), 8ull * n);
+  if (backlogged) std::memcpy(backlogged, hi, 4ull * n);
+  if (running) std::memcpy(running, hi + n, 4ull * n);
+  return EQX_OK;
+}
+
 eqx_status eqx_ledger_checkpoint(eqx_ctx* ctx) {
   if (!ctx) return fail(ctx, EQX_ERR_ARG, "eqx_ledger_checkpoint: NULL context");
   cudaSetDevice(ctx->device);
@@ -770,6 +792,7 @@ eqx_status eqx_ledger_checkpoint(eqx_ctx* ctx) {
 }
 
 eqx_status eqx_ledger_restore_async(eqx_ctx* ctx) {
+  if (ctx) ++ctx->ledger_epoch;  // the published step ledger (eqx_step_ledger) is stale
   if (!ctx || !ctx->snap_valid) return fail(ctx, EQX_ERR_CONFIG, "eqx_ledger_restore_async: no checkpoint");
   cudaSetDevice(ctx->device);
   cudaStream_t s = ctx->stream;
@@ -1119,6 +1142,7 @@ static DrainArgs drain_args(eqx_ctx* ctx) {
 // lift: also apply on_activated / set_backlogged now (a standalone drain); a drain fused into a
 // step leaves that to the selection kernel's prologue (SelectArgs::do_lift).
 static eqx_status drain_enqueue(eqx_ctx* ctx, bool lift, bool keep_qlen = false) {
+  if (ctx) ++ctx->ledger_epoch;  // the published step ledger (eqx_step_ledger) is stale
   cudaStream_t s = ctx->stream;
   const int32_t C = ctx->C;
   if (C == 0) return EQX_OK;
@@ -1509,6 +1533,25 @@ static eqx_status warm_args(eqx_ctx* ctx, const StepPlan& pl, SelectArgs& w) {
   return EQX_OK;
 }
 
+// The mapped host buffer a step's selection writes the ledger to (eqx_step_ledger); allocated
+// outside any graph capture.
+static eqx_status ensure_step_ledger(eqx_ctx* ctx) {
+  const size_t lb = 32ull * std::max(ctx->C, 1);
+  if (ctx->h_ledger_cap >= lb) return EQX_OK;
+  if (ctx->h_ledger) cudaFreeHost(ctx->h_ledger);
+  ctx->h_ledger = nullptr;
+  ctx->h_ledger_dev = nullptr;
+  ctx->h_ledger_cap = 0;
+  void* p = nullptr;
+  CUDA_TRY(ctx, cudaHostAlloc(&p, lb, cudaHostAllocMapped));
+  ctx->h_ledger = static_cast<unsigned char*>(p);
+  ctx->h_ledger_cap = lb;
+  void* d = nullptr;
+  CUDA_TRY(ctx, cudaHostGetDevicePointer(&d, p, 0));
+  ctx->h_ledger_dev = static_cast<unsigned char*>(d);
+  return EQX_OK;
+}
+
 // Stream work of a step.  Scoring (HBM-bound, whole queue) runs on the side stream
 // concurrently with [optional drain ->] selection on the main stream; both join before the
 // summary D2H.  Capturable into a CUDA graph (fork/join through events).
@@ -1556,6 +1599,10 @@ static eqx_status step_enqueue(eqx_ctx* ctx, const StepPlan& pl, bool with_drain
     se.score_done = sc.done;
     se.score_ctas = pl.score_grid;
     wi.score_sig = sc.done;
+    if (ctx->h_ledger_dev && ctx->h_ledger_cap >= 32ull * ctx->C) {
+      se.h_ledger = ctx->h_ledger_dev;
+      ctx->ledger_pub_epoch = ++ctx->ledger_epoch;
+    }
   }
   if (timing) CUDA_TRY(ctx, cudaEventRecord(ctx->ev_k[5], s));
   CUDA_TRY(ctx, launch_pdl(window_kernel, dim3(pl.window_grid), dim3(256), pl.window_smem, s, wi));
@@ -1610,6 +1657,7 @@ eqx_status eqx_drain(eqx_ctx* ctx, const eqx_requests* r) {
 eqx_status eqx_step_async(eqx_ctx* ctx, double now) {
   StepPlan pl;
   eqx_status st = step_prepare(ctx, now, pl);
+  if (st == EQX_OK) st = ensure_step_ledger(ctx);
   if (st != EQX_OK) return st;
   ctx->shard_W = 0;
   st = step_enqueue(ctx, pl, false);
@@ -1638,6 +1686,10 @@ eqx_status eqx_drain_step_async(eqx_ctx* ctx, const eqx_requests* r, double now)
   // parameter (pointers, sizes, policy, `now`, smem/tiling plan); two graphs are cached, for a
   // resident queue or the staging buffer sets of host batches (whose H2D and release events
   // stay outside the graph).
+  {
+    eqx_status le = ensure_step_ledger(ctx);
+    if (le != EQX_OK) return le;
+  }
   if (ctx->C > 0) {  // the selection code warm-up's problem and stream (outside any capture)
     eqx_status we = warm_args(ctx, pl, ctx->warm_se);
     if (we != EQX_OK) return we;
@@ -1647,11 +1699,12 @@ eqx_status eqx_drain_step_async(eqx_ctx* ctx, const eqx_requests* r, double now)
       CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->ev_warm_done, cudaEventDisableTiming));
     }
   }
-  std::vector<unsigned char> key(sizeof(StepPlan) + 8 * sizeof(int64_t));
+  std::vector<unsigned char> key(sizeof(StepPlan) + 9 * sizeof(int64_t));
   std::memcpy(key.data(), &pl, sizeof(StepPlan));
-  const int64_t extra[8] = {ctx->tile_rows, ctx->n_tiles, ctx->counter_lift, static_cast<int64_t>(ctx->hist_smem),
+  const int64_t extra[9] = {ctx->tile_rows, ctx->n_tiles, ctx->counter_lift, static_cast<int64_t>(ctx->hist_smem),
                             static_cast<int64_t>(ctx->rank_smem), ctx->staged,
-                            static_cast<int64_t>(reinterpret_cast<uintptr_t>(ctx->q_id)), ctx->id_base};
+                            static_cast<int64_t>(reinterpret_cast<uintptr_t>(ctx->q_id)), ctx->id_base,
+                            static_cast<int64_t>(reinterpret_cast<uintptr_t>(ctx->h_ledger_dev))};
   std::memcpy(key.data() + sizeof(StepPlan), extra, sizeof(extra));
   int slot = -1;
   for (int i = 0; i < eqx_ctx::kGraphs; ++i)
@@ -1678,6 +1731,10 @@ eqx_status eqx_drain_step_async(eqx_ctx* ctx, const eqx_requests* r, double now)
   }
   ctx->graph_used[slot] = ++ctx->graph_clock;
   CUDA_TRY(ctx, cudaGraphLaunch(ctx->graphs[slot], s));
+  // a replay drains (the ledger changes) and, on a non-empty queue, publishes the step ledger
+  // exactly as the captured step_enqueue did (the graph key holds h_ledger_dev)
+  ++ctx->ledger_epoch;
+  if (ctx->n > 0 && ctx->h_ledger_dev && ctx->h_ledger_cap >= 32ull * ctx->C) ctx->ledger_pub_epoch = ++ctx->ledger_epoch;
   if (r->location != EQX_DEVICE) st = release_stage(ctx);
   if (st != EQX_OK) return st;
   ctx->step_pending = true;
@@ -1702,6 +1759,7 @@ eqx_status eqx_set_timing(eqx_ctx* ctx, double prefill_linear_ms, double prefill
 }
 
 eqx_status eqx_replay(eqx_ctx* ctx, const eqx_replays* R, eqx_replay_out* O) {
+  if (ctx) ++ctx->ledger_epoch;  // the published step ledger (eqx_step_ledger) is stale
   if (!ctx || !R || !O) return fail(ctx, EQX_ERR_ARG, "eqx_replay: NULL argument");
   if (!ctx->policy_set || !ctx->model_set || !ctx->profile_set)
     return fail(ctx, EQX_ERR_CONFIG, "eqx_replay: policy, predictor and GPU profile must be set first");
@@ -1913,6 +1971,7 @@ eqx_status eqx_replay(eqx_ctx* ctx, const eqx_replays* R, eqx_replay_out* O) {
 
 // ---- live queues -----------------------------------------------------
 eqx_status eqx_append(eqx_ctx* ctx, const eqx_requests* r) {
+  if (ctx) ++ctx->ledger_epoch;  // the published step ledger (eqx_step_ledger) is stale
   if (!ctx || !r) return fail(ctx, EQX_ERR_ARG, "eqx_append: NULL argument");
   if (!ctx->model_set || !ctx->profile_set)
     return fail(ctx, EQX_ERR_CONFIG, "eqx_append: predictor and GPU profile must be set first");
@@ -2041,6 +2100,7 @@ eqx_status eqx_append(eqx_ctx* ctx, const eqx_requests* r) {
 
 // ---- completion / feedback ------------------------------------------
 eqx_status eqx_feedback(eqx_ctx* ctx, const int64_t* tokens, const eqx_completions* done, double ema_alpha) {
+  if (ctx) ++ctx->ledger_epoch;  // the published step ledger (eqx_step_ledger) is stale
   if (!ctx) return fail(ctx, EQX_ERR_ARG, "eqx_feedback: NULL context");
   if (!ctx->policy_set || !ctx->profile_set) return fail(ctx, EQX_ERR_CONFIG, "eqx_feedback: policy and profile must be set first");
   const int64_t n = done ? done->n : 0;
@@ -2177,6 +2237,7 @@ int64_t eqx_shard_record_bytes(int32_t cmax, int32_t W) {
 }
 
 eqx_status eqx_shard_export_async(eqx_ctx* ctx, double now, int32_t cmax, int32_t W, void* rec) {
+  if (ctx) ++ctx->ledger_epoch;  // the published step ledger (eqx_step_ledger) is stale
   if (!ctx || !rec) return fail(ctx, EQX_ERR_ARG, "eqx_shard_export_async: NULL argument");
   if (W < 1) return fail(ctx, EQX_ERR_ARG, "eqx_shard_export_async: window depth must be >= 1");
   if (cmax < ctx->C) return fail(ctx, EQX_ERR_ARG, "eqx_shard_export_async: cmax is smaller than the shard's client count");
@@ -2211,6 +2272,7 @@ eqx_status eqx_shard_export_async(eqx_ctx* ctx, double now, int32_t cmax, int32_
 
 eqx_status eqx_shard_select_async(eqx_ctx* ctx, const void* recs, int32_t world, int64_t stride,
                                   const int32_t* client_off, int32_t cmax, int32_t W, double now) {
+  if (ctx) ++ctx->ledger_epoch;  // the published step ledger (eqx_step_ledger) is stale
   if (!ctx || !recs || !client_off) return fail(ctx, EQX_ERR_ARG, "eqx_shard_select_async: NULL argument");
   if (world < 1 || world > kMaxWorld) return fail(ctx, EQX_ERR_ARG, "eqx_shard_select_async: world size out of range (1..64)");
   if (W < 1 || cmax < 0) return fail(ctx, EQX_ERR_ARG, "eqx_shard_select_async: bad window depth / cmax");

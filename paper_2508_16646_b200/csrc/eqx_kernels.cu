@@ -1425,6 +1425,15 @@ __global__ void __launch_bounds__(kTopkThreads, 1) select_topk_kernel(const Sele
       a.head[c] = h[j];
       a.backlogged[c] = (f[j] & kBacklogged) ? 1 : 0;
       a.running[c] = run[j] + ad[j];
+      if (a.h_ledger) {  // [ufc C][rfc C][counter C] f64, [backlogged C][running C] i32
+        double* hd = reinterpret_cast<double*>(a.h_ledger);
+        int32_t* hi = reinterpret_cast<int32_t*>(hd + 3 * static_cast<int64_t>(C));
+        hd[c] = u[j];
+        hd[C + c] = r[j];
+        hd[2 * C + c] = k[j];
+        hi[c] = (f[j] & kBacklogged) ? 1 : 0;
+        hi[C + c] = run[j] + ad[j];
+      }
     }
   }
   if (tid == 0) {

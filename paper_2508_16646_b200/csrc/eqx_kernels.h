@@ -203,6 +203,7 @@ struct SelectArgs {
   int64_t ev_cap;
   DevState* st;
   DevState* h_st;        // mapped host copy the epilogue writes the step's DevState to (or nullptr)
+  unsigned char* h_ledger;  // mapped host copy of the written-back ledger (eqx_step_ledger layout), or nullptr
   unsigned long long* score_done;  // ... with the scoring's counts from here (ScoreArgs::done)
   int32_t score_ctas;
   const ModelTables* model;

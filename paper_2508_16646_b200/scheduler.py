@@ -437,6 +437,20 @@ class GpuScheduler:
                                               out["running"].ctypes.data_as(L._i32p)))
         return out
 
+    def step_ledger(self) -> dict:
+        """ledger() as the last collected step left it, from the mapped host copy its selection
+        CTA wrote (eqx_step_ledger: no device copy); raises once the device ledger has changed."""
+        n = len(self.client_ids)
+        out = {k: np.zeros(n) for k in ("ufc", "rfc", "counter")}
+        out["backlogged"] = np.zeros(n, np.int32)
+        out["running"] = np.zeros(n, np.int32)
+        self._check(self._lib.eqx_step_ledger(self._ctx, n, out["ufc"].ctypes.data_as(L._dp),
+                                              out["rfc"].ctypes.data_as(L._dp),
+                                              out["counter"].ctypes.data_as(L._dp),
+                                              out["backlogged"].ctypes.data_as(L._i32p),
+                                              out["running"].ctypes.data_as(L._i32p)))
+        return out
+
     def clients(self) -> list:
         led = self.ledger()
         return [ClientState(cid, ufc=float(led["ufc"][i]), rfc=float(led["rfc"][i]),

@@ -70,3 +70,29 @@ def test_noisy_near_ties_per_step():
         assert res.noisy_near_ties == fresh.noisy_near_ties
         assert res.n_admitted == fresh.n_admitted and res.n_rejected == fresh.n_rejected
         np.testing.assert_array_equal(res.ids, fresh.ids)
+
+
+def test_step_ledger_matches_device_ledger():
+    """eqx_step_ledger: the ledger the step's selection CTA wrote to mapped host memory equals
+    the device ledger read back by eqx_get_clients, on split and graph steps; once the device
+    ledger changes (restore, drain) the published copy is refused."""
+    from test_gpu_parity import _random_case
+    from paper_2508_16646_b200.scheduler import ConfigError
+    for C in (64, 1000):
+        case = _random_case(6300 + C, 40_000, C, pred_kind=H.PRED_MOPE)
+        sch = _scheduler(case)  # finalizes the case
+        cols = case_columns(case)
+        for graph in (False, True, False):
+            sch.restore_async()
+            if graph:
+                sch.drain_step_async(case.now, **cols)
+                sch.collect()
+            else:
+                sch.drain(**cols)
+                sch.step(case.now)
+            pub, dev = sch.step_ledger(), sch.ledger()
+            for k in dev:
+                np.testing.assert_array_equal(pub[k], dev[k], err_msg=k)
+        sch.restore_async()
+        with pytest.raises(ConfigError):
+            sch.step_ledger()

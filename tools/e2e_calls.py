@@ -23,7 +23,7 @@ def loop(steps, acc=None):
         sch.restore_async(); t.append(time.perf_counter())
         sch.drain_step_async(1.0, **hosts[i % 3]); t.append(time.perf_counter())
         sch.collect(with_events=True); t.append(time.perf_counter())
-        sch.ledger(); t.append(time.perf_counter())
+        (sch.step_ledger() if os.environ.get("STEP_LEDGER") else sch.ledger()); t.append(time.perf_counter())
         if acc is not None:
             for k, n in enumerate(names):
                 acc[n] += t[k + 1] - t[k]
