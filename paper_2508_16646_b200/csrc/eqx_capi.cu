@@ -852,9 +852,20 @@ static eqx_status stage_fill(eqx_ctx* ctx, const eqx_requests* r, int b) {
   }
   int64_t pk_bytes = 0;  // the packed column's size is its first word
   if (packed && n > 0) std::memcpy(&pk_bytes, r->arrival_s, 8);
-  if (packed && n > 0 && (pk_bytes < 16 + 16 * ((n + 255) / 256) + 6 * n ||
-                          pk_bytes > 16 + 32 * ((n + 255) / 256) + 8 * n))
-    return fail(ctx, EQX_ERR_ARG, "packed arrivals: not an eqx_pack_arrivals column of n rows");
+  if (packed && n > 0) {  // the header's block offsets must stay inside the column (device reads)
+    const int64_t nb = (n + 255) / 256, hdr = (8 + 16 * nb + 15) & ~int64_t(15);
+    bool ok = pk_bytes >= hdr + 6 * n && pk_bytes <= hdr + 16 * nb + 8 * n;
+    const unsigned char* hp = static_cast<const unsigned char*>(static_cast<const void*>(r->arrival_s));
+    for (int64_t b = 0; b < nb && ok; ++b) {
+      uint64_t base;
+      int64_t off;
+      std::memcpy(&base, hp + 8 + 8 * b, 8);
+      std::memcpy(&off, hp + 8 + 8 * nb + 8 * b, 8);
+      const int64_t rows = std::min<int64_t>(256, n - 256 * b);
+      ok = off >= hdr && (off & 15) == 0 && off + (base == ~0ull ? 8 : 6) * rows <= pk_bytes;
+    }
+    if (!ok) return fail(ctx, EQX_ERR_ARG, "packed arrivals: not an eqx_pack_arrivals column of n rows");
+  }
   if (packed) CUDA_TRY(ctx, st.apk.ensure(static_cast<size_t>(pk_bytes) + 16));
   CUDA_TRY(ctx, cudaStreamWaitEvent(cs, st.free_, 0));
   auto h2d = [&](void* dst, const void* src, size_t bytes) {

@@ -216,6 +216,24 @@ def test_packed_arrival_host_columns(narrow):
             compare_step(res, sch, want)
 
 
+def test_packed_arrivals_rejects_corrupt_header():
+    """A packed column whose header points outside itself is refused before any device read."""
+    from helpers import case_batch, case_clients, case_kwargs
+    from paper_2508_16646_b200 import scheduler as S
+    case = _random_case(64, 5000, 8)
+    H.run_step(case, "oracle")  # finalizes the case
+    cols = case_columns(case)
+    pk = S.pack_arrivals(cols["arrival_s"])
+    nb = (len(cols["arrival_s"]) + 255) // 256
+    bad = pk.data.copy()
+    bad[8 + 8 * nb:16 + 8 * nb] = np.frombuffer(np.int64(1 << 40).tobytes(), np.uint8)  # block 0 offset
+    cols["arrival_s"] = S.PackedArrivals(bad, pk.n)
+    sch = S.GpuScheduler(case_clients(case), running=case.running, **case_kwargs(case))
+    sch.set_batch(*case_batch(case))
+    with pytest.raises(ValueError):
+        sch.drain(**cols)
+
+
 def _graph_step(case, device_columns: bool, staged: bool = False, reps: int = 2):
     """The path bench.py times: eqx_drain_step_async (one CUDA-graph replay of drain, windows
     with the counter lift, scoring and selection), repeated on the restored ledger so the cached
