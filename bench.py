@@ -538,6 +538,8 @@ def run_cfg5(args, rank, world):
     sch = S.GpuScheduler([S.ClientState("client1"), S.ClientState("client2")], policy=S.PolicySpec(),
                          perf=S.PerfParams(), profile=prof, predictor="oracle", device=local)
     cap = 1  # run_sweep_alpha reads the reports only: no event log comes back
+    # the trace columns live in the library's pinned arena, as the other e2e legs' host batches do
+    cat = {k: S.pinned_copy(v) for k, v in cat.items()}
     times, kms = [], []
     for i in range(args.warmup + args.steps):
         torch.cuda.synchronize()
